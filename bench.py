@@ -1,0 +1,337 @@
+"""Benchmark: FilterGS per-frame render on the cfg-3 workload (BASELINE.json configs[2]).
+
+Workload: synthetic 10,039,185-node LoD tree (131x131 roots, L=3, K=8, gamma 0.5,
+scene seed 1, build seed 7 -- tree_builder.cpp generator), 1920x1080, a 300-frame
+fly-through (keyframes descending from altitude 400 through 200 to 140, with
+oblique segments; CameraPath slerp sampling, camera_path.cpp:126-180), tau_R = 3,
+three-sigma extents.  A step = one frame.  value = frames/s with the tree resident in
+HBM (device-timed, CUDA events on the scene stream, max over ranks); e2e = the same
+frames through the reference-shaped synchronous C-ABI call lodgs_gpu_render with the
+image copied back to pinned host memory every frame.
+
+Multi-GPU (torchrun): the tree is replicated, every rank renders its own K frames of
+the path (start offset rank*300/N), no collective on the data path ("weak").
+--impl reference: the reference renderer itself (oracle/_ref, compiled from
+/root/reference) on the host cores, bounded sample of the same path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FPS @1080p on 10M-node LoD tree; filter+sort HBM GB/s vs peak; tile pairs"
+TREE = dict(nx=131, ny=131, seed=1, depth=3, build_seed=7)
+W, H, FOCAL, TAU_R = 1920, 1080, 1000.0, 3.0
+PATH_SAMPLES = (100, 100, 99)  # 300 frames = sum + 1
+
+
+def _normalize(v):
+    return v / np.linalg.norm(v)
+
+
+def look_at(eye, target, up=(0.0, 1.0, 0.0)):
+    """World->camera rotation rows (x right, y down, z forward) and translation."""
+    eye = np.asarray(eye, np.float64)
+    f = _normalize(np.asarray(target, np.float64) - eye)
+    x = _normalize(np.cross(f, np.asarray(up, np.float64)))
+    y = np.cross(f, x)
+    R = np.stack([x, y, f])
+    t = -R @ eye
+    return tuple(R.reshape(-1)), tuple(t)
+
+
+def flythrough(L):
+    """cfg 3 camera path: 4 keyframes, 300 frames."""
+    keys = []
+    for eye, target in (((0.0, 0.0, 400.0), (0.0, 0.0001, 0.0)),
+                        ((30.0, -60.0, 260.0), (10.0, 10.0, 0.0)),
+                        ((-20.0, 10.0, 200.0), (-20.0, 10.0001, 0.0)),
+                        ((40.0, -30.0, 140.0), (50.0, 40.0, 0.0))):
+        R, t = look_at(eye, target)
+        keys.append(L.Camera(W, H, FOCAL, FOCAL, W / 2.0, H / 2.0, R, t, 0.01, 1000.0))
+    return L.sample_camera_path(keys, PATH_SAMPLES)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_reference_sample(L, tree, cams, threads, budget_s=20.0, max_frames=6):
+    """The reference renderer (oracle/_ref) on host cores over a bounded, evenly
+    strided sample of the path. FPS = frames / sum(T_total) as bench.cpp:160."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import Ref
+
+    ref = Ref()
+    h = ref.tree_from(tree)
+    stride = max(1, len(cams) // max_frames)
+    sample = cams[::stride][:max_frames]
+    total_ms, wall, frames = 0.0, 0.0, 0
+    t_start = time.perf_counter()
+    for cam in sample:
+        t0 = time.perf_counter()
+        r = ref.render(h, cam, TAU_R, L.ShrinkMode.three_sigma(), workers=threads)
+        wall += time.perf_counter() - t0
+        total_ms += r["total_ms"]
+        frames += 1
+        if time.perf_counter() - t_start > budget_s:
+            break
+    ref.free_tree(h)
+    return {"value": frames / (total_ms / 1000.0), "unit": "frames/s", "cores": threads,
+            "kind": "reference",
+            "sample": f"{frames} frames of the 300-frame cfg-3 path (stride {stride}), "
+                      f"lodgs::render T_total (bench.cpp:160); wall incl. per-frame "
+                      f"validation {frames / wall:.3f} frames/s"}
+
+
+def run_reference(args, rank, world):
+    from paper_2603_23891_b200 import lodgs as L
+
+    if rank != 0:
+        return
+    tree = L.build_synthetic_tree(**TREE)
+    cams = flythrough(L)
+    threads = os.cpu_count() or 1
+    per = []
+    for _ in range(args.warmup):
+        pass  # the reference has no device warm-up; keep W for the contract
+    sample = cpu_reference_sample(L, tree, cams, threads, budget_s=60.0, max_frames=max(3, args.steps_ref))
+    val = sample["value"]
+    line = {"metric": METRIC, "value": val, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / val,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator, seeds 1/7)",
+            "config": {"workload": "cfg3: 10,039,185-node LoD tree, 1920x1080, 300-frame fly-through, "
+                                   "tau_R=3, three-sigma", "nodes": tree.node_count(),
+                       "width": W, "height": H},
+            "impl": "reference", "cpu_baseline": sample,
+            "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank, world, local):
+    import ctypes as C
+
+    import torch
+
+    from paper_2603_23891_b200 import lodgs as L
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    t_build = time.perf_counter()
+    tree = L.build_synthetic_tree(**TREE)
+    cams = flythrough(L)
+    n_path = len(cams)
+    scene = L.GpuScene(tree, local)
+    build_s = time.perf_counter() - t_build
+    stream = torch.cuda.ExternalStream(scene.stream_ptr(), device=torch.device("cuda", local))
+    params = L.RenderParamsC(TAU_R, 0.0, 0, 0)
+    start = (rank * n_path) // world
+    order = [cams[(start + i) % n_path] for i in range(args.warmup + args.steps)]
+
+    # size the pair buffer on the whole path once (untimed)
+    for cam in cams[:: max(1, n_path // 30)]:
+        scene.render(cam, L.FilterConfig(TAU_R), L.ShrinkMode.three_sigma())
+
+    def device_loop(frames, profile=False):
+        scene.take_totals()
+        if profile:
+            scene.profile(True)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ev0.record(stream)
+        for cam in frames:
+            scene.render_async(cam, params)
+        ev1.record(stream)
+        ev1.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        tot = scene.take_totals()
+        prof = scene.profile_read() if profile else None
+        if profile:
+            scene.profile(False)
+        return ms, tot, prof
+
+    for cam in order[: args.warmup]:
+        scene.render_async(cam, params)
+    scene.sync()
+    timed = order[args.warmup:]
+    with ClockSampler(local) as clocks:
+        for attempt in range(3):
+            try:
+                ms, (nf, sum_sel, sum_pairs), _ = device_loop(timed)
+                break
+            except L.InternalError:
+                continue  # pair buffer grew; re-run the timed region
+    # per-stage device times over a second pass of the same frames (events between kernels)
+    _, _, (pf, stage_ms) = device_loop(timed, profile=True)
+
+    # e2e: reference-shaped synchronous call, pinned host image, every frame
+    host_img = C.c_void_p()
+    img_bytes = W * H * 3 * 4
+    L._check(L.load_library().lodgs_gpu_host_alloc(img_bytes, C.byref(host_img)))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e2e_frames = timed[: max(1, min(len(timed), args.e2e_steps))]
+    t0 = time.perf_counter()
+    st = L.RenderStatsC()
+    for cam in e2e_frames:
+        c = cam.to_c()
+        L._check(L.load_library().lodgs_gpu_render(scene.handle, C.byref(c), C.byref(params),
+                                                   host_img, C.byref(st)))
+    e2e_s = time.perf_counter() - t0
+    L.load_library().lodgs_gpu_host_free(host_img)
+
+    # max over ranks
+    vals = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms_max, e2e_max = float(vals[0]), float(vals[1])
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    K = len(timed)
+    fps = world * K / (ms_max / 1000.0)
+    e2e_fps = world * len(e2e_frames) / e2e_max
+    peak, peak_kind = measured_peak_gbs()
+    n = tree.node_count()
+    n_int = int(tree.level_offsets[-1])  # internal nodes precede the leaf level
+    mean_sel = sum_sel / max(1, nf)
+    mean_pairs = sum_pairs / max(1, nf)
+    # B_f = 29 N + 16 N_int + 4 N_sel per frame (mark + select)
+    filt_bytes = 29 * n + 16 * n_int + 4 * mean_sel
+    filt_ms = (stage_ms[0] + stage_ms[1]) / max(1, pf)
+    mark_ms = stage_ms[0] / max(1, pf)
+    sort_ms = stage_ms[3] / max(1, pf)
+    sort_bytes = 16 * mean_pairs  # read + write of each 8-byte key
+    stage_names = ["filter_mark", "filter_select", "preprocess_keys", "tile_sort", "blend"]
+    per_stage = {k: round(stage_ms[i] / max(1, pf), 5) for i, k in enumerate(stage_names)}
+    dominant = max(range(5), key=lambda i: stage_ms[i])
+    filt_gbs = filt_bytes / (filt_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator, seeds 1/7; tree resident in HBM)",
+        "config": {"workload": "cfg3: 10,039,185-node LoD tree, 1920x1080, 300-frame fly-through, "
+                               "tau_R=3, three-sigma", "nodes": n, "width": W, "height": H,
+                   "frames_per_rank": K, "l2": "inputs larger than L2 (tree 1.1 GB in HBM, "
+                   "filter streams 0.3 GB per frame)", "parallelism": f"view-sharded x{world}"},
+        "mean_selected": mean_sel, "mean_pairs": mean_pairs,
+        "stage_ms_per_frame": per_stage,
+        "roofline": {"kernel": "filter (mark+select)", "bound": "hbm",
+                     "achieved": filt_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": filt_gbs / peak, "traffic": None,
+                     "algorithmic_bytes_per_frame": filt_bytes,
+                     "dominant_stage": stage_names[dominant]},
+        "sort": {"achieved_gbs": sort_bytes / (sort_ms * 1e-3) / 1e9 if sort_ms > 0 else None,
+                 "bytes_per_frame": sort_bytes},
+        "e2e": {"value": e2e_fps, "unit": "frames/s",
+                "h2d_bytes_per_step": C.sizeof(L.CameraC) + C.sizeof(L.RenderParamsC),
+                "d2h_bytes_per_step": img_bytes + 64, "frames": len(e2e_frames)},
+        "gpu_launches": 9 * K,
+        "clocks": clocks.summary(),
+        "setup_s": build_s,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_reference_sample(L, tree, cams, os.cpu_count() or 1,
+                                                    budget_s=args.cpu_budget)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--steps-ref", type=int, default=6)
+    ap.add_argument("--cpu-budget", type=float, default=25.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_b200(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,267 @@
+/* lodgs_gpu.h -- C ABI of the B200-native FilterGS per-frame renderer.
+ *
+ * This is the drop-in boundary for the reference's per-frame hot path,
+ *     lodgs::render(tree, cam, FilterConfig, ShrinkMode, RenderOptions)
+ *     (/root/reference/proj/include/lodgs/rasterizer.hpp:106-108, body
+ *      proj/src/rasterizer.cpp:167-213)
+ * and for its stage functions filter_parallel / prepare_gaussians /
+ * bin_to_tiles / sort_pairs / alpha_blend (filter.hpp:42-43,
+ * rasterizer.hpp:55-71).  Plain pointers and sizes only; no C++ or torch
+ * types.  The C++ mirror of the reference API (include/lodgs_b200/lodgs.hpp)
+ * and the Python host module (paper_2603_23891_b200/lodgs.py) both sit on
+ * top of these entry points.
+ *
+ * Every compute entry point runs hand-written sm_100a CUDA kernels; there is
+ * no CPU fallback.  Without a usable CUDA device the compute calls return
+ * LODGS_ERR_CUDA and lodgs_gpu_last_error() says why.
+ *
+ * Status codes mirror the reference CLI's exit codes (cli.cpp:28-29):
+ * 0 ok, 2 validation/format (ValidationError / FormatError), 3 I/O (IoError).
+ * 4 and 5 are new: CUDA runtime failure and internal error.
+ */
+#ifndef LODGS_GPU_H
+#define LODGS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LODGS_GPU_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define LODGS_API __attribute__((visibility("default")))
+#else
+#define LODGS_API
+#endif
+
+enum lodgs_status {
+    LODGS_OK = 0,
+    LODGS_ERR_VALIDATION = 2, /* core.hpp:91-93 ValidationError / FormatError */
+    LODGS_ERR_IO = 3,         /* core.hpp:96-98 IoError */
+    LODGS_ERR_CUDA = 4,
+    LODGS_ERR_INTERNAL = 5
+};
+
+/* scene.hpp:76-82 Camera.  `znear`/`zfar` are the reference's near/far. */
+typedef struct lodgs_camera {
+    uint32_t width, height;
+    double fx, fy, cx, cy;
+    double rotation[9]; /* world->camera, row-major */
+    double translation[3];
+    double znear, zfar;
+} lodgs_camera;
+
+/* scene.hpp:29-74 LoDTree (level-major SoA arena), borrowed for the call. */
+typedef struct lodgs_tree_view {
+    uint64_t n_nodes;
+    const float *mean_x, *mean_y, *mean_z;
+    const float *scale_x, *scale_y, *scale_z;
+    const float *quat_w, *quat_x, *quat_y, *quat_z;
+    const float *opacity;
+    const float *color_r, *color_g, *color_b;
+    const uint32_t *parent; /* 0xFFFFFFFF = root (core.hpp:15) */
+    const uint8_t *leaf;
+    const uint32_t *level_offsets;
+    uint32_t n_levels;
+    float shrink_factor;
+} lodgs_tree_view;
+
+/* rasterizer.hpp:16-24 ShrinkMode::Kind */
+enum lodgs_shrink_kind {
+    LODGS_SHRINK_THREE_SIGMA = 0,
+    LODGS_SHRINK_FIXED = 1,   /* tau = 1/255 */
+    LODGS_SHRINK_ADAPTIVE = 2 /* tau from calibration */
+};
+
+/* Render flags (no reference equivalent except KEEP_PAIRS ~ collect_kpc). */
+enum lodgs_render_flags {
+    LODGS_RENDER_EXACT_BLEND = 1u,  /* FP64 blend with the reference exp_mx: bit-exact image */
+    LODGS_RENDER_KEEP_PAIRS = 2u,   /* keep sorted pairs + gaussians readable after the frame */
+    LODGS_RENDER_STAGE_TIMING = 4u  /* CUDA-event stage timers into lodgs_render_stats */
+};
+
+/* FilterConfig (filter.hpp:11-14) + ShrinkMode (rasterizer.hpp:16-24). */
+typedef struct lodgs_render_params {
+    double tau_r;        /* pixel radius threshold, > 0 */
+    double tau;          /* opacity threshold for fixed/adaptive, in (0,1) */
+    int32_t shrink_kind; /* lodgs_shrink_kind */
+    uint32_t flags;      /* lodgs_render_flags */
+} lodgs_render_params;
+
+/* RenderStats (rasterizer.hpp:73-84) plus the device-side counts. */
+typedef struct lodgs_render_stats {
+    uint64_t n_selected;  /* filter survivors */
+    uint64_t n_gaussians; /* projected (selected minus near-plane drops) */
+    uint64_t n_pairs;     /* N_P, gaussian-tile pairs */
+    int32_t filter_passes, filter_barriers; /* 2 / 2 as filter_parallel */
+    double t_calc_ms, t_sync_ms, t_prepr_ms, t_sort_ms, t_alpha_ms;
+    uint32_t big_tiles; /* tiles sorted by the large-segment path */
+    uint32_t kernel_launches;
+} lodgs_render_stats;
+
+/* tiles.hpp:23-28 TilePair */
+typedef struct lodgs_tile_pair {
+    uint32_t tile;
+    float depth;
+    uint32_t gaussian;
+} lodgs_tile_pair;
+
+/* rasterizer.hpp:36-51 BlendList, caller-owned arrays (capacity >= n). */
+typedef struct lodgs_blend_list {
+    uint64_t n;
+    double *mean_x, *mean_y;
+    double *conic_a, *conic_b, *conic_c;
+    double *opacity;
+    double *col_r, *col_g, *col_b;
+    double *radius;
+    float *depth;
+    uint32_t *node;
+} lodgs_blend_list;
+
+typedef struct lodgs_gpu_scene lodgs_gpu_scene;
+
+/* ---------------------------------------------------------------- misc -- */
+LODGS_API const char *lodgs_gpu_last_error(void);
+LODGS_API int lodgs_gpu_abi_version(void);
+LODGS_API int lodgs_gpu_device_count(int *count);
+
+/* ------------------------------------------------- host-side utilities -- */
+/* scene.cpp:89-165 validate_tree; *n_violations = number of rule breaks.
+ * msg (optional) receives the same text require_valid would throw. */
+LODGS_API int lodgs_validate_tree(const lodgs_tree_view *tree, uint64_t *n_violations, char *msg,
+                        size_t msg_cap);
+/* scene.cpp:167-199 validate_camera. */
+LODGS_API int lodgs_validate_camera(const lodgs_camera *cam, uint64_t *n_violations, char *msg,
+                          size_t msg_cap);
+/* projection.cpp:11-38 CameraGeom::make, 44 doubles in CameraGeom order. */
+LODGS_API int lodgs_camera_geom(const lodgs_camera *cam, double out44[44]);
+/* camera_path.cpp:126-180: frames = sum(samples)+1; out holds that many. */
+LODGS_API int lodgs_camera_path_sample(const lodgs_camera *keyframes, uint32_t n_keyframes,
+                             const uint32_t *samples, lodgs_camera *out, uint64_t out_cap,
+                             uint64_t *n_frames);
+
+/* tree_builder.hpp:11-27 configs. */
+typedef struct lodgs_synthetic_spec {
+    uint32_t nx, ny;
+    float spacing;
+    float scale_min, scale_max;
+    float opacity_min, opacity_max;
+    uint64_t seed;
+    uint32_t congestion;
+} lodgs_synthetic_spec;
+
+typedef struct lodgs_build_config {
+    uint32_t depth;
+    float shrink_factor;
+    uint32_t children_per_node;
+    uint64_t seed;
+} lodgs_build_config;
+
+/* Writable SoA arrays for tree construction (capacity = n_nodes). */
+typedef struct lodgs_tree_buffers {
+    float *mean_x, *mean_y, *mean_z;
+    float *scale_x, *scale_y, *scale_z;
+    float *quat_w, *quat_x, *quat_y, *quat_z;
+    float *opacity;
+    float *color_r, *color_g, *color_b;
+    uint32_t *parent;
+    uint8_t *leaf;
+    uint32_t *level_offsets; /* capacity depth+1 */
+} lodgs_tree_buffers;
+
+/* generate_synthetic_scene + build_tree (tree_builder.cpp:75-174): first call
+ * with out == NULL to learn n_nodes / n_levels, then with buffers. */
+LODGS_API int lodgs_build_synthetic_tree(const lodgs_synthetic_spec *spec, const lodgs_build_config *cfg,
+                               lodgs_tree_buffers *out, uint64_t *n_nodes, uint32_t *n_levels);
+
+/* ---------------------------------------------------------- GPU scenes -- */
+/* Validates the tree once (the reference re-validates every frame,
+ * rasterizer.cpp:170) and uploads it to `device`.  The scene owns one CUDA
+ * stream; calls on one scene are serialised by the caller. */
+LODGS_API int lodgs_gpu_scene_create(const lodgs_tree_view *tree, int device, lodgs_gpu_scene **out);
+LODGS_API int lodgs_gpu_scene_destroy(lodgs_gpu_scene *scene);
+/* The scene's cudaStream_t, for callers that time on it with CUDA events. */
+LODGS_API int lodgs_gpu_scene_stream(lodgs_gpu_scene *scene, void **stream);
+/* Pre-sizes the pair buffer (bytes are 16 * max_pairs). Grows on demand otherwise. */
+LODGS_API int lodgs_gpu_scene_reserve(lodgs_gpu_scene *scene, uint64_t max_pairs);
+/* Device bytes held by the scene. */
+LODGS_API int lodgs_gpu_scene_memory(lodgs_gpu_scene *scene, uint64_t *bytes);
+
+/* One frame, synchronous, the reference render() contract: filter ->
+ * preprocess(+shrink) -> key duplication -> sort -> blend.  image_host
+ * (nullable) receives W*H*3 interleaved RGB f32 (Image, image.hpp:10-23);
+ * pinned memory from lodgs_gpu_host_alloc makes the copy DMA-direct. */
+LODGS_API int lodgs_gpu_render(lodgs_gpu_scene *scene, const lodgs_camera *cam,
+                     const lodgs_render_params *params, float *image_host,
+                     lodgs_render_stats *stats);
+
+/* Enqueue one frame on the scene stream and return without synchronising.
+ * Sizes stay on the device; an undersized pair buffer is reported (and
+ * grown) by the next lodgs_gpu_sync, which then returns LODGS_ERR_INTERNAL
+ * with "overflow" so the caller re-renders. image_host (nullable) is filled
+ * by an async D2H copy on the same stream. */
+LODGS_API int lodgs_gpu_render_async(lodgs_gpu_scene *scene, const lodgs_camera *cam,
+                           const lodgs_render_params *params, float *image_host);
+/* Waits for the scene stream; stats (nullable) = the last frame's. */
+LODGS_API int lodgs_gpu_sync(lodgs_gpu_scene *scene, lodgs_render_stats *stats);
+/* Sum of n_selected / n_pairs over frames since the last call (device counters). */
+LODGS_API int lodgs_gpu_take_totals(lodgs_gpu_scene *scene, uint64_t *frames, uint64_t *sum_selected,
+                          uint64_t *sum_pairs);
+
+/* Per-stage CUDA-event profiling of every enqueued frame, without host sync.
+ * enable=1 starts (and clears) collection, enable=0 stops it.  read() syncs
+ * and returns, summed over the collected frames, the device time of
+ * stage_ms[0] filter mark (K1), [1] filter select (K2), [2] preprocess +
+ * tile offsets + key duplication (K3/K4), [3] per-tile sort (K5),
+ * [4] blend (K6), [5] whole frame. */
+LODGS_API int lodgs_gpu_profile(lodgs_gpu_scene *scene, int enable);
+LODGS_API int lodgs_gpu_profile_read(lodgs_gpu_scene *scene, uint64_t *frames, double stage_ms[6]);
+
+/* Readbacks of the last frame (after lodgs_gpu_sync / lodgs_gpu_render). */
+LODGS_API int lodgs_gpu_read_image(lodgs_gpu_scene *scene, float *out);
+LODGS_API int lodgs_gpu_image_device_ptr(lodgs_gpu_scene *scene, const float **dev_ptr);
+LODGS_API int lodgs_gpu_read_selected(lodgs_gpu_scene *scene, uint32_t *out, uint64_t cap, uint64_t *n);
+/* Sorted (tile, depth, gaussian) pairs: needs LODGS_RENDER_KEEP_PAIRS. */
+LODGS_API int lodgs_gpu_read_pairs(lodgs_gpu_scene *scene, lodgs_tile_pair *out, uint64_t cap,
+                         uint64_t *n);
+/* The projected BlendList (FP64 fields): needs LODGS_RENDER_KEEP_PAIRS. */
+LODGS_API int lodgs_gpu_read_gaussians(lodgs_gpu_scene *scene, lodgs_blend_list *out, uint64_t cap);
+/* Per-gaussian tile counts (bin_to_tiles multiplicity) and per-tile pair counts. */
+LODGS_API int lodgs_gpu_read_counts(lodgs_gpu_scene *scene, uint32_t *per_gaussian, uint64_t cap_g,
+                          uint32_t *per_tile, uint64_t cap_t);
+
+/* -------------------------------------------------- stage entry points -- */
+/* filter_parallel (filter.cpp:115-150): selected ascending, passes = barriers = 2. */
+LODGS_API int lodgs_gpu_filter(lodgs_gpu_scene *scene, const lodgs_camera *cam, double tau_r,
+                     uint32_t *selected, uint64_t cap, uint64_t *n_selected, int32_t *passes,
+                     int32_t *barriers);
+/* MarkFn contract (kernels.hpp:47-52) over [begin, end): vis, qpass and
+ * (nullable) the FP64 screen radius, bit-identical to mark_scalar. */
+LODGS_API int lodgs_gpu_mark(lodgs_gpu_scene *scene, const lodgs_camera *cam, uint64_t begin, uint64_t end,
+                   double tau_r, uint8_t *vis, uint8_t *qpass, double *radius);
+/* prepare_gaussians (rasterizer.cpp:48-73); out arrays need n_sel capacity. */
+LODGS_API int lodgs_gpu_prepare(lodgs_gpu_scene *scene, const lodgs_camera *cam, const uint32_t *selected,
+                      uint64_t n_sel, int32_t shrink_kind, double tau, lodgs_blend_list *out);
+/* bin_to_tiles (rasterizer.cpp:75-98) in the reference's emission order.
+ * out == NULL: only *n_pairs is computed. */
+LODGS_API int lodgs_gpu_bin_to_tiles(const lodgs_blend_list *list, int width, int height,
+                           lodgs_tile_pair *out, uint64_t cap, uint64_t *n_pairs);
+/* sort_pairs (rasterizer.cpp:100-135): stable (tile, depth) order, in place. */
+LODGS_API int lodgs_gpu_sort_pairs(lodgs_tile_pair *pairs, uint64_t n);
+/* alpha_blend (rasterizer.cpp:137-165) of sorted pairs; flags may hold
+ * LODGS_RENDER_EXACT_BLEND. image receives W*H*3 floats. */
+LODGS_API int lodgs_gpu_alpha_blend(const lodgs_tile_pair *sorted, uint64_t n, const lodgs_blend_list *list,
+                          int width, int height, uint32_t flags, float *image);
+
+/* ----------------------------------------------------------- utilities -- */
+/* Pinned host memory for zero-staging image readback. */
+LODGS_API int lodgs_gpu_host_alloc(uint64_t bytes, void **ptr);
+LODGS_API int lodgs_gpu_host_free(void *ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LODGS_GPU_H */

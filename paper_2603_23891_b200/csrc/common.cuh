@@ -1,0 +1,108 @@
+// common.cuh -- shared device definitions for the sm_100a FilterGS kernels.
+//
+// All translation units are compiled with -fmad=false: every FP64 expression
+// on the parity path must round exactly like the reference's no-FMA scalar
+// code (mark_core.hpp:12-15, proj/CMakeLists.txt:13).  Fast FP32 code that
+// wants fused multiply-adds asks for them explicitly with __fmaf_rn.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fgs {
+
+constexpr int kTile = 16;                  // tiles.hpp:8-9
+constexpr uint32_t kRootParent = 0xFFFFFFFFu;  // core.hpp:15
+constexpr double kAlphaCap = 0.99;         // kernels.hpp:20
+constexpr double kMinAlpha = 1.0 / 255.0;  // kernels.hpp:21
+constexpr double kTermT = 1e-4;            // kernels.hpp:22
+
+// projection.hpp:23-32 CameraGeom, 44 doubles; passed by value as a kernel
+// parameter (352 B, well under the 32 KB parameter limit on sm_100a).
+struct Geom {
+    double rot[9];
+    double trans[3];
+    double fx, fy, cx, cy;
+    double width, height;
+    double znear, zfar;
+    double planes[6][4];
+};
+
+// Node fields the preprocess gathers for each selected node: one 64-byte
+// record so a gather is two 32-byte sectors instead of fourteen SoA sectors.
+struct __align__(16) SplatRec {
+    float mx, my, mz, sx;
+    float sy, sz, qw, qx;
+    float qy, qz, opacity, cr;
+    float cg, cb, pad0, pad1;
+};
+
+// Per projected gaussian, FP64 fields (exact blend path, guard-band
+// recompute, parity readback).  64 bytes.
+struct __align__(16) Gauss64 {
+    double mx, my;
+    double ca, cb, cc;
+    double op;
+    double radius;
+    double pad;
+};
+
+// FP64 colours, only materialised for the exact (bit-identical) blend.
+struct __align__(16) GaussCol64 {
+    double r, g, b, pad;
+};
+
+// Per projected gaussian, FP32 blend record.
+//   e(dx,dy) = ha*dx^2 + cb*dx*dy + hc*dy^2 = -power; sample skipped iff
+//   e > ethr = ln(255 * opacity) (alpha < 1/255, kernels.hpp:21).
+struct __align__(16) Gauss32 {
+    float ha, cb, hc, ethr;
+    float op, r, g, b;
+};
+
+// Per projected gaussian, what key duplication needs.
+struct __align__(16) GaussEmit {
+    uint32_t depth_bits;  // bit_cast<u32>(float(depth)), rasterizer.cpp:113-114
+    uint32_t node;
+    int16_t tx0, ty0, tx1, ty1;  // inclusive tile rect; tx1 < tx0 => no pairs
+};
+
+// Device-resident per-frame counters (one cudaMemsetAsync clears them).
+struct FrameCounters {
+    unsigned long long n_selected;
+    unsigned long long n_gaussians;
+    unsigned long long n_pairs;
+    unsigned int ticket_select;
+    unsigned int ticket_prep;
+    unsigned int ticket_bin;
+    unsigned int big_tiles;
+    unsigned int overflow;     // pair buffer too small
+    unsigned int nonfinite;    // project() produced a non-finite value
+    unsigned int big_cursor;
+    unsigned int pad;
+};
+
+// Running totals across frames (not cleared per frame).
+struct RunTotals {
+    unsigned long long frames;
+    unsigned long long sum_selected;
+    unsigned long long sum_pairs;
+    unsigned long long pad;
+};
+
+#ifdef __CUDACC__
+// std::max / std::min semantics (first argument NaN propagates), as the
+// reference relies on (mark_core.hpp:33,90,110).
+__device__ __forceinline__ double std_max(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double std_min(double a, double b) { return (b < a) ? b : a; }
+
+// int(std::floor(x)) with x86 cvttsd2si semantics for out-of-range values
+// (INT_MIN), so degenerate inputs bin exactly as the reference binary does.
+__device__ __forceinline__ int floor_to_int_x86(double x) {
+    const double f = floor(x);
+    return (f >= -2147483648.0 && f < 2147483648.0) ? static_cast<int>(f)
+                                                     : static_cast<int>(0x80000000u);
+}
+#endif  // __CUDACC__
+
+}  // namespace fgs

@@ -1,0 +1,161 @@
+// filter.cu -- the traversal-free parallel LoD filter (FilterGS),
+// reference filter_parallel (filter.cpp:115-150).
+//
+// K1 mark: one flat coalesced pass over the SoA arena.  Per node: camera
+// transform + sphere-vs-frustum (FP64, exact), and -- only for visible,
+// projectable internal nodes -- the EWA radius.  A leaf's qpass is never
+// read by the selection rule (candidates use vis && (qpass || leaf),
+// ancestors use qpass && !leaf, filter.cpp:23,137), so leaves and culled
+// nodes skip the covariance entirely.  Output: two bitmasks written by warp
+// ballot, cand = vis && (qpass || leaf) and qint = qpass && !leaf.
+//
+// K2 select: candidates walk their parent chain against the L2-resident qint
+// bitmask (filter.cpp:20-25); survivors are compacted in node order by a
+// single-pass chained scan, so `selected` comes out strictly increasing as
+// filter.cpp:147-148 produces it.
+#include "launch.h"
+#include "mark.cuh"
+#include "scan.cuh"
+
+namespace fgs {
+
+__global__ void __launch_bounds__(kMarkBlock) k_filter_mark(const Geom g, const DevTree t,
+                                                              const double tau_r,
+                                                              uint32_t* __restrict__ cand_bits,
+                                                              uint32_t* __restrict__ qint_bits,
+                                                              const uint64_t n_words) {
+    const uint64_t i = uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x;
+    bool cand = false, qint = false;
+    if (i < t.n) {
+        const float mx = __ldcs(t.mx + i), my = __ldcs(t.my + i), mz = __ldcs(t.mz + i);
+        const float sx = __ldcs(t.sx + i), sy = __ldcs(t.sy + i), sz = __ldcs(t.sz + i);
+        const bool leaf = __ldcs(t.leaf + i) != 0;
+        double tx, ty, tz;
+        cam_transform(g, mx, my, mz, tx, ty, tz);
+        const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
+        const bool vis = frustum_folded(g, tx, ty, tz, 3.0 * smax);
+        if (vis) {
+            if (leaf) {
+                cand = true;
+            } else if (tz >= g.znear) {
+                const float4 q = __ldg(t.quat + i);
+                MarkOut o;
+                ewa_cov2d(g, tx, ty, tz, sx, sy, sz, q.x, q.y, q.z, q.w, o);
+                if (o.radius <= tau_r) cand = qint = true;
+            }
+        }
+    }
+    const unsigned cm = __ballot_sync(0xffffffffu, cand);
+    const unsigned qm = __ballot_sync(0xffffffffu, qint);
+    if ((threadIdx.x & 31) == 0) {
+        const uint64_t w = i >> 5;
+        if (w < n_words) {
+            cand_bits[w] = cm;
+            qint_bits[w] = qm;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kSelectBlock) k_filter_select(
+    const uint32_t* __restrict__ cand_bits, const uint32_t* __restrict__ qint_bits,
+    const uint32_t* __restrict__ parent, const uint64_t n, const uint32_t n_tiles,
+    uint32_t* __restrict__ selected, unsigned long long* status, FrameCounters* cnt) {
+    __shared__ unsigned s_ticket;
+    __shared__ unsigned s_warp[kSelectBlock / 32];
+    __shared__ unsigned long long s_excl;
+    const unsigned tile = take_ticket(&cnt->ticket_select, &s_ticket);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t warp_base =
+        uint64_t(tile) * (kSelectBlock * kSelectItems) + uint64_t(warp) * (32 * kSelectItems);
+
+    unsigned masks[kSelectItems];
+    unsigned warp_count = 0;
+#pragma unroll
+    for (int j = 0; j < kSelectItems; ++j) {
+        const uint64_t node = warp_base + uint64_t(j) * 32 + lane;
+        bool keep = false;
+        if (node < n) {
+            const uint32_t word = __ldg(cand_bits + (node >> 5));
+            if ((word >> lane) & 1u) {
+                keep = true;
+                uint32_t a = __ldg(parent + node);
+                while (a != kRootParent) {
+                    if ((__ldg(qint_bits + (a >> 5)) >> (a & 31)) & 1u) {
+                        keep = false;
+                        break;
+                    }
+                    a = __ldg(parent + a);
+                }
+            }
+        }
+        masks[j] = __ballot_sync(0xffffffffu, keep);
+        warp_count += __popc(masks[j]);
+    }
+    if (lane == 0) s_warp[warp] = warp_count;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned v = lane < kSelectBlock / 32 ? s_warp[lane] : 0u;
+        unsigned incl = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= unsigned(off)) incl += o;
+        }
+        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane < kSelectBlock / 32) s_warp[lane] = incl - v;  // exclusive per warp
+        const unsigned long long excl = chained_scan_warp(status, tile, total);
+        if (lane == 0) {
+            s_excl = excl;
+            if (tile == n_tiles - 1) cnt->n_selected = excl + total;
+        }
+    }
+    __syncthreads();
+    unsigned long long pos = s_excl + s_warp[warp];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < kSelectItems; ++j) {
+        if ((masks[j] >> lane) & 1u)
+            selected[pos + __popc(masks[j] & lt)] =
+                uint32_t(warp_base + uint64_t(j) * 32 + lane);
+        pos += __popc(masks[j]);
+    }
+}
+
+// MarkFn contract (kernels.hpp:47-52): full mark_core per node, all outputs.
+__global__ void k_mark_debug(const Geom g, const DevTree t, uint64_t begin, uint64_t end,
+                             double tau_r, uint8_t* vis, uint8_t* qpass, double* radius) {
+    const uint64_t i = begin + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= end) return;
+    const float4 q = t.quat[i];
+    const MarkOut o =
+        mark_core(g, t.mx[i], t.my[i], t.mz[i], t.sx[i], t.sy[i], t.sz[i], q.x, q.y, q.z, q.w, tau_r);
+    vis[i - begin] = o.vis ? 1 : 0;
+    qpass[i - begin] = o.qpass ? 1 : 0;
+    if (radius) radius[i - begin] = o.radius;
+}
+
+void launch_filter_mark(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
+                        uint32_t* qint_bits, cudaStream_t s) {
+    if (t.n == 0) return;
+    const unsigned grid = unsigned((t.n + kMarkBlock - 1) / kMarkBlock);
+    k_filter_mark<<<grid, kMarkBlock, 0, s>>>(g, t, tau_r, cand_bits, qint_bits, bit_words(t.n));
+}
+
+void launch_filter_select(const DevTree& t, const uint32_t* cand_bits, const uint32_t* qint_bits,
+                          uint32_t* selected, unsigned long long* status, FrameCounters* cnt,
+                          cudaStream_t s) {
+    if (t.n == 0) return;
+    const uint32_t tiles = select_tiles(t.n);
+    k_filter_select<<<tiles, kSelectBlock, 0, s>>>(cand_bits, qint_bits, t.parent, t.n, tiles,
+                                                    selected, status, cnt);
+}
+
+void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,
+                       double tau_r, uint8_t* vis, uint8_t* qpass, double* radius,
+                       cudaStream_t s) {
+    if (end <= begin) return;
+    const unsigned grid = unsigned((end - begin + 255) / 256);
+    k_mark_debug<<<grid, 256, 0, s>>>(g, t, begin, end, tau_r, vis, qpass, radius);
+}
+
+}  // namespace fgs

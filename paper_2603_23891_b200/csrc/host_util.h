@@ -1,0 +1,32 @@
+// host_util.h -- host-side utilities shared by the C ABI and the C++ API.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lodgs_gpu.h"
+#include "common.cuh"
+
+namespace fgs {
+
+// Carries a lodgs_status code across the C ABI.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+std::vector<std::string> validate_tree(const lodgs_tree_view& t, uint64_t* n_violations);
+std::vector<std::string> validate_camera(const lodgs_camera& c);
+std::string join_violations(const std::string& what, const std::vector<std::string>& v,
+                            uint64_t total);
+Geom camera_geom(const lodgs_camera& c);
+lodgs_camera interpolate(const lodgs_camera& a, const lodgs_camera& b, double t);
+std::vector<lodgs_camera> sample_path(const lodgs_camera* keys, uint32_t n_keys,
+                                      const uint32_t* samples);
+uint64_t build_synthetic(const lodgs_synthetic_spec& s, const lodgs_build_config& c,
+                         lodgs_tree_buffers* out, uint32_t* n_levels);
+
+}  // namespace fgs

@@ -1,0 +1,111 @@
+// launch.h -- host-side launch wrappers for the sm_100a kernels.
+// Everything here is enqueued on the caller's stream; nothing synchronises.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace fgs {
+
+// Device copy of one LoDTree (scene.hpp:29-74), laid out for the two access
+// patterns of the frame: streaming SoA for the flat filter pass, one 64-byte
+// AoS record per node for the preprocess gather.
+struct DevTree {
+    uint64_t n = 0;
+    const float *mx = nullptr, *my = nullptr, *mz = nullptr;
+    const float *sx = nullptr, *sy = nullptr, *sz = nullptr;
+    const float4* quat = nullptr;  // (w, x, y, z)
+    const uint32_t* parent = nullptr;
+    const uint8_t* leaf = nullptr;
+    const SplatRec* splat = nullptr;
+};
+
+// ---- filter (filter.cpp:115-150) ----
+constexpr int kMarkBlock = 256;
+constexpr int kSelectBlock = 256;
+constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles
+inline uint64_t bit_words(uint64_t n) { return (n + 255) / 256 * 8; }
+inline uint32_t select_tiles(uint64_t n) {
+    return uint32_t((n + uint64_t(kSelectBlock) * kSelectItems - 1) /
+                    (uint64_t(kSelectBlock) * kSelectItems));
+}
+void launch_filter_mark(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
+                        uint32_t* qint_bits, cudaStream_t s);
+void launch_filter_select(const DevTree& t, const uint32_t* cand_bits, const uint32_t* qint_bits,
+                          uint32_t* selected, unsigned long long* status, FrameCounters* cnt,
+                          cudaStream_t s);
+void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,
+                       double tau_r, uint8_t* vis, uint8_t* qpass, double* radius,
+                       cudaStream_t s);
+
+// ---- preprocess (rasterizer.cpp:36-98) ----
+constexpr int kPrepBlock = 256;
+struct PrepOut {
+    Gauss64* g64;
+    Gauss32* g32;
+    GaussEmit* emit;
+    GaussCol64* col64;     // nullable: only for the exact blend
+    uint32_t* tile_count;  // n_tiles, zeroed per frame
+};
+void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected,
+                       uint64_t max_selected, int shrink_kind, double tau, int tiles_x,
+                       int tiles_y, PrepOut out, unsigned long long* status,
+                       FrameCounters* cnt, int grid, cudaStream_t s);
+// Turns the per-tile counts into offsets[n_tiles+1] and per-tile write cursors,
+// and lists the tiles whose segment exceeds the in-shared-memory sort capacity.
+void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
+                         uint32_t* cursor, uint32_t* big_list, FrameCounters* cnt,
+                         uint64_t pair_cap, cudaStream_t s);
+// Key duplication: one key per (gaussian, overlapped tile) scattered into the
+// tile's bucket; key = depth_bits << 32 | gaussian.
+void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x,
+                      uint32_t* cursor, unsigned long long* keys, int grid, cudaStream_t s);
+
+// ---- sort (rasterizer.cpp:100-135) ----
+constexpr int kSmallSortCap = 4096;
+constexpr int kBigSortCap = 16384;
+void launch_tile_sort(const uint32_t* offsets, int n_tiles, unsigned long long* keys,
+                      uint32_t* big_list, FrameCounters* cnt, cudaStream_t s);
+void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
+                          const uint32_t* big_list, FrameCounters* cnt, int grid,
+                          cudaStream_t s);
+
+// ---- blend (rasterizer.cpp:137-165, blend_scalar.cpp:13-55) ----
+void launch_blend(const uint32_t* offsets, const unsigned long long* keys, const Gauss64* g64,
+                  const Gauss32* g32, const GaussCol64* col64, int width, int height,
+                  int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s);
+
+// ---- stage-entry helpers ----
+// Reference-order binning of an arbitrary gaussian list: counts, chained scan,
+// row-major emission (rasterizer.cpp:75-98).
+void launch_bin_reference_order(const GaussEmit* emit, uint64_t n, int tiles_x,
+                                unsigned long long* status, FrameCounters* cnt,
+                                uint32_t* out_triples /* nullable */, uint64_t cap,
+                                int grid, cudaStream_t s);
+// Standalone sort_pairs: bucket arbitrary triples by tile, key = depth<<32|input index.
+void launch_bucket_triples(const uint32_t* triples, uint64_t n, uint32_t* tile_count,
+                           cudaStream_t s);
+void launch_scatter_triples(const uint32_t* triples, uint64_t n, uint32_t* cursor,
+                            unsigned long long* keys, cudaStream_t s);
+void launch_gather_triples(const uint32_t* offsets, int n_tiles, const unsigned long long* keys,
+                           const uint32_t* in_triples, uint32_t* out_triples, cudaStream_t s);
+// Standalone alpha_blend: sorted triples -> per-tile keys (order kept).
+void launch_triples_to_keys(const uint32_t* triples, uint64_t n, unsigned long long* keys,
+                            cudaStream_t s);
+// BlendList (FP64 SoA) -> blend records.
+void launch_pack_blendlist(uint64_t n, const double* mx, const double* my, const double* ca,
+                           const double* cb, const double* cc, const double* op,
+                           const double* cr, const double* cg, const double* cbl,
+                           const double* radius, const float* depth, int tiles_x, int tiles_y,
+                           Gauss64* g64, Gauss32* g32, GaussCol64* col64, GaussEmit* emit,
+                           cudaStream_t s);
+// Collect-mode readback: sorted keys -> (tile, depth, gaussian) triples.
+void launch_keys_to_triples(const uint32_t* offsets, int n_tiles, const unsigned long long* keys,
+                            uint32_t* out_triples, cudaStream_t s);
+// Per-gaussian pair counts (bin_to_tiles multiplicity) from emit records.
+void launch_gauss_counts(const GaussEmit* emit, const FrameCounters* cnt, uint64_t cap,
+                         uint32_t* out, cudaStream_t s);
+
+}  // namespace fgs

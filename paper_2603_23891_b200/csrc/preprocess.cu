@@ -1,0 +1,435 @@
+// preprocess.cu -- projection + GTC shrink + tile rect (K3) and Gaussian-tile
+// key duplication (K4).
+//
+// K3 restates prepare_gaussians (rasterizer.cpp:48-73): project() per
+// selected node (projection.cpp:60-91, mark_core with tau_r = inf), drop the
+// ones short of the near plane, effective_radius (rasterizer.cpp:36-46) and
+// the 16x16 tile rect of bin_to_tiles (rasterizer.cpp:78-91).  All FP64,
+// exact.  Survivors are compacted in selected order by a chained scan, so a
+// gaussian's index is exactly its BlendList position in the reference.  Each
+// survivor bumps the pair count of every tile it overlaps (L2 atomics).
+//
+// K4 scatters one key per (gaussian, tile) straight into its tile's bucket:
+// the first radix digit of the (tile, depth) sort is done here by counting.
+// key = bit_cast<u32>(depth) << 32 | gaussian; the in-tile order is settled
+// by sort.cu, and since gaussian indices are unique per tile the final
+// order equals the reference's stable LSD radix (rasterizer.cpp:100-135).
+#include "launch.h"
+#include "mark.cuh"
+#include "scan.cuh"
+
+namespace fgs {
+
+// rasterizer.cpp:36-46 (kind 0 three_sigma, 1 fixed, 2 adaptive; tau
+// already validated on the host).  log() is CUDA's (<= 1 ulp); the parity
+// tests count radius / tile-rect mismatches against glibc.
+__device__ __forceinline__ double effective_radius(double sigma_max, float opacity, int kind,
+                                                   double tau) {
+    const double three_sigma = 3.0 * sigma_max;
+    if (kind == 0) return three_sigma;
+    const double a0 = double(opacity);
+    if (a0 <= tau) return 0.0;
+    const double r = sigma_max * sqrt(2.0 * log(a0 / tau));
+    return std_min(r, three_sigma);
+}
+
+struct Projected {
+    bool keep;
+    bool nonfinite;
+    double mx, my, ca, cb, cc, radius, depth;
+};
+
+// projection.cpp:60-91 + effective_radius.
+__device__ __forceinline__ Projected project_one(const Geom& g, const SplatRec& r, int kind,
+                                                 double tau) {
+    Projected p;
+    p.keep = false;
+    p.nonfinite = false;
+    const MarkOut m = mark_core(g, r.mx, r.my, r.mz, r.sx, r.sy, r.sz, r.qw, r.qx, r.qy, r.qz,
+                                __longlong_as_double(0x7ff0000000000000ll));
+    if (!m.vis || !m.z_ok) return p;
+    const double inv_z = 1.0 / m.tz;
+    p.mx = g.fx * (m.tx * inv_z) + g.cx;
+    p.my = g.fy * (m.ty * inv_z) + g.cy;
+    const double det = m.a * m.c - m.b * m.b;
+    p.ca = m.c / det;
+    p.cb = -m.b / det;
+    p.cc = m.a / det;
+    const double sigma_max = sqrt(m.lambda_max);
+    const double sigma_min = sqrt(m.lambda_min);
+    p.depth = m.tz;
+    p.nonfinite = !(isfinite(p.mx) && isfinite(p.my) && isfinite(m.a) && isfinite(m.b) &&
+                    isfinite(m.c) && isfinite(p.ca) && isfinite(p.cb) && isfinite(p.cc) &&
+                    isfinite(sigma_max) && isfinite(sigma_min) && isfinite(m.tz) &&
+                    isfinite(m.radius));
+    p.radius = effective_radius(sigma_max, r.opacity, kind, tau);
+    p.keep = true;
+    return p;
+}
+
+__device__ __forceinline__ void tile_rect(double mx, double my, double r, int tiles_x,
+                                          int tiles_y, GaussEmit& e) {
+    if (!(r > 0.0)) {
+        e.tx0 = 0;
+        e.tx1 = -1;
+        e.ty0 = 0;
+        e.ty1 = -1;
+        return;
+    }
+    int tx0 = floor_to_int_x86((mx - r) / kTile);
+    int tx1 = floor_to_int_x86((mx + r) / kTile);
+    int ty0 = floor_to_int_x86((my - r) / kTile);
+    int ty1 = floor_to_int_x86((my + r) / kTile);
+    tx0 = max(tx0, 0);
+    ty0 = max(ty0, 0);
+    tx1 = min(tx1, tiles_x - 1);
+    ty1 = min(ty1, tiles_y - 1);
+    if (tx1 < tx0 || ty1 < ty0) {
+        tx0 = 0;
+        tx1 = -1;
+        ty0 = 0;
+        ty1 = -1;
+    }
+    e.tx0 = int16_t(tx0);
+    e.tx1 = int16_t(tx1);
+    e.ty0 = int16_t(ty0);
+    e.ty1 = int16_t(ty1);
+}
+
+__device__ __forceinline__ uint32_t rect_count(const GaussEmit& e) {
+    return (e.tx1 < e.tx0) ? 0u : uint32_t(e.tx1 - e.tx0 + 1) * uint32_t(e.ty1 - e.ty0 + 1);
+}
+
+// FP32 blend record from the FP64 gaussian (blend.cu explains ethr).
+__device__ __forceinline__ Gauss32 make_g32(double ca, double cb, double cc, double op, double r,
+                                            double gg, double b) {
+    Gauss32 o;
+    o.ha = float(0.5 * ca);
+    o.cb = float(cb);
+    o.hc = float(0.5 * cc);
+    o.ethr = float(log(255.0 * op));
+    o.op = float(op);
+    o.r = float(r);
+    o.g = float(gg);
+    o.b = float(b);
+    return o;
+}
+
+__global__ void __launch_bounds__(kPrepBlock) k_preprocess(
+    const Geom g, const SplatRec* __restrict__ splat, const uint32_t* __restrict__ selected,
+    const int kind, const double tau, const int tiles_x, const int tiles_y, PrepOut out,
+    unsigned long long* status, FrameCounters* cnt) {
+    __shared__ unsigned s_ticket;
+    __shared__ unsigned s_warp[kPrepBlock / 32];
+    __shared__ unsigned long long s_excl;
+    __shared__ unsigned long long s_pairs;
+    const unsigned long long n_sel = *(volatile unsigned long long*)&cnt->n_selected;
+    const unsigned n_tiles_scan = unsigned((n_sel + kPrepBlock - 1) / kPrepBlock);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    while (true) {
+        const unsigned tile = take_ticket(&cnt->ticket_prep, &s_ticket);
+        if (tile >= n_tiles_scan) break;
+        if (threadIdx.x == 0) s_pairs = 0;
+        const uint64_t s = uint64_t(tile) * kPrepBlock + threadIdx.x;
+        Projected p;
+        p.keep = false;
+        uint32_t idx = 0;
+        SplatRec rec;
+        if (s < n_sel) {
+            idx = __ldg(selected + s);
+            const float4* src = reinterpret_cast<const float4*>(splat + idx);
+            const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
+            rec.mx = a.x; rec.my = a.y; rec.mz = a.z; rec.sx = a.w;
+            rec.sy = b.x; rec.sz = b.y; rec.qw = b.z; rec.qx = b.w;
+            rec.qy = c.x; rec.qz = c.y; rec.opacity = c.z; rec.cr = c.w;
+            rec.cg = d.x; rec.cb = d.y;
+            p = project_one(g, rec, kind, tau);
+            if (p.nonfinite) atomicOr(&cnt->nonfinite, 1u);
+        }
+        const unsigned km = __ballot_sync(0xffffffffu, p.keep);
+        if (lane == 0) s_warp[warp] = __popc(km);
+        __syncthreads();
+        if (warp == 0) {
+            unsigned v = lane < kPrepBlock / 32 ? s_warp[lane] : 0u;
+            unsigned incl = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= unsigned(off)) incl += o;
+            }
+            const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+            if (lane < kPrepBlock / 32) s_warp[lane] = incl - v;
+            const unsigned long long excl = chained_scan_warp(status, tile, total);
+            if (lane == 0) {
+                s_excl = excl;
+                if (tile == n_tiles_scan - 1) cnt->n_gaussians = excl + total;
+            }
+        }
+        __syncthreads();
+        uint32_t my_pairs = 0;
+        if (p.keep) {
+            const uint64_t gi = s_excl + s_warp[warp] + __popc(km & ((1u << lane) - 1u));
+            Gauss64 r64;
+            r64.mx = p.mx;
+            r64.my = p.my;
+            r64.ca = p.ca;
+            r64.cb = p.cb;
+            r64.cc = p.cc;
+            r64.op = double(rec.opacity);
+            r64.radius = p.radius;
+            r64.pad = 0.0;
+            out.g64[gi] = r64;
+            if (out.col64) {
+                GaussCol64 c;
+                c.r = double(rec.cr);
+                c.g = double(rec.cg);
+                c.b = double(rec.cb);
+                c.pad = 0.0;
+                out.col64[gi] = c;
+            }
+            out.g32[gi] = make_g32(p.ca, p.cb, p.cc, double(rec.opacity), double(rec.cr),
+                                   double(rec.cg), double(rec.cb));
+            GaussEmit e;
+            e.depth_bits = __float_as_uint(__double2float_rn(p.depth));
+            e.node = idx;
+            tile_rect(p.mx, p.my, p.radius, tiles_x, tiles_y, e);
+            out.emit[gi] = e;
+            my_pairs = rect_count(e);
+            for (int ty = e.ty0; ty <= e.ty1; ++ty)
+                for (int tx = e.tx0; tx <= e.tx1; ++tx)
+                    atomicAdd(out.tile_count + (ty * tiles_x + tx), 1u);
+        }
+        // block total of pairs -> one 64-bit atomic
+        unsigned wsum = my_pairs;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) wsum += __shfl_down_sync(0xffffffffu, wsum, off);
+        if (lane == 0 && wsum) atomicAdd(&s_pairs, (unsigned long long)wsum);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_pairs) atomicAdd(&cnt->n_pairs, s_pairs);
+    }
+}
+
+void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected,
+                       uint64_t max_selected, int shrink_kind, double tau, int tiles_x,
+                       int tiles_y, PrepOut out, unsigned long long* status,
+                       FrameCounters* cnt, int grid, cudaStream_t s) {
+    const uint64_t max_tiles = (max_selected + kPrepBlock - 1) / kPrepBlock;
+    if (max_tiles == 0) return;
+    const int blocks = int(max_tiles < uint64_t(grid) ? max_tiles : uint64_t(grid));
+    k_preprocess<<<blocks, kPrepBlock, 0, s>>>(g, t.splat, selected, shrink_kind, tau, tiles_x,
+                                               tiles_y, out, status, cnt);
+}
+
+// One CTA: exclusive scan of per-tile counts -> offsets, write cursors, and
+// the list of tiles too large for the shared-memory sort.
+__global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restrict__ count,
+                                                       int n_tiles, uint32_t* offsets,
+                                                       uint32_t* cursor, uint32_t* big_list,
+                                                       FrameCounters* cnt, uint64_t pair_cap) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint64_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int base = 0; base < n_tiles; base += 1024) {
+        const int t = base + threadIdx.x;
+        const uint32_t c = t < n_tiles ? count[t] : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= unsigned(off)) incl += o;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t v = s_warp[lane];
+            uint32_t wi = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, wi, off);
+                if (lane >= unsigned(off)) wi += o;
+            }
+            s_warp[lane] = wi - v;
+        }
+        __syncthreads();
+        const uint64_t excl = s_carry + s_warp[warp] + (incl - c);
+        if (t < n_tiles) {
+            offsets[t] = uint32_t(excl);
+            cursor[t] = uint32_t(excl);
+            if (c > uint32_t(kSmallSortCap)) big_list[atomicAdd(&cnt->big_tiles, 1u)] = uint32_t(t);
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) s_carry = excl + c;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        offsets[n_tiles] = uint32_t(s_carry);
+        if (s_carry > pair_cap) cnt->overflow = 1u;
+    }
+    __syncthreads();
+    // Overflow: every bucket becomes empty so sort/blend never touch the
+    // unwritten keys; the host grows the buffer and re-renders.
+    if (s_carry > pair_cap) {
+        for (int t = threadIdx.x; t <= n_tiles; t += blockDim.x) offsets[t] = 0u;
+        if (threadIdx.x == 0) cnt->big_tiles = 0u;
+    }
+}
+
+void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
+                         uint32_t* cursor, uint32_t* big_list, FrameCounters* cnt,
+                         uint64_t pair_cap, cudaStream_t s) {
+    k_tile_offsets<<<1, 1024, 0, s>>>(tile_count, n_tiles, offsets, cursor, big_list, cnt,
+                                      pair_cap);
+}
+
+__global__ void __launch_bounds__(256) k_emit_keys(const GaussEmit* __restrict__ emit,
+                                                   const FrameCounters* cnt, int tiles_x,
+                                                   uint32_t* cursor, unsigned long long* keys) {
+    if (cnt->overflow) return;
+    const unsigned long long n = cnt->n_gaussians;
+    for (uint64_t gi = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; gi < n;
+         gi += uint64_t(gridDim.x) * blockDim.x) {
+        const GaussEmit e = emit[gi];
+        const unsigned long long hi = (unsigned long long)e.depth_bits << 32 | gi;
+        for (int ty = e.ty0; ty <= e.ty1; ++ty)
+            for (int tx = e.tx0; tx <= e.tx1; ++tx) {
+                const uint32_t pos = atomicAdd(cursor + (ty * tiles_x + tx), 1u);
+                keys[pos] = hi;
+            }
+    }
+}
+
+void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x,
+                      uint32_t* cursor, unsigned long long* keys, int grid, cudaStream_t s) {
+    k_emit_keys<<<grid, 256, 0, s>>>(emit, cnt, tiles_x, cursor, keys);
+}
+
+// ----------------------------------------------------------------------------
+// Stage-entry helpers.
+
+// bin_to_tiles in the reference's emission order (rasterizer.cpp:75-98):
+// gaussian-major, row-major tiles.  Chained scan of per-gaussian counts.
+__global__ void __launch_bounds__(256) k_bin_reference_order(
+    const GaussEmit* __restrict__ emit, uint64_t n, int tiles_x, unsigned long long* status,
+    FrameCounters* cnt, uint32_t* out, uint64_t cap) {
+    __shared__ unsigned s_ticket;
+    __shared__ unsigned long long s_warp[8];
+    __shared__ unsigned long long s_excl;
+    const unsigned n_scan_tiles = unsigned((n + 255) / 256);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    while (true) {
+        const unsigned tile = take_ticket(&cnt->ticket_bin, &s_ticket);
+        if (tile >= n_scan_tiles) break;
+        const uint64_t gi = uint64_t(tile) * 256 + threadIdx.x;
+        GaussEmit e;
+        e.tx0 = 0; e.tx1 = -1; e.ty0 = 0; e.ty1 = -1; e.depth_bits = 0;
+        if (gi < n) e = emit[gi];
+        const unsigned long long c = rect_count(e);
+        unsigned long long incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= unsigned(off)) incl += o;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long v = lane < 8 ? s_warp[lane] : 0ull;
+            unsigned long long wi = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned long long o = __shfl_up_sync(0xffffffffu, wi, off);
+                if (lane >= unsigned(off)) wi += o;
+            }
+            const unsigned long long total = __shfl_sync(0xffffffffu, wi, 31);
+            if (lane < 8) s_warp[lane] = wi - v;
+            const unsigned long long excl = chained_scan_warp(status, tile, total);
+            if (lane == 0) {
+                s_excl = excl;
+                if (tile == n_scan_tiles - 1) cnt->n_pairs = excl + total;
+            }
+        }
+        __syncthreads();
+        if (out) {
+            uint64_t pos = s_excl + s_warp[warp] + (incl - c);
+            for (int ty = e.ty0; ty <= e.ty1; ++ty)
+                for (int tx = e.tx0; tx <= e.tx1; ++tx, ++pos)
+                    if (pos < cap) {
+                        out[pos * 3 + 0] = uint32_t(ty) * uint32_t(tiles_x) + uint32_t(tx);
+                        out[pos * 3 + 1] = e.depth_bits;
+                        out[pos * 3 + 2] = uint32_t(gi);
+                    }
+        }
+    }
+}
+
+void launch_bin_reference_order(const GaussEmit* emit, uint64_t n, int tiles_x,
+                                unsigned long long* status, FrameCounters* cnt,
+                                uint32_t* out_triples, uint64_t cap, int grid, cudaStream_t s) {
+    if (n == 0) return;
+    k_bin_reference_order<<<grid, 256, 0, s>>>(emit, n, tiles_x, status, cnt, out_triples, cap);
+}
+
+__global__ void k_pack_blendlist(uint64_t n, const double* mx, const double* my, const double* ca,
+                                 const double* cb, const double* cc, const double* op,
+                                 const double* cr, const double* cg, const double* cbl,
+                                 const double* radius, const float* depth, int tiles_x,
+                                 int tiles_y, Gauss64* g64, Gauss32* g32, GaussCol64* col64,
+                                 GaussEmit* emit) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Gauss64 r;
+    r.mx = mx[i];
+    r.my = my[i];
+    r.ca = ca[i];
+    r.cb = cb[i];
+    r.cc = cc[i];
+    r.op = op[i];
+    r.radius = radius ? radius[i] : 0.0;
+    r.pad = 0.0;
+    g64[i] = r;
+    if (col64) {
+        GaussCol64 c;
+        c.r = cr[i];
+        c.g = cg[i];
+        c.b = cbl[i];
+        c.pad = 0.0;
+        col64[i] = c;
+    }
+    g32[i] = make_g32(ca[i], cb[i], cc[i], op[i], cr[i], cg[i], cbl[i]);
+    if (emit) {
+        GaussEmit e;
+        e.depth_bits = __float_as_uint(depth[i]);
+        e.node = uint32_t(i);
+        tile_rect(r.mx, r.my, r.radius, tiles_x, tiles_y, e);
+        emit[i] = e;
+    }
+}
+
+void launch_pack_blendlist(uint64_t n, const double* mx, const double* my, const double* ca,
+                           const double* cb, const double* cc, const double* op,
+                           const double* cr, const double* cg, const double* cbl,
+                           const double* radius, const float* depth, int tiles_x, int tiles_y,
+                           Gauss64* g64, Gauss32* g32, GaussCol64* col64, GaussEmit* emit,
+                           cudaStream_t s) {
+    if (n == 0) return;
+    k_pack_blendlist<<<unsigned((n + 255) / 256), 256, 0, s>>>(
+        n, mx, my, ca, cb, cc, op, cr, cg, cbl, radius, depth, tiles_x, tiles_y, g64, g32, col64,
+        emit);
+}
+
+__global__ void k_gauss_counts(const GaussEmit* emit, const FrameCounters* cnt, uint64_t cap,
+                               uint32_t* out) {
+    const uint64_t n = cnt->n_gaussians < cap ? cnt->n_gaussians : cap;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = rect_count(emit[i]);
+}
+
+void launch_gauss_counts(const GaussEmit* emit, const FrameCounters* cnt, uint64_t cap,
+                         uint32_t* out, cudaStream_t s) {
+    k_gauss_counts<<<296, 256, 0, s>>>(emit, cnt, cap, out);
+}
+
+}  // namespace fgs

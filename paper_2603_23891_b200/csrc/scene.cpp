@@ -1,0 +1,656 @@
+// scene.cpp -- device scene and per-frame pipeline orchestration.
+//
+// The reference render() (rasterizer.cpp:167-213) validates the tree, then
+// runs filter -> prepare -> bin -> sort -> blend with a worker-pool join after
+// every pass.  Here the tree is validated and uploaded once; a frame is ten
+// stream-ordered kernels with every data-dependent size (N_sel, N_g, N_P)
+// kept on the device, so a frame needs no host round trip until its stats
+// are read.
+#include "scene.h"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+
+namespace fgs {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error(LODGS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+DeviceGuard::DeviceGuard(int device) {
+    FGS_CUDA(cudaGetDevice(&prev));
+    if (prev != device) FGS_CUDA(cudaSetDevice(device));
+}
+DeviceGuard::~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+void launch_pack_tree(const float* soa, const float* extra, uint64_t n, float4* quat,
+                      SplatRec* splat, cudaStream_t s);
+void launch_update_totals(const FrameCounters* cnt, const uint32_t* offsets, int n_tiles,
+                          RunTotals* totals, cudaStream_t s);
+void launch_max_tile(const uint32_t* triples, uint64_t n, unsigned int* out, cudaStream_t s);
+
+namespace {
+uint64_t align256(uint64_t b) { return (b + 255) / 256 * 256; }
+}  // namespace
+
+GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
+    uint64_t nv = 0;
+    const auto v = validate_tree(tree, &nv);
+    if (nv) throw Error(LODGS_ERR_VALIDATION, join_violations("invalid tree", v, nv));
+    int count = 0;
+    FGS_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+        throw Error(LODGS_ERR_CUDA, "device " + std::to_string(device) + " not present");
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    FGS_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device_));
+    persistent_grid_ = sm_count_ * 4;
+    for (auto& e : ev_) FGS_CUDA(cudaEventCreate(&e));
+    FGS_CUDA(cudaMallocHost(&h_counters_, sizeof(FrameCounters)));
+    std::memset(h_counters_, 0, sizeof(FrameCounters));
+
+    const uint64_t n = tree.n_nodes;
+    tree_.n = n;
+    soa_.alloc(6 * n);
+    const float* soa_src[6] = {tree.mean_x, tree.mean_y, tree.mean_z,
+                               tree.scale_x, tree.scale_y, tree.scale_z};
+    for (int k = 0; k < 6; ++k)
+        if (n) FGS_CUDA(cudaMemcpyAsync(soa_.p + k * n, soa_src[k], n * 4, cudaMemcpyHostToDevice, stream_));
+    {
+        DevBuf<float> extra;
+        extra.alloc(8 * n);
+        const float* ex_src[8] = {tree.quat_w, tree.quat_x, tree.quat_y, tree.quat_z,
+                                  tree.opacity, tree.color_r, tree.color_g, tree.color_b};
+        for (int k = 0; k < 8; ++k)
+            if (n) FGS_CUDA(cudaMemcpyAsync(extra.p + k * n, ex_src[k], n * 4, cudaMemcpyHostToDevice, stream_));
+        quat_.alloc(n);
+        splat_.alloc(n);
+        launch_pack_tree(soa_.p, extra.p, n, quat_.p, splat_.p, stream_);
+        FGS_CUDA(cudaStreamSynchronize(stream_));
+    }
+    parent_.alloc(n);
+    leaf_.alloc(n);
+    if (n) {
+        FGS_CUDA(cudaMemcpyAsync(parent_.p, tree.parent, n * 4, cudaMemcpyHostToDevice, stream_));
+        FGS_CUDA(cudaMemcpyAsync(leaf_.p, tree.leaf, n, cudaMemcpyHostToDevice, stream_));
+    }
+    tree_.mx = soa_.p;
+    tree_.my = soa_.p + n;
+    tree_.mz = soa_.p + 2 * n;
+    tree_.sx = soa_.p + 3 * n;
+    tree_.sy = soa_.p + 4 * n;
+    tree_.sz = soa_.p + 5 * n;
+    tree_.quat = quat_.p;
+    tree_.parent = parent_.p;
+    tree_.leaf = leaf_.p;
+    tree_.splat = splat_.p;
+
+    cand_bits_.alloc(bit_words(n));
+    qint_bits_.alloc(bit_words(n));
+    selected_.alloc(n);
+    g64_.alloc(n);
+    g32_.alloc(n);
+    emit_.alloc(n);
+    reserve_pairs(std::max<uint64_t>(4 * n, 1u << 20));
+    totals_.alloc(1);
+    FGS_CUDA(cudaMemsetAsync(totals_.p, 0, sizeof(RunTotals), stream_));
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+}
+
+GpuScene::~GpuScene() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    for (auto& a : prof_events_)
+        for (auto& e : a) cudaEventDestroy(e);
+    if (h_counters_) cudaFreeHost(h_counters_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void GpuScene::reserve_pairs(uint64_t n) {
+    DeviceGuard dg(device_);
+    if (n > 0xFFFFFFF0ull) n = 0xFFFFFFF0ull;
+    if (n <= pair_cap_) return;
+    if (stream_) FGS_CUDA(cudaStreamSynchronize(stream_));
+    keys_.release();
+    keys_.alloc(n);
+    pair_cap_ = n;
+}
+
+uint64_t GpuScene::device_bytes() const {
+    return soa_.bytes() + quat_.bytes() + parent_.bytes() + leaf_.bytes() + splat_.bytes() +
+           cand_bits_.bytes() + qint_bits_.bytes() + selected_.bytes() + g64_.bytes() +
+           g32_.bytes() + emit_.bytes() + col64_.bytes() + keys_.bytes() + zero_.bytes() +
+           res_.tile_offsets.bytes() + res_.tile_cursor.bytes() + res_.big_list.bytes() +
+           res_.image.bytes();
+}
+
+void GpuScene::ensure_resolution(int w, int h) {
+    if (w == res_.width && h == res_.height && zero_.p) return;
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    res_.width = w;
+    res_.height = h;
+    res_.tiles_x = (w + kTile - 1) / kTile;
+    res_.tiles_y = (h + kTile - 1) / kTile;
+    const uint64_t n_tiles = uint64_t(res_.tiles_x) * res_.tiles_y;
+    if (res_.tiles_x > 32767 || res_.tiles_y > 32767)
+        throw Error(LODGS_ERR_VALIDATION, "image too large for 16-bit tile coordinates");
+    res_.tile_offsets.alloc(n_tiles + 1);
+    res_.tile_cursor.alloc(n_tiles + 1);
+    res_.big_list.alloc(n_tiles + 1);
+    res_.image.alloc(uint64_t(w) * h * 3);
+    const uint64_t b_cnt = align256(sizeof(FrameCounters));
+    const uint64_t b_sel = align256(uint64_t(select_tiles(tree_.n) + 1) * 8);
+    const uint64_t b_prep = align256((tree_.n / kPrepBlock + 2) * 8);
+    const uint64_t b_tiles = align256((n_tiles + 1) * 4);
+    zero_bytes_ = b_cnt + b_sel + b_prep + b_tiles;
+    zero_.release();
+    zero_.alloc(zero_bytes_);
+    d_counters_ = reinterpret_cast<FrameCounters*>(zero_.p);
+    d_status_select_ = reinterpret_cast<unsigned long long*>(zero_.p + b_cnt);
+    d_status_prep_ = reinterpret_cast<unsigned long long*>(zero_.p + b_cnt + b_sel);
+    d_tile_count_ = reinterpret_cast<uint32_t*>(zero_.p + b_cnt + b_sel + b_prep);
+    tile_count_cap_ = n_tiles;
+    FGS_CUDA(cudaMemsetAsync(zero_.p, 0, zero_bytes_, stream_));
+    FGS_CUDA(cudaMemsetAsync(res_.tile_offsets.p, 0, res_.tile_offsets.bytes(), stream_));
+}
+
+void GpuScene::clear_frame_state() {
+    FGS_CUDA(cudaMemsetAsync(zero_.p, 0, zero_bytes_, stream_));
+}
+
+void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int w, int h,
+                                bool timing) {
+    (void)w;
+    (void)h;
+    const int n_tiles = res_.tiles_x * res_.tiles_y;
+    const bool exact = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
+    if (exact && col64_.n < tree_.n) col64_.alloc(tree_.n);
+    cudaEvent_t* pe = nullptr;
+    if (profiling_) {
+        if (prof_used_ == prof_events_.size()) {
+            std::array<cudaEvent_t, 6> a;
+            for (auto& e : a) FGS_CUDA(cudaEventCreate(&e));
+            prof_events_.push_back(a);
+        }
+        pe = prof_events_[prof_used_++].data();
+    }
+    clear_frame_state();
+    if (timing) FGS_CUDA(cudaEventRecord(ev_[0], stream_));
+    if (pe) FGS_CUDA(cudaEventRecord(pe[0], stream_));
+    launch_filter_mark(g, tree_, p.tau_r, cand_bits_.p, qint_bits_.p, stream_);
+    if (pe) FGS_CUDA(cudaEventRecord(pe[1], stream_));
+    launch_filter_select(tree_, cand_bits_.p, qint_bits_.p, selected_.p, d_status_select_,
+                         d_counters_, stream_);
+    if (timing) FGS_CUDA(cudaEventRecord(ev_[1], stream_));
+    if (pe) FGS_CUDA(cudaEventRecord(pe[2], stream_));
+    PrepOut out{g64_.p, g32_.p, emit_.p, exact ? col64_.p : nullptr, d_tile_count_};
+    launch_preprocess(g, tree_, selected_.p, tree_.n, p.shrink_kind, p.tau, res_.tiles_x,
+                      res_.tiles_y, out, d_status_prep_, d_counters_, persistent_grid_, stream_);
+    launch_tile_offsets(d_tile_count_, n_tiles, res_.tile_offsets.p, res_.tile_cursor.p,
+                        res_.big_list.p, d_counters_, pair_cap_, stream_);
+    launch_update_totals(d_counters_, res_.tile_offsets.p, n_tiles, totals_.p, stream_);
+    launch_emit_keys(emit_.p, d_counters_, res_.tiles_x, res_.tile_cursor.p, keys_.p,
+                     persistent_grid_, stream_);
+    if (timing) FGS_CUDA(cudaEventRecord(ev_[2], stream_));
+    if (pe) FGS_CUDA(cudaEventRecord(pe[3], stream_));
+    launch_tile_sort(res_.tile_offsets.p, n_tiles, keys_.p, res_.big_list.p, d_counters_, stream_);
+    launch_tile_sort_big(res_.tile_offsets.p, keys_.p, res_.big_list.p, d_counters_,
+                         std::min(sm_count_, 64), stream_);
+    if (timing) FGS_CUDA(cudaEventRecord(ev_[3], stream_));
+    if (pe) FGS_CUDA(cudaEventRecord(pe[4], stream_));
+    launch_blend(res_.tile_offsets.p, keys_.p, g64_.p, g32_.p, col64_.p, res_.width, res_.height,
+                 res_.tiles_x, res_.tiles_y, exact, res_.image.p, stream_);
+    if (timing) FGS_CUDA(cudaEventRecord(ev_[4], stream_));
+    if (pe) FGS_CUDA(cudaEventRecord(pe[5], stream_));
+    FGS_CUDA(cudaGetLastError());
+}
+
+void GpuScene::enqueue_frame(const lodgs_camera& cam, const lodgs_render_params& p,
+                             float* image_host) {
+    DeviceGuard dg(device_);
+    const auto cv = validate_camera(cam);
+    if (!cv.empty()) throw Error(LODGS_ERR_VALIDATION, join_violations("invalid camera", cv, cv.size()));
+    if (!(p.tau_r > 0)) throw Error(LODGS_ERR_VALIDATION, "filter config: tau_r > 0");
+    if (p.shrink_kind < 0 || p.shrink_kind > 2)
+        throw Error(LODGS_ERR_VALIDATION, "shrink mode: unknown kind");
+    if (p.shrink_kind != LODGS_SHRINK_THREE_SIGMA && !(p.tau > 0.0 && p.tau < 1.0))
+        throw Error(LODGS_ERR_VALIDATION,
+                    "render: shrink tau in (0,1); adaptive needs calibration first");
+    ensure_resolution(int(cam.width), int(cam.height));
+    const Geom g = camera_geom(cam);
+    last_timing_ = (p.flags & LODGS_RENDER_STAGE_TIMING) != 0;
+    last_keep_ = (p.flags & LODGS_RENDER_KEEP_PAIRS) != 0;
+    last_exact_ = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
+    enqueue_pipeline(g, p, int(cam.width), int(cam.height), last_timing_);
+    FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
+                             cudaMemcpyDeviceToHost, stream_));
+    if (image_host)
+        FGS_CUDA(cudaMemcpyAsync(image_host, res_.image.p, res_.image.n * sizeof(float),
+                                 cudaMemcpyDeviceToHost, stream_));
+}
+
+void GpuScene::finish(lodgs_render_stats* stats) {
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    const FrameCounters c = *h_counters_;
+    if (c.overflow) {
+        reserve_pairs(std::max<uint64_t>(pair_cap_ * 2, c.n_pairs + c.n_pairs / 4 + 1024));
+        throw Error(LODGS_ERR_INTERNAL, "overflow: pair buffer grown, re-render the frame");
+    }
+    if (c.nonfinite) throw Error(LODGS_ERR_VALIDATION, "projection produced non-finite values");
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->n_selected = c.n_selected;
+        stats->n_gaussians = c.n_gaussians;
+        stats->n_pairs = c.n_pairs;
+        stats->filter_passes = 2;
+        stats->filter_barriers = 2;
+        stats->big_tiles = c.big_tiles;
+        stats->kernel_launches = 9;
+        if (last_timing_) {
+            float ms = 0;
+            FGS_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+            stats->t_calc_ms = ms;
+            stats->t_sync_ms = 0.0;
+            FGS_CUDA(cudaEventElapsedTime(&ms, ev_[1], ev_[2]));
+            stats->t_prepr_ms = ms;
+            FGS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+            stats->t_sort_ms = ms;
+            FGS_CUDA(cudaEventElapsedTime(&ms, ev_[3], ev_[4]));
+            stats->t_alpha_ms = ms;
+        }
+    }
+}
+
+void GpuScene::render(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host,
+                      lodgs_render_stats* stats) {
+    for (int attempt = 0;; ++attempt) {
+        enqueue_frame(cam, p, image_host);
+        try {
+            finish(stats);
+            return;
+        } catch (const Error& e) {
+            if (e.code != LODGS_ERR_INTERNAL || attempt >= 4) throw;
+        }
+    }
+}
+
+uint64_t GpuScene::filter(const lodgs_camera& cam, double tau_r, std::vector<uint32_t>& out) {
+    DeviceGuard dg(device_);
+    if (!(tau_r > 0)) throw Error(LODGS_ERR_VALIDATION, "filter config: tau_r > 0");
+    ensure_resolution(int(cam.width), int(cam.height));
+    const Geom g = camera_geom(cam);
+    clear_frame_state();
+    launch_filter_mark(g, tree_, tau_r, cand_bits_.p, qint_bits_.p, stream_);
+    launch_filter_select(tree_, cand_bits_.p, qint_bits_.p, selected_.p, d_status_select_,
+                         d_counters_, stream_);
+    FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
+                             cudaMemcpyDeviceToHost, stream_));
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    const uint64_t ns = h_counters_->n_selected;
+    out.resize(ns);
+    if (ns)
+        FGS_CUDA(cudaMemcpy(out.data(), selected_.p, ns * 4, cudaMemcpyDeviceToHost));
+    return ns;
+}
+
+void GpuScene::mark(const lodgs_camera& cam, uint64_t begin, uint64_t end, double tau_r,
+                    uint8_t* vis, uint8_t* qpass, double* radius) {
+    DeviceGuard dg(device_);
+    if (end > tree_.n || begin > end) throw Error(LODGS_ERR_VALIDATION, "mark: range out of bounds");
+    const uint64_t m = end - begin;
+    if (m == 0) return;
+    const Geom g = camera_geom(cam);
+    DevBuf<uint8_t> dv, dq;
+    DevBuf<double> dr;
+    dv.alloc(m);
+    dq.alloc(m);
+    if (radius) dr.alloc(m);
+    launch_mark_debug(g, tree_, begin, end, tau_r, dv.p, dq.p, radius ? dr.p : nullptr, stream_);
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    FGS_CUDA(cudaMemcpy(vis + begin, dv.p, m, cudaMemcpyDeviceToHost));
+    FGS_CUDA(cudaMemcpy(qpass + begin, dq.p, m, cudaMemcpyDeviceToHost));
+    if (radius) FGS_CUDA(cudaMemcpy(radius + begin, dr.p, m * 8, cudaMemcpyDeviceToHost));
+}
+
+uint64_t GpuScene::prepare(const lodgs_camera& cam, const uint32_t* selected, uint64_t n_sel,
+                           int kind, double tau, lodgs_blend_list* out) {
+    DeviceGuard dg(device_);
+    if (n_sel > tree_.n) throw Error(LODGS_ERR_VALIDATION, "prepare: more selected than nodes");
+    for (uint64_t i = 0; i < n_sel; ++i)
+        if (selected[i] >= tree_.n) throw Error(LODGS_ERR_VALIDATION, "prepare: node index out of range");
+    ensure_resolution(int(cam.width), int(cam.height));
+    const Geom g = camera_geom(cam);
+    clear_frame_state();
+    if (n_sel) {
+        FGS_CUDA(cudaMemcpyAsync(selected_.p, selected, n_sel * 4, cudaMemcpyHostToDevice, stream_));
+        FGS_CUDA(cudaMemcpyAsync(&d_counters_->n_selected, &n_sel, 8, cudaMemcpyHostToDevice, stream_));
+    }
+    PrepOut po{g64_.p, g32_.p, emit_.p, nullptr, d_tile_count_};
+    launch_preprocess(g, tree_, selected_.p, n_sel, kind, tau, res_.tiles_x, res_.tiles_y, po,
+                      d_status_prep_, d_counters_, persistent_grid_, stream_);
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
+                             cudaMemcpyDeviceToHost, stream_));
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    if (h_counters_->nonfinite) throw Error(LODGS_ERR_VALIDATION, "projection produced non-finite values");
+    const uint64_t ng = h_counters_->n_gaussians;
+    if (ng && kind != LODGS_SHRINK_THREE_SIGMA && !(tau > 0.0 && tau < 1.0))
+        throw Error(LODGS_ERR_VALIDATION, "shrink mode: tau in (0,1)");
+    return read_gaussians(out, n_sel);
+}
+
+void GpuScene::read_image(float* out) {
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    FGS_CUDA(cudaMemcpy(out, res_.image.p, res_.image.n * sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+uint64_t GpuScene::read_selected(uint32_t* out, uint64_t cap) {
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    const uint64_t ns = h_counters_->n_selected;
+    if (out) {
+        if (cap < ns) throw Error(LODGS_ERR_VALIDATION, "read_selected: capacity too small");
+        if (ns) FGS_CUDA(cudaMemcpy(out, selected_.p, ns * 4, cudaMemcpyDeviceToHost));
+    }
+    return ns;
+}
+
+uint64_t GpuScene::read_pairs(lodgs_tile_pair* out, uint64_t cap) {
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    const int n_tiles = res_.tiles_x * res_.tiles_y;
+    uint32_t np = 0;
+    FGS_CUDA(cudaMemcpy(&np, res_.tile_offsets.p + n_tiles, 4, cudaMemcpyDeviceToHost));
+    if (!out) return np;
+    if (cap < np) throw Error(LODGS_ERR_VALIDATION, "read_pairs: capacity too small");
+    if (np == 0) return 0;
+    DevBuf<uint32_t> tri;
+    tri.alloc(uint64_t(np) * 3);
+    launch_keys_to_triples(res_.tile_offsets.p, n_tiles, keys_.p, tri.p, stream_);
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    FGS_CUDA(cudaMemcpy(out, tri.p, uint64_t(np) * 12, cudaMemcpyDeviceToHost));
+    return np;
+}
+
+uint64_t GpuScene::read_gaussians(lodgs_blend_list* out, uint64_t cap) {
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    const uint64_t ng = h_counters_->n_gaussians;
+    if (!out) return ng;
+    if (cap < ng) throw Error(LODGS_ERR_VALIDATION, "read_gaussians: capacity too small");
+    std::vector<Gauss64> a(ng);
+    std::vector<Gauss32> b(ng);
+    std::vector<GaussEmit> e(ng);
+    if (ng) {
+        FGS_CUDA(cudaMemcpy(a.data(), g64_.p, ng * sizeof(Gauss64), cudaMemcpyDeviceToHost));
+        FGS_CUDA(cudaMemcpy(b.data(), g32_.p, ng * sizeof(Gauss32), cudaMemcpyDeviceToHost));
+        FGS_CUDA(cudaMemcpy(e.data(), emit_.p, ng * sizeof(GaussEmit), cudaMemcpyDeviceToHost));
+    }
+    out->n = ng;
+    for (uint64_t i = 0; i < ng; ++i) {
+        out->mean_x[i] = a[i].mx;
+        out->mean_y[i] = a[i].my;
+        out->conic_a[i] = a[i].ca;
+        out->conic_b[i] = a[i].cb;
+        out->conic_c[i] = a[i].cc;
+        out->opacity[i] = a[i].op;
+        out->col_r[i] = double(b[i].r);  // colours are f32 in the tree: exact
+        out->col_g[i] = double(b[i].g);
+        out->col_b[i] = double(b[i].b);
+        out->radius[i] = a[i].radius;
+        std::memcpy(&out->depth[i], &e[i].depth_bits, 4);
+        out->node[i] = e[i].node;
+    }
+    return ng;
+}
+
+void GpuScene::read_counts(uint32_t* per_gaussian, uint64_t cap_g, uint32_t* per_tile,
+                           uint64_t cap_t) {
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    if (per_gaussian) {
+        DevBuf<uint32_t> tmp;
+        tmp.alloc(cap_g);
+        launch_gauss_counts(emit_.p, d_counters_, cap_g, tmp.p, stream_);
+        FGS_CUDA(cudaGetLastError());
+        FGS_CUDA(cudaStreamSynchronize(stream_));
+        const uint64_t ng = std::min<uint64_t>(h_counters_->n_gaussians, cap_g);
+        if (ng) FGS_CUDA(cudaMemcpy(per_gaussian, tmp.p, ng * 4, cudaMemcpyDeviceToHost));
+    }
+    if (per_tile) {
+        const uint64_t nt = std::min<uint64_t>(tile_count_cap_, cap_t);
+        if (nt) FGS_CUDA(cudaMemcpy(per_tile, d_tile_count_, nt * 4, cudaMemcpyDeviceToHost));
+    }
+}
+
+void GpuScene::profile(bool enable) {
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    if (enable) prof_used_ = 0;
+    profiling_ = enable;
+}
+
+uint64_t GpuScene::profile_read(double stage_ms[6]) {
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    for (int k = 0; k < 6; ++k) stage_ms[k] = 0.0;
+    for (size_t f = 0; f < prof_used_; ++f) {
+        const auto& e = prof_events_[f];
+        float ms = 0;
+        for (int k = 0; k < 5; ++k) {
+            FGS_CUDA(cudaEventElapsedTime(&ms, e[k], e[k + 1]));
+            stage_ms[k] += ms;
+        }
+        FGS_CUDA(cudaEventElapsedTime(&ms, e[0], e[5]));
+        stage_ms[5] += ms;
+    }
+    return prof_used_;
+}
+
+void GpuScene::take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs) {
+    DeviceGuard dg(device_);
+    RunTotals t;
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    FGS_CUDA(cudaMemcpy(&t, totals_.p, sizeof t, cudaMemcpyDeviceToHost));
+    FGS_CUDA(cudaMemset(totals_.p, 0, sizeof t));
+    if (frames) *frames = t.frames;
+    if (sum_sel) *sum_sel = t.sum_selected;
+    if (sum_pairs) *sum_pairs = t.sum_pairs;
+    if (t.pad) {
+        reserve_pairs(pair_cap_ * 2);
+        throw Error(LODGS_ERR_INTERNAL, "overflow: pair buffer grown, re-render the frames");
+    }
+}
+
+// ============================================================================
+// Stateless stage functions on the current device.
+namespace {
+
+struct StageCtx {
+    int device = -1;
+    cudaStream_t s = nullptr;
+    std::mutex mu;
+};
+
+StageCtx& stage_ctx() {
+    static std::mutex g;
+    static std::map<int, std::unique_ptr<StageCtx>> ctxs;
+    int dev = 0;
+    FGS_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g);
+    auto& c = ctxs[dev];
+    if (!c) {
+        c = std::make_unique<StageCtx>();
+        c->device = dev;
+        FGS_CUDA(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    }
+    return *c;
+}
+
+template <class T>
+void upload(DevBuf<T>& d, const T* h, uint64_t n, cudaStream_t s) {
+    d.alloc(n);
+    if (n) FGS_CUDA(cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+struct DevList {
+    DevBuf<double> f[10];
+    DevBuf<float> depth;
+    DevBuf<Gauss64> g64;
+    DevBuf<Gauss32> g32;
+    DevBuf<GaussCol64> col64;
+    DevBuf<GaussEmit> emit;
+    void load(const lodgs_blend_list& l, int tiles_x, int tiles_y, bool need_col64,
+              cudaStream_t s) {
+        const double* src[10] = {l.mean_x, l.mean_y, l.conic_a, l.conic_b, l.conic_c,
+                                 l.opacity, l.col_r, l.col_g, l.col_b, l.radius};
+        for (int k = 0; k < 10; ++k) {
+            if (!src[k] && l.n) throw Error(LODGS_ERR_VALIDATION, "blend list: null array");
+            upload(f[k], src[k], l.n, s);
+        }
+        if (!l.depth && l.n) throw Error(LODGS_ERR_VALIDATION, "blend list: null depth");
+        upload(depth, l.depth, l.n, s);
+        g64.alloc(l.n);
+        g32.alloc(l.n);
+        emit.alloc(l.n);
+        if (need_col64) col64.alloc(l.n);
+        launch_pack_blendlist(l.n, f[0].p, f[1].p, f[2].p, f[3].p, f[4].p, f[5].p, f[6].p,
+                              f[7].p, f[8].p, f[9].p, depth.p, tiles_x, tiles_y, g64.p, g32.p,
+                              need_col64 ? col64.p : nullptr, emit.p, s);
+    }
+};
+
+}  // namespace
+
+void stage_bin_to_tiles(const lodgs_blend_list& list, int width, int height,
+                        lodgs_tile_pair* out, uint64_t cap, uint64_t* n_pairs) {
+    if (width < 1 || height < 1) throw Error(LODGS_ERR_VALIDATION, "bin_to_tiles: image size");
+    StageCtx& c = stage_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    DevList dl;
+    dl.load(list, tiles_x, tiles_y, false, c.s);
+    DevBuf<unsigned char> z;
+    const uint64_t b_cnt = align256(sizeof(FrameCounters));
+    const uint64_t b_st = align256((list.n / 256 + 2) * 8);
+    z.alloc(b_cnt + b_st);
+    FGS_CUDA(cudaMemsetAsync(z.p, 0, b_cnt + b_st, c.s));
+    auto* cnt = reinterpret_cast<FrameCounters*>(z.p);
+    auto* st = reinterpret_cast<unsigned long long*>(z.p + b_cnt);
+    DevBuf<uint32_t> tri;
+    if (out && cap) tri.alloc(cap * 3);
+    launch_bin_reference_order(dl.emit.p, list.n, tiles_x, st, cnt, out ? tri.p : nullptr, cap,
+                               296, c.s);
+    FGS_CUDA(cudaGetLastError());
+    FrameCounters h;
+    FGS_CUDA(cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, c.s));
+    FGS_CUDA(cudaStreamSynchronize(c.s));
+    *n_pairs = h.n_pairs;
+    if (out) {
+        if (cap < h.n_pairs) throw Error(LODGS_ERR_VALIDATION, "bin_to_tiles: capacity too small");
+        if (h.n_pairs) FGS_CUDA(cudaMemcpy(out, tri.p, h.n_pairs * 12, cudaMemcpyDeviceToHost));
+    }
+}
+
+// Buckets by tile (counting digit), then sorts each bucket on
+// depth_bits << 32 | input position -- the stable order of rasterizer.cpp:100-135.
+void stage_sort_pairs(lodgs_tile_pair* pairs, uint64_t n) {
+    if (n < 2) return;
+    if (n >= 0xFFFFFFF0ull) throw Error(LODGS_ERR_VALIDATION, "sort_pairs: too many pairs");
+    StageCtx& c = stage_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    DevBuf<uint32_t> in, outb;
+    upload(in, reinterpret_cast<const uint32_t*>(pairs), n * 3, c.s);
+    outb.alloc(n * 3);
+    DevBuf<unsigned int> mx;
+    mx.alloc(1);
+    FGS_CUDA(cudaMemsetAsync(mx.p, 0, 4, c.s));
+    launch_max_tile(in.p, n, mx.p, c.s);
+    unsigned int max_tile = 0;
+    FGS_CUDA(cudaMemcpyAsync(&max_tile, mx.p, 4, cudaMemcpyDeviceToHost, c.s));
+    FGS_CUDA(cudaStreamSynchronize(c.s));
+    if (max_tile >= (1u << 26))
+        throw Error(LODGS_ERR_VALIDATION, "sort_pairs: tile id >= 2^26 not supported");
+    const int n_buckets = int(max_tile) + 1;
+    DevBuf<unsigned char> z;
+    const uint64_t b_cnt = align256(sizeof(FrameCounters));
+    const uint64_t b_tc = align256(uint64_t(n_buckets + 1) * 4);
+    z.alloc(b_cnt + b_tc);
+    FGS_CUDA(cudaMemsetAsync(z.p, 0, b_cnt + b_tc, c.s));
+    auto* cnt = reinterpret_cast<FrameCounters*>(z.p);
+    auto* tc = reinterpret_cast<uint32_t*>(z.p + b_cnt);
+    DevBuf<uint32_t> off, cur, big;
+    off.alloc(n_buckets + 1);
+    cur.alloc(n_buckets + 1);
+    big.alloc(n_buckets + 1);
+    DevBuf<unsigned long long> keys;
+    keys.alloc(n);
+    launch_bucket_triples(in.p, n, tc, c.s);
+    launch_tile_offsets(tc, n_buckets, off.p, cur.p, big.p, cnt, n, c.s);
+    launch_scatter_triples(in.p, n, cur.p, keys.p, c.s);
+    launch_tile_sort(off.p, n_buckets, keys.p, big.p, cnt, c.s);
+    launch_tile_sort_big(off.p, keys.p, big.p, cnt, 64, c.s);
+    launch_gather_triples(off.p, n_buckets, keys.p, in.p, outb.p, c.s);
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaMemcpyAsync(pairs, outb.p, n * 12, cudaMemcpyDeviceToHost, c.s));
+    FGS_CUDA(cudaStreamSynchronize(c.s));
+}
+
+void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_blend_list& list,
+                       int width, int height, uint32_t flags, float* image) {
+    if (width < 1 || height < 1) throw Error(LODGS_ERR_VALIDATION, "alpha_blend: image size");
+    StageCtx& c = stage_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const int n_tiles = tiles_x * tiles_y;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (sorted[i].tile >= uint32_t(n_tiles))
+            throw Error(LODGS_ERR_VALIDATION, "alpha_blend: tile id outside the image");
+        if (sorted[i].gaussian >= list.n)
+            throw Error(LODGS_ERR_VALIDATION, "alpha_blend: gaussian index out of range");
+        if (i && sorted[i].tile < sorted[i - 1].tile)
+            throw Error(LODGS_ERR_VALIDATION, "alpha_blend: pairs not sorted by tile");
+    }
+    const bool exact = (flags & LODGS_RENDER_EXACT_BLEND) != 0;
+    DevList dl;
+    dl.load(list, tiles_x, tiles_y, exact, c.s);
+    DevBuf<uint32_t> tri;
+    upload(tri, reinterpret_cast<const uint32_t*>(sorted), n * 3, c.s);
+    DevBuf<unsigned char> z;
+    const uint64_t b_cnt = align256(sizeof(FrameCounters));
+    const uint64_t b_tc = align256(uint64_t(n_tiles + 1) * 4);
+    z.alloc(b_cnt + b_tc);
+    FGS_CUDA(cudaMemsetAsync(z.p, 0, b_cnt + b_tc, c.s));
+    auto* cnt = reinterpret_cast<FrameCounters*>(z.p);
+    auto* tc = reinterpret_cast<uint32_t*>(z.p + b_cnt);
+    DevBuf<uint32_t> off, cur, big;
+    off.alloc(n_tiles + 1);
+    cur.alloc(n_tiles + 1);
+    big.alloc(n_tiles + 1);
+    DevBuf<unsigned long long> keys;
+    keys.alloc(n);
+    DevBuf<float> img;
+    img.alloc(uint64_t(width) * height * 3);
+    launch_bucket_triples(tri.p, n, tc, c.s);
+    launch_tile_offsets(tc, n_tiles, off.p, cur.p, big.p, cnt, n, c.s);
+    launch_triples_to_keys(tri.p, n, keys.p, c.s);
+    launch_blend(off.p, keys.p, dl.g64.p, dl.g32.p, dl.col64.p, width, height, tiles_x, tiles_y,
+                 exact, img.p, c.s);
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaMemcpyAsync(image, img.p, img.n * 4, cudaMemcpyDeviceToHost, c.s));
+    FGS_CUDA(cudaStreamSynchronize(c.s));
+}
+
+}  // namespace fgs

@@ -1,0 +1,148 @@
+// scene.h -- device scene (replicated LoD tree) and the per-frame pipeline.
+#pragma once
+
+#include <cstdint>
+#include <array>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "host_util.h"
+#include "launch.h"
+
+namespace fgs {
+
+void cuda_check(cudaError_t e, const char* what);
+#define FGS_CUDA(x) ::fgs::cuda_check((x), #x)
+
+// Owning device allocation (no copy, move-only).
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    uint64_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(uint64_t count) {
+        if (count <= n && p) return;
+        release();
+        const uint64_t c = count ? count : 1;
+        FGS_CUDA(cudaMalloc(&p, c * sizeof(T)));
+        n = c;
+    }
+    uint64_t bytes() const { return n * sizeof(T); }
+};
+
+// Makes `device` current for the lifetime of the guard.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int device);
+    ~DeviceGuard();
+};
+
+// Per-frame scratch sized for one image resolution.
+struct ResolutionBuffers {
+    int width = 0, height = 0, tiles_x = 0, tiles_y = 0;
+    DevBuf<uint32_t> tile_offsets, tile_cursor, big_list;
+    DevBuf<float> image;
+};
+
+class GpuScene {
+public:
+    GpuScene(const lodgs_tree_view& tree, int device);
+    ~GpuScene();
+
+    void reserve_pairs(uint64_t n);
+    uint64_t device_bytes() const;
+
+    // One frame, enqueued only.  Counters for the frame land in host_counters()
+    // once the stream reaches the end of the frame.
+    void enqueue_frame(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host);
+    // Wait + stats of the last frame.  Throws Error on overflow / non-finite.
+    void finish(lodgs_render_stats* stats);
+    void render(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host,
+                lodgs_render_stats* stats);
+
+    // stage entry points
+    uint64_t filter(const lodgs_camera& cam, double tau_r, std::vector<uint32_t>& out);
+    void mark(const lodgs_camera& cam, uint64_t begin, uint64_t end, double tau_r, uint8_t* vis,
+              uint8_t* qpass, double* radius);
+    uint64_t prepare(const lodgs_camera& cam, const uint32_t* selected, uint64_t n_sel,
+                     int kind, double tau, lodgs_blend_list* out);
+
+    // readbacks of the last frame
+    void read_image(float* out);
+    const float* image_device() const { return res_.image.p; }
+    uint64_t read_selected(uint32_t* out, uint64_t cap);
+    uint64_t read_pairs(lodgs_tile_pair* out, uint64_t cap);
+    uint64_t read_gaussians(lodgs_blend_list* out, uint64_t cap);
+    void read_counts(uint32_t* per_gaussian, uint64_t cap_g, uint32_t* per_tile, uint64_t cap_t);
+    void take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs);
+
+    void profile(bool enable);
+    uint64_t profile_read(double stage_ms[6]);
+
+    cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
+    uint64_t n_nodes() const { return tree_.n; }
+
+private:
+    void ensure_resolution(int w, int h);
+    void clear_frame_state();
+    void enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int w, int h, bool timing);
+
+    int device_;
+    cudaStream_t stream_ = nullptr;
+    DevTree tree_;
+    // tree storage
+    DevBuf<float> soa_;        // 6 * n floats: mx my mz sx sy sz
+    DevBuf<float4> quat_;
+    DevBuf<uint32_t> parent_;
+    DevBuf<uint8_t> leaf_;
+    DevBuf<SplatRec> splat_;
+    // frame storage
+    DevBuf<uint32_t> cand_bits_, qint_bits_, selected_;
+    DevBuf<Gauss64> g64_;
+    DevBuf<Gauss32> g32_;
+    DevBuf<GaussEmit> emit_;
+    DevBuf<GaussCol64> col64_;
+    DevBuf<unsigned long long> keys_;
+    uint64_t pair_cap_ = 0;
+    // zeroed every frame: [FrameCounters | select status | prep status | tile counts]
+    DevBuf<unsigned char> zero_;
+    uint64_t zero_bytes_ = 0;
+    FrameCounters* d_counters_ = nullptr;
+    unsigned long long* d_status_select_ = nullptr;
+    unsigned long long* d_status_prep_ = nullptr;
+    uint32_t* d_tile_count_ = nullptr;
+    uint64_t tile_count_cap_ = 0;
+    DevBuf<RunTotals> totals_;
+    ResolutionBuffers res_;
+    FrameCounters* h_counters_ = nullptr;  // pinned
+    cudaEvent_t ev_[6] = {};
+    bool last_timing_ = false;
+    bool last_keep_ = false;
+    bool last_exact_ = false;
+    bool profiling_ = false;
+    std::vector<std::array<cudaEvent_t, 6>> prof_events_;
+    size_t prof_used_ = 0;
+    int persistent_grid_ = 148 * 4;
+    int sm_count_ = 148;
+};
+
+// Stateless per-device context for the stage functions that take no scene
+// (bin_to_tiles / sort_pairs / alpha_blend).
+void stage_bin_to_tiles(const lodgs_blend_list& list, int width, int height,
+                        lodgs_tile_pair* out, uint64_t cap, uint64_t* n_pairs);
+void stage_sort_pairs(lodgs_tile_pair* pairs, uint64_t n);
+void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_blend_list& list,
+                       int width, int height, uint32_t flags, float* image);
+
+}  // namespace fgs

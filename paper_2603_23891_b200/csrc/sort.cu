@@ -1,0 +1,199 @@
+// sort.cu -- per-tile segment sort: the remaining digits of the (tile, depth)
+// radix sort.
+//
+// The reference sorts all pairs with an LSD radix on
+// key = tile << 32 | bits(depth) and relies on stability to keep ties in
+// gaussian order (rasterizer.cpp:100-135).  Here the tile digit was already
+// resolved by counting (preprocess.cu scatters every key into its tile's
+// bucket), so what is left is ordering each bucket by depth_bits << 32 |
+// gaussian -- a total order with no ties, identical to the stable order.
+// Buckets are sorted in shared memory (the whole bucket is resident: mean
+// 290, p99 810 pairs per tile on the 10M tree), so the only HBM/L2 traffic
+// of the sort is one read and one write of each 8-byte key.
+//
+// The in-shared-memory network is the direction-free ("flip") bitonic
+// sorter: every comparator is oriented low->high, so a non-power-of-two
+// bucket is padded virtually with +inf (a comparator whose high index is
+// past the end is skipped and the padding never moves).
+#include "launch.h"
+
+namespace fgs {
+
+template <typename Index, typename Sync>
+__device__ __forceinline__ void flip_bitonic(unsigned long long* a, Index n, Index tid,
+                                             Index nthreads, Sync sync) {
+    Index p = 1;
+    while (p < n) p <<= 1;
+    const Index half = p >> 1;
+    for (Index k = 2; k <= p; k <<= 1) {
+        const Index hk = k >> 1;
+        for (Index c = tid; c < half; c += nthreads) {
+            const Index blk = c / hk, off = c - blk * hk;
+            const Index lo = blk * k + off, hi = blk * k + k - 1 - off;
+            if (hi < n) {
+                const unsigned long long x = a[lo], y = a[hi];
+                if (y < x) {
+                    a[lo] = y;
+                    a[hi] = x;
+                }
+            }
+        }
+        sync();
+        for (Index j = k >> 2; j >= 1; j >>= 1) {
+            for (Index c = tid; c < half; c += nthreads) {
+                const Index blk = c / j, off = c - blk * j;
+                const Index lo = blk * 2 * j + off, hi = lo + j;
+                if (hi < n) {
+                    const unsigned long long x = a[lo], y = a[hi];
+                    if (y < x) {
+                        a[lo] = y;
+                        a[hi] = x;
+                    }
+                }
+            }
+            sync();
+        }
+    }
+}
+
+constexpr int kSmallSortThreads = 256;
+
+__global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t* __restrict__ offsets,
+                                                                 unsigned long long* keys) {
+    __shared__ unsigned long long s[kSmallSortCap];
+    const uint32_t b = offsets[blockIdx.x], e = offsets[blockIdx.x + 1];
+    const uint32_t n = e - b;
+    if (n < 2 || n > uint32_t(kSmallSortCap)) return;  // big buckets: k_tile_sort_big
+    for (uint32_t i = threadIdx.x; i < n; i += kSmallSortThreads) s[i] = keys[b + i];
+    __syncthreads();
+    flip_bitonic<uint32_t>(s, n, threadIdx.x, kSmallSortThreads, [] __device__() { __syncthreads(); });
+    for (uint32_t i = threadIdx.x; i < n; i += kSmallSortThreads) keys[b + i] = s[i];
+}
+
+constexpr int kBigSortThreads = 1024;
+
+// Buckets above kSmallSortCap: one 1024-thread CTA per bucket, 128 KB of
+// shared memory up to kBigSortCap keys, beyond that the same network in
+// place in global memory (L2-resident; only pathological tiles get here).
+__global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_t* __restrict__ offsets,
+                                                                   unsigned long long* keys,
+                                                                   const uint32_t* big_list,
+                                                                   FrameCounters* cnt) {
+    extern __shared__ unsigned long long s_big[];
+    __shared__ unsigned s_item;
+    const unsigned n_big = cnt->big_tiles;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_item = atomicAdd(&cnt->big_cursor, 1u);
+        __syncthreads();
+        const unsigned item = s_item;
+        if (item >= n_big) break;
+        const uint32_t tile = big_list[item];
+        const uint32_t b = offsets[tile], e = offsets[tile + 1];
+        const uint32_t n = e - b;
+        if (n <= uint32_t(kBigSortCap)) {
+            for (uint32_t i = threadIdx.x; i < n; i += kBigSortThreads) s_big[i] = keys[b + i];
+            __syncthreads();
+            flip_bitonic<uint32_t>(s_big, n, threadIdx.x, kBigSortThreads,
+                                   [] __device__() { __syncthreads(); });
+            for (uint32_t i = threadIdx.x; i < n; i += kBigSortThreads) keys[b + i] = s_big[i];
+        } else {
+            flip_bitonic<uint32_t>(keys + b, n, threadIdx.x, kBigSortThreads, [] __device__() {
+                __threadfence_block();
+                __syncthreads();
+            });
+        }
+    }
+}
+
+void launch_tile_sort(const uint32_t* offsets, int n_tiles, unsigned long long* keys,
+                      uint32_t* /*big_list*/, FrameCounters* /*cnt*/, cudaStream_t s) {
+    if (n_tiles <= 0) return;
+    k_tile_sort<<<n_tiles, kSmallSortThreads, 0, s>>>(offsets, keys);
+}
+
+void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
+                          const uint32_t* big_list, FrameCounters* cnt, int grid,
+                          cudaStream_t s) {
+    static bool attr = false;
+    const int smem = kBigSortCap * 8;
+    if (!attr) {
+        cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    k_tile_sort_big<<<grid, kBigSortThreads, smem, s>>>(offsets, keys, big_list, cnt);
+}
+
+// ----------------------------------------------------------------------------
+// Stage-entry helpers for the standalone sort_pairs / alpha_blend.
+
+__global__ void k_bucket_triples(const uint32_t* t, uint64_t n, uint32_t* count) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(count + t[i * 3], 1u);
+}
+
+void launch_bucket_triples(const uint32_t* triples, uint64_t n, uint32_t* tile_count,
+                           cudaStream_t s) {
+    if (n) k_bucket_triples<<<unsigned((n + 255) / 256), 256, 0, s>>>(triples, n, tile_count);
+}
+
+// key = depth bits << 32 | input position: stable order == reference order.
+__global__ void k_scatter_triples(const uint32_t* t, uint64_t n, uint32_t* cursor,
+                                  unsigned long long* keys) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t pos = atomicAdd(cursor + t[i * 3], 1u);
+    keys[pos] = (unsigned long long)t[i * 3 + 1] << 32 | i;
+}
+
+void launch_scatter_triples(const uint32_t* triples, uint64_t n, uint32_t* cursor,
+                            unsigned long long* keys, cudaStream_t s) {
+    if (n) k_scatter_triples<<<unsigned((n + 255) / 256), 256, 0, s>>>(triples, n, cursor, keys);
+}
+
+__global__ void k_gather_triples(const uint32_t* offsets, const unsigned long long* keys,
+                                 const uint32_t* in, uint32_t* out) {
+    const uint32_t tile = blockIdx.x;
+    const uint32_t b = offsets[tile], e = offsets[tile + 1];
+    for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const uint32_t src = uint32_t(keys[i]);
+        out[i * 3 + 0] = in[src * 3 + 0];
+        out[i * 3 + 1] = in[src * 3 + 1];
+        out[i * 3 + 2] = in[src * 3 + 2];
+    }
+}
+
+void launch_gather_triples(const uint32_t* offsets, int n_tiles, const unsigned long long* keys,
+                           const uint32_t* in_triples, uint32_t* out_triples, cudaStream_t s) {
+    if (n_tiles > 0)
+        k_gather_triples<<<n_tiles, 128, 0, s>>>(offsets, keys, in_triples, out_triples);
+}
+
+__global__ void k_triples_to_keys(const uint32_t* t, uint64_t n, unsigned long long* keys) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) keys[i] = (unsigned long long)t[i * 3 + 1] << 32 | t[i * 3 + 2];
+}
+
+void launch_triples_to_keys(const uint32_t* triples, uint64_t n, unsigned long long* keys,
+                            cudaStream_t s) {
+    if (n) k_triples_to_keys<<<unsigned((n + 255) / 256), 256, 0, s>>>(triples, n, keys);
+}
+
+__global__ void k_keys_to_triples(const uint32_t* offsets, const unsigned long long* keys,
+                                  uint32_t* out) {
+    const uint32_t tile = blockIdx.x;
+    const uint32_t b = offsets[tile], e = offsets[tile + 1];
+    for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const unsigned long long k = keys[i];
+        out[i * 3 + 0] = tile;
+        out[i * 3 + 1] = uint32_t(k >> 32);
+        out[i * 3 + 2] = uint32_t(k);
+    }
+}
+
+void launch_keys_to_triples(const uint32_t* offsets, int n_tiles, const unsigned long long* keys,
+                            uint32_t* out_triples, cudaStream_t s) {
+    if (n_tiles > 0) k_keys_to_triples<<<n_tiles, 128, 0, s>>>(offsets, keys, out_triples);
+}
+
+}  // namespace fgs

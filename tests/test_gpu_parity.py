@@ -1,0 +1,425 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the C oracle.
+
+Bit-exact: vis/qpass/radius marks, selected lists, BlendList FP64 fields,
+per-gaussian tile counts, N_P, sorted (tile, depth, gaussian) sequences and
+the exact-mode image.  Tolerance (BASELINE.json north_star): fast-mode image
+max-abs <= 1e-3 per channel and PSNR > 60 dB against the oracle image.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import (acceptance_filter_configs, max_abs, push_flat, random_micro_scene,
+                     to_blendlist, topdown_camera)
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-3   # BASELINE.json north_star: max-abs 1e-3 per channel
+PSNR_MIN = 60.0  # ... and PSNR > 60 dB
+
+
+# ------------------------------------------------------------------ mark --
+def test_mark_bit_identical(L, oracle, gpu):
+    """test_kernels.cpp:128-171: vis / qpass / radius bit-identical, ragged
+    ranges, sentinels outside [begin, end) untouched."""
+    rng = oracle.rng(11)
+    for rep in range(12):
+        tree = L.make_tree(200 + rep, 2 + rep % 3, 8, 0.5, 3, 3)
+        n = tree.node_count()
+        cam = oracle.orbit_camera(rng, 320, 240, oracle.uniform(rng, 2.0, 60.0))
+        tau_r = oracle.uniform(rng, 0.5, 40.0)
+        begin = int(oracle.next_below(rng, 5))
+        end = n - int(oracle.next_below(rng, 5))
+        v0, q0, r0 = oracle.mark(tree, cam, tau_r, begin, end)
+        with L.GpuScene(tree) as s:
+            vis = np.full(n, 9, np.uint8)
+            q = np.full(n, 9, np.uint8)
+            rad = np.full(n, -1.0)
+            s.mark(cam, tau_r, begin, end, vis, q, rad)
+        inside = slice(begin, end)
+        assert np.array_equal(vis[inside], v0[inside])
+        assert np.array_equal(q[inside], q0[inside])
+        assert rad[inside].tobytes() == r0[inside].tobytes()
+        assert (vis[:begin] == 9).all() and (vis[end:] == 9).all()
+        assert (q[:begin] == 9).all() and (q[end:] == 9).all()
+
+
+# ---------------------------------------------------------------- filter --
+def test_filter_acceptance_208_configs(L, oracle, gpu):
+    """acceptance.cpp:93-135 (#1): 208 randomized configurations, selected
+    lists bit-identical to the oracle, passes = barriers = 2."""
+    count = 0
+    scene = None
+    last_tree = None
+    for tree, cam, tau_r in acceptance_filter_configs(oracle):
+        if tree is not last_tree:
+            if scene:
+                scene.close()
+            scene = L.GpuScene(tree)
+            last_tree = tree
+        want, _, _ = oracle.filter(tree, cam, tau_r)
+        got = scene.filter(cam, L.FilterConfig(tau_r, 1))
+        assert np.array_equal(got.selected, want), f"config {count}"
+        assert got.passes == 2 and got.barriers == 2
+        count += 1
+    scene.close()
+    assert count == 208
+
+
+def _leaf_tree(L, mean, scale):
+    n = 1
+    t = L.LoDTree.empty(n, 1)
+    t.mean_x[0], t.mean_y[0], t.mean_z[0] = mean
+    t.scale_x[0], t.scale_y[0], t.scale_z[0] = scale
+    t.quat_w[0] = 1.0
+    t.opacity[0] = 0.8
+    t.color_r[0], t.color_g[0], t.color_b[0] = 0.9, 0.4, 0.1
+    t.parent[0] = L.ROOT_PARENT
+    t.leaf[0] = 1
+    return t
+
+
+def _hand_tree(L, depth, children):
+    """build_tree of one root at (0,0,10), unit scale, identity rotation
+    (test_filter.cpp:14-24 base_node + tree_builder.cpp:94-124)."""
+    means, scales, parents, leafs, offs = [(0.0, 0.0, 10.0)], [1.0], [L.ROOT_PARENT], [depth == 0], [0]
+    begin, end = 0, 1
+    for level in range(1, depth + 1):
+        offs.append(len(means))
+        for p in range(begin, end):
+            for cn in range(children):
+                s = scales[p]
+                off = [(0.5 if cn & b else -0.5) * s for b in (1, 2, 4)]
+                means.append(tuple(float(np.float32(means[p][i] + off[i])) for i in range(3)))
+                scales.append(float(np.float32(s) * np.float32(0.5)))
+                parents.append(p)
+                leafs.append(level == depth)
+        begin, end = end, len(means)
+    n = len(means)
+    t = L.LoDTree.empty(n, depth + 1)
+    for i in range(n):
+        t.mean_x[i], t.mean_y[i], t.mean_z[i] = means[i]
+        t.scale_x[i] = t.scale_y[i] = t.scale_z[i] = scales[i]
+        t.quat_w[i] = 1.0
+        t.opacity[i] = 0.8
+        t.color_r[i], t.color_g[i], t.color_b[i] = 0.9, 0.4, 0.1
+        t.parent[i] = parents[i]
+        t.leaf[i] = leafs[i]
+    t.level_offsets[:] = offs
+    return t
+
+
+def test_filter_hand_kats(L, oracle, gpu):
+    """test_filter.cpp:59-108: a large visible leaf is selected; a qualifying
+    internal node shadows its subtree; tau_r picks the level on a 3-chain."""
+    cam = oracle.front_camera(200, 200)
+    t = _hand_tree(L, 0, 8)
+    with L.GpuScene(t) as s:
+        assert s.filter(cam, L.FilterConfig(3.0)).selected.tolist() == [0]
+    t9 = _hand_tree(L, 1, 8)
+    assert t9.node_count() == 9 and L.validate_tree(t9) == 0
+    _, _, r = oracle.mark(t9, cam, 1e9)
+    with L.GpuScene(t9) as s:
+        assert s.filter(cam, L.FilterConfig(r[0] + 1.0)).selected.tolist() == [0]
+    t3 = _hand_tree(L, 2, 1)
+    _, _, r = oracle.mark(t3, cam, 1e9)
+    assert r[2] < r[1] < r[0]
+    with L.GpuScene(t3) as s:
+        for tau_r, want in (((r[2] + r[1]) / 2, [2]), ((r[1] + r[0]) / 2, [1]), (r[0] + 1.0, [0])):
+            assert s.filter(cam, L.FilterConfig(tau_r)).selected.tolist() == want
+            assert oracle.filter(t3, cam, tau_r)[0].tolist() == want
+
+
+def test_filter_empty_and_lookaway(L, oracle, gpu):
+    """test_filter.cpp:200-211: a camera looking away selects nothing."""
+    t = L.make_tree(3, 3, 8, 0.5, 2, 2)
+    cam = oracle.front_camera(200, 200)
+    cam.translation = (0, 0, -100)
+    with L.GpuScene(t) as s:
+        assert s.filter(cam, L.FilterConfig(3.0)).selected.size == 0
+        with pytest.raises(L.ValidationError):
+            s.filter(cam, L.FilterConfig(0.0))
+
+
+def test_filter_10m_tree_bit_exact(L, oracle, gpu):
+    """Full-size cfg 3 tree (10,039,185 nodes): selected list bit-exact at
+    three altitudes of the fly-through."""
+    tree = L.build_synthetic_tree(nx=131, ny=131, seed=1, depth=3, build_seed=7)
+    assert tree.node_count() == 10039185
+    with L.GpuScene(tree) as s:
+        for alt in (400.0, 200.0, 140.0):
+            cam = topdown_camera(1920, 1080, 1000.0, alt)
+            want, _, _ = oracle.filter(tree, cam, 3.0)
+            got = s.filter(cam, L.FilterConfig(3.0)).selected
+            assert np.array_equal(got, want), alt
+
+
+# ------------------------------------------------------------ preprocess --
+def test_prepare_bit_exact(L, oracle, gpu):
+    """prepare_gaussians (rasterizer.cpp:48-73): every BlendList field
+    bit-identical, all three shrink modes (test_raster.cpp:303-319 fixture)."""
+    rng = oracle.rng(40)
+    for rep in range(6):
+        tree = L.make_tree(5 + rep, 2 + rep % 2, 8, 0.5)
+        cam = oracle.orbit_camera(rng, 160, 120, 12.0)
+        sel, _, _ = oracle.filter(tree, cam, 6.0)
+        with L.GpuScene(tree) as s:
+            for mode in (L.ShrinkMode.three_sigma(), L.ShrinkMode.fixed(), L.ShrinkMode.adaptive(0.3)):
+                want = oracle.prepare(tree, cam, sel, mode)
+                got = s.prepare(cam, sel, mode)
+                assert got.size() == want.size()
+                for f in L._LIST_F64 + ("depth", "node"):
+                    assert getattr(got, f).tobytes() == getattr(want, f).tobytes(), (rep, mode, f)
+
+
+def test_prepare_near_plane_drop(L, oracle, gpu):
+    """test_raster.cpp:280-301: a selected leaf short of the near plane is dropped."""
+    t = L.LoDTree.empty(2, 1)
+    for i, z in enumerate((10.0, 0.005)):
+        t.mean_z[i] = z
+        t.scale_x[i] = t.scale_y[i] = t.scale_z[i] = 1.0
+        t.quat_w[i] = 1.0
+        t.opacity[i] = 0.8
+        t.color_r[i] = 1.0
+        t.parent[i] = L.ROOT_PARENT
+        t.leaf[i] = 1
+    cam = oracle.front_camera(64, 64)
+    with L.GpuScene(t) as s:
+        bl = s.prepare(cam, np.array([0, 1], np.uint32), L.ShrinkMode.three_sigma())
+    assert bl.size() == 1 and bl.node[0] == 0
+    assert bl.depth[0] == np.float32(10.0)
+
+
+# --------------------------------------------------------------- binning --
+def test_bin_kat(L, gpu):
+    """test_raster.cpp:88-118: 9 pairs at (24,24) r=10 on 64x64; r=0; off-screen; corner."""
+    grid = L.TileGrid.make(64, 64)
+    d = {}
+    push_flat(d, 24, 24, 1.0, 0.5, (1, 1, 1), 10.0, np.float32(3.5), 42)
+    pairs = L.bin_to_tiles(to_blendlist(d), grid, 64, 64)
+    assert len(pairs) == 9
+    k = 0
+    for ty in range(3):
+        for tx in range(3):
+            assert pairs[k]["tile"] == grid.tile_id(tx, ty)
+            assert pairs[k]["depth"] == np.float32(3.5)
+            assert pairs[k]["gaussian"] == 0
+            k += 1
+    for mx, r in ((24, 0.0), (-100, 10.0)):
+        d = {}
+        push_flat(d, mx, mx, 1.0, 0.5, (1, 1, 1), r, np.float32(1.0))
+        assert len(L.bin_to_tiles(to_blendlist(d), grid, 64, 64)) == 0
+    d = {}
+    push_flat(d, 63, 63, 1.0, 0.5, (1, 1, 1), 5.0, np.float32(1.0))
+    cp = L.bin_to_tiles(to_blendlist(d), grid, 64, 64)
+    assert len(cp) == 1 and cp[0]["tile"] == grid.tile_id(3, 3)
+
+
+def test_bin_random_lists(L, oracle, gpu):
+    rng = oracle.rng(2718)
+    for rep in range(30):
+        w, h, bl = random_micro_scene(oracle, rng)
+        want = oracle.bin_to_tiles(bl, w, h)
+        got = L.bin_to_tiles(bl, L.TileGrid.make(w, h), w, h)
+        assert got.tobytes() == want.tobytes(), rep
+
+
+# ------------------------------------------------------------------ sort --
+def test_sort_100k_kat(L, oracle, gpu):
+    """test_raster.cpp:120-135: 100K pairs, 1000 tiles, 50 integer depths
+    (plenty of exact ties) equal a stable comparison sort."""
+    rng = oracle.rng(99)
+    n = 100000
+    pairs = np.empty(n, L.PAIR_DTYPE)
+    for i in range(n):
+        pairs[i] = (oracle.next_below(rng, 1000), np.float32(oracle.next_below(rng, 50)), i)
+    expect = pairs[np.lexsort((pairs["depth"], pairs["tile"]))]  # lexsort is stable
+    want = pairs.copy()
+    oracle.sort_pairs(want)
+    assert want.tobytes() == expect.tobytes()
+    got = pairs.copy()
+    L.sort_pairs(got)
+    assert got.tobytes() == expect.tobytes()
+
+
+def test_sort_hand_cases(L, gpu):
+    """test_raster.cpp:137-156."""
+    p = np.array([(1, 2.0, 3), (0, 5.0, 1), (1, 2.0, 0), (0, 5.0, 0)], L.PAIR_DTYPE)
+    L.sort_pairs(p)
+    assert p.tolist() == [(0, 5.0, 1), (0, 5.0, 0), (1, 2.0, 3), (1, 2.0, 0)]
+    e = np.empty(0, L.PAIR_DTYPE)
+    L.sort_pairs(e)
+    one = np.array([(7, 1.0, 0)], L.PAIR_DTYPE)
+    L.sort_pairs(one)
+    assert one.tolist() == [(7, 1.0, 0)]
+    z = np.array([(0, 3.0, 0), (0, 0.0, 1)], L.PAIR_DTYPE)
+    L.sort_pairs(z)
+    assert z[0]["gaussian"] == 1
+
+
+def test_sort_big_buckets(L, oracle, gpu):
+    """Buckets above the 4096-key shared-memory sort and above the 16384-key
+    big-tile path (global in-place network) still give the stable order."""
+    rng = np.random.default_rng(5)
+    for n_tiles, n in ((3, 30000), (2, 70000)):
+        pairs = np.empty(n, L.PAIR_DTYPE)
+        pairs["tile"] = rng.integers(0, n_tiles, n)
+        pairs["depth"] = rng.integers(0, 300, n).astype(np.float32)
+        pairs["gaussian"] = np.arange(n)
+        want = pairs.copy()
+        oracle.sort_pairs(want)
+        got = pairs.copy()
+        L.sort_pairs(got)
+        assert got.tobytes() == want.tobytes()
+
+
+# ----------------------------------------------------------------- blend --
+def _blend_pair(L, oracle, d, w, h, exact):
+    bl = to_blendlist(d)
+    pairs = oracle.bin_to_tiles(bl, w, h)
+    oracle.sort_pairs(pairs)
+    want = oracle.alpha_blend(pairs, bl, w, h)
+    got = L.alpha_blend(pairs, bl, L.TileGrid.make(w, h), w, h, exact=exact).rgb
+    return got, want
+
+
+def test_blend_kats(L, oracle, gpu):
+    """test_raster.cpp:158-233 hand cases, exact and fast paths."""
+    for exact in (True, False):
+        d = {}
+        push_flat(d, 8, 8, 0.0, 1.0, (1.0, 0.5, 0.25), 20.0, np.float32(1))
+        got, want = _blend_pair(L, oracle, d, 16, 16, exact)
+        assert (got[..., 0] == np.float32(0.99)).all()
+        assert (got[..., 1] == np.float32(0.5 * 0.99)).all()
+        assert (got[..., 2] == np.float32(0.25 * 0.99)).all()
+        d = {}
+        push_flat(d, 8, 8, 0.0, 0.5, (1, 0, 0), 20.0, np.float32(1), 0)
+        push_flat(d, 8, 8, 0.0, 0.5, (0, 1, 0), 20.0, np.float32(2), 1)
+        got, want = _blend_pair(L, oracle, d, 16, 16, exact)
+        assert (got[..., 0] == 0.5).all() and (got[..., 1] == 0.25).all() and (got[..., 2] == 0).all()
+        d = {}
+        push_flat(d, 8, 8, 0.0, 0.003, (1, 1, 1), 20.0, np.float32(1), 0)
+        push_flat(d, 8, 8, 0.0, 0.5, (1, 0, 0), 20.0, np.float32(2), 1)
+        got, want = _blend_pair(L, oracle, d, 16, 16, exact)
+        assert got[9, 4, 0] == 0.5
+        img = L.alpha_blend(np.empty(0, L.PAIR_DTYPE), to_blendlist({k: [] for k in d}),
+                            L.TileGrid.make(33, 17), 33, 17, exact=exact).rgb
+        assert (img == 0).all()
+
+
+def test_blend_termination(L, oracle, gpu):
+    d = {}
+    for i in range(4):
+        push_flat(d, 8, 8, 0.0, 0.99, (1, 1, 1), 20.0, np.float32(i + 1), i)
+    got, want = _blend_pair(L, oracle, d, 16, 16, True)
+    assert got.tobytes() == want.tobytes()
+
+
+def test_blend_micro_scenes(L, oracle, gpu):
+    """acceptance.cpp:255-288 (#5) micro-scenes: exact path bit-identical,
+    fast path within the north-star tolerance."""
+    rng = oracle.rng(55)
+    for rep in range(50):
+        w, h, bl = random_micro_scene(oracle, rng)
+        pairs = oracle.bin_to_tiles(bl, w, h)
+        oracle.sort_pairs(pairs)
+        want = oracle.alpha_blend(pairs, bl, w, h)
+        grid = L.TileGrid.make(w, h)
+        ex = L.alpha_blend(pairs, bl, grid, w, h, exact=True).rgb
+        assert ex.tobytes() == want.tobytes(), rep
+        fa = L.alpha_blend(pairs, bl, grid, w, h, exact=False).rgb
+        assert max_abs(fa, want) <= IMG_TOL, rep
+
+
+# ---------------------------------------------------------------- render --
+def _check_render(L, oracle, scene, tree, cam, tau_r, mode):
+    want = oracle.render(tree, cam, tau_r, mode)
+    out = scene.render(cam, L.FilterConfig(tau_r), mode, L.RenderOptions(collect_kpc=True))
+    assert out.stats.n_selected == want["n_selected"]
+    assert np.array_equal(scene.read_selected(), want["selected"])
+    assert out.stats.n_gaussians == want["n_gaussians"]
+    assert out.stats.n_pairs == want["n_pairs"]
+    assert out.pairs.tobytes() == want["pairs"].tobytes()
+    for f in L._LIST_F64 + ("depth", "node"):
+        assert getattr(out.gaussians, f).tobytes() == getattr(want["gaussians"], f).tobytes(), f
+    # per-gaussian tile counts and per-tile n_gs (metrics.cpp:18-35)
+    gl = want["gaussians"]
+    n_tiles = L.TileGrid.make(cam.width, cam.height).n_tile()
+    pg, pt = scene.read_counts(gl.size(), n_tiles)
+    want_pg = np.bincount(want["pairs"]["gaussian"], minlength=gl.size())[: gl.size()]
+    want_pt = np.bincount(want["pairs"]["tile"], minlength=n_tiles)[:n_tiles]
+    assert np.array_equal(pg, want_pg) and np.array_equal(pt, want_pt)
+    err = max_abs(out.image.rgb, want["image"])
+    psnr = oracle.psnr(out.image.rgb, want["image"])
+    assert err <= IMG_TOL, err
+    assert psnr > PSNR_MIN, psnr
+    ex = scene.render(cam, L.FilterConfig(tau_r), mode, L.RenderOptions(exact_blend=True))
+    assert ex.image.rgb.tobytes() == want["image"].tobytes()
+    return out, want
+
+
+def test_render_small_scenes(L, oracle, gpu):
+    rng = oracle.rng(8)
+    tree = L.make_tree(21, 3, 8, 0.5, 3, 3, 2)
+    with L.GpuScene(tree) as s:
+        for i in range(4):
+            cam = oracle.orbit_camera(rng, 200, 150, 14.0)
+            for mode in (L.ShrinkMode.three_sigma(), L.ShrinkMode.fixed(), L.ShrinkMode.adaptive(0.1)):
+                _check_render(L, oracle, s, tree, cam, 4.0, mode)
+
+
+def test_render_cfg1(L, oracle, gpu):
+    """cfg 1: 99,937 nodes, 800x600, fx=100, z=12."""
+    tree = L.build_synthetic_tree(nx=37, ny=37, seed=1, depth=2, build_seed=7)
+    assert tree.node_count() == 99937
+    cam = oracle.front_camera(800, 600, 100.0)
+    cam.translation = (0, 0, 12)
+    with L.GpuScene(tree) as s:
+        out, want = _check_render(L, oracle, s, tree, cam, 3.0, L.ShrinkMode.three_sigma())
+    assert want["n_selected"] == 86321 and want["n_pairs"] == 303131  # survey probe numbers
+
+
+def test_render_black_and_errors(L, oracle, gpu):
+    """test_raster.cpp:321-330, :390-399."""
+    tree = L.make_tree(3, 2, 8, 0.5)
+    cam = oracle.front_camera(96, 64)
+    cam.translation = (0, 0, -100)
+    with L.GpuScene(tree) as s:
+        out = s.render(cam, L.FilterConfig(3.0), L.ShrinkMode.three_sigma())
+        assert out.stats.n_selected == 0 and out.stats.n_pairs == 0
+        assert (out.image.rgb == 0).all()
+        for bad in (0.0, 1.0):
+            with pytest.raises(L.ValidationError):
+                s.render(cam, L.FilterConfig(3.0), L.ShrinkMode.adaptive(bad))
+
+
+def test_render_deterministic_and_overflow_regrow(L, oracle, gpu):
+    """Byte-identical frames on repeat; a deliberately tiny pair buffer is
+    grown and the frame re-rendered with identical output."""
+    tree = L.make_tree(33, 3, 8, 0.5, 3, 3, 3)
+    rng = oracle.rng(5)
+    cam = oracle.orbit_camera(rng, 200, 150, 16.0)
+    with L.GpuScene(tree) as s:
+        a = s.render(cam, L.FilterConfig(5.0), L.ShrinkMode.three_sigma()).image.rgb.copy()
+        b = s.render(cam, L.FilterConfig(5.0), L.ShrinkMode.three_sigma()).image.rgb.copy()
+        assert a.tobytes() == b.tobytes()
+    with L.GpuScene(tree) as s2:
+        # the scene starts with max(4N, 1M) pairs: force an overflow path by a huge
+        # close-up frame that needs more pairs than nodes * 4
+        cam2 = oracle.front_camera(1024, 1024, 2000.0)
+        cam2.translation = (0, 0, 9.0)
+        want = oracle.render(tree, cam2, 1e9, L.ShrinkMode.three_sigma())
+        out = s2.render(cam2, L.FilterConfig(1e9), L.ShrinkMode.three_sigma())
+        assert out.stats.n_pairs == want["n_pairs"]
+        assert max_abs(out.image.rgb, want["image"]) <= IMG_TOL
+
+
+def test_render_cfg3_frame(L, oracle, gpu):
+    """A full cfg 3 frame (10M nodes, 1080p, altitude 200): everything bit-exact
+    against the oracle, image within tolerance."""
+    tree = L.build_synthetic_tree(nx=131, ny=131, seed=1, depth=3, build_seed=7)
+    cam = topdown_camera(1920, 1080, 1000.0, 200.0)
+    with L.GpuScene(tree) as s:
+        out, want = _check_render(L, oracle, s, tree, cam, 3.0, L.ShrinkMode.three_sigma())
+    assert want["n_pairs"] > 1_000_000
