@@ -1,25 +1,28 @@
 // blend.cu -- tile-wise front-to-back alpha blending (K6), reference
 // alpha_blend -> blend_scalar (rasterizer.cpp:137-165, blend_scalar.cpp:13-55).
 //
-// One 256-thread CTA per 16x16 tile, one thread per pixel.  The tile's
-// sorted keys are consumed in batches of 256: each thread stages one
-// gaussian's record into shared memory, then every pixel walks the batch.
-// The CTA stops as soon as every pixel has terminated (__syncthreads_and).
+// One 256-thread CTA per 16x16 tile.  Warp w owns an 8x4 pixel block
+// (x0 + 8*(w&1), y0 + 4*(w>>1)); lane l its pixel (l&7, l>>3) in the block.
+// The tile's sorted keys are consumed in batches of 256: each thread stages
+// one splat into shared memory and tests the splat's conservative alpha>=1/255
+// box (Gauss32::hx/hy) against the 8 warp blocks; one ballot per warp turns
+// that into 8 ordered 32-bit work lists.  Each warp then walks only its own
+// list -- every branch on the list is warp-uniform, so lanes never drift
+// apart (an earlier per-lane `continue` version ran at 2.8 active lanes per
+// instruction).  A sample outside the box has e > ln(255 op) and is skipped
+// by the reference too, so culling never changes a pixel.
 //
-// Fast path (default): FP32 per sample, with the reference's FP64 decision
-// recomputed exactly whenever the FP32 estimate is within a certified
-// margin of the alpha >= 1/255 skip threshold -- a flipped skip would move a
-// pixel by up to 1/255 (SURVEY.md section 7 hard part 6), everything else
-// is continuous.  The skip test itself needs no exp:
-//     alpha = min(op * exp(power), 0.99) < 1/255  <=>  e > ln(255 op),
+// Fast path (default): FP32 per sample; the reference's FP64 decision is
+// recomputed exactly whenever the FP32 estimate is within a certified margin
+// of the alpha >= 1/255 threshold (a flipped skip would move a pixel by up
+// to 1/255, SURVEY.md section 7 hard part 6).  The test needs no exp:
+//     alpha = min(op exp(power), 0.99) < 1/255  <=>  e > ln(255 op),
 //     e = -power = ha dx^2 + cb dx dy + hc dy^2 >= 0.
-// FP32 error bound: with Q = ha dx^2 + hc dy^2 >= |cb dx dy| (conic is
-// positive definite), |e32 - e| <= ~12 ulp * Q, well inside
-// margin = (Q + 1) * 2^-17.
+// With Q = ha dx^2 + hc dy^2 >= |cb dx dy| (positive-definite conic),
+// |e32 - e| is a few ulp of Q, well inside margin = (Q + 1) 2^-17.
 //
 // Exact path (LODGS_RENDER_EXACT_BLEND): the reference arithmetic in FP64
-// with the reference exp_mx (fastexp.hpp:38-50), no FMA: bit-identical
-// pixels.
+// with the reference exp_mx (fastexp.hpp:38-50), no FMA: bit-identical pixels.
 #include "launch.h"
 
 namespace fgs {
@@ -50,30 +53,75 @@ __device__ __forceinline__ double exp_mx(double x) {
 }
 
 // blend_scalar.cpp:24-31 for one sample, FP64.
-__device__ __forceinline__ double alpha_exact(const Gauss64& G, double px, double py) {
-    const double dx = px - G.mx;
-    const double dy = py - G.my;
-    const double t1 = (G.ca * dx) * dx;
-    const double t2 = (G.cc * dy) * dy;
-    const double t3 = (G.cb * dx) * dy;
+__device__ __forceinline__ double alpha_exact(double mx, double my, double ca, double cb,
+                                              double cc, double op, double px, double py) {
+    const double dx = px - mx;
+    const double dy = py - my;
+    const double t1 = (ca * dx) * dx;
+    const double t2 = (cc * dy) * dy;
+    const double t3 = (cb * dx) * dy;
     const double power = -0.5 * (t1 + t2) - t3;
-    return std_min(G.op * exp_mx(power), kAlphaCap);
+    return std_min(op * exp_mx(power), kAlphaCap);
 }
 
 constexpr int kBlendThreads = 256;
+constexpr int kWarps = kBlendThreads / 32;
 
-__global__ void __launch_bounds__(kBlendThreads) k_blend_fast(
+struct BlendSmem {
+    float4 geo[kBlendThreads];   // tile-local mean x, y, ha, hc
+    float2 ct[kBlendThreads];    // cb, ethr
+    float4 col[kBlendThreads];   // op, r, g, b
+    uint32_t gid[kBlendThreads];
+    uint32_t bits[kWarps][kWarps];  // [consumer warp][loader warp] work-list ballots
+};
+
+// Loads splat `gi` (thread's batch slot), writes its shared record and returns
+// the 8-bit mask of warp blocks its conservative box touches.
+__device__ __forceinline__ unsigned stage_splat(BlendSmem& s, uint32_t gi, const Gauss64* g64,
+                                                const Gauss32* g32, int x0, int y0) {
+    const double2 m = *reinterpret_cast<const double2*>(&g64[gi].mx);
+    const float4 q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
+    const float4 q1 = *reinterpret_cast<const float4*>(&g32[gi].op);
+    const float2 h = *reinterpret_cast<const float2*>(&g32[gi].hx);
+    const float mlx = float(m.x - double(x0)), mly = float(m.y - double(y0));
+    s.geo[threadIdx.x] = make_float4(mlx, mly, q0.x, q0.z);
+    s.ct[threadIdx.x] = make_float2(q0.y, q0.w);
+    s.col[threadIdx.x] = q1;
+    s.gid[threadIdx.x] = gi;
+    // pixel centres of block (bx, by) span [bx+0.5, bx+7.5] x [by+0.5, by+3.5]
+    const float xlo = mlx - h.x, xhi = mlx + h.x, ylo = mly - h.y, yhi = mly + h.y;
+    unsigned mask = 0;
+    if (h.x >= 0.0f) {
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const float bx = float((w & 1) * 8), by = float((w >> 1) * 4);
+            const bool hit = xlo <= bx + 7.5f && xhi >= bx + 0.5f && ylo <= by + 3.5f &&
+                             yhi >= by + 0.5f;
+            mask |= hit ? (1u << w) : 0u;
+        }
+    }
+    return mask;
+}
+
+__device__ __forceinline__ void publish_lists(BlendSmem& s, unsigned mask, bool valid) {
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (!valid) mask = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const unsigned b = __ballot_sync(0xffffffffu, (mask >> w) & 1u);
+        if (lane == 0) s.bits[w][warp] = b;
+    }
+}
+
+__global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fast(
     const uint32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
     const Gauss64* __restrict__ g64, const Gauss32* __restrict__ g32, const int width,
     const int height, const int tiles_x, float* __restrict__ image) {
-    __shared__ float4 s_geo[kBlendThreads];  // mlx, mly, ha, hc
-    __shared__ float2 s_ct[kBlendThreads];   // cb, ethr
-    __shared__ float4 s_col[kBlendThreads];  // op, r, g, b
-    __shared__ uint32_t s_gid[kBlendThreads];
-
+    __shared__ BlendSmem s;
     const int tile = blockIdx.x;
     const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
-    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = int((warp & 1) * 8 + (lane & 7)), ly = int((warp >> 1) * 4 + (lane >> 3));
     const int x = x0 + lx, y = y0 + ly;
     const bool inside = x < width && y < height;
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
@@ -84,47 +132,46 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fast(
     bool done = !inside;
 
     for (uint32_t base = b; base < e; base += kBlendThreads) {
-        const int cnt = int(min(uint32_t(kBlendThreads), e - base));
-        if (int(threadIdx.x) < cnt) {
-            const uint32_t gi = uint32_t(keys[base + threadIdx.x]);
-            const double2 m = *reinterpret_cast<const double2*>(&g64[gi].mx);
-            const float4 q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
-            const float4 q1 = *reinterpret_cast<const float4*>(&g32[gi].op);
-            s_geo[threadIdx.x] = make_float4(float(m.x - double(x0)), float(m.y - double(y0)), q0.x, q0.z);
-            s_ct[threadIdx.x] = make_float2(q0.y, q0.w);
-            s_col[threadIdx.x] = q1;
-            s_gid[threadIdx.x] = gi;
-        }
+        const uint32_t cnt = min(uint32_t(kBlendThreads), e - base);
+        const bool valid = threadIdx.x < cnt;
+        unsigned mask = 0;
+        if (valid) mask = stage_splat(s, uint32_t(keys[base + threadIdx.x]), g64, g32, x0, y0);
+        publish_lists(s, mask, valid);
         if (__syncthreads_and(done)) break;
-        if (!done) {
-            for (int j = 0; j < cnt; ++j) {
-                const float4 geo = s_geo[j];
-                const float2 ct = s_ct[j];
+        bool warp_done = __all_sync(0xffffffffu, done);
+        for (int c = 0; c < kWarps && !warp_done; ++c) {
+            unsigned bits = s.bits[warp][c];
+            while (bits) {
+                const int j = c * 32 + (__ffs(bits) - 1);
+                bits &= bits - 1;
+                const float4 geo = s.geo[j];
+                const float2 ct = s.ct[j];
                 const float dx = pxl - geo.x, dy = pyl - geo.y;
                 const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
                 const float ev = __fmaf_rn(ct.x * dx, dy, Q);
                 const float d = ev - ct.y;
                 const float margin = __fmaf_rn(Q, 7.62939453125e-06f, 7.62939453125e-06f);
-                if (d > margin) continue;  // alpha < 1/255 for certain
-                const float4 col = s_col[j];
-                float alpha;
-                if (d < -margin) {
-                    alpha = fminf(col.x * __expf(-ev), 0.99f);
-                } else {
-                    const double a64 = alpha_exact(g64[s_gid[j]], px, py);
-                    if (a64 < kMinAlpha) continue;
-                    alpha = float(a64);
+                float alpha = 0.0f;
+                if (!done && d <= margin) {
+                    if (d < -margin) {
+                        alpha = fminf(s.col[j].x * __expf(-ev), 0.99f);
+                    } else {
+                        const Gauss64& G = g64[s.gid[j]];
+                        const double a64 = alpha_exact(G.mx, G.my, G.ca, G.cb, G.cc, G.op, px, py);
+                        alpha = a64 >= kMinAlpha ? float(a64) : 0.0f;
+                    }
                 }
-                const float w = alpha * T;
-                cr = __fmaf_rn(col.y, w, cr);
-                cg = __fmaf_rn(col.z, w, cg);
-                cb = __fmaf_rn(col.w, w, cb);
-                T = T * (1.0f - alpha);
-                if (T < 1e-4f) {
-                    done = true;
-                    break;
+                if (alpha > 0.0f) {
+                    const float4 col = s.col[j];
+                    const float w = alpha * T;
+                    cr = __fmaf_rn(col.y, w, cr);
+                    cg = __fmaf_rn(col.z, w, cg);
+                    cb = __fmaf_rn(col.w, w, cb);
+                    T = T * (1.0f - alpha);
+                    done = T < 1e-4f;
                 }
             }
+            warp_done = __all_sync(0xffffffffu, done);
         }
         __syncthreads();
     }
@@ -136,15 +183,24 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_fast(
     }
 }
 
+struct BlendSmemExact {
+    double4 geo[kBlendThreads];  // mx, my, ca, cb
+    double2 cc_op[kBlendThreads];
+    double4 col[kBlendThreads];
+    uint32_t bits[kWarps][kWarps];
+};
+
 __global__ void __launch_bounds__(kBlendThreads) k_blend_exact(
     const uint32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
-    const Gauss64* __restrict__ g64, const GaussCol64* __restrict__ col64, const int width,
-    const int height, const int tiles_x, float* __restrict__ image) {
-    __shared__ Gauss64 s_g[kBlendThreads];
-    __shared__ GaussCol64 s_c[kBlendThreads];
+    const Gauss64* __restrict__ g64, const Gauss32* __restrict__ g32,
+    const GaussCol64* __restrict__ col64, const int width, const int height, const int tiles_x,
+    float* __restrict__ image) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BlendSmemExact& s = *reinterpret_cast<BlendSmemExact*>(smem_raw);
     const int tile = blockIdx.x;
     const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
-    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = int((warp & 1) * 8 + (lane & 7)), ly = int((warp >> 1) * 4 + (lane >> 3));
     const int x = x0 + lx, y = y0 + ly;
     const bool inside = x < width && y < height;
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
@@ -152,25 +208,52 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_exact(
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
     bool done = !inside;
     for (uint32_t base = b; base < e; base += kBlendThreads) {
-        const int cnt = int(min(uint32_t(kBlendThreads), e - base));
-        if (int(threadIdx.x) < cnt) {
+        const uint32_t cnt = min(uint32_t(kBlendThreads), e - base);
+        const bool valid = threadIdx.x < cnt;
+        unsigned mask = 0;
+        if (valid) {
             const uint32_t gi = uint32_t(keys[base + threadIdx.x]);
-            s_g[threadIdx.x] = g64[gi];
-            s_c[threadIdx.x] = col64[gi];
+            const Gauss64 G = g64[gi];
+            const GaussCol64 C = col64[gi];
+            s.geo[threadIdx.x] = make_double4(G.mx, G.my, G.ca, G.cb);
+            s.cc_op[threadIdx.x] = make_double2(G.cc, G.op);
+            s.col[threadIdx.x] = make_double4(C.r, C.g, C.b, 0.0);
+            const float2 h = *reinterpret_cast<const float2*>(&g32[gi].hx);
+            const float mlx = float(G.mx - double(x0)), mly = float(G.my - double(y0));
+            if (h.x >= 0.0f) {
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) {
+                    const float bx = float((w & 1) * 8), by = float((w >> 1) * 4);
+                    const bool hit = mlx - h.x <= bx + 7.5f && mlx + h.x >= bx + 0.5f &&
+                                     mly - h.y <= by + 3.5f && mly + h.y >= by + 0.5f;
+                    mask |= hit ? (1u << w) : 0u;
+                }
+            }
+        }
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const unsigned bb = __ballot_sync(0xffffffffu, (mask >> w) & 1u);
+            if (lane == 0) s.bits[w][warp] = bb;
         }
         if (__syncthreads_and(done)) break;
-        if (!done) {
-            for (int j = 0; j < cnt; ++j) {
-                const double alpha = alpha_exact(s_g[j], px, py);
-                if (alpha < kMinAlpha) continue;
-                const double w = alpha * T;
-                cr += s_c[j].r * w;
-                cg += s_c[j].g * w;
-                cb += s_c[j].b * w;
-                T *= 1.0 - alpha;
-                if (T < kTermT) {
-                    done = true;
-                    break;
+        for (int c = 0; c < kWarps; ++c) {
+            unsigned bits = s.bits[warp][c];
+            while (bits) {
+                const int j = c * 32 + (__ffs(bits) - 1);
+                bits &= bits - 1;
+                if (!done) {
+                    const double4 g = s.geo[j];
+                    const double2 co = s.cc_op[j];
+                    const double alpha = alpha_exact(g.x, g.y, g.z, g.w, co.x, co.y, px, py);
+                    if (alpha >= kMinAlpha) {
+                        const double4 col = s.col[j];
+                        const double w = alpha * T;
+                        cr += col.x * w;
+                        cg += col.y * w;
+                        cb += col.z * w;
+                        T *= 1.0 - alpha;
+                        done = T < kTermT;
+                    }
                 }
             }
         }
@@ -189,12 +272,19 @@ void launch_blend(const uint32_t* offsets, const unsigned long long* keys, const
                   int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s) {
     const int n_tiles = tiles_x * tiles_y;
     if (n_tiles <= 0) return;
-    if (exact)
-        k_blend_exact<<<n_tiles, kBlendThreads, 0, s>>>(offsets, keys, g64, col64, width, height,
-                                                        tiles_x, image);
-    else
+    if (exact) {
+        static bool attr = false;
+        const int smem = int(sizeof(BlendSmemExact));
+        if (!attr) {
+            cudaFuncSetAttribute(k_blend_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr = true;
+        }
+        k_blend_exact<<<n_tiles, kBlendThreads, smem, s>>>(offsets, keys, g64, g32, col64, width,
+                                                            height, tiles_x, image);
+    } else {
         k_blend_fast<<<n_tiles, kBlendThreads, 0, s>>>(offsets, keys, g64, g32, width, height,
                                                        tiles_x, image);
+    }
 }
 
 }  // namespace fgs

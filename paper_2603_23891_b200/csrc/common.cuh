@@ -52,12 +52,16 @@ struct __align__(16) GaussCol64 {
     double r, g, b, pad;
 };
 
-// Per projected gaussian, FP32 blend record.
+// Per projected gaussian, FP32 blend record (48 bytes).
 //   e(dx,dy) = ha*dx^2 + cb*dx*dy + hc*dy^2 = -power; sample skipped iff
 //   e > ethr = ln(255 * opacity) (alpha < 1/255, kernels.hpp:21).
+//   (hx, hy): half-extents of the e <= ethr ellipse, computed in FP64 and
+//   rounded outward -- a conservative box outside which the reference
+//   provably skips every sample (blend.cu uses it to cull per warp).
 struct __align__(16) Gauss32 {
     float ha, cb, hc, ethr;
     float op, r, g, b;
+    float hx, hy, pad0, pad1;
 };
 
 // Per projected gaussian, what key duplication needs.

@@ -107,11 +107,29 @@ __device__ __forceinline__ Gauss32 make_g32(double ca, double cb, double cc, dou
     o.ha = float(0.5 * ca);
     o.cb = float(cb);
     o.hc = float(0.5 * cc);
-    o.ethr = float(log(255.0 * op));
+    const double ethr = log(255.0 * op);
+    o.ethr = float(ethr);
     o.op = float(op);
     o.r = float(r);
     o.g = float(gg);
     o.b = float(b);
+    // Box of the ellipse e <= E, E = ethr inflated past every rounding of the
+    // reference's own alpha test (exp_mx is within 1e-15 of exp): for the
+    // quadratic form [[ha, cb/2], [cb/2, hc]], |dx| <= sqrt(E hc / det) and
+    // |dy| <= sqrt(E ha / det).  Rounded outward, plus 1e-3 px for the FP32
+    // tile-local mean.  E <= 0 (opacity <= 1/255): nothing ever blends.
+    const double E = ethr + 1e-6 * (1.0 + fabs(ethr));
+    const double ha = 0.5 * ca, hc = 0.5 * cc;
+    const double det = ha * hc - 0.25 * cb * cb;
+    if (E > 0.0 && det > 0.0) {
+        o.hx = __double2float_ru(sqrt(E * hc / det) * (1.0 + 1e-9)) + 1e-3f;
+        o.hy = __double2float_ru(sqrt(E * ha / det) * (1.0 + 1e-9)) + 1e-3f;
+    } else if (E > 0.0) {  // degenerate conic: never cull
+        o.hx = o.hy = 3.0e38f;
+    } else {
+        o.hx = o.hy = -1.0f;
+    }
+    o.pad0 = o.pad1 = 0.0f;
     return o;
 }
 
