@@ -19,7 +19,66 @@
 
 namespace fgs {
 
-__global__ void __launch_bounds__(kMarkBlock) k_filter_mark(const Geom g, const DevTree t,
+// FP32 copy of the camera for the certified pre-test.
+struct GeomF {
+    float r[9], t[3];
+    float p2x, p2z, p3x, p3z, p4y, p4z, p5y, p5z;  // side-plane coefficients
+    float znear, zfar;
+    float c0;  // max(|t_i|, znear, zfar) + 1: magnitude term of the error bound
+};
+
+GeomF make_geomf(const Geom& g) {
+    GeomF f;
+    for (int i = 0; i < 9; ++i) f.r[i] = float(g.rot[i]);
+    double c0 = 0.0;
+    for (int i = 0; i < 3; ++i) {
+        f.t[i] = float(g.trans[i]);
+        c0 = fmax(c0, fabs(g.trans[i]));
+    }
+    f.p2x = float(g.planes[2][0]);
+    f.p2z = float(g.planes[2][2]);
+    f.p3x = float(g.planes[3][0]);
+    f.p3z = float(g.planes[3][2]);
+    f.p4y = float(g.planes[4][1]);
+    f.p4z = float(g.planes[4][2]);
+    f.p5y = float(g.planes[5][1]);
+    f.p5z = float(g.planes[5][2]);
+    f.znear = float(g.znear);
+    f.zfar = float(g.zfar);
+    f.c0 = float(fmax(c0, fmax(g.znear, g.zfar)) + 1.0);
+    return f;
+}
+
+// Certified FP32 frustum pre-test.  With |R_ij| <= 1 and unit plane normals,
+// every FP32 camera-space coordinate is within B = 2^-20 (|x|+|y|+|z|+c0) of
+// the exact value (16 ulp of the magnitude sum, covering coefficient
+// rounding and the three FMA roundings), and every plane distance within
+// 3B + 2^-22 |.|.  When min_p(d_p + r3) clears +-E, E = 4B + 2^-22 r3, the
+// FP64 reference decision (mark_core.hpp:32-40) is certain; only the
+// remainder (nodes within ~1e-3 world units of a frustum plane) recompute in
+// FP64.  Returns 1 visible, 0 culled, -1 undecided; *zs likewise for z_ok.
+__device__ __forceinline__ int frustum_fp32(const GeomF& f, float mx, float my, float mz,
+                                            float r3, float& tz_out, int& zs) {
+    const float tx = __fmaf_rn(f.r[0], mx, __fmaf_rn(f.r[1], my, __fmaf_rn(f.r[2], mz, f.t[0])));
+    const float ty = __fmaf_rn(f.r[3], mx, __fmaf_rn(f.r[4], my, __fmaf_rn(f.r[5], mz, f.t[1])));
+    const float tz = __fmaf_rn(f.r[6], mx, __fmaf_rn(f.r[7], my, __fmaf_rn(f.r[8], mz, f.t[2])));
+    const float B = 9.5367431640625e-07f * (fabsf(mx) + fabsf(my) + fabsf(mz) + f.c0);
+    const float E = __fmaf_rn(4.0f, B, 2.384185791015625e-07f * r3);
+    const float dn = (tz - f.znear) + r3;
+    const float df = (f.zfar - tz) + r3;
+    const float dl = __fmaf_rn(f.p2x, tx, f.p2z * tz) + r3;
+    const float dr = __fmaf_rn(f.p3x, tx, f.p3z * tz) + r3;
+    const float dt = __fmaf_rn(f.p4y, ty, f.p4z * tz) + r3;
+    const float db = __fmaf_rn(f.p5y, ty, f.p5z * tz) + r3;
+    const float m = fminf(fminf(fminf(dn, df), fminf(dl, dr)), fminf(dt, db));
+    const float dz = tz - f.znear;
+    zs = dz > E ? 1 : (dz < -E ? 0 : -1);
+    tz_out = tz;
+    return m > E ? 1 : (m < -E ? 0 : -1);
+}
+
+__global__ void __launch_bounds__(kMarkBlock) k_filter_mark(const Geom g, const GeomF f,
+                                                              const DevTree t,
                                                               const double tau_r,
                                                               uint32_t* __restrict__ cand_bits,
                                                               uint32_t* __restrict__ qint_bits,
@@ -30,20 +89,25 @@ __global__ void __launch_bounds__(kMarkBlock) k_filter_mark(const Geom g, const 
         const float mx = __ldcs(t.mx + i), my = __ldcs(t.my + i), mz = __ldcs(t.mz + i);
         const float sx = __ldcs(t.sx + i), sy = __ldcs(t.sy + i), sz = __ldcs(t.sz + i);
         const bool leaf = __ldcs(t.leaf + i) != 0;
-        double tx, ty, tz;
-        cam_transform(g, mx, my, mz, tx, ty, tz);
-        const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
-        const bool vis = frustum_folded(g, tx, ty, tz, 3.0 * smax);
-        if (vis) {
-            if (leaf) {
-                cand = true;
-            } else if (tz >= g.znear) {
+        const float smaxf = fmaxf(fmaxf(sx, sy), sz);  // scales are finite and > 0 (validated)
+        float tz32;
+        int zs;
+        int vs = frustum_fp32(f, mx, my, mz, 3.0f * smaxf, tz32, zs);
+        if (vs < 0 || (!leaf && vs != 0)) {
+            // exact FP64 path: undecided nodes, and every visible internal node
+            // (its qpass needs the EWA radius, which is always FP64).
+            double tx, ty, tz;
+            cam_transform(g, mx, my, mz, tx, ty, tz);
+            const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
+            vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
+            if (vs && !leaf && tz >= g.znear) {
                 const float4 q = __ldg(t.quat + i);
                 MarkOut o;
                 ewa_cov2d(g, tx, ty, tz, sx, sy, sz, q.x, q.y, q.z, q.w, o);
-                if (o.radius <= tau_r) cand = qint = true;
+                if (o.radius <= tau_r) qint = true;
             }
         }
+        cand = vs == 1 && (leaf || qint);
     }
     const unsigned cm = __ballot_sync(0xffffffffu, cand);
     const unsigned qm = __ballot_sync(0xffffffffu, qint);
@@ -138,7 +202,8 @@ void launch_filter_mark(const Geom& g, const DevTree& t, double tau_r, uint32_t*
                         uint32_t* qint_bits, cudaStream_t s) {
     if (t.n == 0) return;
     const unsigned grid = unsigned((t.n + kMarkBlock - 1) / kMarkBlock);
-    k_filter_mark<<<grid, kMarkBlock, 0, s>>>(g, t, tau_r, cand_bits, qint_bits, bit_words(t.n));
+    k_filter_mark<<<grid, kMarkBlock, 0, s>>>(g, make_geomf(g), t, tau_r, cand_bits, qint_bits,
+                                              bit_words(t.n));
 }
 
 void launch_filter_select(const DevTree& t, const uint32_t* cand_bits, const uint32_t* qint_bits,

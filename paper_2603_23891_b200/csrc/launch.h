@@ -49,10 +49,11 @@ struct PrepOut {
     GaussCol64* col64;     // nullable: only for the exact blend
     uint32_t* tile_count;  // n_tiles, zeroed per frame
 };
+constexpr int kHistMaxTiles = 12288;  // shared-memory tile histograms up to 48 KB
+constexpr int16_t kDropped = -32768;  // GaussEmit::ty0 of a slot dropped by project()
 void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected,
                        uint64_t max_selected, int shrink_kind, double tau, int tiles_x,
-                       int tiles_y, PrepOut out, unsigned long long* status,
-                       FrameCounters* cnt, int grid, cudaStream_t s);
+                       int tiles_y, PrepOut out, FrameCounters* cnt, int grid, cudaStream_t s);
 // Turns the per-tile counts into offsets[n_tiles+1] and per-tile write cursors,
 // and lists the tiles whose segment exceeds the in-shared-memory sort capacity.
 void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
@@ -60,8 +61,16 @@ void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offs
                          uint64_t pair_cap, cudaStream_t s);
 // Key duplication: one key per (gaussian, overlapped tile) scattered into the
 // tile's bucket; key = depth_bits << 32 | gaussian.
-void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x,
+void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x, int n_tiles,
                       uint32_t* cursor, unsigned long long* keys, int grid, cudaStream_t s);
+// Readbacks: slot -> BlendList index map, and slot-indexed records compacted
+// into BlendList order.
+void launch_slot_map(const GaussEmit* emit, uint64_t n, unsigned long long* status,
+                     FrameCounters* cnt, uint32_t* g_of_slot, uint32_t* slot_of_g, int grid,
+                     cudaStream_t s);
+void launch_compact_records(const uint32_t* slot_of_g, uint64_t n_g, const Gauss64* g64,
+                            const Gauss32* g32, const GaussEmit* emit, Gauss64* o64, Gauss32* o32,
+                            GaussEmit* oe, cudaStream_t s);
 
 // ---- sort (rasterizer.cpp:100-135) ----
 constexpr int kSmallSortCap = 4096;
@@ -103,7 +112,8 @@ void launch_pack_blendlist(uint64_t n, const double* mx, const double* my, const
                            cudaStream_t s);
 // Collect-mode readback: sorted keys -> (tile, depth, gaussian) triples.
 void launch_keys_to_triples(const uint32_t* offsets, int n_tiles, const unsigned long long* keys,
-                            uint32_t* out_triples, cudaStream_t s);
+                            const uint32_t* g_of_slot /* nullable */, uint32_t* out_triples,
+                            cudaStream_t s);
 // Per-gaussian pair counts (bin_to_tiles multiplicity) from emit records.
 void launch_gauss_counts(const GaussEmit* emit, const FrameCounters* cnt, uint64_t cap,
                          uint32_t* out, cudaStream_t s);

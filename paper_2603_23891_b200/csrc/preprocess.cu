@@ -133,60 +133,66 @@ __device__ __forceinline__ Gauss32 make_g32(double ca, double cb, double cc, dou
     return o;
 }
 
+// Contiguous slice [lo, hi) of n items for this CTA (keeps a CTA's splats
+// spatially coherent, so its shared-memory tile histogram stays sparse).
+__device__ __forceinline__ void cta_range(uint64_t n, uint64_t& lo, uint64_t& hi) {
+    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+    lo = min(n, uint64_t(blockIdx.x) * per);
+    hi = min(n, lo + per);
+}
+
+// Block-wide sum of two counters, added once to global memory.
+__device__ __forceinline__ void block_add2(uint32_t a, uint32_t b, unsigned long long* ga,
+                                           unsigned long long* gb) {
+    __shared__ unsigned long long s_sum[2];
+    if (threadIdx.x == 0) s_sum[0] = s_sum[1] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, off);
+        b += __shfl_down_sync(0xffffffffu, b, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (a) atomicAdd(&s_sum[0], (unsigned long long)a);
+        if (b) atomicAdd(&s_sum[1], (unsigned long long)b);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_sum[0]) atomicAdd(ga, s_sum[0]);
+        if (s_sum[1]) atomicAdd(gb, s_sum[1]);
+    }
+}
+
+// Records are indexed by selected slot s; a slot whose node fails projection
+// (rasterizer.cpp:56, near-plane drop) gets an empty rect tagged kDropped.
+// Keys carry the slot, whose order equals BlendList order, so the sort is
+// unchanged; the slot -> BlendList index map is only built for readbacks.
 __global__ void __launch_bounds__(kPrepBlock) k_preprocess(
     const Geom g, const SplatRec* __restrict__ splat, const uint32_t* __restrict__ selected,
     const int kind, const double tau, const int tiles_x, const int tiles_y, PrepOut out,
-    unsigned long long* status, FrameCounters* cnt) {
-    __shared__ unsigned s_ticket;
-    __shared__ unsigned s_warp[kPrepBlock / 32];
-    __shared__ unsigned long long s_excl;
-    __shared__ unsigned long long s_pairs;
-    const unsigned long long n_sel = *(volatile unsigned long long*)&cnt->n_selected;
-    const unsigned n_tiles_scan = unsigned((n_sel + kPrepBlock - 1) / kPrepBlock);
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    while (true) {
-        const unsigned tile = take_ticket(&cnt->ticket_prep, &s_ticket);
-        if (tile >= n_tiles_scan) break;
-        if (threadIdx.x == 0) s_pairs = 0;
-        const uint64_t s = uint64_t(tile) * kPrepBlock + threadIdx.x;
-        Projected p;
-        p.keep = false;
-        uint32_t idx = 0;
+    FrameCounters* cnt, const int use_hist) {
+    extern __shared__ uint32_t s_hist[];
+    const int n_tiles = tiles_x * tiles_y;
+    uint64_t lo, hi;
+    cta_range(cnt->n_selected, lo, hi);
+    if (use_hist)
+        for (int t = threadIdx.x; t < n_tiles; t += kPrepBlock) s_hist[t] = 0u;
+    __syncthreads();
+    uint32_t kept = 0, pairs = 0;
+    for (uint64_t s = lo + threadIdx.x; s < hi; s += kPrepBlock) {
+        const uint32_t idx = __ldg(selected + s);
+        const float4* src = reinterpret_cast<const float4*>(splat + idx);
+        const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
         SplatRec rec;
-        if (s < n_sel) {
-            idx = __ldg(selected + s);
-            const float4* src = reinterpret_cast<const float4*>(splat + idx);
-            const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
-            rec.mx = a.x; rec.my = a.y; rec.mz = a.z; rec.sx = a.w;
-            rec.sy = b.x; rec.sz = b.y; rec.qw = b.z; rec.qx = b.w;
-            rec.qy = c.x; rec.qz = c.y; rec.opacity = c.z; rec.cr = c.w;
-            rec.cg = d.x; rec.cb = d.y;
-            p = project_one(g, rec, kind, tau);
-            if (p.nonfinite) atomicOr(&cnt->nonfinite, 1u);
-        }
-        const unsigned km = __ballot_sync(0xffffffffu, p.keep);
-        if (lane == 0) s_warp[warp] = __popc(km);
-        __syncthreads();
-        if (warp == 0) {
-            unsigned v = lane < kPrepBlock / 32 ? s_warp[lane] : 0u;
-            unsigned incl = v;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= unsigned(off)) incl += o;
-            }
-            const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-            if (lane < kPrepBlock / 32) s_warp[lane] = incl - v;
-            const unsigned long long excl = chained_scan_warp(status, tile, total);
-            if (lane == 0) {
-                s_excl = excl;
-                if (tile == n_tiles_scan - 1) cnt->n_gaussians = excl + total;
-            }
-        }
-        __syncthreads();
-        uint32_t my_pairs = 0;
+        rec.mx = a.x; rec.my = a.y; rec.mz = a.z; rec.sx = a.w;
+        rec.sy = b.x; rec.sz = b.y; rec.qw = b.z; rec.qx = b.w;
+        rec.qy = c.x; rec.qz = c.y; rec.opacity = c.z; rec.cr = c.w;
+        rec.cg = d.x; rec.cb = d.y;
+        const Projected p = project_one(g, rec, kind, tau);
+        GaussEmit e;
+        e.node = idx;
         if (p.keep) {
-            const uint64_t gi = s_excl + s_warp[warp] + __popc(km & ((1u << lane) - 1u));
+            if (p.nonfinite) atomicOr(&cnt->nonfinite, 1u);
             Gauss64 r64;
             r64.mx = p.mx;
             r64.my = p.my;
@@ -196,46 +202,56 @@ __global__ void __launch_bounds__(kPrepBlock) k_preprocess(
             r64.op = double(rec.opacity);
             r64.radius = p.radius;
             r64.pad = 0.0;
-            out.g64[gi] = r64;
+            out.g64[s] = r64;
             if (out.col64) {
-                GaussCol64 c;
-                c.r = double(rec.cr);
-                c.g = double(rec.cg);
-                c.b = double(rec.cb);
-                c.pad = 0.0;
-                out.col64[gi] = c;
+                GaussCol64 col;
+                col.r = double(rec.cr);
+                col.g = double(rec.cg);
+                col.b = double(rec.cb);
+                col.pad = 0.0;
+                out.col64[s] = col;
             }
-            out.g32[gi] = make_g32(p.ca, p.cb, p.cc, double(rec.opacity), double(rec.cr),
-                                   double(rec.cg), double(rec.cb));
-            GaussEmit e;
+            out.g32[s] = make_g32(p.ca, p.cb, p.cc, double(rec.opacity), double(rec.cr),
+                                  double(rec.cg), double(rec.cb));
             e.depth_bits = __float_as_uint(__double2float_rn(p.depth));
-            e.node = idx;
             tile_rect(p.mx, p.my, p.radius, tiles_x, tiles_y, e);
-            out.emit[gi] = e;
-            my_pairs = rect_count(e);
+            ++kept;
+            pairs += rect_count(e);
             for (int ty = e.ty0; ty <= e.ty1; ++ty)
-                for (int tx = e.tx0; tx <= e.tx1; ++tx)
-                    atomicAdd(out.tile_count + (ty * tiles_x + tx), 1u);
+                for (int tx = e.tx0; tx <= e.tx1; ++tx) {
+                    if (use_hist)
+                        atomicAdd(s_hist + (ty * tiles_x + tx), 1u);
+                    else
+                        atomicAdd(out.tile_count + (ty * tiles_x + tx), 1u);
+                }
+        } else {
+            e.depth_bits = 0;
+            e.tx0 = 1;
+            e.tx1 = 0;
+            e.ty0 = kDropped;
+            e.ty1 = 0;
         }
-        // block total of pairs -> one 64-bit atomic
-        unsigned wsum = my_pairs;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) wsum += __shfl_down_sync(0xffffffffu, wsum, off);
-        if (lane == 0 && wsum) atomicAdd(&s_pairs, (unsigned long long)wsum);
+        out.emit[s] = e;
+    }
+    block_add2(kept, pairs, &cnt->n_gaussians, &cnt->n_pairs);
+    if (use_hist) {
         __syncthreads();
-        if (threadIdx.x == 0 && s_pairs) atomicAdd(&cnt->n_pairs, s_pairs);
+        for (int t = threadIdx.x; t < n_tiles; t += kPrepBlock) {
+            const uint32_t c = s_hist[t];
+            if (c) atomicAdd(out.tile_count + t, c);
+        }
     }
 }
 
 void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected,
                        uint64_t max_selected, int shrink_kind, double tau, int tiles_x,
-                       int tiles_y, PrepOut out, unsigned long long* status,
-                       FrameCounters* cnt, int grid, cudaStream_t s) {
-    const uint64_t max_tiles = (max_selected + kPrepBlock - 1) / kPrepBlock;
-    if (max_tiles == 0) return;
-    const int blocks = int(max_tiles < uint64_t(grid) ? max_tiles : uint64_t(grid));
-    k_preprocess<<<blocks, kPrepBlock, 0, s>>>(g, t.splat, selected, shrink_kind, tau, tiles_x,
-                                               tiles_y, out, status, cnt);
+                       int tiles_y, PrepOut out, FrameCounters* cnt, int grid, cudaStream_t s) {
+    if (max_selected == 0) return;
+    const int n_tiles = tiles_x * tiles_y;
+    const int use_hist = n_tiles <= kHistMaxTiles ? 1 : 0;
+    const size_t smem = use_hist ? size_t(n_tiles) * 4 : 0;
+    k_preprocess<<<grid, kPrepBlock, smem, s>>>(g, t.splat, selected, shrink_kind, tau, tiles_x,
+                                                tiles_y, out, cnt, use_hist);
 }
 
 // One CTA: exclusive scan of per-tile counts -> offsets, write cursors, and
@@ -301,26 +317,124 @@ void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offs
                                       pair_cap);
 }
 
+// Key duplication with CTA-level aggregation: each CTA counts its slice's
+// pairs per tile in shared memory, reserves one contiguous run per touched
+// tile with a single global atomic, then scatters its keys into the runs.
 __global__ void __launch_bounds__(256) k_emit_keys(const GaussEmit* __restrict__ emit,
                                                    const FrameCounters* cnt, int tiles_x,
-                                                   uint32_t* cursor, unsigned long long* keys) {
+                                                   int n_tiles, uint32_t* cursor,
+                                                   unsigned long long* keys, int use_hist) {
+    extern __shared__ uint32_t s_hist[];
     if (cnt->overflow) return;
-    const unsigned long long n = cnt->n_gaussians;
-    for (uint64_t gi = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; gi < n;
-         gi += uint64_t(gridDim.x) * blockDim.x) {
-        const GaussEmit e = emit[gi];
-        const unsigned long long hi = (unsigned long long)e.depth_bits << 32 | gi;
+    uint64_t lo, hi;
+    cta_range(cnt->n_selected, lo, hi);
+    if (!use_hist) {
+        for (uint64_t s = lo + threadIdx.x; s < hi; s += blockDim.x) {
+            const GaussEmit e = emit[s];
+            const unsigned long long key = (unsigned long long)e.depth_bits << 32 | s;
+            for (int ty = e.ty0; ty <= e.ty1; ++ty)
+                for (int tx = e.tx0; tx <= e.tx1; ++tx)
+                    keys[atomicAdd(cursor + (ty * tiles_x + tx), 1u)] = key;
+        }
+        return;
+    }
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_hist[t] = 0u;
+    __syncthreads();
+    for (uint64_t s = lo + threadIdx.x; s < hi; s += blockDim.x) {
+        const GaussEmit e = emit[s];
         for (int ty = e.ty0; ty <= e.ty1; ++ty)
-            for (int tx = e.tx0; tx <= e.tx1; ++tx) {
-                const uint32_t pos = atomicAdd(cursor + (ty * tiles_x + tx), 1u);
-                keys[pos] = hi;
-            }
+            for (int tx = e.tx0; tx <= e.tx1; ++tx) atomicAdd(s_hist + (ty * tiles_x + tx), 1u);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint32_t c = s_hist[t];
+        if (c) s_hist[t] = atomicAdd(cursor + t, c);
+    }
+    __syncthreads();
+    for (uint64_t s = lo + threadIdx.x; s < hi; s += blockDim.x) {
+        const GaussEmit e = emit[s];
+        const unsigned long long key = (unsigned long long)e.depth_bits << 32 | s;
+        for (int ty = e.ty0; ty <= e.ty1; ++ty)
+            for (int tx = e.tx0; tx <= e.tx1; ++tx)
+                keys[atomicAdd(s_hist + (ty * tiles_x + tx), 1u)] = key;
     }
 }
 
-void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x,
+void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x, int n_tiles,
                       uint32_t* cursor, unsigned long long* keys, int grid, cudaStream_t s) {
-    k_emit_keys<<<grid, 256, 0, s>>>(emit, cnt, tiles_x, cursor, keys);
+    const int use_hist = n_tiles <= kHistMaxTiles ? 1 : 0;
+    const size_t smem = use_hist ? size_t(n_tiles) * 4 : 0;
+    k_emit_keys<<<grid, 256, smem, s>>>(emit, cnt, tiles_x, n_tiles, cursor, keys, use_hist);
+}
+
+// Readback support: slot -> BlendList index (chained scan over kept flags),
+// and the inverse list.
+__global__ void __launch_bounds__(256) k_slot_map(const GaussEmit* __restrict__ emit,
+                                                  uint64_t n, unsigned long long* status,
+                                                  FrameCounters* cnt, uint32_t* g_of_slot,
+                                                  uint32_t* slot_of_g) {
+    __shared__ unsigned s_ticket;
+    __shared__ unsigned s_warp[8];
+    __shared__ unsigned long long s_excl;
+    const unsigned n_tiles = unsigned((n + 255) / 256);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    while (true) {
+        const unsigned tile = take_ticket(&cnt->ticket_prep, &s_ticket);
+        if (tile >= n_tiles) break;
+        const uint64_t s = uint64_t(tile) * 256 + threadIdx.x;
+        const bool kept = s < n && emit[s].ty0 != kDropped;
+        const unsigned km = __ballot_sync(0xffffffffu, kept);
+        if (lane == 0) s_warp[warp] = __popc(km);
+        __syncthreads();
+        if (warp == 0) {
+            unsigned v = lane < 8 ? s_warp[lane] : 0u;
+            unsigned incl = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= unsigned(off)) incl += o;
+            }
+            const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+            if (lane < 8) s_warp[lane] = incl - v;
+            const unsigned long long excl = chained_scan_warp(status, tile, total);
+            if (lane == 0) s_excl = excl;
+        }
+        __syncthreads();
+        if (s < n) {
+            if (kept) {
+                const uint32_t gi = uint32_t(s_excl + s_warp[warp] + __popc(km & ((1u << lane) - 1u)));
+                g_of_slot[s] = gi;
+                slot_of_g[gi] = uint32_t(s);
+            } else {
+                g_of_slot[s] = 0xFFFFFFFFu;
+            }
+        }
+    }
+}
+
+void launch_slot_map(const GaussEmit* emit, uint64_t n, unsigned long long* status,
+                     FrameCounters* cnt, uint32_t* g_of_slot, uint32_t* slot_of_g, int grid,
+                     cudaStream_t s) {
+    if (n) k_slot_map<<<grid, 256, 0, s>>>(emit, n, status, cnt, g_of_slot, slot_of_g);
+}
+
+__global__ void k_compact_records(const uint32_t* slot_of_g, uint64_t n_g, const Gauss64* g64,
+                                  const Gauss32* g32, const GaussEmit* emit, Gauss64* o64,
+                                  Gauss32* o32, GaussEmit* oe) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_g) return;
+    const uint32_t s = slot_of_g[i];
+    o64[i] = g64[s];
+    o32[i] = g32[s];
+    oe[i] = emit[s];
+}
+
+void launch_compact_records(const uint32_t* slot_of_g, uint64_t n_g, const Gauss64* g64,
+                            const Gauss32* g32, const GaussEmit* emit, Gauss64* o64, Gauss32* o32,
+                            GaussEmit* oe, cudaStream_t s) {
+    if (n_g)
+        k_compact_records<<<unsigned((n_g + 255) / 256), 256, 0, s>>>(slot_of_g, n_g, g64, g32,
+                                                                    emit, o64, o32, oe);
 }
 
 // ----------------------------------------------------------------------------

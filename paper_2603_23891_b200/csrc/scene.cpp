@@ -193,12 +193,13 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     if (pe) FGS_CUDA(cudaEventRecord(pe[2], stream_));
     PrepOut out{g64_.p, g32_.p, emit_.p, exact ? col64_.p : nullptr, d_tile_count_};
     launch_preprocess(g, tree_, selected_.p, tree_.n, p.shrink_kind, p.tau, res_.tiles_x,
-                      res_.tiles_y, out, d_status_prep_, d_counters_, persistent_grid_, stream_);
+                      res_.tiles_y, out, d_counters_, persistent_grid_, stream_);
     launch_tile_offsets(d_tile_count_, n_tiles, res_.tile_offsets.p, res_.tile_cursor.p,
                         res_.big_list.p, d_counters_, pair_cap_, stream_);
     launch_update_totals(d_counters_, res_.tile_offsets.p, n_tiles, totals_.p, stream_);
-    launch_emit_keys(emit_.p, d_counters_, res_.tiles_x, res_.tile_cursor.p, keys_.p,
+    launch_emit_keys(emit_.p, d_counters_, res_.tiles_x, n_tiles, res_.tile_cursor.p, keys_.p,
                      persistent_grid_, stream_);
+    maps_valid_ = false;
     if (timing) FGS_CUDA(cudaEventRecord(ev_[2], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[3], stream_));
     launch_tile_sort(res_.tile_offsets.p, n_tiles, keys_.p, res_.big_list.p, d_counters_, stream_);
@@ -337,7 +338,8 @@ uint64_t GpuScene::prepare(const lodgs_camera& cam, const uint32_t* selected, ui
     }
     PrepOut po{g64_.p, g32_.p, emit_.p, nullptr, d_tile_count_};
     launch_preprocess(g, tree_, selected_.p, n_sel, kind, tau, res_.tiles_x, res_.tiles_y, po,
-                      d_status_prep_, d_counters_, persistent_grid_, stream_);
+                      d_counters_, persistent_grid_, stream_);
+    maps_valid_ = false;
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
                              cudaMemcpyDeviceToHost, stream_));
@@ -366,6 +368,28 @@ uint64_t GpuScene::read_selected(uint32_t* out, uint64_t cap) {
     return ns;
 }
 
+// Slot -> BlendList index map and BlendList-ordered copies of the records,
+// built on demand for parity readbacks (the hot path never needs them).
+void GpuScene::build_readback_maps() {
+    if (maps_valid_) return;
+    const uint64_t ns = h_counters_->n_selected;
+    const uint64_t ng = h_counters_->n_gaussians;
+    g_of_slot_.alloc(ns);
+    slot_of_g_.alloc(ng);
+    rb_g64_.alloc(ng);
+    rb_g32_.alloc(ng);
+    rb_emit_.alloc(ng);
+    FGS_CUDA(cudaMemsetAsync(&d_counters_->ticket_prep, 0, sizeof(unsigned), stream_));
+    FGS_CUDA(cudaMemsetAsync(d_status_prep_, 0, (ns / 256 + 2) * 8, stream_));
+    launch_slot_map(emit_.p, ns, d_status_prep_, d_counters_, g_of_slot_.p, slot_of_g_.p,
+                    persistent_grid_, stream_);
+    launch_compact_records(slot_of_g_.p, ng, g64_.p, g32_.p, emit_.p, rb_g64_.p, rb_g32_.p,
+                           rb_emit_.p, stream_);
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    maps_valid_ = true;
+}
+
 uint64_t GpuScene::read_pairs(lodgs_tile_pair* out, uint64_t cap) {
     DeviceGuard dg(device_);
     FGS_CUDA(cudaStreamSynchronize(stream_));
@@ -375,9 +399,10 @@ uint64_t GpuScene::read_pairs(lodgs_tile_pair* out, uint64_t cap) {
     if (!out) return np;
     if (cap < np) throw Error(LODGS_ERR_VALIDATION, "read_pairs: capacity too small");
     if (np == 0) return 0;
+    build_readback_maps();
     DevBuf<uint32_t> tri;
     tri.alloc(uint64_t(np) * 3);
-    launch_keys_to_triples(res_.tile_offsets.p, n_tiles, keys_.p, tri.p, stream_);
+    launch_keys_to_triples(res_.tile_offsets.p, n_tiles, keys_.p, g_of_slot_.p, tri.p, stream_);
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaStreamSynchronize(stream_));
     FGS_CUDA(cudaMemcpy(out, tri.p, uint64_t(np) * 12, cudaMemcpyDeviceToHost));
@@ -390,13 +415,14 @@ uint64_t GpuScene::read_gaussians(lodgs_blend_list* out, uint64_t cap) {
     const uint64_t ng = h_counters_->n_gaussians;
     if (!out) return ng;
     if (cap < ng) throw Error(LODGS_ERR_VALIDATION, "read_gaussians: capacity too small");
+    build_readback_maps();
     std::vector<Gauss64> a(ng);
     std::vector<Gauss32> b(ng);
     std::vector<GaussEmit> e(ng);
     if (ng) {
-        FGS_CUDA(cudaMemcpy(a.data(), g64_.p, ng * sizeof(Gauss64), cudaMemcpyDeviceToHost));
-        FGS_CUDA(cudaMemcpy(b.data(), g32_.p, ng * sizeof(Gauss32), cudaMemcpyDeviceToHost));
-        FGS_CUDA(cudaMemcpy(e.data(), emit_.p, ng * sizeof(GaussEmit), cudaMemcpyDeviceToHost));
+        FGS_CUDA(cudaMemcpy(a.data(), rb_g64_.p, ng * sizeof(Gauss64), cudaMemcpyDeviceToHost));
+        FGS_CUDA(cudaMemcpy(b.data(), rb_g32_.p, ng * sizeof(Gauss32), cudaMemcpyDeviceToHost));
+        FGS_CUDA(cudaMemcpy(e.data(), rb_emit_.p, ng * sizeof(GaussEmit), cudaMemcpyDeviceToHost));
     }
     out->n = ng;
     for (uint64_t i = 0; i < ng; ++i) {
@@ -421,9 +447,10 @@ void GpuScene::read_counts(uint32_t* per_gaussian, uint64_t cap_g, uint32_t* per
     DeviceGuard dg(device_);
     FGS_CUDA(cudaStreamSynchronize(stream_));
     if (per_gaussian) {
+        build_readback_maps();
         DevBuf<uint32_t> tmp;
         tmp.alloc(cap_g);
-        launch_gauss_counts(emit_.p, d_counters_, cap_g, tmp.p, stream_);
+        launch_gauss_counts(rb_emit_.p, d_counters_, cap_g, tmp.p, stream_);
         FGS_CUDA(cudaGetLastError());
         FGS_CUDA(cudaStreamSynchronize(stream_));
         const uint64_t ng = std::min<uint64_t>(h_counters_->n_gaussians, cap_g);

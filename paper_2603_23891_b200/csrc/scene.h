@@ -95,6 +95,7 @@ public:
 
 private:
     void ensure_resolution(int w, int h);
+    void build_readback_maps();
     void clear_frame_state();
     void enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int w, int h, bool timing);
 
@@ -114,6 +115,12 @@ private:
     DevBuf<GaussEmit> emit_;
     DevBuf<GaussCol64> col64_;
     DevBuf<unsigned long long> keys_;
+    // readback-only: slot <-> BlendList index maps and compacted records
+    DevBuf<uint32_t> g_of_slot_, slot_of_g_;
+    DevBuf<Gauss64> rb_g64_;
+    DevBuf<Gauss32> rb_g32_;
+    DevBuf<GaussEmit> rb_emit_;
+    bool maps_valid_ = false;
     uint64_t pair_cap_ = 0;
     // zeroed every frame: [FrameCounters | select status | prep status | tile counts]
     DevBuf<unsigned char> zero_;

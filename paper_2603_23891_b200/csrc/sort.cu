@@ -180,20 +180,21 @@ void launch_triples_to_keys(const uint32_t* triples, uint64_t n, unsigned long l
 }
 
 __global__ void k_keys_to_triples(const uint32_t* offsets, const unsigned long long* keys,
-                                  uint32_t* out) {
+                                  const uint32_t* g_of_slot, uint32_t* out) {
     const uint32_t tile = blockIdx.x;
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
     for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
         const unsigned long long k = keys[i];
         out[i * 3 + 0] = tile;
         out[i * 3 + 1] = uint32_t(k >> 32);
-        out[i * 3 + 2] = uint32_t(k);
+        out[i * 3 + 2] = g_of_slot ? g_of_slot[uint32_t(k)] : uint32_t(k);
     }
 }
 
 void launch_keys_to_triples(const uint32_t* offsets, int n_tiles, const unsigned long long* keys,
-                            uint32_t* out_triples, cudaStream_t s) {
-    if (n_tiles > 0) k_keys_to_triples<<<n_tiles, 128, 0, s>>>(offsets, keys, out_triples);
+                            const uint32_t* g_of_slot, uint32_t* out_triples, cudaStream_t s) {
+    if (n_tiles > 0)
+        k_keys_to_triples<<<n_tiles, 128, 0, s>>>(offsets, keys, g_of_slot, out_triples);
 }
 
 }  // namespace fgs
