@@ -132,27 +132,49 @@ __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
     const uint64_t warp_base =
         uint64_t(tile) * (kSelectBlock * kSelectItems) + uint64_t(warp) * (32 * kSelectItems);
 
+    // All kSelectItems parent chains of a thread advance one level per round,
+    // so their dependent L2 loads overlap instead of running back to back.
+    uint32_t a[kSelectItems];
+    bool keep[kSelectItems];
+#pragma unroll
+    for (int j = 0; j < kSelectItems; ++j) {
+        const uint64_t node = warp_base + uint64_t(j) * 32 + lane;
+        keep[j] = node < n && ((__ldg(cand_bits + (node >> 5)) >> lane) & 1u);
+        a[j] = kRootParent;
+    }
+#pragma unroll
+    for (int j = 0; j < kSelectItems; ++j)
+        if (keep[j]) a[j] = __ldg(parent + warp_base + uint64_t(j) * 32 + lane);
+    while (true) {
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < kSelectItems; ++j) any |= a[j] != kRootParent;
+        if (!any) break;
+        uint32_t w[kSelectItems], p[kSelectItems];
+#pragma unroll
+        for (int j = 0; j < kSelectItems; ++j) {
+            if (a[j] != kRootParent) {
+                w[j] = __ldg(qint_bits + (a[j] >> 5));
+                p[j] = __ldg(parent + a[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kSelectItems; ++j) {
+            if (a[j] != kRootParent) {
+                if ((w[j] >> (a[j] & 31)) & 1u) {
+                    keep[j] = false;
+                    a[j] = kRootParent;
+                } else {
+                    a[j] = p[j];
+                }
+            }
+        }
+    }
     unsigned masks[kSelectItems];
     unsigned warp_count = 0;
 #pragma unroll
     for (int j = 0; j < kSelectItems; ++j) {
-        const uint64_t node = warp_base + uint64_t(j) * 32 + lane;
-        bool keep = false;
-        if (node < n) {
-            const uint32_t word = __ldg(cand_bits + (node >> 5));
-            if ((word >> lane) & 1u) {
-                keep = true;
-                uint32_t a = __ldg(parent + node);
-                while (a != kRootParent) {
-                    if ((__ldg(qint_bits + (a >> 5)) >> (a & 31)) & 1u) {
-                        keep = false;
-                        break;
-                    }
-                    a = __ldg(parent + a);
-                }
-            }
-        }
-        masks[j] = __ballot_sync(0xffffffffu, keep);
+        masks[j] = __ballot_sync(0xffffffffu, keep[j]);
         warp_count += __popc(masks[j]);
     }
     if (lane == 0) s_warp[warp] = warp_count;
