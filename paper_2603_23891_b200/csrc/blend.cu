@@ -64,20 +64,36 @@ __device__ __forceinline__ double alpha_exact(double mx, double my, double ca, d
     return std_min(op * exp_mx(power), kAlphaCap);
 }
 
-constexpr int kBlendThreads = 256;
+constexpr int kBlendThreads = 256;  // exact kernel: one CTA per 16x16 tile
 constexpr int kWarps = kBlendThreads / 32;
+constexpr int kFastThreads = 128;   // fast kernel: one CTA per 16x8 half tile
+constexpr int kFastWarps = kFastThreads / 32;
+constexpr int kFastParts = kTile * kTile / kFastThreads;
 
-struct BlendSmem {
-    float4 geo[kBlendThreads];   // tile-local mean x, y, ha, hc
-    float2 ct[kBlendThreads];    // cb, ethr
-    float4 col[kBlendThreads];   // op, r, g, b
-    uint32_t gid[kBlendThreads];
-    uint32_t bits[kWarps][kWarps];  // [consumer warp][loader warp] work-list ballots
+struct FastSmem {
+    float4 geo[kFastThreads];  // region-local mean x, y, ha, hc
+    float2 ct[kFastThreads];   // cb, ethr
+    float4 col[kFastThreads];  // op, r, g, b
+    uint32_t gid[kFastThreads];
+    uint32_t bits[kFastWarps][kFastWarps];  // [consumer warp][loader warp] work-list ballots
 };
 
-// Loads splat `gi` (thread's batch slot), writes its shared record and returns
-// the 8-bit mask of warp blocks its conservative box touches.
-__device__ __forceinline__ unsigned stage_splat(BlendSmem& s, uint32_t gi, const Gauss64* g64,
+// Mask of the NW warp blocks (8x4 pixels each, two per 16-pixel row band)
+// that a splat's conservative box [xlo,xhi]x[ylo,yhi] (region-local) touches.
+template <int NW>
+__device__ __forceinline__ unsigned warp_mask(float xlo, float xhi, float ylo, float yhi) {
+    unsigned mask = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const float bx = float((w & 1) * 8), by = float((w >> 1) * 4);
+        const bool hit = xlo <= bx + 7.5f && xhi >= bx + 0.5f && ylo <= by + 3.5f && yhi >= by + 0.5f;
+        mask |= hit ? (1u << w) : 0u;
+    }
+    return mask;
+}
+
+// Each thread of the batch stages one splat (gi) and returns its warp mask.
+__device__ __forceinline__ unsigned stage_splat(FastSmem& s, uint32_t gi, const Gauss64* g64,
                                                 const Gauss32* g32, int x0, int y0) {
     const double2 m = *reinterpret_cast<const double2*>(&g64[gi].mx);
     const float4 q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
@@ -88,38 +104,18 @@ __device__ __forceinline__ unsigned stage_splat(BlendSmem& s, uint32_t gi, const
     s.ct[threadIdx.x] = make_float2(q0.y, q0.w);
     s.col[threadIdx.x] = q1;
     s.gid[threadIdx.x] = gi;
-    // pixel centres of block (bx, by) span [bx+0.5, bx+7.5] x [by+0.5, by+3.5]
-    const float xlo = mlx - h.x, xhi = mlx + h.x, ylo = mly - h.y, yhi = mly + h.y;
-    unsigned mask = 0;
-    if (h.x >= 0.0f) {
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const float bx = float((w & 1) * 8), by = float((w >> 1) * 4);
-            const bool hit = xlo <= bx + 7.5f && xhi >= bx + 0.5f && ylo <= by + 3.5f &&
-                             yhi >= by + 0.5f;
-            mask |= hit ? (1u << w) : 0u;
-        }
-    }
-    return mask;
+    if (!(h.x >= 0.0f)) return 0u;
+    return warp_mask<kFastWarps>(mlx - h.x, mlx + h.x, mly - h.y, mly + h.y);
 }
 
-__device__ __forceinline__ void publish_lists(BlendSmem& s, unsigned mask, bool valid) {
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (!valid) mask = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        const unsigned b = __ballot_sync(0xffffffffu, (mask >> w) & 1u);
-        if (lane == 0) s.bits[w][warp] = b;
-    }
-}
-
-__global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fast(
+__global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
     const uint32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
     const Gauss64* __restrict__ g64, const Gauss32* __restrict__ g32, const int width,
     const int height, const int tiles_x, float* __restrict__ image) {
-    __shared__ BlendSmem s;
-    const int tile = blockIdx.x;
-    const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
+    __shared__ FastSmem s;
+    const int tile = blockIdx.x / kFastParts, part = blockIdx.x % kFastParts;
+    const int x0 = (tile % tiles_x) * kTile;
+    const int y0 = (tile / tiles_x) * kTile + part * (kFastWarps / 2) * 4;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lx = int((warp & 1) * 8 + (lane & 7)), ly = int((warp >> 1) * 4 + (lane >> 3));
     const int x = x0 + lx, y = y0 + ly;
@@ -131,15 +127,19 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fast(
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
     bool done = !inside;
 
-    for (uint32_t base = b; base < e; base += kBlendThreads) {
-        const uint32_t cnt = min(uint32_t(kBlendThreads), e - base);
-        const bool valid = threadIdx.x < cnt;
+    for (uint32_t base = b; base < e; base += kFastThreads) {
+        const uint32_t cnt = min(uint32_t(kFastThreads), e - base);
         unsigned mask = 0;
-        if (valid) mask = stage_splat(s, uint32_t(keys[base + threadIdx.x]), g64, g32, x0, y0);
-        publish_lists(s, mask, valid);
+        if (threadIdx.x < cnt)
+            mask = stage_splat(s, uint32_t(keys[base + threadIdx.x]), g64, g32, x0, y0);
+#pragma unroll
+        for (int w = 0; w < kFastWarps; ++w) {
+            const unsigned bb = __ballot_sync(0xffffffffu, (mask >> w) & 1u);
+            if (lane == 0) s.bits[w][warp] = bb;
+        }
         if (__syncthreads_and(done)) break;
         bool warp_done = __all_sync(0xffffffffu, done);
-        for (int c = 0; c < kWarps && !warp_done; ++c) {
+        for (int c = 0; c < kFastWarps && !warp_done; ++c) {
             unsigned bits = s.bits[warp][c];
             while (bits) {
                 const int j = c * 32 + (__ffs(bits) - 1);
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend_fast(
             }
             warp_done = __all_sync(0xffffffffu, done);
         }
-        __syncthreads();
+        if (base + kFastThreads < e) __syncthreads();  // no barrier after the last batch
     }
     if (inside) {
         float* o = image + (size_t(y) * width + x) * 3;
@@ -282,8 +282,8 @@ void launch_blend(const uint32_t* offsets, const unsigned long long* keys, const
         k_blend_exact<<<n_tiles, kBlendThreads, smem, s>>>(offsets, keys, g64, g32, col64, width,
                                                             height, tiles_x, image);
     } else {
-        k_blend_fast<<<n_tiles, kBlendThreads, 0, s>>>(offsets, keys, g64, g32, width, height,
-                                                       tiles_x, image);
+        k_blend_fast<<<n_tiles * kFastParts, kFastThreads, 0, s>>>(offsets, keys, g64, g32, width,
+                                                                   height, tiles_x, image);
     }
 }
 

@@ -57,6 +57,92 @@ __device__ __forceinline__ void flip_bitonic(unsigned long long* a, Index n, Ind
 }
 
 constexpr int kSmallSortThreads = 256;
+constexpr int kRegItems = 4;  // keys per thread in the register network
+constexpr int kRegCap = kSmallSortThreads * kRegItems;
+
+__device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v, int m) {
+    const unsigned lo = __shfl_xor_sync(0xffffffffu, unsigned(v), m);
+    const unsigned hi = __shfl_xor_sync(0xffffffffu, unsigned(v >> 32), m);
+    return (unsigned long long)hi << 32 | lo;
+}
+
+// Buckets of up to kRegCap keys: classic bitonic network over P = 2^ceil(log2 n)
+// slots, padded with +inf.  Slot i = r * 256 + tid lives in register r of
+// thread tid, so partners at distance j < 32 are exchanged with warp shuffles,
+// 32 <= j < 256 through shared memory, j >= 256 inside the thread.  Only warps
+// that own slots < P take part (a 40-key bucket is one warp, no barriers).
+__device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint32_t n,
+                                                 unsigned long long* s_x) {
+    uint32_t P = 32;
+    while (P < n) P <<= 1;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t lanes = P < uint32_t(kSmallSortThreads) ? P : uint32_t(kSmallSortThreads);
+    const int R = int((P + kSmallSortThreads - 1) / kSmallSortThreads);
+    if (tid >= lanes) return;  // whole warps (lanes is a multiple of 32)
+    unsigned long long v[kRegItems];
+#pragma unroll
+    for (int r = 0; r < kRegItems; ++r) {
+        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+        v[r] = (r < R && i < n) ? keys[i] : ~0ull;
+    }
+    int parity = 0;
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            if (j >= uint32_t(kSmallSortThreads)) {
+                // partners in registers r and r ^ (j / 256) of this thread
+                auto cas = [&](unsigned long long& a, unsigned long long& b, int r) {
+                    const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+                    const bool up = (i & k) == 0;
+                    const bool sw = up ? (b < a) : (a < b);
+                    const unsigned long long lo = sw ? b : a, hi = sw ? a : b;
+                    a = lo;
+                    b = hi;
+                };
+                if (j == uint32_t(kSmallSortThreads)) {
+                    cas(v[0], v[1], 0);
+                    if (R > 2) cas(v[2], v[3], 2);
+                } else {
+                    cas(v[0], v[2], 0);
+                    cas(v[1], v[3], 1);
+                }
+            } else if (j >= 32) {
+                // partner thread tid ^ j, same register: exchange through smem,
+                // double-buffered so one named barrier (the `lanes` threads in
+                // play) per exchange suffices.
+#pragma unroll
+                for (int r = 0; r < kRegItems; ++r) {
+                    if (r < R) {
+                        unsigned long long* buf = s_x + (parity ? kSmallSortThreads : 0);
+                        parity ^= 1;
+                        buf[tid] = v[r];
+                        asm volatile("bar.sync 1, %0;" ::"r"(lanes) : "memory");
+                        const unsigned long long o = buf[tid ^ j];
+                        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+                        const bool up = (i & k) == 0;
+                        const bool lower = (tid & j) == 0;
+                        v[r] = (lower == up) ? (o < v[r] ? o : v[r]) : (o < v[r] ? v[r] : o);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < kRegItems; ++r) {
+                    if (r < R) {
+                        const unsigned long long o = shfl_xor_u64(v[r], int(j));
+                        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+                        const bool up = (i & k) == 0;
+                        const bool lower = (tid & j) == 0;
+                        v[r] = (lower == up) ? (o < v[r] ? o : v[r]) : (o < v[r] ? v[r] : o);
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kRegItems; ++r) {
+        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+        if (r < R && i < n) keys[i] = v[r];
+    }
+}
 
 __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t* __restrict__ offsets,
                                                                  unsigned long long* keys) {
@@ -64,6 +150,10 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t*
     const uint32_t b = offsets[blockIdx.x], e = offsets[blockIdx.x + 1];
     const uint32_t n = e - b;
     if (n < 2 || n > uint32_t(kSmallSortCap)) return;  // big buckets: k_tile_sort_big
+    if (n <= uint32_t(kRegCap)) {
+        register_bitonic(keys + b, n, s);
+        return;
+    }
     for (uint32_t i = threadIdx.x; i < n; i += kSmallSortThreads) s[i] = keys[b + i];
     __syncthreads();
     flip_bitonic<uint32_t>(s, n, threadIdx.x, kSmallSortThreads, [] __device__() { __syncthreads(); });
