@@ -66,30 +66,39 @@ __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v,
     return (unsigned long long)hi << 32 | lo;
 }
 
-// Buckets of up to kRegCap keys: classic bitonic network over P = 2^ceil(log2 n)
+// Compare-exchange step of element i (partner i ^ j) in a bitonic network of
+// stage k: keep the smaller value iff (i is the lower of the pair) == (the
+// block of size k is ascending).
+__device__ __forceinline__ unsigned long long bitonic_pick(unsigned long long mine,
+                                                           unsigned long long other, uint32_t i,
+                                                           uint32_t j, uint32_t k) {
+    const bool keep_min = ((i & j) == 0) == ((i & k) == 0);
+    return (other < mine) == keep_min ? other : mine;
+}
+
+// Buckets of up to 256*R keys: bitonic network over P = 2^ceil(log2 n) >= 32
 // slots, padded with +inf.  Slot i = r * 256 + tid lives in register r of
 // thread tid, so partners at distance j < 32 are exchanged with warp shuffles,
-// 32 <= j < 256 through shared memory, j >= 256 inside the thread.  Only warps
-// that own slots < P take part (a 40-key bucket is one warp, no barriers).
+// 32 <= j < 256 through (double-buffered) shared memory with one named barrier
+// over the threads in play, j >= 256 inside the thread.  Only warps owning
+// slots < P take part: a 40-key bucket is one warp and never waits.
+template <int R>
 __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint32_t n,
-                                                 unsigned long long* s_x) {
-    uint32_t P = 32;
-    while (P < n) P <<= 1;
+                                                 uint32_t P, unsigned long long* s_x) {
     const uint32_t tid = threadIdx.x;
     const uint32_t lanes = P < uint32_t(kSmallSortThreads) ? P : uint32_t(kSmallSortThreads);
-    const int R = int((P + kSmallSortThreads - 1) / kSmallSortThreads);
     if (tid >= lanes) return;  // whole warps (lanes is a multiple of 32)
-    unsigned long long v[kRegItems];
+    unsigned long long v[R];
 #pragma unroll
-    for (int r = 0; r < kRegItems; ++r) {
+    for (int r = 0; r < R; ++r) {
         const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
-        v[r] = (r < R && i < n) ? keys[i] : ~0ull;
+        v[r] = i < n ? keys[i] : ~0ull;
     }
     int parity = 0;
     for (uint32_t k = 2; k <= P; k <<= 1) {
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
             if (j >= uint32_t(kSmallSortThreads)) {
-                // partners in registers r and r ^ (j / 256) of this thread
+                // partners in registers r and r ^ (j / 256); indices kept static
                 auto cas = [&](unsigned long long& a, unsigned long long& b, int r) {
                     const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
                     const bool up = (i & k) == 0;
@@ -98,49 +107,41 @@ __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint3
                     a = lo;
                     b = hi;
                 };
-                if (j == uint32_t(kSmallSortThreads)) {
+                if constexpr (R == 2) {
                     cas(v[0], v[1], 0);
-                    if (R > 2) cas(v[2], v[3], 2);
-                } else {
-                    cas(v[0], v[2], 0);
-                    cas(v[1], v[3], 1);
+                } else if constexpr (R == 4) {
+                    if (j == uint32_t(kSmallSortThreads)) {
+                        cas(v[0], v[1], 0);
+                        cas(v[2], v[3], 2);
+                    } else {
+                        cas(v[0], v[2], 0);
+                        cas(v[1], v[3], 1);
+                    }
                 }
             } else if (j >= 32) {
-                // partner thread tid ^ j, same register: exchange through smem,
-                // double-buffered so one named barrier (the `lanes` threads in
-                // play) per exchange suffices.
+                unsigned long long* buf = s_x + (parity ? R * kSmallSortThreads : 0);
+                parity ^= 1;
 #pragma unroll
-                for (int r = 0; r < kRegItems; ++r) {
-                    if (r < R) {
-                        unsigned long long* buf = s_x + (parity ? kSmallSortThreads : 0);
-                        parity ^= 1;
-                        buf[tid] = v[r];
-                        asm volatile("bar.sync 1, %0;" ::"r"(lanes) : "memory");
-                        const unsigned long long o = buf[tid ^ j];
-                        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
-                        const bool up = (i & k) == 0;
-                        const bool lower = (tid & j) == 0;
-                        v[r] = (lower == up) ? (o < v[r] ? o : v[r]) : (o < v[r] ? v[r] : o);
-                    }
+                for (int r = 0; r < R; ++r) buf[r * kSmallSortThreads + tid] = v[r];
+                asm volatile("bar.sync 1, %0;" ::"r"(lanes) : "memory");
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+                    v[r] = bitonic_pick(v[r], buf[r * kSmallSortThreads + (tid ^ j)], i, j, k);
                 }
             } else {
 #pragma unroll
-                for (int r = 0; r < kRegItems; ++r) {
-                    if (r < R) {
-                        const unsigned long long o = shfl_xor_u64(v[r], int(j));
-                        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
-                        const bool up = (i & k) == 0;
-                        const bool lower = (tid & j) == 0;
-                        v[r] = (lower == up) ? (o < v[r] ? o : v[r]) : (o < v[r] ? v[r] : o);
-                    }
+                for (int r = 0; r < R; ++r) {
+                    const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+                    v[r] = bitonic_pick(v[r], shfl_xor_u64(v[r], int(j)), i, j, k);
                 }
             }
         }
     }
 #pragma unroll
-    for (int r = 0; r < kRegItems; ++r) {
+    for (int r = 0; r < R; ++r) {
         const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
-        if (r < R && i < n) keys[i] = v[r];
+        if (i < n) keys[i] = v[r];
     }
 }
 
@@ -151,7 +152,14 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t*
     const uint32_t n = e - b;
     if (n < 2 || n > uint32_t(kSmallSortCap)) return;  // big buckets: k_tile_sort_big
     if (n <= uint32_t(kRegCap)) {
-        register_bitonic(keys + b, n, s);
+        uint32_t P = 32;
+        while (P < n) P <<= 1;
+        if (P <= uint32_t(kSmallSortThreads))
+            register_bitonic<1>(keys + b, n, P, s);
+        else if (P <= 2u * kSmallSortThreads)
+            register_bitonic<2>(keys + b, n, P, s);
+        else
+            register_bitonic<4>(keys + b, n, P, s);
         return;
     }
     for (uint32_t i = threadIdx.x; i < n; i += kSmallSortThreads) s[i] = keys[b + i];

@@ -7,7 +7,7 @@ import sys
 
 
 def main(path, kern, n=25):
-    out = subprocess.run(["ncu", "-i", path, "-k", f"regex:{kern}", "--page", "source", "--csv",
+    out = subprocess.run(["ncu", "-i", path, "-k", kern, "--page", "source", "--csv",
                           "--print-source", "sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
@@ -19,7 +19,7 @@ def main(path, kern, n=25):
     for i, r in enumerate(rows[2:]):
         try:
             ni, nw = int(r[ie]), int(r[ws] or 0)
-        except ValueError:
+        except (ValueError, IndexError):
             continue
         tot_i += ni
         tot_w += nw
