@@ -196,8 +196,9 @@ def run_b200(args, rank, world, local):
     build_s = time.perf_counter() - t_build
     stream = torch.cuda.ExternalStream(scene.stream_ptr(), device=torch.device("cuda", local))
     params = L.RenderParamsC(TAU_R, 0.0, 0, 0)
-    start = (rank * n_path) // world
-    order = [cams[(start + i) % n_path] for i in range(args.warmup + args.steps)]
+    from paper_2603_23891_b200.sharding import reduce_timing, rotated_frames
+
+    order = [cams[i] for i in rotated_frames(n_path, rank, world, args.warmup + args.steps)]
 
     # size the pair buffer on the whole path once (untimed)
     for cam in cams[:: max(1, n_path // 30)]:
@@ -245,7 +246,7 @@ def run_b200(args, rank, world, local):
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    e2e_frames = timed[: max(1, min(len(timed), args.e2e_steps))]
+    e2e_frames = timed if args.e2e_steps <= 0 else timed[: max(1, min(len(timed), args.e2e_steps))]
     t0 = time.perf_counter()
     st = L.RenderStatsC()
     for cam in e2e_frames:
@@ -255,11 +256,11 @@ def run_b200(args, rank, world, local):
     e2e_s = time.perf_counter() - t0
     L.load_library().lodgs_gpu_host_free(host_img)
 
-    # max over ranks
-    vals = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms_max, e2e_max = float(vals[0]), float(vals[1])
+    # max over ranks of the timed regions; per-rank counters summed
+    ms_max, _ = reduce_timing(dist, ms, [], device="cuda")
+    e2e_max, (sum_sel_all, sum_pairs_all, nf_all) = reduce_timing(
+        dist, e2e_s, [sum_sel, sum_pairs, nf], device="cuda")
+    sum_sel, sum_pairs, nf = sum_sel_all, sum_pairs_all, int(nf_all)
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -321,7 +322,7 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="frames for e2e (0 = all timed frames)")
     ap.add_argument("--steps-ref", type=int, default=6)
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--no-cpu", action="store_true")
