@@ -83,54 +83,75 @@ __global__ void __launch_bounds__(kMarkBlock) k_filter_mark(const Geom g, const 
                                                               uint32_t* __restrict__ cand_bits,
                                                               uint32_t* __restrict__ qint_bits,
                                                               const uint64_t n_words) {
-    const uint64_t i = uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x;
-    bool cand = false, qint = false;
-    if (i < t.n) {
-        const float mx = __ldcs(t.mx + i), my = __ldcs(t.my + i), mz = __ldcs(t.mz + i);
-        const float sx = __ldcs(t.sx + i), sy = __ldcs(t.sy + i), sz = __ldcs(t.sz + i);
-        const bool leaf = __ldcs(t.leaf + i) != 0;
-        const float smaxf = fmaxf(fmaxf(sx, sy), sz);  // scales are finite and > 0 (validated)
-        float tz32;
-        int zs;
-        int vs = frustum_fp32(f, mx, my, mz, 3.0f * smaxf, tz32, zs);
-        if (vs < 0 || (!leaf && vs != 0)) {
-            // exact FP64 path: undecided nodes, and every visible internal node
-            // (its qpass needs the EWA radius, which is always FP64).
-            double tx, ty, tz;
-            cam_transform(g, mx, my, mz, tx, ty, tz);
-            const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
-            vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
-            if (vs && !leaf && tz >= g.znear) {
-                const float4 q = __ldg(t.quat + i);
-                MarkOut o;
-                ewa_cov2d(g, tx, ty, tz, sx, sy, sz, q.x, q.y, q.z, q.w, o);
-                if (o.radius <= tau_r) qint = true;
+    // Four consecutive nodes per thread: one 16-byte load per SoA array (the
+    // arrays are padded to a multiple of 256 nodes, so every float4 is aligned).
+    const uint64_t i0 = (uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x) * 4;
+    unsigned cnib = 0, qnib = 0;
+    if (i0 < t.n) {
+        const float4 MX = __ldcs(reinterpret_cast<const float4*>(t.mx + i0));
+        const float4 MY = __ldcs(reinterpret_cast<const float4*>(t.my + i0));
+        const float4 MZ = __ldcs(reinterpret_cast<const float4*>(t.mz + i0));
+        const float4 SX = __ldcs(reinterpret_cast<const float4*>(t.sx + i0));
+        const float4 SY = __ldcs(reinterpret_cast<const float4*>(t.sy + i0));
+        const float4 SZ = __ldcs(reinterpret_cast<const float4*>(t.sz + i0));
+        const uint32_t LF = __ldcs(reinterpret_cast<const unsigned int*>(t.leaf + i0));
+        const float mxa[4] = {MX.x, MX.y, MX.z, MX.w}, mya[4] = {MY.x, MY.y, MY.z, MY.w};
+        const float mza[4] = {MZ.x, MZ.y, MZ.z, MZ.w}, sxa[4] = {SX.x, SX.y, SX.z, SX.w};
+        const float sya[4] = {SY.x, SY.y, SY.z, SY.w}, sza[4] = {SZ.x, SZ.y, SZ.z, SZ.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (i0 + k >= t.n) break;
+            const float mx = mxa[k], my = mya[k], mz = mza[k];
+            const float sx = sxa[k], sy = sya[k], sz = sza[k];
+            const bool leaf = ((LF >> (8 * k)) & 0xffu) != 0;
+            const float smaxf = fmaxf(fmaxf(sx, sy), sz);  // scales finite and > 0 (validated)
+            float tz32;
+            int zs;
+            int vs = frustum_fp32(f, mx, my, mz, 3.0f * smaxf, tz32, zs);
+            bool qint = false;
+            if (vs < 0 || (!leaf && vs != 0)) {
+                // exact FP64 path: undecided nodes, and every visible internal
+                // node (its qpass needs the EWA radius, which is always FP64).
+                double tx, ty, tz;
+                cam_transform(g, mx, my, mz, tx, ty, tz);
+                const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
+                vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
+                if (vs && !leaf && tz >= g.znear) {
+                    const float4 q = __ldg(t.quat + i0 + k);
+                    MarkOut o;
+                    ewa_cov2d(g, tx, ty, tz, sx, sy, sz, q.x, q.y, q.z, q.w, o);
+                    qint = o.radius <= tau_r;
+                }
             }
+            cnib |= (vs == 1 && (leaf || qint)) ? (1u << k) : 0u;
+            qnib |= qint ? (1u << k) : 0u;
         }
-        cand = vs == 1 && (leaf || qint);
     }
-    const unsigned cm = __ballot_sync(0xffffffffu, cand);
-    const unsigned qm = __ballot_sync(0xffffffffu, qint);
-    if ((threadIdx.x & 31) == 0) {
-        const uint64_t w = i >> 5;
+    // A warp covers 128 nodes = 4 words; word k gathers the nibbles of lanes 8k..8k+7.
+    const unsigned lane = threadIdx.x & 31;
+    unsigned cw = cnib << (4 * (lane & 7)), qw = qnib << (4 * (lane & 7));
+#pragma unroll
+    for (int m = 1; m < 8; m <<= 1) {
+        cw |= __shfl_xor_sync(0xffffffffu, cw, m);
+        qw |= __shfl_xor_sync(0xffffffffu, qw, m);
+    }
+    if ((lane & 7) == 0) {
+        const uint64_t w = i0 >> 5;
         if (w < n_words) {
-            cand_bits[w] = cm;
-            qint_bits[w] = qm;
+            cand_bits[w] = cw;
+            qint_bits[w] = qw;
         }
     }
 }
 
+// K2a: candidates walk their parent chains (filter.cpp:20-25); the keep bits
+// overwrite cand_bits in place (each word is read and written by one warp).
 __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
-    const uint32_t* __restrict__ cand_bits, const uint32_t* __restrict__ qint_bits,
-    const uint32_t* __restrict__ parent, const uint64_t n, const uint32_t n_tiles,
-    uint32_t* __restrict__ selected, unsigned long long* status, FrameCounters* cnt) {
-    __shared__ unsigned s_ticket;
-    __shared__ unsigned s_warp[kSelectBlock / 32];
-    __shared__ unsigned long long s_excl;
-    const unsigned tile = take_ticket(&cnt->ticket_select, &s_ticket);
+    uint32_t* __restrict__ cand_bits, const uint32_t* __restrict__ qint_bits,
+    const uint32_t* __restrict__ parent, const uint64_t n) {
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t warp_base =
-        uint64_t(tile) * (kSelectBlock * kSelectItems) + uint64_t(warp) * (32 * kSelectItems);
+        uint64_t(blockIdx.x) * (kSelectBlock * kSelectItems) + uint64_t(warp) * (32 * kSelectItems);
 
     // All kSelectItems parent chains of a thread advance one level per round,
     // so their dependent L2 loads overlap instead of running back to back.
@@ -139,7 +160,7 @@ __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
 #pragma unroll
     for (int j = 0; j < kSelectItems; ++j) {
         const uint64_t node = warp_base + uint64_t(j) * 32 + lane;
-        keep[j] = node < n && ((__ldg(cand_bits + (node >> 5)) >> lane) & 1u);
+        keep[j] = node < n && ((cand_bits[node >> 5] >> lane) & 1u);
         a[j] = kRootParent;
     }
 #pragma unroll
@@ -170,25 +191,54 @@ __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
             }
         }
     }
-    unsigned masks[kSelectItems];
-    unsigned warp_count = 0;
 #pragma unroll
     for (int j = 0; j < kSelectItems; ++j) {
-        masks[j] = __ballot_sync(0xffffffffu, keep[j]);
-        warp_count += __popc(masks[j]);
+        const unsigned m = __ballot_sync(0xffffffffu, keep[j]);
+        if (lane == 0) cand_bits[(warp_base >> 5) + j] = m;
     }
-    if (lane == 0) s_warp[warp] = warp_count;
+}
+
+// K2b: ordered compaction of the keep bitmask into `selected` (strictly
+// increasing, filter.cpp:147-148): per-thread popcounts over 8 consecutive
+// words, block scan, chained-scan look-back across 65,536-node tiles.
+constexpr int kCompactWords = 8;
+__global__ void __launch_bounds__(256) k_compact_bits(const uint32_t* __restrict__ bits,
+                                                      const uint64_t n_words,
+                                                      const uint32_t n_tiles,
+                                                      uint32_t* __restrict__ selected,
+                                                      unsigned long long* status,
+                                                      FrameCounters* cnt) {
+    __shared__ unsigned s_ticket;
+    __shared__ unsigned s_warp[8];
+    __shared__ unsigned long long s_excl;
+    const unsigned tile = take_ticket(&cnt->ticket_select, &s_ticket);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t w0 = (uint64_t(tile) * 256 + threadIdx.x) * kCompactWords;
+    uint32_t words[kCompactWords];
+    unsigned c = 0;
+#pragma unroll
+    for (int k = 0; k < kCompactWords; ++k) {
+        words[k] = (w0 + k < n_words) ? __ldg(bits + w0 + k) : 0u;
+        c += __popc(words[k]);
+    }
+    unsigned incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= unsigned(off)) incl += o;
+    }
+    if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        unsigned v = lane < kSelectBlock / 32 ? s_warp[lane] : 0u;
-        unsigned incl = v;
+        const unsigned v = lane < 8 ? s_warp[lane] : 0u;
+        unsigned wi = v;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= unsigned(off)) incl += o;
+        for (int off = 1; off < 8; off <<= 1) {
+            const unsigned o = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= unsigned(off)) wi += o;
         }
-        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-        if (lane < kSelectBlock / 32) s_warp[lane] = incl - v;  // exclusive per warp
+        const unsigned total = __shfl_sync(0xffffffffu, wi, 7);
+        if (lane < 8) s_warp[lane] = wi - v;
         const unsigned long long excl = chained_scan_warp(status, tile, total);
         if (lane == 0) {
             s_excl = excl;
@@ -196,14 +246,15 @@ __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
         }
     }
     __syncthreads();
-    unsigned long long pos = s_excl + s_warp[warp];
-    const unsigned lt = (1u << lane) - 1u;
+    unsigned long long pos = s_excl + s_warp[warp] + (incl - c);
 #pragma unroll
-    for (int j = 0; j < kSelectItems; ++j) {
-        if ((masks[j] >> lane) & 1u)
-            selected[pos + __popc(masks[j] & lt)] =
-                uint32_t(warp_base + uint64_t(j) * 32 + lane);
-        pos += __popc(masks[j]);
+    for (int k = 0; k < kCompactWords; ++k) {
+        uint32_t m = words[k];
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            selected[pos++] = uint32_t((w0 + k) * 32 + b);
+        }
     }
 }
 
@@ -223,18 +274,19 @@ __global__ void k_mark_debug(const Geom g, const DevTree t, uint64_t begin, uint
 void launch_filter_mark(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
                         uint32_t* qint_bits, cudaStream_t s) {
     if (t.n == 0) return;
-    const unsigned grid = unsigned((t.n + kMarkBlock - 1) / kMarkBlock);
+    const unsigned grid = unsigned((t.n + 4 * kMarkBlock - 1) / (4 * kMarkBlock));
     k_filter_mark<<<grid, kMarkBlock, 0, s>>>(g, make_geomf(g), t, tau_r, cand_bits, qint_bits,
                                               bit_words(t.n));
 }
 
-void launch_filter_select(const DevTree& t, const uint32_t* cand_bits, const uint32_t* qint_bits,
+void launch_filter_select(const DevTree& t, uint32_t* cand_bits, const uint32_t* qint_bits,
                           uint32_t* selected, unsigned long long* status, FrameCounters* cnt,
                           cudaStream_t s) {
     if (t.n == 0) return;
-    const uint32_t tiles = select_tiles(t.n);
-    k_filter_select<<<tiles, kSelectBlock, 0, s>>>(cand_bits, qint_bits, t.parent, t.n, tiles,
-                                                    selected, status, cnt);
+    k_filter_select<<<select_tiles(t.n), kSelectBlock, 0, s>>>(cand_bits, qint_bits, t.parent, t.n);
+    const uint64_t n_words = bit_words(t.n);
+    const uint32_t tiles = uint32_t((n_words + 256 * kCompactWords - 1) / (256 * kCompactWords));
+    k_compact_bits<<<tiles, 256, 0, s>>>(cand_bits, n_words, tiles, selected, status, cnt);
 }
 
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,

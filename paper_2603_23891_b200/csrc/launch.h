@@ -26,14 +26,15 @@ struct DevTree {
 constexpr int kMarkBlock = 256;
 constexpr int kSelectBlock = 256;
 constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles
-inline uint64_t bit_words(uint64_t n) { return (n + 255) / 256 * 8; }
+// bitmask words, rounded up to whole 2048-node select tiles
+inline uint64_t bit_words(uint64_t n) { return (n + 2047) / 2048 * 64; }
 inline uint32_t select_tiles(uint64_t n) {
     return uint32_t((n + uint64_t(kSelectBlock) * kSelectItems - 1) /
                     (uint64_t(kSelectBlock) * kSelectItems));
 }
 void launch_filter_mark(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
                         uint32_t* qint_bits, cudaStream_t s);
-void launch_filter_select(const DevTree& t, const uint32_t* cand_bits, const uint32_t* qint_bits,
+void launch_filter_select(const DevTree& t, uint32_t* cand_bits, const uint32_t* qint_bits,
                           uint32_t* selected, unsigned long long* status, FrameCounters* cnt,
                           cudaStream_t s);
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,

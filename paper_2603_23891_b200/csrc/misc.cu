@@ -6,17 +6,18 @@ namespace fgs {
 
 // SoA upload -> float4 quaternions (filter) + 64-byte splat records
 // (preprocess gather).  soa = [mx|my|mz|sx|sy|sz], extra = [qw|qx|qy|qz|op|cr|cg|cb].
-__global__ void k_pack_tree(const float* __restrict__ soa, const float* __restrict__ ex,
-                            uint64_t n, float4* quat, SplatRec* splat) {
+__global__ void k_pack_tree(const float* __restrict__ soa, uint64_t stride,
+                            const float* __restrict__ ex, uint64_t n, float4* quat,
+                            SplatRec* splat) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     SplatRec r;
     r.mx = soa[i];
-    r.my = soa[n + i];
-    r.mz = soa[2 * n + i];
-    r.sx = soa[3 * n + i];
-    r.sy = soa[4 * n + i];
-    r.sz = soa[5 * n + i];
+    r.my = soa[stride + i];
+    r.mz = soa[2 * stride + i];
+    r.sx = soa[3 * stride + i];
+    r.sy = soa[4 * stride + i];
+    r.sz = soa[5 * stride + i];
     r.qw = ex[i];
     r.qx = ex[n + i];
     r.qy = ex[2 * n + i];
@@ -31,9 +32,9 @@ __global__ void k_pack_tree(const float* __restrict__ soa, const float* __restri
     splat[i] = r;
 }
 
-void launch_pack_tree(const float* soa, const float* extra, uint64_t n, float4* quat,
-                      SplatRec* splat, cudaStream_t s) {
-    if (n) k_pack_tree<<<unsigned((n + 255) / 256), 256, 0, s>>>(soa, extra, n, quat, splat);
+void launch_pack_tree(const float* soa, uint64_t stride, const float* extra, uint64_t n,
+                      float4* quat, SplatRec* splat, cudaStream_t s) {
+    if (n) k_pack_tree<<<unsigned((n + 255) / 256), 256, 0, s>>>(soa, stride, extra, n, quat, splat);
 }
 
 __global__ void k_update_totals(const FrameCounters* cnt, const uint32_t* offsets, int n_tiles,

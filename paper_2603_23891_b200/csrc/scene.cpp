@@ -29,8 +29,8 @@ DeviceGuard::~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);
 }
 
-void launch_pack_tree(const float* soa, const float* extra, uint64_t n, float4* quat,
-                      SplatRec* splat, cudaStream_t s);
+void launch_pack_tree(const float* soa, uint64_t stride, const float* extra, uint64_t n,
+                      float4* quat, SplatRec* splat, cudaStream_t s);
 void launch_update_totals(const FrameCounters* cnt, const uint32_t* offsets, int n_tiles,
                           RunTotals* totals, cudaStream_t s);
 void launch_max_tile(const uint32_t* triples, uint64_t n, unsigned int* out, cudaStream_t s);
@@ -56,12 +56,16 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
     std::memset(h_counters_, 0, sizeof(FrameCounters));
 
     const uint64_t n = tree.n_nodes;
+    // SoA stride padded to 256 nodes: every array starts 1 KB-aligned, so the
+    // mark pass can use 16-byte loads of four consecutive nodes.
+    const uint64_t np = (n + 255) / 256 * 256;
     tree_.n = n;
-    soa_.alloc(6 * n);
+    soa_.alloc(6 * np);
+    FGS_CUDA(cudaMemsetAsync(soa_.p, 0, soa_.bytes(), stream_));
     const float* soa_src[6] = {tree.mean_x, tree.mean_y, tree.mean_z,
                                tree.scale_x, tree.scale_y, tree.scale_z};
     for (int k = 0; k < 6; ++k)
-        if (n) FGS_CUDA(cudaMemcpyAsync(soa_.p + k * n, soa_src[k], n * 4, cudaMemcpyHostToDevice, stream_));
+        if (n) FGS_CUDA(cudaMemcpyAsync(soa_.p + k * np, soa_src[k], n * 4, cudaMemcpyHostToDevice, stream_));
     {
         DevBuf<float> extra;
         extra.alloc(8 * n);
@@ -71,21 +75,22 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
             if (n) FGS_CUDA(cudaMemcpyAsync(extra.p + k * n, ex_src[k], n * 4, cudaMemcpyHostToDevice, stream_));
         quat_.alloc(n);
         splat_.alloc(n);
-        launch_pack_tree(soa_.p, extra.p, n, quat_.p, splat_.p, stream_);
+        launch_pack_tree(soa_.p, np, extra.p, n, quat_.p, splat_.p, stream_);
         FGS_CUDA(cudaStreamSynchronize(stream_));
     }
     parent_.alloc(n);
-    leaf_.alloc(n);
+    leaf_.alloc(np);
+    FGS_CUDA(cudaMemsetAsync(leaf_.p, 0, np, stream_));
     if (n) {
         FGS_CUDA(cudaMemcpyAsync(parent_.p, tree.parent, n * 4, cudaMemcpyHostToDevice, stream_));
         FGS_CUDA(cudaMemcpyAsync(leaf_.p, tree.leaf, n, cudaMemcpyHostToDevice, stream_));
     }
     tree_.mx = soa_.p;
-    tree_.my = soa_.p + n;
-    tree_.mz = soa_.p + 2 * n;
-    tree_.sx = soa_.p + 3 * n;
-    tree_.sy = soa_.p + 4 * n;
-    tree_.sz = soa_.p + 5 * n;
+    tree_.my = soa_.p + np;
+    tree_.mz = soa_.p + 2 * np;
+    tree_.sx = soa_.p + 3 * np;
+    tree_.sy = soa_.p + 4 * np;
+    tree_.sz = soa_.p + 5 * np;
     tree_.quat = quat_.p;
     tree_.parent = parent_.p;
     tree_.leaf = leaf_.p;
