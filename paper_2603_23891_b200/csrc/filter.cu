@@ -199,9 +199,11 @@ __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
 }
 
 // K2b: ordered compaction of the keep bitmask into `selected` (strictly
-// increasing, filter.cpp:147-148): per-thread popcounts over 8 consecutive
-// words, block scan, chained-scan look-back across 65,536-node tiles.
-constexpr int kCompactWords = 8;
+// increasing, filter.cpp:147-148).  A warp owns 128 consecutive words; for
+// each word (broadcast by shuffle) lane b tests bit b, so one ballot + popc
+// places 32 nodes with a coalesced store.  CTA totals are chained by a
+// look-back across 32,768-node tiles.
+constexpr int kCompactIters = 4;  // words per lane
 __global__ void __launch_bounds__(256) k_compact_bits(const uint32_t* __restrict__ bits,
                                                       const uint64_t n_words,
                                                       const uint32_t n_tiles,
@@ -213,21 +215,18 @@ __global__ void __launch_bounds__(256) k_compact_bits(const uint32_t* __restrict
     __shared__ unsigned long long s_excl;
     const unsigned tile = take_ticket(&cnt->ticket_select, &s_ticket);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t w0 = (uint64_t(tile) * 256 + threadIdx.x) * kCompactWords;
-    uint32_t words[kCompactWords];
+    const uint64_t wbase = (uint64_t(tile) * 8 + warp) * (32 * kCompactIters);
+    uint32_t words[kCompactIters];
     unsigned c = 0;
 #pragma unroll
-    for (int k = 0; k < kCompactWords; ++k) {
-        words[k] = (w0 + k < n_words) ? __ldg(bits + w0 + k) : 0u;
-        c += __popc(words[k]);
+    for (int it = 0; it < kCompactIters; ++it) {
+        const uint64_t w = wbase + uint64_t(it) * 32 + lane;
+        words[it] = w < n_words ? __ldg(bits + w) : 0u;
+        c += __popc(words[it]);
     }
-    unsigned incl = c;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= unsigned(off)) incl += o;
-    }
-    if (lane == 31) s_warp[warp] = incl;
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    if (lane == 0) s_warp[warp] = c;
     __syncthreads();
     if (warp == 0) {
         const unsigned v = lane < 8 ? s_warp[lane] : 0u;
@@ -246,14 +245,19 @@ __global__ void __launch_bounds__(256) k_compact_bits(const uint32_t* __restrict
         }
     }
     __syncthreads();
-    unsigned long long pos = s_excl + s_warp[warp] + (incl - c);
+    unsigned long long pos = s_excl + s_warp[warp];
+    const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int k = 0; k < kCompactWords; ++k) {
-        uint32_t m = words[k];
-        while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            selected[pos++] = uint32_t((w0 + k) * 32 + b);
+    for (int it = 0; it < kCompactIters; ++it) {
+        if (__ballot_sync(0xffffffffu, words[it] != 0u) == 0u) continue;
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t word = __shfl_sync(0xffffffffu, words[it], k);
+            if (word == 0u) continue;  // warp-uniform
+            const bool bit = (word >> lane) & 1u;
+            if (bit)
+                selected[pos + __popc(word & lt)] =
+                    uint32_t((wbase + uint64_t(it) * 32 + k) * 32 + lane);
+            pos += __popc(word);
         }
     }
 }
@@ -285,7 +289,8 @@ void launch_filter_select(const DevTree& t, uint32_t* cand_bits, const uint32_t*
     if (t.n == 0) return;
     k_filter_select<<<select_tiles(t.n), kSelectBlock, 0, s>>>(cand_bits, qint_bits, t.parent, t.n);
     const uint64_t n_words = bit_words(t.n);
-    const uint32_t tiles = uint32_t((n_words + 256 * kCompactWords - 1) / (256 * kCompactWords));
+    const uint64_t per_tile = 8ull * 32 * kCompactIters;
+    const uint32_t tiles = uint32_t((n_words + per_tile - 1) / per_tile);
     k_compact_bits<<<tiles, 256, 0, s>>>(cand_bits, n_words, tiles, selected, status, cnt);
 }
 
