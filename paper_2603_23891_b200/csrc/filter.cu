@@ -77,39 +77,53 @@ __device__ __forceinline__ int frustum_fp32(const GeomF& f, float mx, float my, 
     return m > E ? 1 : (m < -E ? 0 : -1);
 }
 
-__global__ void __launch_bounds__(kMarkBlock) k_filter_mark(const Geom g, const GeomF f,
+// ALL_LEAF: the launch covers a range known (at upload) to hold only leaves --
+// the last level of a level-major tree -- so the EWA covariance is never
+// needed and the kernel stays register-light (full occupancy for the
+// bandwidth-bound bulk of the arena).
+template <bool ALL_LEAF>
+__global__ void __launch_bounds__(kMarkBlock, ALL_LEAF ? 4 : 2) k_filter_mark(const Geom g, const GeomF f,
                                                               const DevTree t,
                                                               const double tau_r,
+                                                              const uint64_t begin,
+                                                              const uint64_t end,
                                                               uint32_t* __restrict__ cand_bits,
                                                               uint32_t* __restrict__ qint_bits,
                                                               const uint64_t n_words) {
     // Four consecutive nodes per thread: one 16-byte load per SoA array (the
-    // arrays are padded to a multiple of 256 nodes, so every float4 is aligned).
-    const uint64_t i0 = (uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x) * 4;
+    // arrays are padded to a multiple of 256 nodes, so every float4 is aligned;
+    // `begin` is a multiple of 1024).
+    const uint64_t i0 = begin + (uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x) * 4;
     unsigned cnib = 0, qnib = 0;
-    if (i0 < t.n) {
+    if (i0 < end) {
         const float4 MX = __ldcs(reinterpret_cast<const float4*>(t.mx + i0));
         const float4 MY = __ldcs(reinterpret_cast<const float4*>(t.my + i0));
         const float4 MZ = __ldcs(reinterpret_cast<const float4*>(t.mz + i0));
         const float4 SX = __ldcs(reinterpret_cast<const float4*>(t.sx + i0));
         const float4 SY = __ldcs(reinterpret_cast<const float4*>(t.sy + i0));
         const float4 SZ = __ldcs(reinterpret_cast<const float4*>(t.sz + i0));
-        const uint32_t LF = __ldcs(reinterpret_cast<const unsigned int*>(t.leaf + i0));
+        const uint32_t LF =
+            ALL_LEAF ? 0x01010101u : __ldcs(reinterpret_cast<const unsigned int*>(t.leaf + i0));
         const float mxa[4] = {MX.x, MX.y, MX.z, MX.w}, mya[4] = {MY.x, MY.y, MY.z, MY.w};
         const float mza[4] = {MZ.x, MZ.y, MZ.z, MZ.w}, sxa[4] = {SX.x, SX.y, SX.z, SX.w};
         const float sya[4] = {SY.x, SY.y, SY.z, SY.w}, sza[4] = {SZ.x, SZ.y, SZ.z, SZ.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (i0 + k >= t.n) break;
+            if (i0 + k >= end) break;
             const float mx = mxa[k], my = mya[k], mz = mza[k];
             const float sx = sxa[k], sy = sya[k], sz = sza[k];
-            const bool leaf = ((LF >> (8 * k)) & 0xffu) != 0;
+            const bool leaf = ALL_LEAF || ((LF >> (8 * k)) & 0xffu) != 0;
             const float smaxf = fmaxf(fmaxf(sx, sy), sz);  // scales finite and > 0 (validated)
             float tz32;
             int zs;
             int vs = frustum_fp32(f, mx, my, mz, 3.0f * smaxf, tz32, zs);
             bool qint = false;
-            if (vs < 0 || (!leaf && vs != 0)) {
+            if (ALL_LEAF && vs < 0) {
+                double tx, ty, tz;
+                cam_transform(g, mx, my, mz, tx, ty, tz);
+                const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
+                vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
+            } else if (!ALL_LEAF && (vs < 0 || (!leaf && vs != 0))) {
                 // exact FP64 path: undecided nodes, and every visible internal
                 // node (its qpass needs the EWA radius, which is always FP64).
                 double tx, ty, tz;
@@ -203,7 +217,7 @@ __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
 // each word (broadcast by shuffle) lane b tests bit b, so one ballot + popc
 // places 32 nodes with a coalesced store.  CTA totals are chained by a
 // look-back across 32,768-node tiles.
-constexpr int kCompactIters = 4;  // words per lane
+constexpr int kCompactIters = 1;  // words per lane (small tiles: one wave of short CTAs)
 __global__ void __launch_bounds__(256) k_compact_bits(const uint32_t* __restrict__ bits,
                                                       const uint64_t n_words,
                                                       const uint32_t n_tiles,
@@ -278,9 +292,15 @@ __global__ void k_mark_debug(const Geom g, const DevTree t, uint64_t begin, uint
 void launch_filter_mark(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
                         uint32_t* qint_bits, cudaStream_t s) {
     if (t.n == 0) return;
-    const unsigned grid = unsigned((t.n + 4 * kMarkBlock - 1) / (4 * kMarkBlock));
-    k_filter_mark<<<grid, kMarkBlock, 0, s>>>(g, make_geomf(g), t, tau_r, cand_bits, qint_bits,
-                                              bit_words(t.n));
+    const GeomF f = make_geomf(g);
+    const uint64_t per_cta = 4 * kMarkBlock;
+    const uint64_t split = t.leaf_begin;  // multiple of per_cta; [split, n) are all leaves
+    if (split > 0)
+        k_filter_mark<false><<<unsigned((split + per_cta - 1) / per_cta), kMarkBlock, 0, s>>>(
+            g, f, t, tau_r, 0, split, cand_bits, qint_bits, bit_words(t.n));
+    if (t.n > split)
+        k_filter_mark<true><<<unsigned((t.n - split + per_cta - 1) / per_cta), kMarkBlock, 0, s>>>(
+            g, f, t, tau_r, split, t.n, cand_bits, qint_bits, bit_words(t.n));
 }
 
 void launch_filter_select(const DevTree& t, uint32_t* cand_bits, const uint32_t* qint_bits,

@@ -20,6 +20,9 @@ struct DevTree {
     const uint32_t* parent = nullptr;
     const uint8_t* leaf = nullptr;
     const SplatRec* splat = nullptr;
+    // Nodes [leaf_begin, n) are all leaves (leaf_begin a multiple of 1024):
+    // the filter's mark pass skips the covariance code path there.
+    uint64_t leaf_begin = 0;
 };
 
 // ---- filter (filter.cpp:115-150) ----

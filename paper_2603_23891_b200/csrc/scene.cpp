@@ -95,6 +95,12 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
     tree_.parent = parent_.p;
     tree_.leaf = leaf_.p;
     tree_.splat = splat_.p;
+    {
+        // first index of the all-leaf suffix, rounded up to a 1024-node mark CTA
+        uint64_t first = n;
+        while (first > 0 && tree.leaf[first - 1]) --first;
+        tree_.leaf_begin = std::min<uint64_t>(n, (first + 1023) / 1024 * 1024);
+    }
 
     cand_bits_.alloc(bit_words(n));
     qint_bits_.alloc(bit_words(n));
