@@ -1,27 +1,29 @@
 // blend.cu -- tile-wise front-to-back alpha blending (K6), reference
 // alpha_blend -> blend_scalar (rasterizer.cpp:137-165, blend_scalar.cpp:13-55).
 //
-// One 256-thread CTA per 16x16 tile.  Warp w owns an 8x4 pixel block
-// (x0 + 8*(w&1), y0 + 4*(w>>1)); lane l its pixel (l&7, l>>3) in the block.
-// The tile's sorted keys are consumed in batches of 256: each thread stages
-// one splat into shared memory and tests the splat's conservative alpha>=1/255
-// box (Gauss32::hx/hy) against the 8 warp blocks; one ballot per warp turns
-// that into 8 ordered 32-bit work lists.  Each warp then walks only its own
-// list -- every branch on the list is warp-uniform, so lanes never drift
-// apart (an earlier per-lane `continue` version ran at 2.8 active lanes per
-// instruction).  A sample outside the box has e > ln(255 op) and is skipped
-// by the reference too, so culling never changes a pixel.
+// Fast kernel: one 128-thread CTA per 16x8 half tile; warp w owns an 8x4
+// pixel block (8*(w&1), 4*(w>>1)) of the half tile, lane l its pixel
+// (l&7, l>>3).  Warps never synchronise with each other: each walks the
+// tile's sorted pair list 32 splats at a time, every lane tests one splat's
+// conservative alpha>=1/255 box (Gauss32::hx/hy) against the warp's block,
+// hits are staged in the warp's own shared-memory slice, and one ballot
+// gives the warp an ordered work list.  All control flow on the list is
+// warp-uniform, so lanes never drift apart.  The four warps of a CTA read
+// the same splat records, which therefore come from L1 after the first.
+// A sample outside the box has e > ln(255 op) and is skipped by the
+// reference too, so culling never changes a pixel.
 //
-// Fast path (default): FP32 per sample; the reference's FP64 decision is
-// recomputed exactly whenever the FP32 estimate is within a certified margin
-// of the alpha >= 1/255 threshold (a flipped skip would move a pixel by up
-// to 1/255, SURVEY.md section 7 hard part 6).  The test needs no exp:
+// FP32 per sample, with the reference's FP64 decision recomputed exactly
+// (warp vote, rare) whenever the FP32 estimate is within a certified margin
+// of the alpha >= 1/255 threshold -- a flipped skip would move a pixel by up
+// to 1/255 (SURVEY.md section 7 hard part 6).  The test needs no exp:
 //     alpha = min(op exp(power), 0.99) < 1/255  <=>  e > ln(255 op),
 //     e = -power = ha dx^2 + cb dx dy + hc dy^2 >= 0.
 // With Q = ha dx^2 + hc dy^2 >= |cb dx dy| (positive-definite conic),
 // |e32 - e| is a few ulp of Q, well inside margin = (Q + 1) 2^-17.
+// Accepted samples blend branch-free: w = alpha T, C += c w, T -= w.
 //
-// Exact path (LODGS_RENDER_EXACT_BLEND): the reference arithmetic in FP64
+// Exact kernel (LODGS_RENDER_EXACT_BLEND): the reference arithmetic in FP64
 // with the reference exp_mx (fastexp.hpp:38-50), no FMA: bit-identical pixels.
 #include "launch.h"
 
@@ -64,116 +66,97 @@ __device__ __forceinline__ double alpha_exact(double mx, double my, double ca, d
     return std_min(op * exp_mx(power), kAlphaCap);
 }
 
-constexpr int kBlendThreads = 256;  // exact kernel: one CTA per 16x16 tile
-constexpr int kWarps = kBlendThreads / 32;
-constexpr int kFastThreads = 128;   // fast kernel: one CTA per 16x8 half tile
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+constexpr int kFastThreads = 128;  // fast kernel: one CTA per 16x8 half tile
 constexpr int kFastWarps = kFastThreads / 32;
 constexpr int kFastParts = kTile * kTile / kFastThreads;
 
-struct FastSmem {
-    float4 geo[kFastThreads];  // region-local mean x, y, ha, hc
-    float2 ct[kFastThreads];   // cb, ethr
-    float4 col[kFastThreads];  // op, r, g, b
-    uint32_t gid[kFastThreads];
-    uint32_t bits[kFastWarps][kFastWarps];  // [consumer warp][loader warp] work-list ballots
+struct WarpStage {
+    float4 geo[32];  // block-relative mean x, y, ha, hc
+    float2 ct[32];   // cb, ethr
+    float4 col[32];  // op, r, g, b
+    uint32_t gid[32];
 };
-
-// Mask of the NW warp blocks (8x4 pixels each, two per 16-pixel row band)
-// that a splat's conservative box [xlo,xhi]x[ylo,yhi] (region-local) touches.
-template <int NW>
-__device__ __forceinline__ unsigned warp_mask(float xlo, float xhi, float ylo, float yhi) {
-    unsigned mask = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        const float bx = float((w & 1) * 8), by = float((w >> 1) * 4);
-        const bool hit = xlo <= bx + 7.5f && xhi >= bx + 0.5f && ylo <= by + 3.5f && yhi >= by + 0.5f;
-        mask |= hit ? (1u << w) : 0u;
-    }
-    return mask;
-}
-
-// Each thread of the batch stages one splat (gi) and returns its warp mask.
-__device__ __forceinline__ unsigned stage_splat(FastSmem& s, uint32_t gi, const Gauss64* g64,
-                                                const Gauss32* g32, int x0, int y0) {
-    const double2 m = *reinterpret_cast<const double2*>(&g64[gi].mx);
-    const float4 q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
-    const float4 q1 = *reinterpret_cast<const float4*>(&g32[gi].op);
-    const float2 h = *reinterpret_cast<const float2*>(&g32[gi].hx);
-    const float mlx = float(m.x - double(x0)), mly = float(m.y - double(y0));
-    s.geo[threadIdx.x] = make_float4(mlx, mly, q0.x, q0.z);
-    s.ct[threadIdx.x] = make_float2(q0.y, q0.w);
-    s.col[threadIdx.x] = q1;
-    s.gid[threadIdx.x] = gi;
-    if (!(h.x >= 0.0f)) return 0u;
-    return warp_mask<kFastWarps>(mlx - h.x, mlx + h.x, mly - h.y, mly + h.y);
-}
 
 __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
     const uint32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
     const Gauss64* __restrict__ g64, const Gauss32* __restrict__ g32, const int width,
     const int height, const int tiles_x, float* __restrict__ image) {
-    __shared__ FastSmem s;
+    __shared__ WarpStage stage[kFastWarps];
     const int tile = blockIdx.x / kFastParts, part = blockIdx.x % kFastParts;
-    const int x0 = (tile % tiles_x) * kTile;
-    const int y0 = (tile / tiles_x) * kTile + part * (kFastWarps / 2) * 4;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = int((warp & 1) * 8 + (lane & 7)), ly = int((warp >> 1) * 4 + (lane >> 3));
-    const int x = x0 + lx, y = y0 + ly;
+    WarpStage& st = stage[warp];
+    // this warp's 8x4 block origin in image pixels
+    const int bx = (tile % tiles_x) * kTile + int(warp & 1) * 8;
+    const int by = (tile / tiles_x) * kTile + part * 8 + int(warp >> 1) * 4;
+    const int x = bx + int(lane & 7), y = by + int(lane >> 3);
     const bool inside = x < width && y < height;
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
 
-    const float pxl = float(lx) + 0.5f, pyl = float(ly) + 0.5f;
+    const float pxl = float(lane & 7) + 0.5f, pyl = float(lane >> 3) + 0.5f;
     const double px = double(x) + 0.5, py = double(y) + 0.5;
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
     bool done = !inside;
+    if (__all_sync(0xffffffffu, done)) return;
 
-    for (uint32_t base = b; base < e; base += kFastThreads) {
-        const uint32_t cnt = min(uint32_t(kFastThreads), e - base);
-        unsigned mask = 0;
-        if (threadIdx.x < cnt)
-            mask = stage_splat(s, uint32_t(keys[base + threadIdx.x]), g64, g32, x0, y0);
-#pragma unroll
-        for (int w = 0; w < kFastWarps; ++w) {
-            const unsigned bb = __ballot_sync(0xffffffffu, (mask >> w) & 1u);
-            if (lane == 0) s.bits[w][warp] = bb;
+    for (uint32_t base = b; base < e; base += 32) {
+        // ---- stage the next 32 splats that touch this warp's block
+        bool hit = false;
+        if (base + lane < e) {
+            const uint32_t gi = uint32_t(keys[base + lane]);
+            const double2 m = *reinterpret_cast<const double2*>(&g64[gi].mx);
+            const float2 h = *reinterpret_cast<const float2*>(&g32[gi].hx);
+            const float mlx = float(m.x - double(bx)), mly = float(m.y - double(by));
+            // pixel centres of the block span [0.5, 7.5] x [0.5, 3.5]
+            hit = h.x >= 0.0f && mlx - h.x <= 7.5f && mlx + h.x >= 0.5f && mly - h.y <= 3.5f &&
+                  mly + h.y >= 0.5f;
+            if (hit) {
+                const float4 q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
+                st.geo[lane] = make_float4(mlx, mly, q0.x, q0.z);
+                st.ct[lane] = make_float2(q0.y, q0.w);
+                st.col[lane] = *reinterpret_cast<const float4*>(&g32[gi].op);
+                st.gid[lane] = gi;
+            }
         }
-        if (__syncthreads_and(done)) break;
-        bool warp_done = __all_sync(0xffffffffu, done);
-        for (int c = 0; c < kFastWarps && !warp_done; ++c) {
-            unsigned bits = s.bits[warp][c];
-            while (bits) {
-                const int j = c * 32 + (__ffs(bits) - 1);
-                bits &= bits - 1;
-                const float4 geo = s.geo[j];
-                const float2 ct = s.ct[j];
-                const float dx = pxl - geo.x, dy = pyl - geo.y;
-                const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
-                const float ev = __fmaf_rn(ct.x * dx, dy, Q);
-                const float d = ev - ct.y;
-                const float margin = __fmaf_rn(Q, 7.62939453125e-06f, 7.62939453125e-06f);
-                float alpha = 0.0f;
-                if (!done && d <= margin) {
-                    if (d < -margin) {
-                        alpha = fminf(s.col[j].x * __expf(-ev), 0.99f);
-                    } else {
-                        const Gauss64& G = g64[s.gid[j]];
-                        const double a64 = alpha_exact(G.mx, G.my, G.ca, G.cb, G.cc, G.op, px, py);
-                        alpha = a64 >= kMinAlpha ? float(a64) : 0.0f;
-                    }
-                }
-                if (alpha > 0.0f) {
-                    const float4 col = s.col[j];
-                    const float w = alpha * T;
-                    cr = __fmaf_rn(col.y, w, cr);
-                    cg = __fmaf_rn(col.z, w, cg);
-                    cb = __fmaf_rn(col.w, w, cb);
-                    T = T * (1.0f - alpha);
-                    done = T < 1e-4f;
+        unsigned bits = __ballot_sync(0xffffffffu, hit);
+        __syncwarp();
+        // ---- blend them front to back
+        while (bits) {
+            const int j = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const float4 geo = st.geo[j];
+            const float2 ct = st.ct[j];
+            const float dx = pxl - geo.x, dy = pyl - geo.y;
+            const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
+            const float ev = __fmaf_rn(ct.x * dx, dy, Q);
+            const float d = ev - ct.y;
+            const float margin = __fmaf_rn(Q, 7.62939453125e-06f, 7.62939453125e-06f);
+            const float4 col = st.col[j];
+            float alpha = fminf(col.x * ex2_approx(ev * -1.4426950408889634f), 0.99f);
+            bool take = d < -margin;
+            const bool unsure = !done && fabsf(d) <= margin;
+            if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decision
+                if (unsure) {
+                    const Gauss64& G = g64[st.gid[j]];
+                    const double a64 = alpha_exact(G.mx, G.my, G.ca, G.cb, G.cc, G.op, px, py);
+                    take = a64 >= kMinAlpha;
+                    alpha = float(a64);
                 }
             }
-            warp_done = __all_sync(0xffffffffu, done);
+            const float w = (take && !done) ? alpha * T : 0.0f;
+            cr = __fmaf_rn(col.y, w, cr);
+            cg = __fmaf_rn(col.z, w, cg);
+            cb = __fmaf_rn(col.w, w, cb);
+            T = T - w;
+            done = done || T < 1e-4f;
         }
-        if (base + kFastThreads < e) __syncthreads();  // no barrier after the last batch
+        if (__all_sync(0xffffffffu, done)) break;
+        __syncwarp();
     }
     if (inside) {
         float* o = image + (size_t(y) * width + x) * 3;
@@ -182,6 +165,9 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
         o[2] = cb;
     }
 }
+
+constexpr int kBlendThreads = 256;  // exact kernel: one CTA per 16x16 tile
+constexpr int kWarps = kBlendThreads / 32;
 
 struct BlendSmemExact {
     double4 geo[kBlendThreads];  // mx, my, ca, cb
@@ -223,9 +209,9 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_exact(
             if (h.x >= 0.0f) {
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w) {
-                    const float bx = float((w & 1) * 8), by = float((w >> 1) * 4);
-                    const bool hit = mlx - h.x <= bx + 7.5f && mlx + h.x >= bx + 0.5f &&
-                                     mly - h.y <= by + 3.5f && mly + h.y >= by + 0.5f;
+                    const float bxf = float((w & 1) * 8), byf = float((w >> 1) * 4);
+                    const bool hit = mlx - h.x <= bxf + 7.5f && mlx + h.x >= bxf + 0.5f &&
+                                     mly - h.y <= byf + 3.5f && mly + h.y >= byf + 0.5f;
                     mask |= hit ? (1u << w) : 0u;
                 }
             }
