@@ -158,6 +158,42 @@ __global__ void __launch_bounds__(kMarkBlock, ALL_LEAF ? 4 : 2) k_filter_mark(co
     }
 }
 
+// Internal levels (the FP64-heavy 1/8 of the arena): one node per thread so
+// the long covariance dependency chains of many warps overlap.
+__global__ void __launch_bounds__(kMarkBlock) k_filter_mark_internal(
+    const Geom g, const GeomF f, const DevTree t, const double tau_r, const uint64_t end,
+    uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ qint_bits, const uint64_t n_words) {
+    const uint64_t i = uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x;
+    bool cand = false, qint = false;
+    if (i < end) {
+        const float mx = __ldcs(t.mx + i), my = __ldcs(t.my + i), mz = __ldcs(t.mz + i);
+        const float sx = __ldcs(t.sx + i), sy = __ldcs(t.sy + i), sz = __ldcs(t.sz + i);
+        const bool leaf = __ldcs(t.leaf + i) != 0;
+        float tz32;
+        int zs;
+        int vs = frustum_fp32(f, mx, my, mz, 3.0f * fmaxf(fmaxf(sx, sy), sz), tz32, zs);
+        if (vs < 0 || (!leaf && vs != 0)) {
+            double tx, ty, tz;
+            cam_transform(g, mx, my, mz, tx, ty, tz);
+            const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
+            vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
+            if (vs && !leaf && tz >= g.znear) {
+                const float4 q = __ldg(t.quat + i);
+                MarkOut o;
+                ewa_cov2d(g, tx, ty, tz, sx, sy, sz, q.x, q.y, q.z, q.w, o);
+                qint = o.radius <= tau_r;
+            }
+        }
+        cand = vs == 1 && (leaf || qint);
+    }
+    const unsigned cm = __ballot_sync(0xffffffffu, cand);
+    const unsigned qm = __ballot_sync(0xffffffffu, qint);
+    if ((threadIdx.x & 31) == 0 && (i >> 5) < n_words) {
+        cand_bits[i >> 5] = cm;
+        qint_bits[i >> 5] = qm;
+    }
+}
+
 // K2a: candidates walk their parent chains (filter.cpp:20-25); the keep bits
 // overwrite cand_bits in place (each word is read and written by one warp).
 __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
@@ -296,8 +332,8 @@ void launch_filter_mark(const Geom& g, const DevTree& t, double tau_r, uint32_t*
     const uint64_t per_cta = 4 * kMarkBlock;
     const uint64_t split = t.leaf_begin;  // multiple of per_cta; [split, n) are all leaves
     if (split > 0)
-        k_filter_mark<false><<<unsigned((split + per_cta - 1) / per_cta), kMarkBlock, 0, s>>>(
-            g, f, t, tau_r, 0, split, cand_bits, qint_bits, bit_words(t.n));
+        k_filter_mark_internal<<<unsigned((split + kMarkBlock - 1) / kMarkBlock), kMarkBlock, 0, s>>>(
+            g, f, t, tau_r, split, cand_bits, qint_bits, bit_words(t.n));
     if (t.n > split)
         k_filter_mark<true><<<unsigned((t.n - split + per_cta - 1) / per_cta), kMarkBlock, 0, s>>>(
             g, f, t, tau_r, split, t.n, cand_bits, qint_bits, bit_words(t.n));

@@ -167,7 +167,7 @@ __device__ __forceinline__ void block_add2(uint32_t a, uint32_t b, unsigned long
 // (rasterizer.cpp:56, near-plane drop) gets an empty rect tagged kDropped.
 // Keys carry the slot, whose order equals BlendList order, so the sort is
 // unchanged; the slot -> BlendList index map is only built for readbacks.
-__global__ void __launch_bounds__(kPrepBlock) k_preprocess(
+__global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
     const Geom g, const SplatRec* __restrict__ splat, const uint32_t* __restrict__ selected,
     const int kind, const double tau, const int tiles_x, const int tiles_y, PrepOut out,
     FrameCounters* cnt, const int use_hist) {
