@@ -104,27 +104,50 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
     bool done = !inside;
     if (__all_sync(0xffffffffu, done)) return;
 
+    // Software pipeline over 32-splat batches: keys are fetched two batches
+    // ahead and splat records one batch ahead, so the dependent key -> record
+    // global loads overlap the blending of the previous batch.
+    constexpr uint32_t kNone = 0xFFFFFFFFu;
+    struct Rec {
+        double2 m;
+        float4 q0, col;
+        float2 h;
+    };
+    auto load_key = [&](uint32_t at) -> uint32_t {
+        return at + lane < e ? uint32_t(keys[at + lane]) : kNone;
+    };
+    auto load_rec = [&](uint32_t gi, Rec& r) {
+        if (gi != kNone) {
+            r.m = *reinterpret_cast<const double2*>(&g64[gi].mx);
+            r.q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
+            r.col = *reinterpret_cast<const float4*>(&g32[gi].op);
+            r.h = *reinterpret_cast<const float2*>(&g32[gi].hx);
+        }
+    };
+    uint32_t gi_cur = load_key(b), gi_next = load_key(b + 32);
+    Rec cur, nxt;
+    load_rec(gi_cur, cur);
     for (uint32_t base = b; base < e; base += 32) {
-        // ---- stage the next 32 splats that touch this warp's block
+        // ---- stage the splats of this batch that touch this warp's block
         bool hit = false;
-        if (base + lane < e) {
-            const uint32_t gi = uint32_t(keys[base + lane]);
-            const double2 m = *reinterpret_cast<const double2*>(&g64[gi].mx);
-            const float2 h = *reinterpret_cast<const float2*>(&g32[gi].hx);
-            const float mlx = float(m.x - double(bx)), mly = float(m.y - double(by));
+        if (gi_cur != kNone) {
+            const float mlx = float(cur.m.x - double(bx)), mly = float(cur.m.y - double(by));
             // pixel centres of the block span [0.5, 7.5] x [0.5, 3.5]
+            const float2 h = cur.h;
             hit = h.x >= 0.0f && mlx - h.x <= 7.5f && mlx + h.x >= 0.5f && mly - h.y <= 3.5f &&
                   mly + h.y >= 0.5f;
             if (hit) {
-                const float4 q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
-                st.geo[lane] = make_float4(mlx, mly, q0.x, q0.z);
-                st.ct[lane] = make_float2(q0.y, q0.w);
-                st.col[lane] = *reinterpret_cast<const float4*>(&g32[gi].op);
-                st.gid[lane] = gi;
+                st.geo[lane] = make_float4(mlx, mly, cur.q0.x, cur.q0.z);
+                st.ct[lane] = make_float2(cur.q0.y, cur.q0.w);
+                st.col[lane] = cur.col;
+                st.gid[lane] = gi_cur;
             }
         }
         unsigned bits = __ballot_sync(0xffffffffu, hit);
         __syncwarp();
+        // ---- prefetch: records of the next batch, keys of the one after
+        const uint32_t gi_after = load_key(base + 64);
+        load_rec(gi_next, nxt);
         // ---- blend them front to back
         while (bits) {
             const int j = __ffs(bits) - 1;
@@ -157,6 +180,9 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
         }
         if (__all_sync(0xffffffffu, done)) break;
         __syncwarp();
+        gi_cur = gi_next;
+        gi_next = gi_after;
+        cur = nxt;
     }
     if (inside) {
         float* o = image + (size_t(y) * width + x) * 3;
