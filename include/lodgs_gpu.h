@@ -198,6 +198,15 @@ LODGS_API int lodgs_gpu_render(lodgs_gpu_scene *scene, const lodgs_camera *cam,
                      const lodgs_render_params *params, float *image_host,
                      lodgs_render_stats *stats);
 
+/* n frames through the render() contract, pipelined: frame i+1 is computed
+ * while frame i's image is copied to images_host[i] on a second stream
+ * (double-buffered device images).  images_host[i] may repeat a buffer only
+ * if the caller does not need frame i's image after frame i+2 starts.
+ * stats (nullable) receives n entries.  Overflowing frames are re-rendered. */
+LODGS_API int lodgs_gpu_render_batch(lodgs_gpu_scene *scene, const lodgs_camera *cams,
+                                     uint64_t n, const lodgs_render_params *params,
+                                     float *const *images_host, lodgs_render_stats *stats);
+
 /* Enqueue one frame on the scene stream and return without synchronising.
  * Sizes stay on the device; an undersized pair buffer is reported (and
  * grown) by the next lodgs_gpu_sync, which then returns LODGS_ERR_INTERNAL

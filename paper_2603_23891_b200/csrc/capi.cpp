@@ -173,6 +173,16 @@ int lodgs_gpu_render(lodgs_gpu_scene* scene, const lodgs_camera* cam,
     });
 }
 
+int lodgs_gpu_render_batch(lodgs_gpu_scene* scene, const lodgs_camera* cams, uint64_t n,
+                           const lodgs_render_params* params, float* const* images_host,
+                           lodgs_render_stats* stats) {
+    return guarded([&] {
+        if (n) need(cams, "cams");
+        need(params, "params");
+        S(scene).render_batch(cams, n, *params, images_host, stats);
+    });
+}
+
 int lodgs_gpu_render_async(lodgs_gpu_scene* scene, const lodgs_camera* cam,
                            const lodgs_render_params* params, float* image_host) {
     return guarded([&] {

@@ -26,6 +26,9 @@ struct DevTree {
 };
 
 // ---- filter (filter.cpp:115-150) ----
+// kernels enqueued per frame: mark (internal + leaf), select, compact,
+// preprocess, tile offsets, totals, emit, tile sort, big-tile sort, blend
+constexpr int kLaunchesPerFrame = 11;
 constexpr int kMarkBlock = 256;
 constexpr int kSelectBlock = 256;
 constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles

@@ -122,6 +122,15 @@ GpuScene::~GpuScene() {
     for (auto& a : prof_events_)
         for (auto& e : a) cudaEventDestroy(e);
     if (h_counters_) cudaFreeHost(h_counters_);
+    if (h_batch_counters_) cudaFreeHost(h_batch_counters_);
+    if (copy_stream_) {
+        cudaStreamSynchronize(copy_stream_);
+        cudaStreamDestroy(copy_stream_);
+        for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(frame_done_[k]);
+            cudaEventDestroy(copy_done_[k]);
+        }
+    }
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -219,7 +228,8 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     if (timing) FGS_CUDA(cudaEventRecord(ev_[3], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[4], stream_));
     launch_blend(res_.tile_offsets.p, keys_.p, g64_.p, g32_.p, col64_.p, res_.width, res_.height,
-                 res_.tiles_x, res_.tiles_y, exact, res_.image.p, stream_);
+                 res_.tiles_x, res_.tiles_y, exact, image_target_ ? image_target_ : res_.image.p,
+                 stream_);
     if (timing) FGS_CUDA(cudaEventRecord(ev_[4], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[5], stream_));
     FGS_CUDA(cudaGetLastError());
@@ -266,7 +276,7 @@ void GpuScene::finish(lodgs_render_stats* stats) {
         stats->filter_passes = 2;
         stats->filter_barriers = 2;
         stats->big_tiles = c.big_tiles;
-        stats->kernel_launches = 9;
+        stats->kernel_launches = kLaunchesPerFrame;
         if (last_timing_) {
             float ms = 0;
             FGS_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
@@ -291,6 +301,87 @@ void GpuScene::render(const lodgs_camera& cam, const lodgs_render_params& p, flo
             return;
         } catch (const Error& e) {
             if (e.code != LODGS_ERR_INTERNAL || attempt >= 4) throw;
+        }
+    }
+}
+
+void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_render_params& p,
+                            float* const* images_host, lodgs_render_stats* stats) {
+    DeviceGuard dg(device_);
+    if (n == 0) return;
+    for (uint64_t i = 0; i < n; ++i) {
+        const auto cv = validate_camera(cams[i]);
+        if (!cv.empty())
+            throw Error(LODGS_ERR_VALIDATION, join_violations("invalid camera", cv, cv.size()));
+        if (cams[i].width != cams[0].width || cams[i].height != cams[0].height)
+            throw Error(LODGS_ERR_VALIDATION, "render_batch: all frames share one image size");
+    }
+    if (!(p.tau_r > 0)) throw Error(LODGS_ERR_VALIDATION, "filter config: tau_r > 0");
+    if (p.shrink_kind < 0 || p.shrink_kind > 2)
+        throw Error(LODGS_ERR_VALIDATION, "shrink mode: unknown kind");
+    if (p.shrink_kind != LODGS_SHRINK_THREE_SIGMA && !(p.tau > 0.0 && p.tau < 1.0))
+        throw Error(LODGS_ERR_VALIDATION,
+                    "render: shrink tau in (0,1); adaptive needs calibration first");
+    ensure_resolution(int(cams[0].width), int(cams[0].height));
+    if (!copy_stream_) {
+        FGS_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            FGS_CUDA(cudaEventCreateWithFlags(&frame_done_[k], cudaEventDisableTiming));
+            FGS_CUDA(cudaEventCreateWithFlags(&copy_done_[k], cudaEventDisableTiming));
+        }
+    }
+    image2_.alloc(res_.image.n);
+    if (h_batch_cap_ < n) {
+        if (h_batch_counters_) FGS_CUDA(cudaFreeHost(h_batch_counters_));
+        FGS_CUDA(cudaMallocHost(&h_batch_counters_, n * sizeof(FrameCounters)));
+        h_batch_cap_ = n;
+    }
+    const uint64_t img_bytes = res_.image.n * sizeof(float);
+    float* bufs[2] = {res_.image.p, image2_.p};
+    last_timing_ = false;
+    last_keep_ = false;
+    last_exact_ = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const int k = int(i & 1);
+        // the blend may overwrite bufs[k] only once frame i-2's copy out of it is done
+        if (i >= 2) FGS_CUDA(cudaStreamWaitEvent(stream_, copy_done_[k], 0));
+        image_target_ = bufs[k];
+        enqueue_pipeline(camera_geom(cams[i]), p, int(cams[i].width), int(cams[i].height), false);
+        image_target_ = nullptr;
+        FGS_CUDA(cudaMemcpyAsync(h_batch_counters_ + i, d_counters_, sizeof(FrameCounters),
+                                 cudaMemcpyDeviceToHost, stream_));
+        FGS_CUDA(cudaEventRecord(frame_done_[k], stream_));
+        FGS_CUDA(cudaStreamWaitEvent(copy_stream_, frame_done_[k], 0));
+        if (images_host && images_host[i])
+            FGS_CUDA(cudaMemcpyAsync(images_host[i], bufs[k], img_bytes, cudaMemcpyDeviceToHost,
+                                     copy_stream_));
+        FGS_CUDA(cudaEventRecord(copy_done_[k], copy_stream_));
+    }
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    FGS_CUDA(cudaStreamSynchronize(copy_stream_));
+    // the last frame's image also lives in res_.image for read_image()
+    if (bufs[(n - 1) & 1] != res_.image.p)
+        FGS_CUDA(cudaMemcpy(res_.image.p, bufs[(n - 1) & 1], img_bytes, cudaMemcpyDeviceToDevice));
+    *h_counters_ = h_batch_counters_[n - 1];
+    for (uint64_t i = 0; i < n; ++i) {
+        const FrameCounters& c = h_batch_counters_[i];
+        if (c.nonfinite) throw Error(LODGS_ERR_VALIDATION, "projection produced non-finite values");
+        if (c.overflow) {  // rare: grow, then redo this frame synchronously
+            reserve_pairs(std::max<uint64_t>(pair_cap_ * 2, c.n_pairs + c.n_pairs / 4 + 1024));
+            render(cams[i], p, images_host ? images_host[i] : nullptr,
+                   stats ? stats + i : nullptr);
+            continue;
+        }
+        if (stats) {
+            lodgs_render_stats& s = stats[i];
+            std::memset(&s, 0, sizeof s);
+            s.n_selected = c.n_selected;
+            s.n_gaussians = c.n_gaussians;
+            s.n_pairs = c.n_pairs;
+            s.filter_passes = 2;
+            s.filter_barriers = 2;
+            s.big_tiles = c.big_tiles;
+            s.kernel_launches = kLaunchesPerFrame;
         }
     }
 }

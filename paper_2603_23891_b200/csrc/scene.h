@@ -69,6 +69,8 @@ public:
     void finish(lodgs_render_stats* stats);
     void render(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host,
                 lodgs_render_stats* stats);
+    void render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_render_params& p,
+                      float* const* images_host, lodgs_render_stats* stats);
 
     // stage entry points
     uint64_t filter(const lodgs_camera& cam, double tau_r, std::vector<uint32_t>& out);
@@ -137,6 +139,13 @@ private:
     bool last_timing_ = false;
     bool last_keep_ = false;
     bool last_exact_ = false;
+    // pipelined batches: second image buffer, copy stream, per-frame counters
+    float* image_target_ = nullptr;  // blend output override (nullptr: res_.image)
+    DevBuf<float> image2_;
+    cudaStream_t copy_stream_ = nullptr;
+    cudaEvent_t frame_done_[2] = {}, copy_done_[2] = {};
+    FrameCounters* h_batch_counters_ = nullptr;
+    uint64_t h_batch_cap_ = 0;
     bool profiling_ = false;
     std::vector<std::array<cudaEvent_t, 6>> prof_events_;
     size_t prof_used_ = 0;

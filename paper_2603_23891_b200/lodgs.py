@@ -161,6 +161,7 @@ ABI_SYMBOLS = (
     "lodgs_camera_path_sample", "lodgs_build_synthetic_tree",
     "lodgs_gpu_scene_create", "lodgs_gpu_scene_destroy", "lodgs_gpu_scene_stream",
     "lodgs_gpu_scene_reserve", "lodgs_gpu_scene_memory", "lodgs_gpu_render",
+    "lodgs_gpu_render_batch",
     "lodgs_gpu_render_async", "lodgs_gpu_sync", "lodgs_gpu_take_totals",
     "lodgs_gpu_profile", "lodgs_gpu_profile_read",
     "lodgs_gpu_read_image", "lodgs_gpu_image_device_ptr", "lodgs_gpu_read_selected",
@@ -204,6 +205,9 @@ def load_library():
         "lodgs_gpu_scene_memory": (C.c_int, [P, C.POINTER(C.c_uint64)]),
         "lodgs_gpu_render": (C.c_int, [P, C.POINTER(CameraC), C.POINTER(RenderParamsC), P,
                                        C.POINTER(RenderStatsC)]),
+        "lodgs_gpu_render_batch": (C.c_int, [P, C.POINTER(CameraC), C.c_uint64,
+                                             C.POINTER(RenderParamsC), C.POINTER(P),
+                                             C.POINTER(RenderStatsC)]),
         "lodgs_gpu_render_async": (C.c_int, [P, C.POINTER(CameraC), C.POINTER(RenderParamsC), P]),
         "lodgs_gpu_sync": (C.c_int, [P, C.POINTER(RenderStatsC)]),
         "lodgs_gpu_take_totals": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
@@ -666,6 +670,18 @@ class GpuScene:
             out.pairs = self.read_pairs()
             out.gaussians = self.read_gaussians()
         return out
+
+    def render_batch(self, cams, filter: FilterConfig, mode: ShrinkMode,
+                     opts: RenderOptions = RenderOptions(), host_ptrs=None):
+        """Pipelined frames (lodgs_gpu_render_batch): frame i+1 computes while frame i's
+        image is copied to host_ptrs[i] (raw pointers, e.g. pinned buffers)."""
+        n = len(cams)
+        cc = (CameraC * n)(*[c.to_c() for c in cams])
+        p = self.params(filter, mode, opts)
+        ptrs = (C.c_void_p * n)(*(host_ptrs if host_ptrs is not None else [None] * n))
+        st = (RenderStatsC * n)()
+        _check(self._lib.lodgs_gpu_render_batch(self._h, cc, n, C.byref(p), ptrs, st))
+        return [RenderStats.from_c(s) for s in st]
 
     def render_async(self, cam: Camera, params: RenderParamsC, image_host_ptr=None):
         c = cam.to_c()

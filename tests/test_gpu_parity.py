@@ -423,3 +423,25 @@ def test_render_cfg3_frame(L, oracle, gpu):
     with L.GpuScene(tree) as s:
         out, want = _check_render(L, oracle, s, tree, cam, 3.0, L.ShrinkMode.three_sigma())
     assert want["n_pairs"] > 1_000_000
+
+
+def test_render_batch_matches_single_frames(L, oracle, gpu):
+    """lodgs_gpu_render_batch (pipelined, double-buffered) returns the same images and
+    stats as one lodgs_gpu_render per frame."""
+    import ctypes as C
+
+    tree = L.make_tree(21, 3, 8, 0.5, 3, 3, 2)
+    rng = oracle.rng(17)
+    cams = [oracle.orbit_camera(rng, 200, 150, 14.0) for _ in range(5)]
+    for c in cams:
+        c.fx = c.fy = 150.0  # one intrinsics set: batch frames share the image size
+    imgs = [np.empty((150, 200, 3), np.float32) for _ in cams]
+    with L.GpuScene(tree) as s:
+        stats = s.render_batch(cams, L.FilterConfig(4.0), L.ShrinkMode.three_sigma(),
+                               host_ptrs=[im.ctypes.data for im in imgs])
+        for cam, im, st in zip(cams, imgs, stats):
+            one = s.render(cam, L.FilterConfig(4.0), L.ShrinkMode.three_sigma())
+            assert im.tobytes() == one.image.rgb.tobytes()
+            assert st.n_pairs == one.stats.n_pairs and st.n_selected == one.stats.n_selected
+            want = oracle.render(tree, cam, 4.0, L.ShrinkMode.three_sigma())
+            assert max_abs(im, want["image"]) <= IMG_TOL
