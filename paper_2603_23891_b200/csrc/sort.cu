@@ -82,11 +82,15 @@ __device__ __forceinline__ unsigned long long bitonic_pick(unsigned long long mi
 // 32 <= j < 256 through (double-buffered) shared memory with one named barrier
 // over the threads in play, j >= 256 inside the thread.  Only warps owning
 // slots < P take part: a 40-key bucket is one warp and never waits.
-template <int R>
+// P is a compile-time power of two (32..1024): every stage below unrolls with
+// constant distances, so the network is straight-line code.
+template <int LOGP>
 __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint32_t n,
-                                                 uint32_t P, unsigned long long* s_x) {
+                                                 unsigned long long* s_x) {
+    constexpr uint32_t P = 1u << LOGP;
+    constexpr int R = P > uint32_t(kSmallSortThreads) ? int(P / kSmallSortThreads) : 1;
+    constexpr uint32_t lanes = P < uint32_t(kSmallSortThreads) ? P : uint32_t(kSmallSortThreads);
     const uint32_t tid = threadIdx.x;
-    const uint32_t lanes = P < uint32_t(kSmallSortThreads) ? P : uint32_t(kSmallSortThreads);
     if (tid >= lanes) return;  // whole warps (lanes is a multiple of 32)
     unsigned long long v[R];
 #pragma unroll
@@ -95,7 +99,9 @@ __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint3
         v[r] = i < n ? keys[i] : ~0ull;
     }
     int parity = 0;
+#pragma unroll
     for (uint32_t k = 2; k <= P; k <<= 1) {
+#pragma unroll
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
             if (j >= uint32_t(kSmallSortThreads)) {
                 // partners in registers r and r ^ (j / 256); indices kept static
@@ -152,14 +158,12 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t*
     const uint32_t n = e - b;
     if (n < 2 || n > uint32_t(kSmallSortCap)) return;  // big buckets: k_tile_sort_big
     if (n <= uint32_t(kRegCap)) {
-        uint32_t P = 32;
-        while (P < n) P <<= 1;
-        if (P <= uint32_t(kSmallSortThreads))
-            register_bitonic<1>(keys + b, n, P, s);
-        else if (P <= 2u * kSmallSortThreads)
-            register_bitonic<2>(keys + b, n, P, s);
-        else
-            register_bitonic<4>(keys + b, n, P, s);
+        if (n <= 32u) register_bitonic<5>(keys + b, n, s);
+        else if (n <= 64u) register_bitonic<6>(keys + b, n, s);
+        else if (n <= 128u) register_bitonic<7>(keys + b, n, s);
+        else if (n <= 256u) register_bitonic<8>(keys + b, n, s);
+        else if (n <= 512u) register_bitonic<9>(keys + b, n, s);
+        else register_bitonic<10>(keys + b, n, s);
         return;
     }
     for (uint32_t i = threadIdx.x; i < n; i += kSmallSortThreads) s[i] = keys[b + i];
