@@ -76,12 +76,37 @@ constexpr int kFastThreads = 128;  // fast kernel: one CTA per 16x8 half tile
 constexpr int kFastWarps = kFastThreads / 32;
 constexpr int kFastParts = kTile * kTile / kFastThreads;
 
+// A hit splat, expanded around the centre of the warp's 8x4 block:
+//   e'(x, y) = A x^2 + B xy + C y^2 + D x + E y + F = e - ln(255 op),
+// (x, y) = pixel centre minus block centre, so x in [-3.5, 3.5], y in [-1.5, 1.5].
+// alpha = op exp(-e) = exp(-e') / 255; the reference skips iff e' > 0.
 struct WarpStage {
-    float4 geo[32];  // block-relative mean x, y, ha, hc
-    float2 ct[32];   // cb, ethr
-    float4 col[32];  // op, r, g, b
-    uint32_t gid[32];
+    float4 c0[32];   // A, B, C, D
+    float4 c1[32];   // E, F, M (certified |e'32 - e'| bound over the block), gid bits
+    float4 col[32];  // r, g, b, -
 };
+
+// Coefficients and the error bound M for one splat relative to block centre (u, v).
+// Every FP32 rounding in forming D, E, F and in the five-FMA evaluation is at
+// most 2^-24 of a magnitude that S below dominates term by term (the quadratic
+// and linear parts at |x| <= 3.5, |y| <= 1.5, the expansion of F, and ethr);
+// with the FP32 conic itself off by 2^-24 relative, |e'32 - e'| <= 2^-21 S.
+// M = 2^-20 S leaves a further factor of two.
+__device__ __forceinline__ void expand_splat(float u, float v, float ha, float cb, float hc,
+                                             float ethr, float4& c0, float4& c1,
+                                             uint32_t gid) {
+    const float hu = ha * u, hv = hc * v, bu = cb * u, bv = cb * v;
+    const float D = -__fmaf_rn(2.0f, hu, bv);
+    const float E = -__fmaf_rn(2.0f, hv, bu);
+    const float quad = __fmaf_rn(hu, u, __fmaf_rn(bu, v, hv * v));
+    const float F = quad - ethr;
+    const float S = ha * 12.25f + fabsf(cb) * 5.25f + hc * 2.25f +
+                    (fabsf(D) + 2.0f * fabsf(hu) + fabsf(bv)) * 3.5f +
+                    (fabsf(E) + fabsf(bu) + 2.0f * fabsf(hv)) * 1.5f + fabsf(F) +
+                    fabsf(hu * u) + fabsf(bu * v) + fabsf(hv * v) + fabsf(ethr);
+    c0 = make_float4(ha, cb, hc, D);
+    c1 = make_float4(E, F, S * 9.5367431640625e-07f + 1e-30f, __uint_as_float(gid));
+}
 
 __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
     const uint32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
@@ -98,8 +123,11 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
     const bool inside = x < width && y < height;
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
 
-    const float pxl = float(lane & 7) + 0.5f, pyl = float(lane >> 3) + 0.5f;
+    // pixel centre relative to the block centre (bx + 4, by + 2); exact in FP32
+    const float qx = float(lane & 7) - 3.5f, qy = float(lane >> 3) - 1.5f;
+    const float qxx = qx * qx, qxy = qx * qy, qyy = qy * qy;
     const double px = double(x) + 0.5, py = double(y) + 0.5;
+    const double cx = double(bx) + 4.0, cy = double(by) + 2.0;
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
     bool done = !inside;
     if (__all_sync(0xffffffffu, done)) return;
@@ -131,16 +159,17 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
         // ---- stage the splats of this batch that touch this warp's block
         bool hit = false;
         if (gi_cur != kNone) {
-            const float mlx = float(cur.m.x - double(bx)), mly = float(cur.m.y - double(by));
-            // pixel centres of the block span [0.5, 7.5] x [0.5, 3.5]
+            const float u = float(cur.m.x - cx), v = float(cur.m.y - cy);
+            // pixel centres of the block span [-3.5, 3.5] x [-1.5, 1.5]
             const float2 h = cur.h;
-            hit = h.x >= 0.0f && mlx - h.x <= 7.5f && mlx + h.x >= 0.5f && mly - h.y <= 3.5f &&
-                  mly + h.y >= 0.5f;
+            hit = h.x >= 0.0f && u - h.x <= 3.5f && u + h.x >= -3.5f && v - h.y <= 1.5f &&
+                  v + h.y >= -1.5f;
             if (hit) {
-                st.geo[lane] = make_float4(mlx, mly, cur.q0.x, cur.q0.z);
-                st.ct[lane] = make_float2(cur.q0.y, cur.q0.w);
-                st.col[lane] = cur.col;
-                st.gid[lane] = gi_cur;
+                float4 c0, c1;
+                expand_splat(u, v, cur.q0.x, cur.q0.y, cur.q0.z, cur.q0.w, c0, c1, gi_cur);
+                st.c0[lane] = c0;
+                st.c1[lane] = c1;
+                st.col[lane] = make_float4(cur.col.y, cur.col.z, cur.col.w, 0.0f);
             }
         }
         unsigned bits = __ballot_sync(0xffffffffu, hit);
@@ -152,29 +181,29 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
         while (bits) {
             const int j = __ffs(bits) - 1;
             bits &= bits - 1;
-            const float4 geo = st.geo[j];
-            const float2 ct = st.ct[j];
-            const float dx = pxl - geo.x, dy = pyl - geo.y;
-            const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
-            const float ev = __fmaf_rn(ct.x * dx, dy, Q);
-            const float d = ev - ct.y;
-            const float margin = __fmaf_rn(Q, 7.62939453125e-06f, 7.62939453125e-06f);
-            const float4 col = st.col[j];
-            float alpha = fminf(col.x * ex2_approx(ev * -1.4426950408889634f), 0.99f);
-            bool take = d < -margin;
-            const bool unsure = !done && fabsf(d) <= margin;
+            const float4 c0 = st.c0[j];
+            const float4 c1 = st.c1[j];
+            const float ep = __fmaf_rn(c0.x, qxx, __fmaf_rn(c0.y, qxy, __fmaf_rn(c0.z, qyy,
+                             __fmaf_rn(c0.w, qx, __fmaf_rn(c1.x, qy, c1.y)))));
+            const float M = c1.z;
+            // alpha = exp(-e') / 255 = 2^(-e' log2(e) - log2(255))
+            float alpha = fminf(ex2_approx(__fmaf_rn(ep, -1.4426950408889634f, -7.9943534368588578f)),
+                                0.99f);
+            bool take = ep < -M;
+            const bool unsure = !done && fabsf(ep) <= M;
             if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decision
                 if (unsure) {
-                    const Gauss64& G = g64[st.gid[j]];
+                    const Gauss64& G = g64[__float_as_uint(c1.w)];
                     const double a64 = alpha_exact(G.mx, G.my, G.ca, G.cb, G.cc, G.op, px, py);
                     take = a64 >= kMinAlpha;
                     alpha = float(a64);
                 }
             }
             const float w = (take && !done) ? alpha * T : 0.0f;
-            cr = __fmaf_rn(col.y, w, cr);
-            cg = __fmaf_rn(col.z, w, cg);
-            cb = __fmaf_rn(col.w, w, cb);
+            const float4 col = st.col[j];
+            cr = __fmaf_rn(col.x, w, cr);
+            cg = __fmaf_rn(col.y, w, cg);
+            cb = __fmaf_rn(col.z, w, cb);
             T = T - w;
             done = done || T < 1e-4f;
         }
