@@ -76,67 +76,18 @@ constexpr int kFastThreads = 128;  // fast kernel: one CTA per 16x8 half tile
 constexpr int kFastWarps = kFastThreads / 32;
 constexpr int kFastParts = kTile * kTile / kFastThreads;
 
-// A hit splat, expanded around the centre of the warp's 8x4 block:
-//   e'(x, y) = A x^2 + B xy + C y^2 + D x + E y + F = e - ln(255 op),
-// (x, y) = pixel centre minus block centre, so x in [-3.5, 3.5], y in [-1.5, 1.5].
-// alpha = op exp(-e) = exp(-e') / 255; the reference skips iff e' > 0.
 struct WarpStage {
-    float4 c0[32];   // A, B, C, D
-    float4 c1[32];   // E, F, M (certified |e'32 - e'| bound over the block), gid bits
-    float4 col[32];  // r, g, b, -
+    float4 geo[32];  // block-relative mean x, y, ha, hc
+    float2 ct[32];   // cb, ethr
+    float4 col[32];  // op, r, g, b
+    uint32_t gid[32];
 };
 
-// Coefficients and the error bound M for one splat relative to block centre (u, v).
-// Every FP32 rounding in forming D, E, F and in the five-FMA evaluation is at
-// most 2^-24 of a magnitude that S below dominates term by term (the quadratic
-// and linear parts at |x| <= 3.5, |y| <= 1.5, the expansion of F, and ethr);
-// with the FP32 conic itself off by 2^-24 relative, |e'32 - e'| <= 2^-21 S.
-// M = 2^-20 S leaves a further factor of two.
-__device__ __forceinline__ void expand_splat(float u, float v, float ha, float cb, float hc,
-                                             float ethr, float4& c0, float4& c1,
-                                             uint32_t gid) {
-    const float hu = ha * u, hv = hc * v, bu = cb * u, bv = cb * v;
-    const float D = -__fmaf_rn(2.0f, hu, bv);
-    const float E = -__fmaf_rn(2.0f, hv, bu);
-    const float quad = __fmaf_rn(hu, u, __fmaf_rn(bu, v, hv * v));
-    const float F = quad - ethr;
-    const float S = ha * 12.25f + fabsf(cb) * 5.25f + hc * 2.25f +
-                    (fabsf(D) + 2.0f * fabsf(hu) + fabsf(bv)) * 3.5f +
-                    (fabsf(E) + fabsf(bu) + 2.0f * fabsf(hv)) * 1.5f + fabsf(F) +
-                    fabsf(hu * u) + fabsf(bu * v) + fabsf(hv * v) + fabsf(ethr);
-    c0 = make_float4(ha, cb, hc, D);
-    c1 = make_float4(E, F, S * 9.5367431640625e-07f + 1e-30f, __uint_as_float(gid));
-}
-
-// One splat's blend inputs as copied by cp.async (4 x 16 B).
-struct __align__(16) RecSlot {
-    double2 m;   // mean x, y (Gauss64)
-    float4 q0;   // ha, cb, hc, ethr
-    float4 col;  // op, r, g, b
-    float4 h;    // hx, hy, pad, pad
-};
-struct RecBuf {
-    RecSlot s[32];
-};
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-__global__ void __launch_bounds__(kFastThreads, 10) k_blend_fast(
+__global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
     const uint32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
     const Gauss64* __restrict__ g64, const Gauss32* __restrict__ g32, const int width,
     const int height, const int tiles_x, float* __restrict__ image) {
     __shared__ WarpStage stage[kFastWarps];
-    __shared__ __align__(16) RecBuf recs[kFastWarps][2];
     const int tile = blockIdx.x / kFastParts, part = blockIdx.x % kFastParts;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpStage& st = stage[warp];
@@ -147,88 +98,83 @@ __global__ void __launch_bounds__(kFastThreads, 10) k_blend_fast(
     const bool inside = x < width && y < height;
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
 
-    // pixel centre relative to the block centre (bx + 4, by + 2); exact in FP32
-    const float qx = float(lane & 7) - 3.5f, qy = float(lane >> 3) - 1.5f;
+    const float pxl = float(lane & 7) + 0.5f, pyl = float(lane >> 3) + 0.5f;
     const double px = double(x) + 0.5, py = double(y) + 0.5;
-    const double cx = double(bx) + 4.0, cy = double(by) + 2.0;
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
     bool done = !inside;
     if (__all_sync(0xffffffffu, done)) return;
 
-    // Pipeline over 32-splat batches: each lane cp.async-copies the record of
-    // "its" splat of the next batch into the warp's shared buffer while the
-    // current batch is blended; keys are fetched two batches ahead.  Only the
-    // copying lane reads a slot, so per-thread wait_group suffices.
+    // Software pipeline over 32-splat batches: keys are fetched two batches
+    // ahead and splat records one batch ahead, so the dependent key -> record
+    // global loads overlap the blending of the previous batch.
     constexpr uint32_t kNone = 0xFFFFFFFFu;
+    struct Rec {
+        double2 m;
+        float4 q0, col;
+        float2 h;
+    };
     auto load_key = [&](uint32_t at) -> uint32_t {
         return at + lane < e ? uint32_t(keys[at + lane]) : kNone;
     };
-    auto fetch = [&](uint32_t gi, int buf) {
+    auto load_rec = [&](uint32_t gi, Rec& r) {
         if (gi != kNone) {
-            RecSlot& d = recs[warp][buf].s[lane];
-            cp_async16(&d.m, &g64[gi].mx);
-            cp_async16(&d.q0, &g32[gi].ha);
-            cp_async16(&d.col, &g32[gi].op);
-            cp_async16(&d.h, &g32[gi].hx);
+            r.m = *reinterpret_cast<const double2*>(&g64[gi].mx);
+            r.q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
+            r.col = *reinterpret_cast<const float4*>(&g32[gi].op);
+            r.h = *reinterpret_cast<const float2*>(&g32[gi].hx);
         }
-        cp_async_commit();
     };
     uint32_t gi_cur = load_key(b), gi_next = load_key(b + 32);
-    fetch(gi_cur, 0);
-    int buf = 0;
-    for (uint32_t base = b; base < e; base += 32, buf ^= 1) {
-        fetch(gi_next, buf ^ 1);
-        const uint32_t gi_after = load_key(base + 64);
-        cp_async_wait<1>();  // this lane's record of the current batch has landed
+    Rec cur, nxt;
+    load_rec(gi_cur, cur);
+    for (uint32_t base = b; base < e; base += 32) {
         // ---- stage the splats of this batch that touch this warp's block
         bool hit = false;
         if (gi_cur != kNone) {
-            const RecSlot& r = recs[warp][buf].s[lane];
-            const double2 m = r.m;
-            const float4 h4 = r.h;
-            const float u = float(m.x - cx), v = float(m.y - cy);
-            // pixel centres of the block span [-3.5, 3.5] x [-1.5, 1.5]
-            hit = h4.x >= 0.0f && u - h4.x <= 3.5f && u + h4.x >= -3.5f && v - h4.y <= 1.5f &&
-                  v + h4.y >= -1.5f;
+            const float mlx = float(cur.m.x - double(bx)), mly = float(cur.m.y - double(by));
+            // pixel centres of the block span [0.5, 7.5] x [0.5, 3.5]
+            const float2 h = cur.h;
+            hit = h.x >= 0.0f && mlx - h.x <= 7.5f && mlx + h.x >= 0.5f && mly - h.y <= 3.5f &&
+                  mly + h.y >= 0.5f;
             if (hit) {
-                const float4 q0 = r.q0, col = r.col;
-                float4 c0, c1;
-                expand_splat(u, v, q0.x, q0.y, q0.z, q0.w, c0, c1, gi_cur);
-                st.c0[lane] = c0;
-                st.c1[lane] = c1;
-                st.col[lane] = make_float4(col.y, col.z, col.w, 0.0f);
+                st.geo[lane] = make_float4(mlx, mly, cur.q0.x, cur.q0.z);
+                st.ct[lane] = make_float2(cur.q0.y, cur.q0.w);
+                st.col[lane] = cur.col;
+                st.gid[lane] = gi_cur;
             }
         }
         unsigned bits = __ballot_sync(0xffffffffu, hit);
         __syncwarp();
+        // ---- prefetch: records of the next batch, keys of the one after
+        const uint32_t gi_after = load_key(base + 64);
+        load_rec(gi_next, nxt);
         // ---- blend them front to back
-        const float qxx = qx * qx, qxy = qx * qy, qyy = qy * qy;
         while (bits) {
             const int j = __ffs(bits) - 1;
             bits &= bits - 1;
-            const float4 c0 = st.c0[j];
-            const float4 c1 = st.c1[j];
+            const float4 geo = st.geo[j];
+            const float2 ct = st.ct[j];
+            const float dx = pxl - geo.x, dy = pyl - geo.y;
+            const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
+            const float ev = __fmaf_rn(ct.x * dx, dy, Q);
+            const float d = ev - ct.y;
+            const float margin = __fmaf_rn(Q, 7.62939453125e-06f, 7.62939453125e-06f);
             const float4 col = st.col[j];
-            const float ep = __fmaf_rn(c0.x, qxx, __fmaf_rn(c0.y, qxy, __fmaf_rn(c0.z, qyy,
-                             __fmaf_rn(c0.w, qx, __fmaf_rn(c1.x, qy, c1.y)))));
-            const float M = c1.z;
-            // alpha = exp(-e') / 255 = 2^(-e' log2(e) - log2(255))
-            float alpha = fminf(ex2_approx(__fmaf_rn(ep, -1.4426950408889634f, -7.9943534368588578f)),
-                                0.99f);
-            bool take = ep < -M;
-            const bool unsure = !done && fabsf(ep) <= M;
+            float alpha = fminf(col.x * ex2_approx(ev * -1.4426950408889634f), 0.99f);
+            bool take = d < -margin;
+            const bool unsure = !done && fabsf(d) <= margin;
             if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decision
                 if (unsure) {
-                    const Gauss64& G = g64[__float_as_uint(c1.w)];
+                    const Gauss64& G = g64[st.gid[j]];
                     const double a64 = alpha_exact(G.mx, G.my, G.ca, G.cb, G.cc, G.op, px, py);
                     take = a64 >= kMinAlpha;
                     alpha = float(a64);
                 }
             }
             const float w = (take && !done) ? alpha * T : 0.0f;
-            cr = __fmaf_rn(col.x, w, cr);
-            cg = __fmaf_rn(col.y, w, cg);
-            cb = __fmaf_rn(col.z, w, cb);
+            cr = __fmaf_rn(col.y, w, cr);
+            cg = __fmaf_rn(col.z, w, cg);
+            cb = __fmaf_rn(col.w, w, cb);
             T = T - w;
             done = done || T < 1e-4f;
         }
@@ -236,8 +182,8 @@ __global__ void __launch_bounds__(kFastThreads, 10) k_blend_fast(
         __syncwarp();
         gi_cur = gi_next;
         gi_next = gi_after;
+        cur = nxt;
     }
-    cp_async_wait<0>();
     if (inside) {
         float* o = image + (size_t(y) * width + x) * 3;
         o[0] = cr;
