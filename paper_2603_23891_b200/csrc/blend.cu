@@ -84,11 +84,13 @@ struct WarpStage {
 };
 
 __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
-    const uint32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
-    const Gauss64* __restrict__ g64, const Gauss32* __restrict__ g32, const int width,
-    const int height, const int tiles_x, float* __restrict__ image) {
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
+    const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
+    const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
+    float* __restrict__ image) {
     __shared__ WarpStage stage[kFastWarps];
-    const int tile = blockIdx.x / kFastParts, part = blockIdx.x % kFastParts;
+    // heaviest tiles first (k_tile_offsets' schedule), halves of a tile adjacent
+    const int tile = int(order[blockIdx.x / kFastParts]), part = blockIdx.x % kFastParts;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpStage& st = stage[warp];
     // this warp's 8x4 block origin in image pixels
@@ -279,9 +281,9 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_exact(
     }
 }
 
-void launch_blend(const uint32_t* offsets, const unsigned long long* keys, const Gauss64* g64,
-                  const Gauss32* g32, const GaussCol64* col64, int width, int height,
-                  int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s) {
+void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
+                  const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
+                  int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s) {
     const int n_tiles = tiles_x * tiles_y;
     if (n_tiles <= 0) return;
     if (exact) {
@@ -294,8 +296,8 @@ void launch_blend(const uint32_t* offsets, const unsigned long long* keys, const
         k_blend_exact<<<n_tiles, kBlendThreads, smem, s>>>(offsets, keys, g64, g32, col64, width,
                                                             height, tiles_x, image);
     } else {
-        k_blend_fast<<<n_tiles * kFastParts, kFastThreads, 0, s>>>(offsets, keys, g64, g32, width,
-                                                                   height, tiles_x, image);
+        k_blend_fast<<<n_tiles * kFastParts, kFastThreads, 0, s>>>(offsets, order, keys, g64, g32,
+                                                                   width, height, tiles_x, image);
     }
 }
 

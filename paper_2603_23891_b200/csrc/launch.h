@@ -62,10 +62,11 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
                        uint64_t max_selected, int shrink_kind, double tau, int tiles_x,
                        int tiles_y, PrepOut out, FrameCounters* cnt, int grid, cudaStream_t s);
 // Turns the per-tile counts into offsets[n_tiles+1] and per-tile write cursors,
-// and lists the tiles whose segment exceeds the in-shared-memory sort capacity.
+// lists the tiles whose segment exceeds the in-shared-memory sort capacity, and
+// writes order[n_tiles]: tiles heaviest-first (log2 buckets) for the per-tile grids.
 void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
-                         uint32_t* cursor, uint32_t* big_list, FrameCounters* cnt,
-                         uint64_t pair_cap, cudaStream_t s);
+                         uint32_t* cursor, uint32_t* big_list, uint32_t* order,
+                         FrameCounters* cnt, uint64_t pair_cap, cudaStream_t s);
 // Key duplication: one key per (gaussian, overlapped tile) scattered into the
 // tile's bucket; key = depth_bits << 32 | gaussian.
 void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x, int n_tiles,
@@ -82,16 +83,16 @@ void launch_compact_records(const uint32_t* slot_of_g, uint64_t n_g, const Gauss
 // ---- sort (rasterizer.cpp:100-135) ----
 constexpr int kSmallSortCap = 4096;
 constexpr int kBigSortCap = 16384;
-void launch_tile_sort(const uint32_t* offsets, int n_tiles, unsigned long long* keys,
-                      uint32_t* big_list, FrameCounters* cnt, cudaStream_t s);
+void launch_tile_sort(const uint32_t* offsets, const uint32_t* order, int n_tiles,
+                      unsigned long long* keys, cudaStream_t s);
 void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
                           const uint32_t* big_list, FrameCounters* cnt, int grid,
                           cudaStream_t s);
 
 // ---- blend (rasterizer.cpp:137-165, blend_scalar.cpp:13-55) ----
-void launch_blend(const uint32_t* offsets, const unsigned long long* keys, const Gauss64* g64,
-                  const Gauss32* g32, const GaussCol64* col64, int width, int height,
-                  int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s);
+void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
+                  const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
+                  int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s);
 
 // ---- stage-entry helpers ----
 // Reference-order binning of an arbitrary gaussian list: counts, chained scan,

@@ -259,7 +259,8 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
 __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restrict__ count,
                                                        int n_tiles, uint32_t* offsets,
                                                        uint32_t* cursor, uint32_t* big_list,
-                                                       FrameCounters* cnt, uint64_t pair_cap) {
+                                                       uint32_t* order, FrameCounters* cnt,
+                                                       uint64_t pair_cap) {
     __shared__ uint32_t s_warp[32];
     __shared__ uint64_t s_carry;
     if (threadIdx.x == 0) s_carry = 0;
@@ -308,12 +309,37 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
         for (int t = threadIdx.x; t <= n_tiles; t += blockDim.x) offsets[t] = 0u;
         if (threadIdx.x == 0) cnt->big_tiles = 0u;
     }
+    // Longest-first schedule for the per-tile kernels (sort, blend): tiles
+    // counting-sorted by descending floor(log2(pairs)), so the heaviest CTAs
+    // start first and the tail of the grid is made of cheap ones.
+    __shared__ uint32_t s_bkt[34];
+    if (threadIdx.x < 34) s_bkt[threadIdx.x] = 0u;
+    __syncthreads();
+    const bool ovf = s_carry > pair_cap;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint32_t c = ovf ? 0u : count[t];
+        atomicAdd(&s_bkt[c ? 32 - __clz(c) : 0], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int k = 33; k >= 0; --k) {
+            const uint32_t c = s_bkt[k];
+            s_bkt[k] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint32_t c = ovf ? 0u : count[t];
+        order[atomicAdd(&s_bkt[c ? 32 - __clz(c) : 0], 1u)] = uint32_t(t);
+    }
 }
 
 void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
-                         uint32_t* cursor, uint32_t* big_list, FrameCounters* cnt,
-                         uint64_t pair_cap, cudaStream_t s) {
-    k_tile_offsets<<<1, 1024, 0, s>>>(tile_count, n_tiles, offsets, cursor, big_list, cnt,
+                         uint32_t* cursor, uint32_t* big_list, uint32_t* order,
+                         FrameCounters* cnt, uint64_t pair_cap, cudaStream_t s) {
+    k_tile_offsets<<<1, 1024, 0, s>>>(tile_count, n_tiles, offsets, cursor, big_list, order, cnt,
                                       pair_cap);
 }
 

@@ -165,6 +165,7 @@ void GpuScene::ensure_resolution(int w, int h) {
     res_.tile_offsets.alloc(n_tiles + 1);
     res_.tile_cursor.alloc(n_tiles + 1);
     res_.big_list.alloc(n_tiles + 1);
+    res_.tile_order.alloc(n_tiles + 1);
     res_.image.alloc(uint64_t(w) * h * 3);
     const uint64_t b_cnt = align256(sizeof(FrameCounters));
     const uint64_t b_sel = align256(uint64_t(select_tiles(tree_.n) + 1) * 8);
@@ -215,21 +216,21 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     launch_preprocess(g, tree_, selected_.p, tree_.n, p.shrink_kind, p.tau, res_.tiles_x,
                       res_.tiles_y, out, d_counters_, persistent_grid_, stream_);
     launch_tile_offsets(d_tile_count_, n_tiles, res_.tile_offsets.p, res_.tile_cursor.p,
-                        res_.big_list.p, d_counters_, pair_cap_, stream_);
+                        res_.big_list.p, res_.tile_order.p, d_counters_, pair_cap_, stream_);
     launch_update_totals(d_counters_, res_.tile_offsets.p, n_tiles, totals_.p, stream_);
     launch_emit_keys(emit_.p, d_counters_, res_.tiles_x, n_tiles, res_.tile_cursor.p, keys_.p,
                      persistent_grid_, stream_);
     maps_valid_ = false;
     if (timing) FGS_CUDA(cudaEventRecord(ev_[2], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[3], stream_));
-    launch_tile_sort(res_.tile_offsets.p, n_tiles, keys_.p, res_.big_list.p, d_counters_, stream_);
+    launch_tile_sort(res_.tile_offsets.p, res_.tile_order.p, n_tiles, keys_.p, stream_);
     launch_tile_sort_big(res_.tile_offsets.p, keys_.p, res_.big_list.p, d_counters_,
                          std::min(sm_count_, 64), stream_);
     if (timing) FGS_CUDA(cudaEventRecord(ev_[3], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[4], stream_));
-    launch_blend(res_.tile_offsets.p, keys_.p, g64_.p, g32_.p, col64_.p, res_.width, res_.height,
-                 res_.tiles_x, res_.tiles_y, exact, image_target_ ? image_target_ : res_.image.p,
-                 stream_);
+    launch_blend(res_.tile_offsets.p, res_.tile_order.p, keys_.p, g64_.p, g32_.p, col64_.p,
+                 res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact,
+                 image_target_ ? image_target_ : res_.image.p, stream_);
     if (timing) FGS_CUDA(cudaEventRecord(ev_[4], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[5], stream_));
     FGS_CUDA(cudaGetLastError());
@@ -720,16 +721,17 @@ void stage_sort_pairs(lodgs_tile_pair* pairs, uint64_t n) {
     FGS_CUDA(cudaMemsetAsync(z.p, 0, b_cnt + b_tc, c.s));
     auto* cnt = reinterpret_cast<FrameCounters*>(z.p);
     auto* tc = reinterpret_cast<uint32_t*>(z.p + b_cnt);
-    DevBuf<uint32_t> off, cur, big;
+    DevBuf<uint32_t> off, cur, big, ord;
     off.alloc(n_buckets + 1);
     cur.alloc(n_buckets + 1);
     big.alloc(n_buckets + 1);
+    ord.alloc(n_buckets + 1);
     DevBuf<unsigned long long> keys;
     keys.alloc(n);
     launch_bucket_triples(in.p, n, tc, c.s);
-    launch_tile_offsets(tc, n_buckets, off.p, cur.p, big.p, cnt, n, c.s);
+    launch_tile_offsets(tc, n_buckets, off.p, cur.p, big.p, ord.p, cnt, n, c.s);
     launch_scatter_triples(in.p, n, cur.p, keys.p, c.s);
-    launch_tile_sort(off.p, n_buckets, keys.p, big.p, cnt, c.s);
+    launch_tile_sort(off.p, ord.p, n_buckets, keys.p, c.s);
     launch_tile_sort_big(off.p, keys.p, big.p, cnt, 64, c.s);
     launch_gather_triples(off.p, n_buckets, keys.p, in.p, outb.p, c.s);
     FGS_CUDA(cudaGetLastError());
@@ -764,19 +766,20 @@ void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_bl
     FGS_CUDA(cudaMemsetAsync(z.p, 0, b_cnt + b_tc, c.s));
     auto* cnt = reinterpret_cast<FrameCounters*>(z.p);
     auto* tc = reinterpret_cast<uint32_t*>(z.p + b_cnt);
-    DevBuf<uint32_t> off, cur, big;
+    DevBuf<uint32_t> off, cur, big, ord;
     off.alloc(n_tiles + 1);
     cur.alloc(n_tiles + 1);
     big.alloc(n_tiles + 1);
+    ord.alloc(n_tiles + 1);
     DevBuf<unsigned long long> keys;
     keys.alloc(n);
     DevBuf<float> img;
     img.alloc(uint64_t(width) * height * 3);
     launch_bucket_triples(tri.p, n, tc, c.s);
-    launch_tile_offsets(tc, n_tiles, off.p, cur.p, big.p, cnt, n, c.s);
+    launch_tile_offsets(tc, n_tiles, off.p, cur.p, big.p, ord.p, cnt, n, c.s);
     launch_triples_to_keys(tri.p, n, keys.p, c.s);
-    launch_blend(off.p, keys.p, dl.g64.p, dl.g32.p, dl.col64.p, width, height, tiles_x, tiles_y,
-                 exact, img.p, c.s);
+    launch_blend(off.p, ord.p, keys.p, dl.g64.p, dl.g32.p, dl.col64.p, width, height, tiles_x,
+                 tiles_y, exact, img.p, c.s);
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaMemcpyAsync(image, img.p, img.n * 4, cudaMemcpyDeviceToHost, c.s));
     FGS_CUDA(cudaStreamSynchronize(c.s));

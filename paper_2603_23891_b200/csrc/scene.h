@@ -50,7 +50,7 @@ struct DeviceGuard {
 // Per-frame scratch sized for one image resolution.
 struct ResolutionBuffers {
     int width = 0, height = 0, tiles_x = 0, tiles_y = 0;
-    DevBuf<uint32_t> tile_offsets, tile_cursor, big_list;
+    DevBuf<uint32_t> tile_offsets, tile_cursor, big_list, tile_order;
     DevBuf<float> image;
 };
 

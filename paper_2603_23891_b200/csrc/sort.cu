@@ -152,9 +152,11 @@ __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint3
 }
 
 __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t* __restrict__ offsets,
+                                                                 const uint32_t* __restrict__ order,
                                                                  unsigned long long* keys) {
     __shared__ unsigned long long s[kSmallSortCap];
-    const uint32_t b = offsets[blockIdx.x], e = offsets[blockIdx.x + 1];
+    const uint32_t tile = order[blockIdx.x];  // heaviest buckets first
+    const uint32_t b = offsets[tile], e = offsets[tile + 1];
     const uint32_t n = e - b;
     if (n < 2 || n > uint32_t(kSmallSortCap)) return;  // big buckets: k_tile_sort_big
     if (n <= uint32_t(kRegCap)) {
@@ -208,10 +210,10 @@ __global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_
     }
 }
 
-void launch_tile_sort(const uint32_t* offsets, int n_tiles, unsigned long long* keys,
-                      uint32_t* /*big_list*/, FrameCounters* /*cnt*/, cudaStream_t s) {
+void launch_tile_sort(const uint32_t* offsets, const uint32_t* order, int n_tiles,
+                      unsigned long long* keys, cudaStream_t s) {
     if (n_tiles <= 0) return;
-    k_tile_sort<<<n_tiles, kSmallSortThreads, 0, s>>>(offsets, keys);
+    k_tile_sort<<<n_tiles, kSmallSortThreads, 0, s>>>(offsets, order, keys);
 }
 
 void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
