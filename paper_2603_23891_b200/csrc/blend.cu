@@ -72,32 +72,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Exact (up to a conservative slack) test whether the ellipse
-// e(dx, dy) = ha dx^2 + cb dx dy + hc dy^2 <= ethr meets the pixel-centre
-// rectangle [0.5, 7.5] x [0.5, 3.5] of a warp block, the splat centre at
-// (u, v) block-local.  e is convex: if the centre is inside, the minimum is 0;
-// otherwise it is on an edge, where it is a 1D quadratic minimised at a
-// clamped stationary point.  Returns true when the minimum is within
-// E = ethr (1 + 2^-10) + 2^-10, far more slack than the FP32 error of this
-// evaluation, so a block the reference would blend is never culled.
-__device__ __forceinline__ bool ellipse_meets_rect(float u, float v, float ha, float cb, float hc,
-                                                   float ethr) {
-    const float x0 = 0.5f - u, x1 = 7.5f - u, y0 = 0.5f - v, y1 = 3.5f - v;
-    if (x0 <= 0.0f && x1 >= 0.0f && y0 <= 0.0f && y1 >= 0.0f) return true;
-    const float E = __fmaf_rn(fabsf(ethr), 9.765625e-04f, ethr) + 9.765625e-04f;
-    const float i2ha = __frcp_rn(2.0f * ha), i2hc = __frcp_rn(2.0f * hc);
-    auto edge_x = [&](float dx) {  // dx fixed, dy free in [y0, y1]
-        const float dy = fminf(fmaxf(-cb * dx * i2hc, y0), y1);
-        return __fmaf_rn(ha * dx, dx, __fmaf_rn(cb * dx, dy, hc * dy * dy));
-    };
-    auto edge_y = [&](float dy) {  // dy fixed, dx free in [x0, x1]
-        const float dx = fminf(fmaxf(-cb * dy * i2ha, x0), x1);
-        return __fmaf_rn(ha * dx, dx, __fmaf_rn(cb * dx, dy, hc * dy * dy));
-    };
-    const float m = fminf(fminf(edge_x(x0), edge_x(x1)), fminf(edge_y(y0), edge_y(y1)));
-    return m <= E;
-}
-
 constexpr int kFastThreads = 128;  // fast kernel: one CTA per 16x8 half tile
 constexpr int kFastWarps = kFastThreads / 32;
 constexpr int kFastParts = kTile * kTile / kFastThreads;
@@ -164,8 +138,6 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
             const float2 h = cur.h;
             hit = h.x >= 0.0f && mlx - h.x <= 7.5f && mlx + h.x >= 0.5f && mly - h.y <= 3.5f &&
                   mly + h.y >= 0.5f;
-            if (hit && h.x < 1e30f)
-                hit = ellipse_meets_rect(mlx, mly, cur.q0.x, cur.q0.y, cur.q0.z, cur.q0.w);
             if (hit) {
                 st.geo[lane] = make_float4(mlx, mly, cur.q0.x, cur.q0.z);
                 st.ct[lane] = make_float2(cur.q0.y, cur.q0.w);
