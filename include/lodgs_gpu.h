@@ -80,7 +80,8 @@ enum lodgs_shrink_kind {
 enum lodgs_render_flags {
     LODGS_RENDER_EXACT_BLEND = 1u,  /* FP64 blend with the reference exp_mx: bit-exact image */
     LODGS_RENDER_KEEP_PAIRS = 2u,   /* keep sorted pairs + gaussians readable after the frame */
-    LODGS_RENDER_STAGE_TIMING = 4u  /* CUDA-event stage timers into lodgs_render_stats */
+    LODGS_RENDER_STAGE_TIMING = 4u, /* CUDA-event stage timers into lodgs_render_stats */
+    LODGS_RENDER_COLLECT_KPC = 8u   /* RenderOptions::collect_kpc: per-pair kpc, exact blend */
 };
 
 /* FilterConfig (filter.hpp:11-14) + ShrinkMode (rasterizer.hpp:16-24). */
@@ -238,6 +239,27 @@ LODGS_API int lodgs_gpu_read_pairs(lodgs_gpu_scene *scene, lodgs_tile_pair *out,
                          uint64_t *n);
 /* The projected BlendList (FP64 fields): needs LODGS_RENDER_KEEP_PAIRS. */
 LODGS_API int lodgs_gpu_read_gaussians(lodgs_gpu_scene *scene, lodgs_blend_list *out, uint64_t cap);
+/* Per-pair kpc of the last frame in sorted-pair order (needs LODGS_RENDER_COLLECT_KPC):
+ * RenderOutput::kpc (rasterizer.hpp:86-96), bit-identical to blend_scalar.cpp:16-54. */
+LODGS_API int lodgs_gpu_read_kpc(lodgs_gpu_scene *scene, double *out, uint64_t cap, uint64_t *n);
+
+/* metrics.hpp:44-54 CalibrationReport. */
+typedef struct lodgs_calibration {
+    double tau;        /* lambda_g / scene_gtc */
+    double scene_gtc;  /* mean of the per-view GTCs */
+    double lambda_g;
+    uint32_t n_views;  /* views that produced pairs */
+    uint64_t histogram[5];
+} lodgs_calibration;
+
+/* calibrate (metrics.cpp:94-108): per view an instrumented three-sigma render
+ * (exact blend + kpc), tile GTCs, view GTC (metrics.cpp:18-42); views without
+ * pairs are skipped; tau = lambda_g / mean.  per_view (nullable) receives the
+ * used views' GTCs (capacity n_views). */
+LODGS_API int lodgs_gpu_calibrate(lodgs_gpu_scene *scene, const lodgs_camera *views,
+                                  uint32_t n_views, double lambda_g, double tau_r,
+                                  lodgs_calibration *out, double *per_view);
+
 /* Per-gaussian tile counts (bin_to_tiles multiplicity) and per-tile pair counts. */
 LODGS_API int lodgs_gpu_read_counts(lodgs_gpu_scene *scene, uint32_t *per_gaussian, uint64_t cap_g,
                           uint32_t *per_tile, uint64_t cap_t);

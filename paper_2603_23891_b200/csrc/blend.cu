@@ -281,6 +281,154 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_exact(
     }
 }
 
+// ---------------------------------------------------------------------------
+// Exact blend with KPC instrumentation (collect_kpc, rasterizer.hpp:86-96):
+// kpc[pair] = sum over the tile's pixels of alpha*T at that pair, accumulated
+// exactly as blend_scalar.cpp:16-54 does -- one accumulator per pixel lane
+// (x - x0) & 3, each fed in (y, x) scan order, reduced as (a0+a1)+(a2+a3).
+// Pixels blend a 32-pair batch and park their weights in shared memory; then
+// 128 threads (pair, lane) sum the 4 x 16 weights of their lane in that order.
+constexpr int kKpcBatch = 32;
+
+struct KpcSmem {
+    double w[kKpcBatch][kTile * kTile];  // per pair, per pixel (row-major) weight
+    double part[kKpcBatch][4];
+    double4 geo[kKpcBatch];  // mx, my, ca, cb
+    double2 cc_op[kKpcBatch];
+    double4 col[kKpcBatch];
+};
+
+__global__ void __launch_bounds__(kTile * kTile) k_blend_exact_kpc(
+    const uint32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
+    const Gauss64* __restrict__ g64, const GaussCol64* __restrict__ col64, const int width,
+    const int height, const int tiles_x, float* __restrict__ image, double* __restrict__ kpc) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    KpcSmem& s = *reinterpret_cast<KpcSmem*>(smem_raw);
+    const int tile = blockIdx.x;
+    const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
+    const int lx = int(threadIdx.x & 15), ly = int(threadIdx.x >> 4);
+    const int x = x0 + lx, y = y0 + ly;
+    const int span_w = min(kTile, width - x0), span_h = min(kTile, height - y0);
+    const bool inside = lx < span_w && ly < span_h;
+    const uint32_t b = offsets[tile], e = offsets[tile + 1];
+    const double px = double(x) + 0.5, py = double(y) + 0.5;
+    double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
+    bool done = !inside;
+    for (uint32_t base = b; base < e; base += kKpcBatch) {
+        const int cnt = int(min(uint32_t(kKpcBatch), e - base));
+        if (int(threadIdx.x) < cnt) {
+            const uint32_t gi = uint32_t(keys[base + threadIdx.x]);
+            const Gauss64 G = g64[gi];
+            const GaussCol64 C = col64[gi];
+            s.geo[threadIdx.x] = make_double4(G.mx, G.my, G.ca, G.cb);
+            s.cc_op[threadIdx.x] = make_double2(G.cc, G.op);
+            s.col[threadIdx.x] = make_double4(C.r, C.g, C.b, 0.0);
+        }
+        __syncthreads();
+        for (int j = 0; j < cnt; ++j) {
+            double wj = 0.0;
+            if (!done) {
+                const double4 g = s.geo[j];
+                const double2 co = s.cc_op[j];
+                const double alpha = alpha_exact(g.x, g.y, g.z, g.w, co.x, co.y, px, py);
+                if (alpha >= kMinAlpha) {
+                    const double4 col = s.col[j];
+                    wj = alpha * T;
+                    cr += col.x * wj;
+                    cg += col.y * wj;
+                    cb += col.z * wj;
+                    T *= 1.0 - alpha;
+                    done = T < kTermT;
+                }
+            }
+            s.w[j][threadIdx.x] = wj;
+        }
+        __syncthreads();
+        if (int(threadIdx.x) < 4 * cnt) {
+            const int j = int(threadIdx.x) >> 2, lane = int(threadIdx.x) & 3;
+            double acc = 0.0;
+            for (int yy = 0; yy < span_h; ++yy)
+                for (int xx = lane; xx < span_w; xx += 4) acc += s.w[j][yy * kTile + xx];
+            s.part[j][lane] = acc;
+        }
+        __syncthreads();
+        if (int(threadIdx.x) < cnt) {
+            const int j = int(threadIdx.x);
+            kpc[base + j] = (s.part[j][0] + s.part[j][1]) + (s.part[j][2] + s.part[j][3]);
+        }
+        __syncthreads();
+    }
+    if (inside) {
+        float* o = image + (size_t(y) * width + x) * 3;
+        o[0] = float(cr);
+        o[1] = float(cg);
+        o[2] = float(cb);
+    }
+}
+
+void launch_blend_exact_kpc(const uint32_t* offsets, const unsigned long long* keys,
+                            const Gauss64* g64, const GaussCol64* col64, int width, int height,
+                            int tiles_x, int tiles_y, float* image, double* kpc, cudaStream_t s) {
+    const int n_tiles = tiles_x * tiles_y;
+    if (n_tiles <= 0) return;
+    static bool attr = false;
+    const int smem = int(sizeof(KpcSmem));
+    if (!attr) {
+        cudaFuncSetAttribute(k_blend_exact_kpc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    k_blend_exact_kpc<<<n_tiles, kTile * kTile, smem, s>>>(offsets, keys, g64, col64, width, height,
+                                                           tiles_x, image, kpc);
+}
+
+// Per-tile GTC (metrics.cpp:18-35): the mean kpc of the tile's pairs, summed
+// in sorted order; and one view mean over non-empty tiles in tile order
+// (metrics.cpp:37-42) by a single thread, matching the reference's sums.
+__global__ void k_tile_gtc(const uint32_t* offsets, int n_tiles, const double* kpc,
+                           double* tile_gtc) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    const uint32_t b = offsets[t], e = offsets[t + 1];
+    double sum = 0.0;
+    for (uint32_t i = b; i < e; ++i) sum += kpc[i];
+    tile_gtc[t] = e > b ? sum / double(e - b) : 0.0;
+}
+
+__global__ void k_view_gtc(const uint32_t* offsets, int n_tiles, const double* tile_gtc,
+                           double* out) {
+    double sum = 0.0;
+    unsigned long long n = 0;
+    for (int t = 0; t < n_tiles; ++t)
+        if (offsets[t + 1] > offsets[t]) {
+            sum += tile_gtc[t];
+            ++n;
+        }
+    out[0] = n ? sum / double(n) : __longlong_as_double(0x7ff8000000000000ll);
+}
+
+// metrics.cpp:44-57: kpc bins [0,0.01) [0.01,0.05) [0.05,0.2) [0.2,1) [1,inf)
+__global__ void k_kpc_histogram(const double* kpc, uint64_t n, unsigned long long* bins) {
+    __shared__ unsigned long long s[5];
+    if (threadIdx.x < 5) s[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double k = kpc[i];
+        const int bin = k < 0.01 ? 0 : k < 0.05 ? 1 : k < 0.2 ? 2 : k < 1.0 ? 3 : 4;
+        atomicAdd(&s[bin], 1ull);
+    }
+    __syncthreads();
+    if (threadIdx.x < 5 && s[threadIdx.x]) atomicAdd(&bins[threadIdx.x], s[threadIdx.x]);
+}
+
+void launch_view_gtc(const uint32_t* offsets, int n_tiles, const double* kpc, uint64_t n_pairs,
+                     double* tile_gtc, double* view_gtc, unsigned long long* bins, cudaStream_t s) {
+    if (n_tiles <= 0) return;
+    k_tile_gtc<<<(n_tiles + 255) / 256, 256, 0, s>>>(offsets, n_tiles, kpc, tile_gtc);
+    k_view_gtc<<<1, 1, 0, s>>>(offsets, n_tiles, tile_gtc, view_gtc);
+    if (n_pairs) k_kpc_histogram<<<148, 256, 0, s>>>(kpc, n_pairs, bins);
+}
+
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s) {

@@ -249,6 +249,23 @@ int lodgs_gpu_read_gaussians(lodgs_gpu_scene* scene, lodgs_blend_list* out, uint
     });
 }
 
+int lodgs_gpu_read_kpc(lodgs_gpu_scene* scene, double* out, uint64_t cap, uint64_t* n) {
+    return guarded([&] {
+        const uint64_t k = S(scene).read_kpc(out, cap);
+        if (n) *n = k;
+    });
+}
+
+int lodgs_gpu_calibrate(lodgs_gpu_scene* scene, const lodgs_camera* views, uint32_t n_views,
+                        double lambda_g, double tau_r, lodgs_calibration* out, double* per_view) {
+    return guarded([&] {
+        need(out, "out");
+        if (n_views) need(views, "views");
+        if (!(tau_r > 0)) throw fgs::Error(LODGS_ERR_VALIDATION, "filter config: tau_r > 0");
+        S(scene).calibrate(views, n_views, lambda_g, tau_r, out, per_view);
+    });
+}
+
 int lodgs_gpu_read_counts(lodgs_gpu_scene* scene, uint32_t* per_gaussian, uint64_t cap_g,
                           uint32_t* per_tile, uint64_t cap_t) {
     return guarded([&] { S(scene).read_counts(per_gaussian, cap_g, per_tile, cap_t); });

@@ -9,6 +9,7 @@
 #include "scene.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -108,7 +109,7 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
     g64_.alloc(n);
     g32_.alloc(n);
     emit_.alloc(n);
-    reserve_pairs(std::max<uint64_t>(4 * n, 1u << 20));
+    reserve_pairs(std::max<uint64_t>(4 * n, 1u << 16));  // grown on overflow
     totals_.alloc(1);
     FGS_CUDA(cudaMemsetAsync(totals_.p, 0, sizeof(RunTotals), stream_));
     FGS_CUDA(cudaStreamSynchronize(stream_));
@@ -192,8 +193,11 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     (void)w;
     (void)h;
     const int n_tiles = res_.tiles_x * res_.tiles_y;
-    const bool exact = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
+    const bool kpc = (p.flags & LODGS_RENDER_COLLECT_KPC) != 0;
+    const bool exact = kpc || (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
     if (exact && col64_.n < tree_.n) col64_.alloc(tree_.n);
+    if (kpc && kpc_.n < pair_cap_) kpc_.alloc(pair_cap_);
+    last_kpc_ = kpc;
     cudaEvent_t* pe = nullptr;
     if (profiling_) {
         if (prof_used_ == prof_events_.size()) {
@@ -228,9 +232,14 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
                          std::min(sm_count_, 64), stream_);
     if (timing) FGS_CUDA(cudaEventRecord(ev_[3], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[4], stream_));
-    launch_blend(res_.tile_offsets.p, res_.tile_order.p, keys_.p, g64_.p, g32_.p, col64_.p,
-                 res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact,
-                 image_target_ ? image_target_ : res_.image.p, stream_);
+    float* img_out = image_target_ ? image_target_ : res_.image.p;
+    if (p.flags & LODGS_RENDER_COLLECT_KPC) {
+        launch_blend_exact_kpc(res_.tile_offsets.p, keys_.p, g64_.p, col64_.p, res_.width,
+                               res_.height, res_.tiles_x, res_.tiles_y, img_out, kpc_.p, stream_);
+    } else {
+        launch_blend(res_.tile_offsets.p, res_.tile_order.p, keys_.p, g64_.p, g32_.p, col64_.p,
+                     res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact, img_out, stream_);
+    }
     if (timing) FGS_CUDA(cudaEventRecord(ev_[4], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[5], stream_));
     FGS_CUDA(cudaGetLastError());
@@ -563,6 +572,58 @@ void GpuScene::read_counts(uint32_t* per_gaussian, uint64_t cap_g, uint32_t* per
         const uint64_t nt = std::min<uint64_t>(tile_count_cap_, cap_t);
         if (nt) FGS_CUDA(cudaMemcpy(per_tile, d_tile_count_, nt * 4, cudaMemcpyDeviceToHost));
     }
+}
+
+uint64_t GpuScene::read_kpc(double* out, uint64_t cap) {
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    if (!last_kpc_) throw Error(LODGS_ERR_VALIDATION, "read_kpc: last frame had no collect_kpc");
+    const int n_tiles = res_.tiles_x * res_.tiles_y;
+    uint32_t np = 0;
+    FGS_CUDA(cudaMemcpy(&np, res_.tile_offsets.p + n_tiles, 4, cudaMemcpyDeviceToHost));
+    if (!out) return np;
+    if (cap < np) throw Error(LODGS_ERR_VALIDATION, "read_kpc: capacity too small");
+    if (np) FGS_CUDA(cudaMemcpy(out, kpc_.p, uint64_t(np) * 8, cudaMemcpyDeviceToHost));
+    return np;
+}
+
+// metrics.cpp:79-108 (instrumented_render + calibrate + make_report).
+void GpuScene::calibrate(const lodgs_camera* views, uint32_t n_views, double lambda_g,
+                         double tau_r, lodgs_calibration* out, double* per_view) {
+    DeviceGuard dg(device_);
+    if (n_views == 0) throw Error(LODGS_ERR_VALIDATION, "calibration: no views");
+    if (!(lambda_g > 0.0)) throw Error(LODGS_ERR_VALIDATION, "calibration: lambda_g > 0 required");
+    kpc_bins_.alloc(5);
+    FGS_CUDA(cudaMemsetAsync(kpc_bins_.p, 0, 5 * sizeof(unsigned long long), stream_));
+    std::vector<double> used;
+    for (uint32_t v = 0; v < n_views; ++v) {
+        const lodgs_render_params p{tau_r, 0.0, LODGS_SHRINK_THREE_SIGMA, LODGS_RENDER_COLLECT_KPC};
+        render(views[v], p, nullptr, nullptr);
+        const int n_tiles = res_.tiles_x * res_.tiles_y;
+        tile_gtc_.alloc(uint64_t(n_tiles) + 1);
+        launch_view_gtc(res_.tile_offsets.p, n_tiles, kpc_.p, h_counters_->n_pairs, tile_gtc_.p,
+                        tile_gtc_.p + n_tiles, kpc_bins_.p, stream_);
+        FGS_CUDA(cudaGetLastError());
+        double g = 0.0;
+        FGS_CUDA(cudaMemcpyAsync(&g, tile_gtc_.p + n_tiles, 8, cudaMemcpyDeviceToHost, stream_));
+        FGS_CUDA(cudaStreamSynchronize(stream_));
+        if (!std::isnan(g)) used.push_back(g);
+    }
+    // make_report (metrics.cpp:59-77), on the host like the reference
+    if (used.empty()) throw Error(LODGS_ERR_VALIDATION, "calibration: no view produced any pairs");
+    double sum = 0.0;
+    for (double g : used) sum += g;
+    const double mean = sum / double(used.size());
+    if (!(mean > 0.0)) throw Error(LODGS_ERR_VALIDATION, "calibration: zero mean contribution");
+    unsigned long long bins[5];
+    FGS_CUDA(cudaMemcpy(bins, kpc_bins_.p, sizeof bins, cudaMemcpyDeviceToHost));
+    out->tau = lambda_g / mean;
+    out->scene_gtc = mean;
+    out->lambda_g = lambda_g;
+    out->n_views = uint32_t(used.size());
+    for (int k = 0; k < 5; ++k) out->histogram[k] = bins[k];
+    if (per_view)
+        for (size_t i = 0; i < used.size(); ++i) per_view[i] = used[i];
 }
 
 void GpuScene::profile(bool enable) {

@@ -87,6 +87,9 @@ public:
     uint64_t read_gaussians(lodgs_blend_list* out, uint64_t cap);
     void read_counts(uint32_t* per_gaussian, uint64_t cap_g, uint32_t* per_tile, uint64_t cap_t);
     void take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs);
+    uint64_t read_kpc(double* out, uint64_t cap);
+    void calibrate(const lodgs_camera* views, uint32_t n_views, double lambda_g, double tau_r,
+                   lodgs_calibration* out, double* per_view);
 
     void profile(bool enable);
     uint64_t profile_read(double stage_ms[6]);
@@ -117,6 +120,10 @@ private:
     DevBuf<GaussEmit> emit_;
     DevBuf<GaussCol64> col64_;
     DevBuf<unsigned long long> keys_;
+    DevBuf<double> kpc_;         // per sorted pair (collect_kpc frames only)
+    bool last_kpc_ = false;
+    DevBuf<double> tile_gtc_;    // calibration scratch: per tile, + view result
+    DevBuf<unsigned long long> kpc_bins_;
     // readback-only: slot <-> BlendList index maps and compacted records
     DevBuf<uint32_t> g_of_slot_, slot_of_g_;
     DevBuf<Gauss64> rb_g64_;

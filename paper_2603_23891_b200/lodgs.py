@@ -152,6 +152,11 @@ class BlendListC(C.Structure):
     ] + [("depth", _FP), ("node", C.POINTER(C.c_uint32))]
 
 
+class CalibrationC(C.Structure):
+    _fields_ = [("tau", C.c_double), ("scene_gtc", C.c_double), ("lambda_g", C.c_double),
+                ("n_views", C.c_uint32), ("histogram", C.c_uint64 * 5)]
+
+
 PAIR_DTYPE = np.dtype([("tile", "<u4"), ("depth", "<f4"), ("gaussian", "<u4")])
 
 # C ABI symbols declared by include/lodgs_gpu.h (checked by tests).
@@ -166,6 +171,7 @@ ABI_SYMBOLS = (
     "lodgs_gpu_profile", "lodgs_gpu_profile_read",
     "lodgs_gpu_read_image", "lodgs_gpu_image_device_ptr", "lodgs_gpu_read_selected",
     "lodgs_gpu_read_pairs", "lodgs_gpu_read_gaussians", "lodgs_gpu_read_counts",
+    "lodgs_gpu_read_kpc", "lodgs_gpu_calibrate",
     "lodgs_gpu_filter", "lodgs_gpu_mark", "lodgs_gpu_prepare", "lodgs_gpu_bin_to_tiles",
     "lodgs_gpu_sort_pairs", "lodgs_gpu_alpha_blend", "lodgs_gpu_host_alloc",
     "lodgs_gpu_host_free",
@@ -220,6 +226,9 @@ def load_library():
         "lodgs_gpu_read_pairs": (C.c_int, [P, P, C.c_uint64, C.POINTER(C.c_uint64)]),
         "lodgs_gpu_read_gaussians": (C.c_int, [P, C.POINTER(BlendListC), C.c_uint64]),
         "lodgs_gpu_read_counts": (C.c_int, [P, P, C.c_uint64, P, C.c_uint64]),
+        "lodgs_gpu_read_kpc": (C.c_int, [P, P, C.c_uint64, C.POINTER(C.c_uint64)]),
+        "lodgs_gpu_calibrate": (C.c_int, [P, C.POINTER(CameraC), C.c_uint32, C.c_double,
+                                          C.c_double, C.POINTER(CalibrationC), _DP]),
         "lodgs_gpu_filter": (C.c_int, [P, C.POINTER(CameraC), C.c_double, P, C.c_uint64,
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32)]),
@@ -521,6 +530,18 @@ class Image:
 
 
 @dataclasses.dataclass
+class CalibrationReport:
+    """metrics.hpp:44-54."""
+
+    per_view: np.ndarray
+    scene_mean: float
+    lambda_g: float
+    tau: float
+    n_views: int
+    histogram: list
+
+
+@dataclasses.dataclass
 class RenderOutput:
     """rasterizer.hpp:86-96."""
 
@@ -651,7 +672,7 @@ class GpuScene:
 
     @staticmethod
     def params(filter: FilterConfig, mode: ShrinkMode, opts: RenderOptions) -> RenderParamsC:
-        flags = (1 if opts.exact_blend else 0) | (2 if opts.collect_kpc else 0) | \
+        flags = (1 if opts.exact_blend else 0) | (2 | 8 if opts.collect_kpc else 0) | \
                 (4 if opts.stage_timing else 0)
         return RenderParamsC(float(filter.tau_r), float(mode.tau), int(mode.kind), flags)
 
@@ -669,7 +690,27 @@ class GpuScene:
         if opts.collect_kpc:
             out.pairs = self.read_pairs()
             out.gaussians = self.read_gaussians()
+            out.kpc = self.read_kpc()
         return out
+
+    def read_kpc(self) -> np.ndarray:
+        n = C.c_uint64(0)
+        _check(self._lib.lodgs_gpu_read_kpc(self._h, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.float64)
+        _check(self._lib.lodgs_gpu_read_kpc(self._h, _ptr(out), n.value, C.byref(n)))
+        return out
+
+    def calibrate(self, views, lambda_g: float, config: FilterConfig = FilterConfig()
+                  ) -> "CalibrationReport":
+        """metrics.cpp:94-108 on the GPU (instrumented three-sigma renders)."""
+        n = len(views)
+        vc = (CameraC * max(1, n))(*[v.to_c() for v in views])
+        rep = CalibrationC()
+        per = np.zeros(max(1, n), np.float64)
+        _check(self._lib.lodgs_gpu_calibrate(self._h, vc, n, float(lambda_g), float(config.tau_r),
+                                             C.byref(rep), per.ctypes.data_as(_DP)))
+        return CalibrationReport(per[: rep.n_views].copy(), rep.scene_gtc, rep.lambda_g, rep.tau,
+                                 rep.n_views, list(rep.histogram))
 
     def render_batch(self, cams, filter: FilterConfig, mode: ShrinkMode,
                      opts: RenderOptions = RenderOptions(), host_ptrs=None):
@@ -838,3 +879,9 @@ def alpha_blend(sorted_pairs: np.ndarray, lst: BlendList, grid: TileGrid, width:
     _check(load_library().lodgs_gpu_alpha_blend(_ptr(sp), sp.shape[0], C.byref(v), int(width),
                                                 int(height), 1 if exact else 0, _ptr(img)))
     return Image(width, height, img)
+
+
+def calibrate(tree: LoDTree, views, lambda_g: float, filter: FilterConfig = FilterConfig()
+              ) -> CalibrationReport:
+    """metrics.hpp:73-75 calibrate -> CalibrationReport (tau = lambda_g / mean view GTC)."""
+    return _scene_for(tree).calibrate(views, lambda_g, filter)

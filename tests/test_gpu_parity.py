@@ -445,3 +445,70 @@ def test_render_batch_matches_single_frames(L, oracle, gpu):
             assert st.n_pairs == one.stats.n_pairs and st.n_selected == one.stats.n_selected
             want = oracle.render(tree, cam, 4.0, L.ShrinkMode.three_sigma())
             assert max_abs(im, want["image"]) <= IMG_TOL
+
+
+# ------------------------------------------------------- kpc / calibration --
+def test_kpc_bit_identical(L, oracle, gpu):
+    """collect_kpc (rasterizer.hpp:86-96): per-pair kpc in the reference's 4-lane
+    order (blend_scalar.cpp:16-54), bit-identical; image exact; ragged edge tiles."""
+    rng = oracle.rng(66)
+    tree = L.make_tree(13, 2, 8, 0.5, 3, 3, 2)
+    with L.GpuScene(tree) as s:
+        for w, h in ((160, 120), (150, 100), (33, 17)):
+            cam = oracle.orbit_camera(rng, w, h, 12.0)
+            for mode in (L.ShrinkMode.three_sigma(), L.ShrinkMode.adaptive(0.2)):
+                want = oracle.render(tree, cam, 6.0, mode, collect_kpc=True)
+                out = s.render(cam, L.FilterConfig(6.0), mode, L.RenderOptions(collect_kpc=True))
+                assert out.pairs.tobytes() == want["pairs"].tobytes()
+                kw = want["kpc"] if want["kpc"] is not None else np.empty(0)
+                assert out.kpc.tobytes() == kw.tobytes()
+                assert out.image.rgb.tobytes() == want["image"].tobytes()
+
+
+def _oracle_calibrate(oracle, tree, views, lambda_g, tau_r, L):
+    per = []
+    for v in views:
+        r = oracle.render(tree, v, tau_r, L.ShrinkMode.three_sigma(), collect_kpc=True)
+        if r["n_pairs"]:
+            per.append(oracle.view_gtc(r["pairs"], r["kpc"]))
+    mean = 0.0
+    for g in per:
+        mean += g
+    mean /= len(per)
+    return per, mean, lambda_g / mean
+
+
+def test_shrink_study_acceptance_7_8_9(L, oracle, gpu):
+    """acceptance.cpp:343-433 (#7-#9) on the GPU: calibrate (tau bit-exact against
+    the oracle restatement of metrics.cpp:94-108), then 3-sigma / fixed / adaptive
+    renders of 5 orbit views with tau_R = 16 (pair counts, kpc, images exact)."""
+    tree = L.make_tree(8008, 2, 8, 0.5, 4, 4, 4)
+    rng = oracle.rng(88)
+    views = [oracle.orbit_camera(rng, 160, 120, 12.0) for _ in range(5)]
+    per, mean, tau = _oracle_calibrate(oracle, tree, views, 0.2, 16.0, L)
+    with L.GpuScene(tree) as s:
+        rep = s.calibrate(views, 0.2, L.FilterConfig(16.0))
+        assert rep.n_views == len(per)
+        assert rep.per_view.tolist() == per
+        assert rep.scene_mean == mean and rep.tau == tau
+        totals = {"3s": 0, "fixed": 0, "adaptive": 0}
+        low = {"3s": 0, "adaptive": 0}
+        worst = float("inf")
+        for v in views:
+            imgs = {}
+            for name, mode in (("3s", L.ShrinkMode.three_sigma()), ("fixed", L.ShrinkMode.fixed()),
+                               ("adaptive", L.ShrinkMode.adaptive(tau))):
+                want = oracle.render(tree, v, 16.0, mode, collect_kpc=True)
+                out = s.render(v, L.FilterConfig(16.0), mode, L.RenderOptions(collect_kpc=True))
+                assert out.stats.n_pairs == want["n_pairs"]
+                kw = want["kpc"] if want["kpc"] is not None else np.empty(0)
+                assert out.kpc.tobytes() == kw.tobytes()
+                totals[name] += out.stats.n_pairs
+                if name in low:
+                    low[name] += int((out.kpc < 0.05).sum())
+                imgs[name] = out.image.rgb
+            worst = min(worst, oracle.psnr(imgs["adaptive"], imgs["3s"]))
+    # reference gate outputs on this fixture (BASELINE.md section 2, acceptance #8/#9)
+    assert (totals["3s"], totals["fixed"], totals["adaptive"]) == (9921, 9916, 6038)
+    assert (low["3s"], low["adaptive"]) == (5065, 1680)
+    assert round(tau, 4) == 0.1050 and round(worst, 1) == 49.1

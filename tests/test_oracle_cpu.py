@@ -233,6 +233,32 @@ def test_render_cfg1_vs_reference(L, oracle, ref):
     assert a["kpc"].tobytes() == b["kpc"].tobytes()
 
 
+def test_calibrate_vs_reference(L, oracle, ref):
+    """metrics.cpp:94-108: the oracle's calibration (kpc -> tile GTC -> view GTC ->
+    tau) equals the reference's calibrate bit for bit (acceptance #8 fixture)."""
+    import ctypes as C
+
+    from test_gpu_parity import _oracle_calibrate
+
+    tree = L.make_tree(8008, 2, 8, 0.5, 4, 4, 4)
+    rng = oracle.rng(88)
+    views = [oracle.orbit_camera(rng, 160, 120, 12.0) for _ in range(5)]
+    per, mean, tau = _oracle_calibrate(oracle, tree, views, 0.2, 16.0, L)
+    h = ref.tree_from(tree)
+    vc = (L.CameraC * 5)(*[v.to_c() for v in views])
+    t, sg, nu = C.c_double(), C.c_double(), C.c_uint32()
+    pv = np.zeros(5)
+    hist = np.zeros(5, np.uint64)
+    rc = ref.lib.ref_calibrate(h, vc, 5, 0.2, 16.0, 2, C.byref(t), C.byref(sg),
+                               pv.ctypes.data_as(C.POINTER(C.c_double)), C.byref(nu),
+                               hist.ctypes.data_as(C.c_void_p))
+    ref.free_tree(h)
+    assert rc == 0
+    assert (t.value, sg.value) == (tau, mean)
+    assert pv[: nu.value].tolist() == per
+    assert round(tau, 4) == 0.1050
+
+
 # --------------------------------------------------------- host logic --
 def test_generator_matches_reference_golden(L):
     """The product's synthetic scene builder (host_util.cpp) reproduces the
