@@ -265,7 +265,7 @@ void GpuScene::enqueue_frame(const lodgs_camera& cam, const lodgs_render_params&
     FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
                              cudaMemcpyDeviceToHost, stream_));
     if (image_host)
-        FGS_CUDA(cudaMemcpyAsync(image_host, res_.image.p, res_.image.n * sizeof(float),
+        FGS_CUDA(cudaMemcpyAsync(image_host, res_.image.p, image_floats() * sizeof(float),
                                  cudaMemcpyDeviceToHost, stream_));
 }
 
@@ -340,13 +340,13 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
             FGS_CUDA(cudaEventCreateWithFlags(&copy_done_[k], cudaEventDisableTiming));
         }
     }
-    image2_.alloc(res_.image.n);
+    image2_.alloc(image_floats());
     if (h_batch_cap_ < n) {
         if (h_batch_counters_) FGS_CUDA(cudaFreeHost(h_batch_counters_));
         FGS_CUDA(cudaMallocHost(&h_batch_counters_, n * sizeof(FrameCounters)));
         h_batch_cap_ = n;
     }
-    const uint64_t img_bytes = res_.image.n * sizeof(float);
+    const uint64_t img_bytes = image_floats() * sizeof(float);
     float* bufs[2] = {res_.image.p, image2_.p};
     last_timing_ = false;
     last_keep_ = false;
@@ -466,7 +466,7 @@ uint64_t GpuScene::prepare(const lodgs_camera& cam, const uint32_t* selected, ui
 void GpuScene::read_image(float* out) {
     DeviceGuard dg(device_);
     FGS_CUDA(cudaStreamSynchronize(stream_));
-    FGS_CUDA(cudaMemcpy(out, res_.image.p, res_.image.n * sizeof(float), cudaMemcpyDeviceToHost));
+    FGS_CUDA(cudaMemcpy(out, res_.image.p, image_floats() * sizeof(float), cudaMemcpyDeviceToHost));
 }
 
 uint64_t GpuScene::read_selected(uint32_t* out, uint64_t cap) {

@@ -82,6 +82,9 @@ public:
     // readbacks of the last frame
     void read_image(float* out);
     const float* image_device() const { return res_.image.p; }
+    // floats of the current frame's image (buffers may be larger after a
+    // resolution change: DevBuf only ever grows)
+    uint64_t image_floats() const { return uint64_t(res_.width) * res_.height * 3; }
     uint64_t read_selected(uint32_t* out, uint64_t cap);
     uint64_t read_pairs(lodgs_tile_pair* out, uint64_t cap);
     uint64_t read_gaussians(lodgs_blend_list* out, uint64_t cap);
