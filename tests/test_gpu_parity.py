@@ -447,6 +447,20 @@ def test_render_batch_matches_single_frames(L, oracle, gpu):
             assert max_abs(im, want["image"]) <= IMG_TOL
 
 
+def test_cfg4_50m_4k(L, oracle, gpu):
+    """cfg 4 scale (50,142,872 nodes, 3840x2160, fx = 2000): selected list
+    bit-exact at altitude 300, and a full frame at altitude 400 (pairs, counts,
+    exact image bit-identical, fast image within tolerance)."""
+    tree = L.build_synthetic_tree(nx=103, ny=104, seed=1, depth=4, build_seed=7)
+    assert tree.node_count() == 50142872
+    with L.GpuScene(tree) as s:
+        cam = topdown_camera(3840, 2160, 2000.0, 300.0)
+        want, _, _ = oracle.filter(tree, cam, 3.0)
+        assert np.array_equal(s.filter(cam, L.FilterConfig(3.0)).selected, want)
+        cam = topdown_camera(3840, 2160, 2000.0, 400.0)
+        _check_render(L, oracle, s, tree, cam, 3.0, L.ShrinkMode.three_sigma())
+
+
 # ------------------------------------------------------- kpc / calibration --
 def test_kpc_bit_identical(L, oracle, gpu):
     """collect_kpc (rasterizer.hpp:86-96): per-pair kpc in the reference's 4-lane
