@@ -1,0 +1,19 @@
+#!/bin/bash
+# One gpurun call: GPU parity tests, a bench line, a launch list and an ncu --set full
+# capture of the frame kernels.  Usage (on the box): bash tools/gpu_check.sh TAG [skip-tests]
+set -u
+TAG=${1:-run}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/smi.txt 2>&1
+if [ "${2:-}" != "skip-tests" ]; then
+  timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log
+  tail -3 $OUT/pytest_gpu.log
+fi
+timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?"
+tail -c 3000 $OUT/bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 400 --csv \
+   --log-file $OUT/launches.csv python bench.py --steps 60 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1; echo "ncu launches exit $?"
+timeout 900 ncu --set full --clock-control none --import-source on \
+   -k regex:'k_filter|k_compact|k_blend_fast|k_tile_sort|k_preprocess|k_emit' -s 30 -c 8 \
+   -o $OUT/prof python tools/profile_frames.py --alt 200 --frames 6 > $OUT/ncu_full.log 2>&1; echo "ncu full exit $?"
