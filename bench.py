@@ -290,7 +290,7 @@ def run_b200(args, rank, world, local):
     mark_ms = stage_ms[0] / max(1, pf)
     sort_ms = stage_ms[3] / max(1, pf)
     sort_bytes = 16 * mean_pairs  # read + write of each 8-byte key
-    stage_names = ["filter_mark", "filter_select", "preprocess_keys", "tile_sort", "blend"]
+    stage_names = ["filter_internal", "filter_leaves_compact", "preprocess_keys", "tile_sort", "blend"]
     per_stage = {k: round(stage_ms[i] / max(1, pf), 5) for i, k in enumerate(stage_names)}
     dominant = max(range(5), key=lambda i: stage_ms[i])
     filt_gbs = filt_bytes / (filt_ms * 1e-3) / 1e9

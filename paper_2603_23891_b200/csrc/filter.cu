@@ -1,33 +1,50 @@
 // filter.cu -- the traversal-free parallel LoD filter (FilterGS),
 // reference filter_parallel (filter.cpp:115-150).
 //
-// K1 mark: one flat coalesced pass over the SoA arena.  Per node: camera
-// transform + sphere-vs-frustum (FP64, exact), and -- only for visible,
-// projectable internal nodes -- the EWA radius.  A leaf's qpass is never
-// read by the selection rule (candidates use vis && (qpass || leaf),
-// ancestors use qpass && !leaf, filter.cpp:23,137), so leaves and culled
-// nodes skip the covariance entirely.  Output: two bitmasks written by warp
-// ballot, cand = vis && (qpass || leaf) and qint = qpass && !leaf.
+// The reference marks every node (pass 1), then lets every candidate walk its
+// parent chain against the marks (pass 2) and compacts the survivors in node
+// order.  On the device the arena splits at `leaf_begin`: [0, leaf_begin)
+// holds every internal node (1/8 of a K=8 tree), [leaf_begin, n) only leaves
+// (DevTree::leaf_begin).  Three kernels per frame:
 //
-// K2 select: candidates walk their parent chain against the L2-resident qint
-// bitmask (filter.cpp:20-25); survivors are compacted in node order by a
-// single-pass chained scan, so `selected` comes out strictly increasing as
-// filter.cpp:147-148 produces it.
+//   F1 k_mark_internal    [0, leaf_begin): frustum + (for visible internal
+//                         nodes) the EWA radius -> cand / qint bitmasks.
+//   F2 k_select_internal  [0, leaf_begin): parent-chain walks
+//                         (filter.cpp:20-25) -> keep bits, compacted into
+//                         `selected` in node order; the qint words are
+//                         overwritten in place with blk = qint | disq, i.e.
+//                         "a child of this node is disqualified".
+//   F3 k_filter_leaves    [leaf_begin, n): frustum, keep = vis && !blk[parent],
+//                         compacted straight into `selected` -- the leaf bulk
+//                         of the arena is read exactly once and never
+//                         re-visited.  The chained scan continues F2's, so
+//                         `selected` comes out strictly increasing as
+//                         filter.cpp:147-148 produces it.
+//
+// All decisions are the reference's FP64 decisions (mark_core.hpp:24-116,
+// bit-exact).  They are reached in FP32 with certified error bounds, and only
+// the nodes whose FP32 value falls inside the bound recompute in FP64.
+#include <cmath>
+
 #include "launch.h"
 #include "mark.cuh"
 #include "scan.cuh"
 
 namespace fgs {
 
-// FP32 copy of the camera for the certified pre-test.
+// FP32 copy of the camera for the certified pre-tests.
 struct GeomF {
     float r[9], t[3];
     float p2x, p2z, p3x, p3z, p4y, p4z, p5y, p5z;  // side-plane coefficients
     float znear, zfar;
     float c0;  // max(|t_i|, znear, zfar) + 1: magnitude term of the error bound
+    float fx, fy;
+    // qpass thresholds on lambda_max: radius = 3 sqrt(lambda) <= tau_r is
+    // certain below thr_pass and impossible above thr_fail
+    float thr_pass, thr_fail;
 };
 
-GeomF make_geomf(const Geom& g) {
+GeomF make_geomf(const Geom& g, double tau_r) {
     GeomF f;
     for (int i = 0; i < 9; ++i) f.r[i] = float(g.rot[i]);
     double c0 = 0.0;
@@ -46,6 +63,17 @@ GeomF make_geomf(const Geom& g) {
     f.znear = float(g.znear);
     f.zfar = float(g.zfar);
     f.c0 = float(fmax(c0, fmax(g.znear, g.zfar)) + 1.0);
+    f.fx = float(g.fx);
+    f.fy = float(g.fy);
+    // (tau/3)^2 with a relative margin of 2^-20 each way, rounded outward to
+    // float; the FP64 3*sqrt(lambda) <= tau test cannot flip inside it.
+    const double l = (tau_r / 3.0) * (tau_r / 3.0);
+    const double lp = l * (1.0 - 0x1p-20), lf = l * (1.0 + 0x1p-20);
+    float fp = float(lp), ff = float(lf);
+    if (double(fp) > lp) fp = nextafterf(fp, 0.0f);
+    if (double(ff) < lf) ff = nextafterf(ff, INFINITY);
+    f.thr_pass = std::isfinite(lp) ? fp : 0.0f;  // tau_r huge: no FP32 pass decision
+    f.thr_fail = std::isfinite(lf) ? ff : INFINITY;
     return f;
 }
 
@@ -56,9 +84,12 @@ GeomF make_geomf(const Geom& g) {
 // 3B + 2^-22 |.|.  When min_p(d_p + r3) clears +-E, E = 4B + 2^-22 r3, the
 // FP64 reference decision (mark_core.hpp:32-40) is certain; only the
 // remainder (nodes within ~1e-3 world units of a frustum plane) recompute in
-// FP64.  Returns 1 visible, 0 culled, -1 undecided; *zs likewise for z_ok.
+// FP64.  Returns 1 visible, 0 culled, -1 undecided; zs likewise for z_ok.
+struct Cam32 {
+    float tx, ty, tz, B;
+};
 __device__ __forceinline__ int frustum_fp32(const GeomF& f, float mx, float my, float mz,
-                                            float r3, float& tz_out, int& zs) {
+                                            float r3, Cam32& c, int& zs) {
     const float tx = __fmaf_rn(f.r[0], mx, __fmaf_rn(f.r[1], my, __fmaf_rn(f.r[2], mz, f.t[0])));
     const float ty = __fmaf_rn(f.r[3], mx, __fmaf_rn(f.r[4], my, __fmaf_rn(f.r[5], mz, f.t[1])));
     const float tz = __fmaf_rn(f.r[6], mx, __fmaf_rn(f.r[7], my, __fmaf_rn(f.r[8], mz, f.t[2])));
@@ -73,149 +104,218 @@ __device__ __forceinline__ int frustum_fp32(const GeomF& f, float mx, float my, 
     const float m = fminf(fminf(fminf(dn, df), fminf(dl, dr)), fminf(dt, db));
     const float dz = tz - f.znear;
     zs = dz > E ? 1 : (dz < -E ? 0 : -1);
-    tz_out = tz;
+    c.tx = tx;
+    c.ty = ty;
+    c.tz = tz;
+    c.B = B;
     return m > E ? 1 : (m < -E ? 0 : -1);
 }
 
-// ALL_LEAF: the launch covers a range known (at upload) to hold only leaves --
-// the last level of a level-major tree -- so the EWA covariance is never
-// needed and the kernel stays register-light (full occupancy for the
-// bandwidth-bound bulk of the arena).
-template <bool ALL_LEAF>
-__global__ void __launch_bounds__(kMarkBlock, ALL_LEAF ? 4 : 2) k_filter_mark(const Geom g, const GeomF f,
-                                                              const DevTree t,
-                                                              const double tau_r,
-                                                              const uint64_t begin,
-                                                              const uint64_t end,
-                                                              uint32_t* __restrict__ cand_bits,
-                                                              uint32_t* __restrict__ qint_bits,
-                                                              const uint64_t n_words) {
-    // Four consecutive nodes per thread: one 16-byte load per SoA array (the
-    // arrays are padded to a multiple of 256 nodes, so every float4 is aligned;
-    // `begin` is a multiple of 1024).
-    const uint64_t i0 = begin + (uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x) * 4;
-    unsigned cnib = 0, qnib = 0;
+// Certified FP32 qpass pre-test for a visible internal node with z_ok
+// certain: 1 if the reference's radius = 3 sqrt(lambda_max) <= tau_r
+// (mark_core.hpp:90-112), 0 if not, -1 undecided (recompute in FP64).
+//
+// lambda_max - 0.3 = sigma_max(M)^2 with M = J W R_q S (2x3), so the FP32
+// route forms M directly (A = J W, then M = A R_q S) and bounds its error:
+//   |sigma(M~) - sigma(M)| <= ||M~ - M||_F <= e,
+//   e = smax * sum_i (3 dJ_i + 4 eps_R J_i),  J_i = |j_i0| + |j_i2|,
+// where dJ_i bounds the error of row i of J (camera-space coordinates off by
+// at most B, relative depth error rho = B / tz <= 2^-12) and eps_R = 2^-17
+// bounds the FP32 rotation entries (rsqrt-normalised quaternion).  The 2x2
+// Gram matrix and its closed-form top eigenvalue add at most 2^-18 (a'+c').
+// e enters with a safety factor of 4; the final interval is widened by a
+// further 2^-18 relative, far above the FP64 reference's own rounding
+// (<= 3e-8 relative, dominated by the mid^2 - det cancellation).
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// (rcp/sqrt/rsqrt below are the approximate MUFU forms, each within 2^-22
+// relative; the constants of the bound cover them.)
+__device__ __forceinline__ int qpass_fp32(const GeomF& f, const Cam32& c, float sx, float sy,
+                                          float sz, float4 q) {
+    if (!(c.tz > 0.0f) || c.B > 2.44140625e-4f * c.tz) return -1;  // rho > 2^-12
+    const float iz = rcp_approx(c.tz);
+    const float rho = c.B * iz * 1.0001f;
+    const float fxz = f.fx * iz, fyz = f.fy * iz;
+    const float j00 = fxz, j02 = -fxz * (c.tx * iz);
+    const float j11 = fyz, j12 = -fyz * (c.ty * iz);
+    const float J1 = fabsf(j00) + fabsf(j02), J2 = fabsf(j11) + fabsf(j12);
+    const float fB1 = fxz * iz * c.B, fB2 = fyz * iz * c.B;
+    const float dJ1 = fabsf(j00) * (1.02f * rho + 1e-6f) + fabsf(j02) * (2.05f * rho + 1.5e-6f) +
+                      1.02f * fB1;
+    const float dJ2 = fabsf(j11) * (1.02f * rho + 1e-6f) + fabsf(j12) * (2.05f * rho + 1.5e-6f) +
+                      1.02f * fB2;
+    // A = J W (rows 1, 2)
+    const float a0 = __fmaf_rn(j00, f.r[0], j02 * f.r[6]);
+    const float a1 = __fmaf_rn(j00, f.r[1], j02 * f.r[7]);
+    const float a2 = __fmaf_rn(j00, f.r[2], j02 * f.r[8]);
+    const float b0 = __fmaf_rn(j11, f.r[3], j12 * f.r[6]);
+    const float b1 = __fmaf_rn(j11, f.r[4], j12 * f.r[7]);
+    const float b2 = __fmaf_rn(j11, f.r[5], j12 * f.r[8]);
+    // R_q S (mark_core.hpp:44-60 rotation convention)
+    const float n2 = __fmaf_rn(q.x, q.x, __fmaf_rn(q.y, q.y, __fmaf_rn(q.z, q.z, q.w * q.w)));
+    const float inv = rsqrtf(n2);
+    const float iw = q.x * inv, ix = q.y * inv, iy = q.z * inv, izq = q.w * inv;
+    const float m00 = 1.0f - 2.0f * __fmaf_rn(iy, iy, izq * izq);
+    const float m01 = 2.0f * __fmaf_rn(ix, iy, -(iw * izq));
+    const float m02 = 2.0f * __fmaf_rn(ix, izq, iw * iy);
+    const float m10 = 2.0f * __fmaf_rn(ix, iy, iw * izq);
+    const float m11 = 1.0f - 2.0f * __fmaf_rn(ix, ix, izq * izq);
+    const float m12 = 2.0f * __fmaf_rn(iy, izq, -(iw * ix));
+    const float m20 = 2.0f * __fmaf_rn(ix, izq, -(iw * iy));
+    const float m21 = 2.0f * __fmaf_rn(iy, izq, iw * ix);
+    const float m22 = 1.0f - 2.0f * __fmaf_rn(ix, ix, iy * iy);
+    // M = A (R_q S): column j of R_q scaled by s_j
+    const float u0 = __fmaf_rn(a0, m00, __fmaf_rn(a1, m10, a2 * m20)) * sx;
+    const float u1 = __fmaf_rn(a0, m01, __fmaf_rn(a1, m11, a2 * m21)) * sy;
+    const float u2 = __fmaf_rn(a0, m02, __fmaf_rn(a1, m12, a2 * m22)) * sz;
+    const float v0 = __fmaf_rn(b0, m00, __fmaf_rn(b1, m10, b2 * m20)) * sx;
+    const float v1 = __fmaf_rn(b0, m01, __fmaf_rn(b1, m11, b2 * m21)) * sy;
+    const float v2 = __fmaf_rn(b0, m02, __fmaf_rn(b1, m12, b2 * m22)) * sz;
+    const float ga = __fmaf_rn(u0, u0, __fmaf_rn(u1, u1, u2 * u2));
+    const float gc = __fmaf_rn(v0, v0, __fmaf_rn(v1, v1, v2 * v2));
+    const float gb = __fmaf_rn(u0, v0, __fmaf_rn(u1, v1, u2 * v2));
+    const float h = 0.5f * (ga - gc);
+    const float s2 = 0.5f * (ga + gc) + sqrt_approx(__fmaf_rn(h, h, gb * gb));
+    const float gerr = 3.814697265625e-06f * (ga + gc);  // 2^-18 (a'+c')
+    const float smax = fmaxf(fmaxf(sx, sy), sz);
+    const float e = 4.0f * smax * (3.0f * (dJ1 + dJ2) + 3.0517578125e-05f * (J1 + J2));
+    const float sig_hi = sqrt_approx(s2 + gerr) * 1.000001f + e;
+    const float sig_lo = fmaxf(sqrt_approx(fmaxf(s2 - gerr, 0.0f)) * 0.999999f - e, 0.0f);
+    const float lam_hi = __fmaf_rn(sig_hi, sig_hi, 0.3f) * 1.0000039f;
+    const float lam_lo = __fmaf_rn(sig_lo, sig_lo, 0.3f) * 0.9999961f;
+    if (!(lam_hi == lam_hi)) return -1;  // NaN guard (validated inputs never get here)
+    if (lam_hi <= f.thr_pass) return 1;
+    if (lam_lo > f.thr_fail) return 0;
+    return -1;
+}
+
+// Exact reference decision for one node (FP64, mark_core.hpp:27-112);
+// `need_q`: the node is internal (its qpass matters).
+__device__ __noinline__ void mark_fp64(const Geom& g, const DevTree& t, uint64_t i, float mx,
+                                       float my, float mz, float sx, float sy, float sz,
+                                       bool need_q, double tau_r, int* vis, int* qint) {
+    double tx, ty, tz;
+    cam_transform(g, mx, my, mz, tx, ty, tz);
+    const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
+    const int vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
+    int qi = 0;
+    if (vs && need_q && tz >= g.znear) {
+        const float4 q = __ldg(t.quat + i);
+        MarkOut o;
+        ewa_cov2d(g, tx, ty, tz, sx, sy, sz, q.x, q.y, q.z, q.w, o);
+        qi = o.radius <= tau_r;
+    }
+    *vis = vs;
+    *qint = qi;
+}
+
+// Exact frustum decision for leaf i (operands loaded here, so the caller keeps
+// nothing live across this rarely taken call).
+__device__ __noinline__ bool vis_fp64(const Geom& g, const DevTree& t, uint64_t i) {
+    double tx, ty, tz;
+    const float sx = t.sx[i], sy = t.sy[i], sz = t.sz[i];
+    cam_transform(g, t.mx[i], t.my[i], t.mz[i], tx, ty, tz);
+    const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
+    return frustum_folded(g, tx, ty, tz, 3.0 * smax);
+}
+
+// F1: internal region [0, leaf_begin), two adjacent nodes per thread with
+// every load of both nodes (SoA pairs, leaf bytes, quaternions) in flight at
+// once: frustum, and for visible internal nodes the EWA radius -> cand / qint
+// words.  A warp covers 64 nodes = 2 words.
+__global__ void __launch_bounds__(kMarkBlock, 4) k_mark_internal(
+    const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
+    const double tau_r, uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ qint_bits) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t i0 = (uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x) * 2;
+    const uint64_t end = t.leaf_begin;
+    unsigned cb = 0, qb = 0;
     if (i0 < end) {
-        const float4 MX = __ldcs(reinterpret_cast<const float4*>(t.mx + i0));
-        const float4 MY = __ldcs(reinterpret_cast<const float4*>(t.my + i0));
-        const float4 MZ = __ldcs(reinterpret_cast<const float4*>(t.mz + i0));
-        const float4 SX = __ldcs(reinterpret_cast<const float4*>(t.sx + i0));
-        const float4 SY = __ldcs(reinterpret_cast<const float4*>(t.sy + i0));
-        const float4 SZ = __ldcs(reinterpret_cast<const float4*>(t.sz + i0));
-        const uint32_t LF =
-            ALL_LEAF ? 0x01010101u : __ldcs(reinterpret_cast<const unsigned int*>(t.leaf + i0));
-        const float mxa[4] = {MX.x, MX.y, MX.z, MX.w}, mya[4] = {MY.x, MY.y, MY.z, MY.w};
-        const float mza[4] = {MZ.x, MZ.y, MZ.z, MZ.w}, sxa[4] = {SX.x, SX.y, SX.z, SX.w};
-        const float sya[4] = {SY.x, SY.y, SY.z, SY.w}, sza[4] = {SZ.x, SZ.y, SZ.z, SZ.w};
+        const float2 MX = __ldcs(reinterpret_cast<const float2*>(t.mx + i0));
+        const float2 MY = __ldcs(reinterpret_cast<const float2*>(t.my + i0));
+        const float2 MZ = __ldcs(reinterpret_cast<const float2*>(t.mz + i0));
+        const float2 SX = __ldcs(reinterpret_cast<const float2*>(t.sx + i0));
+        const float2 SY = __ldcs(reinterpret_cast<const float2*>(t.sy + i0));
+        const float2 SZ = __ldcs(reinterpret_cast<const float2*>(t.sz + i0));
+        const unsigned short LF = __ldcs(reinterpret_cast<const unsigned short*>(t.leaf + i0));
+        const float4 Q0 = __ldcs(t.quat + i0), Q1 = __ldcs(t.quat + i0 + 1);
+        const float mxa[2] = {MX.x, MX.y}, mya[2] = {MY.x, MY.y}, mza[2] = {MZ.x, MZ.y};
+        const float sxa[2] = {SX.x, SX.y}, sya[2] = {SY.x, SY.y}, sza[2] = {SZ.x, SZ.y};
+        const float4 qa[2] = {Q0, Q1};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (i0 + k >= end) break;
-            const float mx = mxa[k], my = mya[k], mz = mza[k];
-            const float sx = sxa[k], sy = sya[k], sz = sza[k];
-            const bool leaf = ALL_LEAF || ((LF >> (8 * k)) & 0xffu) != 0;
-            const float smaxf = fmaxf(fmaxf(sx, sy), sz);  // scales finite and > 0 (validated)
-            float tz32;
+        for (int k = 0; k < 2; ++k) {
+            const bool leaf = ((LF >> (8 * k)) & 0xffu) != 0;
+            Cam32 c;
             int zs;
-            int vs = frustum_fp32(f, mx, my, mz, 3.0f * smaxf, tz32, zs);
-            bool qint = false;
-            if (ALL_LEAF && vs < 0) {
-                double tx, ty, tz;
-                cam_transform(g, mx, my, mz, tx, ty, tz);
-                const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
-                vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
-            } else if (!ALL_LEAF && (vs < 0 || (!leaf && vs != 0))) {
-                // exact FP64 path: undecided nodes, and every visible internal
-                // node (its qpass needs the EWA radius, which is always FP64).
-                double tx, ty, tz;
-                cam_transform(g, mx, my, mz, tx, ty, tz);
-                const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
-                vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
-                if (vs && !leaf && tz >= g.znear) {
-                    const float4 q = __ldg(t.quat + i0 + k);
-                    MarkOut o;
-                    ewa_cov2d(g, tx, ty, tz, sx, sy, sz, q.x, q.y, q.z, q.w, o);
-                    qint = o.radius <= tau_r;
-                }
+            int vs = frustum_fp32(f, mxa[k], mya[k], mza[k],
+                                  3.0f * fmaxf(fmaxf(sxa[k], sya[k]), sza[k]), c, zs);
+            int qs = 0;
+            if (vs == 1 && !leaf) {
+                if (zs == 1) qs = qpass_fp32(f, c, sxa[k], sya[k], sza[k], qa[k]);
+                else if (zs < 0) qs = -1;  // zs == 0: z_ok false, qpass false for certain
             }
-            cnib |= (vs == 1 && (leaf || qint)) ? (1u << k) : 0u;
-            qnib |= qint ? (1u << k) : 0u;
+            if (vs < 0 || qs < 0) {
+                int v, qi;
+                mark_fp64(g, t, i0 + k, mxa[k], mya[k], mza[k], sxa[k], sya[k], sza[k], !leaf,
+                          tau_r, &v, &qi);
+                vs = v;
+                qs = qi;
+            }
+            const bool qint = vs == 1 && qs == 1;
+            const bool cand = vs == 1 && (leaf || qint);
+            if (i0 + k < end) {
+                cb |= cand ? (1u << k) : 0u;
+                qb |= qint ? (1u << k) : 0u;
+            }
         }
     }
-    // A warp covers 128 nodes = 4 words; word k gathers the nibbles of lanes 8k..8k+7.
-    const unsigned lane = threadIdx.x & 31;
-    unsigned cw = cnib << (4 * (lane & 7)), qw = qnib << (4 * (lane & 7));
+    // lanes 16h..16h+15 fill word h of the warp's two
+    unsigned cw = cb << (2 * (lane & 15)), qw = qb << (2 * (lane & 15));
 #pragma unroll
-    for (int m = 1; m < 8; m <<= 1) {
+    for (int m = 1; m < 16; m <<= 1) {
         cw |= __shfl_xor_sync(0xffffffffu, cw, m);
         qw |= __shfl_xor_sync(0xffffffffu, qw, m);
     }
-    if ((lane & 7) == 0) {
-        const uint64_t w = i0 >> 5;
-        if (w < n_words) {
-            cand_bits[w] = cw;
-            qint_bits[w] = qw;
-        }
+    if ((lane & 15) == 0 && i0 < end) {
+        cand_bits[i0 >> 5] = cw;
+        qint_bits[i0 >> 5] = qw;
     }
 }
 
-// Internal levels (the FP64-heavy 1/8 of the arena): one node per thread so
-// the long covariance dependency chains of many warps overlap.
-__global__ void __launch_bounds__(kMarkBlock) k_filter_mark_internal(
-    const Geom g, const GeomF f, const DevTree t, const double tau_r, const uint64_t end,
-    uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ qint_bits, const uint64_t n_words) {
-    const uint64_t i = uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x;
-    bool cand = false, qint = false;
-    if (i < end) {
-        const float mx = __ldcs(t.mx + i), my = __ldcs(t.my + i), mz = __ldcs(t.mz + i);
-        const float sx = __ldcs(t.sx + i), sy = __ldcs(t.sy + i), sz = __ldcs(t.sz + i);
-        const bool leaf = __ldcs(t.leaf + i) != 0;
-        float tz32;
-        int zs;
-        int vs = frustum_fp32(f, mx, my, mz, 3.0f * fmaxf(fmaxf(sx, sy), sz), tz32, zs);
-        if (vs < 0 || (!leaf && vs != 0)) {
-            double tx, ty, tz;
-            cam_transform(g, mx, my, mz, tx, ty, tz);
-            const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
-            vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
-            if (vs && !leaf && tz >= g.znear) {
-                const float4 q = __ldg(t.quat + i);
-                MarkOut o;
-                ewa_cov2d(g, tx, ty, tz, sx, sy, sz, q.x, q.y, q.z, q.w, o);
-                qint = o.radius <= tau_r;
-            }
-        }
-        cand = vs == 1 && (leaf || qint);
-    }
-    const unsigned cm = __ballot_sync(0xffffffffu, cand);
-    const unsigned qm = __ballot_sync(0xffffffffu, qint);
-    if ((threadIdx.x & 31) == 0 && (i >> 5) < n_words) {
-        cand_bits[i >> 5] = cm;
-        qint_bits[i >> 5] = qm;
-    }
-}
+// Survivor counts are kept per 8192-node tile (one count per k_compact CTA).
+constexpr int kTileNodes = 8192;
 
-// K2a: candidates walk their parent chains (filter.cpp:20-25); the keep bits
-// overwrite cand_bits in place (each word is read and written by one warp).
-__global__ void __launch_bounds__(kSelectBlock) k_filter_select(
-    uint32_t* __restrict__ cand_bits, const uint32_t* __restrict__ qint_bits,
-    const uint32_t* __restrict__ parent, const uint64_t n) {
+// F2: internal region.  Every node walks its parent chain (filter.cpp:20-25)
+// against the qint bitmask (L2-resident: 1 bit per internal node); the
+// kSelectItems chains of a thread advance one level per round so their
+// dependent loads overlap.  keep = cand && !disq replaces the cand word; the
+// qint word is replaced by blk = qint | disq ("a child of this node is
+// disqualified").  Another warp may read either value of a qint word while
+// walking: for any descendant the OR along its chain is the same, so the
+// result does not depend on the interleaving.
+__global__ void __launch_bounds__(kSelectBlock) k_select_internal(
+    uint32_t* __restrict__ cand_bits, uint32_t* qint_bits, const uint32_t* __restrict__ parent,
+    const uint64_t end, uint32_t* __restrict__ tile_count) {
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t warp_base =
         uint64_t(blockIdx.x) * (kSelectBlock * kSelectItems) + uint64_t(warp) * (32 * kSelectItems);
-
-    // All kSelectItems parent chains of a thread advance one level per round,
-    // so their dependent L2 loads overlap instead of running back to back.
+    if (warp_base >= end) return;  // warp-uniform
     uint32_t a[kSelectItems];
-    bool keep[kSelectItems];
+    bool disq[kSelectItems];
 #pragma unroll
     for (int j = 0; j < kSelectItems; ++j) {
-        const uint64_t node = warp_base + uint64_t(j) * 32 + lane;
-        keep[j] = node < n && ((cand_bits[node >> 5] >> lane) & 1u);
-        a[j] = kRootParent;
+        a[j] = __ldg(parent + warp_base + uint64_t(j) * 32 + lane);
+        disq[j] = false;
     }
-#pragma unroll
-    for (int j = 0; j < kSelectItems; ++j)
-        if (keep[j]) a[j] = __ldg(parent + warp_base + uint64_t(j) * 32 + lane);
     while (true) {
         bool any = false;
 #pragma unroll
@@ -225,7 +325,7 @@ __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
 #pragma unroll
         for (int j = 0; j < kSelectItems; ++j) {
             if (a[j] != kRootParent) {
-                w[j] = __ldg(qint_bits + (a[j] >> 5));
+                w[j] = *(volatile const uint32_t*)(qint_bits + (a[j] >> 5));
                 p[j] = __ldg(parent + a[j]);
             }
         }
@@ -233,7 +333,7 @@ __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
         for (int j = 0; j < kSelectItems; ++j) {
             if (a[j] != kRootParent) {
                 if ((w[j] >> (a[j] & 31)) & 1u) {
-                    keep[j] = false;
+                    disq[j] = true;
                     a[j] = kRootParent;
                 } else {
                     a[j] = p[j];
@@ -241,74 +341,148 @@ __global__ void __launch_bounds__(kSelectBlock) k_filter_select(
             }
         }
     }
+    uint32_t mine = 0;  // lane j < kSelectItems takes word j
 #pragma unroll
     for (int j = 0; j < kSelectItems; ++j) {
-        const unsigned m = __ballot_sync(0xffffffffu, keep[j]);
-        if (lane == 0) cand_bits[(warp_base >> 5) + j] = m;
+        const uint32_t dm = __ballot_sync(0xffffffffu, disq[j]);
+        if (lane == unsigned(j)) mine = dm;
     }
+    const uint64_t wi = (warp_base >> 5) + lane;
+    unsigned cntw = 0;
+    if (lane < unsigned(kSelectItems) && wi * 32 < end) {
+        const uint32_t keep = cand_bits[wi] & ~mine;
+        cand_bits[wi] = keep;
+        if (mine) qint_bits[wi] |= mine;
+        cntw = __popc(keep);
+    }
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) cntw += __shfl_xor_sync(0xffffffffu, cntw, off);
+    if (lane == 0 && cntw) atomicAdd(tile_count + warp_base / kTileNodes, cntw);
 }
 
-// K2b: ordered compaction of the keep bitmask into `selected` (strictly
-// increasing, filter.cpp:147-148).  A warp owns 128 consecutive words; for
-// each word (broadcast by shuffle) lane b tests bit b, so one ballot + popc
-// places 32 nodes with a coalesced store.  CTA totals are chained by a
-// look-back across 32,768-node tiles.
-constexpr int kCompactIters = 1;  // words per lane (small tiles: one wave of short CTAs)
-__global__ void __launch_bounds__(256) k_compact_bits(const uint32_t* __restrict__ bits,
-                                                      const uint64_t n_words,
-                                                      const uint32_t n_tiles,
-                                                      uint32_t* __restrict__ selected,
-                                                      unsigned long long* status,
-                                                      FrameCounters* cnt) {
-    __shared__ unsigned s_ticket;
-    __shared__ unsigned s_warp[8];
-    __shared__ unsigned long long s_excl;
-    const unsigned tile = take_ticket(&cnt->ticket_select, &s_ticket);
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t wbase = (uint64_t(tile) * 8 + warp) * (32 * kCompactIters);
-    uint32_t words[kCompactIters];
-    unsigned c = 0;
+// F3: the all-leaf suffix [leaf_begin, n): one streaming pass, four leaves
+// per thread, every load (one 16-byte load per SoA array and the four parent
+// indices; arrays padded to a multiple of 256 nodes, leaf_begin a multiple of
+// 1024) issued up front.  A leaf's qpass is never read (filter.cpp:23,137):
+// it is a candidate iff visible, and kept iff its parent's blk bit (F2) is
+// clear.  Writes keep words and the per-tile survivor counts.
+__global__ void __launch_bounds__(256) k_filter_leaves(
+    const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
+    const uint32_t* __restrict__ blk_bits, uint32_t* __restrict__ keep_bits,
+    uint32_t* __restrict__ tile_count) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t end = t.n;
+    const uint64_t i0 = t.leaf_begin + (uint64_t(blockIdx.x) * 256 + threadIdx.x) * 4;
+    unsigned nib = 0;
+    if (i0 < end) {
+        const float4 MX = __ldcs(reinterpret_cast<const float4*>(t.mx + i0));
+        const float4 MY = __ldcs(reinterpret_cast<const float4*>(t.my + i0));
+        const float4 MZ = __ldcs(reinterpret_cast<const float4*>(t.mz + i0));
+        const float4 SX = __ldcs(reinterpret_cast<const float4*>(t.sx + i0));
+        const float4 SY = __ldcs(reinterpret_cast<const float4*>(t.sy + i0));
+        const float4 SZ = __ldcs(reinterpret_cast<const float4*>(t.sz + i0));
+        const uint4 P = __ldcs(reinterpret_cast<const uint4*>(t.parent + i0));
+        const float mxa[4] = {MX.x, MX.y, MX.z, MX.w}, mya[4] = {MY.x, MY.y, MY.z, MY.w};
+        const float mza[4] = {MZ.x, MZ.y, MZ.z, MZ.w}, sxa[4] = {SX.x, SX.y, SX.z, SX.w};
+        const float sya[4] = {SY.x, SY.y, SY.z, SY.w}, sza[4] = {SZ.x, SZ.y, SZ.z, SZ.w};
+        unsigned undec = 0;
 #pragma unroll
-    for (int it = 0; it < kCompactIters; ++it) {
-        const uint64_t w = wbase + uint64_t(it) * 32 + lane;
-        words[it] = w < n_words ? __ldg(bits + w) : 0u;
-        c += __popc(words[it]);
+        for (int k = 0; k < 4; ++k) {
+            Cam32 c;
+            int zs;
+            const int vs = frustum_fp32(f, mxa[k], mya[k], mza[k],
+                                        3.0f * fmaxf(fmaxf(sxa[k], sya[k]), sza[k]), c, zs);
+            nib |= vs == 1 ? (1u << k) : 0u;
+            undec |= vs < 0 ? (1u << k) : 0u;
+        }
+        if (undec) {
+            // rare: within ~1e-3 world units of a frustum plane -> exact FP64
+            // decision; operands re-read so nothing stays live across the call
+            for (int k = 0; k < 4; ++k)
+                if ((undec >> k) & 1u) nib |= vis_fp64(g, t, i0 + k) ? (1u << k) : 0u;
+        }
+        if (i0 + 4 > end) nib &= (1u << unsigned(end - i0)) - 1u;  // padding past n
+        const uint32_t pa[4] = {P.x, P.y, P.z, P.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t p = pa[k];
+            if (((nib >> k) & 1u) && p != kRootParent &&
+                ((__ldg(blk_bits + (p >> 5)) >> (p & 31)) & 1u))
+                nib &= ~(1u << k);
+        }
     }
+    // a warp covers 128 leaves = 4 words; word q gathers the nibbles of lanes 8q..8q+7
+    unsigned w = nib << (4 * (lane & 7));
+#pragma unroll
+    for (int m = 1; m < 8; m <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, m);
+    if ((lane & 7) == 0 && i0 < end) keep_bits[i0 >> 5] = w;
+    unsigned c = __popc(nib);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-    if (lane == 0) s_warp[warp] = c;
-    __syncthreads();
-    if (warp == 0) {
-        const unsigned v = lane < 8 ? s_warp[lane] : 0u;
-        unsigned wi = v;
+    // a warp's 128 leaves lie in one 8192-node tile (leaf_begin is a multiple of 1024)
+    const uint64_t wbase = t.leaf_begin + (uint64_t(blockIdx.x) * 256 + (threadIdx.x & ~31u)) * 4;
+    if (lane == 0 && c) atomicAdd(tile_count + wbase / kTileNodes, c);
+}
+
+// F4: ordered compaction of the keep words into `selected` (strictly
+// increasing, filter.cpp:147-148).  One CTA per 8192-node tile; its first
+// output position is the sum of the counts of all preceding tiles (read
+// directly: no look-back chain, CTAs never wait on each other).  Warp w owns
+// 32 words; for every non-empty word (broadcast by shuffle) lane b tests bit
+// b, so one popc places 32 nodes with a coalesced store.
+__global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ keep_bits,
+                                                 const uint64_t n_words,
+                                                 const uint32_t* __restrict__ tile_count,
+                                                 uint32_t* __restrict__ selected,
+                                                 FrameCounters* cnt) {
+    __shared__ unsigned s_red[8];
+    __shared__ unsigned s_warp[8];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned tile = blockIdx.x;
+    unsigned pre = 0;
+    {
+        unsigned p4[4] = {0u, 0u, 0u, 0u};
+        unsigned k = threadIdx.x;
+        for (; k + 768 < tile; k += 1024) {
 #pragma unroll
-        for (int off = 1; off < 8; off <<= 1) {
-            const unsigned o = __shfl_up_sync(0xffffffffu, wi, off);
-            if (lane >= unsigned(off)) wi += o;
+            for (int u = 0; u < 4; ++u) p4[u] += __ldg(tile_count + k + 256 * u);
         }
-        const unsigned total = __shfl_sync(0xffffffffu, wi, 7);
-        if (lane < 8) s_warp[lane] = wi - v;
-        const unsigned long long excl = chained_scan_warp(status, tile, total);
-        if (lane == 0) {
-            s_excl = excl;
-            if (tile == n_tiles - 1) cnt->n_selected = excl + total;
-        }
+        for (; k < tile; k += 256) p4[0] += __ldg(tile_count + k);
+        pre = (p4[0] + p4[1]) + (p4[2] + p4[3]);
     }
-    __syncthreads();
-    unsigned long long pos = s_excl + s_warp[warp];
-    const unsigned lt = (1u << lane) - 1u;
+    const uint64_t wi = uint64_t(tile) * (kTileNodes / 32) + warp * 32 + lane;
+    const uint32_t keepw = wi < n_words ? __ldg(keep_bits + wi) : 0u;
+    unsigned c = __popc(keepw);
+    unsigned incl = c;
 #pragma unroll
-    for (int it = 0; it < kCompactIters; ++it) {
-        if (__ballot_sync(0xffffffffu, words[it] != 0u) == 0u) continue;
-        for (int k = 0; k < 32; ++k) {
-            const uint32_t word = __shfl_sync(0xffffffffu, words[it], k);
-            if (word == 0u) continue;  // warp-uniform
-            const bool bit = (word >> lane) & 1u;
-            if (bit)
-                selected[pos + __popc(word & lt)] =
-                    uint32_t((wbase + uint64_t(it) * 32 + k) * 32 + lane);
-            pos += __popc(word);
-        }
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= unsigned(off)) incl += o;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, off);
+    if (lane == 31) s_warp[warp] = incl;
+    if (lane == 0) s_red[warp] = pre;
+    __syncthreads();
+    unsigned base = 0, before = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        base += s_red[k];
+        before += k < int(warp) ? s_warp[k] : 0u;
+        total += s_warp[k];
+    }
+    if (tile == gridDim.x - 1 && threadIdx.x == 0) cnt->n_selected = uint64_t(base) + total;
+    const unsigned long long pos = uint64_t(base) + before;
+    const unsigned lt = (1u << lane) - 1u;
+    unsigned nz = __ballot_sync(0xffffffffu, keepw != 0u);
+    const uint64_t warp_node = (uint64_t(tile) * (kTileNodes / 32) + warp * 32) * 32;
+    while (nz) {  // non-empty words only (warp-uniform)
+        const int j = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const uint32_t word = __shfl_sync(0xffffffffu, keepw, j);
+        const unsigned at = __shfl_sync(0xffffffffu, incl, j) - __popc(word);
+        if ((word >> lane) & 1u)
+            selected[pos + at + __popc(word & lt)] = uint32_t(warp_node + uint64_t(j) * 32 + lane);
     }
 }
 
@@ -325,29 +499,32 @@ __global__ void k_mark_debug(const Geom g, const DevTree t, uint64_t begin, uint
     if (radius) radius[i - begin] = o.radius;
 }
 
-void launch_filter_mark(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
-                        uint32_t* qint_bits, cudaStream_t s) {
-    if (t.n == 0) return;
-    const GeomF f = make_geomf(g);
-    const uint64_t per_cta = 4 * kMarkBlock;
-    const uint64_t split = t.leaf_begin;  // multiple of per_cta; [split, n) are all leaves
-    if (split > 0)
-        k_filter_mark_internal<<<unsigned((split + kMarkBlock - 1) / kMarkBlock), kMarkBlock, 0, s>>>(
-            g, f, t, tau_r, split, cand_bits, qint_bits, bit_words(t.n));
-    if (t.n > split)
-        k_filter_mark<true><<<unsigned((t.n - split + per_cta - 1) / per_cta), kMarkBlock, 0, s>>>(
-            g, f, t, tau_r, split, t.n, cand_bits, qint_bits, bit_words(t.n));
+uint32_t filter_status_entries(uint64_t n) {
+    return uint32_t((n + kTileNodes - 1) / kTileNodes + 1);
 }
 
-void launch_filter_select(const DevTree& t, uint32_t* cand_bits, const uint32_t* qint_bits,
-                          uint32_t* selected, unsigned long long* status, FrameCounters* cnt,
-                          cudaStream_t s) {
-    if (t.n == 0) return;
-    k_filter_select<<<select_tiles(t.n), kSelectBlock, 0, s>>>(cand_bits, qint_bits, t.parent, t.n);
-    const uint64_t n_words = bit_words(t.n);
-    const uint64_t per_tile = 8ull * 32 * kCompactIters;
-    const uint32_t tiles = uint32_t((n_words + per_tile - 1) / per_tile);
-    k_compact_bits<<<tiles, 256, 0, s>>>(cand_bits, n_words, tiles, selected, status, cnt);
+void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
+                   uint32_t* qint_bits, uint32_t* tile_count, uint32_t* selected,
+                   FrameCounters* cnt, cudaStream_t s, cudaEvent_t mid) {
+    if (t.n == 0) {
+        if (mid) cudaEventRecord(mid, s);
+        return;
+    }
+    const GeomF f = make_geomf(g, tau_r);
+    const uint64_t split = t.leaf_begin;  // [split, n) are all leaves
+    if (split > 0) {
+        k_mark_internal<<<unsigned((split + 2 * kMarkBlock - 1) / (2 * kMarkBlock)), kMarkBlock, 0,
+                          s>>>(g, f, t, tau_r, cand_bits, qint_bits);
+        const uint64_t per = uint64_t(kSelectBlock) * kSelectItems;
+        k_select_internal<<<unsigned((split + per - 1) / per), kSelectBlock, 0, s>>>(
+            cand_bits, qint_bits, t.parent, split, tile_count);
+    }
+    if (mid) cudaEventRecord(mid, s);
+    if (t.n > split)
+        k_filter_leaves<<<unsigned((t.n - split + 1023) / 1024), 256, 0, s>>>(
+            g, f, t, qint_bits, cand_bits, tile_count);
+    k_compact<<<unsigned((t.n + kTileNodes - 1) / kTileNodes), 256, 0, s>>>(
+        cand_bits, (t.n + 31) / 32, tile_count, selected, cnt);
 }
 
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,

@@ -26,23 +26,26 @@ struct DevTree {
 };
 
 // ---- filter (filter.cpp:115-150) ----
-// kernels enqueued per frame: mark (internal + leaf), select, compact,
-// preprocess, tile offsets, totals, emit, tile sort, big-tile sort, blend
+// kernels enqueued per frame: filter mark, select internal, select leaves,
+// compact, preprocess, tile offsets, totals, emit, tile sort, big-tile sort, blend
 constexpr int kLaunchesPerFrame = 11;
 constexpr int kMarkBlock = 256;
 constexpr int kSelectBlock = 256;
 constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles
-// bitmask words, rounded up to whole 2048-node select tiles
-inline uint64_t bit_words(uint64_t n) { return (n + 2047) / 2048 * 64; }
+// bitmask words, rounded up to whole 8192-node compaction tiles
+inline uint64_t bit_words(uint64_t n) { return (n + 8191) / 8192 * 256; }
 inline uint32_t select_tiles(uint64_t n) {
     return uint32_t((n + uint64_t(kSelectBlock) * kSelectItems - 1) /
                     (uint64_t(kSelectBlock) * kSelectItems));
 }
-void launch_filter_mark(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
-                        uint32_t* qint_bits, cudaStream_t s);
-void launch_filter_select(const DevTree& t, uint32_t* cand_bits, const uint32_t* qint_bits,
-                          uint32_t* selected, unsigned long long* status, FrameCounters* cnt,
-                          cudaStream_t s);
+// The whole filter, four kernels: F1 internal marks, F2 internal chain walks,
+// F3 fused leaf pass, F4 ordered compaction into `selected` (n_selected lands
+// in cnt).  `mid` (optional) is recorded between F2 and F3.  tile_count: zeroed per frame, filter_status_entries(n) words.
+void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
+                   uint32_t* qint_bits, uint32_t* tile_count, uint32_t* selected,
+                   FrameCounters* cnt, cudaStream_t s, cudaEvent_t mid = nullptr);
+// per-tile survivor counters the filter needs for an n-node tree
+uint32_t filter_status_entries(uint64_t n);
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,
                        double tau_r, uint8_t* vis, uint8_t* qpass, double* radius,
                        cudaStream_t s);

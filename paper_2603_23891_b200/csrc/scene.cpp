@@ -79,7 +79,8 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
         launch_pack_tree(soa_.p, np, extra.p, n, quat_.p, splat_.p, stream_);
         FGS_CUDA(cudaStreamSynchronize(stream_));
     }
-    parent_.alloc(n);
+    parent_.alloc(np);  // padded: the leaf filter reads parents four at a time
+    FGS_CUDA(cudaMemsetAsync(parent_.p, 0xFF, np * 4, stream_));
     leaf_.alloc(np);
     FGS_CUDA(cudaMemsetAsync(leaf_.p, 0, np, stream_));
     if (n) {
@@ -169,7 +170,7 @@ void GpuScene::ensure_resolution(int w, int h) {
     res_.tile_order.alloc(n_tiles + 1);
     res_.image.alloc(uint64_t(w) * h * 3);
     const uint64_t b_cnt = align256(sizeof(FrameCounters));
-    const uint64_t b_sel = align256(uint64_t(select_tiles(tree_.n) + 1) * 8);
+    const uint64_t b_sel = align256(uint64_t(filter_status_entries(tree_.n)) * 4);
     const uint64_t b_prep = align256((tree_.n / kPrepBlock + 2) * 8);
     const uint64_t b_tiles = align256((n_tiles + 1) * 4);
     zero_bytes_ = b_cnt + b_sel + b_prep + b_tiles;
@@ -210,10 +211,9 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     clear_frame_state();
     if (timing) FGS_CUDA(cudaEventRecord(ev_[0], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[0], stream_));
-    launch_filter_mark(g, tree_, p.tau_r, cand_bits_.p, qint_bits_.p, stream_);
-    if (pe) FGS_CUDA(cudaEventRecord(pe[1], stream_));
-    launch_filter_select(tree_, cand_bits_.p, qint_bits_.p, selected_.p, d_status_select_,
-                         d_counters_, stream_);
+    launch_filter(g, tree_, p.tau_r, cand_bits_.p, qint_bits_.p,
+                  reinterpret_cast<uint32_t*>(d_status_select_), selected_.p, d_counters_,
+                  stream_, pe ? pe[1] : nullptr);
     if (timing) FGS_CUDA(cudaEventRecord(ev_[1], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[2], stream_));
     PrepOut out{g64_.p, g32_.p, emit_.p, exact ? col64_.p : nullptr, d_tile_count_};
@@ -402,9 +402,9 @@ uint64_t GpuScene::filter(const lodgs_camera& cam, double tau_r, std::vector<uin
     ensure_resolution(int(cam.width), int(cam.height));
     const Geom g = camera_geom(cam);
     clear_frame_state();
-    launch_filter_mark(g, tree_, tau_r, cand_bits_.p, qint_bits_.p, stream_);
-    launch_filter_select(tree_, cand_bits_.p, qint_bits_.p, selected_.p, d_status_select_,
-                         d_counters_, stream_);
+    launch_filter(g, tree_, tau_r, cand_bits_.p, qint_bits_.p,
+                  reinterpret_cast<uint32_t*>(d_status_select_), selected_.p, d_counters_,
+                  stream_);
     FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
                              cudaMemcpyDeviceToHost, stream_));
     FGS_CUDA(cudaStreamSynchronize(stream_));

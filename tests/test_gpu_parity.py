@@ -155,6 +155,46 @@ def test_filter_10m_tree_bit_exact(L, oracle, gpu):
             assert np.array_equal(got, want), alt
 
 
+def test_filter_mid_trees_leaf_suffix(L, oracle, gpu):
+    """Trees large enough that the all-leaf suffix (the fused leaf pass F3)
+    starts inside the arena with a ragged last tile, random orbit cameras and
+    tau_r: selected lists bit-exact."""
+    rng = oracle.rng(77)
+    for rep, (nx, depth, k) in enumerate(((6, 3, 8), (9, 3, 8), (5, 4, 6), (13, 3, 8),
+                                          (7, 2, 8), (4, 5, 4))):
+        tree = L.make_tree(500 + rep, depth, k, 0.5, nx, nx)
+        with L.GpuScene(tree) as s:
+            for _ in range(6):
+                cam = oracle.orbit_camera(rng, 640, 480, oracle.uniform(rng, 3.0, 120.0))
+                tau_r = oracle.uniform(rng, 0.5, 40.0)
+                want, _, _ = oracle.filter(tree, cam, tau_r)
+                got = s.filter(cam, L.FilterConfig(tau_r)).selected
+                assert np.array_equal(got, want), (rep, tree.node_count(), tau_r)
+
+
+def test_filter_qpass_threshold_stress(L, oracle, gpu):
+    """The FP32-certified qpass pre-test must defer to FP64 whenever a radius
+    sits at tau_r: tau_r is set to the exact FP64 radius of visible internal
+    nodes and to its neighbouring doubles, selected lists bit-exact."""
+    tree = L.build_synthetic_tree(nx=41, ny=42, seed=1, depth=3, build_seed=7)
+    n = tree.node_count()
+    n_int = int(tree.level_offsets[-1])
+    rng = np.random.default_rng(5)
+    with L.GpuScene(tree) as s:
+        for alt in (50.0, 120.0):
+            cam = topdown_camera(1920, 1080, 1000.0, alt)
+            vis, _, rad = oracle.mark(tree, cam, 1e300)
+            cand = np.flatnonzero(vis[:n_int].astype(bool) & np.isfinite(rad[:n_int]))
+            picks = rng.choice(cand, size=min(12, cand.size), replace=False)
+            for i in picks:
+                r = float(rad[i])
+                for tau_r in (r, math.nextafter(r, 0.0), math.nextafter(r, math.inf)):
+                    want, _, _ = oracle.filter(tree, cam, tau_r)
+                    got = s.filter(cam, L.FilterConfig(tau_r)).selected
+                    assert np.array_equal(got, want), (alt, int(i), tau_r)
+    assert n > n_int
+
+
 # ------------------------------------------------------------ preprocess --
 def test_prepare_bit_exact(L, oracle, gpu):
     """prepare_gaussians (rasterizer.cpp:48-73): every BlendList field

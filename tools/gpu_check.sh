@@ -15,5 +15,10 @@ tail -c 3000 $OUT/bench.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 400 --csv \
    --log-file $OUT/launches.csv python bench.py --steps 60 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1; echo "ncu launches exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-   -k regex:'k_filter|k_compact|k_blend_fast|k_tile_sort|k_preprocess|k_emit' -s 30 -c 8 \
-   -o $OUT/prof python tools/profile_frames.py --alt 200 --frames 6 > $OUT/ncu_full.log 2>&1; echo "ncu full exit $?"
+   -k regex:'k_filter_mark|k_select_internal|k_select_leaves|k_compact' -s 12 -c 4 \
+   -o $OUT/prof_filter python tools/profile_frames.py --alt 200 --frames 5 > $OUT/ncu_filter.log 2>&1; echo "ncu filter exit $?"
+if [ "${3:-}" != "filter-only" ]; then
+timeout 900 ncu --set full --clock-control none --import-source on \
+   -k regex:'k_blend_fast|k_tile_sort|k_preprocess|k_emit|k_tile_offsets' -s 15 -c 6 \
+   -o $OUT/prof_render python tools/profile_frames.py --alt 200 --frames 5 > $OUT/ncu_render.log 2>&1; echo "ncu render exit $?"
+fi
