@@ -202,7 +202,8 @@ def run_b200(args, rank, world, local):
 
     # size the pair buffer on the whole path once (untimed)
     for cam in cams[:: max(1, n_path // 30)]:
-        scene.render(cam, L.FilterConfig(TAU_R), L.ShrinkMode.three_sigma())
+        launches_per_frame = scene.render(cam, L.FilterConfig(TAU_R),
+                                          L.ShrinkMode.three_sigma()).stats.kernel_launches
 
     def device_loop(frames, profile=False):
         scene.take_totals()
@@ -305,7 +306,8 @@ def run_b200(args, rank, world, local):
                    "filter streams 0.3 GB per frame)", "parallelism": f"view-sharded x{world}"},
         "mean_selected": mean_sel, "mean_pairs": mean_pairs,
         "stage_ms_per_frame": per_stage,
-        "roofline": {"kernel": "filter (mark+select)", "bound": "hbm",
+        "roofline": {"kernel": "filter (k_mark_internal + k_select_internal + "
+                                "k_filter_leaves + k_compact)", "bound": "hbm",
                      "achieved": filt_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": filt_gbs / peak, "traffic": None,
                      "algorithmic_bytes_per_frame": filt_bytes,
@@ -316,7 +318,7 @@ def run_b200(args, rank, world, local):
                 "h2d_bytes_per_step": C.sizeof(L.CameraC) + C.sizeof(L.RenderParamsC),
                 "d2h_bytes_per_step": img_bytes + 64, "frames": len(e2e_frames),
                 "call": "lodgs_gpu_render" if args.e2e_sync else "lodgs_gpu_render_batch"},
-        "gpu_launches": 11 * K,
+        "gpu_launches": int(launches_per_frame) * K,
         "clocks": clocks.summary(),
         "setup_s": build_s,
     }

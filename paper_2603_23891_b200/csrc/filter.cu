@@ -24,6 +24,7 @@
 // All decisions are the reference's FP64 decisions (mark_core.hpp:24-116,
 // bit-exact).  They are reached in FP32 with certified error bounds, and only
 // the nodes whose FP32 value falls inside the bound recompute in FP64.
+#include <algorithm>
 #include <cmath>
 
 #include "launch.h"
@@ -42,9 +43,12 @@ struct GeomF {
     // qpass thresholds on lambda_max: radius = 3 sqrt(lambda) <= tau_r is
     // certain below thr_pass and impossible above thr_fail
     float thr_pass, thr_fail;
+    // 4 B_max, B_max = 2^-20 (max_i |m_i|_1 + c0) over the whole tree: the
+    // leaf pre-test's error term without per-node magnitude arithmetic
+    float e0;
 };
 
-GeomF make_geomf(const Geom& g, double tau_r) {
+GeomF make_geomf(const Geom& g, double tau_r, double max_l1) {
     GeomF f;
     for (int i = 0; i < 9; ++i) f.r[i] = float(g.rot[i]);
     double c0 = 0.0;
@@ -74,6 +78,8 @@ GeomF make_geomf(const Geom& g, double tau_r) {
     if (double(ff) < lf) ff = nextafterf(ff, INFINITY);
     f.thr_pass = std::isfinite(lp) ? fp : 0.0f;  // tau_r huge: no FP32 pass decision
     f.thr_fail = std::isfinite(lf) ? ff : INFINITY;
+    // rounded up: f.c0 is already >= its double value + 1 - ulp; 2^-18 slack
+    f.e0 = float(4.0 * 0x1p-20 * (max_l1 + double(f.c0)) * (1.0 + 0x1p-18));
     return f;
 }
 
@@ -108,6 +114,28 @@ __device__ __forceinline__ int frustum_fp32(const GeomF& f, float mx, float my, 
     c.ty = ty;
     c.tz = tz;
     c.B = B;
+    return m > E ? 1 : (m < -E ? 0 : -1);
+}
+
+// Leaf variant of the frustum pre-test: only vis (a leaf's z_ok and qpass are
+// never read), and the magnitude term B replaced by the tree-wide bound
+// B_max, so per node: transform, six plane distances, one min, and
+// min_p d_p + r3 against +-(4 B_max + 2^-22 r3).  A larger B only widens the
+// undecided band; decided nodes keep the reference decision.
+__device__ __forceinline__ int frustum_leaf_fp32(const GeomF& f, float mx, float my, float mz,
+                                                 float smax) {
+    const float tx = __fmaf_rn(f.r[0], mx, __fmaf_rn(f.r[1], my, __fmaf_rn(f.r[2], mz, f.t[0])));
+    const float ty = __fmaf_rn(f.r[3], mx, __fmaf_rn(f.r[4], my, __fmaf_rn(f.r[5], mz, f.t[1])));
+    const float tz = __fmaf_rn(f.r[6], mx, __fmaf_rn(f.r[7], my, __fmaf_rn(f.r[8], mz, f.t[2])));
+    const float r3 = 3.0f * smax;
+    const float E = __fmaf_rn(2.384185791015625e-07f, r3, f.e0);
+    const float dn = tz - f.znear;
+    const float df = f.zfar - tz;
+    const float dl = __fmaf_rn(f.p2x, tx, f.p2z * tz);
+    const float dr = __fmaf_rn(f.p3x, tx, f.p3z * tz);
+    const float dt = __fmaf_rn(f.p4y, ty, f.p4z * tz);
+    const float db = __fmaf_rn(f.p5y, ty, f.p5z * tz);
+    const float m = fminf(fminf(fminf(dn, df), fminf(dl, dr)), fminf(dt, db)) + r3;
     return m > E ? 1 : (m < -E ? 0 : -1);
 }
 
@@ -209,7 +237,7 @@ __device__ __noinline__ void mark_fp64(const Geom& g, const DevTree& t, uint64_t
     const int vs = frustum_folded(g, tx, ty, tz, 3.0 * smax) ? 1 : 0;
     int qi = 0;
     if (vs && need_q && tz >= g.znear) {
-        const float4 q = __ldg(t.quat + i);
+        const float4 q = __ldg(t.iquat + i);
         MarkOut o;
         ewa_cov2d(g, tx, ty, tz, sx, sy, sz, q.x, q.y, q.z, q.w, o);
         qi = o.radius <= tau_r;
@@ -222,72 +250,65 @@ __device__ __noinline__ void mark_fp64(const Geom& g, const DevTree& t, uint64_t
 // nothing live across this rarely taken call).
 __device__ __noinline__ bool vis_fp64(const Geom& g, const DevTree& t, uint64_t i) {
     double tx, ty, tz;
-    const float sx = t.sx[i], sy = t.sy[i], sz = t.sz[i];
-    cam_transform(g, t.mx[i], t.my[i], t.mz[i], tx, ty, tz);
-    const double smax = std_max(std_max(double(sx), double(sy)), double(sz));
-    return frustum_folded(g, tx, ty, tz, 3.0 * smax);
+    const float4 a = t.geo[i];
+    cam_transform(g, a.x, a.y, a.z, tx, ty, tz);
+    return frustum_folded(g, tx, ty, tz, 3.0 * double(a.w));
 }
 
-// F1: internal region [0, leaf_begin), two adjacent nodes per thread with
-// every load of both nodes (SoA pairs, leaf bytes, quaternions) in flight at
-// once: frustum, and for visible internal nodes the EWA radius -> cand / qint
-// words.  A warp covers 64 nodes = 2 words.
-__global__ void __launch_bounds__(kMarkBlock, 4) k_mark_internal(
+// F1: internal region [0, leaf_begin).  Persistent grid; each warp walks
+// 32-node groups (one node per lane) and issues the three 16-byte records of
+// its next group (mean + max scale, scales + leaf flag, quaternion) before
+// evaluating the current one, so loads overlap the FP32 EWA arithmetic:
+// frustum, and for visible internal nodes the radius -> cand / qint words by
+// ballot.
+__global__ void __launch_bounds__(kMarkBlock, 3) k_mark_internal(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const double tau_r, uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ qint_bits) {
     const unsigned lane = threadIdx.x & 31;
-    const uint64_t i0 = (uint64_t(blockIdx.x) * kMarkBlock + threadIdx.x) * 2;
     const uint64_t end = t.leaf_begin;
-    unsigned cb = 0, qb = 0;
-    if (i0 < end) {
-        const float2 MX = __ldcs(reinterpret_cast<const float2*>(t.mx + i0));
-        const float2 MY = __ldcs(reinterpret_cast<const float2*>(t.my + i0));
-        const float2 MZ = __ldcs(reinterpret_cast<const float2*>(t.mz + i0));
-        const float2 SX = __ldcs(reinterpret_cast<const float2*>(t.sx + i0));
-        const float2 SY = __ldcs(reinterpret_cast<const float2*>(t.sy + i0));
-        const float2 SZ = __ldcs(reinterpret_cast<const float2*>(t.sz + i0));
-        const unsigned short LF = __ldcs(reinterpret_cast<const unsigned short*>(t.leaf + i0));
-        const float4 Q0 = __ldcs(t.quat + i0), Q1 = __ldcs(t.quat + i0 + 1);
-        const float mxa[2] = {MX.x, MX.y}, mya[2] = {MY.x, MY.y}, mza[2] = {MZ.x, MZ.y};
-        const float sxa[2] = {SX.x, SX.y}, sya[2] = {SY.x, SY.y}, sza[2] = {SZ.x, SZ.y};
-        const float4 qa[2] = {Q0, Q1};
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const bool leaf = ((LF >> (8 * k)) & 0xffu) != 0;
+    const uint64_t n_groups = (end + 31) / 32;
+    const uint64_t stride = uint64_t(gridDim.x) * (kMarkBlock / 32);
+    uint64_t grp = uint64_t(blockIdx.x) * (kMarkBlock / 32) + (threadIdx.x >> 5);
+    float4 a, sc, q;
+    auto load = [&](uint64_t gi) {
+        const uint64_t i = gi * 32 + lane;
+        if (gi < n_groups && i < end) {
+            a = __ldcs(t.geo + i);
+            sc = __ldcs(t.iscale + i);
+            q = __ldcs(t.iquat + i);
+        }
+    };
+    load(grp);
+    for (; grp < n_groups; grp += stride) {
+        const uint64_t i = grp * 32 + lane;
+        const float4 ca = a, csc = sc, cq = q;
+        load(grp + stride);
+        bool cand = false, qint = false;
+        if (i < end) {
+            const bool leaf = csc.w != 0.0f;
             Cam32 c;
             int zs;
-            int vs = frustum_fp32(f, mxa[k], mya[k], mza[k],
-                                  3.0f * fmaxf(fmaxf(sxa[k], sya[k]), sza[k]), c, zs);
+            int vs = frustum_fp32(f, ca.x, ca.y, ca.z, 3.0f * ca.w, c, zs);
             int qs = 0;
             if (vs == 1 && !leaf) {
-                if (zs == 1) qs = qpass_fp32(f, c, sxa[k], sya[k], sza[k], qa[k]);
+                if (zs == 1) qs = qpass_fp32(f, c, csc.x, csc.y, csc.z, cq);
                 else if (zs < 0) qs = -1;  // zs == 0: z_ok false, qpass false for certain
             }
             if (vs < 0 || qs < 0) {
                 int v, qi;
-                mark_fp64(g, t, i0 + k, mxa[k], mya[k], mza[k], sxa[k], sya[k], sza[k], !leaf,
-                          tau_r, &v, &qi);
+                mark_fp64(g, t, i, ca.x, ca.y, ca.z, csc.x, csc.y, csc.z, !leaf, tau_r, &v, &qi);
                 vs = v;
                 qs = qi;
             }
-            const bool qint = vs == 1 && qs == 1;
-            const bool cand = vs == 1 && (leaf || qint);
-            if (i0 + k < end) {
-                cb |= cand ? (1u << k) : 0u;
-                qb |= qint ? (1u << k) : 0u;
-            }
+            qint = vs == 1 && qs == 1;
+            cand = vs == 1 && (leaf || qint);
         }
-    }
-    // lanes 16h..16h+15 fill word h of the warp's two
-    unsigned cw = cb << (2 * (lane & 15)), qw = qb << (2 * (lane & 15));
-#pragma unroll
-    for (int m = 1; m < 16; m <<= 1) {
-        cw |= __shfl_xor_sync(0xffffffffu, cw, m);
-        qw |= __shfl_xor_sync(0xffffffffu, qw, m);
-    }
-    if ((lane & 15) == 0 && i0 < end) {
-        cand_bits[i0 >> 5] = cw;
-        qint_bits[i0 >> 5] = qw;
+        const unsigned cm = __ballot_sync(0xffffffffu, cand);
+        const unsigned qm = __ballot_sync(0xffffffffu, qint);
+        if (lane == 0) {
+            cand_bits[grp] = cm;
+            qint_bits[grp] = qm;
+        }
     }
 }
 
@@ -360,67 +381,62 @@ __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
     if (lane == 0 && cntw) atomicAdd(tile_count + warp_base / kTileNodes, cntw);
 }
 
-// F3: the all-leaf suffix [leaf_begin, n): one streaming pass, four leaves
-// per thread, every load (one 16-byte load per SoA array and the four parent
-// indices; arrays padded to a multiple of 256 nodes, leaf_begin a multiple of
-// 1024) issued up front.  A leaf's qpass is never read (filter.cpp:23,137):
-// it is a candidate iff visible, and kept iff its parent's blk bit (F2) is
-// clear.  Writes keep words and the per-tile survivor counts.
+// F3: the all-leaf suffix [leaf_begin, n).  A leaf is kept iff visible
+// (filter.cpp:137; a leaf's qpass is never read) and no ancestor is
+// disqualifying, i.e. its parent's blk bit (F2) is clear.  The blk test comes
+// first: it needs only the parent index, and a leaf under a blocked parent is
+// dropped whatever its frustum test says, so its 16-byte geo record is never
+// fetched (siblings are contiguous, so whole sectors are skipped).  Warp =
+// 128 consecutive leaves, lane l taking leaves l, l+32, l+64, l+96: every
+// parent load is one contiguous 128 B warp access (arrays padded to a
+// multiple of 256 nodes; leaf_begin a multiple of 1024).  Writes keep words
+// (one ballot each) and the per-tile survivor counts.
 __global__ void __launch_bounds__(256) k_filter_leaves(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const uint32_t* __restrict__ blk_bits, uint32_t* __restrict__ keep_bits,
     uint32_t* __restrict__ tile_count) {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t end = t.n;
-    const uint64_t i0 = t.leaf_begin + (uint64_t(blockIdx.x) * 256 + threadIdx.x) * 4;
-    unsigned nib = 0;
-    if (i0 < end) {
-        const float4 MX = __ldcs(reinterpret_cast<const float4*>(t.mx + i0));
-        const float4 MY = __ldcs(reinterpret_cast<const float4*>(t.my + i0));
-        const float4 MZ = __ldcs(reinterpret_cast<const float4*>(t.mz + i0));
-        const float4 SX = __ldcs(reinterpret_cast<const float4*>(t.sx + i0));
-        const float4 SY = __ldcs(reinterpret_cast<const float4*>(t.sy + i0));
-        const float4 SZ = __ldcs(reinterpret_cast<const float4*>(t.sz + i0));
-        const uint4 P = __ldcs(reinterpret_cast<const uint4*>(t.parent + i0));
-        const float mxa[4] = {MX.x, MX.y, MX.z, MX.w}, mya[4] = {MY.x, MY.y, MY.z, MY.w};
-        const float mza[4] = {MZ.x, MZ.y, MZ.z, MZ.w}, sxa[4] = {SX.x, SX.y, SX.z, SX.w};
-        const float sya[4] = {SY.x, SY.y, SY.z, SY.w}, sza[4] = {SZ.x, SZ.y, SZ.z, SZ.w};
-        unsigned undec = 0;
+    const uint64_t wbase = t.leaf_begin + (uint64_t(blockIdx.x) * 256 + (threadIdx.x & ~31u)) * 4;
+    if (wbase >= end) return;  // warp-uniform
+    uint32_t p[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            Cam32 c;
-            int zs;
-            const int vs = frustum_fp32(f, mxa[k], mya[k], mza[k],
-                                        3.0f * fmaxf(fmaxf(sxa[k], sya[k]), sza[k]), c, zs);
-            nib |= vs == 1 ? (1u << k) : 0u;
+    for (int k = 0; k < 4; ++k) p[k] = __ldcs(t.parent + wbase + k * 32 + lane);
+    unsigned need = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const bool in = wbase + k * 32 + lane < end;  // padding past n never survives
+        const bool blocked =
+            p[k] != kRootParent && ((__ldg(blk_bits + (p[k] >> 5)) >> (p[k] & 31)) & 1u);
+        need |= (in && !blocked) ? (1u << k) : 0u;
+    }
+    float4 a[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if ((need >> k) & 1u) a[k] = __ldcs(t.geo + wbase + k * 32 + lane);
+    unsigned keep = 0, undec = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if ((need >> k) & 1u) {
+            const int vs = frustum_leaf_fp32(f, a[k].x, a[k].y, a[k].z, a[k].w);
+            keep |= vs == 1 ? (1u << k) : 0u;
             undec |= vs < 0 ? (1u << k) : 0u;
         }
-        if (undec) {
-            // rare: within ~1e-3 world units of a frustum plane -> exact FP64
-            // decision; operands re-read so nothing stays live across the call
-            for (int k = 0; k < 4; ++k)
-                if ((undec >> k) & 1u) nib |= vis_fp64(g, t, i0 + k) ? (1u << k) : 0u;
-        }
-        if (i0 + 4 > end) nib &= (1u << unsigned(end - i0)) - 1u;  // padding past n
-        const uint32_t pa[4] = {P.x, P.y, P.z, P.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t p = pa[k];
-            if (((nib >> k) & 1u) && p != kRootParent &&
-                ((__ldg(blk_bits + (p >> 5)) >> (p & 31)) & 1u))
-                nib &= ~(1u << k);
-        }
     }
-    // a warp covers 128 leaves = 4 words; word q gathers the nibbles of lanes 8q..8q+7
-    unsigned w = nib << (4 * (lane & 7));
+    if (undec) {
+        // rare: within ~1e-3 world units of a frustum plane -> exact FP64
+        // decision; operands re-read so nothing stays live across the call
+        for (int k = 0; k < 4; ++k)
+            if ((undec >> k) & 1u) keep |= vis_fp64(g, t, wbase + k * 32 + lane) ? (1u << k) : 0u;
+    }
+    unsigned c = 0;
 #pragma unroll
-    for (int m = 1; m < 8; m <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, m);
-    if ((lane & 7) == 0 && i0 < end) keep_bits[i0 >> 5] = w;
-    unsigned c = __popc(nib);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t w = __ballot_sync(0xffffffffu, (keep >> k) & 1u);
+        if (lane == unsigned(k) && (wbase + k * 32) < end) keep_bits[(wbase >> 5) + k] = w;
+        c += __popc(w);
+    }
     // a warp's 128 leaves lie in one 8192-node tile (leaf_begin is a multiple of 1024)
-    const uint64_t wbase = t.leaf_begin + (uint64_t(blockIdx.x) * 256 + (threadIdx.x & ~31u)) * 4;
     if (lane == 0 && c) atomicAdd(tile_count + wbase / kTileNodes, c);
 }
 
@@ -491,12 +507,26 @@ __global__ void k_mark_debug(const Geom g, const DevTree t, uint64_t begin, uint
                              double tau_r, uint8_t* vis, uint8_t* qpass, double* radius) {
     const uint64_t i = begin + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= end) return;
-    const float4 q = t.quat[i];
+    const SplatRec r = t.splat[i];
     const MarkOut o =
-        mark_core(g, t.mx[i], t.my[i], t.mz[i], t.sx[i], t.sy[i], t.sz[i], q.x, q.y, q.z, q.w, tau_r);
+        mark_core(g, r.mx, r.my, r.mz, r.sx, r.sy, r.sz, r.qw, r.qx, r.qy, r.qz, tau_r);
     vis[i - begin] = o.vis ? 1 : 0;
     qpass[i - begin] = o.qpass ? 1 : 0;
     if (radius) radius[i - begin] = o.radius;
+}
+
+// SMs of the current device (persistent grids), cached per device.
+static int sm_count() {
+    static int cache[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = v > 0 ? v : 148;
+    }
+    return cache[dev];
 }
 
 uint32_t filter_status_entries(uint64_t n) {
@@ -510,11 +540,12 @@ void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand
         if (mid) cudaEventRecord(mid, s);
         return;
     }
-    const GeomF f = make_geomf(g, tau_r);
+    const GeomF f = make_geomf(g, tau_r, t.max_l1);
     const uint64_t split = t.leaf_begin;  // [split, n) are all leaves
     if (split > 0) {
-        k_mark_internal<<<unsigned((split + 2 * kMarkBlock - 1) / (2 * kMarkBlock)), kMarkBlock, 0,
-                          s>>>(g, f, t, tau_r, cand_bits, qint_bits);
+        const uint64_t groups = (split + 31) / 32;
+        const unsigned grid = unsigned(std::min<uint64_t>((groups + 7) / 8, uint64_t(sm_count()) * 3));
+        k_mark_internal<<<grid, kMarkBlock, 0, s>>>(g, f, t, tau_r, cand_bits, qint_bits);
         const uint64_t per = uint64_t(kSelectBlock) * kSelectItems;
         k_select_internal<<<unsigned((split + per - 1) / per), kSelectBlock, 0, s>>>(
             cand_bits, qint_bits, t.parent, split, tile_count);

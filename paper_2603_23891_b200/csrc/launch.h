@@ -9,26 +9,31 @@
 
 namespace fgs {
 
-// Device copy of one LoDTree (scene.hpp:29-74), laid out for the two access
-// patterns of the frame: streaming SoA for the flat filter pass, one 64-byte
-// AoS record per node for the preprocess gather.
+// Device copy of one LoDTree (scene.hpp:29-74), laid out for the access
+// patterns of the frame.  The filter streams one 16-byte record per node
+// (mean + max scale: all a frustum test reads) and the parent index; only the
+// internal region [0, leaf_begin) -- 1/8 of a K=8 tree -- also carries the
+// scales and quaternion its EWA radius needs.  The preprocess gathers one
+// 64-byte AoS record per selected node.
 struct DevTree {
     uint64_t n = 0;
-    const float *mx = nullptr, *my = nullptr, *mz = nullptr;
-    const float *sx = nullptr, *sy = nullptr, *sz = nullptr;
-    const float4* quat = nullptr;  // (w, x, y, z)
-    const uint32_t* parent = nullptr;
-    const uint8_t* leaf = nullptr;
+    const float4* geo = nullptr;     // (mx, my, mz, max(sx, sy, sz)), padded to 256 nodes
+    const float4* iscale = nullptr;  // (sx, sy, sz, leaf ? 1 : 0) for [0, leaf_begin)
+    const float4* iquat = nullptr;   // (w, x, y, z) for [0, leaf_begin)
+    const uint32_t* parent = nullptr;  // padded to 256 nodes with kRootParent
     const SplatRec* splat = nullptr;
-    // Nodes [leaf_begin, n) are all leaves (leaf_begin a multiple of 1024):
-    // the filter's mark pass skips the covariance code path there.
+    // Nodes [leaf_begin, n) are all leaves (leaf_begin a multiple of 1024, or n).
     uint64_t leaf_begin = 0;
+    // max_i (|mx| + |my| + |mz|) over the tree (rounded up): the FP32 leaf
+    // frustum pre-test's magnitude bound
+    double max_l1 = 0.0;
 };
 
 // ---- filter (filter.cpp:115-150) ----
-// kernels enqueued per frame: filter mark, select internal, select leaves,
-// compact, preprocess, tile offsets, totals, emit, tile sort, big-tile sort, blend
-constexpr int kLaunchesPerFrame = 11;
+// kernels enqueued per frame: mark internal, select internal, filter leaves,
+// compact, preprocess, tile offsets (+ run totals), emit, tile sort, big-tile
+// sort, blend
+constexpr int kLaunchesPerFrame = 10;
 constexpr int kMarkBlock = 256;
 constexpr int kSelectBlock = 256;
 constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles
@@ -67,9 +72,11 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
 // Turns the per-tile counts into offsets[n_tiles+1] and per-tile write cursors,
 // lists the tiles whose segment exceeds the in-shared-memory sort capacity, and
 // writes order[n_tiles]: tiles heaviest-first (log2 buckets) for the per-tile grids.
+// With `totals`, also accumulates the per-run frame/selected/pair totals.
 void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
                          uint32_t* cursor, uint32_t* big_list, uint32_t* order,
-                         FrameCounters* cnt, uint64_t pair_cap, cudaStream_t s);
+                         FrameCounters* cnt, uint64_t pair_cap, cudaStream_t s,
+                         RunTotals* totals = nullptr);
 // Key duplication: one key per (gaussian, overlapped tile) scattered into the
 // tile's bucket; key = depth_bits << 32 | gaussian.
 void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x, int n_tiles,

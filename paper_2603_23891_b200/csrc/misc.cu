@@ -4,20 +4,21 @@
 
 namespace fgs {
 
-// SoA upload -> float4 quaternions (filter) + 64-byte splat records
-// (preprocess gather).  soa = [mx|my|mz|sx|sy|sz], extra = [qw|qx|qy|qz|op|cr|cg|cb].
-__global__ void k_pack_tree(const float* __restrict__ soa, uint64_t stride,
-                            const float* __restrict__ ex, uint64_t n, float4* quat,
-                            SplatRec* splat) {
+// SoA upload -> the device layout (launch.h DevTree): geo records for every
+// node, scale/quaternion records for the internal region, 64-byte splat
+// records.  soa = [mx|my|mz|sx|sy|sz] (stride n), ex = [qw|qx|qy|qz|op|cr|cg|cb].
+__global__ void k_pack_tree(const float* __restrict__ soa, const float* __restrict__ ex,
+                            const uint8_t* __restrict__ leaf, uint64_t n, uint64_t leaf_begin,
+                            float4* geo, float4* iscale, float4* iquat, SplatRec* splat) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     SplatRec r;
     r.mx = soa[i];
-    r.my = soa[stride + i];
-    r.mz = soa[2 * stride + i];
-    r.sx = soa[3 * stride + i];
-    r.sy = soa[4 * stride + i];
-    r.sz = soa[5 * stride + i];
+    r.my = soa[n + i];
+    r.mz = soa[2 * n + i];
+    r.sx = soa[3 * n + i];
+    r.sy = soa[4 * n + i];
+    r.sz = soa[5 * n + i];
     r.qw = ex[i];
     r.qx = ex[n + i];
     r.qy = ex[2 * n + i];
@@ -28,13 +29,22 @@ __global__ void k_pack_tree(const float* __restrict__ soa, uint64_t stride,
     r.cb = ex[7 * n + i];
     r.pad0 = 0.f;
     r.pad1 = 0.f;
-    quat[i] = make_float4(r.qw, r.qx, r.qy, r.qz);
     splat[i] = r;
+    // std::max(std::max(sx, sy), sz) of mark_core.hpp:33, exact in float (scales finite > 0)
+    const float smax = fmaxf(fmaxf(r.sx, r.sy), r.sz);
+    geo[i] = make_float4(r.mx, r.my, r.mz, smax);
+    if (i < leaf_begin) {
+        iscale[i] = make_float4(r.sx, r.sy, r.sz, leaf[i] ? 1.0f : 0.0f);
+        iquat[i] = make_float4(r.qw, r.qx, r.qy, r.qz);
+    }
 }
 
-void launch_pack_tree(const float* soa, uint64_t stride, const float* extra, uint64_t n,
-                      float4* quat, SplatRec* splat, cudaStream_t s) {
-    if (n) k_pack_tree<<<unsigned((n + 255) / 256), 256, 0, s>>>(soa, stride, extra, n, quat, splat);
+void launch_pack_tree(const float* soa, const float* extra, const uint8_t* leaf, uint64_t n,
+                      uint64_t leaf_begin, float4* geo, float4* iscale, float4* iquat,
+                      SplatRec* splat, cudaStream_t s) {
+    if (n)
+        k_pack_tree<<<unsigned((n + 255) / 256), 256, 0, s>>>(soa, extra, leaf, n, leaf_begin, geo,
+                                                              iscale, iquat, splat);
 }
 
 __global__ void k_update_totals(const FrameCounters* cnt, const uint32_t* offsets, int n_tiles,

@@ -254,93 +254,151 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
                                                 tiles_y, out, cnt, use_hist);
 }
 
-// One CTA: exclusive scan of per-tile counts -> offsets, write cursors, and
-// the list of tiles too large for the shared-memory sort.
-__global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restrict__ count,
+// One CTA: exclusive scan of per-tile counts -> offsets and write cursors,
+// the list of tiles too large for the shared-memory sort, the heavy-first
+// schedule for the per-tile grids, and (optionally) the running totals.
+// Thread k owns the contiguous tiles [k*per, (k+1)*per): a serial sum, one
+// block scan, a serial write-back.
+__device__ __forceinline__ int tile_class(uint32_t c, uint32_t mean) {
+    // 0: >= 4x mean pairs, 1: >= 2x, 2: >= 1x, 3: lighter
+    return c >= 4 * mean ? 0 : (c >= 2 * mean ? 1 : (c >= mean ? 2 : 3));
+}
+
+__global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restrict__ gcount,
                                                        int n_tiles, uint32_t* offsets,
                                                        uint32_t* cursor, uint32_t* big_list,
                                                        uint32_t* order, FrameCounters* cnt,
-                                                       uint64_t pair_cap) {
-    __shared__ uint32_t s_warp[32];
-    __shared__ uint64_t s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
+                                                       uint64_t pair_cap, RunTotals* totals,
+                                                       int staged) {
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint32_t s_cls[4][32];  // per (class, warp): tiles, then first order slot
+    extern __shared__ uint32_t s_count[];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int base = 0; base < n_tiles; base += 1024) {
-        const int t = base + threadIdx.x;
-        const uint32_t c = t < n_tiles ? count[t] : 0u;
-        uint32_t incl = c;
+    // stage the counts with independent coalesced loads (the serial per-thread
+    // passes below would otherwise pay one L2 round trip per tile)
+    const uint32_t* count = gcount;
+    if (staged) {
+#pragma unroll 8
+        for (int t = threadIdx.x; t < n_tiles; t += 1024) s_count[t] = __ldg(gcount + t);
+        __syncthreads();
+        count = s_count;
+    }
+    const int per = (n_tiles + 1023) / 1024;
+    const int t0 = min(n_tiles, int(threadIdx.x) * per), t1 = min(n_tiles, t0 + per);
+    uint64_t sum = 0;
+    for (int t = t0; t < t1; ++t) sum += count[t];
+    uint64_t incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= unsigned(off)) incl += o;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t v = s_warp[lane];
+        uint64_t wi = v;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= unsigned(off)) incl += o;
+            const uint64_t o = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= unsigned(off)) wi += o;
         }
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t v = s_warp[lane];
-            uint32_t wi = v;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, wi, off);
-                if (lane >= unsigned(off)) wi += o;
-            }
-            s_warp[lane] = wi - v;
-        }
-        __syncthreads();
-        const uint64_t excl = s_carry + s_warp[warp] + (incl - c);
-        if (t < n_tiles) {
-            offsets[t] = uint32_t(excl);
-            cursor[t] = uint32_t(excl);
-            if (c > uint32_t(kSmallSortCap)) big_list[atomicAdd(&cnt->big_tiles, 1u)] = uint32_t(t);
-        }
-        __syncthreads();
-        if (threadIdx.x == 1023) s_carry = excl + c;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        offsets[n_tiles] = uint32_t(s_carry);
-        if (s_carry > pair_cap) cnt->overflow = 1u;
+        s_warp[lane] = wi;  // inclusive warp prefix
     }
     __syncthreads();
+    const uint64_t total = s_warp[31];
     // Overflow: every bucket becomes empty so sort/blend never touch the
     // unwritten keys; the host grows the buffer and re-renders.
-    if (s_carry > pair_cap) {
-        for (int t = threadIdx.x; t <= n_tiles; t += blockDim.x) offsets[t] = 0u;
-        if (threadIdx.x == 0) cnt->big_tiles = 0u;
-    }
-    // Longest-first schedule for the per-tile kernels (sort, blend): tiles
-    // counting-sorted by descending floor(log2(pairs)), so the heaviest CTAs
-    // start first and the tail of the grid is made of cheap ones.
-    __shared__ uint32_t s_bkt[34];
-    if (threadIdx.x < 34) s_bkt[threadIdx.x] = 0u;
-    __syncthreads();
-    const bool ovf = s_carry > pair_cap;
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const bool ovf = total > pair_cap;
+    uint64_t run = (warp ? s_warp[warp - 1] : 0ull) + (incl - sum);
+    for (int t = t0; t < t1; ++t) {
         const uint32_t c = ovf ? 0u : count[t];
-        atomicAdd(&s_bkt[c ? 32 - __clz(c) : 0], 1u);
+        const uint32_t o = ovf ? 0u : uint32_t(run);
+        offsets[t] = o;
+        cursor[t] = o;
+        run += c;
+        if (c > uint32_t(kSmallSortCap)) big_list[atomicAdd(&cnt->big_tiles, 1u)] = uint32_t(t);
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int k = 33; k >= 0; --k) {
-            const uint32_t c = s_bkt[k];
-            s_bkt[k] = run;
-            run += c;
+        offsets[n_tiles] = ovf ? 0u : uint32_t(total);
+        if (ovf) cnt->overflow = 1u;
+        if (totals) {
+            totals->frames += 1;
+            totals->sum_selected += cnt->n_selected;
+            totals->sum_pairs += ovf ? 0ull : total;
+            if (ovf) totals->pad = 1;
         }
     }
+    // Heavy-first schedule for the per-tile kernels (sort, blend): a stable
+    // partition of the tiles into four classes by pair count relative to the
+    // mean, heaviest class first, so the longest CTAs start first and the
+    // tail of the grid is made of cheap ones.  Warp ballots count and rank
+    // (no atomics).  The order only schedules work; it never changes a result.
+    const uint32_t mean = uint32_t(total / uint64_t(n_tiles > 0 ? n_tiles : 1)) + 1u;
+    const int rounds = (n_tiles + 1023) / 1024;
+    unsigned my_cnt = 0;  // lane c < 4: tiles of class c seen by this warp
+    for (int k = 0; k < rounds; ++k) {
+        const int t = k * 1024 + int(threadIdx.x);
+        const int cls = t < n_tiles ? tile_class(ovf ? 0u : count[t], mean) : 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const unsigned m = __ballot_sync(0xffffffffu, cls == c);
+            if (lane == unsigned(c)) my_cnt += __popc(m);
+        }
+    }
+    if (lane < 4) s_cls[lane][warp] = my_cnt;
     __syncthreads();
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-        const uint32_t c = ovf ? 0u : count[t];
-        order[atomicAdd(&s_bkt[c ? 32 - __clz(c) : 0], 1u)] = uint32_t(t);
+    if (warp < 4) {  // warp c scans class c over the 32 warps; class offsets follow
+        const uint32_t v = s_cls[warp][lane];
+        uint32_t wi = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= unsigned(off)) wi += o;
+        }
+        s_cls[warp][lane] = wi - v;
+        if (lane == 31) s_warp[warp] = wi;  // class total (s_warp is free again)
+    }
+    __syncthreads();
+    uint32_t rank[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint32_t before = 0;
+        for (int d = 0; d < c; ++d) before += uint32_t(s_warp[d]);
+        rank[c] = before + s_cls[c][warp];
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    for (int k = 0; k < rounds; ++k) {
+        const int t = k * 1024 + int(threadIdx.x);
+        const int cls = t < n_tiles ? tile_class(ovf ? 0u : count[t], mean) : 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const unsigned m = __ballot_sync(0xffffffffu, cls == c);
+            if (cls == c) order[rank[c] + __popc(m & lt)] = uint32_t(t);
+            rank[c] += __popc(m);
+        }
     }
 }
 
 void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
                          uint32_t* cursor, uint32_t* big_list, uint32_t* order,
-                         FrameCounters* cnt, uint64_t pair_cap, cudaStream_t s) {
-    k_tile_offsets<<<1, 1024, 0, s>>>(tile_count, n_tiles, offsets, cursor, big_list, order, cnt,
-                                      pair_cap);
+                         FrameCounters* cnt, uint64_t pair_cap, cudaStream_t s,
+                         RunTotals* totals) {
+    // counts staged in shared memory up to 48K tiles (192 KB; 4K frames are 32,400)
+    const int staged = n_tiles <= 49152 ? 1 : 0;
+    const size_t smem = staged ? size_t(n_tiles) * 4 : 0;
+    if (smem > 48 * 1024) {
+        static bool attr_set[64] = {};  // function attributes are per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+            cudaFuncSetAttribute(k_tile_offsets, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 49152 * 4);
+            if (dev >= 0 && dev < 64) attr_set[dev] = true;
+        }
+    }
+    k_tile_offsets<<<1, 1024, smem, s>>>(tile_count, n_tiles, offsets, cursor, big_list, order,
+                                         cnt, pair_cap, totals, staged);
 }
 
 // Key duplication with CTA-level aggregation: each CTA counts its slice's

@@ -30,8 +30,9 @@ DeviceGuard::~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);
 }
 
-void launch_pack_tree(const float* soa, uint64_t stride, const float* extra, uint64_t n,
-                      float4* quat, SplatRec* splat, cudaStream_t s);
+void launch_pack_tree(const float* soa, const float* extra, const uint8_t* leaf, uint64_t n,
+                      uint64_t leaf_begin, float4* geo, float4* iscale, float4* iquat,
+                      SplatRec* splat, cudaStream_t s);
 void launch_update_totals(const FrameCounters* cnt, const uint32_t* offsets, int n_tiles,
                           RunTotals* totals, cudaStream_t s);
 void launch_max_tile(const uint32_t* triples, uint64_t n, unsigned int* out, cudaStream_t s);
@@ -57,52 +58,58 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
     std::memset(h_counters_, 0, sizeof(FrameCounters));
 
     const uint64_t n = tree.n_nodes;
-    // SoA stride padded to 256 nodes: every array starts 1 KB-aligned, so the
-    // mark pass can use 16-byte loads of four consecutive nodes.
+    // per-node arrays padded to 256 nodes: the filter's vector loads never run
+    // past an allocation
     const uint64_t np = (n + 255) / 256 * 256;
     tree_.n = n;
-    soa_.alloc(6 * np);
-    FGS_CUDA(cudaMemsetAsync(soa_.p, 0, soa_.bytes(), stream_));
-    const float* soa_src[6] = {tree.mean_x, tree.mean_y, tree.mean_z,
-                               tree.scale_x, tree.scale_y, tree.scale_z};
-    for (int k = 0; k < 6; ++k)
-        if (n) FGS_CUDA(cudaMemcpyAsync(soa_.p + k * np, soa_src[k], n * 4, cudaMemcpyHostToDevice, stream_));
     {
-        DevBuf<float> extra;
-        extra.alloc(8 * n);
-        const float* ex_src[8] = {tree.quat_w, tree.quat_x, tree.quat_y, tree.quat_z,
-                                  tree.opacity, tree.color_r, tree.color_g, tree.color_b};
-        for (int k = 0; k < 8; ++k)
-            if (n) FGS_CUDA(cudaMemcpyAsync(extra.p + k * n, ex_src[k], n * 4, cudaMemcpyHostToDevice, stream_));
-        quat_.alloc(n);
-        splat_.alloc(n);
-        launch_pack_tree(soa_.p, np, extra.p, n, quat_.p, splat_.p, stream_);
-        FGS_CUDA(cudaStreamSynchronize(stream_));
-    }
-    parent_.alloc(np);  // padded: the leaf filter reads parents four at a time
-    FGS_CUDA(cudaMemsetAsync(parent_.p, 0xFF, np * 4, stream_));
-    leaf_.alloc(np);
-    FGS_CUDA(cudaMemsetAsync(leaf_.p, 0, np, stream_));
-    if (n) {
-        FGS_CUDA(cudaMemcpyAsync(parent_.p, tree.parent, n * 4, cudaMemcpyHostToDevice, stream_));
-        FGS_CUDA(cudaMemcpyAsync(leaf_.p, tree.leaf, n, cudaMemcpyHostToDevice, stream_));
-    }
-    tree_.mx = soa_.p;
-    tree_.my = soa_.p + np;
-    tree_.mz = soa_.p + 2 * np;
-    tree_.sx = soa_.p + 3 * np;
-    tree_.sy = soa_.p + 4 * np;
-    tree_.sz = soa_.p + 5 * np;
-    tree_.quat = quat_.p;
-    tree_.parent = parent_.p;
-    tree_.leaf = leaf_.p;
-    tree_.splat = splat_.p;
-    {
-        // first index of the all-leaf suffix, rounded up to a 1024-node mark CTA
+        // first index of the all-leaf suffix, rounded up to 1024 nodes
         uint64_t first = n;
         while (first > 0 && tree.leaf[first - 1]) --first;
         tree_.leaf_begin = std::min<uint64_t>(n, (first + 1023) / 1024 * 1024);
     }
+    const uint64_t nb = tree_.leaf_begin;
+    {
+        double m = 0.0;
+        for (uint64_t i = 0; i < n; ++i) {
+            const double l1 = std::fabs(double(tree.mean_x[i])) + std::fabs(double(tree.mean_y[i])) +
+                              std::fabs(double(tree.mean_z[i]));
+            m = l1 > m ? l1 : m;
+        }
+        tree_.max_l1 = m * (1.0 + 0x1p-40);
+    }
+    geo_.alloc(np);
+    FGS_CUDA(cudaMemsetAsync(geo_.p, 0, geo_.bytes(), stream_));
+    iscale_.alloc(nb);
+    iquat_.alloc(nb);
+    splat_.alloc(n);
+    {
+        DevBuf<float> stage;
+        stage.alloc(14 * n);
+        DevBuf<uint8_t> leaf;
+        leaf.alloc(n);
+        const float* src[14] = {tree.mean_x, tree.mean_y, tree.mean_z, tree.scale_x,
+                                tree.scale_y, tree.scale_z, tree.quat_w, tree.quat_x,
+                                tree.quat_y, tree.quat_z, tree.opacity, tree.color_r,
+                                tree.color_g, tree.color_b};
+        if (n) {
+            for (int k = 0; k < 14; ++k)
+                FGS_CUDA(cudaMemcpyAsync(stage.p + k * n, src[k], n * 4, cudaMemcpyHostToDevice,
+                                         stream_));
+            FGS_CUDA(cudaMemcpyAsync(leaf.p, tree.leaf, n, cudaMemcpyHostToDevice, stream_));
+        }
+        launch_pack_tree(stage.p, stage.p + 6 * n, leaf.p, n, nb, geo_.p, iscale_.p, iquat_.p,
+                         splat_.p, stream_);
+        FGS_CUDA(cudaStreamSynchronize(stream_));
+    }
+    parent_.alloc(np);
+    FGS_CUDA(cudaMemsetAsync(parent_.p, 0xFF, np * 4, stream_));
+    if (n) FGS_CUDA(cudaMemcpyAsync(parent_.p, tree.parent, n * 4, cudaMemcpyHostToDevice, stream_));
+    tree_.geo = geo_.p;
+    tree_.iscale = iscale_.p;
+    tree_.iquat = iquat_.p;
+    tree_.parent = parent_.p;
+    tree_.splat = splat_.p;
 
     cand_bits_.alloc(bit_words(n));
     qint_bits_.alloc(bit_words(n));
@@ -147,7 +154,7 @@ void GpuScene::reserve_pairs(uint64_t n) {
 }
 
 uint64_t GpuScene::device_bytes() const {
-    return soa_.bytes() + quat_.bytes() + parent_.bytes() + leaf_.bytes() + splat_.bytes() +
+    return geo_.bytes() + iscale_.bytes() + iquat_.bytes() + parent_.bytes() + splat_.bytes() +
            cand_bits_.bytes() + qint_bits_.bytes() + selected_.bytes() + g64_.bytes() +
            g32_.bytes() + emit_.bytes() + col64_.bytes() + keys_.bytes() + zero_.bytes() +
            res_.tile_offsets.bytes() + res_.tile_cursor.bytes() + res_.big_list.bytes() +
@@ -220,8 +227,8 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     launch_preprocess(g, tree_, selected_.p, tree_.n, p.shrink_kind, p.tau, res_.tiles_x,
                       res_.tiles_y, out, d_counters_, persistent_grid_, stream_);
     launch_tile_offsets(d_tile_count_, n_tiles, res_.tile_offsets.p, res_.tile_cursor.p,
-                        res_.big_list.p, res_.tile_order.p, d_counters_, pair_cap_, stream_);
-    launch_update_totals(d_counters_, res_.tile_offsets.p, n_tiles, totals_.p, stream_);
+                        res_.big_list.p, res_.tile_order.p, d_counters_, pair_cap_, stream_,
+                        totals_.p);
     launch_emit_keys(emit_.p, d_counters_, res_.tiles_x, n_tiles, res_.tile_cursor.p, keys_.p,
                      persistent_grid_, stream_);
     maps_valid_ = false;

@@ -111,10 +111,10 @@ private:
     cudaStream_t stream_ = nullptr;
     DevTree tree_;
     // tree storage
-    DevBuf<float> soa_;        // 6 * n floats: mx my mz sx sy sz
-    DevBuf<float4> quat_;
+    DevBuf<float4> geo_;       // (mean, max scale) per node
+    DevBuf<float4> iscale_;    // internal region: (scales, leaf flag)
+    DevBuf<float4> iquat_;     // internal region: quaternion
     DevBuf<uint32_t> parent_;
-    DevBuf<uint8_t> leaf_;
     DevBuf<SplatRec> splat_;
     // frame storage
     DevBuf<uint32_t> cand_bits_, qint_bits_, selected_;

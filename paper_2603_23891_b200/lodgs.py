@@ -442,6 +442,7 @@ class RenderStats:
     t_sort_ms: float = 0.0
     t_alpha_ms: float = 0.0
     big_tiles: int = 0
+    kernel_launches: int = 0  # sm_100a kernels enqueued for the frame
 
     def total_ms(self) -> float:
         return self.t_calc_ms + self.t_sync_ms + self.t_prepr_ms + self.t_sort_ms + self.t_alpha_ms
@@ -450,7 +451,7 @@ class RenderStats:
     def from_c(s: RenderStatsC) -> "RenderStats":
         return RenderStats(s.n_selected, s.n_pairs, s.n_gaussians, s.filter_passes,
                            s.filter_barriers, s.t_calc_ms, s.t_sync_ms, s.t_prepr_ms,
-                           s.t_sort_ms, s.t_alpha_ms, s.big_tiles)
+                           s.t_sort_ms, s.t_alpha_ms, s.big_tiles, s.kernel_launches)
 
 
 _LIST_F64 = ("mean_x", "mean_y", "conic_a", "conic_b", "conic_c", "opacity",

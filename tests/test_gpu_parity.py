@@ -172,6 +172,25 @@ def test_filter_mid_trees_leaf_suffix(L, oracle, gpu):
                 assert np.array_equal(got, want), (rep, tree.node_count(), tau_r)
 
 
+def test_filter_frustum_boundary_sweep(L, oracle, gpu):
+    """Leaf and internal frustum pre-tests at the planes: the camera slides in
+    1e-4 steps so that node spheres cross the side planes inside the FP32
+    undecided band (where the FP64 decision must take over); selected lists
+    bit-exact at every step."""
+    tree = L.make_tree(31, 3, 8, 0.5, 9, 9)  # leaf suffix starts inside the arena
+    assert tree.node_count() > 4096
+    base = topdown_camera(640, 480, 400.0, 10.0)
+    with L.GpuScene(tree) as s:
+        for step in range(80):
+            cam = topdown_camera(640, 480, 400.0, 10.0)
+            tx, ty, tz = base.translation
+            cam.translation = (tx + 1e-4 * step, ty - 0.7e-4 * step, tz)
+            for tau_r in (3.0, 40.0):
+                want, _, _ = oracle.filter(tree, cam, tau_r)
+                got = s.filter(cam, L.FilterConfig(tau_r)).selected
+                assert np.array_equal(got, want), (step, tau_r)
+
+
 def test_filter_qpass_threshold_stress(L, oracle, gpu):
     """The FP32-certified qpass pre-test must defer to FP64 whenever a radius
     sits at tau_r: tau_r is set to the exact FP64 radius of visible internal

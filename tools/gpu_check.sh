@@ -12,10 +12,11 @@ if [ "${2:-}" != "skip-tests" ]; then
 fi
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?"
 tail -c 3000 $OUT/bench.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 400 -c 400 --csv \
-   --log-file $OUT/launches.csv python bench.py --steps 60 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1; echo "ncu launches exit $?"
+# launch list over the whole 300-frame path (skip the 30 sizing + 3 warm-up frames)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 330 -c 3000 --csv \
+   --log-file $OUT/launches.csv python bench.py --steps 300 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1; echo "ncu launches exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-   -k regex:'k_filter_mark|k_select_internal|k_select_leaves|k_compact' -s 12 -c 4 \
+   -k regex:'k_mark_internal|k_select_internal|k_filter_leaves|k_compact|k_tile_offsets' -s 15 -c 5 \
    -o $OUT/prof_filter python tools/profile_frames.py --alt 200 --frames 5 > $OUT/ncu_filter.log 2>&1; echo "ncu filter exit $?"
 if [ "${3:-}" != "filter-only" ]; then
 timeout 900 ncu --set full --clock-control none --import-source on \
