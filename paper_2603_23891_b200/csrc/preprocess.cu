@@ -14,6 +14,8 @@
 // key = bit_cast<u32>(depth) << 32 | gaussian; the in-tile order is settled
 // by sort.cu, and since gaussian indices are unique per tile the final
 // order equals the reference's stable LSD radix (rasterizer.cpp:100-135).
+#include <cooperative_groups.h>
+
 #include "launch.h"
 #include "mark.cuh"
 #include "scan.cuh"
@@ -270,28 +272,30 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
                                                        uint32_t* order, FrameCounters* cnt,
                                                        uint64_t pair_cap, RunTotals* totals,
                                                        int staged) {
+    // staged: counts, then offsets, in s_buf[0, n]; the order in s_buf[n+1, 2n+1).
+    // Every global write then leaves the SM as coalesced rows -- a single SM's
+    // scattered stores were the bottleneck of this kernel (~1 sector/clk).
     __shared__ uint64_t s_warp[32];
     __shared__ uint32_t s_cls[4][32];  // per (class, warp): tiles, then first order slot
-    extern __shared__ uint32_t s_count[];
+    extern __shared__ uint32_t s_buf[];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // stage the counts with independent coalesced loads (the serial per-thread
-    // passes below would otherwise pay one L2 round trip per tile)
-    const uint32_t* count = gcount;
+    uint32_t* off = staged ? s_buf : offsets;
+    uint32_t* ord = staged ? s_buf + n_tiles + 1 : order;
     if (staged) {
 #pragma unroll 8
-        for (int t = threadIdx.x; t < n_tiles; t += 1024) s_count[t] = __ldg(gcount + t);
+        for (int t = threadIdx.x; t < n_tiles; t += 1024) s_buf[t] = __ldg(gcount + t);
         __syncthreads();
-        count = s_count;
     }
+    const uint32_t* count = staged ? s_buf : gcount;
     const int per = (n_tiles + 1023) / 1024;
     const int t0 = min(n_tiles, int(threadIdx.x) * per), t1 = min(n_tiles, t0 + per);
     uint64_t sum = 0;
     for (int t = t0; t < t1; ++t) sum += count[t];
     uint64_t incl = sum;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t o = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= unsigned(off)) incl += o;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= unsigned(o)) incl += v;
     }
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
@@ -299,9 +303,9 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
         const uint64_t v = s_warp[lane];
         uint64_t wi = v;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint64_t o = __shfl_up_sync(0xffffffffu, wi, off);
-            if (lane >= unsigned(off)) wi += o;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= unsigned(o)) wi += u;
         }
         s_warp[lane] = wi;  // inclusive warp prefix
     }
@@ -312,15 +316,14 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
     const bool ovf = total > pair_cap;
     uint64_t run = (warp ? s_warp[warp - 1] : 0ull) + (incl - sum);
     for (int t = t0; t < t1; ++t) {
-        const uint32_t c = ovf ? 0u : count[t];
-        const uint32_t o = ovf ? 0u : uint32_t(run);
-        offsets[t] = o;
-        cursor[t] = o;
+        const uint32_t c = count[t];  // staged: read before the in-place overwrite
+        off[t] = ovf ? 0u : uint32_t(run);
         run += c;
-        if (c > uint32_t(kSmallSortCap)) big_list[atomicAdd(&cnt->big_tiles, 1u)] = uint32_t(t);
+        if (!ovf && c > uint32_t(kSmallSortCap))
+            big_list[atomicAdd(&cnt->big_tiles, 1u)] = uint32_t(t);
     }
     if (threadIdx.x == 0) {
-        offsets[n_tiles] = ovf ? 0u : uint32_t(total);
+        off[n_tiles] = ovf ? 0u : uint32_t(total);
         if (ovf) cnt->overflow = 1u;
         if (totals) {
             totals->frames += 1;
@@ -328,6 +331,16 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
             totals->sum_pairs += ovf ? 0ull : total;
             if (ovf) totals->pad = 1;
         }
+    }
+    __syncthreads();
+    if (staged) {
+        for (int t = threadIdx.x; t <= n_tiles; t += 1024) {
+            const uint32_t o = s_buf[t];
+            offsets[t] = o;
+            if (t < n_tiles) cursor[t] = o;
+        }
+    } else {
+        for (int t = threadIdx.x; t < n_tiles; t += 1024) cursor[t] = offsets[t];
     }
     // Heavy-first schedule for the per-tile kernels (sort, blend): a stable
     // partition of the tiles into four classes by pair count relative to the
@@ -339,7 +352,7 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
     unsigned my_cnt = 0;  // lane c < 4: tiles of class c seen by this warp
     for (int k = 0; k < rounds; ++k) {
         const int t = k * 1024 + int(threadIdx.x);
-        const int cls = t < n_tiles ? tile_class(ovf ? 0u : count[t], mean) : 4;
+        const int cls = t < n_tiles ? tile_class(off[t + 1] - off[t], mean) : 4;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const unsigned m = __ballot_sync(0xffffffffu, cls == c);
@@ -348,13 +361,13 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
     }
     if (lane < 4) s_cls[lane][warp] = my_cnt;
     __syncthreads();
-    if (warp < 4) {  // warp c scans class c over the 32 warps; class offsets follow
+    if (warp < 4) {  // warp c scans class c over the 32 warps
         const uint32_t v = s_cls[warp][lane];
         uint32_t wi = v;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, wi, off);
-            if (lane >= unsigned(off)) wi += o;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= unsigned(o)) wi += u;
         }
         s_cls[warp][lane] = wi - v;
         if (lane == 31) s_warp[warp] = wi;  // class total (s_warp is free again)
@@ -370,33 +383,191 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
     const unsigned lt = (1u << lane) - 1u;
     for (int k = 0; k < rounds; ++k) {
         const int t = k * 1024 + int(threadIdx.x);
-        const int cls = t < n_tiles ? tile_class(ovf ? 0u : count[t], mean) : 4;
+        const int cls = t < n_tiles ? tile_class(off[t + 1] - off[t], mean) : 4;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const unsigned m = __ballot_sync(0xffffffffu, cls == c);
-            if (cls == c) order[rank[c] + __popc(m & lt)] = uint32_t(t);
+            if (cls == c) ord[rank[c] + __popc(m & lt)] = uint32_t(t);
             rank[c] += __popc(m);
         }
     }
+    if (staged) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < n_tiles; t += 1024) order[t] = ord[t];
+    }
+}
+
+// Cluster variant for up to 8 x 12,288 tiles: the 8 CTAs of one thread-block
+// cluster each own a contiguous chunk of tiles, and exchange their chunk
+// totals and class counts through distributed shared memory (two cluster
+// barriers) -- the single-CTA kernel above is bound by one SM's issue rate.
+namespace cg = cooperative_groups;
+constexpr int kOffCtas = 8;
+constexpr int kOffChunkMax = 12288;
+
+__global__ void __cluster_dims__(kOffCtas, 1, 1) __launch_bounds__(1024) k_tile_offsets_cluster(
+    const uint32_t* __restrict__ gcount, int n_tiles, uint32_t* offsets, uint32_t* cursor,
+    uint32_t* big_list, uint32_t* order, FrameCounters* cnt, uint64_t pair_cap,
+    RunTotals* totals) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned crank = cluster.block_rank();
+    __shared__ unsigned long long s_tot;  // this chunk's pair total (read by every CTA)
+    __shared__ uint32_t s_ccls[4];        // this chunk's tiles per class (read by every CTA)
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint32_t s_wcls[4][32];
+    extern __shared__ uint32_t s_off[];  // chunk counts, then offsets; [m] = chunk end
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int chunk = (n_tiles + kOffCtas - 1) / kOffCtas;
+    const int c0 = min(n_tiles, int(crank) * chunk), m = min(n_tiles, c0 + chunk) - c0;
+#pragma unroll 4
+    for (int t = threadIdx.x; t < m; t += 1024) s_off[t] = __ldg(gcount + c0 + t);
+    __syncthreads();
+    const int per = (chunk + 1023) / 1024;
+    const int t0 = min(m, int(threadIdx.x) * per), t1 = min(m, t0 + per);
+    uint64_t sum = 0;
+    for (int t = t0; t < t1; ++t) sum += s_off[t];
+    uint64_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= unsigned(o)) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t v = s_warp[lane];
+        uint64_t wi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= unsigned(o)) wi += u;
+        }
+        s_warp[lane] = wi;
+        if (lane == 31) s_tot = wi;
+    }
+    cluster.sync();  // #1: chunk totals visible cluster-wide
+    uint64_t total = 0, base = 0;
+#pragma unroll
+    for (int r = 0; r < kOffCtas; ++r) {
+        const uint64_t v = *cluster.map_shared_rank(&s_tot, r);
+        total += v;
+        base += unsigned(r) < crank ? v : 0ull;
+    }
+    // Overflow: every bucket becomes empty so sort/blend never touch the
+    // unwritten keys; the host grows the buffer and re-renders.
+    const bool ovf = total > pair_cap;
+    uint64_t run = base + (warp ? s_warp[warp - 1] : 0ull) + (incl - sum);
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t c = s_off[t];
+        s_off[t] = ovf ? 0u : uint32_t(run);
+        run += c;
+        if (!ovf && c > uint32_t(kSmallSortCap))
+            big_list[atomicAdd(&cnt->big_tiles, 1u)] = uint32_t(c0 + t);
+    }
+    if (threadIdx.x == 0) s_off[m] = ovf ? 0u : uint32_t(base + s_tot);
+    __syncthreads();
+    for (int t = threadIdx.x; t < m; t += 1024) {
+        const uint32_t o = s_off[t];
+        offsets[c0 + t] = o;
+        cursor[c0 + t] = o;
+    }
+    if (threadIdx.x == 0 && c0 + m == n_tiles && m > 0) offsets[n_tiles] = s_off[m];
+    if (crank == 0 && threadIdx.x == 0) {
+        if (n_tiles == 0) offsets[0] = 0u;
+        if (ovf) cnt->overflow = 1u;
+        if (totals) {
+            totals->frames += 1;
+            totals->sum_selected += cnt->n_selected;
+            totals->sum_pairs += ovf ? 0ull : total;
+            if (ovf) totals->pad = 1;
+        }
+    }
+    // heavy-first schedule (see k_tile_offsets): classes by count vs the mean
+    const uint32_t mean = uint32_t(total / uint64_t(n_tiles > 0 ? n_tiles : 1)) + 1u;
+    unsigned my_cnt = 0;
+    for (int k = 0; k < per; ++k) {
+        const int t = k * 1024 + int(threadIdx.x);
+        const int cls = t < m ? tile_class(s_off[t + 1] - s_off[t], mean) : 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const unsigned msk = __ballot_sync(0xffffffffu, cls == c);
+            if (lane == unsigned(c)) my_cnt += __popc(msk);
+        }
+    }
+    if (lane < 4) s_wcls[lane][warp] = my_cnt;
+    __syncthreads();
+    if (warp < 4) {  // warp c scans class c over the 32 warps
+        const uint32_t v = s_wcls[warp][lane];
+        uint32_t wi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= unsigned(o)) wi += u;
+        }
+        s_wcls[warp][lane] = wi - v;
+        if (lane == 31) s_ccls[warp] = wi;
+    }
+    cluster.sync();  // #2: chunk class counts visible cluster-wide
+    uint32_t rank[4];
+    {
+        uint32_t all[4] = {0u, 0u, 0u, 0u}, before[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int r = 0; r < kOffCtas; ++r) {
+            const uint32_t* rc = cluster.map_shared_rank(s_ccls, r);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t v = rc[c];
+                all[c] += v;
+                before[c] += unsigned(r) < crank ? v : 0u;
+            }
+        }
+        uint32_t cb = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            rank[c] = cb + before[c] + s_wcls[c][warp];
+            cb += all[c];
+        }
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    for (int k = 0; k < per; ++k) {
+        const int t = k * 1024 + int(threadIdx.x);
+        const int cls = t < m ? tile_class(s_off[t + 1] - s_off[t], mean) : 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const unsigned msk = __ballot_sync(0xffffffffu, cls == c);
+            if (cls == c) order[rank[c] + __popc(msk & lt)] = uint32_t(c0 + t);
+            rank[c] += __popc(msk);
+        }
+    }
+    cluster.sync();  // no CTA leaves while its shared memory may still be read
 }
 
 void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
                          uint32_t* cursor, uint32_t* big_list, uint32_t* order,
                          FrameCounters* cnt, uint64_t pair_cap, cudaStream_t s,
                          RunTotals* totals) {
-    // counts staged in shared memory up to 48K tiles (192 KB; 4K frames are 32,400)
-    const int staged = n_tiles <= 49152 ? 1 : 0;
-    const size_t smem = staged ? size_t(n_tiles) * 4 : 0;
-    if (smem > 48 * 1024) {
-        static bool attr_set[64] = {};  // function attributes are per device
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-            cudaFuncSetAttribute(k_tile_offsets, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 49152 * 4);
-            if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    if (n_tiles <= kOffCtas * kOffChunkMax) {
+        const int chunk = (n_tiles + kOffCtas - 1) / kOffCtas;
+        const size_t smem = size_t(chunk + 1) * 4;
+        if (smem > 48 * 1024) {
+            static bool attr_set[64] = {};  // function attributes are per device
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+                cudaFuncSetAttribute(k_tile_offsets_cluster,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (kOffChunkMax + 1) * 4);
+                if (dev >= 0 && dev < 64) attr_set[dev] = true;
+            }
         }
+        k_tile_offsets_cluster<<<kOffCtas, 1024, smem, s>>>(tile_count, n_tiles, offsets, cursor,
+                                                            big_list, order, cnt, pair_cap,
+                                                            totals);
+        return;
     }
+    // beyond 98,304 tiles (> 8K frames): one CTA, global memory
+    const int staged = 0;
+    const size_t smem = 0;
     k_tile_offsets<<<1, 1024, smem, s>>>(tile_count, n_tiles, offsets, cursor, big_list, order,
                                          cnt, pair_cap, totals, staged);
 }
