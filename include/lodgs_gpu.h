@@ -269,6 +269,13 @@ LODGS_API int lodgs_gpu_read_counts(lodgs_gpu_scene *scene, uint32_t *per_gaussi
 LODGS_API int lodgs_gpu_filter(lodgs_gpu_scene *scene, const lodgs_camera *cam, double tau_r,
                      uint32_t *selected, uint64_t cap, uint64_t *n_selected, int32_t *passes,
                      int32_t *barriers);
+/* filter_serial (filter.cpp:60-113): level-wise traversal, one kernel and one
+ * barrier per level (the paper's serial baseline); selected
+ * ascending; passes = barriers = levels with an active node.  level_ms
+ * (nullable, n_levels entries) receives each level's device time. */
+LODGS_API int lodgs_gpu_filter_serial(lodgs_gpu_scene *scene, const lodgs_camera *cam, double tau_r,
+                            uint32_t *selected, uint64_t cap, uint64_t *n_selected,
+                            int32_t *passes, int32_t *barriers, double *level_ms);
 /* MarkFn contract (kernels.hpp:47-52) over [begin, end): vis, qpass and
  * (nullable) the FP64 screen radius, bit-identical to mark_scalar. */
 LODGS_API int lodgs_gpu_mark(lodgs_gpu_scene *scene, const lodgs_camera *cam, uint64_t begin, uint64_t end,

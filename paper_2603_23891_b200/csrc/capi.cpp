@@ -288,6 +288,24 @@ int lodgs_gpu_filter(lodgs_gpu_scene* scene, const lodgs_camera* cam, double tau
     });
 }
 
+int lodgs_gpu_filter_serial(lodgs_gpu_scene* scene, const lodgs_camera* cam, double tau_r,
+                            uint32_t* selected, uint64_t cap, uint64_t* n_selected,
+                            int32_t* passes, int32_t* barriers, double* level_ms) {
+    return guarded([&] {
+        need(cam, "cam");
+        std::vector<uint32_t> sel;
+        int32_t ps = 0;
+        const uint64_t ns = S(scene).filter_serial(*cam, tau_r, sel, &ps, level_ms);
+        if (n_selected) *n_selected = ns;
+        if (passes) *passes = ps;
+        if (barriers) *barriers = ps;
+        if (selected) {
+            if (cap < ns) throw fgs::Error(LODGS_ERR_VALIDATION, "filter: capacity too small");
+            std::memcpy(selected, sel.data(), ns * 4);
+        }
+    });
+}
+
 int lodgs_gpu_mark(lodgs_gpu_scene* scene, const lodgs_camera* cam, uint64_t begin, uint64_t end,
                    double tau_r, uint8_t* vis, uint8_t* qpass, double* radius) {
     return guarded([&] {

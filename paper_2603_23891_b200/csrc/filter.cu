@@ -255,6 +255,30 @@ __device__ __noinline__ bool vis_fp64(const Geom& g, const DevTree& t, uint64_t 
     return frustum_folded(g, tx, ty, tz, 3.0 * double(a.w));
 }
 
+// Reference decision (mark_core.hpp:24-116) for node i of the internal
+// region from its three records: vis, and qint = qpass && !leaf.
+__device__ __forceinline__ void decide_internal(const Geom& g, const GeomF& f, const DevTree& t,
+                                                uint64_t i, float4 a, float4 sc, float4 q,
+                                                double tau_r, bool& vis, bool& qint) {
+    const bool leaf = sc.w != 0.0f;
+    Cam32 c;
+    int zs;
+    int vs = frustum_fp32(f, a.x, a.y, a.z, 3.0f * a.w, c, zs);
+    int qs = 0;
+    if (vs == 1 && !leaf) {
+        if (zs == 1) qs = qpass_fp32(f, c, sc.x, sc.y, sc.z, q);
+        else if (zs < 0) qs = -1;  // zs == 0: z_ok false, qpass false for certain
+    }
+    if (vs < 0 || qs < 0) {
+        int v, qi;
+        mark_fp64(g, t, i, a.x, a.y, a.z, sc.x, sc.y, sc.z, !leaf, tau_r, &v, &qi);
+        vs = v;
+        qs = qi;
+    }
+    vis = vs == 1;
+    qint = vs == 1 && qs == 1;
+}
+
 // F1: internal region [0, leaf_begin).  Persistent grid; each warp walks
 // 32-node groups (one node per lane) and issues the three 16-byte records of
 // its next group (mean + max scale, scales + leaf flag, quaternion) before
@@ -285,23 +309,9 @@ __global__ void __launch_bounds__(kMarkBlock, 3) k_mark_internal(
         load(grp + stride);
         bool cand = false, qint = false;
         if (i < end) {
-            const bool leaf = csc.w != 0.0f;
-            Cam32 c;
-            int zs;
-            int vs = frustum_fp32(f, ca.x, ca.y, ca.z, 3.0f * ca.w, c, zs);
-            int qs = 0;
-            if (vs == 1 && !leaf) {
-                if (zs == 1) qs = qpass_fp32(f, c, csc.x, csc.y, csc.z, cq);
-                else if (zs < 0) qs = -1;  // zs == 0: z_ok false, qpass false for certain
-            }
-            if (vs < 0 || qs < 0) {
-                int v, qi;
-                mark_fp64(g, t, i, ca.x, ca.y, ca.z, csc.x, csc.y, csc.z, !leaf, tau_r, &v, &qi);
-                vs = v;
-                qs = qi;
-            }
-            qint = vs == 1 && qs == 1;
-            cand = vs == 1 && (leaf || qint);
+            bool vis;
+            decide_internal(g, f, t, i, ca, csc, cq, tau_r, vis, qint);
+            cand = vis && (csc.w != 0.0f || qint);
         }
         const unsigned cm = __ballot_sync(0xffffffffu, cand);
         const unsigned qm = __ballot_sync(0xffffffffu, qint);
@@ -500,6 +510,82 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ ke
         if ((word >> lane) & 1u)
             selected[pos + at + __popc(word & lt)] = uint32_t(warp_node + uint64_t(j) * 32 + lane);
     }
+}
+
+// ---- serial (level-wise) filter, reference filter_serial (filter.cpp:60-113) --
+// The ablation baseline of the paper's Table 2:
+// one kernel and one barrier per level.  Level l is processed flat over its
+// node range: a node is active iff l == 0 or its parent was expanded (visible,
+// not qpass, not a leaf); an active visible node is selected if qpass or leaf
+// and expanded otherwise -- exactly the reference's active-list recursion,
+// kept as bitmasks so `selected` comes out in node order (the reference's
+// level-major, parent-ordered output is ascending, test_filter.cpp:126).
+// Words straddling a level boundary are merged with atomicOr (both bitmasks
+// are cleared first).  level_flag[l] != 0 iff level l had an active node.
+__global__ void __launch_bounds__(256) k_serial_level(
+    const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
+    const double tau_r, const uint64_t b, const uint64_t e, const int level,
+    uint32_t* __restrict__ sel_bits, uint32_t* __restrict__ exp_bits,
+    uint32_t* __restrict__ tile_count, unsigned* level_flag) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t i = (b & ~uint64_t(31)) + uint64_t(blockIdx.x) * 256 + threadIdx.x;
+    bool sel = false, expand = false, active = false;
+    if (i >= b && i < e) {
+        const uint32_t p = t.parent[i];
+        active = level == 0 || (p != kRootParent && ((exp_bits[p >> 5] >> (p & 31)) & 1u));
+        if (active) {
+            const float4 a = t.geo[i];
+            if (i < t.leaf_begin) {
+                bool vis, qint;
+                decide_internal(g, f, t, i, a, t.iscale[i], t.iquat[i], tau_r, vis, qint);
+                const bool leaf = t.iscale[i].w != 0.0f;
+                sel = vis && (qint || leaf);
+                expand = vis && !qint && !leaf;
+            } else {  // all-leaf suffix: only vis matters
+                int vs = frustum_leaf_fp32(f, a.x, a.y, a.z, a.w);
+                if (vs < 0) vs = vis_fp64(g, t, i) ? 1 : 0;
+                sel = vs == 1;
+            }
+        }
+    }
+    const unsigned sm = __ballot_sync(0xffffffffu, sel);
+    const unsigned em = __ballot_sync(0xffffffffu, expand);
+    const unsigned am = __ballot_sync(0xffffffffu, active);
+    if (lane == 0) {
+        const uint64_t w = i >> 5;
+        const bool whole = (w << 5) >= b && ((w + 1) << 5) <= e;
+        if (whole) {
+            sel_bits[w] = sm;
+            exp_bits[w] = em;
+        } else {
+            if (sm) atomicOr(sel_bits + w, sm);
+            if (em) atomicOr(exp_bits + w, em);
+        }
+        if (sm) atomicAdd(tile_count + (i >> 13), __popc(sm));
+        if (am && !level_flag[level]) atomicOr(level_flag + level, 1u);
+    }
+}
+
+void launch_filter_serial(const Geom& g, const DevTree& t, double tau_r,
+                          const uint64_t* level_begin, int n_levels, uint32_t* sel_bits,
+                          uint32_t* exp_bits, uint32_t* tile_count, unsigned* level_flag,
+                          uint32_t* selected, FrameCounters* cnt, cudaEvent_t* level_events,
+                          cudaStream_t s) {
+    if (t.n == 0) return;
+    const GeomF f = make_geomf(g, tau_r, t.max_l1);
+    cudaMemsetAsync(sel_bits, 0, ((t.n + 31) / 32) * 4, s);
+    cudaMemsetAsync(exp_bits, 0, ((t.n + 31) / 32) * 4, s);
+    for (int l = 0; l < n_levels; ++l) {
+        const uint64_t b = level_begin[l], e = l + 1 < n_levels ? level_begin[l + 1] : t.n;
+        if (level_events) cudaEventRecord(level_events[l], s);
+        if (e <= b) continue;
+        const uint64_t span = e - (b & ~uint64_t(31));
+        k_serial_level<<<unsigned((span + 255) / 256), 256, 0, s>>>(
+            g, f, t, tau_r, b, e, l, sel_bits, exp_bits, tile_count, level_flag);
+    }
+    if (level_events) cudaEventRecord(level_events[n_levels], s);
+    k_compact<<<unsigned((t.n + kTileNodes - 1) / kTileNodes), 256, 0, s>>>(
+        sel_bits, (t.n + 31) / 32, tile_count, selected, cnt);
 }
 
 // MarkFn contract (kernels.hpp:47-52): full mark_core per node, all outputs.

@@ -49,6 +49,14 @@ inline uint32_t select_tiles(uint64_t n) {
 void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
                    uint32_t* qint_bits, uint32_t* tile_count, uint32_t* selected,
                    FrameCounters* cnt, cudaStream_t s, cudaEvent_t mid = nullptr);
+// Serial (level-wise) filter, filter.cpp:60-113: one kernel per level, then
+// the ordered compaction.  level_flag[n_levels] (zeroed) marks the levels with
+// an active node; level_events (nullable, n_levels + 1) time the levels.
+void launch_filter_serial(const Geom& g, const DevTree& t, double tau_r,
+                          const uint64_t* level_begin, int n_levels, uint32_t* sel_bits,
+                          uint32_t* exp_bits, uint32_t* tile_count, unsigned* level_flag,
+                          uint32_t* selected, FrameCounters* cnt, cudaEvent_t* level_events,
+                          cudaStream_t s);
 // per-tile survivor counters the filter needs for an n-node tree
 uint32_t filter_status_entries(uint64_t n);
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,

@@ -62,6 +62,7 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
     // past an allocation
     const uint64_t np = (n + 255) / 256 * 256;
     tree_.n = n;
+    for (uint32_t l = 0; l < tree.n_levels; ++l) level_begin_.push_back(tree.level_offsets[l]);
     {
         // first index of the all-leaf suffix, rounded up to 1024 nodes
         uint64_t first = n;
@@ -419,6 +420,48 @@ uint64_t GpuScene::filter(const lodgs_camera& cam, double tau_r, std::vector<uin
     out.resize(ns);
     if (ns)
         FGS_CUDA(cudaMemcpy(out.data(), selected_.p, ns * 4, cudaMemcpyDeviceToHost));
+    return ns;
+}
+
+uint64_t GpuScene::filter_serial(const lodgs_camera& cam, double tau_r, std::vector<uint32_t>& out,
+                                 int32_t* passes, double* level_ms) {
+    DeviceGuard dg(device_);
+    if (!(tau_r > 0)) throw Error(LODGS_ERR_VALIDATION, "filter config: tau_r > 0");
+    ensure_resolution(int(cam.width), int(cam.height));
+    const Geom g = camera_geom(cam);
+    const int nl = n_levels();
+    clear_frame_state();
+    DevBuf<unsigned> flags;
+    flags.alloc(uint64_t(nl) + 1);
+    FGS_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes(), stream_));
+    std::vector<cudaEvent_t> ev;
+    if (level_ms) {
+        ev.resize(size_t(nl) + 1);
+        for (auto& e : ev) FGS_CUDA(cudaEventCreate(&e));
+    }
+    launch_filter_serial(g, tree_, tau_r, level_begin_.data(), nl, cand_bits_.p, qint_bits_.p,
+                         reinterpret_cast<uint32_t*>(d_status_select_), flags.p, selected_.p,
+                         d_counters_, level_ms ? ev.data() : nullptr, stream_);
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
+                             cudaMemcpyDeviceToHost, stream_));
+    std::vector<unsigned> hf(size_t(nl) + 1, 0u);
+    if (nl) FGS_CUDA(cudaMemcpyAsync(hf.data(), flags.p, size_t(nl) * 4, cudaMemcpyDeviceToHost, stream_));
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    if (level_ms) {
+        for (int l = 0; l < nl; ++l) {
+            float ms = 0.f;
+            FGS_CUDA(cudaEventElapsedTime(&ms, ev[size_t(l)], ev[size_t(l) + 1]));
+            level_ms[l] = ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    int32_t ps = 0;
+    for (int l = 0; l < nl; ++l) ps += hf[size_t(l)] ? 1 : 0;
+    if (passes) *passes = ps;
+    const uint64_t ns = h_counters_->n_selected;
+    out.resize(ns);
+    if (ns) FGS_CUDA(cudaMemcpy(out.data(), selected_.p, ns * 4, cudaMemcpyDeviceToHost));
     return ns;
 }
 

@@ -74,6 +74,12 @@ public:
 
     // stage entry points
     uint64_t filter(const lodgs_camera& cam, double tau_r, std::vector<uint32_t>& out);
+    // filter_serial (filter.cpp:60-113): level-wise, one kernel + barrier per
+    // level; passes = barriers = levels with an active node.  level_ms
+    // (nullable, n_levels entries) receives each level's device time.
+    uint64_t filter_serial(const lodgs_camera& cam, double tau_r, std::vector<uint32_t>& out,
+                           int32_t* passes, double* level_ms);
+    int n_levels() const { return int(level_begin_.size()); }
     void mark(const lodgs_camera& cam, uint64_t begin, uint64_t end, double tau_r, uint8_t* vis,
               uint8_t* qpass, double* radius);
     uint64_t prepare(const lodgs_camera& cam, const uint32_t* selected, uint64_t n_sel,
@@ -110,6 +116,7 @@ private:
     int device_;
     cudaStream_t stream_ = nullptr;
     DevTree tree_;
+    std::vector<uint64_t> level_begin_;  // scene.hpp:53 level_begin(l), host copy
     // tree storage
     DevBuf<float4> geo_;       // (mean, max scale) per node
     DevBuf<float4> iscale_;    // internal region: (scales, leaf flag)

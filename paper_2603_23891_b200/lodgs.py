@@ -172,7 +172,7 @@ ABI_SYMBOLS = (
     "lodgs_gpu_read_image", "lodgs_gpu_image_device_ptr", "lodgs_gpu_read_selected",
     "lodgs_gpu_read_pairs", "lodgs_gpu_read_gaussians", "lodgs_gpu_read_counts",
     "lodgs_gpu_read_kpc", "lodgs_gpu_calibrate",
-    "lodgs_gpu_filter", "lodgs_gpu_mark", "lodgs_gpu_prepare", "lodgs_gpu_bin_to_tiles",
+    "lodgs_gpu_filter", "lodgs_gpu_filter_serial", "lodgs_gpu_mark", "lodgs_gpu_prepare", "lodgs_gpu_bin_to_tiles",
     "lodgs_gpu_sort_pairs", "lodgs_gpu_alpha_blend", "lodgs_gpu_host_alloc",
     "lodgs_gpu_host_free",
 )
@@ -232,6 +232,9 @@ def load_library():
         "lodgs_gpu_filter": (C.c_int, [P, C.POINTER(CameraC), C.c_double, P, C.c_uint64,
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32)]),
+        "lodgs_gpu_filter_serial": (C.c_int, [P, C.POINTER(CameraC), C.c_double, P, C.c_uint64,
+                                              C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
+                                              C.POINTER(C.c_int32), _DP]),
         "lodgs_gpu_mark": (C.c_int, [P, C.POINTER(CameraC), C.c_uint64, C.c_uint64, C.c_double,
                                      P, P, P]),
         "lodgs_gpu_prepare": (C.c_int, [P, C.POINTER(CameraC), P, C.c_uint64, C.c_int32,
@@ -796,6 +799,27 @@ class GpuScene:
                                           C.byref(n), C.byref(ps), C.byref(bs)))
         return FilterResult(sel[: n.value].copy(), ps.value, bs.value)
 
+    def filter_serial(self, cam: Camera, config: FilterConfig, level_ms=None) -> FilterResult:
+        """filter.cpp:60-113 on the device: one kernel + barrier per level.
+        level_ms: optional float64 array (n_levels) for per-level device times."""
+        if not (config.tau_r > 0):
+            raise ValidationError("filter config: tau_r > 0")
+        if config.worker_count < 1:
+            raise ValidationError("filter config: worker_count >= 1")
+        c = cam.to_c()
+        n = C.c_uint64(0)
+        ps, bs = C.c_int32(0), C.c_int32(0)
+        cap = self.tree.node_count()
+        sel = np.empty(max(1, cap), np.uint32)
+        lm = None
+        if level_ms is not None:
+            assert level_ms.dtype == np.float64 and level_ms.size >= len(self.tree.level_offsets)
+            lm = level_ms.ctypes.data_as(_DP)
+        _check(self._lib.lodgs_gpu_filter_serial(self._h, C.byref(c), float(config.tau_r),
+                                                 _ptr(sel), cap, C.byref(n), C.byref(ps),
+                                                 C.byref(bs), lm))
+        return FilterResult(sel[: n.value].copy(), ps.value, bs.value)
+
     def mark(self, cam: Camera, tau_r: float, begin: int = 0, end: Optional[int] = None,
              vis=None, qpass=None, radius=None):
         n = self.tree.node_count()
@@ -845,6 +869,11 @@ def render(tree: LoDTree, cam: Camera, filter: FilterConfig, mode: ShrinkMode,
 def filter_parallel(tree: LoDTree, cam: Camera, config: FilterConfig) -> FilterResult:
     """filter.hpp:42-43 -- passes = barriers = 2."""
     return _scene_for(tree).filter(cam, config)
+
+
+def filter_serial(tree: LoDTree, cam: Camera, config: FilterConfig) -> FilterResult:
+    """filter.hpp:37-38 -- level-wise; passes = barriers = levels descended."""
+    return _scene_for(tree).filter_serial(cam, config)
 
 
 def prepare_gaussians(tree: LoDTree, cam: Camera, selected, mode: ShrinkMode) -> BlendList:

@@ -172,6 +172,79 @@ def test_filter_mid_trees_leaf_suffix(L, oracle, gpu):
                 assert np.array_equal(got, want), (rep, tree.node_count(), tau_r)
 
 
+def test_filter_serial_random_scenes(L, oracle, gpu):
+    """test_filter.cpp:110-140 restated for the device filter_serial: 40 random
+    scenes, selection and passes/barriers equal to the oracle's serial filter,
+    selection equal to the parallel filter, ascending order."""
+    rng = oracle.rng(4242)
+    for i in range(40):
+        depth = 1 + int(oracle.next_below(rng, 4))
+        children = 1 + int(oracle.next_below(rng, 8))
+        gamma = float(np.float32(oracle.uniform(rng, 0.3, 0.7)))
+        tree = L.make_tree(1000 + i, depth, children, gamma)
+        cam = oracle.orbit_camera(rng, 160, 120, oracle.uniform(rng, 3.0, 80.0))
+        tau_r = oracle.uniform(rng, 0.5, 60.0)
+        oracle.next_below(rng, 4)  # worker count draw
+        want, ps, bs = oracle.filter(tree, cam, tau_r, mode=1)
+        with L.GpuScene(tree) as s:
+            got = s.filter_serial(cam, L.FilterConfig(tau_r))
+            par = s.filter(cam, L.FilterConfig(tau_r))
+        assert np.array_equal(got.selected, want), i
+        assert (got.passes, got.barriers) == (ps, bs), i
+        assert np.array_equal(got.selected, par.selected), i
+        assert np.all(np.diff(got.selected.astype(np.int64)) > 0)
+
+
+def test_filter_serial_barriers_per_level(L, oracle, gpu):
+    """test_filter.cpp:168-186: the serial filter pays one barrier per
+    descended level; everything visible and nothing qualifying selects exactly
+    the leaves.  Per-level device times are reported for every level."""
+    for depth in (2, 4, 6):
+        t = L.make_tree(7, depth, 2, 0.5, 2, 2)
+        cam = oracle.front_camera(200, 200)
+        cam.translation = (0, 0, 30)
+        with L.GpuScene(t) as s:
+            lm = np.full(len(t.level_offsets), -1.0)
+            rs = s.filter_serial(cam, L.FilterConfig(1e-3), level_ms=lm)
+            rp = s.filter(cam, L.FilterConfig(1e-3))
+        assert rs.barriers == depth + 1 and rs.passes == depth + 1
+        assert np.array_equal(rs.selected, rp.selected)
+        assert rs.selected.size == t.node_count() - int(t.level_offsets[depth])
+        assert (lm >= 0).all()
+
+
+def test_filter_serial_descends_only_under_visible_parents(L, oracle, gpu):
+    """A child sphere outside its parent's: the serial filter never reaches it
+    (its parent is culled) while the parallel filter selects it -- the device
+    serial filter keeps the reference's traversal semantics, not the parallel
+    rule."""
+    t = _hand_tree(L, 1, 8)
+    t.mean_x[8] = np.float32(40.0)  # child 8 far to the side of its parent
+    t.mean_z[0] = np.float32(-50.0)  # parent behind the camera
+    cam = oracle.front_camera(200, 200)
+    cam.translation = (-40.0, 0.0, 30.0)
+    want_s, ps, _ = oracle.filter(t, cam, 3.0, mode=1)
+    want_p, _, _ = oracle.filter(t, cam, 3.0, mode=2)
+    with L.GpuScene(t) as s:
+        got_s = s.filter_serial(cam, L.FilterConfig(3.0))
+        got_p = s.filter(cam, L.FilterConfig(3.0))
+    assert np.array_equal(got_s.selected, want_s) and got_s.passes == ps
+    assert np.array_equal(got_p.selected, want_p)
+    assert not np.array_equal(want_s, want_p)
+
+
+def test_filter_serial_10m_tree(L, oracle, gpu):
+    """cfg 3 tree: serial == parallel == oracle at two altitudes, 4 passes."""
+    tree = L.build_synthetic_tree(nx=131, ny=131, seed=1, depth=3, build_seed=7)
+    with L.GpuScene(tree) as s:
+        for alt in (200.0, 140.0):
+            cam = topdown_camera(1920, 1080, 1000.0, alt)
+            want, ps, _ = oracle.filter(tree, cam, 3.0, mode=1)
+            got = s.filter_serial(cam, L.FilterConfig(3.0))
+            assert np.array_equal(got.selected, want) and got.passes == ps == 4
+            assert np.array_equal(got.selected, s.filter(cam, L.FilterConfig(3.0)).selected)
+
+
 def test_filter_frustum_boundary_sweep(L, oracle, gpu):
     """Leaf and internal frustum pre-tests at the planes: the camera slides in
     1e-4 steps so that node spheres cross the side planes inside the FP32
