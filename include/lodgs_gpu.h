@@ -81,7 +81,8 @@ enum lodgs_render_flags {
     LODGS_RENDER_EXACT_BLEND = 1u,  /* FP64 blend with the reference exp_mx: bit-exact image */
     LODGS_RENDER_KEEP_PAIRS = 2u,   /* keep sorted pairs + gaussians readable after the frame */
     LODGS_RENDER_STAGE_TIMING = 4u, /* CUDA-event stage timers into lodgs_render_stats */
-    LODGS_RENDER_COLLECT_KPC = 8u   /* RenderOptions::collect_kpc: per-pair kpc, exact blend */
+    LODGS_RENDER_COLLECT_KPC = 8u,  /* RenderOptions::collect_kpc: per-pair kpc, exact blend */
+    LODGS_RENDER_FILTER_SERIAL = 16u /* RenderOptions::filter_mode = serial (filter.cpp:60-113) */
 };
 
 /* FilterConfig (filter.hpp:11-14) + ShrinkMode (rasterizer.hpp:16-24). */
@@ -293,6 +294,24 @@ LODGS_API int lodgs_gpu_sort_pairs(lodgs_tile_pair *pairs, uint64_t n);
  * LODGS_RENDER_EXACT_BLEND. image receives W*H*3 floats. */
 LODGS_API int lodgs_gpu_alpha_blend(const lodgs_tile_pair *sorted, uint64_t n, const lodgs_blend_list *list,
                           int width, int height, uint32_t flags, float *image);
+
+/* ------------------------------------------- image metrics, 8-bit output -- */
+/* The current image as 8-bit RGB with save_ppm's quantisation (image.cpp:19-22:
+ * clamp to [0,1], floor(v*255+0.5)); out receives W*H*3 bytes (1/4 of the f32
+ * image's PCIe traffic). */
+LODGS_API int lodgs_gpu_read_image_rgb8(lodgs_gpu_scene *scene, uint8_t *out);
+/* Keep the current image on the device as the comparison reference (bench.cpp:
+ * the first combination's frames are the reference of the others). */
+LODGS_API int lodgs_gpu_set_reference_image(lodgs_gpu_scene *scene);
+/* psnr / ssim (metrics.cpp:121-192) of the current image against the stored
+ * reference, computed on the device; either output may be NULL.  Same
+ * dimensions required (ValidationError otherwise); psnr = +inf for identical
+ * images.  Per-window SSIM follows the reference's operation order; the sums
+ * over pixels / windows are re-associated (deterministic, not bit-equal). */
+LODGS_API int lodgs_gpu_compare_reference(lodgs_gpu_scene *scene, double *psnr, double *ssim);
+/* psnr / ssim of two host images (W*H*3 floats) on the current device. */
+LODGS_API int lodgs_gpu_image_metrics(const float *a, const float *b, int width, int height,
+                            double *psnr, double *ssim);
 
 /* ----------------------------------------------------------- utilities -- */
 /* Pinned host memory for zero-staging image readback. */

@@ -449,4 +449,15 @@ double ref_psnr(const float* a, const float* b, int w, int h) {
     return psnr(x, y);
 }
 
+// metrics.cpp:136-192
+double ref_ssim(const float* a, const float* b, int w, int h) {
+    Image x{w, h, std::vector<float>(a, a + std::size_t(w) * h * 3)};
+    Image y{w, h, std::vector<float>(b, b + std::size_t(w) * h * 3)};
+    try {
+        return ssim(x, y);
+    } catch (const std::exception&) {
+        return -1e300;
+    }
+}
+
 }  // extern "C"

@@ -306,6 +306,30 @@ int lodgs_gpu_filter_serial(lodgs_gpu_scene* scene, const lodgs_camera* cam, dou
     });
 }
 
+int lodgs_gpu_read_image_rgb8(lodgs_gpu_scene* scene, uint8_t* out) {
+    return guarded([&] {
+        need(out, "out");
+        S(scene).read_image_rgb8(out);
+    });
+}
+
+int lodgs_gpu_set_reference_image(lodgs_gpu_scene* scene) {
+    return guarded([&] { S(scene).set_reference_image(); });
+}
+
+int lodgs_gpu_compare_reference(lodgs_gpu_scene* scene, double* psnr, double* ssim) {
+    return guarded([&] { S(scene).compare_reference(psnr, ssim); });
+}
+
+int lodgs_gpu_image_metrics(const float* a, const float* b, int width, int height, double* psnr,
+                            double* ssim) {
+    return guarded([&] {
+        need(a, "a");
+        need(b, "b");
+        fgs::stage_image_metrics(a, b, width, height, psnr, ssim);
+    });
+}
+
 int lodgs_gpu_mark(lodgs_gpu_scene* scene, const lodgs_camera* cam, uint64_t begin, uint64_t end,
                    double tau_r, uint8_t* vis, uint8_t* qpass, double* radius) {
     return guarded([&] {

@@ -83,7 +83,7 @@ struct FrameCounters {
     unsigned int overflow;     // pair buffer too small
     unsigned int nonfinite;    // project() produced a non-finite value
     unsigned int big_cursor;
-    unsigned int ticket_leaf;
+    unsigned int serial_passes;  // filter_serial: levels with an active node
 };
 
 // Running totals across frames (not cleared per frame).

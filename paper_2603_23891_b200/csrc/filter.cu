@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(256) k_serial_level(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const double tau_r, const uint64_t b, const uint64_t e, const int level,
     uint32_t* __restrict__ sel_bits, uint32_t* __restrict__ exp_bits,
-    uint32_t* __restrict__ tile_count, unsigned* level_flag) {
+    uint32_t* __restrict__ tile_count, unsigned* level_flag, FrameCounters* cnt) {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t i = (b & ~uint64_t(31)) + uint64_t(blockIdx.x) * 256 + threadIdx.x;
     bool sel = false, expand = false, active = false;
@@ -562,7 +562,8 @@ __global__ void __launch_bounds__(256) k_serial_level(
             if (em) atomicOr(exp_bits + w, em);
         }
         if (sm) atomicAdd(tile_count + (i >> 13), __popc(sm));
-        if (am && !level_flag[level]) atomicOr(level_flag + level, 1u);
+        if (am && !level_flag[level] && atomicOr(level_flag + level, 1u) == 0u)
+            atomicAdd(&cnt->serial_passes, 1u);
     }
 }
 
@@ -581,7 +582,7 @@ void launch_filter_serial(const Geom& g, const DevTree& t, double tau_r,
         if (e <= b) continue;
         const uint64_t span = e - (b & ~uint64_t(31));
         k_serial_level<<<unsigned((span + 255) / 256), 256, 0, s>>>(
-            g, f, t, tau_r, b, e, l, sel_bits, exp_bits, tile_count, level_flag);
+            g, f, t, tau_r, b, e, l, sel_bits, exp_bits, tile_count, level_flag, cnt);
     }
     if (level_events) cudaEventRecord(level_events[n_levels], s);
     k_compact<<<unsigned((t.n + kTileNodes - 1) / kTileNodes), 256, 0, s>>>(

@@ -445,4 +445,17 @@ uint64_t build_synthetic(const lodgs_synthetic_spec& s, const lodgs_build_config
     return k;
 }
 
+void ssim_window(double w[121]) {
+    const double sigma = 1.5;
+    double sum = 0.0;
+    for (int y = 0; y < 11; ++y)
+        for (int x = 0; x < 11; ++x) {
+            const double dx = x - 11 / 2, dy = y - 11 / 2;
+            const double v = std::exp(-(dx * dx + dy * dy) / (2.0 * sigma * sigma));
+            w[y * 11 + x] = v;
+            sum += v;
+        }
+    for (int i = 0; i < 121; ++i) w[i] /= sum;
+}
+
 }  // namespace fgs

@@ -23,6 +23,8 @@ std::vector<std::string> validate_camera(const lodgs_camera& c);
 std::string join_violations(const std::string& what, const std::vector<std::string>& v,
                             uint64_t total);
 Geom camera_geom(const lodgs_camera& c);
+// metrics.cpp:136-154 SsimWindow: normalised 11x11 Gaussian, sigma 1.5
+void ssim_window(double w[121]);
 lodgs_camera interpolate(const lodgs_camera& a, const lodgs_camera& b, double t);
 std::vector<lodgs_camera> sample_path(const lodgs_camera* keys, uint32_t n_keys,
                                       const uint32_t* samples);

@@ -153,4 +153,14 @@ void launch_keys_to_triples(const uint32_t* offsets, int n_tiles, const unsigned
 void launch_gauss_counts(const GaussEmit* emit, const FrameCounters* cnt, uint64_t cap,
                          uint32_t* out, cudaStream_t s);
 
+// ---- image metrics + 8-bit output (metrics.cpp:121-195, image.cpp:12-28) ----
+constexpr int kMetricParts = 1184;  // per-CTA partial sums, summed in index order
+void launch_rgb8(const float* img, uint64_t n, uint8_t* out, cudaStream_t s);
+// *out = sum (double(a[i]) - double(b[i]))^2; partial: kMetricParts doubles
+void launch_sq_diff(const float* a, const float* b, uint64_t n, double* partial, double* out,
+                    cudaStream_t s);
+// *out = sum over all 11x11 windows of the per-window SSIM (metrics.cpp:150-191)
+void launch_ssim(const float* a, const float* b, int width, int height, const double* weights,
+                 double* partial, double* out, cudaStream_t s);
+
 }  // namespace fgs

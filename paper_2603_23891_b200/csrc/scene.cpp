@@ -219,9 +219,19 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     clear_frame_state();
     if (timing) FGS_CUDA(cudaEventRecord(ev_[0], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[0], stream_));
-    launch_filter(g, tree_, p.tau_r, cand_bits_.p, qint_bits_.p,
-                  reinterpret_cast<uint32_t*>(d_status_select_), selected_.p, d_counters_,
-                  stream_, pe ? pe[1] : nullptr);
+    if (p.flags & LODGS_RENDER_FILTER_SERIAL) {
+        level_flag_.alloc(uint64_t(n_levels()) + 1);
+        FGS_CUDA(cudaMemsetAsync(level_flag_.p, 0, level_flag_.bytes(), stream_));
+        launch_filter_serial(g, tree_, p.tau_r, level_begin_.data(), n_levels(), cand_bits_.p,
+                             qint_bits_.p, reinterpret_cast<uint32_t*>(d_status_select_),
+                             level_flag_.p, selected_.p, d_counters_, nullptr, stream_);
+        if (pe) FGS_CUDA(cudaEventRecord(pe[1], stream_));
+    } else {
+        launch_filter(g, tree_, p.tau_r, cand_bits_.p, qint_bits_.p,
+                      reinterpret_cast<uint32_t*>(d_status_select_), selected_.p, d_counters_,
+                      stream_, pe ? pe[1] : nullptr);
+    }
+    last_serial_ = (p.flags & LODGS_RENDER_FILTER_SERIAL) != 0;
     if (timing) FGS_CUDA(cudaEventRecord(ev_[1], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[2], stream_));
     PrepOut out{g64_.p, g32_.p, emit_.p, exact ? col64_.p : nullptr, d_tile_count_};
@@ -291,10 +301,11 @@ void GpuScene::finish(lodgs_render_stats* stats) {
         stats->n_selected = c.n_selected;
         stats->n_gaussians = c.n_gaussians;
         stats->n_pairs = c.n_pairs;
-        stats->filter_passes = 2;
-        stats->filter_barriers = 2;
+        stats->filter_passes = last_serial_ ? int32_t(c.serial_passes) : 2;
+        stats->filter_barriers = stats->filter_passes;
         stats->big_tiles = c.big_tiles;
-        stats->kernel_launches = kLaunchesPerFrame;
+        stats->kernel_launches =
+            last_serial_ ? uint32_t(kLaunchesPerFrame - 4 + n_levels() + 1) : kLaunchesPerFrame;
         if (last_timing_) {
             float ms = 0;
             FGS_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
@@ -396,10 +407,11 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
             s.n_selected = c.n_selected;
             s.n_gaussians = c.n_gaussians;
             s.n_pairs = c.n_pairs;
-            s.filter_passes = 2;
-            s.filter_barriers = 2;
+            s.filter_passes = last_serial_ ? int32_t(c.serial_passes) : 2;
+            s.filter_barriers = s.filter_passes;
             s.big_tiles = c.big_tiles;
-            s.kernel_launches = kLaunchesPerFrame;
+            s.kernel_launches = last_serial_ ? uint32_t(kLaunchesPerFrame - 4 + n_levels() + 1)
+                                             : kLaunchesPerFrame;
         }
     }
 }
@@ -421,6 +433,58 @@ uint64_t GpuScene::filter(const lodgs_camera& cam, double tau_r, std::vector<uin
     if (ns)
         FGS_CUDA(cudaMemcpy(out.data(), selected_.p, ns * 4, cudaMemcpyDeviceToHost));
     return ns;
+}
+
+void GpuScene::read_image_rgb8(uint8_t* out) {
+    DeviceGuard dg(device_);
+    const uint64_t n = image_floats();
+    rgb8_.alloc(n);
+    launch_rgb8(res_.image.p, n, rgb8_.p, stream_);
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaMemcpyAsync(out, rgb8_.p, n, cudaMemcpyDeviceToHost, stream_));
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void GpuScene::set_reference_image() {
+    DeviceGuard dg(device_);
+    if (!res_.image.p) throw Error(LODGS_ERR_VALIDATION, "set_reference_image: no frame rendered");
+    ref_image_.alloc(image_floats());
+    FGS_CUDA(cudaMemcpyAsync(ref_image_.p, res_.image.p, image_floats() * 4,
+                             cudaMemcpyDeviceToDevice, stream_));
+    ref_w_ = res_.width;
+    ref_h_ = res_.height;
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void GpuScene::compare_reference(double* psnr, double* ssim) {
+    DeviceGuard dg(device_);
+    if (!ref_image_.p || ref_w_ != res_.width || ref_h_ != res_.height)
+        throw Error(LODGS_ERR_VALIDATION, "psnr: image dimensions differ");
+    metric_partial_.alloc(kMetricParts + 2);
+    device_image_metrics(res_.image.p, ref_image_.p, res_.width, res_.height, psnr, ssim,
+                         metric_partial_.p, stream_);
+}
+
+void device_image_metrics(const float* a, const float* b, int width, int height, double* psnr,
+                          double* ssim, double* partial, cudaStream_t s) {
+    if (ssim && (width < 11 || height < 11))
+        throw Error(LODGS_ERR_VALIDATION, "ssim: images smaller than the 11x11 window");
+    const uint64_t n = uint64_t(width) * uint64_t(height) * 3;
+    double h[2] = {0.0, 0.0};
+    if (psnr) launch_sq_diff(a, b, n, partial, partial + kMetricParts, s);
+    if (ssim) {
+        double w[121];
+        ssim_window(w);
+        launch_ssim(a, b, width, height, w, partial, partial + kMetricParts + 1, s);
+    }
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaMemcpyAsync(h, partial + kMetricParts, 16, cudaMemcpyDeviceToHost, s));
+    FGS_CUDA(cudaStreamSynchronize(s));
+    if (psnr) {
+        const double mse = h[0] / double(n);
+        *psnr = mse == 0.0 ? INFINITY : 10.0 * std::log10(1.0 / mse);
+    }
+    if (ssim) *ssim = h[1] / (3.0 * double(width - 10) * double(height - 10));
 }
 
 uint64_t GpuScene::filter_serial(const lodgs_camera& cam, double tau_r, std::vector<uint32_t>& out,
@@ -848,6 +912,22 @@ void stage_sort_pairs(lodgs_tile_pair* pairs, uint64_t n) {
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaMemcpyAsync(pairs, outb.p, n * 12, cudaMemcpyDeviceToHost, c.s));
     FGS_CUDA(cudaStreamSynchronize(c.s));
+}
+
+void stage_image_metrics(const float* a, const float* b, int width, int height, double* psnr,
+                         double* ssim) {
+    if (width < 1 || height < 1) throw Error(LODGS_ERR_VALIDATION, "psnr: image dimensions");
+    StageCtx& c = stage_ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    const uint64_t n = uint64_t(width) * uint64_t(height) * 3;
+    DevBuf<float> da, db;
+    da.alloc(n);
+    db.alloc(n);
+    DevBuf<double> part;
+    part.alloc(kMetricParts + 2);
+    FGS_CUDA(cudaMemcpyAsync(da.p, a, n * 4, cudaMemcpyHostToDevice, c.s));
+    FGS_CUDA(cudaMemcpyAsync(db.p, b, n * 4, cudaMemcpyHostToDevice, c.s));
+    device_image_metrics(da.p, db.p, width, height, psnr, ssim, part.p, c.s);
 }
 
 void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_blend_list& list,

@@ -100,6 +100,13 @@ public:
     void calibrate(const lodgs_camera* views, uint32_t n_views, double lambda_g, double tau_r,
                    lodgs_calibration* out, double* per_view);
 
+    // 8-bit RGB of the current image (save_ppm quantisation, image.cpp:19-22)
+    void read_image_rgb8(uint8_t* out);
+    // Snapshot the current image as the on-device comparison reference, and
+    // psnr / ssim (metrics.cpp:121-192) of the current image against it.
+    void set_reference_image();
+    void compare_reference(double* psnr, double* ssim);
+
     void profile(bool enable);
     uint64_t profile_read(double stage_ms[6]);
 
@@ -117,6 +124,8 @@ private:
     cudaStream_t stream_ = nullptr;
     DevTree tree_;
     std::vector<uint64_t> level_begin_;  // scene.hpp:53 level_begin(l), host copy
+    DevBuf<unsigned> level_flag_;        // serial filter: level had an active node
+    bool last_serial_ = false;
     // tree storage
     DevBuf<float4> geo_;       // (mean, max scale) per node
     DevBuf<float4> iscale_;    // internal region: (scales, leaf flag)
@@ -132,6 +141,10 @@ private:
     DevBuf<unsigned long long> keys_;
     DevBuf<double> kpc_;         // per sorted pair (collect_kpc frames only)
     bool last_kpc_ = false;
+    DevBuf<float> ref_image_;    // comparison reference (set_reference_image)
+    int ref_w_ = 0, ref_h_ = 0;
+    DevBuf<uint8_t> rgb8_;
+    DevBuf<double> metric_partial_;  // kMetricParts + 2
     DevBuf<double> tile_gtc_;    // calibration scratch: per tile, + view result
     DevBuf<unsigned long long> kpc_bins_;
     // readback-only: slot <-> BlendList index maps and compacted records
@@ -175,6 +188,13 @@ private:
 void stage_bin_to_tiles(const lodgs_blend_list& list, int width, int height,
                         lodgs_tile_pair* out, uint64_t cap, uint64_t* n_pairs);
 void stage_sort_pairs(lodgs_tile_pair* pairs, uint64_t n);
+// psnr / ssim of two host images (W*H*3 floats) on the current device;
+// ssim may be null.  Throws ValidationError as metrics.cpp:122-149.
+void stage_image_metrics(const float* a, const float* b, int width, int height, double* psnr,
+                         double* ssim);
+// metrics on device images (any device pointers on the current device)
+void device_image_metrics(const float* a, const float* b, int width, int height, double* psnr,
+                          double* ssim, double* partial, cudaStream_t s);
 void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_blend_list& list,
                        int width, int height, uint32_t flags, float* image);
 

@@ -174,7 +174,8 @@ ABI_SYMBOLS = (
     "lodgs_gpu_read_kpc", "lodgs_gpu_calibrate",
     "lodgs_gpu_filter", "lodgs_gpu_filter_serial", "lodgs_gpu_mark", "lodgs_gpu_prepare", "lodgs_gpu_bin_to_tiles",
     "lodgs_gpu_sort_pairs", "lodgs_gpu_alpha_blend", "lodgs_gpu_host_alloc",
-    "lodgs_gpu_host_free",
+    "lodgs_gpu_host_free", "lodgs_gpu_read_image_rgb8", "lodgs_gpu_set_reference_image",
+    "lodgs_gpu_compare_reference", "lodgs_gpu_image_metrics",
 )
 
 _lib = None
@@ -232,6 +233,10 @@ def load_library():
         "lodgs_gpu_filter": (C.c_int, [P, C.POINTER(CameraC), C.c_double, P, C.c_uint64,
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32)]),
+        "lodgs_gpu_read_image_rgb8": (C.c_int, [P, P]),
+        "lodgs_gpu_set_reference_image": (C.c_int, [P]),
+        "lodgs_gpu_compare_reference": (C.c_int, [P, _DP, _DP]),
+        "lodgs_gpu_image_metrics": (C.c_int, [P, P, C.c_int, C.c_int, _DP, _DP]),
         "lodgs_gpu_filter_serial": (C.c_int, [P, C.POINTER(CameraC), C.c_double, P, C.c_uint64,
                                               C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
                                               C.POINTER(C.c_int32), _DP]),
@@ -676,15 +681,15 @@ class GpuScene:
 
     @staticmethod
     def params(filter: FilterConfig, mode: ShrinkMode, opts: RenderOptions) -> RenderParamsC:
+        if opts.filter_mode not in ("parallel", "serial"):
+            raise ValidationError("render: filter_mode is 'parallel' or 'serial'")
         flags = (1 if opts.exact_blend else 0) | (2 | 8 if opts.collect_kpc else 0) | \
-                (4 if opts.stage_timing else 0)
+                (4 if opts.stage_timing else 0) | (16 if opts.filter_mode == "serial" else 0)
         return RenderParamsC(float(filter.tau_r), float(mode.tau), int(mode.kind), flags)
 
     def render(self, cam: Camera, filter: FilterConfig, mode: ShrinkMode,
                opts: RenderOptions = RenderOptions(), image_out: Optional[np.ndarray] = None
                ) -> RenderOutput:
-        if opts.filter_mode != "parallel":
-            raise ValidationError("the B200 renderer implements FilterMode::parallel only")
         c = cam.to_c()
         p = self.params(filter, mode, opts)
         st = RenderStatsC()
@@ -784,6 +789,24 @@ class GpuScene:
         _check(self._lib.lodgs_gpu_read_image(self._h, _ptr(img)))
         return img
 
+    def read_image_rgb8(self, cam: Camera) -> np.ndarray:
+        """The last frame as 8-bit RGB (save_ppm quantisation, image.cpp:19-22)."""
+        img = np.empty((cam.height, cam.width, 3), np.uint8)
+        _check(self._lib.lodgs_gpu_read_image_rgb8(self._h, _ptr(img)))
+        return img
+
+    def set_reference_image(self) -> None:
+        """Keep the last frame on the device as the psnr/ssim reference."""
+        _check(self._lib.lodgs_gpu_set_reference_image(self._h))
+
+    def compare_reference(self, want_ssim: bool = True):
+        """(psnr, ssim) of the last frame against the stored reference, on the
+        device (metrics.cpp:121-192); ssim is None unless requested."""
+        p, q = C.c_double(0.0), C.c_double(0.0)
+        _check(self._lib.lodgs_gpu_compare_reference(self._h, C.byref(p),
+                                                     C.byref(q) if want_ssim else None))
+        return p.value, (q.value if want_ssim else None)
+
     # stage entry points
     def filter(self, cam: Camera, config: FilterConfig) -> FilterResult:
         if not (config.tau_r > 0):
@@ -869,6 +892,35 @@ def render(tree: LoDTree, cam: Camera, filter: FilterConfig, mode: ShrinkMode,
 def filter_parallel(tree: LoDTree, cam: Camera, config: FilterConfig) -> FilterResult:
     """filter.hpp:42-43 -- passes = barriers = 2."""
     return _scene_for(tree).filter(cam, config)
+
+
+def _image_array(img) -> np.ndarray:
+    a = img.rgb if isinstance(img, Image) else img
+    return np.ascontiguousarray(a, np.float32)
+
+
+def _metrics(a, b, want_psnr, want_ssim):
+    x, y = _image_array(a), _image_array(b)
+    if x.shape != y.shape or x.ndim != 3 or x.shape[2] != 3:
+        raise ValidationError("psnr: image dimensions differ" if want_psnr else
+                              "ssim: image dimensions differ")
+    h, w = x.shape[0], x.shape[1]
+    p, q = C.c_double(0.0), C.c_double(0.0)
+    _check(load_library().lodgs_gpu_image_metrics(_ptr(x), _ptr(y), w, h,
+                                                  C.byref(p) if want_psnr else None,
+                                                  C.byref(q) if want_ssim else None))
+    return p.value, q.value
+
+
+def psnr(a, b) -> float:
+    """metrics.hpp psnr (metrics.cpp:121-132) on the device; +inf if identical."""
+    return _metrics(a, b, True, False)[0]
+
+
+def ssim(a, b) -> float:
+    """metrics.hpp ssim (metrics.cpp:136-192): mean 11x11 Gaussian-window SSIM
+    over the three channels, on the device."""
+    return _metrics(a, b, False, True)[1]
 
 
 def filter_serial(tree: LoDTree, cam: Camera, config: FilterConfig) -> FilterResult:

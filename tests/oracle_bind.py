@@ -332,6 +332,8 @@ class Ref:
         lib.ref_view_gtc.argtypes = [P, P, C.c_uint64]
         lib.ref_psnr.restype = C.c_double
         lib.ref_psnr.argtypes = [P, P, C.c_int, C.c_int]
+        lib.ref_ssim.restype = C.c_double
+        lib.ref_ssim.argtypes = [P, P, C.c_int, C.c_int]
         self.lib = lib
 
     def err(self):
@@ -496,3 +498,10 @@ class Ref:
         a = np.ascontiguousarray(a, np.float32)
         b = np.ascontiguousarray(b, np.float32)
         return self.lib.ref_psnr(_p(a), _p(b), w, h)
+
+    def ssim(self, a, b):
+        h, w = a.shape[:2]
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        return self.lib.ref_ssim(_p(a), _p(b), w, h)
+
