@@ -184,6 +184,20 @@ LODGS_API int lodgs_build_synthetic_tree(const lodgs_synthetic_spec *spec, const
  * rasterizer.cpp:170) and uploads it to `device`.  The scene owns one CUDA
  * stream; calls on one scene are serialised by the caller. */
 LODGS_API int lodgs_gpu_scene_create(const lodgs_tree_view *tree, int device, lodgs_gpu_scene **out);
+/* load_scene (scene_io.cpp:213-226) of an LDGS v1 binary file straight into a
+ * device scene: the payload streams through pinned buffers to the device, where
+ * kernels de-interleave it (scene_io.cpp:90-116) and run validate_tree's
+ * per-node rules (scene.cpp:122-162) once.  Errors as the reference: IoError
+ * (cannot open) -> LODGS_ERR_IO; FormatError (bad magic, unsupported version,
+ * truncated ... reading <section>) and ValidationError -> LODGS_ERR_VALIDATION.
+ * JSON scenes are refused (load them on the host, then lodgs_gpu_scene_create).
+ * timing_ms (nullable, 3): read+H2D, de-interleave, validate+pack wall times. */
+LODGS_API int lodgs_gpu_scene_load(const char *path, int device, lodgs_gpu_scene **out,
+                         double *timing_ms);
+/* Shape of a device scene (for scenes loaded from files): node count, level
+ * begins (capacity cap), shrink factor; any output may be NULL. */
+LODGS_API int lodgs_gpu_scene_info(lodgs_gpu_scene *scene, uint64_t *n_nodes, uint32_t *n_levels,
+                         uint32_t *level_offsets, uint32_t cap, float *shrink_factor);
 LODGS_API int lodgs_gpu_scene_destroy(lodgs_gpu_scene *scene);
 /* The scene's cudaStream_t, for callers that time on it with CUDA events. */
 LODGS_API int lodgs_gpu_scene_stream(lodgs_gpu_scene *scene, void **stream);

@@ -137,6 +137,33 @@ int lodgs_gpu_scene_create(const lodgs_tree_view* tree, int device, lodgs_gpu_sc
     });
 }
 
+int lodgs_gpu_scene_load(const char* path, int device, lodgs_gpu_scene** out,
+                         double* timing_ms) {
+    return guarded([&] {
+        need(path, "path");
+        need(out, "out");
+        *out = nullptr;
+        auto* impl = new fgs::GpuScene(std::string(path), device, timing_ms);
+        *out = new lodgs_gpu_scene{impl};
+    });
+}
+
+int lodgs_gpu_scene_info(lodgs_gpu_scene* scene, uint64_t* n_nodes, uint32_t* n_levels,
+                         uint32_t* level_offsets, uint32_t cap, float* shrink_factor) {
+    return guarded([&] {
+        const auto& s = S(scene);
+        if (n_nodes) *n_nodes = s.n_nodes();
+        if (n_levels) *n_levels = uint32_t(s.n_levels());
+        if (shrink_factor) *shrink_factor = s.shrink_factor();
+        if (level_offsets) {
+            if (cap < uint32_t(s.n_levels()))
+                throw fgs::Error(LODGS_ERR_VALIDATION, "scene_info: capacity too small");
+            for (int l = 0; l < s.n_levels(); ++l)
+                level_offsets[l] = uint32_t(s.level_begin()[size_t(l)]);
+        }
+    });
+}
+
 int lodgs_gpu_scene_destroy(lodgs_gpu_scene* scene) {
     return guarded([&] {
         if (!scene) return;

@@ -16,6 +16,48 @@
 namespace fgs {
 
 // ------------------------------------------------------------ validation --
+bool validate_tree_header(const lodgs_tree_view& t, std::vector<std::string>& out,
+                          uint64_t& count) {
+    auto add = [&](const std::string& rule) {
+        ++count;
+        if (out.size() < 9) out.push_back("tree: " + rule);
+    };
+    const uint64_t n = t.n_nodes;
+    const float* ptrs[] = {t.mean_x, t.mean_y, t.mean_z, t.scale_x, t.scale_y,
+                           t.scale_z, t.quat_w, t.quat_x, t.quat_y, t.quat_z,
+                           t.opacity, t.color_r, t.color_g, t.color_b};
+    bool arrays_ok = true;
+    for (const float* p : ptrs) arrays_ok = arrays_ok && (p != nullptr || n == 0);
+    if (!arrays_ok || (n && (!t.parent || !t.leaf))) {
+        add("field arrays equal length");
+        return false;
+    }
+    if (!(t.shrink_factor > 0.0f && t.shrink_factor < 1.0f)) add("shrink_factor in (0,1)");
+    auto level_end = [&](uint32_t l) -> uint64_t {
+        return l + 1 < t.n_levels ? t.level_offsets[l + 1] : n;
+    };
+    bool offsets_ok = t.n_levels > 0 && t.level_offsets && t.level_offsets[0] == 0;
+    for (uint32_t l = 0; offsets_ok && l < t.n_levels; ++l)
+        offsets_ok = t.level_offsets[l] <= level_end(l) && level_end(l) <= n;
+    if (n > 0 && !offsets_ok) {
+        add("level_offsets monotone in [0, node_count]");
+        return false;
+    }
+    if (n == 0) {
+        if (t.n_levels != 0) add("level_offsets empty for empty tree");
+        return false;
+    }
+    return true;
+}
+
+const char* node_rule_name(int k) {
+    static const char* names[9] = {"all fields finite", "unit quaternion", "scale > 0",
+                                   "opacity in (0,1]", "color in [0,1]", "level-0 parent is ROOT",
+                                   "parent index in range", "parent level == level - 1",
+                                   "leaf iff childless"};
+    return (k >= 0 && k < 9) ? names[k] : "?";
+}
+
 std::vector<std::string> validate_tree(const lodgs_tree_view& t, uint64_t* n_violations) {
     std::vector<std::string> out;
     uint64_t count = 0;

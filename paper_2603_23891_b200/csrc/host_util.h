@@ -19,6 +19,13 @@ struct Error : std::runtime_error {
 };
 
 std::vector<std::string> validate_tree(const lodgs_tree_view& t, uint64_t* n_violations);
+// The tree-level rules of validate_tree (scene.cpp:93-116), with the same
+// messages; returns false when the per-node rules must not run (bad arrays,
+// bad level offsets, empty tree).  Per-node rules then run on the device.
+bool validate_tree_header(const lodgs_tree_view& t, std::vector<std::string>& out,
+                          uint64_t& count);
+// Message of per-node rule bit k (ingest.cu k_validate_nodes order).
+const char* node_rule_name(int k);
 std::vector<std::string> validate_camera(const lodgs_camera& c);
 std::string join_violations(const std::string& what, const std::vector<std::string>& v,
                             uint64_t total);

@@ -153,6 +153,20 @@ void launch_keys_to_triples(const uint32_t* offsets, int n_tiles, const unsigned
 void launch_gauss_counts(const GaussEmit* emit, const FrameCounters* cnt, uint64_t cap,
                          uint32_t* out, cudaStream_t s);
 
+// ---- scene ingest (scene.cpp:89-165, scene_io.cpp:90-116) ----
+// has_child (n bytes, scratch) then the per-node rule masks (9 bits, see
+// ingest.cu) and their total; level_begin: n_levels device words.
+void launch_validate_nodes(const float* soa, const uint32_t* parent, const uint8_t* leaf,
+                           uint8_t* has_child, uint64_t n, const uint64_t* level_begin,
+                           int n_levels, uint16_t* mask, unsigned long long* n_bad,
+                           cudaStream_t s);
+// LDGS v1 payload (after the 20-byte header) -> 14 float SoA arrays + parent + leaf
+void launch_deinterleave(const uint8_t* payload, uint64_t n, float* soa, uint32_t* parent,
+                         uint8_t* leaf, cudaStream_t s);
+// out2[0] = 1 + last non-leaf index (0 if none), out2[1] = bits of max |m|_1 (double)
+void launch_tree_extents(const float* soa, const uint8_t* leaf, uint64_t n,
+                         unsigned long long* out2, cudaStream_t s);
+
 // ---- image metrics + 8-bit output (metrics.cpp:121-195, image.cpp:12-28) ----
 constexpr int kMetricParts = 1184;  // per-CTA partial sums, summed in index order
 void launch_rgb8(const float* img, uint64_t n, uint8_t* out, cudaStream_t s);

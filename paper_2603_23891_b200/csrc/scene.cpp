@@ -9,6 +9,8 @@
 #include "scene.h"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -41,10 +43,7 @@ namespace {
 uint64_t align256(uint64_t b) { return (b + 255) / 256 * 256; }
 }  // namespace
 
-GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
-    uint64_t nv = 0;
-    const auto v = validate_tree(tree, &nv);
-    if (nv) throw Error(LODGS_ERR_VALIDATION, join_violations("invalid tree", v, nv));
+void GpuScene::init_device(int device) {
     int count = 0;
     FGS_CUDA(cudaGetDeviceCount(&count));
     if (device < 0 || device >= count)
@@ -56,56 +55,239 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
     for (auto& e : ev_) FGS_CUDA(cudaEventCreate(&e));
     FGS_CUDA(cudaMallocHost(&h_counters_, sizeof(FrameCounters)));
     std::memset(h_counters_, 0, sizeof(FrameCounters));
+}
 
+GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
+    // tree-level rules on the host (cheap), per-node rules on the device
+    std::vector<std::string> msgs;
+    uint64_t nv = 0;
+    const bool per_node = validate_tree_header(tree, msgs, nv);
+    if (!per_node && nv) throw Error(LODGS_ERR_VALIDATION, join_violations("invalid tree", msgs, nv));
+    init_device(device);
+    DeviceGuard dg(device_);
     const uint64_t n = tree.n_nodes;
+    IngestStage st;
+    st.soa.alloc(14 * n);
+    st.parent.alloc(n);
+    st.leaf.alloc(n);
+    const float* src[14] = {tree.mean_x, tree.mean_y, tree.mean_z, tree.scale_x,
+                            tree.scale_y, tree.scale_z, tree.quat_w, tree.quat_x,
+                            tree.quat_y, tree.quat_z, tree.opacity, tree.color_r,
+                            tree.color_g, tree.color_b};
+    if (n) {
+        for (int k = 0; k < 14; ++k)
+            FGS_CUDA(cudaMemcpyAsync(st.soa.p + k * n, src[k], n * 4, cudaMemcpyHostToDevice,
+                                     stream_));
+        FGS_CUDA(cudaMemcpyAsync(st.parent.p, tree.parent, n * 4, cudaMemcpyHostToDevice, stream_));
+        FGS_CUDA(cudaMemcpyAsync(st.leaf.p, tree.leaf, n, cudaMemcpyHostToDevice, stream_));
+    }
+    std::vector<uint64_t> lb;
+    for (uint32_t l = 0; l < tree.n_levels; ++l) lb.push_back(tree.level_offsets[l]);
+    shrink_factor_ = tree.shrink_factor;
+    ingest(n, lb, per_node, msgs, nv, st);
+}
+
+namespace {
+struct FileCloser {
+    FILE* f;
+    ~FileCloser() {
+        if (f) std::fclose(f);
+    }
+};
+}  // namespace
+
+GpuScene::GpuScene(const std::string& path, int device, double* timing_ms) : device_(device) {
+    using clock = std::chrono::steady_clock;
+    const auto t0 = clock::now();
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw Error(LODGS_ERR_IO, "cannot open for read: " + path);
+    FileCloser closer{f};
+    // scene_io.cpp:216-222: a leading '{' (after whitespace) is a JSON scene
+    int head = std::fgetc(f);
+    while (head == ' ' || head == '\t' || head == '\r' || head == '\n') head = std::fgetc(f);
+    if (head == EOF) throw Error(LODGS_ERR_VALIDATION, "bad magic");
+    if (head == '{')
+        throw Error(LODGS_ERR_VALIDATION,
+                    "JSON scene: the device loader reads LDGS v1 binary; load JSON on the host "
+                    "(scene_io.cpp:153-198) and create the scene from arrays");
+    std::fseek(f, 0, SEEK_SET);
+    std::fseek(f, 0, SEEK_END);
+    const uint64_t fsize = uint64_t(std::ftell(f));
+    std::fseek(f, 0, SEEK_SET);
+    // scene_io.cpp:90-116 header, with the reference's messages
+    auto rd = [&](void* p, size_t nb, const char* what) {
+        if (std::fread(p, 1, nb, f) != nb)
+            throw Error(LODGS_ERR_VALIDATION, std::string("truncated scene file reading ") + what);
+    };
+    char magic[4];
+    rd(magic, 4, "magic");
+    if (std::memcmp(magic, "LDGS", 4) != 0) throw Error(LODGS_ERR_VALIDATION, "bad magic");
+    uint32_t version = 0, n32 = 0, nl = 0;
+    float shrink = 0.f;
+    rd(&version, 4, "version");
+    if (version != 1)
+        throw Error(LODGS_ERR_VALIDATION, "unsupported version " + std::to_string(version));
+    rd(&n32, 4, "node count");
+    rd(&nl, 4, "level count");
+    rd(&shrink, 4, "shrink factor");
+    const uint64_t n = n32;
+    const struct { const char* what; uint64_t bytes; } sections[] = {
+        {"means", 12 * n}, {"scales", 12 * n}, {"quaternions", 16 * n}, {"opacity", 4 * n},
+        {"colors", 12 * n}, {"parents", 4 * n}, {"leaf flags", n}, {"level offsets", 4ull * nl}};
+    uint64_t off = 20;
+    for (const auto& sec : sections) {
+        if (fsize < off + sec.bytes)
+            throw Error(LODGS_ERR_VALIDATION,
+                        std::string("truncated scene file reading ") + sec.what);
+        off += sec.bytes;
+    }
+    const uint64_t payload = 61 * n;  // 14 floats + parent + leaf per node
+    std::vector<uint32_t> offs(nl);
+    std::fseek(f, long(20 + payload), SEEK_SET);
+    if (nl) rd(offs.data(), 4ull * nl, "level offsets");
+    std::fseek(f, 20, SEEK_SET);
+    // tree-level rules (scene.cpp:93-116); per-node rules run on the device
+    static const float dummy = 0.f;
+    static const uint32_t dummy_u = 0;
+    static const uint8_t dummy_b = 0;
+    lodgs_tree_view v{};
+    v.n_nodes = n;
+    v.mean_x = v.mean_y = v.mean_z = v.scale_x = v.scale_y = v.scale_z = &dummy;
+    v.quat_w = v.quat_x = v.quat_y = v.quat_z = v.opacity = &dummy;
+    v.color_r = v.color_g = v.color_b = &dummy;
+    v.parent = &dummy_u;
+    v.leaf = &dummy_b;
+    v.level_offsets = offs.data();
+    v.n_levels = nl;
+    v.shrink_factor = shrink;
+    std::vector<std::string> msgs;
+    uint64_t nv = 0;
+    const bool per_node = validate_tree_header(v, msgs, nv);
+    if (!per_node && nv) throw Error(LODGS_ERR_VALIDATION, join_violations("invalid tree", msgs, nv));
+    init_device(device);
+    DeviceGuard dg(device_);
+    // payload -> device through two pinned chunks (read of chunk k+1 overlaps the copy of k)
+    DevBuf<uint8_t> dpay;
+    dpay.alloc(payload);
+    constexpr uint64_t kChunk = 32ull << 20;
+    uint8_t* pin[2] = {nullptr, nullptr};
+    cudaEvent_t done[2];
+    for (int k = 0; k < 2; ++k) {
+        FGS_CUDA(cudaMallocHost(&pin[k], kChunk));
+        FGS_CUDA(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+    }
+    try {
+        uint64_t pos = 0;
+        int k = 0;
+        bool used[2] = {false, false};
+        while (pos < payload) {
+            const uint64_t nb = std::min<uint64_t>(kChunk, payload - pos);
+            if (used[k]) FGS_CUDA(cudaEventSynchronize(done[k]));
+            if (std::fread(pin[k], 1, nb, f) != nb)
+                throw Error(LODGS_ERR_IO, "read failed: " + path);
+            FGS_CUDA(cudaMemcpyAsync(dpay.p + pos, pin[k], nb, cudaMemcpyHostToDevice, stream_));
+            FGS_CUDA(cudaEventRecord(done[k], stream_));
+            used[k] = true;
+            pos += nb;
+            k ^= 1;
+        }
+        FGS_CUDA(cudaStreamSynchronize(stream_));
+    } catch (...) {
+        for (int k = 0; k < 2; ++k) {
+            cudaFreeHost(pin[k]);
+            cudaEventDestroy(done[k]);
+        }
+        throw;
+    }
+    for (int k = 0; k < 2; ++k) {
+        cudaFreeHost(pin[k]);
+        cudaEventDestroy(done[k]);
+    }
+    const auto t1 = clock::now();
+    IngestStage st;
+    st.soa.alloc(14 * n);
+    st.parent.alloc(n);
+    st.leaf.alloc(n);
+    launch_deinterleave(dpay.p, n, st.soa.p, st.parent.p, st.leaf.p, stream_);
+    FGS_CUDA(cudaGetLastError());
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    dpay.release();
+    const auto t2 = clock::now();
+    std::vector<uint64_t> lb(offs.begin(), offs.end());
+    shrink_factor_ = shrink;
+    ingest(n, lb, per_node, msgs, nv, st);
+    const auto t3 = clock::now();
+    if (timing_ms) {
+        auto ms = [](clock::time_point a, clock::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        timing_ms[0] = ms(t0, t1);
+        timing_ms[1] = ms(t1, t2);
+        timing_ms[2] = ms(t2, t3);
+    }
+}
+
+void GpuScene::ingest(uint64_t n, const std::vector<uint64_t>& level_begin, bool per_node,
+                      std::vector<std::string>& msgs, uint64_t nv, IngestStage& st) {
+    level_begin_ = level_begin;
+    if (per_node && n) {
+        // scene.cpp:118-162 on the device: one pass for has_child, one for the rules
+        DevBuf<uint8_t> has_child;
+        has_child.alloc(n);
+        DevBuf<uint16_t> mask;
+        mask.alloc(n);
+        DevBuf<uint64_t> dlb;
+        dlb.alloc(level_begin.size());
+        DevBuf<unsigned long long> bad;
+        bad.alloc(1);
+        FGS_CUDA(cudaMemcpyAsync(dlb.p, level_begin.data(), level_begin.size() * 8,
+                                 cudaMemcpyHostToDevice, stream_));
+        FGS_CUDA(cudaMemsetAsync(bad.p, 0, 8, stream_));
+        launch_validate_nodes(st.soa.p, st.parent.p, st.leaf.p, has_child.p, n, dlb.p,
+                              int(level_begin.size()), mask.p, bad.p, stream_);
+        FGS_CUDA(cudaGetLastError());
+        unsigned long long h_bad = 0;
+        FGS_CUDA(cudaMemcpyAsync(&h_bad, bad.p, 8, cudaMemcpyDeviceToHost, stream_));
+        FGS_CUDA(cudaStreamSynchronize(stream_));
+        if (h_bad) {  // error path: the first messages in (node, rule) order
+            std::vector<uint16_t> hm(n);
+            FGS_CUDA(cudaMemcpy(hm.data(), mask.p, n * 2, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < n && msgs.size() < 9; ++i)
+                for (int k = 0; k < 9 && msgs.size() < 9; ++k)
+                    if ((hm[i] >> k) & 1u)
+                        msgs.push_back("node " + std::to_string(i) + ": " + node_rule_name(k));
+            nv += h_bad;
+        }
+    }
+    if (nv) throw Error(LODGS_ERR_VALIDATION, join_violations("invalid tree", msgs, nv));
+
     // per-node arrays padded to 256 nodes: the filter's vector loads never run
     // past an allocation
     const uint64_t np = (n + 255) / 256 * 256;
     tree_.n = n;
-    for (uint32_t l = 0; l < tree.n_levels; ++l) level_begin_.push_back(tree.level_offsets[l]);
-    {
-        // first index of the all-leaf suffix, rounded up to 1024 nodes
-        uint64_t first = n;
-        while (first > 0 && tree.leaf[first - 1]) --first;
-        tree_.leaf_begin = std::min<uint64_t>(n, (first + 1023) / 1024 * 1024);
-    }
+    DevBuf<unsigned long long> ext;
+    ext.alloc(2);
+    launch_tree_extents(st.soa.p, st.leaf.p, n, ext.p, stream_);
+    unsigned long long h_ext[2] = {0, 0};
+    FGS_CUDA(cudaMemcpyAsync(h_ext, ext.p, 16, cudaMemcpyDeviceToHost, stream_));
+    FGS_CUDA(cudaStreamSynchronize(stream_));
+    // first index of the all-leaf suffix, rounded up to 1024 nodes
+    tree_.leaf_begin = std::min<uint64_t>(n, (h_ext[0] + 1023) / 1024 * 1024);
+    double max_l1 = 0.0;
+    std::memcpy(&max_l1, &h_ext[1], 8);
+    tree_.max_l1 = max_l1 * (1.0 + 0x1p-40);
     const uint64_t nb = tree_.leaf_begin;
-    {
-        double m = 0.0;
-        for (uint64_t i = 0; i < n; ++i) {
-            const double l1 = std::fabs(double(tree.mean_x[i])) + std::fabs(double(tree.mean_y[i])) +
-                              std::fabs(double(tree.mean_z[i]));
-            m = l1 > m ? l1 : m;
-        }
-        tree_.max_l1 = m * (1.0 + 0x1p-40);
-    }
     geo_.alloc(np);
     FGS_CUDA(cudaMemsetAsync(geo_.p, 0, geo_.bytes(), stream_));
     iscale_.alloc(nb);
     iquat_.alloc(nb);
     splat_.alloc(n);
-    {
-        DevBuf<float> stage;
-        stage.alloc(14 * n);
-        DevBuf<uint8_t> leaf;
-        leaf.alloc(n);
-        const float* src[14] = {tree.mean_x, tree.mean_y, tree.mean_z, tree.scale_x,
-                                tree.scale_y, tree.scale_z, tree.quat_w, tree.quat_x,
-                                tree.quat_y, tree.quat_z, tree.opacity, tree.color_r,
-                                tree.color_g, tree.color_b};
-        if (n) {
-            for (int k = 0; k < 14; ++k)
-                FGS_CUDA(cudaMemcpyAsync(stage.p + k * n, src[k], n * 4, cudaMemcpyHostToDevice,
-                                         stream_));
-            FGS_CUDA(cudaMemcpyAsync(leaf.p, tree.leaf, n, cudaMemcpyHostToDevice, stream_));
-        }
-        launch_pack_tree(stage.p, stage.p + 6 * n, leaf.p, n, nb, geo_.p, iscale_.p, iquat_.p,
-                         splat_.p, stream_);
-        FGS_CUDA(cudaStreamSynchronize(stream_));
-    }
+    launch_pack_tree(st.soa.p, st.soa.p + 6 * n, st.leaf.p, n, nb, geo_.p, iscale_.p, iquat_.p,
+                     splat_.p, stream_);
     parent_.alloc(np);
     FGS_CUDA(cudaMemsetAsync(parent_.p, 0xFF, np * 4, stream_));
-    if (n) FGS_CUDA(cudaMemcpyAsync(parent_.p, tree.parent, n * 4, cudaMemcpyHostToDevice, stream_));
+    if (n) FGS_CUDA(cudaMemcpyAsync(parent_.p, st.parent.p, n * 4, cudaMemcpyDeviceToDevice, stream_));
+    FGS_CUDA(cudaStreamSynchronize(stream_));
     tree_.geo = geo_.p;
     tree_.iscale = iscale_.p;
     tree_.iquat = iquat_.p;

@@ -54,9 +54,22 @@ struct ResolutionBuffers {
     DevBuf<float> image;
 };
 
+// Device staging of a tree before validation and packing: 14 float SoA
+// arrays (mean xyz, scale xyz, quat wxyz, opacity, colour rgb), parent, leaf.
+struct IngestStage {
+    DevBuf<float> soa;
+    DevBuf<uint32_t> parent;
+    DevBuf<uint8_t> leaf;
+};
+
 class GpuScene {
 public:
     GpuScene(const lodgs_tree_view& tree, int device);
+    // load_scene (scene_io.cpp:213-226) for LDGS v1 binary files, straight to the
+    // device: the payload streams through two pinned buffers into device memory,
+    // is de-interleaved and validated by kernels.  `timing_ms` (nullable, 3):
+    // read+H2D, de-interleave, validate+pack wall times.
+    GpuScene(const std::string& ldgs_path, int device, double* timing_ms);
     ~GpuScene();
 
     void reserve_pairs(uint64_t n);
@@ -114,7 +127,13 @@ public:
     int device() const { return device_; }
     uint64_t n_nodes() const { return tree_.n; }
 
+    float shrink_factor() const { return shrink_factor_; }
+    const std::vector<uint64_t>& level_begin() const { return level_begin_; }
+
 private:
+    void init_device(int device);
+    void ingest(uint64_t n, const std::vector<uint64_t>& level_begin, bool per_node,
+                std::vector<std::string>& msgs, uint64_t nv, IngestStage& st);
     void ensure_resolution(int w, int h);
     void build_readback_maps();
     void clear_frame_state();
@@ -124,6 +143,7 @@ private:
     cudaStream_t stream_ = nullptr;
     DevTree tree_;
     std::vector<uint64_t> level_begin_;  // scene.hpp:53 level_begin(l), host copy
+    float shrink_factor_ = 0.5f;
     DevBuf<unsigned> level_flag_;        // serial filter: level had an active node
     bool last_serial_ = false;
     // tree storage

@@ -175,7 +175,8 @@ ABI_SYMBOLS = (
     "lodgs_gpu_filter", "lodgs_gpu_filter_serial", "lodgs_gpu_mark", "lodgs_gpu_prepare", "lodgs_gpu_bin_to_tiles",
     "lodgs_gpu_sort_pairs", "lodgs_gpu_alpha_blend", "lodgs_gpu_host_alloc",
     "lodgs_gpu_host_free", "lodgs_gpu_read_image_rgb8", "lodgs_gpu_set_reference_image",
-    "lodgs_gpu_compare_reference", "lodgs_gpu_image_metrics",
+    "lodgs_gpu_compare_reference", "lodgs_gpu_image_metrics", "lodgs_gpu_scene_load",
+    "lodgs_gpu_scene_info",
 )
 
 _lib = None
@@ -234,6 +235,9 @@ def load_library():
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32)]),
         "lodgs_gpu_read_image_rgb8": (C.c_int, [P, P]),
+        "lodgs_gpu_scene_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(P), _DP]),
+        "lodgs_gpu_scene_info": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), P,
+                                           C.c_uint32, C.POINTER(C.c_float)]),
         "lodgs_gpu_set_reference_image": (C.c_int, [P]),
         "lodgs_gpu_compare_reference": (C.c_int, [P, _DP, _DP]),
         "lodgs_gpu_image_metrics": (C.c_int, [P, P, C.c_int, C.c_int, _DP, _DP]),
@@ -634,6 +638,18 @@ def make_tree(seed, depth, children=8, gamma=0.5, nx=3, ny=3, congestion=1) -> L
 # ------------------------------------------------------------ GPU scene --
 
 
+class _TreeShape:
+    """Shape of a tree that lives only on the device (GpuScene.load)."""
+
+    def __init__(self, n, level_offsets, shrink_factor):
+        self._n = int(n)
+        self.level_offsets = level_offsets
+        self.shrink_factor = shrink_factor
+
+    def node_count(self) -> int:
+        return self._n
+
+
 class GpuScene:
     """Device-resident copy of one LoDTree (validated once at upload)."""
 
@@ -644,6 +660,27 @@ class GpuScene:
         self._h = C.c_void_p(None)
         v = tree.view()
         _check(self._lib.lodgs_gpu_scene_create(C.byref(v), int(device), C.byref(self._h)))
+
+    @classmethod
+    def load(cls, path: str, device: int = 0, timing_ms=None) -> "GpuScene":
+        """load_scene (scene_io.cpp:213-226) of an LDGS v1 binary file straight to
+        the device (de-interleave + validate_tree on the GPU).  timing_ms: optional
+        float64 array of 3 (read+H2D, de-interleave, validate+pack ms)."""
+        self = cls.__new__(cls)
+        self._lib = load_library()
+        self.device = device
+        self._h = C.c_void_p(None)
+        tm = None
+        if timing_ms is not None:
+            assert timing_ms.dtype == np.float64 and timing_ms.size >= 3
+            tm = timing_ms.ctypes.data_as(_DP)
+        _check(self._lib.lodgs_gpu_scene_load(os.fsencode(path), int(device), C.byref(self._h), tm))
+        n, nl, sf = C.c_uint64(0), C.c_uint32(0), C.c_float(0.0)
+        _check(self._lib.lodgs_gpu_scene_info(self._h, C.byref(n), C.byref(nl), None, 0, C.byref(sf)))
+        offs = np.zeros(max(1, nl.value), np.uint32)
+        _check(self._lib.lodgs_gpu_scene_info(self._h, None, None, _ptr(offs), nl.value, None))
+        self.tree = _TreeShape(n.value, offs[: nl.value].copy(), sf.value)
+        return self
 
     def close(self):
         if self._h and self._h.value:

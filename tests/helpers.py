@@ -7,6 +7,7 @@ test_util.hpp:19-77).
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -89,3 +90,36 @@ def topdown_camera(width, height, focal, altitude, x=0.0, y=0.0):
 
 def max_abs(a, b):
     return float(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64)).max()) if np.size(a) else 0.0
+
+
+def write_ldgs(tree, path):
+    """save_binary (scene_io.cpp:55-84) restated: LDGS v1 little-endian --
+    magic, version 1, node count, level count, shrink factor, then the
+    interleaved means / scales / quaternions, opacity, interleaved colours,
+    parents, leaf flags, level offsets."""
+    n = tree.node_count()
+    with open(path, "wb") as f:
+        f.write(b"LDGS")
+        f.write(np.array([1, n, len(tree.level_offsets)], np.uint32).tobytes())
+        f.write(np.float32(tree.shrink_factor).tobytes())
+        for fields in ((tree.mean_x, tree.mean_y, tree.mean_z),
+                       (tree.scale_x, tree.scale_y, tree.scale_z),
+                       (tree.quat_w, tree.quat_x, tree.quat_y, tree.quat_z),
+                       (tree.opacity,),
+                       (tree.color_r, tree.color_g, tree.color_b)):
+            f.write(np.stack([np.asarray(a, np.float32) for a in fields], axis=1).tobytes())
+        f.write(np.asarray(tree.parent, np.uint32).tobytes())
+        f.write(np.asarray(tree.leaf, np.uint8).tobytes())
+        f.write(np.asarray(tree.level_offsets, np.uint32).tobytes())
+
+
+REF_LDGS_TOOL = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                             "oracle", "_ref", "ref_ldgs_tool")
+
+
+def ref_ldgs(*args):
+    """Runs the reference's save_scene / load_scene natively (oracle/ref_ldgs_tool.cpp)."""
+    import subprocess
+
+    return subprocess.run([REF_LDGS_TOOL, *map(str, args)], capture_output=True, text=True,
+                          check=True).stdout.strip()

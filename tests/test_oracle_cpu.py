@@ -380,3 +380,23 @@ def test_render_rejects_bad_tau(L):
     for bad in (0.0, 1.0):
         with pytest.raises(L.ValidationError):
             L.render(t, cam, L.FilterConfig(3.0), L.ShrinkMode.adaptive(bad))
+
+
+# ------------------------------------------------------- LDGS scene files --
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "ref_ldgs_tool")),
+                    reason="oracle/_ref not built")
+def test_ldgs_writer_matches_reference_save_scene(L, tmp_path):
+    """tests/helpers.write_ldgs (the restated save_binary) writes the bytes the
+    reference's save_scene writes (scene_io.cpp:55-84), and the reference
+    loads them back."""
+    from helpers import ref_ldgs, write_ldgs
+
+    for nx, ny, seed, depth, bseed in ((5, 5, 1, 3, 7), (3, 4, 9, 2, 1), (2, 2, 3, 4, 5)):
+        ref_path = tmp_path / f"ref_{nx}_{depth}.ldgs"
+        assert ref_ldgs("save", ref_path, nx, ny, seed, depth, bseed) == "SAVED"
+        tree = L.build_synthetic_tree(nx=nx, ny=ny, seed=seed, depth=depth, build_seed=bseed)
+        mine = tmp_path / f"mine_{nx}_{depth}.ldgs"
+        write_ldgs(tree, mine)
+        assert mine.read_bytes() == ref_path.read_bytes()
+        ok, n, levels, _ = ref_ldgs("load", mine).split()
+        assert ok == "OK" and int(n) == tree.node_count() and int(levels) == len(tree.level_offsets)
