@@ -113,6 +113,23 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def filter_traffic_bytes():
+    """DRAM bytes (read + write) of the four filter kernels for one altitude-200
+    frame, from the committed ncu --set full summary (tools/ncu_summary.py)."""
+    path = os.path.join(ROOT, "profiles", "r1_ncu_filter_alt200.txt")
+    try:
+        tot, seen = 0.0, set()
+        for line in open(path):
+            f = line.split()
+            if f and f[0] in ("k_mark_internal", "k_select_internal", "k_filter_leaves",
+                              "k_compact") and f[0] not in seen:
+                seen.add(f[0])
+                tot += (float(f[2]) + float(f[3])) * 1e6
+        return (tot if len(seen) == 4 else None), os.path.relpath(path, ROOT)
+    except OSError:
+        return None, None
+
+
 def measured_peak_gbs():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -295,6 +312,7 @@ def run_b200(args, rank, world, local):
     per_stage = {k: round(stage_ms[i] / max(1, pf), 5) for i, k in enumerate(stage_names)}
     dominant = max(range(5), key=lambda i: stage_ms[i])
     filt_gbs = filt_bytes / (filt_ms * 1e-3) / 1e9
+    traffic, traffic_src = filter_traffic_bytes()
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True,
@@ -309,7 +327,10 @@ def run_b200(args, rank, world, local):
         "roofline": {"kernel": "filter (k_mark_internal + k_select_internal + "
                                 "k_filter_leaves + k_compact)", "bound": "hbm",
                      "achieved": filt_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": filt_gbs / peak, "traffic": None,
+                     "frac": filt_gbs / peak, "traffic": traffic,
+                     "traffic_source": f"ncu --set full dram__bytes_read+write, one altitude-200 "
+                                       f"frame ({traffic_src}); the leaf pass never fetches leaves "
+                                       f"under blocked parents, so traffic < algorithmic bytes",
                      "algorithmic_bytes_per_frame": filt_bytes,
                      "dominant_stage": stage_names[dominant]},
         "sort": {"achieved_gbs": sort_bytes / (sort_ms * 1e-3) / 1e9 if sort_ms > 0 else None,
