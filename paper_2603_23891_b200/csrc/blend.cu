@@ -76,12 +76,73 @@ constexpr int kFastThreads = 128;  // fast kernel: one CTA per 16x8 half tile
 constexpr int kFastWarps = kFastThreads / 32;
 constexpr int kFastParts = kTile * kTile / kFastThreads;
 
+// A batch's hits, compacted in pair order: 12 floats per hit.
 struct WarpStage {
-    float4 geo[32];  // block-relative mean x, y, ha, hc
-    float2 ct[32];   // cb, ethr
-    float4 col[32];  // op, r, g, b
+    float4 geo[32];  // block-relative mean x, y, ha, hc   (log2e-scaled conic)
+    float4 ct[32];   // cb, ethr, op, r
+    float2 gb[32];   // g, b
     uint32_t gid[32];
 };
+
+// One sample of the fast path: e (log2 units) from the staged hit, the
+// certified skip test, alpha and the branch-free blend; T == 0 marks a
+// terminated pixel (every later w is 0).  `unsure` accumulates |d| <= margin:
+// the FP32 decision might differ from the reference's FP64 one.
+struct PixState {
+    float T, cr, cg, cb;
+};
+
+__device__ __forceinline__ void blend_sample_fast(const WarpStage& st, int k, float pxl,
+                                                  float pyl, PixState& p, bool& unsure) {
+    const float4 geo = st.geo[k];
+    const float4 ct = st.ct[k];
+    const float2 gb = st.gb[k];
+    const float dx = pxl - geo.x, dy = pyl - geo.y;
+    const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
+    const float ev = __fmaf_rn(ct.x * dx, dy, Q);
+    const float d = ev - ct.y;
+    // certified: |e32 - e| is a few ulp of Q (+ the rounding of ethr)
+    const float margin = __fmaf_rn(Q, 7.62939453125e-06f, 1.1007e-05f);  // (Q + log2 e) 2^-17
+    unsure = unsure || fabsf(d) <= margin;
+    const float ev_take = d < -margin ? ev : INFINITY;  // skipped: 2^-inf = 0
+    const float alpha = fminf(ct.z * ex2_approx(-ev_take), 0.99f);
+    const float w = alpha * p.T;
+    p.cr = __fmaf_rn(ct.w, w, p.cr);
+    p.cg = __fmaf_rn(gb.x, w, p.cg);
+    p.cb = __fmaf_rn(gb.y, w, p.cb);
+    const float t = p.T - w;
+    p.T = t < 1e-4f ? 0.0f : t;
+}
+
+// The same sample with the reference's FP64 decision wherever the FP32 one is
+// uncertain (used only to re-run a batch in which some lane was unsure).
+__device__ __forceinline__ void blend_sample_checked(const WarpStage& st, int k, float pxl,
+                                                     float pyl, double px, double py,
+                                                     const Gauss64* __restrict__ g64,
+                                                     PixState& p) {
+    const float4 geo = st.geo[k];
+    const float4 ct = st.ct[k];
+    const float2 gb = st.gb[k];
+    const float dx = pxl - geo.x, dy = pyl - geo.y;
+    const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
+    const float ev = __fmaf_rn(ct.x * dx, dy, Q);
+    const float d = ev - ct.y;
+    const float margin = __fmaf_rn(Q, 7.62939453125e-06f, 1.1007e-05f);
+    bool take = d < -margin;
+    float alpha = fminf(ct.z * ex2_approx(-ev), 0.99f);
+    if (fabsf(d) <= margin && p.T > 0.0f) {
+        const Gauss64& G = g64[st.gid[k]];
+        const double a64 = alpha_exact(G.mx, G.my, G.ca, G.cb, G.cc, G.op, px, py);
+        take = a64 >= kMinAlpha;
+        alpha = float(a64);
+    }
+    const float w = take ? alpha * p.T : 0.0f;
+    p.cr = __fmaf_rn(ct.w, w, p.cr);
+    p.cg = __fmaf_rn(gb.x, w, p.cg);
+    p.cb = __fmaf_rn(gb.y, w, p.cb);
+    const float t = p.T - w;
+    p.T = t < 1e-4f ? 0.0f : t;
+}
 
 __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
@@ -102,9 +163,9 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
 
     const float pxl = float(lane & 7) + 0.5f, pyl = float(lane >> 3) + 0.5f;
     const double px = double(x) + 0.5, py = double(y) + 0.5;
-    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-    bool done = !inside;
-    if (__all_sync(0xffffffffu, done)) return;
+    PixState pix{inside ? 1.0f : 0.0f, 0.0f, 0.0f, 0.0f};  // T == 0: nothing to do
+    if (__all_sync(0xffffffffu, !inside)) return;
+    const unsigned lt = (1u << lane) - 1u;
 
     // Software pipeline over 32-splat batches: keys are fetched two batches
     // ahead and splat records one batch ahead, so the dependent key -> record
@@ -130,57 +191,45 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
     Rec cur, nxt;
     load_rec(gi_cur, cur);
     for (uint32_t base = b; base < e; base += 32) {
-        // ---- stage the splats of this batch that touch this warp's block
+        // ---- stage the splats of this batch that touch this warp's block,
+        //      compacted in pair order
         bool hit = false;
+        float mlx = 0.f, mly = 0.f;
         if (gi_cur != kNone) {
-            const float mlx = float(cur.m.x - double(bx)), mly = float(cur.m.y - double(by));
+            mlx = float(cur.m.x - double(bx));
+            mly = float(cur.m.y - double(by));
             // pixel centres of the block span [0.5, 7.5] x [0.5, 3.5]
             const float2 h = cur.h;
             hit = h.x >= 0.0f && mlx - h.x <= 7.5f && mlx + h.x >= 0.5f && mly - h.y <= 3.5f &&
                   mly + h.y >= 0.5f;
-            if (hit) {
-                st.geo[lane] = make_float4(mlx, mly, cur.q0.x, cur.q0.z);
-                st.ct[lane] = make_float2(cur.q0.y, cur.q0.w);
-                st.col[lane] = cur.col;
-                st.gid[lane] = gi_cur;
-            }
         }
-        unsigned bits = __ballot_sync(0xffffffffu, hit);
+        const unsigned bits = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+            const int slot = __popc(bits & lt);
+            st.geo[slot] = make_float4(mlx, mly, cur.q0.x, cur.q0.z);
+            st.ct[slot] = make_float4(cur.q0.y, cur.q0.w, cur.col.x, cur.col.y);
+            st.gb[slot] = make_float2(cur.col.z, cur.col.w);
+            st.gid[slot] = gi_cur;
+        }
         __syncwarp();
         // ---- prefetch: records of the next batch, keys of the one after
         const uint32_t gi_after = load_key(base + 64);
         load_rec(gi_next, nxt);
-        // ---- blend them front to back
-        while (bits) {
-            const int j = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const float4 geo = st.geo[j];
-            const float2 ct = st.ct[j];
-            const float dx = pxl - geo.x, dy = pyl - geo.y;
-            const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
-            const float ev = __fmaf_rn(ct.x * dx, dy, Q);
-            const float d = ev - ct.y;
-            const float margin = __fmaf_rn(Q, 7.62939453125e-06f, 7.62939453125e-06f);
-            const float4 col = st.col[j];
-            float alpha = fminf(col.x * ex2_approx(ev * -1.4426950408889634f), 0.99f);
-            bool take = d < -margin;
-            const bool unsure = !done && fabsf(d) <= margin;
-            if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decision
-                if (unsure) {
-                    const Gauss64& G = g64[st.gid[j]];
-                    const double a64 = alpha_exact(G.mx, G.my, G.ca, G.cb, G.cc, G.op, px, py);
-                    take = a64 >= kMinAlpha;
-                    alpha = float(a64);
-                }
-            }
-            const float w = (take && !done) ? alpha * T : 0.0f;
-            cr = __fmaf_rn(col.y, w, cr);
-            cg = __fmaf_rn(col.z, w, cg);
-            cb = __fmaf_rn(col.w, w, cb);
-            T = T - w;
-            done = done || T < 1e-4f;
+        // ---- blend them front to back (FP32; re-run exactly if any lane was unsure)
+        const int nh = __popc(bits);
+        const PixState saved = pix;
+        bool unsure = false;
+        int k = 0;
+        for (; k + 2 <= nh; k += 2) {
+            blend_sample_fast(st, k, pxl, pyl, pix, unsure);
+            blend_sample_fast(st, k + 1, pxl, pyl, pix, unsure);
         }
-        if (__all_sync(0xffffffffu, done)) break;
+        if (k < nh) blend_sample_fast(st, k, pxl, pyl, pix, unsure);
+        if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
+            pix = saved;
+            for (int j = 0; j < nh; ++j) blend_sample_checked(st, j, pxl, pyl, px, py, g64, pix);
+        }
+        if (__all_sync(0xffffffffu, pix.T == 0.0f)) break;
         __syncwarp();
         gi_cur = gi_next;
         gi_next = gi_after;
@@ -188,9 +237,9 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
     }
     if (inside) {
         float* o = image + (size_t(y) * width + x) * 3;
-        o[0] = cr;
-        o[1] = cg;
-        o[2] = cb;
+        o[0] = pix.cr;
+        o[1] = pix.cg;
+        o[2] = pix.cb;
     }
 }
 

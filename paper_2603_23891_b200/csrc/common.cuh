@@ -53,8 +53,9 @@ struct __align__(16) GaussCol64 {
 };
 
 // Per projected gaussian, FP32 blend record (48 bytes).
-//   e(dx,dy) = ha*dx^2 + cb*dx*dy + hc*dy^2 = -power; sample skipped iff
-//   e > ethr = ln(255 * opacity) (alpha < 1/255, kernels.hpp:21).
+//   e(dx,dy) = ha*dx^2 + cb*dx*dy + hc*dy^2 = -power * log2(e) (coefficients
+//   pre-scaled by log2(e)); sample skipped iff e > ethr = log2(255 * opacity)
+//   (alpha < 1/255, kernels.hpp:21); alpha = min(op * 2^-e, 0.99).
 //   (hx, hy): half-extents of the e <= ethr ellipse, computed in FP64 and
 //   rounded outward -- a conservative box outside which the reference
 //   provably skips every sample (blend.cu uses it to cull per warp).

@@ -106,11 +106,14 @@ __device__ __forceinline__ uint32_t rect_count(const GaussEmit& e) {
 __device__ __forceinline__ Gauss32 make_g32(double ca, double cb, double cc, double op, double r,
                                             double gg, double b) {
     Gauss32 o;
-    o.ha = float(0.5 * ca);
-    o.cb = float(cb);
-    o.hc = float(0.5 * cc);
+    // exponent coefficients pre-scaled by log2(e): the blend evaluates
+    // e' = e log2(e) and alpha = op * 2^-e' with one MUFU.EX2
+    constexpr double kLog2e = 1.4426950408889634074;
+    o.ha = float(0.5 * ca * kLog2e);
+    o.cb = float(cb * kLog2e);
+    o.hc = float(0.5 * cc * kLog2e);
     const double ethr = log(255.0 * op);
-    o.ethr = float(ethr);
+    o.ethr = float(ethr * kLog2e);
     o.op = float(op);
     o.r = float(r);
     o.g = float(gg);
