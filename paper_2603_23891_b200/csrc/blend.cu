@@ -144,7 +144,13 @@ __device__ __forceinline__ void blend_sample_checked(const WarpStage& st, int k,
     p.T = t < 1e-4f ? 0.0f : t;
 }
 
-__global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
+#ifndef BLEND_PREFETCH2
+#define BLEND_PREFETCH2 0
+#endif
+#ifndef BLEND_MIN_CTAS
+#define BLEND_MIN_CTAS 8
+#endif
+__global__ void __launch_bounds__(kFastThreads, BLEND_MIN_CTAS) k_blend_fast(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
     const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
     const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
@@ -187,9 +193,16 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
             r.h = *reinterpret_cast<const float2*>(&g32[gi].hx);
         }
     };
+#if BLEND_PREFETCH2
+    uint32_t gi_cur = load_key(b), gi_next = load_key(b + 32), gi_n2 = load_key(b + 64);
+    Rec cur, nxt, nx2;
+    load_rec(gi_cur, cur);
+    load_rec(gi_next, nxt);
+#else
     uint32_t gi_cur = load_key(b), gi_next = load_key(b + 32);
     Rec cur, nxt;
     load_rec(gi_cur, cur);
+#endif
     for (uint32_t base = b; base < e; base += 32) {
         // ---- stage the splats of this batch that touch this warp's block,
         //      compacted in pair order
@@ -212,9 +225,15 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
             st.gid[slot] = gi_cur;
         }
         __syncwarp();
+#if BLEND_PREFETCH2
+        // ---- prefetch: records two batches ahead, keys three ahead
+        const uint32_t gi_after = load_key(base + 96);
+        load_rec(gi_n2, nx2);
+#else
         // ---- prefetch: records of the next batch, keys of the one after
         const uint32_t gi_after = load_key(base + 64);
         load_rec(gi_next, nxt);
+#endif
         // ---- blend them front to back (FP32; re-run exactly if any lane was unsure)
         const int nh = __popc(bits);
         const PixState saved = pix;
@@ -231,9 +250,17 @@ __global__ void __launch_bounds__(kFastThreads, 8) k_blend_fast(
         }
         if (__all_sync(0xffffffffu, pix.T == 0.0f)) break;
         __syncwarp();
+#if BLEND_PREFETCH2
+        gi_cur = gi_next;
+        gi_next = gi_n2;
+        gi_n2 = gi_after;
+        cur = nxt;
+        nxt = nx2;
+#else
         gi_cur = gi_next;
         gi_next = gi_after;
         cur = nxt;
+#endif
     }
     if (inside) {
         float* o = image + (size_t(y) * width + x) * 3;

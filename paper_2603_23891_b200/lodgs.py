@@ -28,6 +28,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "liblodgs_b200.so")
+# experiment builds (tools/variants.sh) may point elsewhere; the product default is _lib/
+LIB_PATH = os.environ.get("LODGS_B200_LIB", LIB_PATH)
 
 ROOT_PARENT = 0xFFFFFFFF  # core.hpp:15
 TILE = 16  # tiles.hpp:8-9
