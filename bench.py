@@ -130,6 +130,32 @@ def filter_traffic_bytes():
         return None, None
 
 
+def ncu_kernel_row(kernel, fname="r1_ncu_render_alt200.txt"):
+    """One kernel's row of a committed ncu --set full summary (tools/ncu_summary.py)."""
+    path = os.path.join(ROOT, "profiles", fname)
+    try:
+        lines = open(path).read().splitlines()
+        hdr = next(ln.split() for ln in lines if ln.startswith("kernel"))
+        for ln in lines:
+            f = ln.split()
+            if f and f[0] == kernel:
+                return {h: float(v) for h, v in zip(hdr[1:], f[1:])}, os.path.relpath(path, ROOT)
+    except (OSError, StopIteration, ValueError):
+        pass
+    return None, None
+
+
+def blend_evidence():
+    """The dominant kernel is issue-bound (no dense contraction, no HBM roofline):
+    its SM issue utilisation from the committed ncu capture (altitude 200)."""
+    row, src = ncu_kernel_row("k_blend_fast")
+    if not row:
+        return None
+    return {"kernel": "k_blend_fast", "bound": "issue", "issue_slots_busy_pct": row.get("issue%"),
+            "sm_throughput_pct": row.get("sm%"), "achieved_occupancy_pct": row.get("occ%"),
+            "ncu_us_alt200": row.get("us"), "source": src}
+
+
 def measured_peak_gbs():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -237,7 +263,7 @@ def run_b200(args, rank, world, local):
         ev1.record(stream)
         ev1.synchronize()
         ms = ev0.elapsed_time(ev1)
-        tot = scene.take_totals()
+        tot = scene.take_totals(sort_bytes=True)
         prof = scene.profile_read() if profile else None
         if profile:
             scene.profile(False)
@@ -250,7 +276,7 @@ def run_b200(args, rank, world, local):
     with ClockSampler(local) as clocks:
         for attempt in range(3):
             try:
-                ms, (nf, sum_sel, sum_pairs), _ = device_loop(timed)
+                ms, (nf, sum_sel, sum_pairs, sum_sort_bytes), _ = device_loop(timed)
                 break
             except L.InternalError:
                 continue  # pair buffer grew; re-run the timed region
@@ -307,7 +333,9 @@ def run_b200(args, rank, world, local):
     filt_ms = (stage_ms[0] + stage_ms[1]) / max(1, pf)
     mark_ms = stage_ms[0] / max(1, pf)
     sort_ms = stage_ms[3] / max(1, pf)
-    sort_bytes = 16 * mean_pairs  # read + write of each 8-byte key
+    # the reference LSD radix's bytes, (24 x non-uniform 8-bit digits
+    # + 8) per pair, counted per frame on the device from the frame's keys
+    sort_bytes = sum_sort_bytes / max(1, nf)
     stage_names = ["filter_internal", "filter_leaves_compact", "preprocess_keys", "tile_sort", "blend"]
     per_stage = {k: round(stage_ms[i] / max(1, pf), 5) for i, k in enumerate(stage_names)}
     dominant = max(range(5), key=lambda i: stage_ms[i])
@@ -333,8 +361,15 @@ def run_b200(args, rank, world, local):
                                        f"under blocked parents, so traffic < algorithmic bytes",
                      "algorithmic_bytes_per_frame": filt_bytes,
                      "dominant_stage": stage_names[dominant]},
-        "sort": {"achieved_gbs": sort_bytes / (sort_ms * 1e-3) / 1e9 if sort_ms > 0 else None,
-                 "bytes_per_frame": sort_bytes},
+        "sort": {"kernel": "k_tile_sort + k_tile_sort_big (per-tile register bitonic on "
+                           "(depth, slot) after the counting tile digit)", "bound": "hbm",
+                 "achieved_gbs": sort_bytes / (sort_ms * 1e-3) / 1e9 if sort_ms > 0 else None,
+                 "frac": (sort_bytes / (sort_ms * 1e-3) / 1e9) / peak if sort_ms > 0 else None,
+                 "peak_gbs": peak, "algorithmic_bytes_per_frame": sort_bytes,
+                 "bytes_definition": "SURVEY 8(d): (24 B x non-uniform 8-bit digits of the "
+                                     "reference key tile<<32|depth + 8 B) per pair",
+                 "device_traffic_per_frame": 16 * mean_pairs},
+        "blend": blend_evidence(),
         "e2e": {"value": e2e_fps, "unit": "frames/s",
                 "h2d_bytes_per_step": C.sizeof(L.CameraC) + C.sizeof(L.RenderParamsC),
                 "d2h_bytes_per_step": img_bytes + 64, "frames": len(e2e_frames),

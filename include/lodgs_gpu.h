@@ -232,9 +232,11 @@ LODGS_API int lodgs_gpu_render_async(lodgs_gpu_scene *scene, const lodgs_camera 
                            const lodgs_render_params *params, float *image_host);
 /* Waits for the scene stream; stats (nullable) = the last frame's. */
 LODGS_API int lodgs_gpu_sync(lodgs_gpu_scene *scene, lodgs_render_stats *stats);
-/* Sum of n_selected / n_pairs over frames since the last call (device counters). */
+/* Sum of n_selected / n_pairs over frames since the last call (device counters);
+ * sum_sort_bytes (nullable): the SURVEY 8(d) radix-sort bytes of those frames,
+ * (24 B x non-uniform 8-bit digits of the reference key + 8 B) per pair. */
 LODGS_API int lodgs_gpu_take_totals(lodgs_gpu_scene *scene, uint64_t *frames, uint64_t *sum_selected,
-                          uint64_t *sum_pairs);
+                          uint64_t *sum_pairs, uint64_t *sum_sort_bytes);
 
 /* Per-stage CUDA-event profiling of every enqueued frame, without host sync.
  * enable=1 starts (and clears) collection, enable=0 stops it.  read() syncs

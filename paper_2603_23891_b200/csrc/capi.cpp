@@ -224,9 +224,11 @@ int lodgs_gpu_sync(lodgs_gpu_scene* scene, lodgs_render_stats* stats) {
 }
 
 int lodgs_gpu_take_totals(lodgs_gpu_scene* scene, uint64_t* frames, uint64_t* sum_selected,
-                          uint64_t* sum_pairs) {
-    return guarded([&] { S(scene).take_totals(frames, sum_selected, sum_pairs); });
+                          uint64_t* sum_pairs, uint64_t* sum_sort_bytes) {
+    return guarded(
+        [&] { S(scene).take_totals(frames, sum_selected, sum_pairs, sum_sort_bytes); });
 }
+
 
 int lodgs_gpu_profile(lodgs_gpu_scene* scene, int enable) {
     return guarded([&] { S(scene).profile(enable != 0); });

@@ -85,6 +85,9 @@ struct FrameCounters {
     unsigned int nonfinite;    // project() produced a non-finite value
     unsigned int big_cursor;
     unsigned int serial_passes;  // filter_serial: levels with an active node
+    // OR and OR-of-complement of every reference sort key (tile << 32 | depth bits,
+    // rasterizer.cpp:111-115): digit d needs an LSD pass iff it is not uniform
+    unsigned long long key_or, key_nand;
 };
 
 // Running totals across frames (not cleared per frame).
@@ -93,6 +96,9 @@ struct RunTotals {
     unsigned long long sum_selected;
     unsigned long long sum_pairs;
     unsigned long long pad;
+    // sum over frames of SURVEY 8(d)'s radix-sort bytes (24 B per pair per
+    // non-uniform 8-bit digit + 8 B per pair for the histogram)
+    unsigned long long sum_sort_bytes;
 };
 
 #ifdef __CUDACC__

@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
         for (int t = threadIdx.x; t < n_tiles; t += kPrepBlock) s_hist[t] = 0u;
     __syncthreads();
     uint32_t kept = 0, pairs = 0;
+    unsigned long long kor = 0, knand = 0;
     for (uint64_t s = lo + threadIdx.x; s < hi; s += kPrepBlock) {
         const uint32_t idx = __ldg(selected + s);
         const float4* src = reinterpret_cast<const float4*>(splat + idx);
@@ -224,10 +225,15 @@ __global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
             pairs += rect_count(e);
             for (int ty = e.ty0; ty <= e.ty1; ++ty)
                 for (int tx = e.tx0; tx <= e.tx1; ++tx) {
+                    const unsigned tile = unsigned(ty * tiles_x + tx);
+                    const unsigned long long key =
+                        (unsigned long long)tile << 32 | e.depth_bits;
+                    kor |= key;
+                    knand |= ~key;
                     if (use_hist)
-                        atomicAdd(s_hist + (ty * tiles_x + tx), 1u);
+                        atomicAdd(s_hist + tile, 1u);
                     else
-                        atomicAdd(out.tile_count + (ty * tiles_x + tx), 1u);
+                        atomicAdd(out.tile_count + tile, 1u);
                 }
         } else {
             e.depth_bits = 0;
@@ -239,6 +245,15 @@ __global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
         out.emit[s] = e;
     }
     block_add2(kept, pairs, &cnt->n_gaussians, &cnt->n_pairs);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        kor |= __shfl_xor_sync(0xffffffffu, kor, off);
+        knand |= __shfl_xor_sync(0xffffffffu, knand, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (kor) atomicOr(&cnt->key_or, kor);
+        if (knand) atomicOr(&cnt->key_nand, knand);
+    }
     if (use_hist) {
         __syncthreads();
         for (int t = threadIdx.x; t < n_tiles; t += kPrepBlock) {
@@ -264,6 +279,19 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
 // schedule for the per-tile grids, and (optionally) the running totals.
 // Thread k owns the contiguous tiles [k*per, (k+1)*per): a serial sum, one
 // block scan, a serial write-back.
+// SURVEY.md 8(d) sort bytes of the reference's LSD radix (rasterizer.cpp:
+// 100-135): 24 B per pair for every 8-bit digit that is not uniform across
+// the frame's keys (uniform digits are skipped, :117), plus 8 B per pair for
+// the histogram pass.
+__device__ __forceinline__ unsigned long long sort_bytes(const FrameCounters* cnt,
+                                                         unsigned long long n_pairs) {
+    const unsigned long long diff = cnt->key_or & cnt->key_nand;  // bits that differ
+    int passes = 0;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) passes += ((diff >> (8 * d)) & 0xffull) ? 1 : 0;
+    return (24ull * unsigned(passes) + 8ull) * n_pairs;
+}
+
 __device__ __forceinline__ int tile_class(uint32_t c, uint32_t mean) {
     // 0: >= 4x mean pairs, 1: >= 2x, 2: >= 1x, 3: lighter
     return c >= 4 * mean ? 0 : (c >= 2 * mean ? 1 : (c >= mean ? 2 : 3));
@@ -333,6 +361,7 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
             totals->sum_selected += cnt->n_selected;
             totals->sum_pairs += ovf ? 0ull : total;
             if (ovf) totals->pad = 1;
+            totals->sum_sort_bytes += ovf ? 0ull : sort_bytes(cnt, total);
         }
     }
     __syncthreads();
@@ -483,6 +512,7 @@ __global__ void __cluster_dims__(kOffCtas, 1, 1) __launch_bounds__(1024) k_tile_
             totals->sum_selected += cnt->n_selected;
             totals->sum_pairs += ovf ? 0ull : total;
             if (ovf) totals->pad = 1;
+            totals->sum_sort_bytes += ovf ? 0ull : sort_bytes(cnt, total);
         }
     }
     // heavy-first schedule (see k_tile_offsets): classes by count vs the mean

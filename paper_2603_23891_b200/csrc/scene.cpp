@@ -946,7 +946,8 @@ uint64_t GpuScene::profile_read(double stage_ms[6]) {
     return prof_used_;
 }
 
-void GpuScene::take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs) {
+void GpuScene::take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs,
+                           uint64_t* sum_sort_bytes) {
     DeviceGuard dg(device_);
     RunTotals t;
     FGS_CUDA(cudaStreamSynchronize(stream_));
@@ -955,6 +956,7 @@ void GpuScene::take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pa
     if (frames) *frames = t.frames;
     if (sum_sel) *sum_sel = t.sum_selected;
     if (sum_pairs) *sum_pairs = t.sum_pairs;
+    if (sum_sort_bytes) *sum_sort_bytes = t.sum_sort_bytes;
     if (t.pad) {
         reserve_pairs(pair_cap_ * 2);
         throw Error(LODGS_ERR_INTERNAL, "overflow: pair buffer grown, re-render the frames");

@@ -108,7 +108,8 @@ public:
     uint64_t read_pairs(lodgs_tile_pair* out, uint64_t cap);
     uint64_t read_gaussians(lodgs_blend_list* out, uint64_t cap);
     void read_counts(uint32_t* per_gaussian, uint64_t cap_g, uint32_t* per_tile, uint64_t cap_t);
-    void take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs);
+    void take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs,
+                     uint64_t* sum_sort_bytes = nullptr);
     uint64_t read_kpc(double* out, uint64_t cap);
     void calibrate(const lodgs_camera* views, uint32_t n_views, double lambda_g, double tau_r,
                    lodgs_calibration* out, double* per_view);

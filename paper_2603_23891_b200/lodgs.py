@@ -221,7 +221,7 @@ def load_library():
         "lodgs_gpu_render_async": (C.c_int, [P, C.POINTER(CameraC), C.POINTER(RenderParamsC), P]),
         "lodgs_gpu_sync": (C.c_int, [P, C.POINTER(RenderStatsC)]),
         "lodgs_gpu_take_totals": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
-                                            C.POINTER(C.c_uint64)]),
+                                             C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "lodgs_gpu_profile": (C.c_int, [P, C.c_int]),
         "lodgs_gpu_profile_read": (C.c_int, [P, C.POINTER(C.c_uint64), _DP]),
         "lodgs_gpu_read_image": (C.c_int, [P, P]),
@@ -781,9 +781,13 @@ class GpuScene:
         _check(self._lib.lodgs_gpu_sync(self._h, C.byref(st)))
         return RenderStats.from_c(st)
 
-    def take_totals(self):
-        f, s, p = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
-        _check(self._lib.lodgs_gpu_take_totals(self._h, C.byref(f), C.byref(s), C.byref(p)))
+    def take_totals(self, sort_bytes: bool = False):
+        """(frames, sum n_selected, sum n_pairs[, sum radix-sort bytes]) since the last call."""
+        f, s, p, b = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        _check(self._lib.lodgs_gpu_take_totals(self._h, C.byref(f), C.byref(s), C.byref(p),
+                                               C.byref(b)))
+        if sort_bytes:
+            return int(f.value), int(s.value), int(p.value), int(b.value)
         return int(f.value), int(s.value), int(p.value)
 
     def profile(self, enable: bool):
