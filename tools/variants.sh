@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build variant libraries of one CUDA TU with extra -D flags (kernel experiments):
-#   bash tools/variants.sh blend.cu "A=-DX=1" "B=-DX=2"   -> _variants/<name>/liblodgs_b200.so
+#   bash tools/variants.sh "blend.cu sort.cu" "A=-DX=1" "B=-DX=2" -> _variants/<name>/liblodgs_b200.so
 # Select one at run time with LODGS_B200_LIB=_variants/<name>/liblodgs_b200.so.
 set -e
 TU=$1; shift
@@ -11,8 +11,11 @@ NVFLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=
 for spec in "$@"; do
   name=${spec%%=*}; flags=${spec#*=}
   out=$ROOT/_variants/$name; mkdir -p $out
-  nvcc $NVFLAGS $flags -c $CSRC/$TU -o $out/${TU%.cu}.o
-  objs=$(ls $OBJ/*.o | grep -v "/${TU%.cu}.o$")
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $out/liblodgs_b200.so $out/${TU%.cu}.o $objs -lpthread -ldl -lrt
+  objs=$(ls $OBJ/*.o)
+  for tu in $TU; do
+    nvcc $NVFLAGS $flags -c $CSRC/$tu -o $out/${tu%.cu}.o
+    objs=$(echo "$objs" | grep -v "/${tu%.cu}.o$")
+  done
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $out/liblodgs_b200.so $out/*.o $objs -lpthread -ldl -lrt
   echo "built $out"
 done
