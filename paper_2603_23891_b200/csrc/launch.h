@@ -30,10 +30,10 @@ struct DevTree {
 };
 
 // ---- filter (filter.cpp:115-150) ----
-// kernels enqueued per frame: mark internal, select internal, filter leaves,
-// compact, preprocess, tile offsets (+ run totals), emit, tile sort, big-tile
-// sort, blend
-constexpr int kLaunchesPerFrame = 10;
+// kernels enqueued per frame: zero, mark internal, select internal, filter
+// leaves, compact, preprocess, tile offsets (+ run totals), emit, tile sort,
+// big-tile sort, blend
+constexpr int kLaunchesPerFrame = 11;
 constexpr int kMarkBlock = 256;
 constexpr int kSelectBlock = 256;
 constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles
@@ -80,11 +80,12 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
 // Turns the per-tile counts into offsets[n_tiles+1] and per-tile write cursors,
 // lists the tiles whose segment exceeds the in-shared-memory sort capacity, and
 // writes order[n_tiles]: tiles heaviest-first (log2 buckets) for the per-tile grids.
-// With `totals`, also accumulates the per-run frame/selected/pair totals.
+// With `totals`, also accumulates the per-run frame/selected/pair totals; with
+// `log`, copies the frame's final counters there (device-side batch log).
 void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
                          uint32_t* cursor, uint32_t* big_list, uint32_t* order,
                          FrameCounters* cnt, uint64_t pair_cap, cudaStream_t s,
-                         RunTotals* totals = nullptr);
+                         RunTotals* totals = nullptr, FrameCounters* log = nullptr);
 // Key duplication: one key per (gaussian, overlapped tile) scattered into the
 // tile's bucket; key = depth_bits << 32 | gaussian.
 void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x, int n_tiles,
@@ -152,6 +153,9 @@ void launch_keys_to_triples(const uint32_t* offsets, int n_tiles, const unsigned
 // Per-gaussian pair counts (bin_to_tiles multiplicity) from emit records.
 void launch_gauss_counts(const GaussEmit* emit, const FrameCounters* cnt, uint64_t cap,
                          uint32_t* out, cudaStream_t s);
+
+// zeroes `bytes` (a multiple of 16) with a kernel, not a memset
+void launch_zero(void* p, uint64_t bytes, cudaStream_t s);
 
 // ---- scene ingest (scene.cpp:89-165, scene_io.cpp:90-116) ----
 // has_child (n bytes, scratch) then the per-node rule masks (9 bits, see

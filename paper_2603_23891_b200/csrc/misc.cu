@@ -1,5 +1,7 @@
 // misc.cu -- small device utilities: tree packing at upload, run totals,
 // tile-id range for the standalone sort.
+#include <algorithm>
+
 #include "launch.h"
 
 namespace fgs {
@@ -72,6 +74,22 @@ __global__ void k_max_tile(const uint32_t* t, uint64_t n, unsigned int* out) {
 
 void launch_max_tile(const uint32_t* triples, uint64_t n, unsigned int* out, cudaStream_t s) {
     if (n) k_max_tile<<<148, 256, 0, s>>>(triples, n, out);
+}
+
+// Per-frame clearing of the counters / scan state / tile counts by a kernel:
+// a cudaMemsetAsync may be served by a copy engine and would then queue
+// behind the previous frame's image copy (render_batch overlaps the two).
+__global__ void k_zero_words(uint4* p, uint64_t n16) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+void launch_zero(void* p, uint64_t bytes, cudaStream_t s) {
+    const uint64_t n16 = bytes / 16;  // callers pass 256-byte multiples
+    if (n16 == 0) return;
+    const unsigned grid = unsigned(std::min<uint64_t>((n16 + 255) / 256, 148 * 4));
+    k_zero_words<<<grid, 256, 0, s>>>(reinterpret_cast<uint4*>(p), n16);
 }
 
 }  // namespace fgs

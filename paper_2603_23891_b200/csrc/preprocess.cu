@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
                                                        uint32_t* cursor, uint32_t* big_list,
                                                        uint32_t* order, FrameCounters* cnt,
                                                        uint64_t pair_cap, RunTotals* totals,
-                                                       int staged) {
+                                                       int staged, FrameCounters* log) {
     // staged: counts, then offsets, in s_buf[0, n]; the order in s_buf[n+1, 2n+1).
     // Every global write then leaves the SM as coalesced rows -- a single SM's
     // scattered stores were the bottleneck of this kernel (~1 sector/clk).
@@ -427,6 +427,8 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
         __syncthreads();
         for (int t = threadIdx.x; t < n_tiles; t += 1024) order[t] = ord[t];
     }
+    __syncthreads();
+    if (log && threadIdx.x == 0) *log = *cnt;
 }
 
 // Cluster variant for up to 8 x 12,288 tiles: the 8 CTAs of one thread-block
@@ -440,7 +442,7 @@ constexpr int kOffChunkMax = 12288;
 __global__ void __cluster_dims__(kOffCtas, 1, 1) __launch_bounds__(1024) k_tile_offsets_cluster(
     const uint32_t* __restrict__ gcount, int n_tiles, uint32_t* offsets, uint32_t* cursor,
     uint32_t* big_list, uint32_t* order, FrameCounters* cnt, uint64_t pair_cap,
-    RunTotals* totals) {
+    RunTotals* totals, FrameCounters* log) {
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned crank = cluster.block_rank();
     __shared__ unsigned long long s_tot;  // this chunk's pair total (read by every CTA)
@@ -573,12 +575,15 @@ __global__ void __cluster_dims__(kOffCtas, 1, 1) __launch_bounds__(1024) k_tile_
         }
     }
     cluster.sync();  // no CTA leaves while its shared memory may still be read
+    // the frame's final counters into the batch log (no per-frame D2H on the
+    // compute stream: a D2H there would queue behind the image copies)
+    if (log && crank == 0 && threadIdx.x == 0) *log = *cnt;
 }
 
 void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
                          uint32_t* cursor, uint32_t* big_list, uint32_t* order,
                          FrameCounters* cnt, uint64_t pair_cap, cudaStream_t s,
-                         RunTotals* totals) {
+                         RunTotals* totals, FrameCounters* log) {
     if (n_tiles <= kOffCtas * kOffChunkMax) {
         const int chunk = (n_tiles + kOffCtas - 1) / kOffCtas;
         const size_t smem = size_t(chunk + 1) * 4;
@@ -595,14 +600,14 @@ void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offs
         }
         k_tile_offsets_cluster<<<kOffCtas, 1024, smem, s>>>(tile_count, n_tiles, offsets, cursor,
                                                             big_list, order, cnt, pair_cap,
-                                                            totals);
+                                                            totals, log);
         return;
     }
     // beyond 98,304 tiles (> 8K frames): one CTA, global memory
     const int staged = 0;
     const size_t smem = 0;
     k_tile_offsets<<<1, 1024, smem, s>>>(tile_count, n_tiles, offsets, cursor, big_list, order,
-                                         cnt, pair_cap, totals, staged);
+                                         cnt, pair_cap, totals, staged, log);
 }
 
 // Key duplication with CTA-level aggregation: each CTA counts its slice's

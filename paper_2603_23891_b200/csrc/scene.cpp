@@ -376,7 +376,7 @@ void GpuScene::ensure_resolution(int w, int h) {
 }
 
 void GpuScene::clear_frame_state() {
-    FGS_CUDA(cudaMemsetAsync(zero_.p, 0, zero_bytes_, stream_));
+    launch_zero(zero_.p, zero_bytes_, stream_);  // zero_bytes_ is 256-aligned
 }
 
 void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int w, int h,
@@ -421,7 +421,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
                       res_.tiles_y, out, d_counters_, persistent_grid_, stream_);
     launch_tile_offsets(d_tile_count_, n_tiles, res_.tile_offsets.p, res_.tile_cursor.p,
                         res_.big_list.p, res_.tile_order.p, d_counters_, pair_cap_, stream_,
-                        totals_.p);
+                        totals_.p, log_target_);
     launch_emit_keys(emit_.p, d_counters_, res_.tiles_x, n_tiles, res_.tile_cursor.p, keys_.p,
                      persistent_grid_, stream_);
     maps_valid_ = false;
@@ -542,6 +542,7 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
         }
     }
     image2_.alloc(image_floats());
+    frame_log_.alloc(n);
     if (h_batch_cap_ < n) {
         if (h_batch_counters_) FGS_CUDA(cudaFreeHost(h_batch_counters_));
         FGS_CUDA(cudaMallocHost(&h_batch_counters_, n * sizeof(FrameCounters)));
@@ -557,10 +558,10 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
         // the blend may overwrite bufs[k] only once frame i-2's copy out of it is done
         if (i >= 2) FGS_CUDA(cudaStreamWaitEvent(stream_, copy_done_[k], 0));
         image_target_ = bufs[k];
+        log_target_ = frame_log_.p + i;
         enqueue_pipeline(camera_geom(cams[i]), p, int(cams[i].width), int(cams[i].height), false);
         image_target_ = nullptr;
-        FGS_CUDA(cudaMemcpyAsync(h_batch_counters_ + i, d_counters_, sizeof(FrameCounters),
-                                 cudaMemcpyDeviceToHost, stream_));
+        log_target_ = nullptr;
         FGS_CUDA(cudaEventRecord(frame_done_[k], stream_));
         FGS_CUDA(cudaStreamWaitEvent(copy_stream_, frame_done_[k], 0));
         if (images_host && images_host[i])
@@ -568,6 +569,9 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
                                      copy_stream_));
         FGS_CUDA(cudaEventRecord(copy_done_[k], copy_stream_));
     }
+    // every frame's counters in one copy, after the last frame
+    FGS_CUDA(cudaMemcpyAsync(h_batch_counters_, frame_log_.p, n * sizeof(FrameCounters),
+                             cudaMemcpyDeviceToHost, stream_));
     FGS_CUDA(cudaStreamSynchronize(stream_));
     FGS_CUDA(cudaStreamSynchronize(copy_stream_));
     // the last frame's image also lives in res_.image for read_image()

@@ -196,6 +196,8 @@ private:
     cudaStream_t copy_stream_ = nullptr;
     cudaEvent_t frame_done_[2] = {}, copy_done_[2] = {};
     FrameCounters* h_batch_counters_ = nullptr;
+    DevBuf<FrameCounters> frame_log_;      // device-side per-frame counters of a batch
+    FrameCounters* log_target_ = nullptr;  // enqueue_pipeline: where k_tile_offsets logs
     uint64_t h_batch_cap_ = 0;
     bool profiling_ = false;
     std::vector<std::array<cudaEvent_t, 6>> prof_events_;
