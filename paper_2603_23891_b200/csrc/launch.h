@@ -22,6 +22,9 @@ struct DevTree {
     const float4* iquat = nullptr;   // (w, x, y, z) for [0, leaf_begin)
     const uint32_t* parent = nullptr;  // padded to 256 nodes with kRootParent
     const SplatRec* splat = nullptr;
+    // per node, the FP64 world covariance of mark_core (sigma3d, camera
+    // independent): 6 doubles, precomputed at upload for the preprocess
+    const double* sig3 = nullptr;
     // Nodes [leaf_begin, n) are all leaves (leaf_begin a multiple of 1024, or n).
     uint64_t leaf_begin = 0;
     // max_i (|mx| + |my| + |mz|) over the tree (rounded up): the FP32 leaf
@@ -76,7 +79,8 @@ constexpr int kHistMaxTiles = 12288;  // shared-memory tile histograms up to 48 
 constexpr int16_t kDropped = -32768;  // GaussEmit::ty0 of a slot dropped by project()
 void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected,
                        uint64_t max_selected, int shrink_kind, double tau, int tiles_x,
-                       int tiles_y, PrepOut out, FrameCounters* cnt, int grid, cudaStream_t s);
+                       int tiles_y, PrepOut out, FrameCounters* cnt, int grid, cudaStream_t s,
+                       bool known_visible = false);
 // Turns the per-tile counts into offsets[n_tiles+1] and per-tile write cursors,
 // lists the tiles whose segment exceeds the in-shared-memory sort capacity, and
 // writes order[n_tiles]: tiles heaviest-first (log2 buckets) for the per-tile grids.

@@ -41,16 +41,27 @@ struct Projected {
     double mx, my, ca, cb, cc, radius, depth;
 };
 
-// projection.cpp:60-91 + effective_radius.
-__device__ __forceinline__ Projected project_one(const Geom& g, const SplatRec& r, int kind,
-                                                 double tau) {
+// projection.cpp:60-91 + effective_radius, with mark_core's world covariance
+// read precomputed (sigma3d at upload, identical operations).  known_visible:
+// the node passed this frame's filter, whose frustum decision is the same
+// FP64 decision (mark_core.hpp:32-40), so the test is not repeated.
+__device__ __forceinline__ Projected project_one(const Geom& g, const SplatRec& r,
+                                                 const Sigma3& S, int kind, double tau,
+                                                 bool known_visible) {
     Projected p;
     p.keep = false;
     p.nonfinite = false;
-    const MarkOut m = mark_core(g, r.mx, r.my, r.mz, r.sx, r.sy, r.sz, r.qw, r.qx, r.qy, r.qz,
-                                __longlong_as_double(0x7ff0000000000000ll));
-    if (!m.vis || !m.z_ok) return p;
-    const double inv_z = 1.0 / m.tz;
+    MarkOut m;
+    cam_transform(g, r.mx, r.my, r.mz, m.tx, m.ty, m.tz);
+    if (!known_visible) {
+        const double smax = std_max(std_max(double(r.sx), double(r.sy)), double(r.sz));
+        if (!frustum_literal(g, m.tx, m.ty, m.tz, 3.0 * smax)) return p;
+    }
+    if (!(m.tz >= g.znear)) return p;  // z_ok (mark_core.hpp:41)
+    ewa_from_sigma(g, m.tx, m.ty, m.tz, S, m);
+    // projection.cpp:73 divides by tz; ewa used 1 / max(tz, 1e-12), the same
+    // quotient whenever tz >= 1e-12
+    const double inv_z = m.tz < 1e-12 ? 1.0 / m.tz : m.inv_zc;
     p.mx = g.fx * (m.tx * inv_z) + g.cx;
     p.my = g.fy * (m.ty * inv_z) + g.cy;
     const double det = m.a * m.c - m.b * m.b;
@@ -173,9 +184,10 @@ __device__ __forceinline__ void block_add2(uint32_t a, uint32_t b, unsigned long
 // Keys carry the slot, whose order equals BlendList order, so the sort is
 // unchanged; the slot -> BlendList index map is only built for readbacks.
 __global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
-    const Geom g, const SplatRec* __restrict__ splat, const uint32_t* __restrict__ selected,
-    const int kind, const double tau, const int tiles_x, const int tiles_y, PrepOut out,
-    FrameCounters* cnt, const int use_hist) {
+    const Geom g, const SplatRec* __restrict__ splat, const double* __restrict__ sig3,
+    const uint32_t* __restrict__ selected, const int kind, const double tau, const int tiles_x,
+    const int tiles_y, PrepOut out, FrameCounters* cnt, const int use_hist,
+    const int known_visible) {
     extern __shared__ uint32_t s_hist[];
     const int n_tiles = tiles_x * tiles_y;
     uint64_t lo, hi;
@@ -194,7 +206,10 @@ __global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
         rec.sy = b.x; rec.sz = b.y; rec.qw = b.z; rec.qx = b.w;
         rec.qy = c.x; rec.qz = c.y; rec.opacity = c.z; rec.cr = c.w;
         rec.cg = d.x; rec.cb = d.y;
-        const Projected p = project_one(g, rec, kind, tau);
+        const double2* sp = reinterpret_cast<const double2*>(sig3 + 6 * uint64_t(idx));
+        const double2 s0 = __ldg(sp), s1 = __ldg(sp + 1), s2 = __ldg(sp + 2);
+        const Sigma3 S{s0.x, s0.y, s1.x, s1.y, s2.x, s2.y};
+        const Projected p = project_one(g, rec, S, kind, tau, known_visible != 0);
         GaussEmit e;
         e.node = idx;
         if (p.keep) {
@@ -265,13 +280,15 @@ __global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
 
 void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected,
                        uint64_t max_selected, int shrink_kind, double tau, int tiles_x,
-                       int tiles_y, PrepOut out, FrameCounters* cnt, int grid, cudaStream_t s) {
+                       int tiles_y, PrepOut out, FrameCounters* cnt, int grid, cudaStream_t s,
+                       bool known_visible) {
     if (max_selected == 0) return;
     const int n_tiles = tiles_x * tiles_y;
     const int use_hist = n_tiles <= kHistMaxTiles ? 1 : 0;
     const size_t smem = use_hist ? size_t(n_tiles) * 4 : 0;
-    k_preprocess<<<grid, kPrepBlock, smem, s>>>(g, t.splat, selected, shrink_kind, tau, tiles_x,
-                                                tiles_y, out, cnt, use_hist);
+    k_preprocess<<<grid, kPrepBlock, smem, s>>>(g, t.splat, t.sig3, selected, shrink_kind, tau,
+                                                tiles_x, tiles_y, out, cnt, use_hist,
+                                                known_visible ? 1 : 0);
 }
 
 // One CTA: exclusive scan of per-tile counts -> offsets and write cursors,

@@ -34,7 +34,7 @@ DeviceGuard::~DeviceGuard() {
 
 void launch_pack_tree(const float* soa, const float* extra, const uint8_t* leaf, uint64_t n,
                       uint64_t leaf_begin, float4* geo, float4* iscale, float4* iquat,
-                      SplatRec* splat, cudaStream_t s);
+                      SplatRec* splat, double* sig3, cudaStream_t s);
 void launch_update_totals(const FrameCounters* cnt, const uint32_t* offsets, int n_tiles,
                           RunTotals* totals, cudaStream_t s);
 void launch_max_tile(const uint32_t* triples, uint64_t n, unsigned int* out, cudaStream_t s);
@@ -282,8 +282,9 @@ void GpuScene::ingest(uint64_t n, const std::vector<uint64_t>& level_begin, bool
     iscale_.alloc(nb);
     iquat_.alloc(nb);
     splat_.alloc(n);
+    sig3_.alloc(6 * n);
     launch_pack_tree(st.soa.p, st.soa.p + 6 * n, st.leaf.p, n, nb, geo_.p, iscale_.p, iquat_.p,
-                     splat_.p, stream_);
+                     splat_.p, sig3_.p, stream_);
     parent_.alloc(np);
     FGS_CUDA(cudaMemsetAsync(parent_.p, 0xFF, np * 4, stream_));
     if (n) FGS_CUDA(cudaMemcpyAsync(parent_.p, st.parent.p, n * 4, cudaMemcpyDeviceToDevice, stream_));
@@ -293,6 +294,7 @@ void GpuScene::ingest(uint64_t n, const std::vector<uint64_t>& level_begin, bool
     tree_.iquat = iquat_.p;
     tree_.parent = parent_.p;
     tree_.splat = splat_.p;
+    tree_.sig3 = sig3_.p;
 
     cand_bits_.alloc(bit_words(n));
     qint_bits_.alloc(bit_words(n));
@@ -338,6 +340,7 @@ void GpuScene::reserve_pairs(uint64_t n) {
 
 uint64_t GpuScene::device_bytes() const {
     return geo_.bytes() + iscale_.bytes() + iquat_.bytes() + parent_.bytes() + splat_.bytes() +
+           sig3_.bytes() +
            cand_bits_.bytes() + qint_bits_.bytes() + selected_.bytes() + g64_.bytes() +
            g32_.bytes() + emit_.bytes() + col64_.bytes() + keys_.bytes() + zero_.bytes() +
            res_.tile_offsets.bytes() + res_.tile_cursor.bytes() + res_.big_list.bytes() +
@@ -418,7 +421,8 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     if (pe) FGS_CUDA(cudaEventRecord(pe[2], stream_));
     PrepOut out{g64_.p, g32_.p, emit_.p, exact ? col64_.p : nullptr, d_tile_count_};
     launch_preprocess(g, tree_, selected_.p, tree_.n, p.shrink_kind, p.tau, res_.tiles_x,
-                      res_.tiles_y, out, d_counters_, persistent_grid_, stream_);
+                      res_.tiles_y, out, d_counters_, persistent_grid_, stream_,
+                      /*known_visible=*/true);
     launch_tile_offsets(d_tile_count_, n_tiles, res_.tile_offsets.p, res_.tile_cursor.p,
                         res_.big_list.p, res_.tile_order.p, d_counters_, pair_cap_, stream_,
                         totals_.p, log_target_);
