@@ -5,6 +5,12 @@
         0: the reference is SH0-only, so SH3 colours would be parity-unpinned.
   cfg4: 50,142,872-node tree (103x104 roots, L=4), 3840x2160, fx=2000, a descent from
         altitude 400 to 110; GTC shrink off (three-sigma) vs on (adaptive).
+  cfg5: view-batched rendering -- the cfg 3 tree, 1024 poses sampled from the cfg 3
+        fly-through keyframes, sharded contiguously across the ranks of a torchrun
+        launch (one process per GPU, tree replicated, no collective on the data path;
+        max-over-ranks device time).  Device views/s, plus views/s end to end with the
+        8-bit image of every view read back (lodgs_gpu_read_image_rgb8-style bytes
+        through render_batch is f32; the rgb8 path reads 6.2 MB per view).
 
 Device-timed FPS (CUDA events on the scene stream), pairs per frame, the calibrated tau.
 Prints one JSON object per (workload, shrink mode).
@@ -56,7 +62,69 @@ def time_frames(scene, cams, mode, tau_r=3.0, reps=1):
             "mean_selected": sel / frames, "mean_pairs": pairs / frames}
 
 
+def run_cfg5(n_views=1024):
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    tree = L.build_synthetic_tree(**bench.TREE)
+    n = n_views - 1
+    keys_cams = bench.flythrough(L)  # 300 frames; re-sample the same keyframes to 1024
+    keys = [keys_cams[0], keys_cams[100], keys_cams[200], keys_cams[-1]]
+    cams = L.sample_camera_path(keys, (n // 3, n // 3, n - 2 * (n // 3)))
+    assert len(cams) == n_views
+    lo, hi = rank * n_views // world, (rank + 1) * n_views // world
+    mine = cams[lo:hi]
+    with L.GpuScene(tree, local) as scene:
+        mode = L.ShrinkMode.three_sigma()
+        for cam in mine[:: max(1, len(mine) // 16)]:
+            scene.render(cam, L.FilterConfig(bench.TAU_R), mode)  # pair-buffer sizing
+        p = scene.params(L.FilterConfig(bench.TAU_R), mode, L.RenderOptions())
+        stream = torch.cuda.ExternalStream(scene.stream_ptr(), device=torch.device("cuda", local))
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        scene.take_totals()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ev0.record(stream)
+        for cam in mine:
+            scene.render_async(cam, p)
+        ev1.record(stream)
+        ev1.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        frames, sel, pairs = scene.take_totals()
+        # end to end: every view's 8-bit image back to the host
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for cam in mine:
+            scene.render_async(cam, p)
+            scene.read_image_rgb8(cam)  # synchronous: no compute/copy overlap
+        e2e_s = time.perf_counter() - t0
+        t = torch.tensor([ms, e2e_s * 1e3], device="cuda")
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            rec = {"workload": "cfg5", "nodes": tree.node_count(), "views": n_views,
+                   "gpus": world, "views_per_gpu": len(mine),
+                   "views_per_s": n_views / (t[0].item() / 1e3),
+                   "e2e_rgb8_views_per_s": n_views / (t[1].item() / 1e3),
+                   "mean_selected": sel / max(1, frames), "mean_pairs": pairs / max(1, frames)}
+            print(json.dumps(rec), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def run(which, frames, lambda_g):
+    if which == "cfg5":
+        return run_cfg5()
     out = []
     if which == "cfg2":
         t0 = time.perf_counter()
