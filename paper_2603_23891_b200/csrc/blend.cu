@@ -270,6 +270,264 @@ __global__ void __launch_bounds__(kFastThreads, BLEND_MIN_CTAS) k_blend_fast(
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised fast blend: one CTA per 16x16 tile, 8 consumer warps (one
+// 8x4 block each) and 1 producer warp.  The producer walks the tile's sorted
+// pairs 32 at a time -- keys two batches and records one batch ahead in
+// registers -- culls every splat against all 8 blocks at once and writes each
+// block's hits, compacted in pair order, into a ring of kWsStages shared-
+// memory stages; mbarriers hand stages over (full: 32 producer lanes, empty:
+// 8 x 32 consumer lanes).  Each record is loaded and culled once per tile
+// instead of once per warp, and the ring depth hides the gather latency.
+// Consumers run the same per-sample code as k_blend_fast.
+#ifndef WS_STAGES
+#define WS_STAGES 4
+#endif
+constexpr int kWsStages = WS_STAGES;
+constexpr int kWsConsumers = 8;
+#ifndef WS_PRODUCERS
+#define WS_PRODUCERS 2
+#endif
+#ifndef WS_SLEEP
+#define WS_SLEEP 0  // ns of __nanosleep between failed mbarrier polls (0: spin)
+#endif
+constexpr int kWsProducers = WS_PRODUCERS;
+constexpr int kWsThreads = (kWsConsumers + kWsProducers) * 32;
+
+struct WsStage {
+    WarpStage blk[kWsConsumers];
+    uint32_t cnt[kWsConsumers];
+    uint32_t last;  // no stage follows this one
+};
+
+#ifndef WS_RAW
+#define WS_RAW 4
+#endif
+constexpr int kWsRaw = WS_RAW;  // producer's gather ring (batches in flight + 1)
+struct WsRaw {
+    double2 m[32];
+    float4 q0[32], col[32];
+    float2 h[32];
+    uint32_t gid[32];
+};
+
+struct WsShared {
+    WsStage st[kWsStages];
+    WsRaw raw[kWsProducers][kWsRaw];
+    unsigned long long full[kWsStages], empty[kWsStages];
+    uint32_t done_warps;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(
+                     smem_addr(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+#if WS_SLEEP
+    uint32_t ok = 0;
+    while (true) {
+        asm volatile(
+            "{ .reg .pred p;\n"
+            "  mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "  selp.u32 %0, 1, 0, p;\n"
+            "}"
+            : "=r"(ok)
+            : "r"(smem_addr(b)), "r"(parity)
+            : "memory");
+        if (ok) break;
+        __nanosleep(WS_SLEEP);
+    }
+#else
+    asm volatile(
+        "{ .reg .pred p;\n"
+        "WAIT_%=:\n"
+        "  mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "  @!p bra WAIT_%=;\n"
+        "}" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+#endif
+}
+
+__global__ void __launch_bounds__(kWsThreads, 3) k_blend_ws(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
+    const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
+    const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
+    float* __restrict__ image) {
+    extern __shared__ __align__(16) unsigned char ws_raw[];
+    WsShared& sh = *reinterpret_cast<WsShared*>(ws_raw);
+    const int tile = int(order[blockIdx.x]);  // heaviest tiles first
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
+    const uint32_t b = offsets[tile], e = offsets[tile + 1];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kWsStages; ++s) {
+            mbar_init(&sh.full[s], 32);  // one producer warp fills a stage
+            mbar_init(&sh.empty[s], kWsConsumers * 32);
+        }
+        sh.done_warps = 0;
+    }
+    __syncthreads();
+
+    if (warp >= kWsConsumers) {
+        // ---------------- producers ----------------
+        // Producer p fills the stages of batches p, p + 2, p + 4, ...  Records
+        // are gathered with cp.async into a private ring kWsRaw of its batches
+        // ahead (keys one batch further, in registers).  A splat's blocks are
+        // the ones its alpha box overlaps: one range test per axis, then one
+        // ballot per block to compact the hits in pair order.
+        const uint32_t pid = warp - kWsConsumers;
+        constexpr uint32_t kNone = 0xFFFFFFFFu;
+        auto batch_base = [&](uint32_t j) { return b + 32u * (pid + kWsProducers * j); };
+        auto load_key = [&](uint32_t j) -> uint32_t {
+            const uint32_t at = batch_base(j);
+            return at + lane < e ? uint32_t(keys[at + lane]) : kNone;
+        };
+        auto gather = [&](uint32_t gi, int slot) {
+            WsRaw& r = sh.raw[pid][slot];
+            r.gid[lane] = gi;
+            if (gi != kNone) {
+                cp_async16(&r.m[lane], &g64[gi].mx);
+                cp_async16(&r.q0[lane], &g32[gi].ha);
+                cp_async16(&r.col[lane], &g32[gi].op);
+                cp_async8(&r.h[lane], &g32[gi].hx);
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int j = 0; j < kWsRaw - 1; ++j) gather(load_key(j), j);
+        uint32_t gi_ahead = load_key(kWsRaw - 1);
+        const unsigned lt = (1u << lane) - 1u;
+        for (uint32_t j = 0;; ++j) {
+            const uint32_t i = pid + kWsProducers * j;  // global batch index
+            const uint32_t base = batch_base(j);
+            gather(gi_ahead, int((j + kWsRaw - 1) % kWsRaw));
+            gi_ahead = load_key(j + kWsRaw);
+            cp_async_wait<kWsRaw - 1>();  // batch j of this producer has landed
+            __syncwarp();
+            const WsRaw& r = sh.raw[pid][j % kWsRaw];
+            const int s = int(i % kWsStages);
+            const uint32_t use = i / kWsStages;
+            if (use > 0) mbar_wait(&sh.empty[s], (use - 1) & 1u);
+            WsStage& st = sh.st[s];
+            const bool stop = base >= e || *(volatile uint32_t*)&sh.done_warps == kWsConsumers;
+            if (!stop) {
+                const uint32_t gi = r.gid[lane];
+                const double2 m = r.m[lane];
+                const float4 q0 = r.q0[lane], col = r.col[lane];
+                const float2 h = r.h[lane];
+                // tile-relative box; block (bxi, byi) spans pixel centres
+                // [8 bxi + 0.5, 8 bxi + 7.5] x [4 byi + 0.5, 4 byi + 3.5]
+                float mtx = 0.f, mty = 0.f;
+                unsigned xm = 0, ym = 0;  // overlapped block columns / rows
+                if (gi != kNone && h.x >= 0.0f) {
+                    mtx = float(m.x - double(tx0));
+                    mty = float(m.y - double(ty0));
+                    xm = (mtx - h.x <= 7.5f && mtx + h.x >= 0.5f ? 1u : 0u) |
+                         (mtx - h.x <= 15.5f && mtx + h.x >= 8.5f ? 2u : 0u);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        ym |= (mty - h.y <= 4.0f * v + 3.5f && mty + h.y >= 4.0f * v + 0.5f)
+                                  ? (1u << v)
+                                  : 0u;
+                }
+#pragma unroll
+                for (int w = 0; w < kWsConsumers; ++w) {
+                    const bool hit = ((xm >> (w & 1)) & 1u) && ((ym >> (w >> 1)) & 1u);
+                    const unsigned bits = __ballot_sync(0xffffffffu, hit);
+                    if (hit) {
+                        const int slot = __popc(bits & lt);
+                        // block-relative mean, rounded from the FP64 mean exactly as k_blend_fast
+                        const float mlx = float(m.x - double(tx0 + (w & 1) * 8));
+                        const float mly = float(m.y - double(ty0 + (w >> 1) * 4));
+                        st.blk[w].geo[slot] = make_float4(mlx, mly, q0.x, q0.z);
+                        st.blk[w].ct[slot] = make_float4(q0.y, q0.w, col.x, col.y);
+                        st.blk[w].gb[slot] = make_float2(col.z, col.w);
+                        st.blk[w].gid[slot] = gi;
+                    }
+                    if (lane == 0) st.cnt[w] = __popc(bits);
+                }
+            } else if (lane < kWsConsumers) {
+                st.cnt[lane] = 0;
+            }
+            const bool last = stop || base + 32 >= e;
+            if (lane == 0) st.last = last ? 1u : 0u;
+            __syncwarp();
+            mbar_arrive(&sh.full[s]);
+            if (last) break;
+        }
+        cp_async_wait<0>();  // no gather may land after the CTA retires
+        return;
+    }
+
+    // ---------------- consumers: warp w owns the 8x4 block (w & 1, w >> 1) ----
+    const int bx = tx0 + int(warp & 1) * 8, by = ty0 + int(warp >> 1) * 4;
+    const int x = bx + int(lane & 7), y = by + int(lane >> 3);
+    const bool inside = x < width && y < height;
+    const float pxl = float(lane & 7) + 0.5f, pyl = float(lane >> 3) + 0.5f;
+    const double px = double(x) + 0.5, py = double(y) + 0.5;
+    PixState pix{inside ? 1.0f : 0.0f, 0.0f, 0.0f, 0.0f};  // T == 0: nothing to do
+    bool counted = false;
+    for (uint32_t i = 0;; ++i) {
+        const int s = int(i % kWsStages);
+        mbar_wait(&sh.full[s], (i / kWsStages) & 1u);
+        const WarpStage& st = sh.st[s].blk[warp];
+        const int nh = int(sh.st[s].cnt[warp]);
+        const bool last = sh.st[s].last != 0;
+        if (nh > 0 && __any_sync(0xffffffffu, pix.T != 0.0f)) {
+            const PixState saved = pix;
+            bool unsure = false;
+            int k = 0;
+            for (; k + 2 <= nh; k += 2) {
+                blend_sample_fast(st, k, pxl, pyl, pix, unsure);
+                blend_sample_fast(st, k + 1, pxl, pyl, pix, unsure);
+            }
+            if (k < nh) blend_sample_fast(st, k, pxl, pyl, pix, unsure);
+            if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
+                pix = saved;
+                for (int j = 0; j < nh; ++j)
+                    blend_sample_checked(st, j, pxl, pyl, px, py, g64, pix);
+            }
+        }
+        __syncwarp();
+        mbar_arrive(&sh.empty[s]);
+        if (!counted && __all_sync(0xffffffffu, pix.T == 0.0f)) {
+            counted = true;
+            if (lane == 0) atomicAdd(&sh.done_warps, 1u);
+        }
+        if (last) break;
+    }
+    if (inside) {
+        float* o = image + (size_t(y) * width + x) * 3;
+        o[0] = pix.cr;
+        o[1] = pix.cg;
+        o[2] = pix.cb;
+    }
+}
+
 constexpr int kBlendThreads = 256;  // exact kernel: one CTA per 16x16 tile
 constexpr int kWarps = kBlendThreads / 32;
 
@@ -520,6 +778,22 @@ void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned
         k_blend_exact<<<n_tiles, kBlendThreads, smem, s>>>(offsets, keys, g64, g32, col64, width,
                                                             height, tiles_x, image);
     } else {
+#ifndef BLEND_WS
+#define BLEND_WS 1
+#endif
+#if BLEND_WS
+        const int smem = int(sizeof(WsShared));
+        static bool ws_attr[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !ws_attr[dev]) {
+            cudaFuncSetAttribute(k_blend_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (dev >= 0 && dev < 64) ws_attr[dev] = true;
+        }
+        k_blend_ws<<<n_tiles, kWsThreads, smem, s>>>(offsets, order, keys, g64, g32, width, height,
+                                                     tiles_x, image);
+        return;
+#endif
         k_blend_fast<<<n_tiles * kFastParts, kFastThreads, 0, s>>>(offsets, order, keys, g64, g32,
                                                                    width, height, tiles_x, image);
     }
