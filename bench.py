@@ -148,10 +148,10 @@ def ncu_kernel_row(kernel, fname="r1_ncu_render_alt200.txt"):
 def blend_evidence():
     """The dominant kernel is issue-bound (no dense contraction, no HBM roofline):
     its SM issue utilisation from the committed ncu capture (altitude 200)."""
-    row, src = ncu_kernel_row("k_blend_fast")
+    row, src = ncu_kernel_row("k_blend_ws")
     if not row:
         return None
-    return {"kernel": "k_blend_fast", "bound": "issue", "issue_slots_busy_pct": row.get("issue%"),
+    return {"kernel": "k_blend_ws", "bound": "issue", "issue_slots_busy_pct": row.get("issue%"),
             "sm_throughput_pct": row.get("sm%"), "achieved_occupancy_pct": row.get("occ%"),
             "ncu_us_alt200": row.get("us"), "source": src}
 

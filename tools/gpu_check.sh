@@ -20,6 +20,6 @@ timeout 900 ncu --set full --clock-control none --import-source on \
    -o $OUT/prof_filter python tools/profile_frames.py --alt 200 --frames 5 > $OUT/ncu_filter.log 2>&1; echo "ncu filter exit $?"
 if [ "${3:-}" != "filter-only" ]; then
 timeout 900 ncu --set full --clock-control none --import-source on \
-   -k regex:'k_blend_fast|k_tile_sort|k_preprocess|k_emit|k_tile_offsets' -s 15 -c 6 \
+   -k regex:'k_blend_ws|k_tile_sort|k_preprocess|k_emit|k_tile_offsets' -s 15 -c 6 \
    -o $OUT/prof_render python tools/profile_frames.py --alt 200 --frames 5 > $OUT/ncu_render.log 2>&1; echo "ncu render exit $?"
 fi
