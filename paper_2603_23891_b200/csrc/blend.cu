@@ -26,6 +26,7 @@
 // Exact kernel (LODGS_RENDER_EXACT_BLEND): the reference arithmetic in FP64
 // with the reference exp_mx (fastexp.hpp:38-50), no FMA: bit-identical pixels.
 #include "launch.h"
+#include "pdl.cuh"
 
 namespace fgs {
 
@@ -155,6 +156,8 @@ __global__ void __launch_bounds__(kFastThreads, BLEND_MIN_CTAS) k_blend_fast(
     const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
     const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
     float* __restrict__ image) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     __shared__ WarpStage stage[kFastWarps];
     // heaviest tiles first (k_tile_offsets' schedule), halves of a tile adjacent
     const int tile = int(order[blockIdx.x / kFastParts]), part = blockIdx.x % kFastParts;
@@ -377,6 +380,8 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_blend_ws(
     const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
     const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
     float* __restrict__ image) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char ws_raw[];
     WsShared& sh = *reinterpret_cast<WsShared*>(ws_raw);
     const int tile = int(order[blockIdx.x]);  // heaviest tiles first
@@ -790,8 +795,8 @@ void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned
             cudaFuncSetAttribute(k_blend_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (dev >= 0 && dev < 64) ws_attr[dev] = true;
         }
-        k_blend_ws<<<n_tiles, kWsThreads, smem, s>>>(offsets, order, keys, g64, g32, width, height,
-                                                     tiles_x, image);
+        launch_pdl(k_blend_ws, n_tiles, kWsThreads, smem, s, offsets, order, keys, g64, g32, width,
+                   height, tiles_x, image);
         return;
 #endif
         k_blend_fast<<<n_tiles * kFastParts, kFastThreads, 0, s>>>(offsets, order, keys, g64, g32,

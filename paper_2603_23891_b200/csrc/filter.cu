@@ -28,6 +28,7 @@
 #include <cmath>
 
 #include "launch.h"
+#include "pdl.cuh"
 #include "mark.cuh"
 #include "scan.cuh"
 
@@ -288,6 +289,8 @@ __device__ __forceinline__ void decide_internal(const Geom& g, const GeomF& f, c
 __global__ void __launch_bounds__(kMarkBlock, 3) k_mark_internal(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const double tau_r, uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ qint_bits) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     const unsigned lane = threadIdx.x & 31;
     const uint64_t end = t.leaf_begin;
     const uint64_t n_groups = (end + 31) / 32;
@@ -336,6 +339,8 @@ constexpr int kTileNodes = 8192;
 __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
     uint32_t* __restrict__ cand_bits, uint32_t* qint_bits, const uint32_t* __restrict__ parent,
     const uint64_t end, uint32_t* __restrict__ tile_count) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t warp_base =
         uint64_t(blockIdx.x) * (kSelectBlock * kSelectItems) + uint64_t(warp) * (32 * kSelectItems);
@@ -405,6 +410,8 @@ __global__ void __launch_bounds__(256) k_filter_leaves(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const uint32_t* __restrict__ blk_bits, uint32_t* __restrict__ keep_bits,
     uint32_t* __restrict__ tile_count) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     const unsigned lane = threadIdx.x & 31;
     const uint64_t end = t.n;
     const uint64_t wbase = t.leaf_begin + (uint64_t(blockIdx.x) * 256 + (threadIdx.x & ~31u)) * 4;
@@ -461,6 +468,8 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ ke
                                                  const uint32_t* __restrict__ tile_count,
                                                  uint32_t* __restrict__ selected,
                                                  FrameCounters* cnt) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     __shared__ unsigned s_red[8];
     __shared__ unsigned s_warp[8];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -632,17 +641,18 @@ void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand
     if (split > 0) {
         const uint64_t groups = (split + 31) / 32;
         const unsigned grid = unsigned(std::min<uint64_t>((groups + 7) / 8, uint64_t(sm_count()) * 3));
-        k_mark_internal<<<grid, kMarkBlock, 0, s>>>(g, f, t, tau_r, cand_bits, qint_bits);
+        launch_pdl(k_mark_internal, grid, kMarkBlock, 0, s, g, f, t, tau_r, cand_bits, qint_bits);
         const uint64_t per = uint64_t(kSelectBlock) * kSelectItems;
-        k_select_internal<<<unsigned((split + per - 1) / per), kSelectBlock, 0, s>>>(
-            cand_bits, qint_bits, t.parent, split, tile_count);
+        launch_pdl(k_select_internal, unsigned((split + per - 1) / per), kSelectBlock, 0, s,
+                   cand_bits, qint_bits, t.parent, split, tile_count);
     }
     if (mid) cudaEventRecord(mid, s);
     if (t.n > split)
-        k_filter_leaves<<<unsigned((t.n - split + 1023) / 1024), 256, 0, s>>>(
-            g, f, t, qint_bits, cand_bits, tile_count);
-    k_compact<<<unsigned((t.n + kTileNodes - 1) / kTileNodes), 256, 0, s>>>(
-        cand_bits, (t.n + 31) / 32, tile_count, selected, cnt);
+        launch_pdl(k_filter_leaves, unsigned((t.n - split + 1023) / 1024), 256, 0, s, g, f, t,
+                   static_cast<const uint32_t*>(qint_bits), cand_bits, tile_count);
+    launch_pdl(k_compact, unsigned((t.n + kTileNodes - 1) / kTileNodes), 256, 0, s,
+               static_cast<const uint32_t*>(cand_bits), (t.n + 31) / 32,
+               static_cast<const uint32_t*>(tile_count), selected, cnt);
 }
 
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,

@@ -3,6 +3,7 @@
 #include <algorithm>
 
 #include "launch.h"
+#include "pdl.cuh"
 #include "mark.cuh"
 
 namespace fgs {
@@ -90,6 +91,8 @@ void launch_max_tile(const uint32_t* triples, uint64_t n, unsigned int* out, cud
 // a cudaMemsetAsync may be served by a copy engine and would then queue
 // behind the previous frame's image copy (render_batch overlaps the two).
 __global__ void k_zero_words(uint4* p, uint64_t n16) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
          i += uint64_t(gridDim.x) * blockDim.x)
         p[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -99,7 +102,7 @@ void launch_zero(void* p, uint64_t bytes, cudaStream_t s) {
     const uint64_t n16 = bytes / 16;  // callers pass 256-byte multiples
     if (n16 == 0) return;
     const unsigned grid = unsigned(std::min<uint64_t>((n16 + 255) / 256, 148 * 4));
-    k_zero_words<<<grid, 256, 0, s>>>(reinterpret_cast<uint4*>(p), n16);
+    launch_pdl(k_zero_words, grid, 256, 0, s, reinterpret_cast<uint4*>(p), n16);
 }
 
 }  // namespace fgs

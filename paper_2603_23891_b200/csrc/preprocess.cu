@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include "launch.h"
+#include "pdl.cuh"
 #include "mark.cuh"
 #include "scan.cuh"
 
@@ -188,6 +189,8 @@ __global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
     const uint32_t* __restrict__ selected, const int kind, const double tau, const int tiles_x,
     const int tiles_y, PrepOut out, FrameCounters* cnt, const int use_hist,
     const int known_visible) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     extern __shared__ uint32_t s_hist[];
     const int n_tiles = tiles_x * tiles_y;
     uint64_t lo, hi;
@@ -286,9 +289,9 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
     const int n_tiles = tiles_x * tiles_y;
     const int use_hist = n_tiles <= kHistMaxTiles ? 1 : 0;
     const size_t smem = use_hist ? size_t(n_tiles) * 4 : 0;
-    k_preprocess<<<grid, kPrepBlock, smem, s>>>(g, t.splat, t.sig3, selected, shrink_kind, tau,
-                                                tiles_x, tiles_y, out, cnt, use_hist,
-                                                known_visible ? 1 : 0);
+    launch_pdl(k_preprocess, grid, kPrepBlock, smem, s, g, t.splat,
+               static_cast<const double*>(t.sig3), selected, shrink_kind, tau, tiles_x, tiles_y,
+               out, cnt, use_hist, known_visible ? 1 : 0);
 }
 
 // One CTA: exclusive scan of per-tile counts -> offsets and write cursors,
@@ -320,6 +323,8 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
                                                        uint32_t* order, FrameCounters* cnt,
                                                        uint64_t pair_cap, RunTotals* totals,
                                                        int staged, FrameCounters* log) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     // staged: counts, then offsets, in s_buf[0, n]; the order in s_buf[n+1, 2n+1).
     // Every global write then leaves the SM as coalesced rows -- a single SM's
     // scattered stores were the bottleneck of this kernel (~1 sector/clk).
@@ -460,6 +465,8 @@ __global__ void __cluster_dims__(kOffCtas, 1, 1) __launch_bounds__(1024) k_tile_
     const uint32_t* __restrict__ gcount, int n_tiles, uint32_t* offsets, uint32_t* cursor,
     uint32_t* big_list, uint32_t* order, FrameCounters* cnt, uint64_t pair_cap,
     RunTotals* totals, FrameCounters* log) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned crank = cluster.block_rank();
     __shared__ unsigned long long s_tot;  // this chunk's pair total (read by every CTA)
@@ -615,9 +622,8 @@ void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offs
                 if (dev >= 0 && dev < 64) attr_set[dev] = true;
             }
         }
-        k_tile_offsets_cluster<<<kOffCtas, 1024, smem, s>>>(tile_count, n_tiles, offsets, cursor,
-                                                            big_list, order, cnt, pair_cap,
-                                                            totals, log);
+        launch_pdl(k_tile_offsets_cluster, kOffCtas, 1024, smem, s, tile_count, n_tiles, offsets,
+                   cursor, big_list, order, cnt, pair_cap, totals, log);
         return;
     }
     // beyond 98,304 tiles (> 8K frames): one CTA, global memory
@@ -634,6 +640,8 @@ __global__ void __launch_bounds__(256) k_emit_keys(const GaussEmit* __restrict__
                                                    const FrameCounters* cnt, int tiles_x,
                                                    int n_tiles, uint32_t* cursor,
                                                    unsigned long long* keys, int use_hist) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     extern __shared__ uint32_t s_hist[];
     if (cnt->overflow) return;
     uint64_t lo, hi;
@@ -674,7 +682,8 @@ void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles
                       uint32_t* cursor, unsigned long long* keys, int grid, cudaStream_t s) {
     const int use_hist = n_tiles <= kHistMaxTiles ? 1 : 0;
     const size_t smem = use_hist ? size_t(n_tiles) * 4 : 0;
-    k_emit_keys<<<grid, 256, smem, s>>>(emit, cnt, tiles_x, n_tiles, cursor, keys, use_hist);
+    launch_pdl(k_emit_keys, grid, 256, smem, s, emit, cnt, tiles_x, n_tiles, cursor, keys,
+               use_hist);
 }
 
 // Readback support: slot -> BlendList index (chained scan over kept flags),

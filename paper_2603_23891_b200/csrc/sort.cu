@@ -16,6 +16,7 @@
 // bucket is padded virtually with +inf (a comparator whose high index is
 // past the end is skipped and the padding never moves).
 #include "launch.h"
+#include "pdl.cuh"
 
 namespace fgs {
 
@@ -154,6 +155,8 @@ __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint3
 __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t* __restrict__ offsets,
                                                                  const uint32_t* __restrict__ order,
                                                                  unsigned long long* keys) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     __shared__ unsigned long long s[kSmallSortCap];
     const uint32_t tile = order[blockIdx.x];  // heaviest buckets first
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
@@ -183,6 +186,8 @@ __global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_
                                                                    unsigned long long* keys,
                                                                    const uint32_t* big_list,
                                                                    FrameCounters* cnt) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
     extern __shared__ unsigned long long s_big[];
     __shared__ unsigned s_item;
     const unsigned n_big = cnt->big_tiles;
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_
 void launch_tile_sort(const uint32_t* offsets, const uint32_t* order, int n_tiles,
                       unsigned long long* keys, cudaStream_t s) {
     if (n_tiles <= 0) return;
-    k_tile_sort<<<n_tiles, kSmallSortThreads, 0, s>>>(offsets, order, keys);
+    launch_pdl(k_tile_sort, n_tiles, kSmallSortThreads, 0, s, offsets, order, keys);
 }
 
 void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
@@ -225,7 +230,7 @@ void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
         cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    k_tile_sort_big<<<grid, kBigSortThreads, smem, s>>>(offsets, keys, big_list, cnt);
+    launch_pdl(k_tile_sort_big, grid, kBigSortThreads, smem, s, offsets, keys, big_list, cnt);
 }
 
 // ----------------------------------------------------------------------------
