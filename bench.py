@@ -260,6 +260,7 @@ def run_b200(args, rank, world, local):
         ev0.record(stream)
         for cam in frames:
             scene.render_async(cam, params)
+        scene.join()  # frames alternate over two in-flight contexts
         ev1.record(stream)
         ev1.synchronize()
         ms = ev0.elapsed_time(ev1)

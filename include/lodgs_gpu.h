@@ -230,8 +230,18 @@ LODGS_API int lodgs_gpu_render_batch(lodgs_gpu_scene *scene, const lodgs_camera 
  * by an async D2H copy on the same stream. */
 LODGS_API int lodgs_gpu_render_async(lodgs_gpu_scene *scene, const lodgs_camera *cam,
                            const lodgs_render_params *params, float *image_host);
-/* Waits for the scene stream; stats (nullable) = the last frame's. */
+/* Waits for every in-flight frame; stats (nullable) = the last frame's. */
 LODGS_API int lodgs_gpu_sync(lodgs_gpu_scene *scene, lodgs_render_stats *stats);
+/* Frames in flight for lodgs_gpu_render_async: 1, or 2 (default) -- consecutive
+ * frames alternate between the scene and a twin context (own stream and
+ * per-frame buffers over the same device tree), so one frame's latency-bound
+ * kernels overlap the other's.  Both fork from the scene's control stream
+ * (lodgs_gpu_scene_stream): a frame starts after the work already enqueued
+ * there (e.g. a timing event). */
+LODGS_API int lodgs_gpu_scene_set_inflight(lodgs_gpu_scene *scene, int frames);
+/* Makes the control stream wait for every frame enqueued so far (no host sync):
+ * record a timing event on the control stream after this. */
+LODGS_API int lodgs_gpu_join(lodgs_gpu_scene *scene);
 /* Sum of n_selected / n_pairs over frames since the last call (device counters);
  * sum_sort_bytes (nullable): the SURVEY 8(d) radix-sort bytes of those frames,
  * (24 B x non-uniform 8-bit digits of the reference key + 8 B) per pair. */

@@ -215,12 +215,12 @@ int lodgs_gpu_render_async(lodgs_gpu_scene* scene, const lodgs_camera* cam,
     return guarded([&] {
         need(cam, "cam");
         need(params, "params");
-        S(scene).enqueue_frame(*cam, *params, image_host);
+        S(scene).enqueue_async(*cam, *params, image_host);
     });
 }
 
 int lodgs_gpu_sync(lodgs_gpu_scene* scene, lodgs_render_stats* stats) {
-    return guarded([&] { S(scene).finish(stats); });
+    return guarded([&] { S(scene).sync_async(stats); });
 }
 
 int lodgs_gpu_take_totals(lodgs_gpu_scene* scene, uint64_t* frames, uint64_t* sum_selected,
@@ -229,6 +229,14 @@ int lodgs_gpu_take_totals(lodgs_gpu_scene* scene, uint64_t* frames, uint64_t* su
         [&] { S(scene).take_totals(frames, sum_selected, sum_pairs, sum_sort_bytes); });
 }
 
+
+int lodgs_gpu_scene_set_inflight(lodgs_gpu_scene* scene, int frames) {
+    return guarded([&] { S(scene).set_inflight(frames); });
+}
+
+int lodgs_gpu_join(lodgs_gpu_scene* scene) {
+    return guarded([&] { S(scene).join(); });
+}
 
 int lodgs_gpu_profile(lodgs_gpu_scene* scene, int enable) {
     return guarded([&] { S(scene).profile(enable != 0); });

@@ -43,6 +43,13 @@ namespace {
 uint64_t align256(uint64_t b) { return (b + 255) / 256 * 256; }
 }  // namespace
 
+void GpuScene::init_control() {
+    // the control stream (timing events, fork/join of in-flight frames)
+    FGS_CUDA(cudaStreamCreateWithFlags(&ctl_, cudaStreamNonBlocking));
+    FGS_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
+    for (auto& e : join_ev_) FGS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
 void GpuScene::init_device(int device) {
     int count = 0;
     FGS_CUDA(cudaGetDeviceCount(&count));
@@ -65,6 +72,7 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
     if (!per_node && nv) throw Error(LODGS_ERR_VALIDATION, join_violations("invalid tree", msgs, nv));
     init_device(device);
     DeviceGuard dg(device_);
+    init_control();
     const uint64_t n = tree.n_nodes;
     IngestStage st;
     st.soa.alloc(14 * n);
@@ -166,6 +174,7 @@ GpuScene::GpuScene(const std::string& path, int device, double* timing_ms) : dev
     if (!per_node && nv) throw Error(LODGS_ERR_VALIDATION, join_violations("invalid tree", msgs, nv));
     init_device(device);
     DeviceGuard dg(device_);
+    init_control();
     // payload -> device through two pinned chunks (read of chunk k+1 overlaps the copy of k)
     DevBuf<uint8_t> dpay;
     dpay.alloc(payload);
@@ -295,21 +304,92 @@ void GpuScene::ingest(uint64_t n, const std::vector<uint64_t>& level_begin, bool
     tree_.parent = parent_.p;
     tree_.splat = splat_.p;
     tree_.sig3 = sig3_.p;
+    alloc_frame_buffers(std::max<uint64_t>(4 * n, 1u << 16));
+}
 
+void GpuScene::alloc_frame_buffers(uint64_t pairs) {
+    const uint64_t n = tree_.n;
     cand_bits_.alloc(bit_words(n));
     qint_bits_.alloc(bit_words(n));
     selected_.alloc(n);
     g64_.alloc(n);
     g32_.alloc(n);
     emit_.alloc(n);
-    reserve_pairs(std::max<uint64_t>(4 * n, 1u << 16));  // grown on overflow
+    reserve_pairs(pairs);  // grown on overflow
     totals_.alloc(1);
     FGS_CUDA(cudaMemsetAsync(totals_.p, 0, sizeof(RunTotals), stream_));
     FGS_CUDA(cudaStreamSynchronize(stream_));
 }
 
+// A second frame context over the same device tree (frames in flight): its own
+// stream, counters and per-frame buffers; the tree storage stays the owner's.
+GpuScene::GpuScene(const GpuScene& owner, TwinTag) : device_(owner.device_) {
+    init_device(device_);
+    DeviceGuard dg(device_);
+    tree_ = owner.tree_;
+    level_begin_ = owner.level_begin_;
+    shrink_factor_ = owner.shrink_factor_;
+    alloc_frame_buffers(owner.pair_cap_);
+}
+
+void GpuScene::set_inflight(int n) {
+    if (n < 1 || n > 2) throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1 or 2");
+    join();
+    inflight_ = n;
+}
+
+void GpuScene::join() {
+    if (!ctl_) return;
+    DeviceGuard dg(device_);
+    FGS_CUDA(cudaEventRecord(join_ev_[0], stream_));
+    FGS_CUDA(cudaStreamWaitEvent(ctl_, join_ev_[0], 0));
+    if (twin_) {
+        FGS_CUDA(cudaEventRecord(join_ev_[1], twin_->stream_));
+        FGS_CUDA(cudaStreamWaitEvent(ctl_, join_ev_[1], 0));
+    }
+}
+
+void GpuScene::enqueue_async(const lodgs_camera& cam, const lodgs_render_params& p,
+                             float* image_host) {
+    DeviceGuard dg(device_);
+    if (inflight_ < 2 || profiling_ || !ctl_) {
+        if (ctl_) {  // still ordered after the control stream's events
+            FGS_CUDA(cudaEventRecord(fork_ev_, ctl_));
+            FGS_CUDA(cudaStreamWaitEvent(stream_, fork_ev_, 0));
+        }
+        enqueue_frame(cam, p, image_host);
+        last_frame_ = this;
+        return;
+    }
+    if (!twin_) twin_.reset(new GpuScene(*this, TwinTag{}));
+    GpuScene* tgt = (async_frames_++ & 1) ? twin_.get() : this;
+    // fork from the control stream: the frame orders after the caller's events
+    // there (e.g. a timing start), not after the other context's frames
+    FGS_CUDA(cudaEventRecord(fork_ev_, ctl_));
+    FGS_CUDA(cudaStreamWaitEvent(tgt->stream_, fork_ev_, 0));
+    tgt->enqueue_frame(cam, p, image_host);
+    last_frame_ = tgt;
+}
+
+void GpuScene::sync_async(lodgs_render_stats* stats) {
+    DeviceGuard dg(device_);
+    join();
+    if (ctl_) FGS_CUDA(cudaStreamSynchronize(ctl_));
+    (last_frame_ ? last_frame_ : this)->finish(stats);
+}
+
 GpuScene::~GpuScene() {
     cudaSetDevice(device_);
+    if (twin_) {
+        cudaStreamSynchronize(twin_->stream_);
+        twin_.reset();
+    }
+    if (ctl_) {
+        cudaStreamSynchronize(ctl_);
+        cudaStreamDestroy(ctl_);
+        cudaEventDestroy(fork_ev_);
+        for (auto& e : join_ev_) cudaEventDestroy(e);
+    }
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
@@ -330,6 +410,7 @@ GpuScene::~GpuScene() {
 
 void GpuScene::reserve_pairs(uint64_t n) {
     DeviceGuard dg(device_);
+    if (twin_) twin_->reserve_pairs(n);
     if (n > 0xFFFFFFF0ull) n = 0xFFFFFFF0ull;
     if (n <= pair_cap_) return;
     if (stream_) FGS_CUDA(cudaStreamSynchronize(stream_));
@@ -339,7 +420,8 @@ void GpuScene::reserve_pairs(uint64_t n) {
 }
 
 uint64_t GpuScene::device_bytes() const {
-    return geo_.bytes() + iscale_.bytes() + iquat_.bytes() + parent_.bytes() + splat_.bytes() +
+    return (twin_ ? twin_->device_bytes() : 0) + geo_.bytes() + iscale_.bytes() + iquat_.bytes() +
+           parent_.bytes() + splat_.bytes() +
            sig3_.bytes() +
            cand_bits_.bytes() + qint_bits_.bytes() + selected_.bytes() + g64_.bytes() +
            g32_.bytes() + emit_.bytes() + col64_.bytes() + keys_.bytes() + zero_.bytes() +
@@ -509,6 +591,7 @@ void GpuScene::finish(lodgs_render_stats* stats) {
 
 void GpuScene::render(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host,
                       lodgs_render_stats* stats) {
+    last_frame_ = this;
     for (int attempt = 0;; ++attempt) {
         enqueue_frame(cam, p, image_host);
         try {
@@ -627,6 +710,11 @@ uint64_t GpuScene::filter(const lodgs_camera& cam, double tau_r, std::vector<uin
 
 void GpuScene::read_image_rgb8(uint8_t* out) {
     DeviceGuard dg(device_);
+    if (last_frame_ && last_frame_ != this) {
+        join();
+        last_frame_->read_image_rgb8(out);
+        return;
+    }
     const uint64_t n = image_floats();
     rgb8_.alloc(n);
     launch_rgb8(res_.image.p, n, rgb8_.p, stream_);
@@ -769,6 +857,11 @@ uint64_t GpuScene::prepare(const lodgs_camera& cam, const uint32_t* selected, ui
 
 void GpuScene::read_image(float* out) {
     DeviceGuard dg(device_);
+    if (last_frame_ && last_frame_ != this) {  // the last async frame ran on the twin
+        join();
+        last_frame_->read_image(out);
+        return;
+    }
     FGS_CUDA(cudaStreamSynchronize(stream_));
     FGS_CUDA(cudaMemcpy(out, res_.image.p, image_floats() * sizeof(float), cudaMemcpyDeviceToHost));
 }
@@ -956,6 +1049,23 @@ uint64_t GpuScene::profile_read(double stage_ms[6]) {
 
 void GpuScene::take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs,
                            uint64_t* sum_sort_bytes) {
+    DeviceGuard dg(device_);
+    if (twin_) {
+        uint64_t f = 0, s = 0, p = 0, b = 0;
+        twin_->take_totals(&f, &s, &p, &b);  // throws (after growing) on overflow
+        uint64_t f0 = 0, s0 = 0, p0 = 0, b0 = 0;
+        take_totals_own(&f0, &s0, &p0, &b0);
+        if (frames) *frames = f + f0;
+        if (sum_sel) *sum_sel = s + s0;
+        if (sum_pairs) *sum_pairs = p + p0;
+        if (sum_sort_bytes) *sum_sort_bytes = b + b0;
+        return;
+    }
+    take_totals_own(frames, sum_sel, sum_pairs, sum_sort_bytes);
+}
+
+void GpuScene::take_totals_own(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs,
+                               uint64_t* sum_sort_bytes) {
     DeviceGuard dg(device_);
     RunTotals t;
     FGS_CUDA(cudaStreamSynchronize(stream_));

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <array>
 #include <string>
 #include <vector>
@@ -110,6 +111,8 @@ public:
     void read_counts(uint32_t* per_gaussian, uint64_t cap_g, uint32_t* per_tile, uint64_t cap_t);
     void take_totals(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs,
                      uint64_t* sum_sort_bytes = nullptr);
+    void take_totals_own(uint64_t* frames, uint64_t* sum_sel, uint64_t* sum_pairs,
+                         uint64_t* sum_sort_bytes);
     uint64_t read_kpc(double* out, uint64_t cap);
     void calibrate(const lodgs_camera* views, uint32_t n_views, double lambda_g, double tau_r,
                    lodgs_calibration* out, double* per_view);
@@ -121,10 +124,19 @@ public:
     void set_reference_image();
     void compare_reference(double* psnr, double* ssim);
 
+    // Frames in flight (1 or 2, default 2): render_async alternates frames between
+    // this context and a twin context (own stream and per-frame buffers, same
+    // device tree), forked from the control stream; join() makes the control
+    // stream wait for both.  stream() is the control stream once a twin exists.
+    void set_inflight(int n);
+    void enqueue_async(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host);
+    void join();
+    void sync_async(lodgs_render_stats* stats);
+
     void profile(bool enable);
     uint64_t profile_read(double stage_ms[6]);
 
-    cudaStream_t stream() const { return stream_; }
+    cudaStream_t stream() const { return ctl_ ? ctl_ : stream_; }
     int device() const { return device_; }
     uint64_t n_nodes() const { return tree_.n; }
 
@@ -132,7 +144,11 @@ public:
     const std::vector<uint64_t>& level_begin() const { return level_begin_; }
 
 private:
+    struct TwinTag {};
+    GpuScene(const GpuScene& owner, TwinTag);
+    void alloc_frame_buffers(uint64_t pairs);
     void init_device(int device);
+    void init_control();
     void ingest(uint64_t n, const std::vector<uint64_t>& level_begin, bool per_node,
                 std::vector<std::string>& msgs, uint64_t nv, IngestStage& st);
     void ensure_resolution(int w, int h);
@@ -145,6 +161,13 @@ private:
     DevTree tree_;
     std::vector<uint64_t> level_begin_;  // scene.hpp:53 level_begin(l), host copy
     float shrink_factor_ = 0.5f;
+    // frames in flight
+    int inflight_ = 2;
+    std::unique_ptr<GpuScene> twin_;
+    cudaStream_t ctl_ = nullptr;
+    cudaEvent_t fork_ev_ = nullptr, join_ev_[2] = {};
+    uint64_t async_frames_ = 0;
+    GpuScene* last_frame_ = nullptr;
     DevBuf<unsigned> level_flag_;        // serial filter: level had an active node
     bool last_serial_ = false;
     // tree storage

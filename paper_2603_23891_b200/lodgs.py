@@ -178,7 +178,7 @@ ABI_SYMBOLS = (
     "lodgs_gpu_sort_pairs", "lodgs_gpu_alpha_blend", "lodgs_gpu_host_alloc",
     "lodgs_gpu_host_free", "lodgs_gpu_read_image_rgb8", "lodgs_gpu_set_reference_image",
     "lodgs_gpu_compare_reference", "lodgs_gpu_image_metrics", "lodgs_gpu_scene_load",
-    "lodgs_gpu_scene_info",
+    "lodgs_gpu_scene_info", "lodgs_gpu_scene_set_inflight", "lodgs_gpu_join",
 )
 
 _lib = None
@@ -237,6 +237,8 @@ def load_library():
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32)]),
         "lodgs_gpu_read_image_rgb8": (C.c_int, [P, P]),
+        "lodgs_gpu_scene_set_inflight": (C.c_int, [P, C.c_int]),
+        "lodgs_gpu_join": (C.c_int, [P]),
         "lodgs_gpu_scene_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(P), _DP]),
         "lodgs_gpu_scene_info": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), P,
                                            C.c_uint32, C.POINTER(C.c_float)]),
@@ -775,6 +777,14 @@ class GpuScene:
     def render_async(self, cam: Camera, params: RenderParamsC, image_host_ptr=None):
         c = cam.to_c()
         _check(self._lib.lodgs_gpu_render_async(self._h, C.byref(c), C.byref(params), image_host_ptr))
+
+    def join(self) -> None:
+        """The control stream (stream_ptr) waits for every frame enqueued so far."""
+        _check(self._lib.lodgs_gpu_join(self._h))
+
+    def set_inflight(self, frames: int) -> None:
+        """Frames in flight for render_async (1 or 2, default 2)."""
+        _check(self._lib.lodgs_gpu_scene_set_inflight(self._h, int(frames)))
 
     def sync(self) -> RenderStats:
         st = RenderStatsC()

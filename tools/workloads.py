@@ -54,6 +54,7 @@ def time_frames(scene, cams, mode, tau_r=3.0, reps=1):
     for _ in range(reps):
         for cam in cams:
             scene.render_async(cam, p)
+    scene.join()
     ev1.record(stream)
     ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
@@ -96,6 +97,7 @@ def run_cfg5(n_views=1024):
         ev0.record(stream)
         for cam in mine:
             scene.render_async(cam, p)
+        scene.join()
         ev1.record(stream)
         ev1.synchronize()
         ms = ev0.elapsed_time(ev1)
