@@ -579,6 +579,37 @@ def test_render_batch_matches_single_frames(L, oracle, gpu):
             assert max_abs(im, want["image"]) <= IMG_TOL
 
 
+def test_render_async_two_frames_in_flight(L, oracle, gpu):
+    """lodgs_gpu_render_async with two frames in flight (scene + twin context):
+    every frame's image and the run totals equal the synchronous renders; the
+    last frame is what sync() reports and read_image() returns; with one frame
+    in flight the same holds."""
+    tree = L.make_tree(23, 3, 8, 0.5, 4, 4, 2)
+    rng = oracle.rng(29)
+    cams = [oracle.orbit_camera(rng, 200, 150, 16.0) for _ in range(7)]
+    for c in cams:
+        c.fx = c.fy = 150.0
+    mode = L.ShrinkMode.three_sigma()
+    with L.GpuScene(tree) as s:
+        ref = [s.render(cam, L.FilterConfig(4.0), mode) for cam in cams]
+        for inflight in (2, 1):
+            s.set_inflight(inflight)
+            p = s.params(L.FilterConfig(4.0), mode, L.RenderOptions())
+            imgs = [np.empty((150, 200, 3), np.float32) for _ in cams]
+            s.take_totals()
+            for cam, im in zip(cams, imgs):
+                s.render_async(cam, p, im.ctypes.data)
+            last = s.sync()
+            frames, sel, pairs = s.take_totals()
+            assert frames == len(cams)
+            assert sel == sum(r.stats.n_selected for r in ref)
+            assert pairs == sum(r.stats.n_pairs for r in ref)
+            for im, r in zip(imgs, ref):
+                assert im.tobytes() == r.image.rgb.tobytes()
+            assert last.n_pairs == ref[-1].stats.n_pairs
+            assert s.read_image(cams[-1]).tobytes() == ref[-1].image.rgb.tobytes()
+
+
 def test_cfg4_50m_4k(L, oracle, gpu):
     """cfg 4 scale (50,142,872 nodes, 3840x2160, fx = 2000): selected list
     bit-exact at altitude 300, and a full frame at altitude 400 (pairs, counts,
