@@ -453,7 +453,9 @@ uint64_t build_synthetic(const lodgs_synthetic_spec& s, const lodgs_build_config
                     const uint32_t j = i + uint32_t(rng.next_below(8 - i));
                     std::swap(corners[i], corners[j]);
                 }
-                std::sort(corners, corners + c.children_per_node);
+                for (uint32_t a = 1; a < c.children_per_node; ++a)  // sort the chosen corners
+                    for (uint32_t b2 = a; b2 > 0 && corners[b2 - 1] > corners[b2]; --b2)
+                        std::swap(corners[b2 - 1], corners[b2]);
             }
             for (uint32_t ci = 0; ci < c.children_per_node; ++ci) {
                 const uint32_t cn = corners[ci];
