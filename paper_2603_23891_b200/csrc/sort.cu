@@ -152,6 +152,142 @@ __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint3
     }
 }
 
+// 32-bit variant of the register network for buckets whose depth bits span
+// less than 2^20 (a tile's splats sit in a narrow depth band): key32 =
+// (depth_bits - min) << 12 | position in the bucket.  Half the shuffles, one
+// compare and one select per exchange.  Equal depth bits then come out in
+// bucket order, not slot order, so the gathered 64-bit keys get odd-even
+// transposition passes until stable -- adjacent swaps only ever happen inside
+// runs of equal depth, which are short.  Returns false (nothing written) when
+// the bucket's depth range is too wide; the caller then runs the 64-bit
+// network.  All kSmallSortThreads threads of the CTA must call it.
+template <int LOGP>
+__device__ __forceinline__ bool register_bitonic32(unsigned long long* keys, uint32_t n,
+                                                   unsigned long long* s) {
+    constexpr uint32_t P = 1u << LOGP;
+    constexpr int R = P > uint32_t(kSmallSortThreads) ? int(P / kSmallSortThreads) : 1;
+    constexpr uint32_t lanes = P < uint32_t(kSmallSortThreads) ? P : uint32_t(kSmallSortThreads);
+    static_assert(P <= 1024, "positions take 12 bits, the staging 8 KB");
+    __shared__ uint32_t s_red[2][kSmallSortThreads / 32];
+    const uint32_t tid = threadIdx.x;
+    const unsigned lane = tid & 31, warp = tid >> 5;
+    unsigned long long* s_orig = s;                                   // P keys
+    uint32_t* s_x = reinterpret_cast<uint32_t*>(s + P);               // 2 x P exchange
+    unsigned long long* s_out = s + 2 * P;                            // P sorted keys
+    unsigned long long v[R];
+    uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+        v[r] = (tid < lanes && i < n) ? keys[i] : ~0ull;
+        if (tid < lanes && i < n) {
+            s_orig[i] = v[r];
+            const uint32_t d = uint32_t(v[r] >> 32);
+            dmin = min(dmin, d);
+            dmax = max(dmax, d);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        dmin = min(dmin, __shfl_xor_sync(0xffffffffu, dmin, off));
+        dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+    }
+    if (lane == 0) {
+        s_red[0][warp] = dmin;
+        s_red[1][warp] = dmax;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kSmallSortThreads / 32; ++w) {
+        dmin = min(dmin, s_red[0][w]);
+        dmax = max(dmax, s_red[1][w]);
+    }
+    if (dmax - dmin >= (1u << 20)) return false;  // uniform across the CTA
+    uint32_t k32[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+        k32[r] = i < n ? ((uint32_t(v[r] >> 32) - dmin) << 12 | i) : 0xFFFFFFFFu;
+    }
+    if (tid < lanes) {
+        int parity = 0;
+#pragma unroll
+        for (uint32_t k = 2; k <= P; k <<= 1) {
+#pragma unroll
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                if (j >= uint32_t(kSmallSortThreads)) {
+                    auto cas = [&](uint32_t& a, uint32_t& c, int r) {
+                        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+                        const bool up = (i & k) == 0;
+                        const uint32_t lo = min(a, c), hi = max(a, c);
+                        a = up ? lo : hi;
+                        c = up ? hi : lo;
+                    };
+                    if constexpr (R == 2) {
+                        cas(k32[0], k32[1], 0);
+                    } else if constexpr (R == 4) {
+                        if (j == uint32_t(kSmallSortThreads)) {
+                            cas(k32[0], k32[1], 0);
+                            cas(k32[2], k32[3], 2);
+                        } else {
+                            cas(k32[0], k32[2], 0);
+                            cas(k32[1], k32[3], 1);
+                        }
+                    }
+                } else if (j >= 32) {
+                    uint32_t* buf = s_x + (parity ? R * kSmallSortThreads : 0);
+                    parity ^= 1;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) buf[r * kSmallSortThreads + tid] = k32[r];
+                    asm volatile("bar.sync 1, %0;" ::"r"(lanes) : "memory");
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+                        const uint32_t o = buf[r * kSmallSortThreads + (tid ^ j)];
+                        const bool keep_min = ((i & j) == 0) == ((i & k) == 0);
+                        k32[r] = keep_min ? min(o, k32[r]) : max(o, k32[r]);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+                        const uint32_t o = __shfl_xor_sync(0xffffffffu, k32[r], int(j));
+                        const bool keep_min = ((i & j) == 0) == ((i & k) == 0);
+                        k32[r] = keep_min ? min(o, k32[r]) : max(o, k32[r]);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();  // s_orig complete everywhere
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
+        if (tid < lanes && i < n) s_out[i] = s_orig[k32[r] & 0xFFFu];
+    }
+    __syncthreads();
+    // odd-even transposition inside runs of equal depth: (depth, slot) order
+    while (true) {
+        bool swapped = false;
+#pragma unroll
+        for (int ph = 0; ph < 2; ++ph) {
+            for (uint32_t p = tid; 2 * p + ph + 1 < n; p += kSmallSortThreads) {
+                const uint32_t a = 2 * p + ph;
+                const unsigned long long x = s_out[a], y = s_out[a + 1];
+                if (y < x) {
+                    s_out[a] = y;
+                    s_out[a + 1] = x;
+                    swapped = true;
+                }
+            }
+            __syncthreads();
+        }
+        if (!__syncthreads_or(swapped)) break;
+    }
+    for (uint32_t i = tid; i < n; i += kSmallSortThreads) keys[i] = s_out[i];
+    return true;
+}
+
 __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t* __restrict__ offsets,
                                                                  const uint32_t* __restrict__ order,
                                                                  unsigned long long* keys) {
@@ -162,6 +298,22 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t*
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
     const uint32_t n = e - b;
     if (n < 2 || n > uint32_t(kSmallSortCap)) return;  // big buckets: k_tile_sort_big
+#ifndef SORT32
+#define SORT32 1
+#endif
+#if SORT32
+    if (n <= 1024u) {
+        bool done;
+        if (n <= 32u) done = register_bitonic32<5>(keys + b, n, s);
+        else if (n <= 64u) done = register_bitonic32<6>(keys + b, n, s);
+        else if (n <= 128u) done = register_bitonic32<7>(keys + b, n, s);
+        else if (n <= 256u) done = register_bitonic32<8>(keys + b, n, s);
+        else if (n <= 512u) done = register_bitonic32<9>(keys + b, n, s);
+        else done = register_bitonic32<10>(keys + b, n, s);
+        if (done) return;
+        __syncthreads();  // staging in s is reused by the 64-bit network
+    }
+#endif
     if (n <= uint32_t(kRegCap)) {
         if (n <= 32u) register_bitonic<5>(keys + b, n, s);
         else if (n <= 64u) register_bitonic<6>(keys + b, n, s);
