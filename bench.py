@@ -309,11 +309,22 @@ def run_b200(args, rank, world, local):
         scene.render_batch(e2e_frames, L.FilterConfig(TAU_R), L.ShrinkMode.three_sigma(),
                            host_ptrs=[ring[i % 4] for i in range(len(e2e_frames))])
     e2e_s = time.perf_counter() - t0
+    # the same frames with 8-bit images out (the reference CLI's render -> save_ppm
+    # bytes; LODGS_RENDER_OUTPUT_RGB8): 6.2 MB per 1080p frame instead of 24.9 MB
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    scene.render_batch(e2e_frames, L.FilterConfig(TAU_R), L.ShrinkMode.three_sigma(),
+                       L.RenderOptions(output_rgb8=True),
+                       host_ptrs=[ring[i % 4] for i in range(len(e2e_frames))])
+    e2e8_s = time.perf_counter() - t0
     for p in ring:
         L.load_library().lodgs_gpu_host_free(p)
 
     # max over ranks of the timed regions; per-rank counters summed
     ms_max, _ = reduce_timing(dist, ms, [], device="cuda")
+    e2e8_max, _ = reduce_timing(dist, e2e8_s, [], device="cuda")
     e2e_max, (sum_sel_all, sum_pairs_all, nf_all) = reduce_timing(
         dist, e2e_s, [sum_sel, sum_pairs, nf], device="cuda")
     sum_sel, sum_pairs, nf = sum_sel_all, sum_pairs_all, int(nf_all)
@@ -374,7 +385,13 @@ def run_b200(args, rank, world, local):
         "e2e": {"value": e2e_fps, "unit": "frames/s",
                 "h2d_bytes_per_step": C.sizeof(L.CameraC) + C.sizeof(L.RenderParamsC),
                 "d2h_bytes_per_step": img_bytes + 64, "frames": len(e2e_frames),
-                "call": "lodgs_gpu_render" if args.e2e_sync else "lodgs_gpu_render_batch"},
+                "call": "lodgs_gpu_render" if args.e2e_sync else "lodgs_gpu_render_batch",
+                "pcie_note": "f32 RGB image per frame (lodgs::render's Image): D2H-bound "
+                             "(~56 GB/s measured, tools/micro/d2h_bw.py)"},
+        "e2e_rgb8": {"value": world * len(e2e_frames) / e2e8_max, "unit": "frames/s",
+                     "h2d_bytes_per_step": C.sizeof(L.CameraC) + C.sizeof(L.RenderParamsC),
+                     "d2h_bytes_per_step": W * H * 3 + 64,
+                     "call": "lodgs_gpu_render_batch + LODGS_RENDER_OUTPUT_RGB8 (save_ppm bytes)"},
         "gpu_launches": int(launches_per_frame) * K,
         "clocks": clocks.summary(),
         "setup_s": build_s,

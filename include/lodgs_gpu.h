@@ -82,7 +82,9 @@ enum lodgs_render_flags {
     LODGS_RENDER_KEEP_PAIRS = 2u,   /* keep sorted pairs + gaussians readable after the frame */
     LODGS_RENDER_STAGE_TIMING = 4u, /* CUDA-event stage timers into lodgs_render_stats */
     LODGS_RENDER_COLLECT_KPC = 8u,  /* RenderOptions::collect_kpc: per-pair kpc, exact blend */
-    LODGS_RENDER_FILTER_SERIAL = 16u /* RenderOptions::filter_mode = serial (filter.cpp:60-113) */
+    LODGS_RENDER_FILTER_SERIAL = 16u, /* RenderOptions::filter_mode = serial (filter.cpp:60-113) */
+    LODGS_RENDER_OUTPUT_RGB8 = 32u  /* render_batch: host images are W*H*3 bytes, save_ppm's
+                                       quantisation (image.cpp:19-22), 1/4 of the PCIe bytes */
 };
 
 /* FilterConfig (filter.hpp:11-14) + ShrinkMode (rasterizer.hpp:16-24). */

@@ -635,8 +635,12 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
         FGS_CUDA(cudaMallocHost(&h_batch_counters_, n * sizeof(FrameCounters)));
         h_batch_cap_ = n;
     }
+    const bool rgb8 = (p.flags & LODGS_RENDER_OUTPUT_RGB8) != 0;
     const uint64_t img_bytes = image_floats() * sizeof(float);
+    const uint64_t out_bytes = rgb8 ? image_floats() : img_bytes;
     float* bufs[2] = {res_.image.p, image2_.p};
+    if (rgb8)
+        for (auto& b8 : rgb8b_) b8.alloc(image_floats());
     last_timing_ = false;
     last_keep_ = false;
     last_exact_ = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
@@ -649,11 +653,13 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
         enqueue_pipeline(camera_geom(cams[i]), p, int(cams[i].width), int(cams[i].height), false);
         image_target_ = nullptr;
         log_target_ = nullptr;
+        if (rgb8) launch_rgb8(bufs[k], image_floats(), rgb8b_[k].p, stream_);
         FGS_CUDA(cudaEventRecord(frame_done_[k], stream_));
         FGS_CUDA(cudaStreamWaitEvent(copy_stream_, frame_done_[k], 0));
         if (images_host && images_host[i])
-            FGS_CUDA(cudaMemcpyAsync(images_host[i], bufs[k], img_bytes, cudaMemcpyDeviceToHost,
-                                     copy_stream_));
+            FGS_CUDA(cudaMemcpyAsync(images_host[i],
+                                     rgb8 ? static_cast<const void*>(rgb8b_[k].p) : bufs[k],
+                                     out_bytes, cudaMemcpyDeviceToHost, copy_stream_));
         FGS_CUDA(cudaEventRecord(copy_done_[k], copy_stream_));
     }
     // every frame's counters in one copy, after the last frame

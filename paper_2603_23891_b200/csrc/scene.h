@@ -217,6 +217,7 @@ private:
     // pipelined batches: second image buffer, copy stream, per-frame counters
     float* image_target_ = nullptr;  // blend output override (nullptr: res_.image)
     DevBuf<float> image2_;
+    DevBuf<uint8_t> rgb8b_[2];  // render_batch with LODGS_RENDER_OUTPUT_RGB8
     cudaStream_t copy_stream_ = nullptr;
     cudaEvent_t frame_done_[2] = {}, copy_done_[2] = {};
     FrameCounters* h_batch_counters_ = nullptr;

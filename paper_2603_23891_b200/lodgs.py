@@ -441,6 +441,7 @@ class RenderOptions:
     filter_mode: str = "parallel"
     exact_blend: bool = False
     stage_timing: bool = False
+    output_rgb8: bool = False  # render_batch host images are W*H*3 bytes (save_ppm quantisation)
 
 
 @dataclasses.dataclass
@@ -725,7 +726,8 @@ class GpuScene:
         if opts.filter_mode not in ("parallel", "serial"):
             raise ValidationError("render: filter_mode is 'parallel' or 'serial'")
         flags = (1 if opts.exact_blend else 0) | (2 | 8 if opts.collect_kpc else 0) | \
-                (4 if opts.stage_timing else 0) | (16 if opts.filter_mode == "serial" else 0)
+                (4 if opts.stage_timing else 0) | (16 if opts.filter_mode == "serial" else 0) | \
+                (32 if opts.output_rgb8 else 0)
         return RenderParamsC(float(filter.tau_r), float(mode.tau), int(mode.kind), flags)
 
     def render(self, cam: Camera, filter: FilterConfig, mode: ShrinkMode,

@@ -96,3 +96,20 @@ def test_render_filter_serial_mode(L, oracle, ref, gpu):
     with pytest.raises(L.ValidationError):
         L.GpuScene.params(L.FilterConfig(3.0), L.ShrinkMode.three_sigma(),
                           L.RenderOptions(filter_mode="oracle"))
+
+
+def test_render_batch_rgb8_output(L, oracle, gpu):
+    """render_batch with LODGS_RENDER_OUTPUT_RGB8: every host image is the
+    save_ppm quantisation of the frame's f32 image."""
+    tree = L.make_tree(21, 3, 8, 0.5, 3, 3, 2)
+    rng = oracle.rng(5)
+    cams = [oracle.orbit_camera(rng, 200, 150, 14.0) for _ in range(4)]
+    for c in cams:
+        c.fx = c.fy = 150.0
+    b8 = [np.zeros((150, 200, 3), np.uint8) for _ in cams]
+    with L.GpuScene(tree) as s:
+        s.render_batch(cams, L.FilterConfig(4.0), L.ShrinkMode.three_sigma(),
+                       L.RenderOptions(output_rgb8=True), host_ptrs=[b.ctypes.data for b in b8])
+        for cam, b in zip(cams, b8):
+            f = s.render(cam, L.FilterConfig(4.0), L.ShrinkMode.three_sigma()).image.rgb
+            assert np.array_equal(b, _rgb8_restated(f))
