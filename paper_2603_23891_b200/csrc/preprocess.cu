@@ -59,7 +59,7 @@ __device__ __forceinline__ Projected project_one(const Geom& g, const SplatRec& 
         if (!frustum_literal(g, m.tx, m.ty, m.tz, 3.0 * smax)) return p;
     }
     if (!(m.tz >= g.znear)) return p;  // z_ok (mark_core.hpp:41)
-    ewa_from_sigma(g, m.tx, m.ty, m.tz, S, m);
+    ewa_from_sigma<false>(g, m.tx, m.ty, m.tz, S, m);
     // projection.cpp:73 divides by tz; ewa used 1 / max(tz, 1e-12), the same
     // quotient whenever tz >= 1e-12
     const double inv_z = m.tz < 1e-12 ? 1.0 / m.tz : m.inv_zc;
@@ -70,12 +70,15 @@ __device__ __forceinline__ Projected project_one(const Geom& g, const SplatRec& 
     p.cb = -m.b / det;
     p.cc = m.a / det;
     const double sigma_max = sqrt(m.lambda_max);
-    const double sigma_min = sqrt(m.lambda_min);
     p.depth = m.tz;
+    // projection.cpp:85-89 checks sigma_min = sqrt(lambda_min) and mark_core's
+    // radius = 3 sqrt(lambda_max) for finiteness: for a finite argument x,
+    // sqrt(x) is finite iff x >= 0 (NaN otherwise; sqrt(-0) = -0), and 3 sigma_max
+    // is finite iff sigma_max is -- the same predicate without the two roots.
+    const bool sigma_min_finite = isfinite(m.lambda_min) && m.lambda_min >= 0.0;
     p.nonfinite = !(isfinite(p.mx) && isfinite(p.my) && isfinite(m.a) && isfinite(m.b) &&
                     isfinite(m.c) && isfinite(p.ca) && isfinite(p.cb) && isfinite(p.cc) &&
-                    isfinite(sigma_max) && isfinite(sigma_min) && isfinite(m.tz) &&
-                    isfinite(m.radius));
+                    isfinite(sigma_max) && sigma_min_finite && isfinite(m.tz));
     p.radius = effective_radius(sigma_max, r.opacity, kind, tau);
     p.keep = true;
     return p;
