@@ -1,0 +1,22 @@
+"""Per-stage device times of cfg-4 frames (50M-node tree, 3840x2160, fx 2000) at a few
+altitudes, three-sigma: where a 4K frame spends its time."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from helpers import topdown_camera  # noqa: E402
+from paper_2603_23891_b200 import lodgs as L  # noqa: E402
+
+tree = L.build_synthetic_tree(nx=103, ny=104, seed=1, depth=4, build_seed=7)
+with L.GpuScene(tree) as s:
+    for alt in (400.0, 300.0, 200.0, 110.0):
+        cam = topdown_camera(3840, 2160, 2000.0, alt)
+        for _ in range(3):
+            out = s.render(cam, L.FilterConfig(3.0), L.ShrinkMode.three_sigma(),
+                           L.RenderOptions(stage_timing=True))
+        st = out.stats
+        print(f"alt {alt}: sel {st.n_selected} pairs {st.n_pairs} big {st.big_tiles} "
+              f"filter {st.t_calc_ms:.3f} prep {st.t_prepr_ms:.3f} sort {st.t_sort_ms:.3f} "
+              f"blend {st.t_alpha_ms:.3f} ms", flush=True)
