@@ -104,7 +104,7 @@ void launch_compact_records(const uint32_t* slot_of_g, uint64_t n_g, const Gauss
                             GaussEmit* oe, cudaStream_t s);
 
 // ---- sort (rasterizer.cpp:100-135) ----
-constexpr int kSmallSortCap = 4096;
+constexpr int kSmallSortCap = 2048;
 constexpr int kBigSortCap = 16384;
 void launch_tile_sort(const uint32_t* offsets, const uint32_t* order, int n_tiles,
                       unsigned long long* keys, cudaStream_t s);

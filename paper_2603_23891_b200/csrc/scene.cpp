@@ -522,7 +522,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     if (pe) FGS_CUDA(cudaEventRecord(pe[3], stream_));
     launch_tile_sort(res_.tile_offsets.p, res_.tile_order.p, n_tiles, keys_.p, stream_);
     launch_tile_sort_big(res_.tile_offsets.p, keys_.p, res_.big_list.p, d_counters_,
-                         std::min(sm_count_, 64), stream_);
+                         sm_count_, stream_);
     if (timing) FGS_CUDA(cudaEventRecord(ev_[3], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[4], stream_));
     float* img_out = image_target_ ? image_target_ : res_.image.p;
@@ -1222,7 +1222,9 @@ void stage_sort_pairs(lodgs_tile_pair* pairs, uint64_t n) {
     launch_tile_offsets(tc, n_buckets, off.p, cur.p, big.p, ord.p, cnt, n, c.s);
     launch_scatter_triples(in.p, n, cur.p, keys.p, c.s);
     launch_tile_sort(off.p, ord.p, n_buckets, keys.p, c.s);
-    launch_tile_sort_big(off.p, keys.p, big.p, cnt, 64, c.s);
+    int n_sm = 148;
+    FGS_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c.device));
+    launch_tile_sort_big(off.p, keys.p, big.p, cnt, n_sm, c.s);
     launch_gather_triples(off.p, n_buckets, keys.p, in.p, outb.p, c.s);
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaMemcpyAsync(pairs, outb.p, n * 12, cudaMemcpyDeviceToHost, c.s));

@@ -60,6 +60,33 @@ __device__ __forceinline__ void flip_bitonic(unsigned long long* a, Index n, Ind
 constexpr int kSmallSortThreads = 256;
 constexpr int kRegItems = 4;  // keys per thread in the register network
 constexpr int kRegCap = kSmallSortThreads * kRegItems;
+constexpr uint32_t kRun = 1024;  // run length of the run-sort + rank-merge path
+
+// Barriers over the threads that sort one bucket (or one run): the whole
+// 256-thread CTA of k_tile_sort, or one 256-thread group of k_tile_sort_big
+// (named barrier per group).
+struct CtaBar {
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ bool sync_or(bool p) const { return __syncthreads_or(p); }
+};
+struct GroupBar {
+    unsigned id;
+    __device__ __forceinline__ void sync() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kSmallSortThreads) : "memory");
+    }
+    __device__ __forceinline__ bool sync_or(bool p) const {
+        unsigned r;
+        asm volatile(
+            "{ .reg .pred q, o;\n\t"
+            "setp.ne.u32 q, %1, 0;\n\t"
+            "bar.red.or.pred o, %2, %3, q;\n\t"
+            "selp.u32 %0, 1, 0, o; }"
+            : "=r"(r)
+            : "r"(unsigned(p)), "r"(id), "r"(kSmallSortThreads)
+            : "memory");
+        return r != 0;
+    }
+};
 
 __device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v, int m) {
     const unsigned lo = __shfl_xor_sync(0xffffffffu, unsigned(v), m);
@@ -81,17 +108,19 @@ __device__ __forceinline__ unsigned long long bitonic_pick(unsigned long long mi
 // slots, padded with +inf.  Slot i = r * 256 + tid lives in register r of
 // thread tid, so partners at distance j < 32 are exchanged with warp shuffles,
 // 32 <= j < 256 through (double-buffered) shared memory with one named barrier
-// over the threads in play, j >= 256 inside the thread.  Only warps owning
-// slots < P take part: a 40-key bucket is one warp and never waits.
+// (xbar) over the threads in play, j >= 256 inside the thread.  Only warps
+// owning slots < P take part: a 40-key bucket is one warp and never waits.
 // P is a compile-time power of two (32..1024): every stage below unrolls with
-// constant distances, so the network is straight-line code.
+// constant distances, so the network is straight-line code.  keys -> out
+// (global or shared); tid is the thread's index among the 256 sorting threads.
 template <int LOGP>
-__device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint32_t n,
-                                                 unsigned long long* s_x) {
+__device__ __forceinline__ void register_bitonic(const unsigned long long* keys, uint32_t n,
+                                                 unsigned long long* out,
+                                                 unsigned long long* s_x, uint32_t tid,
+                                                 unsigned xbar) {
     constexpr uint32_t P = 1u << LOGP;
     constexpr int R = P > uint32_t(kSmallSortThreads) ? int(P / kSmallSortThreads) : 1;
     constexpr uint32_t lanes = P < uint32_t(kSmallSortThreads) ? P : uint32_t(kSmallSortThreads);
-    const uint32_t tid = threadIdx.x;
     if (tid >= lanes) return;  // whole warps (lanes is a multiple of 32)
     unsigned long long v[R];
 #pragma unroll
@@ -130,7 +159,7 @@ __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint3
                 parity ^= 1;
 #pragma unroll
                 for (int r = 0; r < R; ++r) buf[r * kSmallSortThreads + tid] = v[r];
-                asm volatile("bar.sync 1, %0;" ::"r"(lanes) : "memory");
+                asm volatile("bar.sync %0, %1;" ::"r"(xbar), "r"(lanes) : "memory");
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
@@ -148,7 +177,7 @@ __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint3
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
-        if (i < n) keys[i] = v[r];
+        if (i < n) out[i] = v[r];
     }
 }
 
@@ -160,20 +189,20 @@ __device__ __forceinline__ void register_bitonic(unsigned long long* keys, uint3
 // transposition passes until stable -- adjacent swaps only ever happen inside
 // runs of equal depth, which are short.  Returns false (nothing written) when
 // the bucket's depth range is too wide; the caller then runs the 64-bit
-// network.  All kSmallSortThreads threads of the CTA must call it.
-template <int LOGP>
-__device__ __forceinline__ bool register_bitonic32(unsigned long long* keys, uint32_t n,
-                                                   unsigned long long* s) {
+// network.  All 256 threads of the sorting group must call it.
+// Shared memory: s_orig (P keys), s_x (2P words), s_red (16 words); the sorted
+// keys land in s_out (shared) and, when dst is set, are copied there.
+template <int LOGP, class Bar>
+__device__ __forceinline__ bool register_bitonic32(const unsigned long long* keys, uint32_t n,
+                                                   unsigned long long* s_orig, uint32_t* s_x,
+                                                   uint32_t* s_red, unsigned long long* s_out,
+                                                   unsigned long long* dst, uint32_t tid,
+                                                   unsigned xbar, Bar bar) {
     constexpr uint32_t P = 1u << LOGP;
     constexpr int R = P > uint32_t(kSmallSortThreads) ? int(P / kSmallSortThreads) : 1;
     constexpr uint32_t lanes = P < uint32_t(kSmallSortThreads) ? P : uint32_t(kSmallSortThreads);
     static_assert(P <= 1024, "positions take 12 bits, the staging 8 KB");
-    __shared__ uint32_t s_red[2][kSmallSortThreads / 32];
-    const uint32_t tid = threadIdx.x;
     const unsigned lane = tid & 31, warp = tid >> 5;
-    unsigned long long* s_orig = s;                                   // P keys
-    uint32_t* s_x = reinterpret_cast<uint32_t*>(s + P);               // 2 x P exchange
-    unsigned long long* s_out = s + 2 * P;                            // P sorted keys
     unsigned long long v[R];
     uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
 #pragma unroll
@@ -193,16 +222,16 @@ __device__ __forceinline__ bool register_bitonic32(unsigned long long* keys, uin
         dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
     }
     if (lane == 0) {
-        s_red[0][warp] = dmin;
-        s_red[1][warp] = dmax;
+        s_red[warp] = dmin;
+        s_red[kSmallSortThreads / 32 + warp] = dmax;
     }
-    __syncthreads();
+    bar.sync();
 #pragma unroll
     for (int w = 0; w < kSmallSortThreads / 32; ++w) {
-        dmin = min(dmin, s_red[0][w]);
-        dmax = max(dmax, s_red[1][w]);
+        dmin = min(dmin, s_red[w]);
+        dmax = max(dmax, s_red[kSmallSortThreads / 32 + w]);
     }
-    if (dmax - dmin >= (1u << 20)) return false;  // uniform across the CTA
+    if (dmax - dmin >= (1u << 20)) return false;  // uniform across the group
     uint32_t k32[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -239,7 +268,7 @@ __device__ __forceinline__ bool register_bitonic32(unsigned long long* keys, uin
                     parity ^= 1;
 #pragma unroll
                     for (int r = 0; r < R; ++r) buf[r * kSmallSortThreads + tid] = k32[r];
-                    asm volatile("bar.sync 1, %0;" ::"r"(lanes) : "memory");
+                    asm volatile("bar.sync %0, %1;" ::"r"(xbar), "r"(lanes) : "memory");
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
@@ -259,13 +288,13 @@ __device__ __forceinline__ bool register_bitonic32(unsigned long long* keys, uin
             }
         }
     }
-    __syncthreads();  // s_orig complete everywhere
+    bar.sync();  // s_orig complete everywhere
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
         if (tid < lanes && i < n) s_out[i] = s_orig[k32[r] & 0xFFFu];
     }
-    __syncthreads();
+    bar.sync();
     // odd-even transposition inside runs of equal depth: (depth, slot) order
     while (true) {
         bool swapped = false;
@@ -280,12 +309,53 @@ __device__ __forceinline__ bool register_bitonic32(unsigned long long* keys, uin
                     swapped = true;
                 }
             }
-            __syncthreads();
+            bar.sync();
         }
-        if (!__syncthreads_or(swapped)) break;
+        if (!bar.sync_or(swapped)) break;
     }
-    for (uint32_t i = tid; i < n; i += kSmallSortThreads) keys[i] = s_out[i];
+    if (dst)
+        for (uint32_t i = tid; i < n; i += kSmallSortThreads) dst[i] = s_out[i];
     return true;
+}
+
+// One run of up to kRun keys (global) sorted into shared memory by 256
+// threads: the 32-bit network when the run's depth band allows, else the
+// 64-bit one.  stage: kRun keys of staging (s_orig, then the exchange words;
+// the 64-bit network's double buffer reuses all of it).
+template <class Bar>
+__device__ __forceinline__ void sort_run(const unsigned long long* keys, uint32_t n,
+                                         unsigned long long* s_run, unsigned long long* stage,
+                                         uint32_t* s_red, uint32_t tid, unsigned xbar, Bar bar) {
+    if (register_bitonic32<10>(keys, n, stage, reinterpret_cast<uint32_t*>(stage + kRun), s_red,
+                               s_run, nullptr, tid, xbar, bar))
+        return;
+    bar.sync();  // staging reused by the 64-bit network
+    register_bitonic<10>(keys, n, s_run, stage, tid, xbar);
+}
+
+// Sorted runs of kRun keys in shared memory -> the sorted bucket in dst.  Keys
+// are unique (the low word is the emission slot), so a key's final position is
+// its index in its run plus, for every other run, the number of keys below it
+// (a fixed-depth binary search); each key is stored once, straight to HBM.
+__device__ __forceinline__ void rank_merge(const unsigned long long* runs, uint32_t n,
+                                           unsigned long long* dst, uint32_t tid, uint32_t nthr) {
+    const uint32_t n_runs = (n + kRun - 1) / kRun;
+    for (uint32_t i = tid; i < n; i += nthr) {
+        const unsigned long long x = runs[i];
+        const uint32_t r = i / kRun;
+        uint32_t rank = i - r * kRun;
+        for (uint32_t q = 0; q < n_runs; ++q) {
+            if (q == r) continue;
+            const unsigned long long* run = runs + q * kRun;
+            const uint32_t len = min(kRun, n - q * kRun);
+            uint32_t pos = 0;
+#pragma unroll
+            for (uint32_t step = kRun; step > 0; step >>= 1)
+                if (pos + step <= len && run[pos + step - 1] < x) pos += step;
+            rank += pos;
+        }
+        dst[rank] = x;
+    }
 }
 
 __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t* __restrict__ offsets,
@@ -293,47 +363,59 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t*
                                                                  unsigned long long* keys) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
-    __shared__ unsigned long long s[kSmallSortCap];
+    static_assert(kSmallSortCap == 2 * int(kRun), "two runs + their staging fill s");
+    __shared__ unsigned long long s[2 * kSmallSortCap];
+    __shared__ uint32_t s_red[2 * kSmallSortThreads / 32];
     const uint32_t tile = order[blockIdx.x];  // heaviest buckets first
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
     const uint32_t n = e - b;
+    const uint32_t tid = threadIdx.x;
     if (n < 2 || n > uint32_t(kSmallSortCap)) return;  // big buckets: k_tile_sort_big
 #ifndef SORT32
 #define SORT32 1
 #endif
+    if (n > kRun) {  // two runs, then the rank merge
+        for (uint32_t r = 0; r * kRun < n; ++r) {
+            sort_run(keys + b + r * kRun, min(kRun, n - r * kRun), s + r * kRun,
+                     s + kSmallSortCap, s_red, tid, 1, CtaBar{});
+            __syncthreads();
+        }
+        rank_merge(s, n, keys + b, tid, kSmallSortThreads);
+        return;
+    }
 #if SORT32
-    if (n <= 1024u) {
+    {
         bool done;
-        if (n <= 32u) done = register_bitonic32<5>(keys + b, n, s);
-        else if (n <= 64u) done = register_bitonic32<6>(keys + b, n, s);
-        else if (n <= 128u) done = register_bitonic32<7>(keys + b, n, s);
-        else if (n <= 256u) done = register_bitonic32<8>(keys + b, n, s);
-        else if (n <= 512u) done = register_bitonic32<9>(keys + b, n, s);
-        else done = register_bitonic32<10>(keys + b, n, s);
+        uint32_t* sx32 = reinterpret_cast<uint32_t*>(s + kRun);
+        unsigned long long* so = s + 2 * kRun;
+        if (n <= 32u) done = register_bitonic32<5>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
+        else if (n <= 64u) done = register_bitonic32<6>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
+        else if (n <= 128u) done = register_bitonic32<7>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
+        else if (n <= 256u) done = register_bitonic32<8>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
+        else if (n <= 512u) done = register_bitonic32<9>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
+        else done = register_bitonic32<10>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
         if (done) return;
         __syncthreads();  // staging in s is reused by the 64-bit network
     }
 #endif
-    if (n <= uint32_t(kRegCap)) {
-        if (n <= 32u) register_bitonic<5>(keys + b, n, s);
-        else if (n <= 64u) register_bitonic<6>(keys + b, n, s);
-        else if (n <= 128u) register_bitonic<7>(keys + b, n, s);
-        else if (n <= 256u) register_bitonic<8>(keys + b, n, s);
-        else if (n <= 512u) register_bitonic<9>(keys + b, n, s);
-        else register_bitonic<10>(keys + b, n, s);
-        return;
-    }
-    for (uint32_t i = threadIdx.x; i < n; i += kSmallSortThreads) s[i] = keys[b + i];
-    __syncthreads();
-    flip_bitonic<uint32_t>(s, n, threadIdx.x, kSmallSortThreads, [] __device__() { __syncthreads(); });
-    for (uint32_t i = threadIdx.x; i < n; i += kSmallSortThreads) keys[b + i] = s[i];
+    if (n <= 32u) register_bitonic<5>(keys + b, n, keys + b, s, tid, 1);
+    else if (n <= 64u) register_bitonic<6>(keys + b, n, keys + b, s, tid, 1);
+    else if (n <= 128u) register_bitonic<7>(keys + b, n, keys + b, s, tid, 1);
+    else if (n <= 256u) register_bitonic<8>(keys + b, n, keys + b, s, tid, 1);
+    else if (n <= 512u) register_bitonic<9>(keys + b, n, keys + b, s, tid, 1);
+    else register_bitonic<10>(keys + b, n, keys + b, s, tid, 1);
 }
 
-constexpr int kBigSortThreads = 1024;
+constexpr int kBigGroups = 4;
+constexpr int kBigSortThreads = kBigGroups * kSmallSortThreads;
+constexpr int kBigSortSmem = (kBigSortCap + kBigGroups * 2 * int(kRun)) * 8;
 
-// Buckets above kSmallSortCap: one 1024-thread CTA per bucket, 128 KB of
-// shared memory up to kBigSortCap keys, beyond that the same network in
-// place in global memory (L2-resident; only pathological tiles get here).
+// Buckets above kSmallSortCap: persistent CTAs (one per SM) take buckets from
+// a queue; the bucket's runs of kRun keys are sorted by four 256-thread groups
+// (named barriers 1-4 for the exchanges, 5-8 for the group) into shared
+// memory, then all 1024 threads rank-merge them into place.  Beyond
+// kBigSortCap the flip bitonic runs in place in global memory (L2-resident;
+// only pathological tiles get there).
 __global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_t* __restrict__ offsets,
                                                                    unsigned long long* keys,
                                                                    const uint32_t* big_list,
@@ -341,8 +423,12 @@ __global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
     extern __shared__ unsigned long long s_big[];
+    __shared__ uint32_t s_red[kBigGroups][2 * kSmallSortThreads / 32];
     __shared__ unsigned s_item;
     const unsigned n_big = cnt->big_tiles;
+    const uint32_t g = threadIdx.x / kSmallSortThreads, gt = threadIdx.x % kSmallSortThreads;
+    unsigned long long* stage = s_big + kBigSortCap + g * 2 * kRun;
+    const GroupBar gbar{5u + g};
     while (true) {
         __syncthreads();
         if (threadIdx.x == 0) s_item = atomicAdd(&cnt->big_cursor, 1u);
@@ -353,11 +439,13 @@ __global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_
         const uint32_t b = offsets[tile], e = offsets[tile + 1];
         const uint32_t n = e - b;
         if (n <= uint32_t(kBigSortCap)) {
-            for (uint32_t i = threadIdx.x; i < n; i += kBigSortThreads) s_big[i] = keys[b + i];
+            for (uint32_t r = g; r * kRun < n; r += kBigGroups) {
+                sort_run(keys + b + r * kRun, min(kRun, n - r * kRun), s_big + r * kRun, stage,
+                         s_red[g], gt, 1u + g, gbar);
+                gbar.sync();  // staging reuse by the group's next run
+            }
             __syncthreads();
-            flip_bitonic<uint32_t>(s_big, n, threadIdx.x, kBigSortThreads,
-                                   [] __device__() { __syncthreads(); });
-            for (uint32_t i = threadIdx.x; i < n; i += kBigSortThreads) keys[b + i] = s_big[i];
+            rank_merge(s_big, n, keys + b, threadIdx.x, kBigSortThreads);
         } else {
             flip_bitonic<uint32_t>(keys + b, n, threadIdx.x, kBigSortThreads, [] __device__() {
                 __threadfence_block();
@@ -377,12 +465,13 @@ void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
                           const uint32_t* big_list, FrameCounters* cnt, int grid,
                           cudaStream_t s) {
     static bool attr = false;
-    const int smem = kBigSortCap * 8;
     if (!attr) {
-        cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kBigSortSmem);
         attr = true;
     }
-    launch_pdl(k_tile_sort_big, grid, kBigSortThreads, smem, s, offsets, keys, big_list, cnt);
+    launch_pdl(k_tile_sort_big, grid, kBigSortThreads, kBigSortSmem, s, offsets, keys, big_list,
+               cnt);
 }
 
 // ----------------------------------------------------------------------------

@@ -391,19 +391,32 @@ def test_sort_hand_cases(L, gpu):
 
 
 def test_sort_big_buckets(L, oracle, gpu):
-    """Buckets above the 4096-key shared-memory sort and above the 16384-key
-    big-tile path (global in-place network) still give the stable order."""
+    """Every bucket-size regime of the per-tile sort against the reference's
+    stable LSD sort: register networks (<= 1024), two runs + rank merge in the
+    small kernel (<= 2048), 3..16 runs in the big-bucket kernel (<= 16384),
+    the global in-place network beyond; narrow depth bands (32-bit keys, with
+    and without ties), wide ones (64-bit networks), both mixed in one bucket."""
     rng = np.random.default_rng(5)
-    for n_tiles, n in ((3, 30000), (2, 70000)):
-        pairs = np.empty(n, L.PAIR_DTYPE)
-        pairs["tile"] = rng.integers(0, n_tiles, n)
-        pairs["depth"] = rng.integers(0, 300, n).astype(np.float32)
-        pairs["gaussian"] = np.arange(n)
-        want = pairs.copy()
-        oracle.sort_pairs(want)
-        got = pairs.copy()
-        L.sort_pairs(got)
-        assert got.tobytes() == want.tobytes()
+    sizes = (1023, 1024, 1025, 1500, 2047, 2048, 2049, 3000, 4096, 4097, 8263, 16384, 16385, 30000)
+    for k, n in enumerate(sizes):
+        for depth in ("ties32", "narrow", "ties64", "wide"):
+            pairs = np.empty(n, L.PAIR_DTYPE)
+            pairs["tile"] = rng.integers(0, 2, n) * 5 if k % 3 == 0 else 3
+            if depth == "ties32":  # 4 distinct depths 2^17 ulps apart
+                pairs["depth"] = (100 + rng.integers(0, 4, n)).astype(np.float32)
+            elif depth == "ties64":
+                pairs["depth"] = rng.integers(0, 300, n).astype(np.float32)
+            elif depth == "narrow":
+                pairs["depth"] = (50.0 + rng.random(n)).astype(np.float32)
+            else:
+                pairs["depth"] = (rng.random(n) * 1e4).astype(np.float32)
+                pairs["depth"][: n // 7] = np.float32(1e-3)
+            pairs["gaussian"] = rng.permutation(n)
+            want = pairs.copy()
+            oracle.sort_pairs(want)
+            got = pairs.copy()
+            L.sort_pairs(got)
+            assert got.tobytes() == want.tobytes(), (n, depth)
 
 
 # ----------------------------------------------------------------- blend --

@@ -20,3 +20,13 @@ with L.GpuScene(tree) as s:
         print(f"alt {alt}: sel {st.n_selected} pairs {st.n_pairs} big {st.big_tiles} "
               f"filter {st.t_calc_ms:.3f} prep {st.t_prepr_ms:.3f} sort {st.t_sort_ms:.3f} "
               f"blend {st.t_alpha_ms:.3f} ms", flush=True)
+
+    # tile-size distribution of the lowest frame: what the big-bucket sort sees
+    import numpy as np
+    nt = ((3840 + 15) // 16) * ((2160 + 15) // 16)
+    _, pt = s.read_counts(int(st.n_selected), nt)
+    pt = pt.astype(np.int64)
+    for cap in (2048, 4096, 16384):
+        big = pt[pt > cap]
+        print(f"tiles > {cap}: {big.size}, keys {big.sum()} ({big.sum() / max(1, pt.sum()):.1%})")
+    print("percentiles 50/90/99/max:", np.percentile(pt, [50, 90, 99]).tolist(), pt.max())

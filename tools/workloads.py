@@ -124,7 +124,7 @@ def run_cfg5(n_views=1024):
         dist.destroy_process_group()
 
 
-def run(which, frames, lambda_g):
+def run(which, frames, lambda_g, inflight=2):
     if which == "cfg5":
         return run_cfg5()
     out = []
@@ -144,11 +144,13 @@ def run(which, frames, lambda_g):
                     [n // 2, n - n // 2])
     build_s = time.perf_counter() - t0
     with L.GpuScene(tree) as scene:
+        scene.set_inflight(inflight)
         views = cams[:: max(1, len(cams) // 4)][:4]
         rep = scene.calibrate(views, lambda_g, L.FilterConfig(3.0))
         base = {"workload": which, "nodes": tree.node_count(), "width": cams[0].width,
                 "height": cams[0].height, "frames": len(cams), "tau_r": 3.0,
-                "build_s": build_s, "device_bytes": scene.memory_bytes()}
+                "build_s": build_s, "device_bytes": scene.memory_bytes(),
+                "frames_in_flight": inflight}
         modes = [("three_sigma", L.ShrinkMode.three_sigma()),
                  ("adaptive", L.ShrinkMode.adaptive(rep.tau))]
         for name, mode in modes:
@@ -167,9 +169,10 @@ def main():
     ap.add_argument("--which", nargs="+", default=["cfg2", "cfg4"])
     ap.add_argument("--frames", type=int, default=30)
     ap.add_argument("--lambda-g", type=float, default=0.2)
+    ap.add_argument("--inflight", type=int, default=2, choices=(1, 2))
     args = ap.parse_args()
     for w in args.which:
-        run(w, args.frames, args.lambda_g)
+        run(w, args.frames, args.lambda_g, args.inflight)
 
 
 if __name__ == "__main__":
