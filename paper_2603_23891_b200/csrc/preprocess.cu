@@ -187,7 +187,10 @@ __device__ __forceinline__ void block_add2(uint32_t a, uint32_t b, unsigned long
 // (rasterizer.cpp:56, near-plane drop) gets an empty rect tagged kDropped.
 // Keys carry the slot, whose order equals BlendList order, so the sort is
 // unchanged; the slot -> BlendList index map is only built for readbacks.
-__global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
+#ifndef PREP_MIN_CTAS
+#define PREP_MIN_CTAS 4
+#endif
+__global__ void __launch_bounds__(kPrepBlock, PREP_MIN_CTAS) k_preprocess(
     const Geom g, const SplatRec* __restrict__ splat, const double* __restrict__ sig3,
     const uint32_t* __restrict__ selected, const int kind, const double tau, const int tiles_x,
     const int tiles_y, PrepOut out, FrameCounters* cnt, const int use_hist,
@@ -203,17 +206,53 @@ __global__ void __launch_bounds__(kPrepBlock, 4) k_preprocess(
     __syncthreads();
     uint32_t kept = 0, pairs = 0;
     unsigned long long kor = 0, knand = 0;
-    for (uint64_t s = lo + threadIdx.x; s < hi; s += kPrepBlock) {
-        const uint32_t idx = __ldg(selected + s);
+#ifndef PREP_PREFETCH
+#define PREP_PREFETCH 1
+#endif
+    // Software pipeline over the CTA's slots: the next slot's index (level 1;
+    // level 2 also its records, which spills at 64 registers and measured
+    // slower) is in flight while this one is projected.
+    auto load_rec = [&](uint32_t idx, float4 (&r)[4], double2 (&q)[3]) {
         const float4* src = reinterpret_cast<const float4*>(splat + idx);
-        const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = __ldg(src + k);
+        const double2* sp = reinterpret_cast<const double2*>(sig3 + 6 * uint64_t(idx));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) q[k] = __ldg(sp + k);
+    };
+    uint64_t s = lo + threadIdx.x;
+    uint32_t idx_next = s < hi ? __ldg(selected + s) : 0u;
+#if PREP_PREFETCH >= 2
+    float4 nr[4];
+    double2 nq[3];
+    if (s < hi) load_rec(idx_next, nr, nq);
+    uint32_t idx_after = s + kPrepBlock < hi ? __ldg(selected + s + kPrepBlock) : 0u;
+#endif
+    for (; s < hi; s += kPrepBlock) {
+        const uint32_t idx = idx_next;
+#if PREP_PREFETCH >= 2
+        const float4 a = nr[0], b = nr[1], c = nr[2], d = nr[3];
+        const double2 s0 = nq[0], s1 = nq[1], s2 = nq[2];
+        idx_next = idx_after;
+        if (s + kPrepBlock < hi) load_rec(idx_next, nr, nq);
+        if (s + 2 * kPrepBlock < hi) idx_after = __ldg(selected + s + 2 * kPrepBlock);
+#else
+#if PREP_PREFETCH >= 1
+        if (s + kPrepBlock < hi) idx_next = __ldg(selected + s + kPrepBlock);
+#else
+        if (s + kPrepBlock < hi) idx_next = selected[s + kPrepBlock];  // not in flight early
+#endif
+        float4 rr[4];
+        double2 qq[3];
+        load_rec(idx, rr, qq);
+        const float4 a = rr[0], b = rr[1], c = rr[2], d = rr[3];
+        const double2 s0 = qq[0], s1 = qq[1], s2 = qq[2];
+#endif
         SplatRec rec;
         rec.mx = a.x; rec.my = a.y; rec.mz = a.z; rec.sx = a.w;
         rec.sy = b.x; rec.sz = b.y; rec.qw = b.z; rec.qx = b.w;
         rec.qy = c.x; rec.qz = c.y; rec.opacity = c.z; rec.cr = c.w;
         rec.cg = d.x; rec.cb = d.y;
-        const double2* sp = reinterpret_cast<const double2*>(sig3 + 6 * uint64_t(idx));
-        const double2 s0 = __ldg(sp), s1 = __ldg(sp + 1), s2 = __ldg(sp + 2);
         const Sigma3 S{s0.x, s0.y, s1.x, s1.y, s2.x, s2.y};
         const Projected p = project_one(g, rec, S, kind, tau, known_visible != 0);
         GaussEmit e;
