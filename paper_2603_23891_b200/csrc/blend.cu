@@ -291,6 +291,9 @@ constexpr int kWsConsumers = 8;
 #ifndef WS_PRODUCERS
 #define WS_PRODUCERS 2
 #endif
+#ifndef WS_HINT
+#define WS_HINT 0  // suspend-time hint (ns) of the mbarrier waits (0: none)
+#endif
 #ifndef WS_SLEEP
 #define WS_SLEEP 0  // ns of __nanosleep between failed mbarrier polls (0: spin)
 #endif
@@ -304,9 +307,12 @@ struct WsStage {
 };
 
 #ifndef WS_RAW
-#define WS_RAW 4
+#define WS_RAW 2
 #endif
-constexpr int kWsRaw = WS_RAW;  // producer's gather ring (batches in flight + 1)
+// producer's gather ring (batches in flight + 1).  One batch ahead is enough:
+// the records were just written by K3 and are L2-resident; a deeper ring only
+// costs shared memory (2 / 3 / 4: 3010 / 2963 / 2909 frames/s on the cfg-3 path)
+constexpr int kWsRaw = WS_RAW;
 struct WsRaw {
     double2 m[32];
     float4 q0[32], col[32];
@@ -363,6 +369,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
         if (ok) break;
         __nanosleep(WS_SLEEP);
     }
+#elif WS_HINT
+    // suspend-time hint: the warp sleeps in hardware until the phase flips
+    // (or the hint expires) instead of re-issuing the poll
+    asm volatile(
+        "{ .reg .pred p;\n"
+        "WAIT_%=:\n"
+        "  mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "  @!p bra WAIT_%=;\n"
+        "}" ::"r"(smem_addr(b)),
+        "r"(parity), "n"(WS_HINT)
+        : "memory");
 #else
     asm volatile(
         "{ .reg .pred p;\n"
@@ -375,7 +392,10 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
 #endif
 }
 
-__global__ void __launch_bounds__(kWsThreads, 3) k_blend_ws(
+#ifndef WS_MIN_CTAS
+#define WS_MIN_CTAS 3
+#endif
+__global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_ws(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
     const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
     const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
@@ -466,8 +486,13 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_blend_ws(
                     if (hit) {
                         const int slot = __popc(bits & lt);
                         // block-relative mean, rounded from the FP64 mean exactly as k_blend_fast
+#if WS_FASTMEAN  // timing experiment only: not the certified rounding
+                        const float mlx = mtx - float((w & 1) * 8);
+                        const float mly = mty - float((w >> 1) * 4);
+#else
                         const float mlx = float(m.x - double(tx0 + (w & 1) * 8));
                         const float mly = float(m.y - double(ty0 + (w >> 1) * 4));
+#endif
                         st.blk[w].geo[slot] = make_float4(mlx, mly, q0.x, q0.z);
                         st.blk[w].ct[slot] = make_float4(q0.y, q0.w, col.x, col.y);
                         st.blk[w].gb[slot] = make_float2(col.z, col.w);
