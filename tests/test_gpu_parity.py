@@ -477,6 +477,45 @@ def test_blend_micro_scenes(L, oracle, gpu):
         assert max_abs(fa, want) <= IMG_TOL, rep
 
 
+def test_blend_needle_splats(L, oracle, gpu):
+    """Needle-like splats (2D covariance eigenvalue ratios 1e2..3e4 at any
+    angle; the terms of the exponent cancel almost completely): the fast
+    path's skip test stays certified -- within the north-star tolerance of the
+    oracle -- and the exact path stays bit-identical."""
+    rng = np.random.default_rng(77)
+    for rep in range(24):
+        w, h = 48 + 8 * (rep % 5), 40 + 4 * (rep % 7)
+        d: dict = {}
+        for i in range(40):
+            l1 = 10 ** rng.uniform(2.0, 4.0)
+            l2 = rng.uniform(0.3, 1.0)
+            th = rng.uniform(0, np.pi)
+            c_, s_ = np.cos(th), np.sin(th)
+            cov = np.array([[c_ * c_ * l1 + s_ * s_ * l2, c_ * s_ * (l1 - l2)],
+                            [c_ * s_ * (l1 - l2), s_ * s_ * l1 + c_ * c_ * l2]])
+            con = np.linalg.inv(cov)
+            d.setdefault("mean_x", []).append(rng.uniform(0, w))
+            d.setdefault("mean_y", []).append(rng.uniform(0, h))
+            d.setdefault("conic_a", []).append(con[0, 0])
+            d.setdefault("conic_b", []).append(con[0, 1])
+            d.setdefault("conic_c", []).append(con[1, 1])
+            d.setdefault("opacity", []).append(rng.uniform(0.01, 0.99))
+            for c in ("col_r", "col_g", "col_b"):
+                d.setdefault(c, []).append(rng.uniform(0, 1))
+            d.setdefault("radius", []).append(3.0 * np.sqrt(l1))
+            d.setdefault("depth", []).append(np.float32(1.0 + i))
+            d.setdefault("node", []).append(i)
+        bl = to_blendlist(d)
+        pairs = oracle.bin_to_tiles(bl, w, h)
+        oracle.sort_pairs(pairs)
+        want = oracle.alpha_blend(pairs, bl, w, h)
+        grid = L.TileGrid.make(w, h)
+        ex = L.alpha_blend(pairs, bl, grid, w, h, exact=True).rgb
+        assert ex.tobytes() == want.tobytes(), rep
+        fa = L.alpha_blend(pairs, bl, grid, w, h, exact=False).rgb
+        assert max_abs(fa, want) <= IMG_TOL, (rep, max_abs(fa, want))
+
+
 # ---------------------------------------------------------------- render --
 def _check_render(L, oracle, scene, tree, cam, tau_r, mode):
     want = oracle.render(tree, cam, tau_r, mode)
