@@ -25,6 +25,8 @@
 //
 // Exact kernel (LODGS_RENDER_EXACT_BLEND): the reference arithmetic in FP64
 // with the reference exp_mx (fastexp.hpp:38-50), no FMA: bit-identical pixels.
+#include <algorithm>
+
 #include "launch.h"
 #include "pdl.cuh"
 
@@ -291,6 +293,12 @@ constexpr int kWsConsumers = 8;
 #ifndef WS_PRODUCERS
 #define WS_PRODUCERS 2
 #endif
+#ifndef WS_NOSTOP
+#define WS_NOSTOP 0  // timing experiment: no early stop of saturated tiles
+#endif
+#ifndef WS_NOCONSUME
+#define WS_NOCONSUME 0  // timing experiment: producers only
+#endif
 #ifndef WS_HINT
 #define WS_HINT 0  // suspend-time hint (ns) of the mbarrier waits (0: none)
 #endif
@@ -458,7 +466,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_ws(
             const uint32_t use = i / kWsStages;
             if (use > 0) mbar_wait(&sh.empty[s], (use - 1) & 1u);
             WsStage& st = sh.st[s];
-            const bool stop = base >= e || *(volatile uint32_t*)&sh.done_warps == kWsConsumers;
+            const bool stop = base >= e || (!WS_NOSTOP && *(volatile uint32_t*)&sh.done_warps == kWsConsumers);
             if (!stop) {
                 const uint32_t gi = r.gid[lane];
                 const double2 m = r.m[lane];
@@ -527,7 +535,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_ws(
         const WarpStage& st = sh.st[s].blk[warp];
         const int nh = int(sh.st[s].cnt[warp]);
         const bool last = sh.st[s].last != 0;
-        if (nh > 0 && __any_sync(0xffffffffu, pix.T != 0.0f)) {
+        if (!WS_NOCONSUME && nh > 0 && __any_sync(0xffffffffu, pix.T != 0.0f)) {
             const PixState saved = pix;
             bool unsure = false;
             int k = 0;
@@ -555,6 +563,252 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_ws(
         o[0] = pix.cr;
         o[1] = pix.cg;
         o[2] = pix.cb;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent form of k_blend_ws: one CTA per resident slot walks the tiles
+// blockIdx.x, blockIdx.x + G, ... of the heavy-first order.  The stage ring
+// runs across tile boundaries, so the producers gather the next tile's first
+// batches while the consumers still blend the current one (no per-tile CTA
+// start-up, no drained pipeline at tile ends).  A tile contributes
+// max(1, ceil(n / 32)) stages; producer p fills the CTA's global stages p, p + 2,
+// ...; a stage carries its tile and flags (last stage of the tile: consumers
+// store their pixels and start over; last stage of the CTA).
+struct WspStage {
+    WarpStage blk[kWsConsumers];
+    uint32_t cnt[kWsConsumers];
+    int x0, y0;      // pixel origin of the stage's tile
+    uint32_t flags;  // 1: last stage of its tile, 2: last stage of the CTA
+};
+struct WspShared {
+    WspStage st[kWsStages];
+    WsRaw raw[kWsProducers][kWsRaw];
+    unsigned long long full[kWsStages], empty[kWsStages];
+};
+
+// Position in a CTA's stage sequence: k-th tile of the CTA, batch bi of it.
+// The next tile's bucket bounds and the tile after it are loaded one tile
+// ahead, so crossing a tile boundary never waits on a dependent global load
+// (order -> offsets -> keys would be three round trips in the producer loop).
+#ifndef WSP_SNAKE
+#define WSP_SNAKE 1
+#endif
+struct TileCur {
+    uint32_t k, bi, b, e, nb;
+    int tile;  // -1: past the CTA's last tile
+    int tx0, ty0;
+    int ntile, nntile;  // tiles k + 1, k + 2 (-1: none)
+    uint32_t nb_b, nb_e;  // bucket of tile k + 1
+};
+// boustrophedon over the heavy-first order: CTA c takes the c-th tile of even
+// rounds and the (G-1-c)-th of odd ones, so no CTA always draws the heaviest
+// tile of each round
+__device__ __forceinline__ uint32_t wsp_slot(uint32_t k) {
+    return k * gridDim.x +
+           ((WSP_SNAKE && (k & 1u)) ? gridDim.x - 1u - blockIdx.x : blockIdx.x);
+}
+__device__ __forceinline__ int wsp_tile(uint32_t k, const uint32_t* order, uint32_t n_tiles) {
+    const uint32_t slot = wsp_slot(k);
+    return slot < n_tiles ? int(order[slot]) : -1;
+}
+__device__ __forceinline__ void tile_cur_enter(TileCur& c, int tiles_x) {
+    c.bi = 0;
+    if (c.tile < 0) {
+        c.b = c.e = 0;
+        c.nb = 1;
+        return;
+    }
+    c.tx0 = (c.tile % tiles_x) * kTile;
+    c.ty0 = (c.tile / tiles_x) * kTile;
+    c.nb = c.e > c.b ? (c.e - c.b + 31u) / 32u : 1u;
+}
+__device__ __forceinline__ void tile_cur_init(TileCur& c, const uint32_t* order,
+                                              const uint32_t* offsets, uint32_t n_tiles,
+                                              int tiles_x) {
+    c.k = 0;
+    c.tile = wsp_tile(0, order, n_tiles);
+    c.ntile = wsp_tile(1, order, n_tiles);
+    c.nntile = wsp_tile(2, order, n_tiles);
+    if (c.tile >= 0) {
+        c.b = offsets[c.tile];
+        c.e = offsets[c.tile + 1];
+    }
+    if (c.ntile >= 0) {
+        c.nb_b = offsets[c.ntile];
+        c.nb_e = offsets[c.ntile + 1];
+    }
+    tile_cur_enter(c, tiles_x);
+}
+__device__ __forceinline__ void tile_cur_step(TileCur& c, uint32_t n, const uint32_t* order,
+                                              const uint32_t* offsets, uint32_t n_tiles,
+                                              int tiles_x) {
+    c.bi += n;
+    while (c.tile >= 0 && c.bi >= c.nb) {
+        const uint32_t over = c.bi - c.nb;
+        ++c.k;
+        c.tile = c.ntile;
+        c.b = c.nb_b;
+        c.e = c.nb_e;
+        c.ntile = c.nntile;
+        if (c.ntile >= 0) {  // loaded a tile ago
+            c.nb_b = offsets[c.ntile];
+            c.nb_e = offsets[c.ntile + 1];
+        }
+        c.nntile = wsp_tile(c.k + 2, order, n_tiles);
+        tile_cur_enter(c, tiles_x);
+        c.bi = over;
+    }
+}
+
+__global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
+    const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
+    const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
+    const uint32_t n_tiles, float* __restrict__ image) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
+    extern __shared__ __align__(16) unsigned char ws_raw[];
+    WspShared& sh = *reinterpret_cast<WspShared*>(ws_raw);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kWsStages; ++s) {
+            mbar_init(&sh.full[s], 32);
+            mbar_init(&sh.empty[s], kWsConsumers * 32);
+        }
+    }
+    __syncthreads();
+
+    if (warp >= kWsConsumers) {
+        // ---------------- producers ----------------
+        const uint32_t pid = warp - kWsConsumers;
+        constexpr uint32_t kNone = 0xFFFFFFFFu;
+        auto load_key = [&](const TileCur& c) -> uint32_t {
+            const uint32_t at = c.b + 32u * c.bi + lane;
+            return (c.tile >= 0 && at < c.e) ? uint32_t(keys[at]) : kNone;
+        };
+        auto gather = [&](uint32_t gi, int slot) {
+            WsRaw& r = sh.raw[pid][slot];
+            r.gid[lane] = gi;
+            if (gi != kNone) {
+                cp_async16(&r.m[lane], &g64[gi].mx);
+                cp_async16(&r.q0[lane], &g32[gi].ha);
+                cp_async16(&r.col[lane], &g32[gi].op);
+                cp_async8(&r.h[lane], &g32[gi].hx);
+            }
+            cp_async_commit();
+        };
+        TileCur cp;  // the stage being filled
+        tile_cur_init(cp, order, offsets, n_tiles, tiles_x);
+        tile_cur_step(cp, pid, order, offsets, n_tiles, tiles_x);
+        TileCur cg = cp;  // the stage whose key is loaded next
+#pragma unroll
+        for (int j = 0; j < kWsRaw - 1; ++j) {
+            gather(load_key(cg), j);
+            tile_cur_step(cg, kWsProducers, order, offsets, n_tiles, tiles_x);
+        }
+        uint32_t gi_ahead = load_key(cg);
+        tile_cur_step(cg, kWsProducers, order, offsets, n_tiles, tiles_x);
+        const unsigned lt = (1u << lane) - 1u;
+        for (uint32_t j = 0; cp.tile >= 0; ++j) {
+            const uint32_t i = pid + kWsProducers * j;  // the CTA's global stage index
+            gather(gi_ahead, int((j + kWsRaw - 1) % kWsRaw));
+            gi_ahead = load_key(cg);
+            tile_cur_step(cg, kWsProducers, order, offsets, n_tiles, tiles_x);
+            cp_async_wait<kWsRaw - 1>();
+            __syncwarp();
+            const WsRaw& r = sh.raw[pid][j % kWsRaw];
+            const int s = int(i % kWsStages);
+            const uint32_t use = i / kWsStages;
+            if (use > 0) mbar_wait(&sh.empty[s], (use - 1) & 1u);
+            WspStage& st = sh.st[s];
+            const int tx0 = cp.tx0, ty0 = cp.ty0;
+            const uint32_t gi = r.gid[lane];
+            const double2 m = r.m[lane];
+            const float4 q0 = r.q0[lane], col = r.col[lane];
+            const float2 h = r.h[lane];
+            float mtx = 0.f, mty = 0.f;
+            unsigned xm = 0, ym = 0;
+            if (gi != kNone && h.x >= 0.0f) {
+                mtx = float(m.x - double(tx0));
+                mty = float(m.y - double(ty0));
+                xm = (mtx - h.x <= 7.5f && mtx + h.x >= 0.5f ? 1u : 0u) |
+                     (mtx - h.x <= 15.5f && mtx + h.x >= 8.5f ? 2u : 0u);
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    ym |= (mty - h.y <= 4.0f * v + 3.5f && mty + h.y >= 4.0f * v + 0.5f)
+                              ? (1u << v)
+                              : 0u;
+            }
+#pragma unroll
+            for (int w = 0; w < kWsConsumers; ++w) {
+                const bool hit = ((xm >> (w & 1)) & 1u) && ((ym >> (w >> 1)) & 1u);
+                const unsigned bits = __ballot_sync(0xffffffffu, hit);
+                if (hit) {
+                    const int slot = __popc(bits & lt);
+                    const float mlx = float(m.x - double(tx0 + (w & 1) * 8));
+                    const float mly = float(m.y - double(ty0 + (w >> 1) * 4));
+                    st.blk[w].geo[slot] = make_float4(mlx, mly, q0.x, q0.z);
+                    st.blk[w].ct[slot] = make_float4(q0.y, q0.w, col.x, col.y);
+                    st.blk[w].gb[slot] = make_float2(col.z, col.w);
+                    st.blk[w].gid[slot] = gi;
+                }
+                if (lane == 0) st.cnt[w] = __popc(bits);
+            }
+            const bool tile_end = cp.bi + 1 >= cp.nb;
+            const bool cta_end = tile_end && cp.ntile < 0;
+            if (lane == 0) {
+                st.x0 = tx0;
+                st.y0 = ty0;
+                st.flags = (tile_end ? 1u : 0u) | (cta_end ? 2u : 0u);
+            }
+            __syncwarp();
+            mbar_arrive(&sh.full[s]);
+            tile_cur_step(cp, kWsProducers, order, offsets, n_tiles, tiles_x);
+        }
+        cp_async_wait<0>();  // no gather may land after the CTA retires
+        return;
+    }
+
+    // ---------------- consumers: warp w owns the 8x4 block (w & 1, w >> 1) ----
+    const float pxl = float(lane & 7) + 0.5f, pyl = float(lane >> 3) + 0.5f;
+    PixState pix{1.0f, 0.0f, 0.0f, 0.0f};
+    for (uint32_t i = 0;; ++i) {
+        const int s = int(i % kWsStages);
+        mbar_wait(&sh.full[s], (i / kWsStages) & 1u);
+        const WarpStage& st = sh.st[s].blk[warp];
+        const int nh = int(sh.st[s].cnt[warp]);
+        const uint32_t flags = sh.st[s].flags;
+        const int x = sh.st[s].x0 + int(warp & 1) * 8 + int(lane & 7);
+        const int y = sh.st[s].y0 + int(warp >> 1) * 4 + int(lane >> 3);
+        if (nh > 0 && __any_sync(0xffffffffu, pix.T != 0.0f)) {
+            const PixState saved = pix;
+            bool unsure = false;
+            int k = 0;
+            for (; k + 2 <= nh; k += 2) {
+                blend_sample_fast(st, k, pxl, pyl, pix, unsure);
+                blend_sample_fast(st, k + 1, pxl, pyl, pix, unsure);
+            }
+            if (k < nh) blend_sample_fast(st, k, pxl, pyl, pix, unsure);
+            if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
+                pix = saved;
+                const double px = double(x) + 0.5, py = double(y) + 0.5;
+                for (int j = 0; j < nh; ++j)
+                    blend_sample_checked(st, j, pxl, pyl, px, py, g64, pix);
+            }
+        }
+        __syncwarp();
+        mbar_arrive(&sh.empty[s]);
+        if (flags & 1u) {
+            if (x < width && y < height) {
+                float* o = image + (size_t(y) * width + x) * 3;
+                o[0] = pix.cr;
+                o[1] = pix.cg;
+                o[2] = pix.cb;
+            }
+            pix = PixState{1.0f, 0.0f, 0.0f, 0.0f};
+        }
+        if (flags & 2u) break;
     }
 }
 
@@ -820,6 +1074,28 @@ void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned
             cudaFuncSetAttribute(k_blend_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (dev >= 0 && dev < 64) ws_attr[dev] = true;
         }
+#ifndef BLEND_PERSISTENT
+#define BLEND_PERSISTENT 1
+#endif
+#if BLEND_PERSISTENT
+        const int smem_p = int(sizeof(WspShared));
+        static bool wsp_attr[64] = {};
+        static int wsp_grid[64] = {};
+        if (dev < 0 || dev >= 64 || !wsp_attr[dev]) {
+            cudaFuncSetAttribute(k_blend_wsp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p);
+            int per_sm = 0, n_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blend_wsp, kWsThreads, smem_p);
+            cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+            if (dev >= 0 && dev < 64) {
+                wsp_attr[dev] = true;
+                wsp_grid[dev] = std::max(1, per_sm) * std::max(1, n_sm);
+            }
+        }
+        const int grid = std::min(n_tiles, (dev >= 0 && dev < 64) ? wsp_grid[dev] : 444);
+        launch_pdl(k_blend_wsp, grid, kWsThreads, smem_p, s, offsets, order, keys, g64, g32, width,
+                   height, tiles_x, uint32_t(n_tiles), image);
+        return;
+#endif
         launch_pdl(k_blend_ws, n_tiles, kWsThreads, smem, s, offsets, order, keys, g64, g32, width,
                    height, tiles_x, image);
         return;
