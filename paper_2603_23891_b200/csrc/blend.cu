@@ -581,10 +581,13 @@ struct WspStage {
     int x0, y0;      // pixel origin of the stage's tile
     uint32_t flags;  // 1: last stage of its tile, 2: last stage of the CTA
 };
+constexpr int kTq = 16;  // tile-queue ring (producer 0's cursor runs <= 12 tiles ahead)
 struct WspShared {
     WspStage st[kWsStages];
     WsRaw raw[kWsProducers][kWsRaw];
     unsigned long long full[kWsStages], empty[kWsStages];
+    int tq[kTq];
+    uint32_t tq_seq[kTq];
 };
 
 // Position in a CTA's stage sequence: k-th tile of the CTA, batch bi of it.
@@ -593,6 +596,9 @@ struct WspShared {
 // (order -> offsets -> keys would be three round trips in the producer loop).
 #ifndef WSP_SNAKE
 #define WSP_SNAKE 1
+#endif
+#ifndef WSP_DYNAMIC
+#define WSP_DYNAMIC 1  // tiles from the frame's ticket queue (else static slots)
 #endif
 struct TileCur {
     uint32_t k, bi, b, e, nb;
@@ -608,9 +614,42 @@ __device__ __forceinline__ uint32_t wsp_slot(uint32_t k) {
     return k * gridDim.x +
            ((WSP_SNAKE && (k & 1u)) ? gridDim.x - 1u - blockIdx.x : blockIdx.x);
 }
-__device__ __forceinline__ int wsp_tile(uint32_t k, const uint32_t* order, uint32_t n_tiles) {
-    const uint32_t slot = wsp_slot(k);
-    return slot < n_tiles ? int(order[slot]) : -1;
+// The CTA's k-th tile.  Dynamic (ticket != null): tiles are taken from the
+// frame's queue in heavy-first order; producer 0's look-ahead cursor takes the
+// ticket and publishes the tile in a shared ring, every other cursor reads it
+// there (waiting for producer 0 if it is ahead -- producer 0 never waits on
+// producer 1, so this cannot deadlock).  Static: the boustrophedon slot.
+struct WspSrc {
+    const uint32_t* order;
+    uint32_t n_tiles;
+    unsigned* ticket;
+    WspShared* sh;
+};
+__device__ __forceinline__ int wsp_tile(uint32_t k, const WspSrc& src, bool fetch) {
+    if (!src.ticket) {
+        const uint32_t slot = wsp_slot(k);
+        return slot < src.n_tiles ? int(src.order[slot]) : -1;
+    }
+    const uint32_t q = k % kTq;
+    volatile uint32_t* seq = src.sh->tq_seq;
+    volatile int* tq = src.sh->tq;
+    if (fetch) {
+        uint32_t t = 0;
+        if ((threadIdx.x & 31) == 0) t = atomicAdd(src.ticket, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        const int tile = t < src.n_tiles ? int(src.order[t]) : -1;
+        if ((threadIdx.x & 31) == 0) {
+            tq[q] = tile;
+            __threadfence_block();
+            seq[q] = k;
+        }
+        __syncwarp();
+        return tile;
+    }
+    while (seq[q] != k) {
+    }
+    __threadfence_block();
+    return tq[q];
 }
 __device__ __forceinline__ void tile_cur_enter(TileCur& c, int tiles_x) {
     c.bi = 0;
@@ -623,13 +662,12 @@ __device__ __forceinline__ void tile_cur_enter(TileCur& c, int tiles_x) {
     c.ty0 = (c.tile / tiles_x) * kTile;
     c.nb = c.e > c.b ? (c.e - c.b + 31u) / 32u : 1u;
 }
-__device__ __forceinline__ void tile_cur_init(TileCur& c, const uint32_t* order,
-                                              const uint32_t* offsets, uint32_t n_tiles,
-                                              int tiles_x) {
+__device__ __forceinline__ void tile_cur_init(TileCur& c, const WspSrc& src, bool fetch,
+                                              const uint32_t* offsets, int tiles_x) {
     c.k = 0;
-    c.tile = wsp_tile(0, order, n_tiles);
-    c.ntile = wsp_tile(1, order, n_tiles);
-    c.nntile = wsp_tile(2, order, n_tiles);
+    c.tile = wsp_tile(0, src, fetch);
+    c.ntile = wsp_tile(1, src, fetch);
+    c.nntile = wsp_tile(2, src, fetch);
     if (c.tile >= 0) {
         c.b = offsets[c.tile];
         c.e = offsets[c.tile + 1];
@@ -640,9 +678,8 @@ __device__ __forceinline__ void tile_cur_init(TileCur& c, const uint32_t* order,
     }
     tile_cur_enter(c, tiles_x);
 }
-__device__ __forceinline__ void tile_cur_step(TileCur& c, uint32_t n, const uint32_t* order,
-                                              const uint32_t* offsets, uint32_t n_tiles,
-                                              int tiles_x) {
+__device__ __forceinline__ void tile_cur_step(TileCur& c, uint32_t n, const WspSrc& src,
+                                              bool fetch, const uint32_t* offsets, int tiles_x) {
     c.bi += n;
     while (c.tile >= 0 && c.bi >= c.nb) {
         const uint32_t over = c.bi - c.nb;
@@ -655,7 +692,7 @@ __device__ __forceinline__ void tile_cur_step(TileCur& c, uint32_t n, const uint
             c.nb_b = offsets[c.ntile];
             c.nb_e = offsets[c.ntile + 1];
         }
-        c.nntile = wsp_tile(c.k + 2, order, n_tiles);
+        c.nntile = wsp_tile(c.k + 2, src, fetch);
         tile_cur_enter(c, tiles_x);
         c.bi = over;
     }
@@ -665,7 +702,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
     const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
     const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
-    const uint32_t n_tiles, float* __restrict__ image) {
+    const uint32_t n_tiles, unsigned* ticket, float* __restrict__ image) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
     extern __shared__ __align__(16) unsigned char ws_raw[];
@@ -677,6 +714,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
             mbar_init(&sh.empty[s], kWsConsumers * 32);
         }
     }
+    if (threadIdx.x < kTq) sh.tq_seq[threadIdx.x] = 0xFFFFFFFFu;
     __syncthreads();
 
     if (warp >= kWsConsumers) {
@@ -698,23 +736,39 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
             }
             cp_async_commit();
         };
+        const WspSrc src{order, n_tiles, ticket, &sh};
+        const bool lead = pid == 0;  // producer 0's look-ahead cursor takes the tickets
+        TileCur cg;  // the stage whose key is loaded next
+        tile_cur_init(cg, src, lead, offsets, tiles_x);
+        tile_cur_step(cg, pid, src, lead, offsets, tiles_x);
         TileCur cp;  // the stage being filled
-        tile_cur_init(cp, order, offsets, n_tiles, tiles_x);
-        tile_cur_step(cp, pid, order, offsets, n_tiles, tiles_x);
-        TileCur cg = cp;  // the stage whose key is loaded next
+        tile_cur_init(cp, src, false, offsets, tiles_x);
+        tile_cur_step(cp, pid, src, false, offsets, tiles_x);
+        if (pid == 0 && cp.tile < 0) {
+            // the queue was empty when this CTA started: one empty final stage
+            // releases the consumers
+            WspStage& st = sh.st[0];
+            if (lane < kWsConsumers) st.cnt[lane] = 0;
+            if (lane == 0) {
+                st.x0 = st.y0 = 0;
+                st.flags = 2u;
+            }
+            __syncwarp();
+            mbar_arrive(&sh.full[0]);
+        }
 #pragma unroll
         for (int j = 0; j < kWsRaw - 1; ++j) {
             gather(load_key(cg), j);
-            tile_cur_step(cg, kWsProducers, order, offsets, n_tiles, tiles_x);
+            tile_cur_step(cg, kWsProducers, src, lead, offsets, tiles_x);
         }
         uint32_t gi_ahead = load_key(cg);
-        tile_cur_step(cg, kWsProducers, order, offsets, n_tiles, tiles_x);
+        tile_cur_step(cg, kWsProducers, src, lead, offsets, tiles_x);
         const unsigned lt = (1u << lane) - 1u;
         for (uint32_t j = 0; cp.tile >= 0; ++j) {
             const uint32_t i = pid + kWsProducers * j;  // the CTA's global stage index
             gather(gi_ahead, int((j + kWsRaw - 1) % kWsRaw));
             gi_ahead = load_key(cg);
-            tile_cur_step(cg, kWsProducers, order, offsets, n_tiles, tiles_x);
+            tile_cur_step(cg, kWsProducers, src, lead, offsets, tiles_x);
             cp_async_wait<kWsRaw - 1>();
             __syncwarp();
             const WsRaw& r = sh.raw[pid][j % kWsRaw];
@@ -764,7 +818,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
             }
             __syncwarp();
             mbar_arrive(&sh.full[s]);
-            tile_cur_step(cp, kWsProducers, order, offsets, n_tiles, tiles_x);
+            tile_cur_step(cp, kWsProducers, src, false, offsets, tiles_x);
         }
         cp_async_wait<0>();  // no gather may land after the CTA retires
         return;
@@ -1049,7 +1103,7 @@ void launch_view_gtc(const uint32_t* offsets, int n_tiles, const double* kpc, ui
 
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
-                  int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s) {
+                  int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s, unsigned* ticket) {
     const int n_tiles = tiles_x * tiles_y;
     if (n_tiles <= 0) return;
     if (exact) {
@@ -1093,7 +1147,7 @@ void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned
         }
         const int grid = std::min(n_tiles, (dev >= 0 && dev < 64) ? wsp_grid[dev] : 444);
         launch_pdl(k_blend_wsp, grid, kWsThreads, smem_p, s, offsets, order, keys, g64, g32, width,
-                   height, tiles_x, uint32_t(n_tiles), image);
+                   height, tiles_x, uint32_t(n_tiles), WSP_DYNAMIC ? ticket : nullptr, image);
         return;
 #endif
         launch_pdl(k_blend_ws, n_tiles, kWsThreads, smem, s, offsets, order, keys, g64, g32, width,

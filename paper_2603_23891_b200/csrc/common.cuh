@@ -77,7 +77,7 @@ struct FrameCounters {
     unsigned long long n_selected;
     unsigned long long n_gaussians;
     unsigned long long n_pairs;
-    unsigned int ticket_select;
+    unsigned int blend_ticket;  // k_blend_wsp's dynamic tile queue
     unsigned int ticket_prep;
     unsigned int ticket_bin;
     unsigned int big_tiles;

@@ -115,7 +115,8 @@ void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
 // ---- blend (rasterizer.cpp:137-165, blend_scalar.cpp:13-55) ----
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
-                  int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s);
+                  int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,
+                  unsigned* ticket = nullptr);
 
 // Exact blend + per-pair KPC in the reference's 4-lane order (collect_kpc).
 void launch_blend_exact_kpc(const uint32_t* offsets, const unsigned long long* keys,

@@ -534,7 +534,8 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
                                res_.height, res_.tiles_x, res_.tiles_y, img_out, kpc_.p, stream_);
     } else {
         launch_blend(res_.tile_offsets.p, res_.tile_order.p, keys_.p, g64_.p, g32_.p, col64_.p,
-                     res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact, img_out, stream_);
+                     res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact, img_out, stream_,
+                     &d_counters_->blend_ticket);
     }
     if (timing) FGS_CUDA(cudaEventRecord(ev_[4], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[5], stream_));
@@ -1290,7 +1291,7 @@ void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_bl
     launch_tile_offsets(tc, n_tiles, off.p, cur.p, big.p, ord.p, cnt, n, c.s);
     launch_triples_to_keys(tri.p, n, keys.p, c.s);
     launch_blend(off.p, ord.p, keys.p, dl.g64.p, dl.g32.p, dl.col64.p, width, height, tiles_x,
-                 tiles_y, exact, img.p, c.s);
+                 tiles_y, exact, img.p, c.s, &cnt->blend_ticket);
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaMemcpyAsync(image, img.p, img.n * 4, cudaMemcpyDeviceToHost, c.s));
     FGS_CUDA(cudaStreamSynchronize(c.s));
