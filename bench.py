@@ -148,10 +148,13 @@ def ncu_kernel_row(kernel, fname="r1_ncu_render_alt200.txt"):
 def blend_evidence():
     """The dominant kernel is issue-bound (no dense contraction, no HBM roofline):
     its SM issue utilisation from the committed ncu capture (altitude 200)."""
-    row, src = ncu_kernel_row("k_blend_ws")
+    for kern in ("k_blend_wsp", "k_blend_ws"):  # persistent kernel (default build) first
+        row, src = ncu_kernel_row(kern)
+        if row:
+            break
     if not row:
         return None
-    return {"kernel": "k_blend_ws", "bound": "issue", "issue_slots_busy_pct": row.get("issue%"),
+    return {"kernel": kern, "bound": "issue", "issue_slots_busy_pct": row.get("issue%"),
             "sm_throughput_pct": row.get("sm%"), "achieved_occupancy_pct": row.get("occ%"),
             "ncu_us_alt200": row.get("us"), "source": src}
 
