@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kFastThreads, BLEND_MIN_CTAS) k_blend_fast(
 // instead of once per warp, and the ring depth hides the gather latency.
 // Consumers run the same per-sample code as k_blend_fast.
 #ifndef WS_STAGES
-#define WS_STAGES 4
+#define WS_STAGES 5
 #endif
 constexpr int kWsStages = WS_STAGES;
 constexpr int kWsConsumers = 8;
