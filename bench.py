@@ -301,6 +301,14 @@ def run_b200(args, rank, world, local):
     if dist:
         dist.barrier()
     e2e_frames = timed if args.e2e_steps <= 0 else timed[: max(1, min(len(timed), args.e2e_steps))]
+    # untimed warm-up of both e2e legs (W frames each: first-call host allocations and
+    # module loading stay out of the timed region, as for the device loop)
+    warm = order[: max(1, args.warmup)]
+    for rgb8 in (False, True):
+        scene.render_batch(warm, L.FilterConfig(TAU_R), L.ShrinkMode.three_sigma(),
+                           L.RenderOptions(output_rgb8=rgb8),
+                           host_ptrs=[ring[i % 4] for i in range(len(warm))])
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     if args.e2e_sync:
         st = L.RenderStatsC()

@@ -454,6 +454,10 @@ void GpuScene::ensure_resolution(int w, int h) {
     res_.big_list.alloc(n_tiles + 1);
     res_.tile_order.alloc(n_tiles + 1);
     res_.image.alloc(uint64_t(w) * h * 3);
+    // render_batch's second image and 8-bit staging: sized with the resolution so
+    // no batch call allocates (a first cudaMalloc there cost tens of ms)
+    image2_.alloc(uint64_t(w) * h * 3);
+    for (auto& b8 : rgb8b_) b8.alloc(uint64_t(w) * h * 3);
     const uint64_t b_cnt = align256(sizeof(FrameCounters));
     const uint64_t b_sel = align256(uint64_t(filter_status_entries(tree_.n)) * 4);
     const uint64_t b_prep = align256((tree_.n / kPrepBlock + 2) * 8);
@@ -639,19 +643,17 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
             FGS_CUDA(cudaEventCreateWithFlags(&copy_done_[k], cudaEventDisableTiming));
         }
     }
-    image2_.alloc(image_floats());
-    frame_log_.alloc(n);
-    if (h_batch_cap_ < n) {
+    frame_log_.alloc(std::max<uint64_t>(n, 1024));  // one allocation for typical batches
+    if (h_batch_cap_ < n) {  // pinned, grown geometrically (cudaMallocHost is slow)
+        const uint64_t cap = std::max<uint64_t>(n, std::max<uint64_t>(1024, 2 * h_batch_cap_));
         if (h_batch_counters_) FGS_CUDA(cudaFreeHost(h_batch_counters_));
-        FGS_CUDA(cudaMallocHost(&h_batch_counters_, n * sizeof(FrameCounters)));
-        h_batch_cap_ = n;
+        FGS_CUDA(cudaMallocHost(&h_batch_counters_, cap * sizeof(FrameCounters)));
+        h_batch_cap_ = cap;
     }
     const bool rgb8 = (p.flags & LODGS_RENDER_OUTPUT_RGB8) != 0;
     const uint64_t img_bytes = image_floats() * sizeof(float);
     const uint64_t out_bytes = rgb8 ? image_floats() : img_bytes;
     float* bufs[2] = {res_.image.p, image2_.p};
-    if (rgb8)
-        for (auto& b8 : rgb8b_) b8.alloc(image_floats());
     last_timing_ = false;
     last_keep_ = false;
     last_exact_ = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
