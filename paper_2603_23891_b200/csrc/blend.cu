@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
         const uint32_t flags = sh.st[s].flags;
         const int x = sh.st[s].x0 + int(warp & 1) * 8 + int(lane & 7);
         const int y = sh.st[s].y0 + int(warp >> 1) * 4 + int(lane >> 3);
-        if (nh > 0 && __any_sync(0xffffffffu, pix.T != 0.0f)) {
+        if (!WS_NOCONSUME && nh > 0 && __any_sync(0xffffffffu, pix.T != 0.0f)) {
             const PixState saved = pix;
             bool unsure = false;
             int k = 0;
