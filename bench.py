@@ -167,7 +167,7 @@ def measured_peak_gbs():
         return 6650.0, "fallback"
 
 
-def cpu_reference_sample(L, tree, cams, threads, budget_s=20.0, max_frames=6):
+def cpu_reference_sample(L, tree, cams, threads, budget_s=20.0, max_frames=6, extras=False):
     """The reference renderer (oracle/_ref) on host cores over a bounded, evenly
     strided sample of the path. FPS = frames / sum(T_total) as bench.cpp:160."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -187,12 +187,34 @@ def cpu_reference_sample(L, tree, cams, threads, budget_s=20.0, max_frames=6):
         frames += 1
         if time.perf_counter() - t_start > budget_s:
             break
+    # SURVEY 8(d)'s companion figures on two of the same frames: one thread, and
+    # collect_kpc=true (the reference bench always renders that way, bench.cpp:128)
+    extra = {}
+    if extras:
+        few = sample[:: max(1, len(sample) // 2)][:2]
+        for name, kw in (("same_frames_all_threads", dict(workers=threads)),
+                         ("single_thread", dict(workers=1)),
+                         ("collect_kpc", dict(workers=threads, collect_kpc=True))):
+            ms = sum(ref.render(h, cam, TAU_R, L.ShrinkMode.three_sigma(), **kw)["total_ms"]
+                     for cam in few)
+            extra[name] = {"value": len(few) / (ms / 1000.0), "unit": "frames/s",
+                           "cores": kw["workers"], "frames": len(few)}
     ref.free_tree(h)
     return {"value": frames / (total_ms / 1000.0), "unit": "frames/s", "cores": threads,
-            "kind": "reference",
+            "kind": "reference", "cpu_model": cpu_model(),
             "sample": f"{frames} frames of the 300-frame cfg-3 path (stride {stride}), "
                       f"lodgs::render T_total (bench.cpp:160); wall incl. per-frame "
-                      f"validation {frames / wall:.3f} frames/s"}
+                      f"validation {frames / wall:.3f} frames/s", **extra}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args, rank, world):
@@ -409,7 +431,7 @@ def run_b200(args, rank, world, local):
     }
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_reference_sample(L, tree, cams, os.cpu_count() or 1,
-                                                    budget_s=args.cpu_budget)
+                                                    budget_s=args.cpu_budget, extras=True)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
