@@ -24,7 +24,6 @@ struct DevTree {
     const SplatRec* splat = nullptr;
     // per node, the FP64 world covariance of mark_core (sigma3d, camera
     // independent): 6 doubles, precomputed at upload for the preprocess
-    const double* sig3 = nullptr;
     // Nodes [leaf_begin, n) are all leaves (leaf_begin a multiple of 1024, or n).
     uint64_t leaf_begin = 0;
     // max_i (|mx| + |my| + |mz|) over the tree (rounded up): the FP32 leaf

@@ -13,8 +13,7 @@ namespace fgs {
 // records.  soa = [mx|my|mz|sx|sy|sz] (stride n), ex = [qw|qx|qy|qz|op|cr|cg|cb].
 __global__ void k_pack_tree(const float* __restrict__ soa, const float* __restrict__ ex,
                             const uint8_t* __restrict__ leaf, uint64_t n, uint64_t leaf_begin,
-                            float4* geo, float4* iscale, float4* iquat, SplatRec* splat,
-                            double* sig3) {
+                            float4* geo, float4* iscale, float4* iquat, SplatRec* splat) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     SplatRec r;
@@ -35,14 +34,6 @@ __global__ void k_pack_tree(const float* __restrict__ soa, const float* __restri
     r.pad0 = 0.f;
     r.pad1 = 0.f;
     splat[i] = r;
-    const Sigma3 S = sigma3d(r.sx, r.sy, r.sz, r.qw, r.qx, r.qy, r.qz);
-    double* o = sig3 + 6 * i;
-    o[0] = S.s00;
-    o[1] = S.s01;
-    o[2] = S.s02;
-    o[3] = S.s11;
-    o[4] = S.s12;
-    o[5] = S.s22;
     // std::max(std::max(sx, sy), sz) of mark_core.hpp:33, exact in float (scales finite > 0)
     const float smax = fmaxf(fmaxf(r.sx, r.sy), r.sz);
     geo[i] = make_float4(r.mx, r.my, r.mz, smax);
@@ -54,10 +45,10 @@ __global__ void k_pack_tree(const float* __restrict__ soa, const float* __restri
 
 void launch_pack_tree(const float* soa, const float* extra, const uint8_t* leaf, uint64_t n,
                       uint64_t leaf_begin, float4* geo, float4* iscale, float4* iquat,
-                      SplatRec* splat, double* sig3, cudaStream_t s) {
+                      SplatRec* splat, cudaStream_t s) {
     if (n)
         k_pack_tree<<<unsigned((n + 255) / 256), 256, 0, s>>>(soa, extra, leaf, n, leaf_begin, geo,
-                                                              iscale, iquat, splat, sig3);
+                                                              iscale, iquat, splat);
 }
 
 __global__ void k_update_totals(const FrameCounters* cnt, const uint32_t* offsets, int n_tiles,

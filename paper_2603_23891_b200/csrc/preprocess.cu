@@ -43,7 +43,7 @@ struct Projected {
 };
 
 // projection.cpp:60-91 + effective_radius, with mark_core's world covariance
-// read precomputed (sigma3d at upload, identical operations).  known_visible:
+// from sigma3d (mark.cuh, mark_core.hpp's operations).  known_visible:
 // the node passed this frame's filter, whose frustum decision is the same
 // FP64 decision (mark_core.hpp:32-40), so the test is not repeated.
 __device__ __forceinline__ Projected project_one(const Geom& g, const SplatRec& r,
@@ -191,8 +191,7 @@ __device__ __forceinline__ void block_add2(uint32_t a, uint32_t b, unsigned long
 #define PREP_MIN_CTAS 4
 #endif
 __global__ void __launch_bounds__(kPrepBlock, PREP_MIN_CTAS) k_preprocess(
-    const Geom g, const SplatRec* __restrict__ splat, const double* __restrict__ sig3,
-    const uint32_t* __restrict__ selected, const int kind, const double tau, const int tiles_x,
+    const Geom g, const SplatRec* __restrict__ splat, const uint32_t* __restrict__ selected, const int kind, const double tau, const int tiles_x,
     const int tiles_y, PrepOut out, FrameCounters* cnt, const int use_hist,
     const int known_visible) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
@@ -206,54 +205,24 @@ __global__ void __launch_bounds__(kPrepBlock, PREP_MIN_CTAS) k_preprocess(
     __syncthreads();
     uint32_t kept = 0, pairs = 0;
     unsigned long long kor = 0, knand = 0;
-#ifndef PREP_PREFETCH
-#define PREP_PREFETCH 1
-#endif
-    // Software pipeline over the CTA's slots: the next slot's index (level 1;
-    // level 2 also its records, which spills at 64 registers and measured
-    // slower) is in flight while this one is projected.
-    auto load_rec = [&](uint32_t idx, float4 (&r)[4], double2 (&q)[3]) {
-        const float4* src = reinterpret_cast<const float4*>(splat + idx);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) r[k] = __ldg(src + k);
-        const double2* sp = reinterpret_cast<const double2*>(sig3 + 6 * uint64_t(idx));
-#pragma unroll
-        for (int k = 0; k < 3; ++k) q[k] = __ldg(sp + k);
-    };
+    // The next slot's index is in flight while this one is projected (a deeper
+    // prefetch of the 64-byte record spilled at 64 registers and was slower).
+    // The world covariance is recomputed from the record (sigma3d, the same FP64
+    // operations as mark_core) rather than read: 48 B per node less HBM traffic
+    // and storage, for ~200 FP64 instructions the kernel had issue room for.
     uint64_t s = lo + threadIdx.x;
     uint32_t idx_next = s < hi ? __ldg(selected + s) : 0u;
-#if PREP_PREFETCH >= 2
-    float4 nr[4];
-    double2 nq[3];
-    if (s < hi) load_rec(idx_next, nr, nq);
-    uint32_t idx_after = s + kPrepBlock < hi ? __ldg(selected + s + kPrepBlock) : 0u;
-#endif
     for (; s < hi; s += kPrepBlock) {
         const uint32_t idx = idx_next;
-#if PREP_PREFETCH >= 2
-        const float4 a = nr[0], b = nr[1], c = nr[2], d = nr[3];
-        const double2 s0 = nq[0], s1 = nq[1], s2 = nq[2];
-        idx_next = idx_after;
-        if (s + kPrepBlock < hi) load_rec(idx_next, nr, nq);
-        if (s + 2 * kPrepBlock < hi) idx_after = __ldg(selected + s + 2 * kPrepBlock);
-#else
-#if PREP_PREFETCH >= 1
         if (s + kPrepBlock < hi) idx_next = __ldg(selected + s + kPrepBlock);
-#else
-        if (s + kPrepBlock < hi) idx_next = selected[s + kPrepBlock];  // not in flight early
-#endif
-        float4 rr[4];
-        double2 qq[3];
-        load_rec(idx, rr, qq);
-        const float4 a = rr[0], b = rr[1], c = rr[2], d = rr[3];
-        const double2 s0 = qq[0], s1 = qq[1], s2 = qq[2];
-#endif
+        const float4* src = reinterpret_cast<const float4*>(splat + idx);
+        const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
         SplatRec rec;
         rec.mx = a.x; rec.my = a.y; rec.mz = a.z; rec.sx = a.w;
         rec.sy = b.x; rec.sz = b.y; rec.qw = b.z; rec.qx = b.w;
         rec.qy = c.x; rec.qz = c.y; rec.opacity = c.z; rec.cr = c.w;
         rec.cg = d.x; rec.cb = d.y;
-        const Sigma3 S{s0.x, s0.y, s1.x, s1.y, s2.x, s2.y};
+        const Sigma3 S = sigma3d(rec.sx, rec.sy, rec.sz, rec.qw, rec.qx, rec.qy, rec.qz);
         const Projected p = project_one(g, rec, S, kind, tau, known_visible != 0);
         GaussEmit e;
         e.node = idx;
@@ -332,7 +301,7 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
     const int use_hist = n_tiles <= kHistMaxTiles ? 1 : 0;
     const size_t smem = use_hist ? size_t(n_tiles) * 4 : 0;
     launch_pdl(k_preprocess, grid, kPrepBlock, smem, s, g, t.splat,
-               static_cast<const double*>(t.sig3), selected, shrink_kind, tau, tiles_x, tiles_y,
+               selected, shrink_kind, tau, tiles_x, tiles_y,
                out, cnt, use_hist, known_visible ? 1 : 0);
 }
 

@@ -34,7 +34,7 @@ DeviceGuard::~DeviceGuard() {
 
 void launch_pack_tree(const float* soa, const float* extra, const uint8_t* leaf, uint64_t n,
                       uint64_t leaf_begin, float4* geo, float4* iscale, float4* iquat,
-                      SplatRec* splat, double* sig3, cudaStream_t s);
+                      SplatRec* splat, cudaStream_t s);
 void launch_update_totals(const FrameCounters* cnt, const uint32_t* offsets, int n_tiles,
                           RunTotals* totals, cudaStream_t s);
 void launch_max_tile(const uint32_t* triples, uint64_t n, unsigned int* out, cudaStream_t s);
@@ -297,9 +297,8 @@ void GpuScene::ingest(uint64_t n, const std::vector<uint64_t>& level_begin, bool
     iscale_.alloc(nb);
     iquat_.alloc(nb);
     splat_.alloc(n);
-    sig3_.alloc(6 * n);
     launch_pack_tree(st.soa.p, st.soa.p + 6 * n, st.leaf.p, n, nb, geo_.p, iscale_.p, iquat_.p,
-                     splat_.p, sig3_.p, stream_);
+                     splat_.p, stream_);
     parent_.alloc(np);
     FGS_CUDA(cudaMemsetAsync(parent_.p, 0xFF, np * 4, stream_));
     if (n) FGS_CUDA(cudaMemcpyAsync(parent_.p, st.parent.p, n * 4, cudaMemcpyDeviceToDevice, stream_));
@@ -309,7 +308,6 @@ void GpuScene::ingest(uint64_t n, const std::vector<uint64_t>& level_begin, bool
     tree_.iquat = iquat_.p;
     tree_.parent = parent_.p;
     tree_.splat = splat_.p;
-    tree_.sig3 = sig3_.p;
     alloc_frame_buffers(std::max<uint64_t>(4 * n, 1u << 16));
 }
 
@@ -429,7 +427,6 @@ void GpuScene::reserve_pairs(uint64_t n) {
 uint64_t GpuScene::device_bytes() const {
     return (twin_ ? twin_->device_bytes() : 0) + geo_.bytes() + iscale_.bytes() + iquat_.bytes() +
            parent_.bytes() + splat_.bytes() +
-           sig3_.bytes() +
            cand_bits_.bytes() + qint_bits_.bytes() + selected_.bytes() + g64_.bytes() +
            g32_.bytes() + emit_.bytes() + col64_.bytes() + keys_.bytes() + zero_.bytes() +
            res_.tile_offsets.bytes() + res_.tile_cursor.bytes() + res_.big_list.bytes() +

@@ -176,7 +176,6 @@ private:
     DevBuf<float4> iquat_;     // internal region: quaternion
     DevBuf<uint32_t> parent_;
     DevBuf<SplatRec> splat_;
-    DevBuf<double> sig3_;      // per node: mark_core's world covariance (6 doubles)
     // frame storage
     DevBuf<uint32_t> cand_bits_, qint_bits_, selected_;
     DevBuf<Gauss64> g64_;
