@@ -11,7 +11,8 @@ from paper_2603_23891_b200 import lodgs as L  # noqa: E402
 
 tree = L.build_synthetic_tree(nx=103, ny=104, seed=1, depth=4, build_seed=7)
 with L.GpuScene(tree) as s:
-    for alt in (400.0, 300.0, 200.0, 110.0):
+    alts = [float(a) for a in os.environ.get("CFG4_ALTS", "400,300,200,110").split(",")]
+    for alt in alts:
         cam = topdown_camera(3840, 2160, 2000.0, alt)
         for _ in range(3):
             out = s.render(cam, L.FilterConfig(3.0), L.ShrinkMode.three_sigma(),
