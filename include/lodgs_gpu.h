@@ -234,10 +234,10 @@ LODGS_API int lodgs_gpu_render_async(lodgs_gpu_scene *scene, const lodgs_camera 
                            const lodgs_render_params *params, float *image_host);
 /* Waits for every in-flight frame; stats (nullable) = the last frame's. */
 LODGS_API int lodgs_gpu_sync(lodgs_gpu_scene *scene, lodgs_render_stats *stats);
-/* Frames in flight for lodgs_gpu_render_async: 1, or 2 (default) -- consecutive
- * frames alternate between the scene and a twin context (own stream and
+/* Frames in flight for lodgs_gpu_render_async: 1, 2 or 3 (default) -- consecutive
+ * frames rotate over the scene and up to two twin contexts (own stream and
  * per-frame buffers over the same device tree), so one frame's latency-bound
- * kernels overlap the other's.  Both fork from the scene's control stream
+ * kernels overlap the others'.  All fork from the scene's control stream
  * (lodgs_gpu_scene_stream): a frame starts after the work already enqueued
  * there (e.g. a timing event). */
 LODGS_API int lodgs_gpu_scene_set_inflight(lodgs_gpu_scene *scene, int frames);

@@ -93,9 +93,9 @@ GpuScene::GpuScene(const lodgs_tree_view& tree, int device) : device_(device) {
     for (uint32_t l = 0; l < tree.n_levels; ++l) lb.push_back(tree.level_offsets[l]);
     shrink_factor_ = tree.shrink_factor;
     ingest(n, lb, per_node, msgs, nv, st);
-    // the second in-flight context exists from the start, so no allocation ever
+    // the other in-flight contexts exist from the start, so no allocation ever
     // lands inside a caller's timed loop of render_async frames
-    if (inflight_ == 2) twin_.reset(new GpuScene(*this, TwinTag{}));
+    make_contexts(inflight_);
 }
 
 namespace {
@@ -228,9 +228,9 @@ GpuScene::GpuScene(const std::string& path, int device, double* timing_ms) : dev
     std::vector<uint64_t> lb(offs.begin(), offs.end());
     shrink_factor_ = shrink;
     ingest(n, lb, per_node, msgs, nv, st);
-    // the second in-flight context exists from the start, so no allocation ever
+    // the other in-flight contexts exist from the start, so no allocation ever
     // lands inside a caller's timed loop of render_async frames
-    if (inflight_ == 2) twin_.reset(new GpuScene(*this, TwinTag{}));
+    make_contexts(inflight_);
     const auto t3 = clock::now();
     if (timing_ms) {
         auto ms = [](clock::time_point a, clock::time_point b) {
@@ -336,21 +336,36 @@ GpuScene::GpuScene(const GpuScene& owner, TwinTag) : device_(owner.device_) {
     alloc_frame_buffers(owner.pair_cap_);
 }
 
+// Frame contexts in flight: this scene (0), twin_ (1), twin_->twin_ (2).  Each
+// twin owns its stream, counters and per-frame buffers over the shared tree;
+// the per-context operations (reserve, resolution, totals, memory) recurse.
+GpuScene* GpuScene::context(int i) {
+    if (i == 0) return this;
+    if (i == 1) return twin_.get();
+    return twin_ ? twin_->twin_.get() : nullptr;
+}
+
+void GpuScene::make_contexts(int n) {
+    if (n >= 2 && !twin_) twin_.reset(new GpuScene(*this, TwinTag{}));
+    if (n >= 3 && !twin_->twin_) twin_->twin_.reset(new GpuScene(*twin_, TwinTag{}));
+}
+
 void GpuScene::set_inflight(int n) {
-    if (n < 1 || n > 2) throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1 or 2");
+    if (n < 1 || n > kMaxInflight)
+        throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1, 2 or 3");
     join();
     inflight_ = n;
-    if (n == 2 && !twin_) twin_.reset(new GpuScene(*this, TwinTag{}));
+    make_contexts(n);
 }
 
 void GpuScene::join() {
     if (!ctl_) return;
     DeviceGuard dg(device_);
-    FGS_CUDA(cudaEventRecord(join_ev_[0], stream_));
-    FGS_CUDA(cudaStreamWaitEvent(ctl_, join_ev_[0], 0));
-    if (twin_) {
-        FGS_CUDA(cudaEventRecord(join_ev_[1], twin_->stream_));
-        FGS_CUDA(cudaStreamWaitEvent(ctl_, join_ev_[1], 0));
+    for (int i = 0; i < kMaxInflight; ++i) {
+        GpuScene* c = context(i);
+        if (!c) continue;
+        FGS_CUDA(cudaEventRecord(join_ev_[i], c->stream_));
+        FGS_CUDA(cudaStreamWaitEvent(ctl_, join_ev_[i], 0));
     }
 }
 
@@ -366,10 +381,10 @@ void GpuScene::enqueue_async(const lodgs_camera& cam, const lodgs_render_params&
         last_frame_ = this;
         return;
     }
-    if (!twin_) twin_.reset(new GpuScene(*this, TwinTag{}));
-    GpuScene* tgt = (async_frames_++ & 1) ? twin_.get() : this;
+    make_contexts(inflight_);
+    GpuScene* tgt = context(int(async_frames_++ % uint64_t(inflight_)));
     // fork from the control stream: the frame orders after the caller's events
-    // there (e.g. a timing start), not after the other context's frames
+    // there (e.g. a timing start), not after the other contexts' frames
     FGS_CUDA(cudaEventRecord(fork_ev_, ctl_));
     FGS_CUDA(cudaStreamWaitEvent(tgt->stream_, fork_ev_, 0));
     tgt->enqueue_frame(cam, p, image_host);

@@ -162,10 +162,16 @@ private:
     std::vector<uint64_t> level_begin_;  // scene.hpp:53 level_begin(l), host copy
     float shrink_factor_ = 0.5f;
     // frames in flight
-    int inflight_ = 2;
+#ifndef FGS_INFLIGHT_DEFAULT
+#define FGS_INFLIGHT_DEFAULT 3
+#endif
+    static constexpr int kMaxInflight = 3;
+    int inflight_ = FGS_INFLIGHT_DEFAULT;
+    GpuScene* context(int i);
+    void make_contexts(int n);
     std::unique_ptr<GpuScene> twin_;
     cudaStream_t ctl_ = nullptr;
-    cudaEvent_t fork_ev_ = nullptr, join_ev_[2] = {};
+    cudaEvent_t fork_ev_ = nullptr, join_ev_[3] = {};
     uint64_t async_frames_ = 0;
     GpuScene* last_frame_ = nullptr;
     DevBuf<unsigned> level_flag_;        // serial filter: level had an active node
