@@ -234,8 +234,8 @@ LODGS_API int lodgs_gpu_render_async(lodgs_gpu_scene *scene, const lodgs_camera 
                            const lodgs_render_params *params, float *image_host);
 /* Waits for every in-flight frame; stats (nullable) = the last frame's. */
 LODGS_API int lodgs_gpu_sync(lodgs_gpu_scene *scene, lodgs_render_stats *stats);
-/* Frames in flight for lodgs_gpu_render_async: 1, 2 or 3 (default) -- consecutive
- * frames rotate over the scene and up to two twin contexts (own stream and
+/* Frames in flight for lodgs_gpu_render_async: 1 to 4 (default 4) -- consecutive
+ * frames rotate over the scene and up to three twin contexts (own stream and
  * per-frame buffers over the same device tree), so one frame's latency-bound
  * kernels overlap the others'.  All fork from the scene's control stream
  * (lodgs_gpu_scene_stream): a frame starts after the work already enqueued

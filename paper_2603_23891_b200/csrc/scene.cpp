@@ -340,19 +340,22 @@ GpuScene::GpuScene(const GpuScene& owner, TwinTag) : device_(owner.device_) {
 // twin owns its stream, counters and per-frame buffers over the shared tree;
 // the per-context operations (reserve, resolution, totals, memory) recurse.
 GpuScene* GpuScene::context(int i) {
-    if (i == 0) return this;
-    if (i == 1) return twin_.get();
-    return twin_ ? twin_->twin_.get() : nullptr;
+    GpuScene* c = this;
+    for (; c && i > 0; --i) c = c->twin_.get();
+    return c;
 }
 
 void GpuScene::make_contexts(int n) {
-    if (n >= 2 && !twin_) twin_.reset(new GpuScene(*this, TwinTag{}));
-    if (n >= 3 && !twin_->twin_) twin_->twin_.reset(new GpuScene(*twin_, TwinTag{}));
+    GpuScene* c = this;
+    for (int i = 1; i < n; ++i) {
+        if (!c->twin_) c->twin_.reset(new GpuScene(*c, TwinTag{}));
+        c = c->twin_.get();
+    }
 }
 
 void GpuScene::set_inflight(int n) {
     if (n < 1 || n > kMaxInflight)
-        throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1, 2 or 3");
+        throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1 to 4");
     join();
     inflight_ = n;
     make_contexts(n);

@@ -163,15 +163,15 @@ private:
     float shrink_factor_ = 0.5f;
     // frames in flight
 #ifndef FGS_INFLIGHT_DEFAULT
-#define FGS_INFLIGHT_DEFAULT 3
+#define FGS_INFLIGHT_DEFAULT 4
 #endif
-    static constexpr int kMaxInflight = 3;
+    static constexpr int kMaxInflight = 4;
     int inflight_ = FGS_INFLIGHT_DEFAULT;
     GpuScene* context(int i);
     void make_contexts(int n);
     std::unique_ptr<GpuScene> twin_;
     cudaStream_t ctl_ = nullptr;
-    cudaEvent_t fork_ev_ = nullptr, join_ev_[3] = {};
+    cudaEvent_t fork_ev_ = nullptr, join_ev_[4] = {};
     uint64_t async_frames_ = 0;
     GpuScene* last_frame_ = nullptr;
     DevBuf<unsigned> level_flag_;        // serial filter: level had an active node

@@ -785,7 +785,7 @@ class GpuScene:
         _check(self._lib.lodgs_gpu_join(self._h))
 
     def set_inflight(self, frames: int) -> None:
-        """Frames in flight for render_async (1, 2 or 3; default 3)."""
+        """Frames in flight for render_async (1 to 4; default 4)."""
         _check(self._lib.lodgs_gpu_scene_set_inflight(self._h, int(frames)))
 
     def sync(self) -> RenderStats:

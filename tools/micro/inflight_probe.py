@@ -17,7 +17,7 @@ with L.GpuScene(tree) as s:
     p = s.params(L.FilterConfig(bench.TAU_R), L.ShrinkMode.three_sigma(), L.RenderOptions())
     stream = torch.cuda.ExternalStream(s.stream_ptr())
     for rep in range(2):
-        for n in (1, 2, 3):
+        for n in (1, 2, 3, 4):
             s.set_inflight(n)
             for c in cams[:10]:
                 s.render_async(c, p)

@@ -169,7 +169,7 @@ def main():
     ap.add_argument("--which", nargs="+", default=["cfg2", "cfg4"])
     ap.add_argument("--frames", type=int, default=30)
     ap.add_argument("--lambda-g", type=float, default=0.2)
-    ap.add_argument("--inflight", type=int, default=3, choices=(1, 2, 3))
+    ap.add_argument("--inflight", type=int, default=4, choices=(1, 2, 3, 4))
     args = ap.parse_args()
     for w in args.which:
         run(w, args.frames, args.lambda_g, args.inflight)
