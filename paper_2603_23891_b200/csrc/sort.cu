@@ -58,8 +58,6 @@ __device__ __forceinline__ void flip_bitonic(unsigned long long* a, Index n, Ind
 }
 
 constexpr int kSmallSortThreads = 256;
-constexpr int kRegItems = 4;  // keys per thread in the register network
-constexpr int kRegCap = kSmallSortThreads * kRegItems;
 constexpr uint32_t kRun = 1024;  // run length of the run-sort + rank-merge path
 
 // Barriers over the threads that sort one bucket (or one run): the whole
