@@ -423,7 +423,7 @@ GpuScene::~GpuScene() {
     if (copy_stream_) {
         cudaStreamSynchronize(copy_stream_);
         cudaStreamDestroy(copy_stream_);
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kBatchBufs; ++k) {
             cudaEventDestroy(frame_done_[k]);
             cudaEventDestroy(copy_done_[k]);
         }
@@ -471,7 +471,7 @@ void GpuScene::ensure_resolution(int w, int h) {
     res_.image.alloc(uint64_t(w) * h * 3);
     // render_batch's second image and 8-bit staging: sized with the resolution so
     // no batch call allocates (a first cudaMalloc there cost tens of ms)
-    image2_.alloc(uint64_t(w) * h * 3);
+    for (auto& im : image2_) im.alloc(uint64_t(w) * h * 3);
     for (auto& b8 : rgb8b_) b8.alloc(uint64_t(w) * h * 3);
     const uint64_t b_cnt = align256(sizeof(FrameCounters));
     const uint64_t b_sel = align256(uint64_t(filter_status_entries(tree_.n)) * 4);
@@ -653,7 +653,7 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
     ensure_resolution(int(cams[0].width), int(cams[0].height));
     if (!copy_stream_) {
         FGS_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kBatchBufs; ++k) {
             FGS_CUDA(cudaEventCreateWithFlags(&frame_done_[k], cudaEventDisableTiming));
             FGS_CUDA(cudaEventCreateWithFlags(&copy_done_[k], cudaEventDisableTiming));
         }
@@ -668,14 +668,17 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
     const bool rgb8 = (p.flags & LODGS_RENDER_OUTPUT_RGB8) != 0;
     const uint64_t img_bytes = image_floats() * sizeof(float);
     const uint64_t out_bytes = rgb8 ? image_floats() : img_bytes;
-    float* bufs[2] = {res_.image.p, image2_.p};
+    float* bufs[kBatchBufs];
+    bufs[0] = res_.image.p;
+    for (int k = 1; k < kBatchBufs; ++k) bufs[k] = image2_[k - 1].p;
     last_timing_ = false;
     last_keep_ = false;
     last_exact_ = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
     for (uint64_t i = 0; i < n; ++i) {
-        const int k = int(i & 1);
-        // the blend may overwrite bufs[k] only once frame i-2's copy out of it is done
-        if (i >= 2) FGS_CUDA(cudaStreamWaitEvent(stream_, copy_done_[k], 0));
+        const int k = int(i % kBatchBufs);
+        // the blend may overwrite bufs[k] only once the copy out of it (frame
+        // i - kBatchBufs) is done
+        if (i >= uint64_t(kBatchBufs)) FGS_CUDA(cudaStreamWaitEvent(stream_, copy_done_[k], 0));
         image_target_ = bufs[k];
         log_target_ = frame_log_.p + i;
         enqueue_pipeline(camera_geom(cams[i]), p, int(cams[i].width), int(cams[i].height), false);
@@ -696,8 +699,8 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
     FGS_CUDA(cudaStreamSynchronize(stream_));
     FGS_CUDA(cudaStreamSynchronize(copy_stream_));
     // the last frame's image also lives in res_.image for read_image()
-    if (bufs[(n - 1) & 1] != res_.image.p)
-        FGS_CUDA(cudaMemcpy(res_.image.p, bufs[(n - 1) & 1], img_bytes, cudaMemcpyDeviceToDevice));
+    if (bufs[(n - 1) % kBatchBufs] != res_.image.p)
+        FGS_CUDA(cudaMemcpy(res_.image.p, bufs[(n - 1) % kBatchBufs], img_bytes, cudaMemcpyDeviceToDevice));
     *h_counters_ = h_batch_counters_[n - 1];
     for (uint64_t i = 0; i < n; ++i) {
         const FrameCounters& c = h_batch_counters_[i];

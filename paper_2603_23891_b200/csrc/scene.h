@@ -221,10 +221,14 @@ private:
     bool last_exact_ = false;
     // pipelined batches: second image buffer, copy stream, per-frame counters
     float* image_target_ = nullptr;  // blend output override (nullptr: res_.image)
-    DevBuf<float> image2_;
-    DevBuf<uint8_t> rgb8b_[2];  // render_batch with LODGS_RENDER_OUTPUT_RGB8
+#ifndef FGS_BATCH_BUFS
+#define FGS_BATCH_BUFS 3
+#endif
+    static constexpr int kBatchBufs = FGS_BATCH_BUFS;  // render_batch image ring
+    DevBuf<float> image2_[kBatchBufs - 1];
+    DevBuf<uint8_t> rgb8b_[kBatchBufs];  // render_batch with LODGS_RENDER_OUTPUT_RGB8
     cudaStream_t copy_stream_ = nullptr;
-    cudaEvent_t frame_done_[2] = {}, copy_done_[2] = {};
+    cudaEvent_t frame_done_[kBatchBufs] = {}, copy_done_[kBatchBufs] = {};
     FrameCounters* h_batch_counters_ = nullptr;
     DevBuf<FrameCounters> frame_log_;      // device-side per-frame counters of a batch
     FrameCounters* log_target_ = nullptr;  // enqueue_pipeline: where k_tile_offsets logs
