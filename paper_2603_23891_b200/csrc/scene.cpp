@@ -674,18 +674,31 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
     last_timing_ = false;
     last_keep_ = false;
     last_exact_ = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
+    // frames rotate over the in-flight contexts like render_async (the image
+    // ring, the copy stream and the counter log stay this scene's); every
+    // context first orders after the work already on this scene's stream
+    const int nctx = profiling_ ? 1 : inflight_;
+    make_contexts(nctx);
+    if (nctx > 1) {
+        FGS_CUDA(cudaEventRecord(frame_done_[0], stream_));
+        for (int c = 1; c < nctx; ++c)
+            FGS_CUDA(cudaStreamWaitEvent(context(c)->stream_, frame_done_[0], 0));
+    }
     for (uint64_t i = 0; i < n; ++i) {
         const int k = int(i % kBatchBufs);
+        GpuScene* c = context(int(i % uint64_t(nctx)));
         // the blend may overwrite bufs[k] only once the copy out of it (frame
         // i - kBatchBufs) is done
-        if (i >= uint64_t(kBatchBufs)) FGS_CUDA(cudaStreamWaitEvent(stream_, copy_done_[k], 0));
-        image_target_ = bufs[k];
-        log_target_ = frame_log_.p + i;
-        enqueue_pipeline(camera_geom(cams[i]), p, int(cams[i].width), int(cams[i].height), false);
-        image_target_ = nullptr;
-        log_target_ = nullptr;
-        if (rgb8) launch_rgb8(bufs[k], image_floats(), rgb8b_[k].p, stream_);
-        FGS_CUDA(cudaEventRecord(frame_done_[k], stream_));
+        if (i >= uint64_t(kBatchBufs))
+            FGS_CUDA(cudaStreamWaitEvent(c->stream_, copy_done_[k], 0));
+        c->image_target_ = bufs[k];
+        c->log_target_ = frame_log_.p + i;
+        c->enqueue_pipeline(camera_geom(cams[i]), p, int(cams[i].width), int(cams[i].height),
+                            false);
+        c->image_target_ = nullptr;
+        c->log_target_ = nullptr;
+        if (rgb8) launch_rgb8(bufs[k], image_floats(), rgb8b_[k].p, c->stream_);
+        FGS_CUDA(cudaEventRecord(frame_done_[k], c->stream_));
         FGS_CUDA(cudaStreamWaitEvent(copy_stream_, frame_done_[k], 0));
         if (images_host && images_host[i])
             FGS_CUDA(cudaMemcpyAsync(images_host[i],
@@ -693,6 +706,7 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
                                      out_bytes, cudaMemcpyDeviceToHost, copy_stream_));
         FGS_CUDA(cudaEventRecord(copy_done_[k], copy_stream_));
     }
+    for (int c = 1; c < nctx; ++c) FGS_CUDA(cudaStreamSynchronize(context(c)->stream_));
     // every frame's counters in one copy, after the last frame
     FGS_CUDA(cudaMemcpyAsync(h_batch_counters_, frame_log_.p, n * sizeof(FrameCounters),
                              cudaMemcpyDeviceToHost, stream_));
