@@ -400,3 +400,23 @@ def test_ldgs_writer_matches_reference_save_scene(L, tmp_path):
         assert mine.read_bytes() == ref_path.read_bytes()
         ok, n, levels, _ = ref_ldgs("load", mine).split()
         assert ok == "OK" and int(n) == tree.node_count() and int(levels) == len(tree.level_offsets)
+
+
+def test_integration_shim_compiles_against_reference_headers(tmp_path):
+    """INTEGRATION.md's reference-side C++ shim (lodgs::render over the C ABI)
+    type-checks against the reference's own headers and include/lodgs_gpu.h."""
+    import shutil
+    import subprocess
+
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc) or not shutil.which("g++"):
+        pytest.skip("reference headers or g++ absent")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "INTEGRATION.md")).read()
+    start = text.index("```cpp\n// proj/src/rasterizer_b200.cpp") + len("```cpp\n")
+    src = tmp_path / "rasterizer_b200.cpp"
+    src.write_text(text[start:text.index("```", start)])
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", f"-I{ref_inc}",
+                        f"-I{os.path.join(root, 'include')}", str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
