@@ -452,8 +452,8 @@ uint64_t GpuScene::device_bytes() const {
 }
 
 void GpuScene::ensure_resolution(int w, int h) {
-    // the second in-flight context follows, so its first frame at a new
-    // resolution never allocates inside a caller's stream of async frames
+    // the other in-flight contexts follow (recursively), so their first frame at
+    // a new resolution never allocates inside a caller's stream of async frames
     if (twin_) twin_->ensure_resolution(w, h);
     if (w == res_.width && h == res_.height && zero_.p) return;
     FGS_CUDA(cudaStreamSynchronize(stream_));

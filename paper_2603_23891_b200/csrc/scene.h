@@ -124,10 +124,11 @@ public:
     void set_reference_image();
     void compare_reference(double* psnr, double* ssim);
 
-    // Frames in flight (1 or 2, default 2): render_async alternates frames between
-    // this context and a twin context (own stream and per-frame buffers, same
-    // device tree), forked from the control stream; join() makes the control
-    // stream wait for both.  stream() is the control stream once a twin exists.
+    // Frames in flight (1 to kMaxInflight, default 4): render_async and
+    // render_batch rotate frames over this context and chained twin contexts
+    // (own stream and per-frame buffers, same device tree), forked from the
+    // control stream; join() makes the control stream wait for all of them.
+    // stream() is the control stream.
     void set_inflight(int n);
     void enqueue_async(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host);
     void join();
