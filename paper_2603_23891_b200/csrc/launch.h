@@ -73,6 +73,11 @@ struct PrepOut {
     GaussEmit* emit;
     GaussCol64* col64;     // nullable: only for the exact blend
     uint32_t* tile_count;  // n_tiles, zeroed per frame
+    // nullable: each CTA's nonzero (tile, count) entries of its shared tile
+    // histogram (grid x n_tiles capacity) and their number, so K4 reserves its
+    // runs without recounting
+    uint2* tile_lists = nullptr;
+    uint32_t* tile_list_len = nullptr;
 };
 constexpr int kHistMaxTiles = 12288;  // shared-memory tile histograms up to 48 KB
 constexpr int16_t kDropped = -32768;  // GaussEmit::ty0 of a slot dropped by project()
@@ -92,7 +97,8 @@ void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offs
 // Key duplication: one key per (gaussian, overlapped tile) scattered into the
 // tile's bucket; key = depth_bits << 32 | gaussian.
 void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x, int n_tiles,
-                      uint32_t* cursor, unsigned long long* keys, int grid, cudaStream_t s);
+                      uint32_t* cursor, unsigned long long* keys, int grid, cudaStream_t s,
+                      const uint2* tile_lists = nullptr, const uint32_t* tile_list_len = nullptr);
 // Readbacks: slot -> BlendList index map, and slot-indexed records compacted
 // into BlendList order.
 void launch_slot_map(const GaussEmit* emit, uint64_t n, unsigned long long* status,

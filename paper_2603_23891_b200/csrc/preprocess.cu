@@ -284,10 +284,26 @@ __global__ void __launch_bounds__(kPrepBlock, PREP_MIN_CTAS) k_preprocess(
         if (knand) atomicOr(&cnt->key_nand, knand);
     }
     if (use_hist) {
+        __shared__ uint32_t s_nlist;
+        if (threadIdx.x == 0) s_nlist = 0u;
         __syncthreads();
-        for (int t = threadIdx.x; t < n_tiles; t += kPrepBlock) {
-            const uint32_t c = s_hist[t];
+        uint2* list = out.tile_lists ? out.tile_lists + uint64_t(blockIdx.x) * n_tiles : nullptr;
+        const unsigned lane = threadIdx.x & 31;
+        for (int t0 = 0; t0 < n_tiles; t0 += kPrepBlock) {  // warp-uniform trip count
+            const int t = t0 + int(threadIdx.x);
+            const uint32_t c = t < n_tiles ? s_hist[t] : 0u;
             if (c) atomicAdd(out.tile_count + t, c);
+            if (list) {  // compacted append, one shared atomic per warp
+                const unsigned m = __ballot_sync(0xffffffffu, c != 0u);
+                uint32_t base = 0;
+                if (lane == 0 && m) base = atomicAdd(&s_nlist, unsigned(__popc(m)));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (c) list[base + __popc(m & ((1u << lane) - 1u))] = make_uint2(uint32_t(t), c);
+            }
+        }
+        if (list) {
+            __syncthreads();
+            if (threadIdx.x == 0) out.tile_list_len[blockIdx.x] = s_nlist;
         }
     }
 }
@@ -650,7 +666,9 @@ void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offs
 __global__ void __launch_bounds__(256) k_emit_keys(const GaussEmit* __restrict__ emit,
                                                    const FrameCounters* cnt, int tiles_x,
                                                    int n_tiles, uint32_t* cursor,
-                                                   unsigned long long* keys, int use_hist) {
+                                                   unsigned long long* keys, int use_hist,
+                                                   const uint2* __restrict__ tile_lists,
+                                                   const uint32_t* __restrict__ tile_list_len) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
     extern __shared__ uint32_t s_hist[];
@@ -667,17 +685,29 @@ __global__ void __launch_bounds__(256) k_emit_keys(const GaussEmit* __restrict__
         }
         return;
     }
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_hist[t] = 0u;
-    __syncthreads();
-    for (uint64_t s = lo + threadIdx.x; s < hi; s += blockDim.x) {
-        const GaussEmit e = emit[s];
-        for (int ty = e.ty0; ty <= e.ty1; ++ty)
-            for (int tx = e.tx0; tx <= e.tx1; ++tx) atomicAdd(s_hist + (ty * tiles_x + tx), 1u);
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-        const uint32_t c = s_hist[t];
-        if (c) s_hist[t] = atomicAdd(cursor + t, c);
+    if (tile_lists) {
+        // K3 left this CTA's nonzero (tile, count) entries (same slice, same grid):
+        // reserve one run per touched tile; untouched tiles are never read below
+        const uint2* list = tile_lists + uint64_t(blockIdx.x) * n_tiles;
+        const uint32_t nl = tile_list_len[blockIdx.x];
+        for (uint32_t k = threadIdx.x; k < nl; k += blockDim.x) {
+            const uint2 e = list[k];
+            s_hist[e.x] = atomicAdd(cursor + e.x, e.y);
+        }
+    } else {
+        for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) s_hist[t] = 0u;
+        __syncthreads();
+        for (uint64_t s = lo + threadIdx.x; s < hi; s += blockDim.x) {
+            const GaussEmit e = emit[s];
+            for (int ty = e.ty0; ty <= e.ty1; ++ty)
+                for (int tx = e.tx0; tx <= e.tx1; ++tx)
+                    atomicAdd(s_hist + (ty * tiles_x + tx), 1u);
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+            const uint32_t c = s_hist[t];
+            if (c) s_hist[t] = atomicAdd(cursor + t, c);
+        }
     }
     __syncthreads();
     for (uint64_t s = lo + threadIdx.x; s < hi; s += blockDim.x) {
@@ -690,11 +720,12 @@ __global__ void __launch_bounds__(256) k_emit_keys(const GaussEmit* __restrict__
 }
 
 void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles_x, int n_tiles,
-                      uint32_t* cursor, unsigned long long* keys, int grid, cudaStream_t s) {
+                      uint32_t* cursor, unsigned long long* keys, int grid, cudaStream_t s,
+                      const uint2* tile_lists, const uint32_t* tile_list_len) {
     const int use_hist = n_tiles <= kHistMaxTiles ? 1 : 0;
     const size_t smem = use_hist ? size_t(n_tiles) * 4 : 0;
     launch_pdl(k_emit_keys, grid, 256, smem, s, emit, cnt, tiles_x, n_tiles, cursor, keys,
-               use_hist);
+               use_hist, use_hist ? tile_lists : nullptr, use_hist ? tile_list_len : nullptr);
 }
 
 // Readback support: slot -> BlendList index (chained scan over kept flags),

@@ -446,6 +446,7 @@ uint64_t GpuScene::device_bytes() const {
     return (twin_ ? twin_->device_bytes() : 0) + geo_.bytes() + iscale_.bytes() + iquat_.bytes() +
            parent_.bytes() + splat_.bytes() +
            cand_bits_.bytes() + qint_bits_.bytes() + selected_.bytes() + g64_.bytes() +
+           tile_lists_.bytes() + tile_list_len_.bytes() +
            g32_.bytes() + emit_.bytes() + col64_.bytes() + keys_.bytes() + zero_.bytes() +
            res_.tile_offsets.bytes() + res_.tile_cursor.bytes() + res_.big_list.bytes() +
            res_.image.bytes();
@@ -472,6 +473,10 @@ void GpuScene::ensure_resolution(int w, int h) {
     // render_batch's second image and 8-bit staging: sized with the resolution so
     // no batch call allocates (a first cudaMalloc there cost tens of ms)
     for (auto& im : image2_) im.alloc(uint64_t(w) * h * 3);
+    if (n_tiles <= uint64_t(kHistMaxTiles)) {
+        tile_lists_.alloc(uint64_t(persistent_grid_) * n_tiles);
+        tile_list_len_.alloc(uint64_t(persistent_grid_));
+    }
     for (auto& b8 : rgb8b_) b8.alloc(uint64_t(w) * h * 3);
     const uint64_t b_cnt = align256(sizeof(FrameCounters));
     const uint64_t b_sel = align256(uint64_t(filter_status_entries(tree_.n)) * 4);
@@ -530,7 +535,9 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     last_serial_ = (p.flags & LODGS_RENDER_FILTER_SERIAL) != 0;
     if (timing) FGS_CUDA(cudaEventRecord(ev_[1], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[2], stream_));
-    PrepOut out{g64_.p, g32_.p, emit_.p, exact ? col64_.p : nullptr, d_tile_count_};
+    const bool lists = n_tiles <= kHistMaxTiles && tile_lists_.p;
+    PrepOut out{g64_.p, g32_.p, emit_.p, exact ? col64_.p : nullptr, d_tile_count_,
+                lists ? tile_lists_.p : nullptr, lists ? tile_list_len_.p : nullptr};
     launch_preprocess(g, tree_, selected_.p, tree_.n, p.shrink_kind, p.tau, res_.tiles_x,
                       res_.tiles_y, out, d_counters_, persistent_grid_, stream_,
                       /*known_visible=*/true);
@@ -538,7 +545,8 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
                         res_.big_list.p, res_.tile_order.p, d_counters_, pair_cap_, stream_,
                         totals_.p, log_target_);
     launch_emit_keys(emit_.p, d_counters_, res_.tiles_x, n_tiles, res_.tile_cursor.p, keys_.p,
-                     persistent_grid_, stream_);
+                     persistent_grid_, stream_, lists ? tile_lists_.p : nullptr,
+                     lists ? tile_list_len_.p : nullptr);
     maps_valid_ = false;
     if (timing) FGS_CUDA(cudaEventRecord(ev_[2], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[3], stream_));

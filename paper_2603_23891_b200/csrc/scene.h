@@ -185,6 +185,8 @@ private:
     DevBuf<SplatRec> splat_;
     // frame storage
     DevBuf<uint32_t> cand_bits_, qint_bits_, selected_;
+    DevBuf<uint2> tile_lists_;       // K3 -> K4 per-CTA (tile, count) entries (<= kHistMaxTiles)
+    DevBuf<uint32_t> tile_list_len_;
     DevBuf<Gauss64> g64_;
     DevBuf<Gauss32> g32_;
     DevBuf<GaussEmit> emit_;
