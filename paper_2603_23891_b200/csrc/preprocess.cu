@@ -212,9 +212,24 @@ __global__ void __launch_bounds__(kPrepBlock, PREP_MIN_CTAS) k_preprocess(
     // and storage, for ~200 FP64 instructions the kernel had issue room for.
     uint64_t s = lo + threadIdx.x;
     uint32_t idx_next = s < hi ? __ldg(selected + s) : 0u;
+#ifndef PREP_L2PF
+#define PREP_L2PF 1
+#endif
+#if PREP_L2PF
+    // the slot after next's index, and the next slot's record pulled into L2
+    // (no registers held): its load then waits on L2, not HBM
+    uint32_t idx_after = s + kPrepBlock < hi ? __ldg(selected + s + kPrepBlock) : 0u;
+#endif
     for (; s < hi; s += kPrepBlock) {
         const uint32_t idx = idx_next;
+#if PREP_L2PF
+        idx_next = idx_after;
+        if (s + kPrepBlock < hi)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(splat + idx_next));
+        if (s + 2 * kPrepBlock < hi) idx_after = __ldg(selected + s + 2 * kPrepBlock);
+#else
         if (s + kPrepBlock < hi) idx_next = __ldg(selected + s + kPrepBlock);
+#endif
         const float4* src = reinterpret_cast<const float4*>(splat + idx);
         const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3);
         SplatRec rec;
