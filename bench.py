@@ -4,21 +4,34 @@ Workload: synthetic 10,039,185-node LoD tree (131x131 roots, L=3, K=8, gamma 0.5
 scene seed 1, build seed 7 -- tree_builder.cpp generator), 1920x1080, a 300-frame
 fly-through (keyframes descending from altitude 400 through 200 to 140, with
 oblique segments; CameraPath slerp sampling, camera_path.cpp:126-180), tau_R = 3,
-three-sigma extents.  A step = one frame.  value = frames/s with the tree resident in
-HBM (device-timed, CUDA events on the scene stream, max over ranks); e2e = the same
-frames through the reference-shaped synchronous C-ABI call lodgs_gpu_render with the
-image copied back to pinned host memory every frame.
+three-sigma extents.  A step = one frame.
 
-Multi-GPU (torchrun): the tree is replicated, every rank renders its own K frames of
-the path (start offset rank*300/N), no collective on the data path ("weak").
+Timed frames: for any --steps K the N*K frames of the job are spread evenly over the
+whole 300-frame path (frame floor(j*300/(N*K))) and dealt round-robin to the ranks
+(paper_2603_23891_b200/sharding.py: strided_frames), so the timed workload is the
+fly-through, not its first frames, and every rank gets the same altitude mix.
+
+value  = frames/s with the tree resident in HBM (device-timed, CUDA events on the
+         scene's control stream, max over ranks).
+e2e    = the same frames through the public C ABI with host buffers: camera in, f32
+         RGB image (lodgs::render's Image) out to pinned host memory every frame, via
+         the pipelined lodgs_gpu_render_batch; e2e_sync does one synchronous
+         lodgs_gpu_render per frame (the drop-in lodgs::render shim's call);
+         e2e_rgb8 returns the 8-bit image the reference CLI writes.
+
+Multi-GPU (torchrun): the tree is replicated, frames are sharded round-robin, no
+collective on the data path ("weak": K frames per rank).
+
 --impl reference: the reference renderer itself (oracle/_ref, compiled from
-/root/reference) on the host cores, bounded sample of the same path.
+/root/reference's sources) on all host cores, on the SAME frames: tree built by the
+reference's own generator (build_tree), cameras by its own CameraPath::sample, FPS =
+frames / sum of RenderStats::total_ms (bench.cpp:160).  It never loads the product
+library.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -30,10 +43,22 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2603_23891_b200.sharding import reduce_timing, strided_frames  # noqa: E402
+
 METRIC = "FPS @1080p on 10M-node LoD tree; filter+sort HBM GB/s vs peak; tile pairs"
 TREE = dict(nx=131, ny=131, seed=1, depth=3, build_seed=7)
 W, H, FOCAL, TAU_R = 1920, 1080, 1000.0, 3.0
 PATH_SAMPLES = (100, 100, 99)  # 300 frames = sum + 1
+N_PATH = sum(PATH_SAMPLES) + 1
+WORKLOAD = ("cfg3: 10,039,185-node LoD tree, 1920x1080, 300-frame fly-through "
+            "(timed frames strided over the whole path), tau_R=3, three-sigma")
+DTYPE = "f64+f32"
+DTYPE_NOTE = ("filter decisions, projection, shrink radii, binning and sort keys in FP64/integer "
+              "(bit-exact with the reference); blend in FP32 with a certified FP64 re-check of "
+              "uncertain alpha>=1/255 decisions (image within max-abs 1e-3, north_star)")
+# ncu capture of the bench's own frames (tools/ncu_frames.py): per-kernel mean time and
+# DRAM bytes per launch
+NCU_FRAMES = os.path.join(ROOT, "profiles", "r2_ncu_bench_frames.json")
 
 
 def _normalize(v):
@@ -51,8 +76,8 @@ def look_at(eye, target, up=(0.0, 1.0, 0.0)):
     return tuple(R.reshape(-1)), tuple(t)
 
 
-def flythrough(L):
-    """cfg 3 camera path: 4 keyframes, 300 frames."""
+def keyframes(L):
+    """cfg 3 keyframes: top-down at 400, oblique at 260, top-down at 200, oblique at 140."""
     keys = []
     for eye, target in (((0.0, 0.0, 400.0), (0.0, 0.0001, 0.0)),
                         ((30.0, -60.0, 260.0), (10.0, 10.0, 0.0)),
@@ -60,7 +85,19 @@ def flythrough(L):
                         ((40.0, -30.0, 140.0), (50.0, 40.0, 0.0))):
         R, t = look_at(eye, target)
         keys.append(L.Camera(W, H, FOCAL, FOCAL, W / 2.0, H / 2.0, R, t, 0.01, 1000.0))
-    return L.sample_camera_path(keys, PATH_SAMPLES)
+    return keys
+
+
+def flythrough(L):
+    """cfg 3 camera path: 4 keyframes, 300 frames (the product's CameraPath::sample)."""
+    return L.sample_camera_path(keyframes(L), PATH_SAMPLES)
+
+
+def config(world, k):
+    return {"workload": WORKLOAD, "nodes": 10039185, "width": W, "height": H,
+            "frames_per_rank": k, "frame_schedule": "strided_frames(300, rank, N, K)",
+            "l2": "inputs larger than L2 (tree 1.1 GB in HBM, the filter streams ~0.3 GB "
+                  "per frame)", "parallelism": f"view-sharded x{world}"}
 
 
 def dist_env():
@@ -91,7 +128,7 @@ class ClockSampler:
                 self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -113,98 +150,47 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def filter_traffic_bytes():
-    """DRAM bytes (read + write) of the four filter kernels for one altitude-200
-    frame, from the committed ncu --set full summary (tools/ncu_summary.py)."""
-    path = os.path.join(ROOT, "profiles", "r1_ncu_filter_alt200.txt")
-    try:
-        tot, seen = 0.0, set()
-        for line in open(path):
-            f = line.split()
-            if f and f[0] in ("k_mark_internal", "k_select_internal", "k_filter_leaves",
-                              "k_compact") and f[0] not in seen:
-                seen.add(f[0])
-                tot += (float(f[2]) + float(f[3])) * 1e6
-        return (tot if len(seen) == 4 else None), os.path.relpath(path, ROOT)
-    except OSError:
-        return None, None
-
-
-def ncu_kernel_row(kernel, fname="r1_ncu_render_alt200.txt"):
-    """One kernel's row of a committed ncu --set full summary (tools/ncu_summary.py)."""
-    path = os.path.join(ROOT, "profiles", fname)
-    try:
-        lines = open(path).read().splitlines()
-        hdr = next(ln.split() for ln in lines if ln.startswith("kernel"))
-        for ln in lines:
-            f = ln.split()
-            if f and f[0] == kernel:
-                return {h: float(v) for h, v in zip(hdr[1:], f[1:])}, os.path.relpath(path, ROOT)
-    except (OSError, StopIteration, ValueError):
-        pass
-    return None, None
-
-
-def blend_evidence():
-    """The dominant kernel is issue-bound (no dense contraction, no HBM roofline):
-    its SM issue utilisation from the committed ncu capture (altitude 200)."""
-    for kern in ("k_blend_wsp", "k_blend_ws"):  # persistent kernel (default build) first
-        row, src = ncu_kernel_row(kern)
-        if row:
-            break
-    if not row:
-        return None
-    return {"kernel": kern, "bound": "issue", "issue_slots_busy_pct": row.get("issue%"),
-            "sm_throughput_pct": row.get("sm%"), "achieved_occupancy_pct": row.get("occ%"),
-            "ncu_us_alt200": row.get("us"), "source": src}
-
-
 def measured_peak_gbs():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def cpu_reference_sample(L, tree, cams, threads, budget_s=20.0, max_frames=6, extras=False):
-    """The reference renderer (oracle/_ref) on host cores over a bounded, evenly
-    strided sample of the path. FPS = frames / sum(T_total) as bench.cpp:160."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_bind import Ref
+def ncu_frames():
+    """Per-kernel mean device time (us) and DRAM MB read/written per launch over the
+    bench's own timed frames (profiles/r2_ncu_bench_frames.json, tools/ncu_frames.py).
+    ncu replays every launch with cold caches and serialised, so only the kernels'
+    DRAM bytes and their shares of the frame are used from it, not absolute times."""
+    try:
+        with open(NCU_FRAMES) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
 
-    ref = Ref()
-    h = ref.tree_from(tree)
-    stride = max(1, len(cams) // max_frames)
-    sample = cams[::stride][:max_frames]
-    total_ms, wall, frames = 0.0, 0.0, 0
-    t_start = time.perf_counter()
-    for cam in sample:
-        t0 = time.perf_counter()
-        r = ref.render(h, cam, TAU_R, L.ShrinkMode.three_sigma(), workers=threads)
-        wall += time.perf_counter() - t0
-        total_ms += r["total_ms"]
-        frames += 1
-        if time.perf_counter() - t_start > budget_s:
-            break
-    # SURVEY 8(d)'s companion figures on two of the same frames: one thread, and
-    # collect_kpc=true (the reference bench always renders that way, bench.cpp:128)
-    extra = {}
-    if extras:
-        few = sample[:: max(1, len(sample) // 2)][:2]
-        for name, kw in (("same_frames_all_threads", dict(workers=threads)),
-                         ("single_thread", dict(workers=1)),
-                         ("collect_kpc", dict(workers=threads, collect_kpc=True))):
-            ms = sum(ref.render(h, cam, TAU_R, L.ShrinkMode.three_sigma(), **kw)["total_ms"]
-                     for cam in few)
-            extra[name] = {"value": len(few) / (ms / 1000.0), "unit": "frames/s",
-                           "cores": kw["workers"], "frames": len(few)}
-    ref.free_tree(h)
-    return {"value": frames / (total_ms / 1000.0), "unit": "frames/s", "cores": threads,
-            "kind": "reference", "cpu_model": cpu_model(),
-            "sample": f"{frames} frames of the 300-frame cfg-3 path (stride {stride}), "
-                      f"lodgs::render T_total (bench.cpp:160); wall incl. per-frame "
-                      f"validation {frames / wall:.3f} frames/s", **extra}
+
+STAGE_KERNELS = {
+    "filter": ("k_mark_internal", "k_select_internal", "k_filter_leaves", "k_compact"),
+    "preprocess": ("k_preprocess",),
+    "keys": ("k_tile_offsets_cluster", "k_tile_offsets", "k_emit_keys"),
+    "sort": ("k_tile_sort", "k_tile_sort_big"),
+    "blend": ("k_blend_wsp", "k_blend_tma", "k_blend_ws"),
+}
+
+
+def stage_traffic(prof, stage):
+    """DRAM bytes (read + write) per frame of a stage's kernels, from the ncu capture of
+    the bench frames; None without a capture."""
+    if not prof:
+        return None
+    ks = prof.get("kernels", {})
+    tot, seen = 0.0, False
+    for k in STAGE_KERNELS[stage]:
+        if k in ks:
+            seen = True
+            tot += (ks[k]["dram_rd_mb"] + ks[k]["dram_wr_mb"]) * 1e6 * ks[k]["launches_per_frame"]
+    return tot if seen else None
 
 
 def cpu_model():
@@ -217,27 +203,78 @@ def cpu_model():
     return None
 
 
+def _ref():
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import Ref
+
+    return Ref()
+
+
+def cpu_reference_sample(L, ref, h, cams, threads, frames, extras=False):
+    """The reference renderer (oracle/_ref) on host cores over `frames` (indices into
+    the path).  FPS = frames / sum(T_total) as bench.cpp:160."""
+    total_ms, wall, pairs = 0.0, 0.0, 0
+    for i in frames:
+        t0 = time.perf_counter()
+        r = ref.render(h, cams[i], TAU_R, L.ShrinkMode.three_sigma(), workers=threads)
+        wall += time.perf_counter() - t0
+        total_ms += r["total_ms"]
+        pairs += r["n_pairs"]
+    n = len(frames)
+    out = {"value": n / (total_ms / 1000.0), "unit": "frames/s", "cores": threads,
+           "kind": "reference", "cpu_model": cpu_model(), "frames": n,
+           "mean_pairs": pairs / max(1, n), "wall_value": n / wall,
+           "sample": f"{n} frames of the 300-frame cfg-3 path (indices {frames[0]}..{frames[-1]}, "
+                     f"stride {frames[1] - frames[0] if n > 1 else 0}), lodgs::render "
+                     f"T_total (bench.cpp:160); wall incl. the per-frame require_valid "
+                     f"{n / wall:.3f} frames/s"}
+    if extras:
+        # SURVEY 8(d)'s companion figures on two of the same frames: one thread, and
+        # collect_kpc=true (the reference bench always renders that way, bench.cpp:128)
+        few = [frames[len(frames) // 3], frames[(2 * len(frames)) // 3]]
+        for name, kw in (("same_frames_all_threads", dict(workers=threads)),
+                         ("single_thread", dict(workers=1)),
+                         ("collect_kpc", dict(workers=threads, collect_kpc=True))):
+            ms = sum(ref.render(h, cams[i], TAU_R, L.ShrinkMode.three_sigma(), **kw)["total_ms"]
+                     for i in few)
+            out[name] = {"value": len(few) / (ms / 1000.0), "unit": "frames/s",
+                         "cores": kw["workers"], "frames": few}
+    return out
+
+
 def run_reference(args, rank, world):
-    from paper_2603_23891_b200 import lodgs as L
+    """The reference arm: the unmodified reference renderer on the box's host cores,
+    on this arm's config (same tree, same 300-frame path, the same strided frames).
+    Rank 0 only (a CPU arm has nothing to shard over GPUs)."""
+    from paper_2603_23891_b200 import lodgs as L  # data classes only: no library load
 
     if rank != 0:
         return
-    tree = L.build_synthetic_tree(**TREE)
-    cams = flythrough(L)
+    t0 = time.perf_counter()
+    ref = _ref()
+    h = ref.lib.ref_build_synthetic(TREE["nx"], TREE["ny"], 2.0, 0.2, 0.6, 0.3, 0.9,
+                                    TREE["seed"], 1, TREE["depth"], 0.5, 8, TREE["build_seed"])
+    if not h:
+        raise RuntimeError(ref.err())
+    n_nodes = int(ref.lib.ref_tree_size(h))
+    cams = ref.sample_path(keyframes(L), PATH_SAMPLES)
+    setup_s = time.perf_counter() - t0
     threads = os.cpu_count() or 1
-    per = []
-    for _ in range(args.warmup):
-        pass  # the reference has no device warm-up; keep W for the contract
-    sample = cpu_reference_sample(L, tree, cams, threads, budget_s=60.0, max_frames=max(3, args.steps_ref))
+    k = args.steps
+    frames = strided_frames(len(cams), 0, 1, k)
+    for i in strided_frames(len(cams), 0, 1, args.warmup):  # untimed warm-up frames
+        ref.render(h, cams[i], TAU_R, L.ShrinkMode.three_sigma(), workers=threads)
+    sample = cpu_reference_sample(L, ref, h, cams, threads, frames)
+    ref.free_tree(h)
     val = sample["value"]
+    cfg = config(1, k)
+    cfg["nodes"] = n_nodes
     line = {"metric": METRIC, "value": val, "unit": "frames/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / val,
+            "steps": k, "warmup": args.warmup, "ms_per_step": 1000.0 / val,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference generator, seeds 1/7)",
-            "config": {"workload": "cfg3: 10,039,185-node LoD tree, 1920x1080, 300-frame fly-through, "
-                                   "tau_R=3, three-sigma", "nodes": tree.node_count(),
-                       "width": W, "height": H},
-            "impl": "reference", "cpu_baseline": sample,
+            "data": "synthetic (reference generator build_tree, seeds 1/7)",
+            "config": cfg, "impl": "reference", "mean_pairs": sample["mean_pairs"],
+            "cpu_baseline": sample, "setup_s": setup_s,
             "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -262,16 +299,19 @@ def run_b200(args, rank, world, local):
     n_path = len(cams)
     scene = L.GpuScene(tree, local)
     build_s = time.perf_counter() - t_build
+    lib = L.load_library()
     stream = torch.cuda.ExternalStream(scene.stream_ptr(), device=torch.device("cuda", local))
     params = L.RenderParamsC(TAU_R, 0.0, 0, 0)
-    from paper_2603_23891_b200.sharding import reduce_timing, rotated_frames
-
-    order = [cams[i] for i in rotated_frames(n_path, rank, world, args.warmup + args.steps)]
+    K = args.steps
+    timed_idx = strided_frames(n_path, rank, world, K)
+    warm_idx = strided_frames(n_path, rank, world, args.warmup)
+    timed = [cams[i] for i in timed_idx]
+    warm = [cams[i] for i in warm_idx]
+    mode = L.ShrinkMode.three_sigma()
 
     # size the pair buffer on the whole path once (untimed)
-    for cam in cams[:: max(1, n_path // 30)]:
-        launches_per_frame = scene.render(cam, L.FilterConfig(TAU_R),
-                                          L.ShrinkMode.three_sigma()).stats.kernel_launches
+    for cam in cams[::10]:
+        launches_per_frame = scene.render(cam, L.FilterConfig(TAU_R), mode).stats.kernel_launches
 
     def device_loop(frames, profile=False):
         scene.take_totals()
@@ -282,10 +322,11 @@ def run_b200(args, rank, world, local):
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
+        torch.cuda.synchronize()
         ev0.record(stream)
         for cam in frames:
             scene.render_async(cam, params)
-        scene.join()  # frames alternate over two in-flight contexts
+        scene.join()  # frames rotate over the in-flight contexts; the control stream waits
         ev1.record(stream)
         ev1.synchronize()
         ms = ev0.elapsed_time(ev1)
@@ -295,10 +336,9 @@ def run_b200(args, rank, world, local):
             scene.profile(False)
         return ms, tot, prof
 
-    for cam in order[: args.warmup]:
+    for cam in warm:
         scene.render_async(cam, params)
     scene.sync()
-    timed = order[args.warmup:]
     with ClockSampler(local) as clocks:
         for attempt in range(3):
             try:
@@ -306,133 +346,170 @@ def run_b200(args, rank, world, local):
                 break
             except L.InternalError:
                 continue  # pair buffer grew; re-run the timed region
-    # per-stage device times over a second pass of the same frames (events between kernels)
+    # per-stage device times over a second pass of the same frames (events between
+    # kernels, one frame in flight: the stage split, not the throughput)
     _, _, (pf, stage_ms) = device_loop(timed, profile=True)
 
-    # e2e through the public C ABI with host buffers: every frame's camera goes in and its
-    # full f32 RGB image comes back to pinned host memory.  Default: the pipelined
-    # lodgs_gpu_render_batch (frame i+1 computes while frame i copies out; a ring of
-    # 4 host images); --e2e-sync: one synchronous lodgs_gpu_render call per frame.
+    # ---- e2e through the public C ABI with host buffers (pinned ring of 4 images)
     img_bytes = W * H * 3 * 4
     ring = []
     for _ in range(4):
         p = C.c_void_p()
-        L._check(L.load_library().lodgs_gpu_host_alloc(img_bytes, C.byref(p)))
+        L._check(lib.lodgs_gpu_host_alloc(img_bytes, C.byref(p)))
         ring.append(p.value)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    e2e_frames = timed if args.e2e_steps <= 0 else timed[: max(1, min(len(timed), args.e2e_steps))]
-    # untimed warm-up of both e2e legs (W frames each: first-call host allocations and
-    # module loading stay out of the timed region, as for the device loop)
-    warm = order[: max(1, args.warmup)]
+    ptrs = [ring[i % 4] for i in range(len(timed))]
+    # untimed warm-up of every leg (first-call host allocations stay out of the timing)
     for rgb8 in (False, True):
-        scene.render_batch(warm, L.FilterConfig(TAU_R), L.ShrinkMode.three_sigma(),
-                           L.RenderOptions(output_rgb8=rgb8),
-                           host_ptrs=[ring[i % 4] for i in range(len(warm))])
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    if args.e2e_sync:
-        st = L.RenderStatsC()
-        for i, cam in enumerate(e2e_frames):
+        scene.render_batch(warm, L.FilterConfig(TAU_R), mode, L.RenderOptions(output_rgb8=rgb8),
+                           host_ptrs=ptrs[: len(warm)])
+    st = L.RenderStatsC()
+    for i, cam in enumerate(warm):
+        c = cam.to_c()
+        L._check(lib.lodgs_gpu_render(scene.handle, C.byref(c), C.byref(params), ring[i % 4],
+                                      C.byref(st)))
+
+    def timed_host(fn):
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0
+
+    e2e_s = timed_host(lambda: scene.render_batch(timed, L.FilterConfig(TAU_R), mode,
+                                                  host_ptrs=ptrs))
+
+    def sync_leg():
+        for i, cam in enumerate(timed):
             c = cam.to_c()
-            L._check(L.load_library().lodgs_gpu_render(scene.handle, C.byref(c), C.byref(params),
-                                                       ring[i % 4], C.byref(st)))
-    else:
-        scene.render_batch(e2e_frames, L.FilterConfig(TAU_R), L.ShrinkMode.three_sigma(),
-                           host_ptrs=[ring[i % 4] for i in range(len(e2e_frames))])
-    e2e_s = time.perf_counter() - t0
-    # the same frames with 8-bit images out (the reference CLI's render -> save_ppm
-    # bytes; LODGS_RENDER_OUTPUT_RGB8): 6.2 MB per 1080p frame instead of 24.9 MB
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    t0 = time.perf_counter()
-    scene.render_batch(e2e_frames, L.FilterConfig(TAU_R), L.ShrinkMode.three_sigma(),
-                       L.RenderOptions(output_rgb8=True),
-                       host_ptrs=[ring[i % 4] for i in range(len(e2e_frames))])
-    e2e8_s = time.perf_counter() - t0
+            L._check(lib.lodgs_gpu_render(scene.handle, C.byref(c), C.byref(params),
+                                          ring[i % 4], C.byref(st)))
+
+    e2e_sync_s = timed_host(sync_leg)
+    e2e8_s = timed_host(lambda: scene.render_batch(
+        timed, L.FilterConfig(TAU_R), mode, L.RenderOptions(output_rgb8=True), host_ptrs=ptrs))
     for p in ring:
-        L.load_library().lodgs_gpu_host_free(p)
+        lib.lodgs_gpu_host_free(p)
 
     # max over ranks of the timed regions; per-rank counters summed
     ms_max, _ = reduce_timing(dist, ms, [], device="cuda")
-    e2e8_max, _ = reduce_timing(dist, e2e8_s, [], device="cuda")
-    e2e_max, (sum_sel_all, sum_pairs_all, nf_all) = reduce_timing(
-        dist, e2e_s, [sum_sel, sum_pairs, nf], device="cuda")
-    sum_sel, sum_pairs, nf = sum_sel_all, sum_pairs_all, int(nf_all)
+    e2e_max, _ = reduce_timing(dist, e2e_s, [], device="cuda")
+    e2e_sync_max, _ = reduce_timing(dist, e2e_sync_s, [], device="cuda")
+    e2e8_max, (sum_sel, sum_pairs, nf, sum_sort_bytes) = reduce_timing(
+        dist, e2e8_s, [sum_sel, sum_pairs, nf, sum_sort_bytes], device="cuda")
+    nf = int(nf)
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-    K = len(timed)
     fps = world * K / (ms_max / 1000.0)
-    e2e_fps = world * len(e2e_frames) / e2e_max
     peak, peak_kind = measured_peak_gbs()
     n = tree.node_count()
     n_int = int(tree.level_offsets[-1])  # internal nodes precede the leaf level
     mean_sel = sum_sel / max(1, nf)
     mean_pairs = sum_pairs / max(1, nf)
-    # B_f = 29 N + 16 N_int + 4 N_sel per frame (mark + select)
+    stage_names = ["filter_internal", "filter_leaves_compact", "preprocess_keys", "tile_sort",
+                   "blend"]
+    per_stage = {k: stage_ms[i] / max(1, pf) for i, k in enumerate(stage_names)}
+    dominant = max(per_stage, key=per_stage.get)
+    prof = ncu_frames()
+
+    # SURVEY.md 8(d) algorithmic bytes per frame (reference layout) per stage
     filt_bytes = 29 * n + 16 * n_int + 4 * mean_sel
-    filt_ms = (stage_ms[0] + stage_ms[1]) / max(1, pf)
-    mark_ms = stage_ms[0] / max(1, pf)
-    sort_ms = stage_ms[3] / max(1, pf)
-    # the reference LSD radix's bytes, (24 x non-uniform 8-bit digits
-    # + 8) per pair, counted per frame on the device from the frame's keys
-    sort_bytes = sum_sort_bytes / max(1, nf)
-    stage_names = ["filter_internal", "filter_leaves_compact", "preprocess_keys", "tile_sort", "blend"]
-    per_stage = {k: round(stage_ms[i] / max(1, pf), 5) for i, k in enumerate(stage_names)}
-    dominant = max(range(5), key=lambda i: stage_ms[i])
-    filt_gbs = filt_bytes / (filt_ms * 1e-3) / 1e9
-    traffic, traffic_src = filter_traffic_bytes()
+    filt_ms = per_stage["filter_internal"] + per_stage["filter_leaves_compact"]
+    sort_ms = per_stage["tile_sort"]
+    sort_bytes = sum_sort_bytes / max(1, nf)  # (24 x non-uniform digits + 8) B per pair
+
+    def stage_obj(name, alg_bytes, ms, bound, note=None):
+        traffic = stage_traffic(prof, name)
+        o = {"bound": bound, "ms_per_frame": ms, "algorithmic_bytes": alg_bytes,
+             "achieved_gbs": alg_bytes / (ms * 1e-3) / 1e9 if ms > 0 else None,
+             "frac": alg_bytes / (ms * 1e-3) / 1e9 / peak if ms > 0 else None,
+             "traffic": traffic,
+             "physical_gbs": traffic / (ms * 1e-3) / 1e9 if traffic and ms > 0 else None,
+             "physical_frac": traffic / (ms * 1e-3) / 1e9 / peak if traffic and ms > 0 else None}
+        if note:
+            o["note"] = note
+        return o
+
+    # preprocess and key emission share one event-timed stage; split it by the kernels'
+    # shares in the ncu launch list of the same frames
+    pk_ms = per_stage["preprocess_keys"]
+    share_pre = 0.7
+    if prof:
+        ks = prof.get("kernels", {})
+        t_pre = sum(ks[k]["mean_us"] * ks[k]["launches_per_frame"]
+                    for k in STAGE_KERNELS["preprocess"] if k in ks)
+        t_keys = sum(ks[k]["mean_us"] * ks[k]["launches_per_frame"]
+                     for k in STAGE_KERNELS["keys"] if k in ks)
+        if t_pre + t_keys > 0:
+            share_pre = t_pre / (t_pre + t_keys)
+    # mean projected gaussians ~ selected (near-plane drops are rare on this path)
+    stages = {
+        "filter": stage_obj("filter", filt_bytes, filt_ms, "hbm",
+                            "B_f = 29 N + 16 N_int + 4 N_sel; the device skips leaves under "
+                            "blocked parents, so traffic < B_f"),
+        "preprocess": stage_obj("preprocess", 60 * mean_sel + 52 * mean_sel, pk_ms * share_pre,
+                                "hbm+fp64", "60 N_sel read + 52 N_g written (8(d)); split from "
+                                "preprocess_keys by the ncu time shares"),
+        "keys": stage_obj("keys", 16 * mean_sel + 12 * mean_pairs, pk_ms * (1 - share_pre),
+                          "l2 atomics", "16 N_g + 12 N_P (8(d))"),
+        "sort": stage_obj("sort", sort_bytes, sort_ms, "issue",
+                          "reference LSD-radix bytes (24 B x non-uniform 8-bit digits + 8 B per "
+                          "pair); the device sorts per tile in registers and moves 16 B/pair: "
+                          "issue-bound, not HBM-bound"),
+    }
+    filt = stages["filter"]
+    roofline = {"kernel": "filter (k_mark_internal + k_select_internal + k_filter_leaves + "
+                          "k_compact)", "bound": "hbm", "achieved": filt["achieved_gbs"],
+                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": filt["frac"],
+                "traffic": filt["traffic"], "physical_frac": filt["physical_frac"],
+                "traffic_source": (f"ncu dram__bytes_read+write over the bench's own frames "
+                                   f"({os.path.relpath(NCU_FRAMES, ROOT)})" if prof else None),
+                "algorithmic_bytes_per_frame": filt_bytes, "dominant_stage": dominant}
+    blend = {"kernel": "k_blend_wsp", "bound": "issue", "ms_per_frame": per_stage["blend"],
+             "share_of_frame": per_stage["blend"] / max(1e-9, sum(per_stage.values()))}
+    if prof and "k_blend_wsp" in prof.get("kernels", {}):
+        kb = prof["kernels"]["k_blend_wsp"]
+        blend.update({k: kb[k] for k in ("issue_pct", "sm_pct", "occ_pct") if k in kb})
+    e2e_h2d = C.sizeof(L.CameraC) + C.sizeof(L.RenderParamsC)
     line = {
         "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generator, seeds 1/7; tree resident in HBM)",
-        "config": {"workload": "cfg3: 10,039,185-node LoD tree, 1920x1080, 300-frame fly-through, "
-                               "tau_R=3, three-sigma", "nodes": n, "width": W, "height": H,
-                   "frames_per_rank": K, "l2": "inputs larger than L2 (tree 1.1 GB in HBM, "
-                   "filter streams 0.3 GB per frame)", "parallelism": f"view-sharded x{world}"},
+        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "dtype_note": DTYPE_NOTE,
+        "data": "synthetic (reference generator restated bit-for-bit, seeds 1/7; tree "
+                "resident in HBM)",
+        "config": config(world, K),
+        "frames": timed_idx if world == 1 else f"{K} per rank, round-robin over the path",
         "mean_selected": mean_sel, "mean_pairs": mean_pairs,
         "stage_ms_per_frame": per_stage,
-        "roofline": {"kernel": "filter (k_mark_internal + k_select_internal + "
-                                "k_filter_leaves + k_compact)", "bound": "hbm",
-                     "achieved": filt_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": filt_gbs / peak, "traffic": traffic,
-                     "traffic_source": f"ncu --set full dram__bytes_read+write, one altitude-200 "
-                                       f"frame ({traffic_src}); the leaf pass never fetches leaves "
-                                       f"under blocked parents, so traffic < algorithmic bytes",
-                     "algorithmic_bytes_per_frame": filt_bytes,
-                     "dominant_stage": stage_names[dominant]},
-        "sort": {"kernel": "k_tile_sort + k_tile_sort_big (per-tile register bitonic on "
-                           "(depth, slot) after the counting tile digit)", "bound": "hbm",
-                 "achieved_gbs": sort_bytes / (sort_ms * 1e-3) / 1e9 if sort_ms > 0 else None,
-                 "frac": (sort_bytes / (sort_ms * 1e-3) / 1e9) / peak if sort_ms > 0 else None,
-                 "peak_gbs": peak, "algorithmic_bytes_per_frame": sort_bytes,
-                 "bytes_definition": "SURVEY 8(d): (24 B x non-uniform 8-bit digits of the "
-                                     "reference key tile<<32|depth + 8 B) per pair",
-                 "device_traffic_per_frame": 16 * mean_pairs},
-        "blend": blend_evidence(),
-        "e2e": {"value": e2e_fps, "unit": "frames/s",
-                "h2d_bytes_per_step": C.sizeof(L.CameraC) + C.sizeof(L.RenderParamsC),
-                "d2h_bytes_per_step": img_bytes + 64, "frames": len(e2e_frames),
-                "call": "lodgs_gpu_render" if args.e2e_sync else "lodgs_gpu_render_batch",
+        "roofline": roofline, "stages": stages, "blend": blend,
+        "e2e": {"value": world * K / e2e_max, "unit": "frames/s",
+                "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": img_bytes + 64,
+                "frames": K, "call": "lodgs_gpu_render_batch (pipelined over frames in flight)",
                 "pcie_note": "f32 RGB image per frame (lodgs::render's Image): D2H-bound "
                              "(~56 GB/s measured, tools/micro/d2h_bw.py)"},
-        "e2e_rgb8": {"value": world * len(e2e_frames) / e2e8_max, "unit": "frames/s",
-                     "h2d_bytes_per_step": C.sizeof(L.CameraC) + C.sizeof(L.RenderParamsC),
-                     "d2h_bytes_per_step": W * H * 3 + 64,
+        "e2e_sync": {"value": world * K / e2e_sync_max, "unit": "frames/s",
+                     "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": img_bytes + 64,
+                     "call": "lodgs_gpu_render, one synchronous call per frame (the drop-in "
+                             "lodgs::render shim's call)"},
+        "e2e_rgb8": {"value": world * K / e2e8_max, "unit": "frames/s",
+                     "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": W * H * 3 + 64,
                      "call": "lodgs_gpu_render_batch + LODGS_RENDER_OUTPUT_RGB8 (save_ppm bytes)"},
         "gpu_launches": int(launches_per_frame) * K,
         "clocks": clocks.summary(),
         "setup_s": build_s,
     }
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_reference_sample(L, tree, cams, os.cpu_count() or 1,
-                                                    budget_s=args.cpu_budget, extras=True)
+        ref = _ref()
+        h = ref.tree_from(tree)
+        line["cpu_baseline"] = cpu_reference_sample(
+            L, ref, h, cams, os.cpu_count() or 1, strided_frames(n_path, 0, 1, args.cpu_frames),
+            extras=True)
+        ref.free_tree(h)
     print(json.dumps(line), flush=True)
+    scene.close()
     if dist:
         dist.destroy_process_group()
 
@@ -443,13 +520,12 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=0, help="frames for e2e (0 = all timed frames)")
-    ap.add_argument("--steps-ref", type=int, default=6)
-    ap.add_argument("--cpu-budget", type=float, default=25.0)
+    ap.add_argument("--cpu-frames", type=int, default=30,
+                    help="frames of the reference CPU sample (stride 300/n over the path)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-sync", action="store_true",
-                    help="e2e through one synchronous lodgs_gpu_render per frame")
     args = ap.parse_args()
+    if args.warmup < 1 or args.steps < 1:
+        ap.error("--steps and --warmup must be >= 1")
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -11,6 +11,8 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
 #include <utility>
 
 #ifndef USE_PDL
@@ -48,6 +50,20 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 #else
     kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
 #endif
+}
+
+// Raises a kernel's dynamic shared-memory cap (default 48 KB) to `bytes`,
+// once per (kernel, device).  Only the cap changes: occupancy follows the
+// dynamic size of each launch.
+template <typename... KArgs>
+inline void opt_in_smem(void (*kernel)(KArgs...), int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.insert({reinterpret_cast<const void*>(kernel), dev}).second)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 }  // namespace fgs

@@ -331,6 +331,9 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
     const int n_tiles = tiles_x * tiles_y;
     const int use_hist = n_tiles <= kHistMaxTiles ? 1 : 0;
     const size_t smem = use_hist ? size_t(n_tiles) * 4 : 0;
+    // the tile histogram plus the kernel's static shared memory can pass the
+    // default 48 KB per-block limit near kHistMaxTiles (a 2048x1536 frame)
+    opt_in_smem(k_preprocess, kHistMaxTiles * 4 + 1024);
     launch_pdl(k_preprocess, grid, kPrepBlock, smem, s, g, t.splat,
                selected, shrink_kind, tau, tiles_x, tiles_y,
                out, cnt, use_hist, known_visible ? 1 : 0);
@@ -739,6 +742,7 @@ void launch_emit_keys(const GaussEmit* emit, const FrameCounters* cnt, int tiles
                       const uint2* tile_lists, const uint32_t* tile_list_len) {
     const int use_hist = n_tiles <= kHistMaxTiles ? 1 : 0;
     const size_t smem = use_hist ? size_t(n_tiles) * 4 : 0;
+    opt_in_smem(k_emit_keys, kHistMaxTiles * 4 + 1024);
     launch_pdl(k_emit_keys, grid, 256, smem, s, emit, cnt, tiles_x, n_tiles, cursor, keys,
                use_hist, use_hist ? tile_lists : nullptr, use_hist ? tile_list_len : nullptr);
 }

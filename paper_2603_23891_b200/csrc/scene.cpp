@@ -478,6 +478,7 @@ void GpuScene::ensure_resolution(int w, int h) {
         tile_list_len_.alloc(uint64_t(persistent_grid_));
     }
     for (auto& b8 : rgb8b_) b8.alloc(uint64_t(w) * h * 3);
+    rgb8_.alloc(uint64_t(w) * h * 3);
     const uint64_t b_cnt = align256(sizeof(FrameCounters));
     const uint64_t b_sel = align256(uint64_t(filter_status_entries(tree_.n)) * 4);
     const uint64_t b_prep = align256((tree_.n / kPrepBlock + 2) * 8);
@@ -588,9 +589,18 @@ void GpuScene::enqueue_frame(const lodgs_camera& cam, const lodgs_render_params&
     enqueue_pipeline(g, p, int(cam.width), int(cam.height), last_timing_);
     FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
                              cudaMemcpyDeviceToHost, stream_));
-    if (image_host)
-        FGS_CUDA(cudaMemcpyAsync(image_host, res_.image.p, image_floats() * sizeof(float),
-                                 cudaMemcpyDeviceToHost, stream_));
+    if (image_host) {
+        if (p.flags & LODGS_RENDER_OUTPUT_RGB8) {
+            // save_ppm bytes (image.cpp:19-22): the host buffer is W*H*3 bytes
+            rgb8_.alloc(image_floats());
+            launch_rgb8(res_.image.p, image_floats(), rgb8_.p, stream_);
+            FGS_CUDA(cudaMemcpyAsync(image_host, rgb8_.p, image_floats(), cudaMemcpyDeviceToHost,
+                                     stream_));
+        } else {
+            FGS_CUDA(cudaMemcpyAsync(image_host, res_.image.p, image_floats() * sizeof(float),
+                                     cudaMemcpyDeviceToHost, stream_));
+        }
+    }
 }
 
 void GpuScene::finish(lodgs_render_stats* stats) {
@@ -724,6 +734,7 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
     if (bufs[(n - 1) % kBatchBufs] != res_.image.p)
         FGS_CUDA(cudaMemcpy(res_.image.p, bufs[(n - 1) % kBatchBufs], img_bytes, cudaMemcpyDeviceToDevice));
     *h_counters_ = h_batch_counters_[n - 1];
+    last_frame_ = this;  // read_image & co. read this context's res_.image, not a twin's
     for (uint64_t i = 0; i < n; ++i) {
         const FrameCounters& c = h_batch_counters_[i];
         if (c.nonfinite) throw Error(LODGS_ERR_VALIDATION, "projection produced non-finite values");

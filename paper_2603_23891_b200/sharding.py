@@ -20,12 +20,29 @@ def contiguous_shard(n_units: int, rank: int, world: int) -> Tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def rotated_frames(n_path: int, rank: int, world: int, steps: int) -> List[int]:
-    """Weak-scaling schedule used by bench.py: every rank renders `steps` frames
-    of the path starting at its own offset rank * n_path / world, so with
-    steps = n_path every rank renders the whole path once (identical work)."""
-    start = (rank * n_path) // world
-    return [(start + i) % n_path for i in range(steps)]
+def interleaved_shard(n_units: int, rank: int, world: int) -> List[int]:
+    """Units rank, rank + world, rank + 2 world, ... (cfg 5's poses).  A camera
+    path's cost varies 7-25x with altitude, so contiguous
+    spans would hand one rank the cheap high frames and another the expensive
+    low ones; interleaving gives every rank a sample of the whole path."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("rank/world out of range")
+    return list(range(rank, n_units, world))
+
+
+def strided_frames(n_path: int, rank: int, world: int, steps: int) -> List[int]:
+    """Weak-scaling schedule used by bench.py: every rank renders `steps` frames.
+    The world * steps frames of the job are spread evenly over the whole path
+    (frame floor(j * n_path / (world * steps)), j = 0 .. world*steps - 1) and
+    dealt round-robin, rank r taking j = r, r + world, ...  So for any --steps
+    the timed frames cover the whole fly-through (BASELINE cfg 3 is the path, not
+    its first frames) and every rank gets the same mix of altitudes."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("rank/world out of range")
+    if steps <= 0:
+        return []
+    total = world * steps
+    return [((rank + world * i) * n_path) // total for i in range(steps)]
 
 
 def reduce_timing(dist, value_ms: float, sums: List[float], device=None):

@@ -6,7 +6,7 @@
   cfg4: 50,142,872-node tree (103x104 roots, L=4), 3840x2160, fx=2000, a descent from
         altitude 400 to 110; GTC shrink off (three-sigma) vs on (adaptive).
   cfg5: view-batched rendering -- the cfg 3 tree, 1024 poses sampled from the cfg 3
-        fly-through keyframes, sharded contiguously across the ranks of a torchrun
+        fly-through keyframes, dealt round-robin to the ranks of a torchrun
         launch (one process per GPU, tree replicated, no collective on the data path;
         max-over-ranks device time).  Device views/s, plus views/s end to end with the
         8-bit image of every view read back (render_batch with LODGS_RENDER_OUTPUT_RGB8,
@@ -81,8 +81,9 @@ def run_cfg5(n_views=1024):
     keys = [keys_cams[0], keys_cams[100], keys_cams[200], keys_cams[-1]]
     cams = L.sample_camera_path(keys, (n // 3, n // 3, n - 2 * (n // 3)))
     assert len(cams) == n_views
-    lo, hi = rank * n_views // world, (rank + 1) * n_views // world
-    mine = cams[lo:hi]
+    from paper_2603_23891_b200.sharding import interleaved_shard
+
+    mine = [cams[i] for i in interleaved_shard(n_views, rank, world)]
     with L.GpuScene(tree, local) as scene:
         mode = L.ShrinkMode.three_sigma()
         for cam in mine[:: max(1, len(mine) // 16)]:
