@@ -26,6 +26,7 @@
 // Exact kernel (LODGS_RENDER_EXACT_BLEND): the reference arithmetic in FP64
 // with the reference exp_mx (fastexp.hpp:38-50), no FMA: bit-identical pixels.
 #include <algorithm>
+#include <mutex>
 
 #include "launch.h"
 #include "pdl.cuh"
@@ -95,11 +96,8 @@ struct PixState {
     float T, cr, cg, cb;
 };
 
-__device__ __forceinline__ void blend_sample_fast(const WarpStage& st, int k, float pxl,
-                                                  float pyl, PixState& p, bool& unsure) {
-    const float4 geo = st.geo[k];
-    const float4 ct = st.ct[k];
-    const float2 gb = st.gb[k];
+__device__ __forceinline__ void sample_fast(const float4 geo, const float4 ct, const float2 gb,
+                                            float pxl, float pyl, PixState& p, bool& unsure) {
     const float dx = pxl - geo.x, dy = pyl - geo.y;
     const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
     const float ev = __fmaf_rn(ct.x * dx, dy, Q);
@@ -117,15 +115,17 @@ __device__ __forceinline__ void blend_sample_fast(const WarpStage& st, int k, fl
     p.T = t < 1e-4f ? 0.0f : t;
 }
 
+__device__ __forceinline__ void blend_sample_fast(const WarpStage& st, int k, float pxl,
+                                                  float pyl, PixState& p, bool& unsure) {
+    sample_fast(st.geo[k], st.ct[k], st.gb[k], pxl, pyl, p, unsure);
+}
+
 // The same sample with the reference's FP64 decision wherever the FP32 one is
 // uncertain (used only to re-run a batch in which some lane was unsure).
-__device__ __forceinline__ void blend_sample_checked(const WarpStage& st, int k, float pxl,
-                                                     float pyl, double px, double py,
-                                                     const Gauss64* __restrict__ g64,
-                                                     PixState& p) {
-    const float4 geo = st.geo[k];
-    const float4 ct = st.ct[k];
-    const float2 gb = st.gb[k];
+__device__ __forceinline__ void sample_checked(const float4 geo, const float4 ct, const float2 gb,
+                                               uint32_t gid, float pxl, float pyl, double px,
+                                               double py, const Gauss64* __restrict__ g64,
+                                               PixState& p) {
     const float dx = pxl - geo.x, dy = pyl - geo.y;
     const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
     const float ev = __fmaf_rn(ct.x * dx, dy, Q);
@@ -134,7 +134,7 @@ __device__ __forceinline__ void blend_sample_checked(const WarpStage& st, int k,
     bool take = d < -margin;
     float alpha = fminf(ct.z * ex2_approx(-ev), 0.99f);
     if (fabsf(d) <= margin && p.T > 0.0f) {
-        const Gauss64& G = g64[st.gid[k]];
+        const Gauss64& G = g64[gid];
         const double a64 = alpha_exact(G.mx, G.my, G.ca, G.cb, G.cc, G.op, px, py);
         take = a64 >= kMinAlpha;
         alpha = float(a64);
@@ -145,6 +145,13 @@ __device__ __forceinline__ void blend_sample_checked(const WarpStage& st, int k,
     p.cb = __fmaf_rn(gb.y, w, p.cb);
     const float t = p.T - w;
     p.T = t < 1e-4f ? 0.0f : t;
+}
+
+__device__ __forceinline__ void blend_sample_checked(const WarpStage& st, int k, float pxl,
+                                                     float pyl, double px, double py,
+                                                     const Gauss64* __restrict__ g64,
+                                                     PixState& p) {
+    sample_checked(st.geo[k], st.ct[k], st.gb[k], st.gid[k], pxl, pyl, px, py, g64, p);
 }
 
 #ifndef BLEND_PREFETCH2
@@ -866,6 +873,254 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged blend (north_star (4)).  Two kernels:
+//
+// K6a k_pack_blend -- after the sort, every pair p gets a 48-byte blend record
+//     written at p, i.e. each tile's records are contiguous and in blend
+//     order: the splat's tile-relative mean (rounded once from FP64, as the
+//     warp-block means were), its log2e-scaled conic, threshold, opacity,
+//     colour, the 8-bit mask of the tile's 8x4 blocks its alpha box overlaps
+//     (the cull of the old producer warps, done once per pair in a flat,
+//     fully parallel pass) and its slot (for the rare FP64 re-check).
+// K6b k_blend_tma -- persistent, one producer thread + 8 consumer warps per
+//     CTA.  The producer takes tiles from the frame's ticket queue (heavy-first
+//     order) and streams each tile's records into a ring of shared-memory
+//     stages with one cp.async.bulk per 32-record chunk (mbarrier complete_tx);
+//     it holds no registers for the data and runs up to kTmaStages chunks
+//     ahead, across tile boundaries.  Consumer warp w owns the 8x4 block
+//     (w & 1, w >> 1): it takes its hits from the mask bits of the chunk (one
+//     ballot), blends them in pair order in FP32 (the certified skip test of
+//     k_blend_ws; a batch with an uncertain sample is re-run with the FP64
+//     decision), and frees the stage with one mbarrier arrive per warp.  When
+//     all 8 warps of a tile have terminated (T < 1e-4 everywhere) the producer
+//     stops streaming that tile.
+struct __align__(16) BlendRec {
+    float4 geo;  // tile-relative mean x, y, ha, hc
+    float4 ct;   // cb, ethr, op, r
+    float4 gbm;  // g, b, block mask (bits), slot (bits)
+};
+static_assert(sizeof(BlendRec) == 48, "bulk copies move whole 16-byte-aligned records");
+
+__global__ void __launch_bounds__(128) k_pack_blend(const uint32_t* __restrict__ offsets,
+                                                    const unsigned long long* __restrict__ keys,
+                                                    const Gauss64* __restrict__ g64,
+                                                    const Gauss32* __restrict__ g32,
+                                                    const int tiles_x, BlendRec* __restrict__ rec) {
+    pdl_wait();
+    pdl_trigger();
+    const int tile = blockIdx.x;
+    const uint32_t b = offsets[tile], e = offsets[tile + 1];
+    const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
+    for (uint32_t p = b + threadIdx.x; p < e; p += blockDim.x) {
+        const uint32_t gi = uint32_t(keys[p]);
+        const double2 m = *reinterpret_cast<const double2*>(&g64[gi].mx);
+        const float4 q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
+        const float4 col = *reinterpret_cast<const float4*>(&g32[gi].op);
+        const float2 h = *reinterpret_cast<const float2*>(&g32[gi].hx);
+        const float mtx = float(m.x - double(tx0));
+        const float mty = float(m.y - double(ty0));
+        // block (bxi, byi) spans tile-relative pixel centres
+        // [8 bxi + 0.5, 8 bxi + 7.5] x [4 byi + 0.5, 4 byi + 3.5]; warp w = bxi + 2 byi
+        uint32_t mask = 0;
+        if (h.x >= 0.0f) {
+            const uint32_t xm = (mtx - h.x <= 7.5f && mtx + h.x >= 0.5f ? 1u : 0u) |
+                                (mtx - h.x <= 15.5f && mtx + h.x >= 8.5f ? 2u : 0u);
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                if (mty - h.y <= 4.0f * v + 3.5f && mty + h.y >= 4.0f * v + 0.5f)
+                    mask |= xm << (2 * v);
+        }
+        BlendRec r;
+        r.geo = make_float4(mtx, mty, q0.x, q0.z);
+        r.ct = make_float4(q0.y, q0.w, col.x, col.y);
+        r.gbm = make_float4(col.z, col.w, __uint_as_float(mask), __uint_as_float(gi));
+        rec[p] = r;
+    }
+}
+
+#ifndef TMA_STAGES
+#define TMA_STAGES 12
+#endif
+#ifndef TMA_MIN_CTAS
+#define TMA_MIN_CTAS 3
+#endif
+constexpr int kTmaStages = TMA_STAGES;
+constexpr int kTmaConsumers = 8;
+constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
+constexpr int kDoneRing = 32;  // > kTmaStages: a tile has >= 1 stage
+constexpr int kTmaChunk = 32;  // records per stage
+
+struct TmaHdr {
+    int x0, y0;
+    uint32_t n;      // records in the stage (0: none)
+    uint32_t flags;  // 1: last stage of its tile, 2: end of the CTA's work
+};
+struct TmaShared {
+    BlendRec rec[kTmaStages][kTmaChunk];
+    TmaHdr hdr[kTmaStages];
+    unsigned long long full[kTmaStages], empty[kTmaStages];
+    uint32_t done[kDoneRing];  // (tile seq << 4) | consumer warps terminated
+};
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(
+                     smem_addr(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+// one bulk copy global -> this CTA's shared memory, completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
+    const BlendRec* __restrict__ rec, const Gauss64* __restrict__ g64, const int width,
+    const int height, const int tiles_x, const uint32_t n_tiles, unsigned* ticket,
+    float* __restrict__ image) {
+    pdl_wait();  // the record pack (and everything before it) is complete and visible
+    pdl_trigger();
+    extern __shared__ __align__(128) unsigned char tma_raw[];
+    TmaShared& sh = *reinterpret_cast<TmaShared*>(tma_raw);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s) {
+            mbar_init(&sh.full[s], 1);               // the producer's arrive(.expect_tx)
+            mbar_init(&sh.empty[s], kTmaConsumers);  // one arrive per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kTmaConsumers) {
+        // ---------------- producer: one thread ----------------
+        if (lane != 0) return;
+        auto take = [&]() -> int {
+            const uint32_t t = atomicAdd(ticket, 1u);
+            return t < n_tiles ? int(__ldg(order + t)) : -1;
+        };
+        uint32_t i = 0;  // stage sequence
+        uint32_t k = 0;  // tile sequence of this CTA
+        int tile = take();
+        uint32_t b = 0, e = 0;
+        if (tile >= 0) {
+            b = offsets[tile];
+            e = offsets[tile + 1];
+        }
+        while (tile >= 0) {
+            // next tile's ticket and bounds are in flight while this one streams
+            const int next = take();
+            uint32_t nb = 0, ne = 0;
+            if (next >= 0) {
+                nb = offsets[next];
+                ne = offsets[next + 1];
+            }
+            const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
+            volatile uint32_t* done = sh.done;
+            done[k % kDoneRing] = k << 4;  // published by the first stage's arrive
+            for (uint32_t c = b;; c += kTmaChunk) {
+                const int s = int(i % kTmaStages);
+                if (i >= uint32_t(kTmaStages)) mbar_wait(&sh.empty[s], ((i / kTmaStages) - 1) & 1u);
+                const uint32_t n = c < e ? min(uint32_t(kTmaChunk), e - c) : 0u;
+                const bool last = c + kTmaChunk >= e || done[k % kDoneRing] == ((k << 4) | 8u);
+                sh.hdr[s] = TmaHdr{x0, y0, n, last ? 1u : 0u};
+                if (n) {
+                    mbar_expect_tx(&sh.full[s], n * uint32_t(sizeof(BlendRec)));
+                    bulk_g2s(&sh.rec[s][0], rec + c, n * uint32_t(sizeof(BlendRec)), &sh.full[s]);
+                } else {
+                    mbar_arrive(&sh.full[s]);
+                }
+                ++i;
+                if (last) break;
+            }
+            ++k;
+            tile = next;
+            b = nb;
+            e = ne;
+        }
+        const int s = int(i % kTmaStages);
+        if (i >= uint32_t(kTmaStages)) mbar_wait(&sh.empty[s], ((i / kTmaStages) - 1) & 1u);
+        sh.hdr[s] = TmaHdr{0, 0, 0u, 2u};
+        mbar_arrive(&sh.full[s]);
+        return;
+    }
+
+    // ---------------- consumers: warp w owns the 8x4 block (w & 1, w >> 1) ----
+    const int lx = int(warp & 1) * 8 + int(lane & 7), ly = int(warp >> 1) * 4 + int(lane >> 3);
+    const float pxl = float(lx) + 0.5f, pyl = float(ly) + 0.5f;  // tile-relative pixel centre
+    const uint32_t wbit = 1u << warp;
+    PixState pix{0.0f, 0.0f, 0.0f, 0.0f};
+    bool fresh = true, counted = false;
+    int x = 0, y = 0;
+    uint32_t k = 0;
+    for (uint32_t i = 0;; ++i) {
+        const int s = int(i % kTmaStages);
+        mbar_wait(&sh.full[s], (i / kTmaStages) & 1u);
+        const TmaHdr hd = sh.hdr[s];
+        if (hd.flags & 2u) break;
+        if (fresh) {
+            x = hd.x0 + lx;
+            y = hd.y0 + ly;
+            pix = PixState{(x < width && y < height) ? 1.0f : 0.0f, 0.0f, 0.0f, 0.0f};
+            fresh = false;
+            counted = false;
+        }
+        const BlendRec* R = sh.rec[s];
+        const bool mine = lane < hd.n && (__float_as_uint(R[lane].gbm.z) & wbit);
+        const unsigned bits = __ballot_sync(0xffffffffu, mine);
+        if (bits && __any_sync(0xffffffffu, pix.T != 0.0f)) {
+            const PixState saved = pix;
+            bool unsure = false;
+            unsigned bb = bits;
+            while (bb) {
+                const int j0 = __ffs(bb) - 1;
+                bb &= bb - 1;
+                sample_fast(R[j0].geo, R[j0].ct, make_float2(R[j0].gbm.x, R[j0].gbm.y), pxl, pyl,
+                            pix, unsure);
+                if (bb) {
+                    const int j1 = __ffs(bb) - 1;
+                    bb &= bb - 1;
+                    sample_fast(R[j1].geo, R[j1].ct, make_float2(R[j1].gbm.x, R[j1].gbm.y), pxl,
+                                pyl, pix, unsure);
+                }
+            }
+            if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
+                pix = saved;
+                const double px = double(x) + 0.5, py = double(y) + 0.5;
+                bb = bits;
+                while (bb) {
+                    const int j = __ffs(bb) - 1;
+                    bb &= bb - 1;
+                    sample_checked(R[j].geo, R[j].ct, make_float2(R[j].gbm.x, R[j].gbm.y),
+                                   __float_as_uint(R[j].gbm.w), pxl, pyl, px, py, g64, pix);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[s]);
+        if (!counted && __all_sync(0xffffffffu, pix.T == 0.0f)) {
+            counted = true;
+            if (lane == 0) atomicAdd(&sh.done[k % kDoneRing], 1u);
+        }
+        if (hd.flags & 1u) {
+            if (x < width && y < height) {
+                float* o = image + (size_t(y) * width + x) * 3;
+                o[0] = pix.cr;
+                o[1] = pix.cg;
+                o[2] = pix.cb;
+            }
+            fresh = true;
+            ++k;
+        }
+    }
+}
+
 constexpr int kBlendThreads = 256;  // exact kernel: one CTA per 16x16 tile
 constexpr int kWarps = kBlendThreads / 32;
 
@@ -1101,11 +1356,45 @@ void launch_view_gtc(const uint32_t* offsets, int n_tiles, const double* kpc, ui
     if (n_pairs) k_kpc_histogram<<<148, 256, 0, s>>>(kpc, n_pairs, bins);
 }
 
+uint64_t blend_record_bytes() { return sizeof(BlendRec); }
+
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
-                  int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s, unsigned* ticket) {
+                  int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,
+                  unsigned* ticket, void* records) {
     const int n_tiles = tiles_x * tiles_y;
     if (n_tiles <= 0) return;
+#ifndef BLEND_TMA
+#define BLEND_TMA 1
+#endif
+    if (BLEND_TMA && !exact && records && ticket) {
+        BlendRec* rec = static_cast<BlendRec*>(records);
+        launch_pdl(k_pack_blend, n_tiles, 128, 0, s, offsets, keys, g64, g32, tiles_x, rec);
+        const int smem = int(sizeof(TmaShared));
+        static std::mutex mu;
+        static int grid_of[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int grid = 0;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            if (dev < 0 || dev >= 64 || !grid_of[dev]) {
+                cudaFuncSetAttribute(k_blend_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                int per_sm = 0, n_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blend_tma, kTmaThreads, smem);
+                cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+                grid = std::max(1, per_sm) * std::max(1, n_sm);
+                if (dev >= 0 && dev < 64) grid_of[dev] = grid;
+            } else {
+                grid = grid_of[dev];
+            }
+        }
+        grid = std::min(n_tiles, grid);
+        launch_pdl(k_blend_tma, grid, kTmaThreads, smem, s, offsets, order,
+                   static_cast<const BlendRec*>(rec), g64, width, height, tiles_x,
+                   uint32_t(n_tiles), ticket, image);
+        return;
+    }
     if (exact) {
         static bool attr = false;
         const int smem = int(sizeof(BlendSmemExact));

@@ -325,8 +325,20 @@ __global__ void __launch_bounds__(kMarkBlock, 3) k_mark_internal(
     }
 }
 
-// Survivor counts are kept per 8192-node tile (one count per k_compact CTA).
+// Survivor counts are kept per 8192-node tile (one count per k_compact CTA) and
+// per super-tile of 32 tiles (stored after the tile counts), so a compaction CTA
+// finds its output position from at most n/2^18 super-tile counts plus 31 tile
+// counts -- O(n) loads per frame in total, not O(n^2 / 8192^2).
 constexpr int kTileNodes = 8192;
+constexpr int kSuperTiles = 32;
+__host__ __device__ inline uint64_t count_tiles(uint64_t n) {
+    return (n + kTileNodes - 1) / kTileNodes;
+}
+__device__ __forceinline__ void count_survivors(uint32_t* tile_count, uint64_t n_tiles,
+                                                uint64_t tile, uint32_t c) {
+    atomicAdd(tile_count + tile, c);
+    atomicAdd(tile_count + n_tiles + tile / kSuperTiles, c);
+}
 
 // F2: internal region.  Every node walks its parent chain (filter.cpp:20-25)
 // against the qint bitmask (L2-resident: 1 bit per internal node); the
@@ -338,7 +350,7 @@ constexpr int kTileNodes = 8192;
 // result does not depend on the interleaving.
 __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
     uint32_t* __restrict__ cand_bits, uint32_t* qint_bits, const uint32_t* __restrict__ parent,
-    const uint64_t end, uint32_t* __restrict__ tile_count) {
+    const uint64_t end, uint32_t* __restrict__ tile_count, const uint64_t n_tiles) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -393,7 +405,7 @@ __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
     }
 #pragma unroll
     for (int off = 4; off > 0; off >>= 1) cntw += __shfl_xor_sync(0xffffffffu, cntw, off);
-    if (lane == 0 && cntw) atomicAdd(tile_count + warp_base / kTileNodes, cntw);
+    if (lane == 0 && cntw) count_survivors(tile_count, n_tiles, warp_base / kTileNodes, cntw);
 }
 
 // F3: the all-leaf suffix [leaf_begin, n).  A leaf is kept iff visible
@@ -454,7 +466,7 @@ __global__ void __launch_bounds__(256) k_filter_leaves(
         c += __popc(w);
     }
     // a warp's 128 leaves lie in one 8192-node tile (leaf_begin is a multiple of 1024)
-    if (lane == 0 && c) atomicAdd(tile_count + wbase / kTileNodes, c);
+    if (lane == 0 && c) count_survivors(tile_count, count_tiles(t.n), wbase / kTileNodes, c);
 }
 
 // F4: ordered compaction of the keep words into `selected` (strictly
@@ -474,17 +486,12 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ ke
     __shared__ unsigned s_warp[8];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned tile = blockIdx.x;
+    // survivors before this tile: whole super-tiles, then the tiles of its own
+    const uint32_t* super_count = tile_count + gridDim.x;
+    const unsigned sup = tile / kSuperTiles;
     unsigned pre = 0;
-    {
-        unsigned p4[4] = {0u, 0u, 0u, 0u};
-        unsigned k = threadIdx.x;
-        for (; k + 768 < tile; k += 1024) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) p4[u] += __ldg(tile_count + k + 256 * u);
-        }
-        for (; k < tile; k += 256) p4[0] += __ldg(tile_count + k);
-        pre = (p4[0] + p4[1]) + (p4[2] + p4[3]);
-    }
+    for (unsigned k = threadIdx.x; k < sup; k += 256) pre += __ldg(super_count + k);
+    if (threadIdx.x < tile - sup * kSuperTiles) pre += __ldg(tile_count + sup * kSuperTiles + threadIdx.x);
     const uint64_t wi = uint64_t(tile) * (kTileNodes / 32) + warp * 32 + lane;
     const uint32_t keepw = wi < n_words ? __ldg(keep_bits + wi) : 0u;
     unsigned c = __popc(keepw);
@@ -570,7 +577,7 @@ __global__ void __launch_bounds__(256) k_serial_level(
             if (sm) atomicOr(sel_bits + w, sm);
             if (em) atomicOr(exp_bits + w, em);
         }
-        if (sm) atomicAdd(tile_count + (i >> 13), __popc(sm));
+        if (sm) count_survivors(tile_count, count_tiles(t.n), i / kTileNodes, __popc(sm));
         if (am && !level_flag[level] && atomicOr(level_flag + level, 1u) == 0u)
             atomicAdd(&cnt->serial_passes, 1u);
     }
@@ -626,7 +633,8 @@ static int sm_count() {
 }
 
 uint32_t filter_status_entries(uint64_t n) {
-    return uint32_t((n + kTileNodes - 1) / kTileNodes + 1);
+    const uint64_t t = count_tiles(n);
+    return uint32_t(t + (t + kSuperTiles - 1) / kSuperTiles + 1);
 }
 
 void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
@@ -644,7 +652,7 @@ void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand
         launch_pdl(k_mark_internal, grid, kMarkBlock, 0, s, g, f, t, tau_r, cand_bits, qint_bits);
         const uint64_t per = uint64_t(kSelectBlock) * kSelectItems;
         launch_pdl(k_select_internal, unsigned((split + per - 1) / per), kSelectBlock, 0, s,
-                   cand_bits, qint_bits, t.parent, split, tile_count);
+                   cand_bits, qint_bits, t.parent, split, tile_count, count_tiles(t.n));
     }
     if (mid) cudaEventRecord(mid, s);
     if (t.n > split)

@@ -34,8 +34,8 @@ struct DevTree {
 // ---- filter (filter.cpp:115-150) ----
 // kernels enqueued per frame: zero, mark internal, select internal, filter
 // leaves, compact, preprocess, tile offsets (+ run totals), emit, tile sort,
-// big-tile sort, blend
-constexpr int kLaunchesPerFrame = 11;
+// big-tile sort, blend record pack, blend
+constexpr int kLaunchesPerFrame = 12;
 constexpr int kMarkBlock = 256;
 constexpr int kSelectBlock = 256;
 constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles
@@ -118,10 +118,15 @@ void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
                           cudaStream_t s);
 
 // ---- blend (rasterizer.cpp:137-165, blend_scalar.cpp:13-55) ----
+// Fast path with `records` (blend_record_bytes() per pair capacity) and `ticket`:
+// K6a packs each sorted pair's blend record at its pair index, K6b (k_blend_tma)
+// streams every tile's records into shared memory with cp.async.bulk.  Without
+// records: the warp-specialised gather kernel (k_blend_wsp).
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,
-                  unsigned* ticket = nullptr);
+                  unsigned* ticket = nullptr, void* records = nullptr);
+uint64_t blend_record_bytes();
 
 // Exact blend + per-pair KPC in the reference's 4-lane order (collect_kpc).
 void launch_blend_exact_kpc(const uint32_t* offsets, const unsigned long long* keys,

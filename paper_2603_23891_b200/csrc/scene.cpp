@@ -439,6 +439,8 @@ void GpuScene::reserve_pairs(uint64_t n) {
     if (stream_) FGS_CUDA(cudaStreamSynchronize(stream_));
     keys_.release();
     keys_.alloc(n);
+    blend_rec_.release();
+    blend_rec_.alloc(n * blend_record_bytes());
     pair_cap_ = n;
 }
 
@@ -447,7 +449,8 @@ uint64_t GpuScene::device_bytes() const {
            parent_.bytes() + splat_.bytes() +
            cand_bits_.bytes() + qint_bits_.bytes() + selected_.bytes() + g64_.bytes() +
            tile_lists_.bytes() + tile_list_len_.bytes() +
-           g32_.bytes() + emit_.bytes() + col64_.bytes() + keys_.bytes() + zero_.bytes() +
+           g32_.bytes() + emit_.bytes() + col64_.bytes() + keys_.bytes() + blend_rec_.bytes() +
+           zero_.bytes() +
            res_.tile_offsets.bytes() + res_.tile_cursor.bytes() + res_.big_list.bytes() +
            res_.image.bytes();
 }
@@ -563,7 +566,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     } else {
         launch_blend(res_.tile_offsets.p, res_.tile_order.p, keys_.p, g64_.p, g32_.p, col64_.p,
                      res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact, img_out, stream_,
-                     &d_counters_->blend_ticket);
+                     &d_counters_->blend_ticket, blend_rec_.p);
     }
     if (timing) FGS_CUDA(cudaEventRecord(ev_[4], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[5], stream_));
@@ -1343,8 +1346,10 @@ void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_bl
     launch_bucket_triples(tri.p, n, tc, c.s);
     launch_tile_offsets(tc, n_tiles, off.p, cur.p, big.p, ord.p, cnt, n, c.s);
     launch_triples_to_keys(tri.p, n, keys.p, c.s);
+    DevBuf<unsigned char> rec;
+    rec.alloc(n * blend_record_bytes());
     launch_blend(off.p, ord.p, keys.p, dl.g64.p, dl.g32.p, dl.col64.p, width, height, tiles_x,
-                 tiles_y, exact, img.p, c.s, &cnt->blend_ticket);
+                 tiles_y, exact, img.p, c.s, &cnt->blend_ticket, rec.p);
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaMemcpyAsync(image, img.p, img.n * 4, cudaMemcpyDeviceToHost, c.s));
     FGS_CUDA(cudaStreamSynchronize(c.s));

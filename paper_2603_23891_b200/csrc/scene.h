@@ -192,6 +192,7 @@ private:
     DevBuf<GaussEmit> emit_;
     DevBuf<GaussCol64> col64_;
     DevBuf<unsigned long long> keys_;
+    DevBuf<unsigned char> blend_rec_;  // per pair, K6a -> K6b (blend_record_bytes() each)
     DevBuf<double> kpc_;         // per sorted pair (collect_kpc frames only)
     bool last_kpc_ = false;
     DevBuf<float> ref_image_;    // comparison reference (set_reference_image)

@@ -203,9 +203,17 @@ def test_cfg4_50m_4k_production(L, ref, gpu):
             assert out.stats.big_tiles > 0  # the big-bucket sort ran
             a = _async_frames(L, s, [hi, lo], 3.0, mode)
             assert a[1].tobytes() == out.image.rgb.tobytes()
-            rep = s.calibrate([topdown_camera(3840, 2160, 2000.0, z) for z in (400.0, 300.0, 200.0,
-                                                                              110.0)],
-                              0.2, L.FilterConfig(3.0))
+            # tools/workloads.py cfg 4: a 30-frame descent 400 -> 300 -> 110, 4 views
+            b = _bench()
+            keys = []
+            for eye, target in (((0.0, 0.0, 400.0), (0.0, 0.0001, 0.0)),
+                                ((20.0, -10.0, 300.0), (20.0, -9.9999, 0.0)),
+                                ((-10.0, 15.0, 110.0), (-10.0, 15.0001, 0.0))):
+                R, t = b.look_at(eye, target)
+                keys.append(L.Camera(3840, 2160, 2000.0, 2000.0, 1920.0, 1080.0, R, t))
+            path = L.sample_camera_path(keys, [14, 15])
+            rep = s.calibrate(path[::7][:4], 0.2, L.FilterConfig(3.0))
+            assert 0.0 < rep.tau < 1.0, rep.tau
             mode = L.ShrinkMode.adaptive(rep.tau)
             _sync_check(L, ref, rh, s, lo, 3.0, mode, f"cfg4 alt110 adaptive {rep.tau}")
     finally:
