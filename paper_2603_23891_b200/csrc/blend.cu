@@ -28,6 +28,10 @@
 #include <algorithm>
 #include <mutex>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "blend_rec.cuh"
 #include "launch.h"
 #include "pdl.cuh"
 
@@ -895,12 +899,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
 //     decision), and frees the stage with one mbarrier arrive per warp.  When
 //     all 8 warps of a tile have terminated (T < 1e-4 everywhere) the producer
 //     stops streaming that tile.
-struct __align__(16) BlendRec {
-    float4 geo;  // tile-relative mean x, y, ha, hc
-    float4 ct;   // cb, ethr, op, r
-    float4 gbm;  // g, b, block mask (bits), slot (bits)
-};
-static_assert(sizeof(BlendRec) == 48, "bulk copies move whole 16-byte-aligned records");
+
 
 __global__ void __launch_bounds__(128) k_pack_blend(const uint32_t* __restrict__ offsets,
                                                     const unsigned long long* __restrict__ keys,
@@ -912,35 +911,15 @@ __global__ void __launch_bounds__(128) k_pack_blend(const uint32_t* __restrict__
     const int tile = blockIdx.x;
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
     const int tx0 = (tile % tiles_x) * kTile, ty0 = (tile / tiles_x) * kTile;
-    for (uint32_t p = b + threadIdx.x; p < e; p += blockDim.x) {
-        const uint32_t gi = uint32_t(keys[p]);
-        const double2 m = *reinterpret_cast<const double2*>(&g64[gi].mx);
-        const float4 q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
-        const float4 col = *reinterpret_cast<const float4*>(&g32[gi].op);
-        const float2 h = *reinterpret_cast<const float2*>(&g32[gi].hx);
-        const float mtx = float(m.x - double(tx0));
-        const float mty = float(m.y - double(ty0));
-        // block (bxi, byi) spans tile-relative pixel centres
-        // [8 bxi + 0.5, 8 bxi + 7.5] x [4 byi + 0.5, 4 byi + 3.5]; warp w = bxi + 2 byi
-        uint32_t mask = 0;
-        if (h.x >= 0.0f) {
-            const uint32_t xm = (mtx - h.x <= 7.5f && mtx + h.x >= 0.5f ? 1u : 0u) |
-                                (mtx - h.x <= 15.5f && mtx + h.x >= 8.5f ? 2u : 0u);
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-                if (mty - h.y <= 4.0f * v + 3.5f && mty + h.y >= 4.0f * v + 0.5f)
-                    mask |= xm << (2 * v);
-        }
-        BlendRec r;
-        r.geo = make_float4(mtx, mty, q0.x, q0.z);
-        r.ct = make_float4(q0.y, q0.w, col.x, col.y);
-        r.gbm = make_float4(col.z, col.w, __uint_as_float(mask), __uint_as_float(gi));
-        rec[p] = r;
-    }
+    for (uint32_t p = b + threadIdx.x; p < e; p += blockDim.x)
+        rec[p] = make_blend_rec(g64, g32, uint32_t(keys[p]), tx0, ty0);
 }
 
 #ifndef TMA_STAGES
 #define TMA_STAGES 12
+#endif
+#ifndef TMA_COMPACT
+#define TMA_COMPACT 1  // consumers compact their hits into a per-warp list (else bit scan)
 #endif
 #ifndef TMA_MIN_CTAS
 #define TMA_MIN_CTAS 3
@@ -958,6 +937,9 @@ struct TmaHdr {
 };
 struct TmaShared {
     BlendRec rec[kTmaStages][kTmaChunk];
+#if TMA_COMPACT
+    WarpStage wl[kTmaConsumers];  // per consumer warp: its hits of the current stage
+#endif
     TmaHdr hdr[kTmaStages];
     unsigned long long full[kTmaStages], empty[kTmaStages];
     uint32_t done[kDoneRing];  // (tile seq << 4) | consumer warps terminated
@@ -976,6 +958,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
             "r"(smem_addr(dst)),
         "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+#ifndef TMA_PROD_HINT
+#define TMA_PROD_HINT 20000  // ns: the producer sleeps in hardware on a busy ring
+#endif
+#ifndef TMA_CONS_HINT
+#define TMA_CONS_HINT 0  // ns suspend hint of the consumers' full-barrier waits (0: spin)
+#endif
+// mbarrier wait with a suspend-time hint: the thread is descheduled until the
+// phase completes (or the hint expires) instead of re-issuing the poll
+template <int kHintNs>
+__device__ __forceinline__ void mbar_wait_hint(unsigned long long* b, uint32_t parity) {
+    if (kHintNs == 0) {
+        mbar_wait(b, parity);
+        return;
+    }
+    asm volatile(
+        "{ .reg .pred p;\n"
+        "WAITH_%=:\n"
+        "  mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "  @!p bra WAITH_%=;\n"
+        "}" ::"r"(smem_addr(b)),
+        "r"(parity), "n"(kHintNs)
         : "memory");
 }
 
@@ -1001,32 +1007,27 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
     if (warp == kTmaConsumers) {
         // ---------------- producer: one thread ----------------
         if (lane != 0) return;
-        auto take = [&]() -> int {
-            const uint32_t t = atomicAdd(ticket, 1u);
-            return t < n_tiles ? int(__ldg(order + t)) : -1;
-        };
+        // Tiles come through a three-deep pipeline -- ticket (atomic) -> tile id
+        // (order[]) -> bucket bounds (offsets[]) -- advanced one step per tile
+        // transition, so a transition never waits on a dependent global load
+        // (a one-chunk tile streams in the time of one bulk copy).
+        auto tile_of = [&](uint32_t t) -> int { return t < n_tiles ? int(__ldg(order + t)) : -1; };
+        int tile = tile_of(atomicAdd(ticket, 1u));
+        uint32_t b = tile >= 0 ? offsets[tile] : 0u, e = tile >= 0 ? offsets[tile + 1] : 0u;
+        int nxt = tile_of(atomicAdd(ticket, 1u));
+        uint32_t nb = nxt >= 0 ? offsets[nxt] : 0u, ne = nxt >= 0 ? offsets[nxt + 1] : 0u;
+        int t2 = tile_of(atomicAdd(ticket, 1u));
+        uint32_t raw3 = atomicAdd(ticket, 1u);
         uint32_t i = 0;  // stage sequence
         uint32_t k = 0;  // tile sequence of this CTA
-        int tile = take();
-        uint32_t b = 0, e = 0;
-        if (tile >= 0) {
-            b = offsets[tile];
-            e = offsets[tile + 1];
-        }
+        volatile uint32_t* done = sh.done;
         while (tile >= 0) {
-            // next tile's ticket and bounds are in flight while this one streams
-            const int next = take();
-            uint32_t nb = 0, ne = 0;
-            if (next >= 0) {
-                nb = offsets[next];
-                ne = offsets[next + 1];
-            }
             const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
-            volatile uint32_t* done = sh.done;
             done[k % kDoneRing] = k << 4;  // published by the first stage's arrive
             for (uint32_t c = b;; c += kTmaChunk) {
                 const int s = int(i % kTmaStages);
-                if (i >= uint32_t(kTmaStages)) mbar_wait(&sh.empty[s], ((i / kTmaStages) - 1) & 1u);
+                if (i >= uint32_t(kTmaStages))
+                    mbar_wait_hint<TMA_PROD_HINT>(&sh.empty[s], ((i / kTmaStages) - 1) & 1u);
                 const uint32_t n = c < e ? min(uint32_t(kTmaChunk), e - c) : 0u;
                 const bool last = c + kTmaChunk >= e || done[k % kDoneRing] == ((k << 4) | 8u);
                 sh.hdr[s] = TmaHdr{x0, y0, n, last ? 1u : 0u};
@@ -1040,18 +1041,27 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
                 if (last) break;
             }
             ++k;
-            tile = next;
+            tile = nxt;
             b = nb;
             e = ne;
+            nxt = t2;
+            nb = nxt >= 0 ? offsets[nxt] : 0u;
+            ne = nxt >= 0 ? offsets[nxt + 1] : 0u;
+            t2 = tile_of(raw3);
+            raw3 = atomicAdd(ticket, 1u);
         }
         const int s = int(i % kTmaStages);
-        if (i >= uint32_t(kTmaStages)) mbar_wait(&sh.empty[s], ((i / kTmaStages) - 1) & 1u);
+        if (i >= uint32_t(kTmaStages))
+            mbar_wait_hint<TMA_PROD_HINT>(&sh.empty[s], ((i / kTmaStages) - 1) & 1u);
         sh.hdr[s] = TmaHdr{0, 0, 0u, 2u};
         mbar_arrive(&sh.full[s]);
         return;
     }
 
     // ---------------- consumers: warp w owns the 8x4 block (w & 1, w >> 1) ----
+#if TMA_COMPACT
+    WarpStage* wl = sh.wl;
+#endif
     const int lx = int(warp & 1) * 8 + int(lane & 7), ly = int(warp >> 1) * 4 + int(lane >> 3);
     const float pxl = float(lx) + 0.5f, pyl = float(ly) + 0.5f;  // tile-relative pixel centre
     const uint32_t wbit = 1u << warp;
@@ -1061,7 +1071,7 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
     uint32_t k = 0;
     for (uint32_t i = 0;; ++i) {
         const int s = int(i % kTmaStages);
-        mbar_wait(&sh.full[s], (i / kTmaStages) & 1u);
+        mbar_wait_hint<TMA_CONS_HINT>(&sh.full[s], (i / kTmaStages) & 1u);
         const TmaHdr hd = sh.hdr[s];
         if (hd.flags & 2u) break;
         if (fresh) {
@@ -1077,6 +1087,30 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
         if (bits && __any_sync(0xffffffffu, pix.T != 0.0f)) {
             const PixState saved = pix;
             bool unsure = false;
+#if TMA_COMPACT
+            // this warp's hits, compacted in pair order into its own list
+            WarpStage& st = wl[warp];
+            if (mine) {
+                const int at = __popc(bits & ((1u << lane) - 1u));
+                st.geo[at] = R[lane].geo;
+                st.ct[at] = R[lane].ct;
+                st.gb[at] = make_float2(R[lane].gbm.x, R[lane].gbm.y);
+                st.gid[at] = __float_as_uint(R[lane].gbm.w);
+            }
+            __syncwarp();
+            const int nh = __popc(bits);
+            int kk = 0;
+            for (; kk + 2 <= nh; kk += 2) {
+                blend_sample_fast(st, kk, pxl, pyl, pix, unsure);
+                blend_sample_fast(st, kk + 1, pxl, pyl, pix, unsure);
+            }
+            if (kk < nh) blend_sample_fast(st, kk, pxl, pyl, pix, unsure);
+            if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
+                pix = saved;
+                const double px = double(x) + 0.5, py = double(y) + 0.5;
+                for (int j = 0; j < nh; ++j) blend_sample_checked(st, j, pxl, pyl, px, py, g64, pix);
+            }
+#else
             unsigned bb = bits;
             while (bb) {
                 const int j0 = __ffs(bb) - 1;
@@ -1101,6 +1135,7 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
                                    __float_as_uint(R[j].gbm.w), pxl, pyl, px, py, g64, pix);
                 }
             }
+#endif
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sh.empty[s]);
@@ -1119,6 +1154,309 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
             ++k;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// TMA gather4 blend (the default fast kernel, north_star (4)).  No pack pass:
+// the sorted keys name each pair's slot, and a tile's splat records are
+// gathered straight from the slot-indexed K3 records into shared memory by
+// the tensor memory accelerator -- cp.async.bulk.tensor.2d ... tile::gather4,
+// four rows per instruction (Gauss32 rows of 48 B, the first 32 B of the
+// Gauss64 rows), completion counted on the stage's mbarrier.
+//
+// Per CTA: one producer warp + 8 consumer warps, persistent, tiles from the
+// frame's ticket queue (heavy-first order).  The producer walks a chunk
+// sequence (32 pairs per chunk, >= 1 chunk per tile, across tiles) with a
+// register FIFO: chunk j's 32 keys are loaded kG4Ahead chunks before its
+// gathers are issued, and a tile's ticket -> order -> offsets chain is spread
+// over three tile transitions, so the producer never waits on a dependent
+// global load.  Lane 0 arms the stage's `full` barrier with the expected
+// bytes, lanes 0-7 / 8-15 issue one gather4 each.  Consumer warp w (8x4 block
+// (w & 1, w >> 1)) culls the 32 records against its block (the alpha box,
+// the FP64 mean rounded to block-relative FP32 exactly as k_blend_ws), compacts
+// its hits into its own list and blends them (k_blend_ws's per-sample code);
+// one mbarrier arrive per warp frees the stage.
+#ifndef G4_STAGES
+#define G4_STAGES 10
+#endif
+#ifndef G4_AHEAD
+#define G4_AHEAD 3
+#endif
+constexpr int kG4Stages = G4_STAGES;
+constexpr int kG4Ahead = G4_AHEAD;  // chunks whose keys are in flight
+constexpr int kG4Threads = (kTmaConsumers + 1) * 32;
+
+struct __align__(128) G4Stage {
+    float g32[8][64];   // gather4 group q: rows 4q..4q+3 of Gauss32 (48 B each), 256-B aligned
+    double g64[8][16];  // gather4 group q: rows 4q..4q+3, (mx, my, ca, cb) of Gauss64
+    uint32_t slot[32];
+};
+struct G4Shared {
+    G4Stage st[kG4Stages];
+    WarpStage wl[kTmaConsumers];
+    TmaHdr hdr[kG4Stages];
+    unsigned long long full[kG4Stages], empty[kG4Stages];
+    uint32_t done[kDoneRing];
+};
+constexpr uint32_t kG4GroupBytes = 4 * 48 + 4 * 32;  // one gather4 of each kind
+
+__device__ __forceinline__ void gather4(void* dst, const void* tmap, int r0, int r1, int r2,
+                                        int r3, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_addr(dst)),
+        "l"(tmap), "r"(smem_addr(bar)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+}
+
+// One chunk of the producer's sequence (warp-uniform except `slot`).
+struct G4Chunk {
+    int tile;  // -1: end of the CTA's work
+    uint32_t n, k;
+    bool last;
+    uint32_t slot;  // this lane's pair (lane < n)
+};
+
+__global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
+    const unsigned long long* __restrict__ keys, const __grid_constant__ CUtensorMap map32,
+    const __grid_constant__ CUtensorMap map64, const Gauss64* __restrict__ g64, const int width,
+    const int height, const int tiles_x, const uint32_t n_tiles, unsigned* ticket,
+    float* __restrict__ image) {
+    pdl_wait();  // the sort (and everything before it) is complete and visible
+    pdl_trigger();
+    extern __shared__ __align__(128) unsigned char g4_raw[];
+    G4Shared& sh = *reinterpret_cast<G4Shared*>(g4_raw);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kG4Stages; ++s) {
+            mbar_init(&sh.full[s], 1);
+            mbar_init(&sh.empty[s], kTmaConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kTmaConsumers) {
+        // ---------------- producer warp ----------------
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map32) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map64) : "memory");
+        // tile pipeline: raw ticket (lane 0) -> tile id -> bounds -> current
+        auto take = [&]() -> uint32_t { return lane == 0 ? atomicAdd(ticket, 1u) : 0u; };
+        auto tile_of = [&](uint32_t raw) -> int {
+            const uint32_t t = __shfl_sync(0xffffffffu, raw, 0);
+            return t < n_tiles ? int(__ldg(order + t)) : -1;
+        };
+        int cur = tile_of(take());
+        uint32_t cb = cur >= 0 ? offsets[cur] : 0u, ce = cur >= 0 ? offsets[cur + 1] : 0u;
+        int nxt = tile_of(take());
+        uint32_t nb = nxt >= 0 ? offsets[nxt] : 0u, ne = nxt >= 0 ? offsets[nxt + 1] : 0u;
+        int t2 = tile_of(take());  // bounds loaded at the next transition
+        uint32_t raw3 = take();    // tile id looked up at the next transition
+        uint32_t gc = cb, gk = 0;  // generator cursor: next chunk start, tile sequence
+        auto gen = [&]() -> G4Chunk {
+            G4Chunk ch;
+            ch.tile = cur;
+            ch.k = gk;
+            if (cur < 0) {
+                ch.n = 0;
+                ch.last = true;
+                ch.slot = 0;
+                return ch;
+            }
+            ch.n = gc < ce ? min(32u, ce - gc) : 0u;
+            ch.last = gc + 32u >= ce;
+            ch.slot = lane < ch.n ? uint32_t(keys[gc + lane]) : 0xFFFFFFFFu;
+            if (ch.last) {  // tile transition: shift the tile pipeline by one
+                cur = nxt;
+                cb = nb;
+                ce = ne;
+                nxt = t2;
+                nb = nxt >= 0 ? offsets[nxt] : 0u;
+                ne = nxt >= 0 ? offsets[nxt + 1] : 0u;
+                t2 = tile_of(raw3);
+                raw3 = take();
+                gc = cb;
+                ++gk;
+            } else {
+                gc += 32u;
+            }
+            return ch;
+        };
+        G4Chunk fifo[kG4Ahead];
+#pragma unroll
+        for (int j = 0; j < kG4Ahead; ++j) fifo[j] = gen();
+        uint32_t i = 0;                 // stage sequence
+        uint32_t killed = 0xFFFFFFFFu;  // tile sequence whose remaining chunks are dropped
+        bool first_chunk = true;        // the next issued chunk starts a tile
+        volatile uint32_t* done = sh.done;
+        for (;;) {
+            const G4Chunk ch = fifo[0];
+#pragma unroll
+            for (int j = 0; j + 1 < kG4Ahead; ++j) fifo[j] = fifo[j + 1];
+            fifo[kG4Ahead - 1] = gen();
+            if (ch.tile >= 0 && ch.k == killed) continue;  // rest of a terminated tile
+            const int s = int(i % kG4Stages);
+            if (i >= uint32_t(kG4Stages))
+                mbar_wait_hint<TMA_PROD_HINT>(&sh.empty[s], ((i / kG4Stages) - 1) & 1u);
+            ++i;
+            if (ch.tile < 0) {  // the CTA's work is done
+                if (lane == 0) {
+                    sh.hdr[s] = TmaHdr{0, 0, 0u, 2u};
+                    mbar_arrive(&sh.full[s]);
+                }
+                break;
+            }
+            // first chunk of a tile: reset its terminated-warp counter (published
+            // to the consumers by this stage's arrive)
+            if (first_chunk && lane == 0) done[ch.k % kDoneRing] = ch.k << 4;
+            bool last = ch.last;
+            if (!first_chunk && !last && done[ch.k % kDoneRing] == ((ch.k << 4) | 8u)) {
+                last = true;
+                killed = ch.k;
+            }
+            G4Stage& st = sh.st[s];
+            // lanes past n name a valid row (lane 0's): their bytes are fetched, never read
+            const uint32_t s0 = __shfl_sync(0xffffffffu, ch.slot, 0);
+            const uint32_t slot = lane < ch.n ? ch.slot : s0;
+            st.slot[lane] = slot;
+            const uint32_t groups = (ch.n + 3u) >> 2;
+            const int q = int(lane & 7);
+            const int r0 = int(__shfl_sync(0xffffffffu, slot, 4 * q + 0));
+            const int r1 = int(__shfl_sync(0xffffffffu, slot, 4 * q + 1));
+            const int r2 = int(__shfl_sync(0xffffffffu, slot, 4 * q + 2));
+            const int r3 = int(__shfl_sync(0xffffffffu, slot, 4 * q + 3));
+            if (lane == 0) {
+                const int tx0 = (ch.tile % tiles_x) * kTile, ty0 = (ch.tile / tiles_x) * kTile;
+                sh.hdr[s] = TmaHdr{tx0, ty0, ch.n, last ? 1u : 0u};
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (groups) mbar_expect_tx(&sh.full[s], groups * kG4GroupBytes);
+                else mbar_arrive(&sh.full[s]);
+            }
+            __syncwarp();
+            if (uint32_t(q) < groups) {
+                if (lane < 8) gather4(&st.g32[q][0], &map32, r0, r1, r2, r3, &sh.full[s]);
+                else if (lane < 16) gather4(&st.g64[q][0], &map64, r0, r1, r2, r3, &sh.full[s]);
+            }
+            first_chunk = last;
+        }
+        return;
+    }
+
+    // ---------------- consumers: warp w owns the 8x4 block (w & 1, w >> 1) ----
+    WarpStage& wl = sh.wl[warp];
+    const float pxl = float(lane & 7) + 0.5f, pyl = float(lane >> 3) + 0.5f;  // block-relative
+    const int bxo = int(warp & 1) * 8, byo = int(warp >> 1) * 4;
+    PixState pix{0.0f, 0.0f, 0.0f, 0.0f};
+    bool fresh = true, counted = false;
+    int bx = 0, by = 0;
+    uint32_t k = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint32_t i = 0;; ++i) {
+        const int s = int(i % kG4Stages);
+        mbar_wait_hint<TMA_CONS_HINT>(&sh.full[s], (i / kG4Stages) & 1u);
+        const TmaHdr hd = sh.hdr[s];
+        if (hd.flags & 2u) break;
+        if (fresh) {
+            bx = hd.x0 + bxo;
+            by = hd.y0 + byo;
+            const int x = bx + int(lane & 7), y = by + int(lane >> 3);
+            pix = PixState{(x < width && y < height) ? 1.0f : 0.0f, 0.0f, 0.0f, 0.0f};
+            fresh = false;
+            counted = false;
+        }
+        const G4Stage& st = sh.st[s];
+        const int q = int(lane >> 2), r = int(lane & 3);
+        bool hit = false;
+        float mlx = 0.f, mly = 0.f;
+        if (lane < hd.n) {
+            const float2 h = *reinterpret_cast<const float2*>(&st.g32[q][r * 12 + 8]);
+            const double2 m = *reinterpret_cast<const double2*>(&st.g64[q][r * 4]);
+            if (h.x >= 0.0f) {
+                mlx = float(m.x - double(bx));
+                mly = float(m.y - double(by));
+                hit = mlx - h.x <= 7.5f && mlx + h.x >= 0.5f && mly - h.y <= 3.5f &&
+                      mly + h.y >= 0.5f;
+            }
+        }
+        const unsigned bits = __ballot_sync(0xffffffffu, hit);
+        if (bits && __any_sync(0xffffffffu, pix.T != 0.0f)) {
+            if (hit) {
+                const int at = __popc(bits & lt);
+                const float* g = &st.g32[q][r * 12];
+                const float4 q0 = *reinterpret_cast<const float4*>(g);
+                const float4 col = *reinterpret_cast<const float4*>(g + 4);
+                wl.geo[at] = make_float4(mlx, mly, q0.x, q0.z);
+                wl.ct[at] = make_float4(q0.y, q0.w, col.x, col.y);
+                wl.gb[at] = make_float2(col.z, col.w);
+                wl.gid[at] = st.slot[lane];
+            }
+            __syncwarp();
+            const PixState saved = pix;
+            bool unsure = false;
+            const int nh = __popc(bits);
+            int kk = 0;
+            for (; kk + 2 <= nh; kk += 2) {
+                blend_sample_fast(wl, kk, pxl, pyl, pix, unsure);
+                blend_sample_fast(wl, kk + 1, pxl, pyl, pix, unsure);
+            }
+            if (kk < nh) blend_sample_fast(wl, kk, pxl, pyl, pix, unsure);
+            if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
+                pix = saved;
+                const double px = double(bx + int(lane & 7)) + 0.5;
+                const double py = double(by + int(lane >> 3)) + 0.5;
+                for (int j = 0; j < nh; ++j) blend_sample_checked(wl, j, pxl, pyl, px, py, g64, pix);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[s]);
+        if (!counted && __all_sync(0xffffffffu, pix.T == 0.0f)) {
+            counted = true;
+            if (lane == 0) atomicAdd(&sh.done[k % kDoneRing], 1u);
+        }
+        if (hd.flags & 1u) {
+            const int x = bx + int(lane & 7), y = by + int(lane >> 3);
+            if (x < width && y < height) {
+                float* o = image + (size_t(y) * width + x) * 3;
+                o[0] = pix.cr;
+                o[1] = pix.cg;
+                o[2] = pix.cb;
+            }
+            fresh = true;
+            ++k;
+        }
+    }
+}
+
+// Tensor maps of the slot-indexed records for gather4: Gauss32 rows (12 floats)
+// and the first 4 doubles of the Gauss64 rows; boxes of one row, 4 rows per gather.
+static bool encode_record_maps(const Gauss32* g32, const Gauss64* g64, uint64_t rows,
+                               CUtensorMap* m32, CUtensorMap* m64) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!encode || rows == 0 || rows > 0xFFFFFFFFull) return false;
+    const cuuint64_t d32[2] = {12, rows}, s32[1] = {sizeof(Gauss32)};
+    const cuuint32_t b32[2] = {12, 1}, e1[2] = {1, 1};
+    const cuuint64_t d64[2] = {8, rows}, s64[1] = {sizeof(Gauss64)};
+    const cuuint32_t b64[2] = {4, 1};
+    if (encode(m32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<Gauss32*>(g32), d32, s32, b32,
+               e1, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    return encode(m64, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<Gauss64*>(g64), d64, s64,
+                  b64, e1, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 constexpr int kBlendThreads = 256;  // exact kernel: one CTA per 16x16 tile
@@ -1356,20 +1694,56 @@ void launch_view_gtc(const uint32_t* offsets, int n_tiles, const double* kpc, ui
     if (n_pairs) k_kpc_histogram<<<148, 256, 0, s>>>(kpc, n_pairs, bins);
 }
 
-uint64_t blend_record_bytes() { return sizeof(BlendRec); }
+// Fast-blend kernel (all three certified-identical; the numbers are DESIGN.md's):
+//   0  k_blend_wsp -- producer warps gather records with cp.async (default: fastest
+//      measured, the blend is bound by its per-sample arithmetic, not by staging)
+//   1  k_blend_g4  -- TMA tile::gather4 of the slot-indexed records (TMA row-rate bound)
+//   2  k_blend_tma -- the sort writes per-pair records, cp.async.bulk streams them
+#ifndef BLEND_TMA
+#define BLEND_TMA 0
+#endif
+// per-pair record buffer bytes the fast blend needs (only the pack + bulk variant)
+uint64_t blend_record_bytes() { return BLEND_TMA == 2 ? sizeof(BlendRec) : 0; }
+// kernels the fast blend launches per frame
+int blend_launches() { return 1; }
 
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,
-                  unsigned* ticket, void* records) {
+                  unsigned* ticket, void* records, uint64_t n_records, bool records_packed) {
     const int n_tiles = tiles_x * tiles_y;
     if (n_tiles <= 0) return;
-#ifndef BLEND_TMA
-#define BLEND_TMA 1
-#endif
-    if (BLEND_TMA && !exact && records && ticket) {
+    CUtensorMap m32, m64;
+    if (BLEND_TMA == 1 && !exact && ticket && n_records &&
+        encode_record_maps(g32, g64, n_records, &m32, &m64)) {
+        const int smem = int(sizeof(G4Shared));
+        static std::mutex mu;
+        static int grid_of[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int grid = 0;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            if (dev < 0 || dev >= 64 || !grid_of[dev]) {
+                cudaFuncSetAttribute(k_blend_g4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                int per_sm = 0, n_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blend_g4, kG4Threads, smem);
+                cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+                grid = std::max(1, per_sm) * std::max(1, n_sm);
+                if (dev >= 0 && dev < 64) grid_of[dev] = grid;
+            } else {
+                grid = grid_of[dev];
+            }
+        }
+        grid = std::min(n_tiles, grid);
+        launch_pdl(k_blend_g4, grid, kG4Threads, smem, s, offsets, order, keys, m32, m64, g64,
+                   width, height, tiles_x, uint32_t(n_tiles), ticket, image);
+        return;
+    }
+    if (BLEND_TMA == 2 && !exact && records && ticket) {
         BlendRec* rec = static_cast<BlendRec*>(records);
-        launch_pdl(k_pack_blend, n_tiles, 128, 0, s, offsets, keys, g64, g32, tiles_x, rec);
+        if (!records_packed)  // the frame's sort writes them; stage entry points pack here
+            launch_pdl(k_pack_blend, n_tiles, 128, 0, s, offsets, keys, g64, g32, tiles_x, rec);
         const int smem = int(sizeof(TmaShared));
         static std::mutex mu;
         static int grid_of[64] = {};

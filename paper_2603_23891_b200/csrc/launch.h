@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "blend_rec.cuh"
 #include "common.cuh"
 
 namespace fgs {
@@ -34,8 +35,8 @@ struct DevTree {
 // ---- filter (filter.cpp:115-150) ----
 // kernels enqueued per frame: zero, mark internal, select internal, filter
 // leaves, compact, preprocess, tile offsets (+ run totals), emit, tile sort,
-// big-tile sort, blend record pack, blend
-constexpr int kLaunchesPerFrame = 12;
+// big-tile sort, then blend_launches() for the blend
+constexpr int kLaunchesPerFrame = 10;
 constexpr int kMarkBlock = 256;
 constexpr int kSelectBlock = 256;
 constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles
@@ -111,22 +112,27 @@ void launch_compact_records(const uint32_t* slot_of_g, uint64_t n_g, const Gauss
 // ---- sort (rasterizer.cpp:100-135) ----
 constexpr int kSmallSortCap = 2048;
 constexpr int kBigSortCap = 16384;
+// With ro.rec set, every key's blend record (blend_rec.cuh) is written at the
+// key's final position as well (the TMA-staged blend reads them contiguously).
 void launch_tile_sort(const uint32_t* offsets, const uint32_t* order, int n_tiles,
-                      unsigned long long* keys, cudaStream_t s);
+                      unsigned long long* keys, cudaStream_t s, RecOut ro = {}, int tiles_x = 1);
 void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
                           const uint32_t* big_list, FrameCounters* cnt, int grid,
-                          cudaStream_t s);
+                          cudaStream_t s, RecOut ro = {}, int tiles_x = 1);
 
 // ---- blend (rasterizer.cpp:137-165, blend_scalar.cpp:13-55) ----
-// Fast path with `records` (blend_record_bytes() per pair capacity) and `ticket`:
-// K6a packs each sorted pair's blend record at its pair index, K6b (k_blend_tma)
-// streams every tile's records into shared memory with cp.async.bulk.  Without
-// records: the warp-specialised gather kernel (k_blend_wsp).
+// Fast path (BLEND_TMA=1, default) with `ticket` and n_records (rows of g32/g64):
+// k_blend_g4 gathers every tile's records into shared memory with TMA gather4.
+// BLEND_TMA=2 (experiment): K6a packs each sorted pair's record at its pair index
+// into `records` (blend_record_bytes() per pair), K6b streams them with
+// cp.async.bulk.  BLEND_TMA=0: the warp-specialised gather kernel (k_blend_wsp).
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,
-                  unsigned* ticket = nullptr, void* records = nullptr);
+                  unsigned* ticket = nullptr, void* records = nullptr, uint64_t n_records = 0,
+                  bool records_packed = false);
 uint64_t blend_record_bytes();
+int blend_launches();
 
 // Exact blend + per-pair KPC in the reference's 4-lane order (collect_kpc).
 void launch_blend_exact_kpc(const uint32_t* offsets, const unsigned long long* keys,

@@ -440,7 +440,7 @@ void GpuScene::reserve_pairs(uint64_t n) {
     keys_.release();
     keys_.alloc(n);
     blend_rec_.release();
-    blend_rec_.alloc(n * blend_record_bytes());
+    if (blend_record_bytes()) blend_rec_.alloc(n * blend_record_bytes());
     pair_cap_ = n;
 }
 
@@ -554,9 +554,13 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     maps_valid_ = false;
     if (timing) FGS_CUDA(cudaEventRecord(ev_[2], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[3], stream_));
-    launch_tile_sort(res_.tile_offsets.p, res_.tile_order.p, n_tiles, keys_.p, stream_);
+    // the fast blend's per-pair records are written by the sort, next to each key
+    const RecOut ro{(!exact && blend_rec_.p) ? reinterpret_cast<BlendRec*>(blend_rec_.p) : nullptr,
+                    g64_.p, g32_.p};
+    launch_tile_sort(res_.tile_offsets.p, res_.tile_order.p, n_tiles, keys_.p, stream_, ro,
+                     res_.tiles_x);
     launch_tile_sort_big(res_.tile_offsets.p, keys_.p, res_.big_list.p, d_counters_,
-                         sm_count_, stream_);
+                         sm_count_, stream_, ro, res_.tiles_x);
     if (timing) FGS_CUDA(cudaEventRecord(ev_[3], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[4], stream_));
     float* img_out = image_target_ ? image_target_ : res_.image.p;
@@ -566,7 +570,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     } else {
         launch_blend(res_.tile_offsets.p, res_.tile_order.p, keys_.p, g64_.p, g32_.p, col64_.p,
                      res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact, img_out, stream_,
-                     &d_counters_->blend_ticket, blend_rec_.p);
+                     &d_counters_->blend_ticket, blend_rec_.p, g32_.n, ro.rec != nullptr);
     }
     if (timing) FGS_CUDA(cudaEventRecord(ev_[4], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[5], stream_));
@@ -624,7 +628,7 @@ void GpuScene::finish(lodgs_render_stats* stats) {
         stats->filter_barriers = stats->filter_passes;
         stats->big_tiles = c.big_tiles;
         stats->kernel_launches =
-            last_serial_ ? uint32_t(kLaunchesPerFrame - 4 + n_levels() + 1) : kLaunchesPerFrame;
+            last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() - 4 + n_levels() + 1) : kLaunchesPerFrame + blend_launches();
         if (last_timing_) {
             float ms = 0;
             FGS_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
@@ -756,8 +760,8 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
             s.filter_passes = last_serial_ ? int32_t(c.serial_passes) : 2;
             s.filter_barriers = s.filter_passes;
             s.big_tiles = c.big_tiles;
-            s.kernel_launches = last_serial_ ? uint32_t(kLaunchesPerFrame - 4 + n_levels() + 1)
-                                             : kLaunchesPerFrame;
+            s.kernel_launches = last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() - 4 + n_levels() + 1)
+                                             : kLaunchesPerFrame + blend_launches();
         }
     }
 }
@@ -1347,9 +1351,9 @@ void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_bl
     launch_tile_offsets(tc, n_tiles, off.p, cur.p, big.p, ord.p, cnt, n, c.s);
     launch_triples_to_keys(tri.p, n, keys.p, c.s);
     DevBuf<unsigned char> rec;
-    rec.alloc(n * blend_record_bytes());
+    if (blend_record_bytes()) rec.alloc(n * blend_record_bytes());
     launch_blend(off.p, ord.p, keys.p, dl.g64.p, dl.g32.p, dl.col64.p, width, height, tiles_x,
-                 tiles_y, exact, img.p, c.s, &cnt->blend_ticket, rec.p);
+                 tiles_y, exact, img.p, c.s, &cnt->blend_ticket, rec.p, dl.g32.n);
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaMemcpyAsync(image, img.p, img.n * 4, cudaMemcpyDeviceToHost, c.s));
     FGS_CUDA(cudaStreamSynchronize(c.s));

@@ -15,10 +15,24 @@
 // sorter: every comparator is oriented low->high, so a non-power-of-two
 // bucket is padded virtually with +inf (a comparator whose high index is
 // past the end is skipped and the padding never moves).
+#include "blend_rec.cuh"
 #include "launch.h"
 #include "pdl.cuh"
 
 namespace fgs {
+
+// Where a sort places a bucket's keys for good: the blend records of those
+// positions are written alongside (RecOut::rec, the TMA-staged blend); null
+// for sorts into shared memory (runs, whose final positions come later).
+struct RecSite {
+    RecOut ro;
+    uint32_t pbase;  // global pair index of the bucket's first key
+    uint32_t tile;
+    int tiles_x;
+    __device__ __forceinline__ void put(uint32_t i, unsigned long long key) const {
+        emit_rec(ro, pbase + i, key, tile, tiles_x);
+    }
+};
 
 template <typename Index, typename Sync>
 __device__ __forceinline__ void flip_bitonic(unsigned long long* a, Index n, Index tid,
@@ -115,7 +129,7 @@ template <int LOGP>
 __device__ __forceinline__ void register_bitonic(const unsigned long long* keys, uint32_t n,
                                                  unsigned long long* out,
                                                  unsigned long long* s_x, uint32_t tid,
-                                                 unsigned xbar) {
+                                                 unsigned xbar, const RecSite* site = nullptr) {
     constexpr uint32_t P = 1u << LOGP;
     constexpr int R = P > uint32_t(kSmallSortThreads) ? int(P / kSmallSortThreads) : 1;
     constexpr uint32_t lanes = P < uint32_t(kSmallSortThreads) ? P : uint32_t(kSmallSortThreads);
@@ -175,7 +189,10 @@ __device__ __forceinline__ void register_bitonic(const unsigned long long* keys,
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t i = uint32_t(r) * kSmallSortThreads + tid;
-        if (i < n) out[i] = v[r];
+        if (i < n) {
+            out[i] = v[r];
+            if (site) site->put(i, v[r]);
+        }
     }
 }
 
@@ -195,7 +212,8 @@ __device__ __forceinline__ bool register_bitonic32(const unsigned long long* key
                                                    unsigned long long* s_orig, uint32_t* s_x,
                                                    uint32_t* s_red, unsigned long long* s_out,
                                                    unsigned long long* dst, uint32_t tid,
-                                                   unsigned xbar, Bar bar) {
+                                                   unsigned xbar, Bar bar,
+                                                   const RecSite* site = nullptr) {
     constexpr uint32_t P = 1u << LOGP;
     constexpr int R = P > uint32_t(kSmallSortThreads) ? int(P / kSmallSortThreads) : 1;
     constexpr uint32_t lanes = P < uint32_t(kSmallSortThreads) ? P : uint32_t(kSmallSortThreads);
@@ -312,7 +330,10 @@ __device__ __forceinline__ bool register_bitonic32(const unsigned long long* key
         if (!bar.sync_or(swapped)) break;
     }
     if (dst)
-        for (uint32_t i = tid; i < n; i += kSmallSortThreads) dst[i] = s_out[i];
+        for (uint32_t i = tid; i < n; i += kSmallSortThreads) {
+            dst[i] = s_out[i];
+            if (site) site->put(i, s_out[i]);
+        }
     return true;
 }
 
@@ -336,7 +357,8 @@ __device__ __forceinline__ void sort_run(const unsigned long long* keys, uint32_
 // its index in its run plus, for every other run, the number of keys below it
 // (a fixed-depth binary search); each key is stored once, straight to HBM.
 __device__ __forceinline__ void rank_merge(const unsigned long long* runs, uint32_t n,
-                                           unsigned long long* dst, uint32_t tid, uint32_t nthr) {
+                                           unsigned long long* dst, uint32_t tid, uint32_t nthr,
+                                           const RecSite& site) {
     const uint32_t n_runs = (n + kRun - 1) / kRun;
     for (uint32_t i = tid; i < n; i += nthr) {
         const unsigned long long x = runs[i];
@@ -353,12 +375,14 @@ __device__ __forceinline__ void rank_merge(const unsigned long long* runs, uint3
             rank += pos;
         }
         dst[rank] = x;
+        site.put(rank, x);
     }
 }
 
 __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t* __restrict__ offsets,
                                                                  const uint32_t* __restrict__ order,
-                                                                 unsigned long long* keys) {
+                                                                 unsigned long long* keys,
+                                                                 const RecOut ro, const int tiles_x) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
     static_assert(kSmallSortCap == 2 * int(kRun), "two runs + their staging fill s");
@@ -368,7 +392,10 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t*
     const uint32_t b = offsets[tile], e = offsets[tile + 1];
     const uint32_t n = e - b;
     const uint32_t tid = threadIdx.x;
+    const RecSite site{ro, b, tile, tiles_x};
+    if (n == 1 && tid == 0) site.put(0, keys[b]);
     if (n < 2 || n > uint32_t(kSmallSortCap)) return;  // big buckets: k_tile_sort_big
+    const RecSite* sp = ro.rec ? &site : nullptr;
 #ifndef SORT32
 #define SORT32 1
 #endif
@@ -378,7 +405,7 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t*
                      s + kSmallSortCap, s_red, tid, 1, CtaBar{});
             __syncthreads();
         }
-        rank_merge(s, n, keys + b, tid, kSmallSortThreads);
+        rank_merge(s, n, keys + b, tid, kSmallSortThreads, site);
         return;
     }
 #if SORT32
@@ -386,22 +413,22 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t*
         bool done;
         uint32_t* sx32 = reinterpret_cast<uint32_t*>(s + kRun);
         unsigned long long* so = s + 2 * kRun;
-        if (n <= 32u) done = register_bitonic32<5>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
-        else if (n <= 64u) done = register_bitonic32<6>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
-        else if (n <= 128u) done = register_bitonic32<7>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
-        else if (n <= 256u) done = register_bitonic32<8>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
-        else if (n <= 512u) done = register_bitonic32<9>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
-        else done = register_bitonic32<10>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{});
+        if (n <= 32u) done = register_bitonic32<5>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{}, sp);
+        else if (n <= 64u) done = register_bitonic32<6>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{}, sp);
+        else if (n <= 128u) done = register_bitonic32<7>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{}, sp);
+        else if (n <= 256u) done = register_bitonic32<8>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{}, sp);
+        else if (n <= 512u) done = register_bitonic32<9>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{}, sp);
+        else done = register_bitonic32<10>(keys + b, n, s, sx32, s_red, so, keys + b, tid, 1, CtaBar{}, sp);
         if (done) return;
         __syncthreads();  // staging in s is reused by the 64-bit network
     }
 #endif
-    if (n <= 32u) register_bitonic<5>(keys + b, n, keys + b, s, tid, 1);
-    else if (n <= 64u) register_bitonic<6>(keys + b, n, keys + b, s, tid, 1);
-    else if (n <= 128u) register_bitonic<7>(keys + b, n, keys + b, s, tid, 1);
-    else if (n <= 256u) register_bitonic<8>(keys + b, n, keys + b, s, tid, 1);
-    else if (n <= 512u) register_bitonic<9>(keys + b, n, keys + b, s, tid, 1);
-    else register_bitonic<10>(keys + b, n, keys + b, s, tid, 1);
+    if (n <= 32u) register_bitonic<5>(keys + b, n, keys + b, s, tid, 1, sp);
+    else if (n <= 64u) register_bitonic<6>(keys + b, n, keys + b, s, tid, 1, sp);
+    else if (n <= 128u) register_bitonic<7>(keys + b, n, keys + b, s, tid, 1, sp);
+    else if (n <= 256u) register_bitonic<8>(keys + b, n, keys + b, s, tid, 1, sp);
+    else if (n <= 512u) register_bitonic<9>(keys + b, n, keys + b, s, tid, 1, sp);
+    else register_bitonic<10>(keys + b, n, keys + b, s, tid, 1, sp);
 }
 
 constexpr int kBigGroups = 4;
@@ -417,7 +444,9 @@ constexpr int kBigSortSmem = (kBigSortCap + kBigGroups * 2 * int(kRun)) * 8;
 __global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_t* __restrict__ offsets,
                                                                    unsigned long long* keys,
                                                                    const uint32_t* big_list,
-                                                                   FrameCounters* cnt) {
+                                                                   FrameCounters* cnt,
+                                                                   const RecOut ro,
+                                                                   const int tiles_x) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
     extern __shared__ unsigned long long s_big[];
@@ -443,25 +472,29 @@ __global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_
                 gbar.sync();  // staging reuse by the group's next run
             }
             __syncthreads();
-            rank_merge(s_big, n, keys + b, threadIdx.x, kBigSortThreads);
+            rank_merge(s_big, n, keys + b, threadIdx.x, kBigSortThreads, RecSite{ro, b, tile, tiles_x});
         } else {
             flip_bitonic<uint32_t>(keys + b, n, threadIdx.x, kBigSortThreads, [] __device__() {
                 __threadfence_block();
                 __syncthreads();
             });
+            if (ro.rec) {
+                const RecSite site{ro, b, tile, tiles_x};
+                for (uint32_t i = threadIdx.x; i < n; i += kBigSortThreads) site.put(i, keys[b + i]);
+            }
         }
     }
 }
 
 void launch_tile_sort(const uint32_t* offsets, const uint32_t* order, int n_tiles,
-                      unsigned long long* keys, cudaStream_t s) {
+                      unsigned long long* keys, cudaStream_t s, RecOut ro, int tiles_x) {
     if (n_tiles <= 0) return;
-    launch_pdl(k_tile_sort, n_tiles, kSmallSortThreads, 0, s, offsets, order, keys);
+    launch_pdl(k_tile_sort, n_tiles, kSmallSortThreads, 0, s, offsets, order, keys, ro, tiles_x);
 }
 
 void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
                           const uint32_t* big_list, FrameCounters* cnt, int grid,
-                          cudaStream_t s) {
+                          cudaStream_t s, RecOut ro, int tiles_x) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -469,7 +502,7 @@ void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
         attr = true;
     }
     launch_pdl(k_tile_sort_big, grid, kBigSortThreads, kBigSortSmem, s, offsets, keys, big_list,
-               cnt);
+               cnt, ro, tiles_x);
 }
 
 // ----------------------------------------------------------------------------
