@@ -7,9 +7,10 @@
  * and for its stage functions filter_parallel / prepare_gaussians /
  * bin_to_tiles / sort_pairs / alpha_blend (filter.hpp:42-43,
  * rasterizer.hpp:55-71).  Plain pointers and sizes only; no C++ or torch
- * types.  The C++ mirror of the reference API (include/lodgs_b200/lodgs.hpp)
- * and the Python host module (paper_2603_23891_b200/lodgs.py) both sit on
- * top of these entry points.
+ * types.  The reference-side C++ shim (integration/rasterizer_b200.cpp, the
+ * maintainer-added lodgs::render of INTEGRATION.md, linked and run against the
+ * reference library by tests/test_gpu_integration.py) and the Python host module
+ * (paper_2603_23891_b200/lodgs.py) both sit on top of these entry points.
  *
  * Every compute entry point runs hand-written sm_100a CUDA kernels; there is
  * no CPU fallback.  Without a usable CUDA device the compute calls return
@@ -142,45 +143,6 @@ LODGS_API int lodgs_validate_camera(const lodgs_camera *cam, uint64_t *n_violati
                           size_t msg_cap);
 /* projection.cpp:11-38 CameraGeom::make, 44 doubles in CameraGeom order. */
 LODGS_API int lodgs_camera_geom(const lodgs_camera *cam, double out44[44]);
-/* camera_path.cpp:126-180: frames = sum(samples)+1; out holds that many. */
-LODGS_API int lodgs_camera_path_sample(const lodgs_camera *keyframes, uint32_t n_keyframes,
-                             const uint32_t *samples, lodgs_camera *out, uint64_t out_cap,
-                             uint64_t *n_frames);
-
-/* tree_builder.hpp:11-27 configs. */
-typedef struct lodgs_synthetic_spec {
-    uint32_t nx, ny;
-    float spacing;
-    float scale_min, scale_max;
-    float opacity_min, opacity_max;
-    uint64_t seed;
-    uint32_t congestion;
-} lodgs_synthetic_spec;
-
-typedef struct lodgs_build_config {
-    uint32_t depth;
-    float shrink_factor;
-    uint32_t children_per_node;
-    uint64_t seed;
-} lodgs_build_config;
-
-/* Writable SoA arrays for tree construction (capacity = n_nodes). */
-typedef struct lodgs_tree_buffers {
-    float *mean_x, *mean_y, *mean_z;
-    float *scale_x, *scale_y, *scale_z;
-    float *quat_w, *quat_x, *quat_y, *quat_z;
-    float *opacity;
-    float *color_r, *color_g, *color_b;
-    uint32_t *parent;
-    uint8_t *leaf;
-    uint32_t *level_offsets; /* capacity depth+1 */
-} lodgs_tree_buffers;
-
-/* generate_synthetic_scene + build_tree (tree_builder.cpp:75-174): first call
- * with out == NULL to learn n_nodes / n_levels, then with buffers. */
-LODGS_API int lodgs_build_synthetic_tree(const lodgs_synthetic_spec *spec, const lodgs_build_config *cfg,
-                               lodgs_tree_buffers *out, uint64_t *n_nodes, uint32_t *n_levels);
-
 /* ---------------------------------------------------------- GPU scenes -- */
 /* Validates the tree once (the reference re-validates every frame,
  * rasterizer.cpp:170) and uploads it to `device`.  The scene owns one CUDA

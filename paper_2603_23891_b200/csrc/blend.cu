@@ -597,8 +597,7 @@ struct WspShared {
     WspStage st[kWsStages];
     WsRaw raw[kWsProducers][kWsRaw];
     unsigned long long full[kWsStages], empty[kWsStages];
-    int tq[kTq];
-    uint32_t tq_seq[kTq];
+    unsigned long long tq[kTq];  // (k << 32) | tile, see wsp_tile
 };
 
 // Position in a CTA's stage sequence: k-th tile of the CTA, batch bi of it.
@@ -641,26 +640,25 @@ __device__ __forceinline__ int wsp_tile(uint32_t k, const WspSrc& src, bool fetc
         const uint32_t slot = wsp_slot(k);
         return slot < src.n_tiles ? int(src.order[slot]) : -1;
     }
+    // one 64-bit word per ring entry, (k << 32) | tile, written and read with
+    // shared-memory atomics: the reader either sees entry k whole or keeps waiting
     const uint32_t q = k % kTq;
-    volatile uint32_t* seq = src.sh->tq_seq;
-    volatile int* tq = src.sh->tq;
+    unsigned long long* ent = &src.sh->tq[q];
     if (fetch) {
         uint32_t t = 0;
         if ((threadIdx.x & 31) == 0) t = atomicAdd(src.ticket, 1u);
         t = __shfl_sync(0xffffffffu, t, 0);
         const int tile = t < src.n_tiles ? int(src.order[t]) : -1;
-        if ((threadIdx.x & 31) == 0) {
-            tq[q] = tile;
-            __threadfence_block();
-            seq[q] = k;
-        }
+        if ((threadIdx.x & 31) == 0) atomicExch(ent, (unsigned long long)k << 32 | uint32_t(tile));
         __syncwarp();
         return tile;
     }
-    while (seq[q] != k) {
-    }
-    __threadfence_block();
-    return tq[q];
+    unsigned long long v = 0;
+    if ((threadIdx.x & 31) == 0)
+        do {
+            v = atomicOr(ent, 0ull);
+        } while (uint32_t(v >> 32) != k);
+    return int(uint32_t(__shfl_sync(0xffffffffu, (unsigned long long)v, 0)));
 }
 __device__ __forceinline__ void tile_cur_enter(TileCur& c, int tiles_x) {
     c.bi = 0;
@@ -725,7 +723,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
             mbar_init(&sh.empty[s], kWsConsumers * 32);
         }
     }
-    if (threadIdx.x < kTq) sh.tq_seq[threadIdx.x] = 0xFFFFFFFFu;
+    if (threadIdx.x < kTq) sh.tq[threadIdx.x] = ~0ull;
     __syncthreads();
 
     if (warp >= kWsConsumers) {

@@ -102,31 +102,6 @@ int lodgs_camera_geom(const lodgs_camera* cam, double out44[44]) {
     });
 }
 
-int lodgs_camera_path_sample(const lodgs_camera* keyframes, uint32_t n_keyframes,
-                             const uint32_t* samples, lodgs_camera* out, uint64_t out_cap,
-                             uint64_t* n_frames) {
-    return guarded([&] {
-        need(keyframes, "keyframes");
-        if (n_keyframes > 1) need(samples, "samples");
-        const auto f = fgs::sample_path(keyframes, n_keyframes, samples);
-        if (n_frames) *n_frames = f.size();
-        if (out) {
-            if (out_cap < f.size()) throw fgs::Error(LODGS_ERR_VALIDATION, "camera path: capacity");
-            std::memcpy(out, f.data(), f.size() * sizeof(lodgs_camera));
-        }
-    });
-}
-
-int lodgs_build_synthetic_tree(const lodgs_synthetic_spec* spec, const lodgs_build_config* cfg,
-                               lodgs_tree_buffers* out, uint64_t* n_nodes, uint32_t* n_levels) {
-    return guarded([&] {
-        need(spec, "spec");
-        need(cfg, "cfg");
-        const uint64_t n = fgs::build_synthetic(*spec, *cfg, out, n_levels);
-        if (n_nodes) *n_nodes = n;
-    });
-}
-
 int lodgs_gpu_scene_create(const lodgs_tree_view* tree, int device, lodgs_gpu_scene** out) {
     return guarded([&] {
         need(tree, "tree");

@@ -72,6 +72,15 @@ struct __align__(16) GaussEmit {
     int16_t tx0, ty0, tx1, ty1;  // inclusive tile rect; tx1 < tx0 => no pairs
 };
 
+// Per-kernel device time of the filter (stage timing only): for kernel k, the
+// earliest CTA start (stored complemented, so a zeroed slot loses every
+// atomicMax) and the latest CTA end, %globaltimer ns.  Kernels: 0-3 the parallel
+// filter's F1-F4; serial filter: levels 0..kClockLevels-1, then its compaction.
+constexpr int kFilterClocks = 16;
+struct FilterClock {
+    unsigned long long t0n[kFilterClocks], t1[kFilterClocks];
+};
+
 // Device-resident per-frame counters (one cudaMemsetAsync clears them).
 struct FrameCounters {
     unsigned long long n_selected;
@@ -88,6 +97,7 @@ struct FrameCounters {
     // OR and OR-of-complement of every reference sort key (tile << 32 | depth bits,
     // rasterizer.cpp:111-115): digit d needs an LSD pass iff it is not uniform
     unsigned long long key_or, key_nand;
+    FilterClock clock;  // T_calcu / T_synch split of the filter (stage timing)
 };
 
 // Running totals across frames (not cleared per frame).
@@ -102,6 +112,18 @@ struct RunTotals {
 };
 
 #ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void clock_start(FilterClock* c, int k) {
+    if (c && threadIdx.x == 0) atomicMax(&c->t0n[k], ~global_ns());
+}
+__device__ __forceinline__ void clock_end(FilterClock* c, int k) {
+    if (c && threadIdx.x == 0) atomicMax(&c->t1[k], global_ns());
+}
+
 // std::max / std::min semantics (first argument NaN propagates), as the
 // reference relies on (mark_core.hpp:33,90,110).
 __device__ __forceinline__ double std_max(double a, double b) { return (a < b) ? b : a; }

@@ -288,9 +288,11 @@ __device__ __forceinline__ void decide_internal(const Geom& g, const GeomF& f, c
 // ballot.
 __global__ void __launch_bounds__(kMarkBlock, 3) k_mark_internal(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
-    const double tau_r, uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ qint_bits) {
+    const double tau_r, uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ qint_bits,
+    FilterClock* clk) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
+    clock_start(clk, 0);
     const unsigned lane = threadIdx.x & 31;
     const uint64_t end = t.leaf_begin;
     const uint64_t n_groups = (end + 31) / 32;
@@ -323,6 +325,7 @@ __global__ void __launch_bounds__(kMarkBlock, 3) k_mark_internal(
             qint_bits[grp] = qm;
         }
     }
+    clock_end(clk, 0);
 }
 
 // Survivor counts are kept per 8192-node tile (one count per k_compact CTA) and
@@ -350,9 +353,11 @@ __device__ __forceinline__ void count_survivors(uint32_t* tile_count, uint64_t n
 // result does not depend on the interleaving.
 __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
     uint32_t* __restrict__ cand_bits, uint32_t* qint_bits, const uint32_t* __restrict__ parent,
-    const uint64_t end, uint32_t* __restrict__ tile_count, const uint64_t n_tiles) {
+    const uint64_t end, uint32_t* __restrict__ tile_count, const uint64_t n_tiles,
+    FilterClock* clk) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
+    clock_start(clk, 1);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t warp_base =
         uint64_t(blockIdx.x) * (kSelectBlock * kSelectItems) + uint64_t(warp) * (32 * kSelectItems);
@@ -406,6 +411,7 @@ __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
 #pragma unroll
     for (int off = 4; off > 0; off >>= 1) cntw += __shfl_xor_sync(0xffffffffu, cntw, off);
     if (lane == 0 && cntw) count_survivors(tile_count, n_tiles, warp_base / kTileNodes, cntw);
+    clock_end(clk, 1);
 }
 
 // F3: the all-leaf suffix [leaf_begin, n).  A leaf is kept iff visible
@@ -421,9 +427,10 @@ __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
 __global__ void __launch_bounds__(256) k_filter_leaves(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const uint32_t* __restrict__ blk_bits, uint32_t* __restrict__ keep_bits,
-    uint32_t* __restrict__ tile_count) {
+    uint32_t* __restrict__ tile_count, FilterClock* clk) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
+    clock_start(clk, 2);
     const unsigned lane = threadIdx.x & 31;
     const uint64_t end = t.n;
     const uint64_t wbase = t.leaf_begin + (uint64_t(blockIdx.x) * 256 + (threadIdx.x & ~31u)) * 4;
@@ -467,6 +474,7 @@ __global__ void __launch_bounds__(256) k_filter_leaves(
     }
     // a warp's 128 leaves lie in one 8192-node tile (leaf_begin is a multiple of 1024)
     if (lane == 0 && c) count_survivors(tile_count, count_tiles(t.n), wbase / kTileNodes, c);
+    clock_end(clk, 2);
 }
 
 // F4: ordered compaction of the keep words into `selected` (strictly
@@ -479,9 +487,11 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ ke
                                                  const uint64_t n_words,
                                                  const uint32_t* __restrict__ tile_count,
                                                  uint32_t* __restrict__ selected,
-                                                 FrameCounters* cnt) {
+                                                 FrameCounters* cnt, FilterClock* clk,
+                                                 const int clock_slot) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
+    clock_start(clk, clock_slot);
     __shared__ unsigned s_red[8];
     __shared__ unsigned s_warp[8];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -526,6 +536,7 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ ke
         if ((word >> lane) & 1u)
             selected[pos + at + __popc(word & lt)] = uint32_t(warp_node + uint64_t(j) * 32 + lane);
     }
+    clock_end(clk, clock_slot);
 }
 
 // ---- serial (level-wise) filter, reference filter_serial (filter.cpp:60-113) --
@@ -542,7 +553,10 @@ __global__ void __launch_bounds__(256) k_serial_level(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const double tau_r, const uint64_t b, const uint64_t e, const int level,
     uint32_t* __restrict__ sel_bits, uint32_t* __restrict__ exp_bits,
-    uint32_t* __restrict__ tile_count, unsigned* level_flag, FrameCounters* cnt) {
+    uint32_t* __restrict__ tile_count, unsigned* level_flag, FrameCounters* cnt,
+    FilterClock* clk) {
+    const int slot = level < kFilterClocks - 1 ? level : kFilterClocks - 2;
+    clock_start(clk, slot);
     const unsigned lane = threadIdx.x & 31;
     const uint64_t i = (b & ~uint64_t(31)) + uint64_t(blockIdx.x) * 256 + threadIdx.x;
     bool sel = false, expand = false, active = false;
@@ -581,13 +595,14 @@ __global__ void __launch_bounds__(256) k_serial_level(
         if (am && !level_flag[level] && atomicOr(level_flag + level, 1u) == 0u)
             atomicAdd(&cnt->serial_passes, 1u);
     }
+    clock_end(clk, slot);
 }
 
 void launch_filter_serial(const Geom& g, const DevTree& t, double tau_r,
                           const uint64_t* level_begin, int n_levels, uint32_t* sel_bits,
                           uint32_t* exp_bits, uint32_t* tile_count, unsigned* level_flag,
                           uint32_t* selected, FrameCounters* cnt, cudaEvent_t* level_events,
-                          cudaStream_t s) {
+                          cudaStream_t s, FilterClock* clk) {
     if (t.n == 0) return;
     const GeomF f = make_geomf(g, tau_r, t.max_l1);
     cudaMemsetAsync(sel_bits, 0, ((t.n + 31) / 32) * 4, s);
@@ -598,11 +613,11 @@ void launch_filter_serial(const Geom& g, const DevTree& t, double tau_r,
         if (e <= b) continue;
         const uint64_t span = e - (b & ~uint64_t(31));
         k_serial_level<<<unsigned((span + 255) / 256), 256, 0, s>>>(
-            g, f, t, tau_r, b, e, l, sel_bits, exp_bits, tile_count, level_flag, cnt);
+            g, f, t, tau_r, b, e, l, sel_bits, exp_bits, tile_count, level_flag, cnt, clk);
     }
     if (level_events) cudaEventRecord(level_events[n_levels], s);
     k_compact<<<unsigned((t.n + kTileNodes - 1) / kTileNodes), 256, 0, s>>>(
-        sel_bits, (t.n + 31) / 32, tile_count, selected, cnt);
+        sel_bits, (t.n + 31) / 32, tile_count, selected, cnt, clk, kFilterClocks - 1);
 }
 
 // MarkFn contract (kernels.hpp:47-52): full mark_core per node, all outputs.
@@ -639,7 +654,7 @@ uint32_t filter_status_entries(uint64_t n) {
 
 void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
                    uint32_t* qint_bits, uint32_t* tile_count, uint32_t* selected,
-                   FrameCounters* cnt, cudaStream_t s, cudaEvent_t mid) {
+                   FrameCounters* cnt, cudaStream_t s, cudaEvent_t mid, FilterClock* clk) {
     if (t.n == 0) {
         if (mid) cudaEventRecord(mid, s);
         return;
@@ -649,18 +664,19 @@ void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand
     if (split > 0) {
         const uint64_t groups = (split + 31) / 32;
         const unsigned grid = unsigned(std::min<uint64_t>((groups + 7) / 8, uint64_t(sm_count()) * 3));
-        launch_pdl(k_mark_internal, grid, kMarkBlock, 0, s, g, f, t, tau_r, cand_bits, qint_bits);
+        launch_pdl(k_mark_internal, grid, kMarkBlock, 0, s, g, f, t, tau_r, cand_bits, qint_bits,
+                   clk);
         const uint64_t per = uint64_t(kSelectBlock) * kSelectItems;
         launch_pdl(k_select_internal, unsigned((split + per - 1) / per), kSelectBlock, 0, s,
-                   cand_bits, qint_bits, t.parent, split, tile_count, count_tiles(t.n));
+                   cand_bits, qint_bits, t.parent, split, tile_count, count_tiles(t.n), clk);
     }
     if (mid) cudaEventRecord(mid, s);
     if (t.n > split)
         launch_pdl(k_filter_leaves, unsigned((t.n - split + 1023) / 1024), 256, 0, s, g, f, t,
-                   static_cast<const uint32_t*>(qint_bits), cand_bits, tile_count);
+                   static_cast<const uint32_t*>(qint_bits), cand_bits, tile_count, clk);
     launch_pdl(k_compact, unsigned((t.n + kTileNodes - 1) / kTileNodes), 256, 0, s,
                static_cast<const uint32_t*>(cand_bits), (t.n + 31) / 32,
-               static_cast<const uint32_t*>(tile_count), selected, cnt);
+               static_cast<const uint32_t*>(tile_count), selected, cnt, clk, 3);
 }
 
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,

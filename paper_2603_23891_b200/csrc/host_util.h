@@ -32,10 +32,5 @@ std::string join_violations(const std::string& what, const std::vector<std::stri
 Geom camera_geom(const lodgs_camera& c);
 // metrics.cpp:136-154 SsimWindow: normalised 11x11 Gaussian, sigma 1.5
 void ssim_window(double w[121]);
-lodgs_camera interpolate(const lodgs_camera& a, const lodgs_camera& b, double t);
-std::vector<lodgs_camera> sample_path(const lodgs_camera* keys, uint32_t n_keys,
-                                      const uint32_t* samples);
-uint64_t build_synthetic(const lodgs_synthetic_spec& s, const lodgs_build_config& c,
-                         lodgs_tree_buffers* out, uint32_t* n_levels);
 
 }  // namespace fgs

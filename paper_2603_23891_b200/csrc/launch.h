@@ -49,9 +49,12 @@ inline uint32_t select_tiles(uint64_t n) {
 // The whole filter, four kernels: F1 internal marks, F2 internal chain walks,
 // F3 fused leaf pass, F4 ordered compaction into `selected` (n_selected lands
 // in cnt).  `mid` (optional) is recorded between F2 and F3.  tile_count: zeroed per frame, filter_status_entries(n) words.
+// clk (nullable): per-kernel device times (FrameCounters::clock) for the
+// T_calcu / T_synch split of the stage timers.
 void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
                    uint32_t* qint_bits, uint32_t* tile_count, uint32_t* selected,
-                   FrameCounters* cnt, cudaStream_t s, cudaEvent_t mid = nullptr);
+                   FrameCounters* cnt, cudaStream_t s, cudaEvent_t mid = nullptr,
+                   FilterClock* clk = nullptr);
 // Serial (level-wise) filter, filter.cpp:60-113: one kernel per level, then
 // the ordered compaction.  level_flag[n_levels] (zeroed) marks the levels with
 // an active node; level_events (nullable, n_levels + 1) time the levels.
@@ -59,7 +62,7 @@ void launch_filter_serial(const Geom& g, const DevTree& t, double tau_r,
                           const uint64_t* level_begin, int n_levels, uint32_t* sel_bits,
                           uint32_t* exp_bits, uint32_t* tile_count, unsigned* level_flag,
                           uint32_t* selected, FrameCounters* cnt, cudaEvent_t* level_events,
-                          cudaStream_t s);
+                          cudaStream_t s, FilterClock* clk = nullptr);
 // per-tile survivor counters the filter needs for an n-node tree
 uint32_t filter_status_entries(uint64_t n);
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,

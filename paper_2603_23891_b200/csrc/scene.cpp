@@ -529,12 +529,13 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
         FGS_CUDA(cudaMemsetAsync(level_flag_.p, 0, level_flag_.bytes(), stream_));
         launch_filter_serial(g, tree_, p.tau_r, level_begin_.data(), n_levels(), cand_bits_.p,
                              qint_bits_.p, reinterpret_cast<uint32_t*>(d_status_select_),
-                             level_flag_.p, selected_.p, d_counters_, nullptr, stream_);
+                             level_flag_.p, selected_.p, d_counters_, nullptr, stream_,
+                             timing ? &d_counters_->clock : nullptr);
         if (pe) FGS_CUDA(cudaEventRecord(pe[1], stream_));
     } else {
         launch_filter(g, tree_, p.tau_r, cand_bits_.p, qint_bits_.p,
                       reinterpret_cast<uint32_t*>(d_status_select_), selected_.p, d_counters_,
-                      stream_, pe ? pe[1] : nullptr);
+                      stream_, pe ? pe[1] : nullptr, timing ? &d_counters_->clock : nullptr);
     }
     last_serial_ = (p.flags & LODGS_RENDER_FILTER_SERIAL) != 0;
     if (timing) FGS_CUDA(cudaEventRecord(ev_[1], stream_));
@@ -632,8 +633,19 @@ void GpuScene::finish(lodgs_render_stats* stats) {
         if (last_timing_) {
             float ms = 0;
             FGS_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
-            stats->t_calc_ms = ms;
-            stats->t_sync_ms = 0.0;
+            // filter.cpp:95-96 / :144-145 split the filter into compute (T_calcu) and
+            // synchronisation (T_synch).  On the device the passes are kernels and the
+            // barriers are the kernel boundaries: T_calcu = the sum over the filter's
+            // kernels of first-CTA-start .. last-CTA-end (%globaltimer), T_synch = the
+            // rest of the filter's event-timed span (drain, launch and memset gaps).
+            double busy = 0.0;
+            for (int k = 0; k < kFilterClocks; ++k) {
+                const unsigned long long t0 = ~c.clock.t0n[k], t1 = c.clock.t1[k];
+                if (c.clock.t1[k] && t1 > t0) busy += double(t1 - t0) * 1e-6;
+            }
+            busy = std::min(busy, double(ms));
+            stats->t_calc_ms = busy;
+            stats->t_sync_ms = double(ms) - busy;
             FGS_CUDA(cudaEventElapsedTime(&ms, ev_[1], ev_[2]));
             stats->t_prepr_ms = ms;
             FGS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));

@@ -165,7 +165,6 @@ PAIR_DTYPE = np.dtype([("tile", "<u4"), ("depth", "<f4"), ("gaussian", "<u4")])
 ABI_SYMBOLS = (
     "lodgs_gpu_last_error", "lodgs_gpu_abi_version", "lodgs_gpu_device_count",
     "lodgs_validate_tree", "lodgs_validate_camera", "lodgs_camera_geom",
-    "lodgs_camera_path_sample", "lodgs_build_synthetic_tree",
     "lodgs_gpu_scene_create", "lodgs_gpu_scene_destroy", "lodgs_gpu_scene_stream",
     "lodgs_gpu_scene_reserve", "lodgs_gpu_scene_memory", "lodgs_gpu_render",
     "lodgs_gpu_render_batch",
@@ -203,11 +202,6 @@ def load_library():
         "lodgs_validate_tree": (C.c_int, [C.POINTER(TreeViewC), C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
         "lodgs_validate_camera": (C.c_int, [C.POINTER(CameraC), C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
         "lodgs_camera_geom": (C.c_int, [C.POINTER(CameraC), _DP]),
-        "lodgs_camera_path_sample": (C.c_int, [C.POINTER(CameraC), C.c_uint32, C.POINTER(C.c_uint32),
-                                               C.POINTER(CameraC), C.c_uint64, C.POINTER(C.c_uint64)]),
-        "lodgs_build_synthetic_tree": (C.c_int, [C.POINTER(SyntheticSpecC), C.POINTER(BuildConfigC),
-                                                 C.POINTER(TreeBuffersC), C.POINTER(C.c_uint64),
-                                                 C.POINTER(C.c_uint32)]),
         "lodgs_gpu_scene_create": (C.c_int, [C.POINTER(TreeViewC), C.c_int, C.POINTER(P)]),
         "lodgs_gpu_scene_destroy": (C.c_int, [P]),
         "lodgs_gpu_scene_stream": (C.c_int, [P, C.POINTER(P)]),
@@ -266,6 +260,41 @@ def load_library():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+SYNTH_PATH = os.path.join(_HERE, "_lib", "liblodgs_synth.so")
+SYNTH_SYMBOLS = ("lodgs_synth_last_error", "lodgs_camera_path_sample", "lodgs_build_synthetic_tree")
+_synth = None
+
+
+def load_synth_library():
+    """_lib/liblodgs_synth.so (include/lodgs_synth.h): benchmark INPUT generation -- the
+    reference's synthetic tree generator and CameraPath::sample restated -- kept out of
+    the renderer library."""
+    global _synth
+    if _synth is not None:
+        return _synth
+    if not os.path.exists(SYNTH_PATH):
+        raise ImportError(f"{SYNTH_PATH} is missing: run __graft_entry__.build()")
+    lib = C.CDLL(SYNTH_PATH)
+    lib.lodgs_synth_last_error.restype = C.c_char_p
+    lib.lodgs_synth_last_error.argtypes = []
+    lib.lodgs_camera_path_sample.restype = C.c_int
+    lib.lodgs_camera_path_sample.argtypes = [C.POINTER(CameraC), C.c_uint32, C.POINTER(C.c_uint32),
+                                             C.POINTER(CameraC), C.c_uint64, C.POINTER(C.c_uint64)]
+    lib.lodgs_build_synthetic_tree.restype = C.c_int
+    lib.lodgs_build_synthetic_tree.argtypes = [C.POINTER(SyntheticSpecC), C.POINTER(BuildConfigC),
+                                               C.POINTER(TreeBuffersC), C.POINTER(C.c_uint64),
+                                               C.POINTER(C.c_uint32)]
+    _synth = lib
+    return lib
+
+
+def _check_synth(rc: int):
+    if rc == 0:
+        return
+    msg = load_synth_library().lodgs_synth_last_error().decode(errors="replace")
+    raise (ValidationError if rc == 2 else InternalError)(msg)
 
 
 def _check(rc: int):
@@ -600,13 +629,13 @@ def camera_geom(cam: Camera) -> np.ndarray:
 
 def sample_camera_path(keyframes: Sequence[Camera], samples: Sequence[int]) -> list:
     """camera_path.cpp:132-142 CameraPath::sample."""
-    lib = load_library()
+    lib = load_synth_library()
     keys = (CameraC * len(keyframes))(*[k.to_c() for k in keyframes])
     smp = (C.c_uint32 * max(1, len(samples)))(*samples)
     n = C.c_uint64(0)
-    _check(lib.lodgs_camera_path_sample(keys, len(keyframes), smp, None, 0, C.byref(n)))
+    _check_synth(lib.lodgs_camera_path_sample(keys, len(keyframes), smp, None, 0, C.byref(n)))
     out = (CameraC * n.value)()
-    _check(lib.lodgs_camera_path_sample(keys, len(keyframes), smp, out, n.value, C.byref(n)))
+    _check_synth(lib.lodgs_camera_path_sample(keys, len(keyframes), smp, out, n.value, C.byref(n)))
     return [Camera.from_c(out[i]) for i in range(n.value)]
 
 
@@ -615,13 +644,13 @@ def build_synthetic_tree(nx=8, ny=8, spacing=2.0, scale_min=0.2, scale_max=0.6,
                          depth=3, shrink_factor=0.5, children_per_node=8,
                          build_seed=0) -> LoDTree:
     """build_tree(generate_synthetic_scene(spec), cfg) -- tree_builder.cpp:75-174."""
-    lib = load_library()
+    lib = load_synth_library()
     spec = SyntheticSpecC(nx, ny, spacing, scale_min, scale_max, opacity_min, opacity_max,
                           seed, congestion)
     cfg = BuildConfigC(depth, shrink_factor, children_per_node, build_seed)
     n = C.c_uint64(0)
     nl = C.c_uint32(0)
-    _check(lib.lodgs_build_synthetic_tree(C.byref(spec), C.byref(cfg), None, C.byref(n), C.byref(nl)))
+    _check_synth(lib.lodgs_build_synthetic_tree(C.byref(spec), C.byref(cfg), None, C.byref(n), C.byref(nl)))
     t = LoDTree.empty(n.value, nl.value, shrink_factor)
     b = TreeBuffersC()
     for f in _FIELDS:
@@ -629,7 +658,7 @@ def build_synthetic_tree(nx=8, ny=8, spacing=2.0, scale_min=0.2, scale_max=0.6,
     b.parent = t.parent.ctypes.data_as(C.POINTER(C.c_uint32))
     b.leaf = t.leaf.ctypes.data_as(C.POINTER(C.c_uint8))
     b.level_offsets = t.level_offsets.ctypes.data_as(C.POINTER(C.c_uint32))
-    _check(lib.lodgs_build_synthetic_tree(C.byref(spec), C.byref(cfg), C.byref(b), C.byref(n), C.byref(nl)))
+    _check_synth(lib.lodgs_build_synthetic_tree(C.byref(spec), C.byref(cfg), C.byref(b), C.byref(n), C.byref(nl)))
     return t
 
 

@@ -360,6 +360,13 @@ def test_abi_exports_every_declared_symbol(L):
         assert hasattr(lib, name), name
     assert declared == set(L.ABI_SYMBOLS)
     assert lib.lodgs_gpu_abi_version() == 1
+    # input generation (synthetic trees, camera paths) is a separate library
+    synth_h = open(os.path.join(ROOT, "include", "lodgs_synth.h")).read()
+    synth = set(re.findall(r"LODGS_API\s+(?:const\s+char\s*\*|int)\s*(lodgs_\w+)\s*\(", synth_h))
+    assert synth == set(L.SYNTH_SYMBOLS)
+    slib = L.load_synth_library()
+    for name in synth:
+        assert hasattr(slib, name) and not hasattr(lib, name), name
 
 
 def test_no_cpu_fallback_without_device(L):
@@ -414,8 +421,9 @@ def test_integration_shim_compiles_against_reference_headers(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     text = open(os.path.join(root, "INTEGRATION.md")).read()
     start = text.index("```cpp\n// proj/src/rasterizer_b200.cpp") + len("```cpp\n")
-    src = tmp_path / "rasterizer_b200.cpp"
-    src.write_text(text[start:text.index("```", start)])
+    src = os.path.join(root, "integration", "rasterizer_b200.cpp")
+    # the listing in INTEGRATION.md is the file that oracle/_ref/shim_check links and runs
+    assert text[start:text.index("```", start)] == open(src).read()
     r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", f"-I{ref_inc}",
                         f"-I{os.path.join(root, 'include')}", str(src)],
                        capture_output=True, text=True)
