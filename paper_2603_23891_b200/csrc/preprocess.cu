@@ -117,6 +117,9 @@ __device__ __forceinline__ uint32_t rect_count(const GaussEmit& e) {
     return (e.tx1 < e.tx0) ? 0u : uint32_t(e.tx1 - e.tx0 + 1) * uint32_t(e.ty1 - e.ty0 + 1);
 }
 
+#ifndef PREP_FP64_THR
+#define PREP_FP64_THR 0
+#endif
 // FP32 blend record from the FP64 gaussian (blend.cu explains ethr).
 __device__ __forceinline__ Gauss32 make_g32(double ca, double cb, double cc, double op, double r,
                                             double gg, double b) {
@@ -127,24 +130,40 @@ __device__ __forceinline__ Gauss32 make_g32(double ca, double cb, double cc, dou
     o.ha = float(0.5 * ca * kLog2e);
     o.cb = float(cb * kLog2e);
     o.hc = float(0.5 * cc * kLog2e);
-    const double ethr = log(255.0 * op);
-    o.ethr = float(ethr * kLog2e);
+    // The skip threshold in FP32, log2f(255 op) (<= 1 ulp; 255 op rounds once): the
+    // blend's certified margin carries a constant log2(e) 2^-17 = 1.1e-5 for the
+    // threshold's rounding, 20x the error here, so every FP32 decision it trusts is
+    // still the reference's.  (An FP64 log here was ~5 % of the kernel's issue.)
+#if PREP_FP64_THR  // experiment: the FP64 threshold and box of round 1
+    const double ethr64 = log(255.0 * op);
+    const float ethr2 = float(ethr64 * kLog2e);
+#else
+    const float ethr2 = log2f(255.0f * float(op));
+#endif
+    o.ethr = ethr2;
     o.op = float(op);
     o.r = float(r);
     o.g = float(gg);
     o.b = float(b);
-    // Box of the ellipse e <= E, E = ethr inflated past every rounding of the
-    // reference's own alpha test (exp_mx is within 1e-15 of exp): for the
-    // quadratic form [[ha, cb/2], [cb/2, hc]], |dx| <= sqrt(E hc / det) and
-    // |dy| <= sqrt(E ha / det).  Rounded outward, plus 1e-3 px for the FP32
-    // tile-local mean.  E <= 0 (opacity <= 1/255): nothing ever blends.
-    const double E = ethr + 1e-6 * (1.0 + fabs(ethr));
+    // Box of the ellipse e <= E, E the threshold inflated past every rounding of
+    // the FP32 threshold above and of the reference's own alpha test (exp_mx is
+    // within 1e-15 of exp): for the quadratic form [[ha, cb/2], [cb/2, hc]],
+    // |dx| <= sqrt(E hc / det) and |dy| <= sqrt(E ha / det).  det in FP64 (the
+    // cancellation), the rest in FP32 with directed rounding (inputs rounded up,
+    // det down, every operation rounded up), then 1e-3 px for the FP32 tile-local
+    // mean.  E <= 0 (opacity <= 1/255): nothing ever blends.
+    const double ethr = double(ethr2) * 0.69314718055994530942;
+    const double E = ethr + 1e-5 * (1.0 + fabs(ethr));
     const double ha = 0.5 * ca, hc = 0.5 * cc;
     const double det = ha * hc - 0.25 * cb * cb;
-    if (E > 0.0 && det > 0.0) {
-        o.hx = __double2float_ru(sqrt(E * hc / det) * (1.0 + 1e-9)) + 1e-3f;
-        o.hy = __double2float_ru(sqrt(E * ha / det) * (1.0 + 1e-9)) + 1e-3f;
-    } else if (E > 0.0) {  // degenerate conic: never cull
+    const float detf = __double2float_rd(det * (1.0 - 1e-9));
+    if (E > 0.0 && detf > 0.0f) {
+        const float Ef = __double2float_ru(E);
+        const float qx = __fdiv_ru(__fmul_ru(Ef, __double2float_ru(hc)), detf);
+        const float qy = __fdiv_ru(__fmul_ru(Ef, __double2float_ru(ha)), detf);
+        o.hx = __fadd_ru(__fsqrt_ru(qx), 1e-3f);
+        o.hy = __fadd_ru(__fsqrt_ru(qy), 1e-3f);
+    } else if (E > 0.0) {  // degenerate or tiny det: never cull
         o.hx = o.hy = 3.0e38f;
     } else {
         o.hx = o.hy = -1.0f;
@@ -357,6 +376,29 @@ __device__ __forceinline__ unsigned long long sort_bytes(const FrameCounters* cn
     return (24ull * unsigned(passes) + 8ull) * n_pairs;
 }
 
+// Running totals with fire-and-forget reductions: the counters are read once (one
+// round trip, the loads independent) and nothing waits on the RMWs.
+__device__ __forceinline__ void add_totals(RunTotals* totals, const FrameCounters* cnt,
+                                           unsigned long long total, bool ovf) {
+    const unsigned long long sel = cnt->n_selected;
+    const unsigned long long sb = ovf ? 0ull : sort_bytes(cnt, total);
+    atomicAdd(&totals->frames, 1ull);
+    atomicAdd(&totals->sum_selected, sel);
+    if (!ovf) atomicAdd(&totals->sum_pairs, total);
+    if (ovf) atomicOr(&totals->pad, 1ull);
+    if (sb) atomicAdd(&totals->sum_sort_bytes, sb);
+}
+
+// The frame's final counters into the batch log, one 8-byte word per thread.
+__device__ __forceinline__ void copy_counters(FrameCounters* log, const FrameCounters* cnt,
+                                              unsigned tid) {
+    constexpr unsigned kWords = sizeof(FrameCounters) / 8;
+    static_assert(sizeof(FrameCounters) % 8 == 0, "FrameCounters is a whole number of words");
+    if (tid < kWords)
+        reinterpret_cast<unsigned long long*>(log)[tid] =
+            reinterpret_cast<const volatile unsigned long long*>(cnt)[tid];
+}
+
 __device__ __forceinline__ int tile_class(uint32_t c, uint32_t mean) {
     // 0: >= 4x mean pairs, 1: >= 2x, 2: >= 1x, 3: lighter
     return c >= 4 * mean ? 0 : (c >= 2 * mean ? 1 : (c >= mean ? 2 : 3));
@@ -423,13 +465,7 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
     if (threadIdx.x == 0) {
         off[n_tiles] = ovf ? 0u : uint32_t(total);
         if (ovf) cnt->overflow = 1u;
-        if (totals) {
-            totals->frames += 1;
-            totals->sum_selected += cnt->n_selected;
-            totals->sum_pairs += ovf ? 0ull : total;
-            if (ovf) totals->pad = 1;
-            totals->sum_sort_bytes += ovf ? 0ull : sort_bytes(cnt, total);
-        }
+        if (totals) add_totals(totals, cnt, total, ovf);
     }
     __syncthreads();
     if (staged) {
@@ -495,7 +531,7 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
         for (int t = threadIdx.x; t < n_tiles; t += 1024) order[t] = ord[t];
     }
     __syncthreads();
-    if (log && threadIdx.x == 0) *log = *cnt;
+    if (log) copy_counters(log, cnt, threadIdx.x);
 }
 
 // Cluster variant for up to 8 x 12,288 tiles: the 8 CTAs of one thread-block
@@ -578,13 +614,7 @@ __global__ void __cluster_dims__(kOffCtas, 1, 1) __launch_bounds__(1024) k_tile_
     if (crank == 0 && threadIdx.x == 0) {
         if (n_tiles == 0) offsets[0] = 0u;
         if (ovf) cnt->overflow = 1u;
-        if (totals) {
-            totals->frames += 1;
-            totals->sum_selected += cnt->n_selected;
-            totals->sum_pairs += ovf ? 0ull : total;
-            if (ovf) totals->pad = 1;
-            totals->sum_sort_bytes += ovf ? 0ull : sort_bytes(cnt, total);
-        }
+        if (totals) add_totals(totals, cnt, total, ovf);
     }
     // heavy-first schedule (see k_tile_offsets): classes by count vs the mean
     const uint32_t mean = uint32_t(total / uint64_t(n_tiles > 0 ? n_tiles : 1)) + 1u;
@@ -646,7 +676,7 @@ __global__ void __cluster_dims__(kOffCtas, 1, 1) __launch_bounds__(1024) k_tile_
     cluster.sync();  // no CTA leaves while its shared memory may still be read
     // the frame's final counters into the batch log (no per-frame D2H on the
     // compute stream: a D2H there would queue behind the image copies)
-    if (log && crank == 0 && threadIdx.x == 0) *log = *cnt;
+    if (log && crank == 0) copy_counters(log, cnt, threadIdx.x);
 }
 
 void launch_tile_offsets(const uint32_t* tile_count, int n_tiles, uint32_t* offsets,
