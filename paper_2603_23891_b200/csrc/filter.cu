@@ -328,19 +328,18 @@ __global__ void __launch_bounds__(kMarkBlock, 3) k_mark_internal(
     clock_end(clk, 0);
 }
 
-// Survivor counts are kept per 8192-node tile (one count per k_compact CTA) and
-// per super-tile of 32 tiles (stored after the tile counts), so a compaction CTA
-// finds its output position from at most n/2^18 super-tile counts plus 31 tile
-// counts -- O(n) loads per frame in total, not O(n^2 / 8192^2).
+// Survivor counts are kept per 8192-node tile (one count per k_compact CTA).
+// A compaction CTA's output position is the sum of the preceding tiles' counts:
+// summed directly by the CTA up to kDirectPrefixTiles tiles (cfg 3: 1,226), and
+// above that (cfg 4: 6,121 tiles, where the direct sums are O(T^2) = 18.7M loads)
+// scanned once by k_tile_prefix between F3 and F4.
 constexpr int kTileNodes = 8192;
-constexpr int kSuperTiles = 32;
+constexpr uint64_t kDirectPrefixTiles = 2048;
 __host__ __device__ inline uint64_t count_tiles(uint64_t n) {
     return (n + kTileNodes - 1) / kTileNodes;
 }
-__device__ __forceinline__ void count_survivors(uint32_t* tile_count, uint64_t n_tiles,
-                                                uint64_t tile, uint32_t c) {
+__device__ __forceinline__ void count_survivors(uint32_t* tile_count, uint64_t tile, uint32_t c) {
     atomicAdd(tile_count + tile, c);
-    atomicAdd(tile_count + n_tiles + tile / kSuperTiles, c);
 }
 
 // F2: internal region.  Every node walks its parent chain (filter.cpp:20-25)
@@ -353,8 +352,7 @@ __device__ __forceinline__ void count_survivors(uint32_t* tile_count, uint64_t n
 // result does not depend on the interleaving.
 __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
     uint32_t* __restrict__ cand_bits, uint32_t* qint_bits, const uint32_t* __restrict__ parent,
-    const uint64_t end, uint32_t* __restrict__ tile_count, const uint64_t n_tiles,
-    FilterClock* clk) {
+    const uint64_t end, uint32_t* __restrict__ tile_count, FilterClock* clk) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
     clock_start(clk, 1);
@@ -410,7 +408,7 @@ __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
     }
 #pragma unroll
     for (int off = 4; off > 0; off >>= 1) cntw += __shfl_xor_sync(0xffffffffu, cntw, off);
-    if (lane == 0 && cntw) count_survivors(tile_count, n_tiles, warp_base / kTileNodes, cntw);
+    if (lane == 0 && cntw) count_survivors(tile_count, warp_base / kTileNodes, cntw);
     clock_end(clk, 1);
 }
 
@@ -473,8 +471,47 @@ __global__ void __launch_bounds__(256) k_filter_leaves(
         c += __popc(w);
     }
     // a warp's 128 leaves lie in one 8192-node tile (leaf_begin is a multiple of 1024)
-    if (lane == 0 && c) count_survivors(tile_count, count_tiles(t.n), wbase / kTileNodes, c);
+    if (lane == 0 && c) count_survivors(tile_count, wbase / kTileNodes, c);
     clock_end(clk, 2);
+}
+
+// Exclusive scan of the per-tile survivor counts (large trees only): one CTA,
+// thread k owning a contiguous run of tiles.
+__global__ void __launch_bounds__(1024) k_tile_prefix(const uint32_t* __restrict__ tile_count,
+                                                      const uint32_t n_tiles,
+                                                      uint32_t* __restrict__ prefix) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ uint32_t s_warp[32];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t per = (n_tiles + 1023) / 1024;
+    const uint32_t t0 = min(n_tiles, threadIdx.x * per), t1 = min(n_tiles, t0 + per);
+    uint32_t sum = 0;
+    for (uint32_t t = t0; t < t1; ++t) sum += tile_count[t];
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= unsigned(o)) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t v = s_warp[lane];
+        uint32_t wi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= unsigned(o)) wi += u;
+        }
+        s_warp[lane] = wi - v;  // exclusive over warps
+    }
+    __syncthreads();
+    uint32_t run = s_warp[warp] + (incl - sum);
+    for (uint32_t t = t0; t < t1; ++t) {
+        prefix[t] = run;
+        run += tile_count[t];
+    }
 }
 
 // F4: ordered compaction of the keep words into `selected` (strictly
@@ -488,7 +525,8 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ ke
                                                  const uint32_t* __restrict__ tile_count,
                                                  uint32_t* __restrict__ selected,
                                                  FrameCounters* cnt, FilterClock* clk,
-                                                 const int clock_slot) {
+                                                 const int clock_slot,
+                                                 const uint32_t* __restrict__ prefix) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
     clock_start(clk, clock_slot);
@@ -496,12 +534,20 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ ke
     __shared__ unsigned s_warp[8];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned tile = blockIdx.x;
-    // survivors before this tile: whole super-tiles, then the tiles of its own
-    const uint32_t* super_count = tile_count + gridDim.x;
-    const unsigned sup = tile / kSuperTiles;
+    // survivors before this tile: scanned by k_tile_prefix, or summed here
     unsigned pre = 0;
-    for (unsigned k = threadIdx.x; k < sup; k += 256) pre += __ldg(super_count + k);
-    if (threadIdx.x < tile - sup * kSuperTiles) pre += __ldg(tile_count + sup * kSuperTiles + threadIdx.x);
+    if (prefix) {
+        if (threadIdx.x == 0) pre = __ldg(prefix + tile);
+    } else {
+        unsigned p4[4] = {0u, 0u, 0u, 0u};
+        unsigned k = threadIdx.x;
+        for (; k + 768 < tile; k += 1024) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p4[u] += __ldg(tile_count + k + 256 * u);
+        }
+        for (; k < tile; k += 256) p4[0] += __ldg(tile_count + k);
+        pre = (p4[0] + p4[1]) + (p4[2] + p4[3]);
+    }
     const uint64_t wi = uint64_t(tile) * (kTileNodes / 32) + warp * 32 + lane;
     const uint32_t keepw = wi < n_words ? __ldg(keep_bits + wi) : 0u;
     unsigned c = __popc(keepw);
@@ -591,7 +637,7 @@ __global__ void __launch_bounds__(256) k_serial_level(
             if (sm) atomicOr(sel_bits + w, sm);
             if (em) atomicOr(exp_bits + w, em);
         }
-        if (sm) count_survivors(tile_count, count_tiles(t.n), i / kTileNodes, __popc(sm));
+        if (sm) count_survivors(tile_count, i / kTileNodes, __popc(sm));
         if (am && !level_flag[level] && atomicOr(level_flag + level, 1u) == 0u)
             atomicAdd(&cnt->serial_passes, 1u);
     }
@@ -616,8 +662,11 @@ void launch_filter_serial(const Geom& g, const DevTree& t, double tau_r,
             g, f, t, tau_r, b, e, l, sel_bits, exp_bits, tile_count, level_flag, cnt, clk);
     }
     if (level_events) cudaEventRecord(level_events[n_levels], s);
-    k_compact<<<unsigned((t.n + kTileNodes - 1) / kTileNodes), 256, 0, s>>>(
-        sel_bits, (t.n + 31) / 32, tile_count, selected, cnt, clk, kFilterClocks - 1);
+    const uint64_t T = count_tiles(t.n);
+    uint32_t* prefix = T > kDirectPrefixTiles ? tile_count + T : nullptr;
+    if (prefix) k_tile_prefix<<<1, 1024, 0, s>>>(tile_count, uint32_t(T), prefix);
+    k_compact<<<unsigned(T), 256, 0, s>>>(sel_bits, (t.n + 31) / 32, tile_count, selected, cnt,
+                                          clk, kFilterClocks - 1, prefix);
 }
 
 // MarkFn contract (kernels.hpp:47-52): full mark_core per node, all outputs.
@@ -649,8 +698,10 @@ static int sm_count() {
 
 uint32_t filter_status_entries(uint64_t n) {
     const uint64_t t = count_tiles(n);
-    return uint32_t(t + (t + kSuperTiles - 1) / kSuperTiles + 1);
+    return uint32_t(2 * t + 1);  // counts, then (large trees) their exclusive prefix
 }
+
+int filter_launches(uint64_t n) { return count_tiles(n) > kDirectPrefixTiles ? 5 : 4; }
 
 void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand_bits,
                    uint32_t* qint_bits, uint32_t* tile_count, uint32_t* selected,
@@ -668,15 +719,20 @@ void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand
                    clk);
         const uint64_t per = uint64_t(kSelectBlock) * kSelectItems;
         launch_pdl(k_select_internal, unsigned((split + per - 1) / per), kSelectBlock, 0, s,
-                   cand_bits, qint_bits, t.parent, split, tile_count, count_tiles(t.n), clk);
+                   cand_bits, qint_bits, t.parent, split, tile_count, clk);
     }
     if (mid) cudaEventRecord(mid, s);
     if (t.n > split)
         launch_pdl(k_filter_leaves, unsigned((t.n - split + 1023) / 1024), 256, 0, s, g, f, t,
                    static_cast<const uint32_t*>(qint_bits), cand_bits, tile_count, clk);
-    launch_pdl(k_compact, unsigned((t.n + kTileNodes - 1) / kTileNodes), 256, 0, s,
-               static_cast<const uint32_t*>(cand_bits), (t.n + 31) / 32,
-               static_cast<const uint32_t*>(tile_count), selected, cnt, clk, 3);
+    const uint64_t T = count_tiles(t.n);
+    uint32_t* prefix = T > kDirectPrefixTiles ? tile_count + T : nullptr;
+    if (prefix)
+        launch_pdl(k_tile_prefix, 1, 1024, 0, s, static_cast<const uint32_t*>(tile_count),
+                   uint32_t(T), prefix);
+    launch_pdl(k_compact, unsigned(T), 256, 0, s, static_cast<const uint32_t*>(cand_bits),
+               (t.n + 31) / 32, static_cast<const uint32_t*>(tile_count), selected, cnt, clk, 3,
+               static_cast<const uint32_t*>(prefix));
 }
 
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,

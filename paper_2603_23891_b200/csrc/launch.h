@@ -33,10 +33,10 @@ struct DevTree {
 };
 
 // ---- filter (filter.cpp:115-150) ----
-// kernels enqueued per frame: zero, mark internal, select internal, filter
-// leaves, compact, preprocess, tile offsets (+ run totals), emit, tile sort,
-// big-tile sort, then blend_launches() for the blend
-constexpr int kLaunchesPerFrame = 10;
+// kernels enqueued per frame besides the filter's filter_launches(n): zero,
+// preprocess, tile offsets (+ run totals), emit, tile sort, big-tile sort, then
+// blend_launches() for the blend
+constexpr int kLaunchesPerFrame = 6;
 constexpr int kMarkBlock = 256;
 constexpr int kSelectBlock = 256;
 constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles
@@ -65,6 +65,8 @@ void launch_filter_serial(const Geom& g, const DevTree& t, double tau_r,
                           cudaStream_t s, FilterClock* clk = nullptr);
 // per-tile survivor counters the filter needs for an n-node tree
 uint32_t filter_status_entries(uint64_t n);
+// kernels launch_filter enqueues for an n-node tree (4, or 5 with the tile-count scan)
+int filter_launches(uint64_t n);
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,
                        double tau_r, uint8_t* vis, uint8_t* qpass, double* radius,
                        cudaStream_t s);

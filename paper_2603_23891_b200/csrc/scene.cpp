@@ -629,7 +629,7 @@ void GpuScene::finish(lodgs_render_stats* stats) {
         stats->filter_barriers = stats->filter_passes;
         stats->big_tiles = c.big_tiles;
         stats->kernel_launches =
-            last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() - 4 + n_levels() + 1) : kLaunchesPerFrame + blend_launches();
+            last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() + n_levels() + filter_launches(tree_.n) - 3) : kLaunchesPerFrame + blend_launches() + filter_launches(tree_.n);
         if (last_timing_) {
             float ms = 0;
             FGS_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
@@ -772,8 +772,8 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
             s.filter_passes = last_serial_ ? int32_t(c.serial_passes) : 2;
             s.filter_barriers = s.filter_passes;
             s.big_tiles = c.big_tiles;
-            s.kernel_launches = last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() - 4 + n_levels() + 1)
-                                             : kLaunchesPerFrame + blend_launches();
+            s.kernel_launches = last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() + n_levels() + filter_launches(tree_.n) - 3)
+                                             : kLaunchesPerFrame + blend_launches() + filter_launches(tree_.n);
         }
     }
 }

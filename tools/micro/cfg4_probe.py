@@ -19,7 +19,8 @@ with L.GpuScene(tree) as s:
                            L.RenderOptions(stage_timing=True))
         st = out.stats
         print(f"alt {alt}: sel {st.n_selected} pairs {st.n_pairs} big {st.big_tiles} "
-              f"filter {st.t_calc_ms:.3f} prep {st.t_prepr_ms:.3f} sort {st.t_sort_ms:.3f} "
+              f"filter {st.t_calc_ms + st.t_sync_ms:.3f} (calc {st.t_calc_ms:.3f} sync "
+              f"{st.t_sync_ms:.3f}) prep {st.t_prepr_ms:.3f} sort {st.t_sort_ms:.3f} "
               f"blend {st.t_alpha_ms:.3f} ms", flush=True)
 
     # tile-size distribution of the lowest frame: what the big-bucket sort sees
