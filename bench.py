@@ -350,6 +350,20 @@ def run_b200(args, rank, world, local):
     # kernels, one frame in flight: the stage split, not the throughput)
     _, _, (pf, stage_ms) = device_loop(timed, profile=True)
 
+    # the TMA-staged blend kernels, same frames, same loop: evidence
+    # for the kernel choice, not the headline
+    variants = {}
+    default_params = params
+    for name, flag in (("blend_tma", 64), ("blend_gather4", 128)):
+        params = L.RenderParamsC(TAU_R, 0.0, 0, flag)
+        for cam in warm:
+            scene.render_async(cam, params)
+        scene.sync()
+        vms, _, _ = device_loop(timed)
+        vmax, _ = reduce_timing(dist, vms, [], device="cuda")
+        variants[name] = world * K / (vmax / 1000.0)
+    params = default_params
+
     # ---- e2e through the public C ABI with host buffers (pinned ring of 4 images)
     img_bytes = W * H * 3 * 4
     ring = []
@@ -485,6 +499,7 @@ def run_b200(args, rank, world, local):
         "mean_selected": mean_sel, "mean_pairs": mean_pairs,
         "stage_ms_per_frame": per_stage,
         "roofline": roofline, "stages": stages, "blend": blend,
+        "blend_kernel_variants_fps": {"blend_wsp (default)": fps, **variants},
         "e2e": {"value": world * K / e2e_max, "unit": "frames/s",
                 "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": img_bytes + 64,
                 "frames": K, "call": "lodgs_gpu_render_batch (pipelined over frames in flight)",

@@ -84,8 +84,15 @@ enum lodgs_render_flags {
     LODGS_RENDER_STAGE_TIMING = 4u, /* CUDA-event stage timers into lodgs_render_stats */
     LODGS_RENDER_COLLECT_KPC = 8u,  /* RenderOptions::collect_kpc: per-pair kpc, exact blend */
     LODGS_RENDER_FILTER_SERIAL = 16u, /* RenderOptions::filter_mode = serial (filter.cpp:60-113) */
-    LODGS_RENDER_OUTPUT_RGB8 = 32u  /* render_batch: host images are W*H*3 bytes, save_ppm's
-                                       quantisation (image.cpp:19-22), 1/4 of the PCIe bytes */
+    LODGS_RENDER_OUTPUT_RGB8 = 32u, /* host images are W*H*3 bytes, save_ppm's quantisation
+                                       (image.cpp:19-22), 1/4 of the PCIe bytes */
+    /* Fast-blend kernel (all certified-identical).  Default: k_blend_wsp,
+     * cp.async producer warps (fastest measured on the BASELINE configs). */
+    LODGS_RENDER_BLEND_TMA = 64u,   /* k_blend_tma: the sort writes a 48 B record per pair,
+                                       each tile's records stream into shared memory with
+                                       cp.async.bulk (TMA) */
+    LODGS_RENDER_BLEND_GATHER4 = 128u /* k_blend_g4: TMA tile::gather4 of the slot-indexed
+                                         records, no record pass */
 };
 
 /* FilterConfig (filter.hpp:11-14) + ShrinkMode (rasterizer.hpp:16-24). */

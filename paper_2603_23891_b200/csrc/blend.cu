@@ -1692,27 +1692,18 @@ void launch_view_gtc(const uint32_t* offsets, int n_tiles, const double* kpc, ui
     if (n_pairs) k_kpc_histogram<<<148, 256, 0, s>>>(kpc, n_pairs, bins);
 }
 
-// Fast-blend kernel (all three certified-identical; the numbers are DESIGN.md's):
-//   0  k_blend_wsp -- producer warps gather records with cp.async (default: fastest
-//      measured, the blend is bound by its per-sample arithmetic, not by staging)
-//   1  k_blend_g4  -- TMA tile::gather4 of the slot-indexed records (TMA row-rate bound)
-//   2  k_blend_tma -- the sort writes per-pair records, cp.async.bulk streams them
-#ifndef BLEND_TMA
-#define BLEND_TMA 0
-#endif
-// per-pair record buffer bytes the fast blend needs (only the pack + bulk variant)
-uint64_t blend_record_bytes() { return BLEND_TMA == 2 ? sizeof(BlendRec) : 0; }
-// kernels the fast blend launches per frame
+uint64_t blend_record_bytes() { return sizeof(BlendRec); }
 int blend_launches() { return 1; }
 
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,
-                  unsigned* ticket, void* records, uint64_t n_records, bool records_packed) {
+                  unsigned* ticket, void* records, uint64_t n_records, bool records_packed,
+                  int kernel) {
     const int n_tiles = tiles_x * tiles_y;
     if (n_tiles <= 0) return;
     CUtensorMap m32, m64;
-    if (BLEND_TMA == 1 && !exact && ticket && n_records &&
+    if (kernel == kBlendGather4 && !exact && ticket && n_records &&
         encode_record_maps(g32, g64, n_records, &m32, &m64)) {
         const int smem = int(sizeof(G4Shared));
         static std::mutex mu;
@@ -1738,7 +1729,7 @@ void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned
                    width, height, tiles_x, uint32_t(n_tiles), ticket, image);
         return;
     }
-    if (BLEND_TMA == 2 && !exact && records && ticket) {
+    if (kernel == kBlendTma && !exact && records && ticket) {
         BlendRec* rec = static_cast<BlendRec*>(records);
         if (!records_packed)  // the frame's sort writes them; stage entry points pack here
             launch_pdl(k_pack_blend, n_tiles, 128, 0, s, offsets, keys, g64, g32, tiles_x, rec);

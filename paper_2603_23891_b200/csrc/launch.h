@@ -126,16 +126,17 @@ void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
                           cudaStream_t s, RecOut ro = {}, int tiles_x = 1);
 
 // ---- blend (rasterizer.cpp:137-165, blend_scalar.cpp:13-55) ----
-// Fast path (BLEND_TMA=1, default) with `ticket` and n_records (rows of g32/g64):
-// k_blend_g4 gathers every tile's records into shared memory with TMA gather4.
-// BLEND_TMA=2 (experiment): K6a packs each sorted pair's record at its pair index
-// into `records` (blend_record_bytes() per pair), K6b streams them with
-// cp.async.bulk.  BLEND_TMA=0: the warp-specialised gather kernel (k_blend_wsp).
+// Fast-blend kernels (certified-identical): kBlendWsp (default,
+// cp.async producer warps), kBlendTma (`records` holds blend_record_bytes() per
+// pair written by the sort when records_packed, else by a pack pass here; each
+// tile's records stream into shared memory with cp.async.bulk), kBlendGather4
+// (TMA tile::gather4 of the n_records slot-indexed g32/g64 rows).
+enum BlendKernel { kBlendWsp = 0, kBlendTma = 1, kBlendGather4 = 2 };
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,
                   unsigned* ticket = nullptr, void* records = nullptr, uint64_t n_records = 0,
-                  bool records_packed = false);
+                  bool records_packed = false, int kernel = kBlendWsp);
 uint64_t blend_record_bytes();
 int blend_launches();
 

@@ -439,8 +439,10 @@ void GpuScene::reserve_pairs(uint64_t n) {
     if (stream_) FGS_CUDA(cudaStreamSynchronize(stream_));
     keys_.release();
     keys_.alloc(n);
-    blend_rec_.release();
-    if (blend_record_bytes()) blend_rec_.alloc(n * blend_record_bytes());
+    if (blend_rec_.p) {  // the TMA blend's per-pair records, once that kernel has been used
+        blend_rec_.release();
+        blend_rec_.alloc(n * blend_record_bytes());
+    }
     pair_cap_ = n;
 }
 
@@ -555,8 +557,15 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     maps_valid_ = false;
     if (timing) FGS_CUDA(cudaEventRecord(ev_[2], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[3], stream_));
-    // the fast blend's per-pair records are written by the sort, next to each key
-    const RecOut ro{(!exact && blend_rec_.p) ? reinterpret_cast<BlendRec*>(blend_rec_.p) : nullptr,
+    // fast-blend kernel (LODGS_RENDER_BLEND_*); the TMA one reads per-pair records that
+    // the sort writes next to each key
+    const int bk = (p.flags & LODGS_RENDER_BLEND_GATHER4) ? kBlendGather4
+                   : (p.flags & LODGS_RENDER_BLEND_TMA)   ? kBlendTma
+                                                           : kBlendWsp;
+    if (bk == kBlendTma && !exact && blend_rec_.n < pair_cap_ * blend_record_bytes())
+        blend_rec_.alloc(pair_cap_ * blend_record_bytes());
+    const RecOut ro{(bk == kBlendTma && !exact) ? reinterpret_cast<BlendRec*>(blend_rec_.p)
+                                                 : nullptr,
                     g64_.p, g32_.p};
     launch_tile_sort(res_.tile_offsets.p, res_.tile_order.p, n_tiles, keys_.p, stream_, ro,
                      res_.tiles_x);
@@ -571,7 +580,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     } else {
         launch_blend(res_.tile_offsets.p, res_.tile_order.p, keys_.p, g64_.p, g32_.p, col64_.p,
                      res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact, img_out, stream_,
-                     &d_counters_->blend_ticket, blend_rec_.p, g32_.n, ro.rec != nullptr);
+                     &d_counters_->blend_ticket, blend_rec_.p, g32_.n, ro.rec != nullptr, bk);
     }
     if (timing) FGS_CUDA(cudaEventRecord(ev_[4], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[5], stream_));
@@ -1362,10 +1371,13 @@ void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_bl
     launch_bucket_triples(tri.p, n, tc, c.s);
     launch_tile_offsets(tc, n_tiles, off.p, cur.p, big.p, ord.p, cnt, n, c.s);
     launch_triples_to_keys(tri.p, n, keys.p, c.s);
+    const int bk = (flags & LODGS_RENDER_BLEND_GATHER4) ? kBlendGather4
+                   : (flags & LODGS_RENDER_BLEND_TMA)   ? kBlendTma
+                                                         : kBlendWsp;
     DevBuf<unsigned char> rec;
-    if (blend_record_bytes()) rec.alloc(n * blend_record_bytes());
+    if (bk == kBlendTma) rec.alloc(n * blend_record_bytes());
     launch_blend(off.p, ord.p, keys.p, dl.g64.p, dl.g32.p, dl.col64.p, width, height, tiles_x,
-                 tiles_y, exact, img.p, c.s, &cnt->blend_ticket, rec.p, dl.g32.n);
+                 tiles_y, exact, img.p, c.s, &cnt->blend_ticket, rec.p, dl.g32.n, false, bk);
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaMemcpyAsync(image, img.p, img.n * 4, cudaMemcpyDeviceToHost, c.s));
     FGS_CUDA(cudaStreamSynchronize(c.s));

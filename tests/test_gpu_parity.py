@@ -475,6 +475,10 @@ def test_blend_micro_scenes(L, oracle, gpu):
         assert ex.tobytes() == want.tobytes(), rep
         fa = L.alpha_blend(pairs, bl, grid, w, h, exact=False).rgb
         assert max_abs(fa, want) <= IMG_TOL, rep
+        # the TMA-staged kernels run the same certified per-sample code: same image
+        for k in ("tma", "gather4"):
+            fk = L.alpha_blend(pairs, bl, grid, w, h, blend_kernel=k).rgb
+            assert fk.tobytes() == fa.tobytes(), (rep, k)
 
 
 def test_blend_needle_splats(L, oracle, gpu):
@@ -514,6 +518,8 @@ def test_blend_needle_splats(L, oracle, gpu):
         assert ex.tobytes() == want.tobytes(), rep
         fa = L.alpha_blend(pairs, bl, grid, w, h, exact=False).rgb
         assert max_abs(fa, want) <= IMG_TOL, (rep, max_abs(fa, want))
+        for k in ("tma", "gather4"):
+            assert L.alpha_blend(pairs, bl, grid, w, h, blend_kernel=k).rgb.tobytes() == fa.tobytes()
 
 
 # ---------------------------------------------------------------- render --

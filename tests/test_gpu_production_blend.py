@@ -95,6 +95,27 @@ def cfg3(L, ref, gpu):
     ref.free_tree(rh)
 
 
+def test_cfg3_bench_frames_tma_kernels(L, cfg3):
+    """The TMA-staged blend kernels (LODGS_RENDER_BLEND_TMA / _GATHER4) on
+    the driver's strided bench frames, four in flight: images byte-identical to the
+    default kernel's (all three run the same certified per-sample code)."""
+    b, tree, rh, cams, scene = cfg3
+    from paper_2603_23891_b200.sharding import strided_frames
+
+    frames = [cams[i] for i in strided_frames(len(cams), 0, 1, 20)]
+    mode = L.ShrinkMode.three_sigma()
+    base = _async_frames(L, scene, frames, b.TAU_R, mode)
+    for k in ("tma", "gather4"):
+        scene.set_inflight(4)
+        p = scene.params(L.FilterConfig(b.TAU_R), mode, L.RenderOptions(blend_kernel=k))
+        imgs = [np.empty((c.height, c.width, 3), np.float32) for c in frames]
+        for cam, im in zip(frames, imgs):
+            scene.render_async(cam, p, im.ctypes.data)
+        scene.sync()
+        for i, (im, bi) in enumerate(zip(imgs, base)):
+            assert im.tobytes() == bi.tobytes(), (k, i)
+
+
 def test_cfg3_bench_frames_async_and_batch(L, ref, cfg3):
     """The frames the driver's `bench.py --steps 20` times (strided over the whole
     300-frame path), through render_async (4 in flight) and render_batch: every image
