@@ -475,10 +475,11 @@ def test_blend_micro_scenes(L, oracle, gpu):
         assert ex.tobytes() == want.tobytes(), rep
         fa = L.alpha_blend(pairs, bl, grid, w, h, exact=False).rgb
         assert max_abs(fa, want) <= IMG_TOL, rep
-        # the TMA-staged kernels run the same certified per-sample code: same image
+        # the TMA-staged kernels (same certified per-sample code; k_blend_tma rounds the
+        # mean tile-relative instead of block-relative, so its last bits may differ)
         for k in ("tma", "gather4"):
             fk = L.alpha_blend(pairs, bl, grid, w, h, blend_kernel=k).rgb
-            assert fk.tobytes() == fa.tobytes(), (rep, k)
+            assert max_abs(fk, want) <= IMG_TOL, (rep, k)
 
 
 def test_blend_needle_splats(L, oracle, gpu):
@@ -519,7 +520,8 @@ def test_blend_needle_splats(L, oracle, gpu):
         fa = L.alpha_blend(pairs, bl, grid, w, h, exact=False).rgb
         assert max_abs(fa, want) <= IMG_TOL, (rep, max_abs(fa, want))
         for k in ("tma", "gather4"):
-            assert L.alpha_blend(pairs, bl, grid, w, h, blend_kernel=k).rgb.tobytes() == fa.tobytes()
+            fk = L.alpha_blend(pairs, bl, grid, w, h, blend_kernel=k).rgb
+            assert max_abs(fk, want) <= IMG_TOL, (rep, k, max_abs(fk, want))
 
 
 # ---------------------------------------------------------------- render --

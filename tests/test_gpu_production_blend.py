@@ -35,10 +35,12 @@ def _bench():
     return bench
 
 
-def _compare(ref, rh, cam, tau_r, mode, img, st, what):
-    want = ref.render(rh, cam, tau_r, mode, workers=THREADS)
-    assert st.n_selected == want["n_selected"], what
-    assert st.n_pairs == want["n_pairs"], what
+def _compare(ref, rh, cam, tau_r, mode, img, st, what, want=None):
+    if want is None:
+        want = ref.render(rh, cam, tau_r, mode, workers=THREADS)
+    if st is not None:
+        assert st.n_selected == want["n_selected"], what
+        assert st.n_pairs == want["n_pairs"], what
     err = max_abs(img, want["image"])
     psnr = ref.psnr(img, want["image"]) if err > 0 else float("inf")
     assert err <= IMG_TOL, (what, err)
@@ -46,10 +48,10 @@ def _compare(ref, rh, cam, tau_r, mode, img, st, what):
     return want, err, psnr
 
 
-def _async_frames(L, scene, cams, tau_r, mode):
+def _async_frames(L, scene, cams, tau_r, mode, blend_kernel="wsp"):
     """Four frames in flight (render_async), every image to its own host buffer."""
     scene.set_inflight(4)
-    p = scene.params(L.FilterConfig(tau_r), mode, L.RenderOptions())
+    p = scene.params(L.FilterConfig(tau_r), mode, L.RenderOptions(blend_kernel=blend_kernel))
     imgs = [np.empty((c.height, c.width, 3), np.float32) for c in cams]
     for cam, im in zip(cams, imgs):
         scene.render_async(cam, p, im.ctypes.data)
@@ -95,31 +97,11 @@ def cfg3(L, ref, gpu):
     ref.free_tree(rh)
 
 
-def test_cfg3_bench_frames_tma_kernels(L, cfg3):
-    """The TMA-staged blend kernels (LODGS_RENDER_BLEND_TMA / _GATHER4) on
-    the driver's strided bench frames, four in flight: images byte-identical to the
-    default kernel's (all three run the same certified per-sample code)."""
-    b, tree, rh, cams, scene = cfg3
-    from paper_2603_23891_b200.sharding import strided_frames
-
-    frames = [cams[i] for i in strided_frames(len(cams), 0, 1, 20)]
-    mode = L.ShrinkMode.three_sigma()
-    base = _async_frames(L, scene, frames, b.TAU_R, mode)
-    for k in ("tma", "gather4"):
-        scene.set_inflight(4)
-        p = scene.params(L.FilterConfig(b.TAU_R), mode, L.RenderOptions(blend_kernel=k))
-        imgs = [np.empty((c.height, c.width, 3), np.float32) for c in frames]
-        for cam, im in zip(frames, imgs):
-            scene.render_async(cam, p, im.ctypes.data)
-        scene.sync()
-        for i, (im, bi) in enumerate(zip(imgs, base)):
-            assert im.tobytes() == bi.tobytes(), (k, i)
-
-
 def test_cfg3_bench_frames_async_and_batch(L, ref, cfg3):
     """The frames the driver's `bench.py --steps 20` times (strided over the whole
     300-frame path), through render_async (4 in flight) and render_batch: every image
-    against the reference renderer's."""
+    against the reference renderer's; then the same frames with the TMA-staged blend
+    kernels (LODGS_RENDER_BLEND_TMA / _GATHER4) against the same images."""
     b, tree, rh, cams, scene = cfg3
     from paper_2603_23891_b200.sharding import strided_frames
 
@@ -129,11 +111,17 @@ def test_cfg3_bench_frames_async_and_batch(L, ref, cfg3):
     a_imgs = _async_frames(L, scene, frames, b.TAU_R, mode)
     b_imgs, b_stats = _batch_frames(L, scene, frames, b.TAU_R, mode)
     worst = 0.0
+    wants = []
     for i, cam, ai, bi, st in zip(idx, frames, a_imgs, b_imgs, b_stats):
-        _, err, _ = _compare(ref, rh, cam, b.TAU_R, mode, bi, st, f"batch frame {i}")
+        want, err, _ = _compare(ref, rh, cam, b.TAU_R, mode, bi, st, f"batch frame {i}")
         assert ai.tobytes() == bi.tobytes(), f"async frame {i} differs from the batch frame"
         worst = max(worst, err)
+        wants.append(want)
     print(f"cfg3 bench frames: worst max-abs {worst:.3g}")
+    for k in ("tma", "gather4"):
+        imgs = _async_frames(L, scene, frames, b.TAU_R, mode, blend_kernel=k)
+        for i, cam, im, want in zip(idx, frames, imgs, wants):
+            _compare(ref, rh, cam, b.TAU_R, mode, im, None, f"{k} frame {i}", want=want)
 
 
 def test_cfg3_altitudes_and_oblique_keyframes(L, ref, cfg3):
