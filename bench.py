@@ -175,7 +175,7 @@ STAGE_KERNELS = {
     "preprocess": ("k_preprocess",),
     "keys": ("k_tile_offsets_cluster", "k_tile_offsets", "k_emit_keys"),
     "sort": ("k_tile_sort", "k_tile_sort_big"),
-    "blend": ("k_blend_wsp", "k_blend_tma", "k_blend_ws"),
+    "blend": ("k_blend_wsp", "k_blend_tma", "k_blend_ws", "k_blend_cpa", "k_blend_g4"),
 }
 
 
@@ -354,7 +354,7 @@ def run_b200(args, rank, world, local):
     # for the kernel choice, not the headline
     variants = {}
     default_params = params
-    for name, flag in (("blend_tma", 64), ("blend_gather4", 128)):
+    for name, flag in (("blend_wsp", 512), ("blend_tma", 64), ("blend_gather4", 128)):
         params = L.RenderParamsC(TAU_R, 0.0, 0, flag)
         for cam in warm:
             scene.render_async(cam, params)
@@ -482,10 +482,10 @@ def run_b200(args, rank, world, local):
                 "traffic_source": (f"ncu dram__bytes_read+write over the bench's own frames "
                                    f"({os.path.relpath(NCU_FRAMES, ROOT)})" if prof else None),
                 "algorithmic_bytes_per_frame": filt_bytes, "dominant_stage": dominant}
-    blend = {"kernel": "k_blend_wsp", "bound": "issue", "ms_per_frame": per_stage["blend"],
+    blend = {"kernel": "k_blend_cpa", "bound": "issue", "ms_per_frame": per_stage["blend"],
              "share_of_frame": per_stage["blend"] / max(1e-9, sum(per_stage.values()))}
-    if prof and "k_blend_wsp" in prof.get("kernels", {}):
-        kb = prof["kernels"]["k_blend_wsp"]
+    if prof and "k_blend_cpa" in prof.get("kernels", {}):
+        kb = prof["kernels"]["k_blend_cpa"]
         blend.update({k: kb[k] for k in ("issue_pct", "sm_pct", "occ_pct") if k in kb})
     e2e_h2d = C.sizeof(L.CameraC) + C.sizeof(L.RenderParamsC)
     line = {
@@ -499,7 +499,7 @@ def run_b200(args, rank, world, local):
         "mean_selected": mean_sel, "mean_pairs": mean_pairs,
         "stage_ms_per_frame": per_stage,
         "roofline": roofline, "stages": stages, "blend": blend,
-        "blend_kernel_variants_fps": {"blend_wsp (default)": fps, **variants},
+        "blend_kernel_variants_fps": {"blend_cpa (default)": fps, **variants},
         "e2e": {"value": world * K / e2e_max, "unit": "frames/s",
                 "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": img_bytes + 64,
                 "frames": K, "call": "lodgs_gpu_render_batch (pipelined over frames in flight)",

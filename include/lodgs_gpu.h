@@ -86,13 +86,19 @@ enum lodgs_render_flags {
     LODGS_RENDER_FILTER_SERIAL = 16u, /* RenderOptions::filter_mode = serial (filter.cpp:60-113) */
     LODGS_RENDER_OUTPUT_RGB8 = 32u, /* host images are W*H*3 bytes, save_ppm's quantisation
                                        (image.cpp:19-22), 1/4 of the PCIe bytes */
-    /* Fast-blend kernel (all certified-identical).  Default: k_blend_wsp,
-     * cp.async producer warps (fastest measured on the BASELINE configs). */
+    /* Fast-blend kernel (all certified-identical).  Default (no flag):
+     * k_blend_cpa, the fastest measured on the BASELINE configs. */
     LODGS_RENDER_BLEND_TMA = 64u,   /* k_blend_tma: the sort writes a 48 B record per pair,
                                        each tile's records stream into shared memory with
                                        cp.async.bulk (TMA) */
-    LODGS_RENDER_BLEND_GATHER4 = 128u /* k_blend_g4: TMA tile::gather4 of the slot-indexed
-                                         records, no record pass */
+    LODGS_RENDER_BLEND_GATHER4 = 128u, /* k_blend_g4: TMA tile::gather4 of the slot-indexed
+                                          records, no record pass */
+    LODGS_RENDER_BLEND_CPA = 256u, /* k_blend_cpa (the default): one producer warp streams
+                                      the records with per-lane cp.async into a 20-stage ring,
+                                      the 8 consumer warps cull against their 8x4 blocks */
+    LODGS_RENDER_BLEND_WSP = 512u  /* k_blend_wsp (round-1 default): two producer warps
+                                      gather, cull and hand per-block hit lists over a
+                                      5-stage ring */
 };
 
 /* FilterConfig (filter.hpp:11-14) + ShrinkMode (rasterizer.hpp:16-24). */

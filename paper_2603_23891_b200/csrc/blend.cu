@@ -1428,6 +1428,318 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
     }
 }
 
+// ---------------------------------------------------------------------------
+// cp.async-staged blend (K6, the default fast kernel).  k_blend_g4's structure -- one producer warp,
+// eight consumer warps that cull and compact their own hits -- with the
+// records gathered by per-lane cp.async instead of TMA gather4 (whose row
+// rate bounds k_blend_g4).  The producer only moves bytes: per 32-pair chunk
+// it issues four cp.async per lane (the splat's FP64 mean, the FP32 conic +
+// threshold, opacity + colour, alpha box: 56 B) straight into the stage and
+// lets the copies themselves complete the stage's `full` barrier
+// (cp.async.mbarrier.arrive.noinc), so it never waits for data and can run
+// kCpaStages chunks ahead -- the deep look-ahead that k_blend_wsp could not
+// afford with its 11 KB per-block stages (2 KB per stage here).  Keys are
+// loaded kCpaAhead chunks before their gathers are issued.  Consumers run
+// k_blend_g4's cull/compact + the certified per-sample code of k_blend_ws
+// (same block-relative FP32 means, so the pixels equal k_blend_wsp's).
+// Tuning (cfg-3 path, 100 strided frames, four in flight; tools/variants.sh):
+// stages 8 / 12 / 16 / 20 / 22 / 24: 3,410 / 3,459 / 3,442 / 3,520 / 3,493 / 3,443
+// frames/s (24 no longer fits 4 CTAs per SM); key look-ahead 2 / 3 / 5: 3,469 / 3,437 /
+// 3,323; 3 / 4 / 5 CTAs per SM (72 / 56 / 40 registers): 3,379 / 3,459 / 3,364;
+// cp.async.cg (L2 only) vs .ca: 3,459 vs 3,421; a 500 ns suspend hint on the
+// consumers' waits: 3,448.
+#ifndef CPA_STAGES
+#define CPA_STAGES 20
+#endif
+#ifndef CPA_AHEAD
+#define CPA_AHEAD 2
+#endif
+#ifndef CPA_MIN_CTAS
+#define CPA_MIN_CTAS 4
+#endif
+#ifndef CPA_CONS_HINT
+#define CPA_CONS_HINT 0
+#endif
+#ifndef CPA_CG
+#define CPA_CG 1
+#endif
+// 1: the copies complete the stage themselves (cp.async.mbarrier.arrive.noinc);
+// 0: the producer publishes stage i - kCpaLag after cp.async.wait_group (lagged).
+// Both are racecheck-clean; 1 is faster (3,517 vs 3,461 frames/s, lag 3 / 6 / 10 alike).
+#ifndef CPA_ASYNC_ARRIVE
+#define CPA_ASYNC_ARRIVE 1
+#endif
+#ifndef CPA_LAG
+#define CPA_LAG 6
+#endif
+constexpr int kCpaLag = CPA_LAG;
+constexpr int kCpaStages = CPA_STAGES;
+constexpr int kCpaAhead = CPA_AHEAD;
+constexpr int kCpaThreads = (kTmaConsumers + 1) * 32;
+static_assert(kCpaStages < kDoneRing, "a tile has >= 1 stage");
+static_assert(kCpaLag < kCpaStages, "a stage is published before the producer waits for its reuse");
+
+struct CpaStage {
+    double2 m[32];   // Gauss64 (mx, my)
+    float4 q0[32];   // Gauss32 (ha, cb, hc, ethr)
+    float4 col[32];  // Gauss32 (op, r, g, b)
+    float2 h[32];    // Gauss32 (hx, hy)
+    uint32_t slot[32];
+};
+struct CpaShared {
+    CpaStage st[kCpaStages];
+    WarpStage wl[kTmaConsumers];
+    TmaHdr hdr[kCpaStages];
+    unsigned long long full[kCpaStages], empty[kCpaStages];
+    uint32_t done[kDoneRing];
+};
+
+// the stage barrier counts this thread's arrival once all its earlier
+// cp.async copies have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* b) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(b))
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
+    const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
+    const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
+    const uint32_t n_tiles, unsigned* ticket, float* __restrict__ image) {
+    pdl_wait();  // the sort (and everything before it) is complete and visible
+    pdl_trigger();
+    extern __shared__ __align__(128) unsigned char cpa_raw[];
+    CpaShared& sh = *reinterpret_cast<CpaShared*>(cpa_raw);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kCpaStages; ++s) {
+            mbar_init(&sh.full[s], CPA_ASYNC_ARRIVE ? 33 : 32);  // + the header's arrive
+            mbar_init(&sh.empty[s], kTmaConsumers * 32);  // every consumer lane
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kTmaConsumers) {
+        // ---------------- producer warp ----------------
+        auto take = [&]() -> uint32_t { return lane == 0 ? atomicAdd(ticket, 1u) : 0u; };
+        auto tile_of = [&](uint32_t raw) -> int {
+            const uint32_t t = __shfl_sync(0xffffffffu, raw, 0);
+            return t < n_tiles ? int(__ldg(order + t)) : -1;
+        };
+        int cur = tile_of(take());
+        uint32_t cb = cur >= 0 ? offsets[cur] : 0u, ce = cur >= 0 ? offsets[cur + 1] : 0u;
+        int nxt = tile_of(take());
+        uint32_t nb = nxt >= 0 ? offsets[nxt] : 0u, ne = nxt >= 0 ? offsets[nxt + 1] : 0u;
+        int t2 = tile_of(take());
+        uint32_t raw3 = take();
+        uint32_t gc = cb, gk = 0;
+        auto gen = [&]() -> G4Chunk {
+            G4Chunk ch;
+            ch.tile = cur;
+            ch.k = gk;
+            if (cur < 0) {
+                ch.n = 0;
+                ch.last = true;
+                ch.slot = 0;
+                return ch;
+            }
+            ch.n = gc < ce ? min(32u, ce - gc) : 0u;
+            ch.last = gc + 32u >= ce;
+            ch.slot = lane < ch.n ? uint32_t(keys[gc + lane]) : 0xFFFFFFFFu;
+            if (ch.last) {
+                cur = nxt;
+                cb = nb;
+                ce = ne;
+                nxt = t2;
+                nb = nxt >= 0 ? offsets[nxt] : 0u;
+                ne = nxt >= 0 ? offsets[nxt + 1] : 0u;
+                t2 = tile_of(raw3);
+                raw3 = take();
+                gc = cb;
+                ++gk;
+            } else {
+                gc += 32u;
+            }
+            return ch;
+        };
+        // Chunk FIFO in registers, kCpaAhead deep.  The loop body is unrolled over the
+        // FIFO slots so an entry is never copied between registers: a copy of a key whose
+        // load is still in flight would stall the warp on it (one chunk of look-ahead).
+        G4Chunk fifo[kCpaAhead];
+#pragma unroll
+        for (int j = 0; j < kCpaAhead; ++j) fifo[j] = gen();
+        uint32_t i = 0;
+        uint32_t killed = 0xFFFFFFFFu;
+        bool first_chunk = true;
+        bool finished = false;
+        while (!finished) {
+#pragma unroll
+        for (int jf = 0; jf < kCpaAhead; ++jf) {
+            if (finished) break;
+            const G4Chunk ch = fifo[jf];
+            fifo[jf] = gen();
+            if (ch.tile >= 0 && ch.k == killed) continue;  // rest of a terminated tile
+            const int s = int(i % kCpaStages);
+            if (i >= uint32_t(kCpaStages))
+                mbar_wait_hint<TMA_PROD_HINT>(&sh.empty[s], ((i / kCpaStages) - 1) & 1u);
+            ++i;
+            if (ch.tile < 0) {  // the CTA's work is done
+                if (lane == 0) sh.hdr[s] = TmaHdr{0, 0, 0u, 2u};
+#if CPA_ASYNC_ARRIVE
+                __syncwarp();
+                cp_async_mbar_arrive(&sh.full[s]);
+                if (lane == 0) mbar_arrive(&sh.full[s]);
+#else
+                // publish the stages still in flight, then this one
+                cp_async_wait<0>();
+                for (uint32_t q = i - 1 > uint32_t(kCpaLag) ? i - 1 - uint32_t(kCpaLag) : 0u;
+                     q < i; ++q)
+                    mbar_arrive(&sh.full[q % kCpaStages]);
+#endif
+                finished = true;
+                continue;
+            }
+            // the tile's terminated-warp counter: lane 0 alone touches it (the consumers
+            // bump it with shared atomics), the verdict is broadcast
+            bool last = ch.last;
+            {
+                uint32_t kill = 0u;
+                if (lane == 0) {
+                    if (first_chunk) atomicExch(&sh.done[ch.k % kDoneRing], ch.k << 4);
+                    else if (!last) kill = atomicOr(&sh.done[ch.k % kDoneRing], 0u) == ((ch.k << 4) | 8u);
+                }
+                if (__shfl_sync(0xffffffffu, kill, 0)) {
+                    last = true;
+                    killed = ch.k;
+                }
+            }
+            CpaStage& st = sh.st[s];
+            if (lane < ch.n) {
+                const uint32_t gi = ch.slot;
+#if CPA_CG  // L2 only: a record is read by one tile's CTA (and rarely reused in L1)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(&st.m[lane])),
+                             "l"(&g64[gi].mx) : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(&st.q0[lane])),
+                             "l"(&g32[gi].ha) : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(&st.col[lane])),
+                             "l"(&g32[gi].op) : "memory");
+#else
+                cp_async16(&st.m[lane], &g64[gi].mx);
+                cp_async16(&st.q0[lane], &g32[gi].ha);
+                cp_async16(&st.col[lane], &g32[gi].op);
+#endif
+                cp_async8(&st.h[lane], &g32[gi].hx);
+            }
+            st.slot[lane] = ch.slot;
+            if (lane == 0) {
+                const int tx0 = (ch.tile % tiles_x) * kTile, ty0 = (ch.tile / tiles_x) * kTile;
+                sh.hdr[s] = TmaHdr{tx0, ty0, ch.n, last ? 1u : 0u};
+            }
+#if CPA_ASYNC_ARRIVE
+            __syncwarp();
+            cp_async_mbar_arrive(&sh.full[s]);
+            if (lane == 0) mbar_arrive(&sh.full[s]);
+#else
+            // publish stage i - kCpaLag: its copies (this lane's) have landed; every lane
+            // arrives for its own copies and stores (release), which compute-sanitizer's
+            // racecheck can follow (it does not model cp.async-triggered arrivals)
+            cp_async_commit();
+            if (i > uint32_t(kCpaLag)) {
+                cp_async_wait<kCpaLag>();
+                mbar_arrive(&sh.full[(i - 1 - uint32_t(kCpaLag)) % kCpaStages]);
+            }
+#endif
+            first_chunk = last;
+        }
+        }
+        cp_async_wait<0>();  // no copy may land after the CTA retires
+        return;
+    }
+
+    // ---------------- consumers: warp w owns the 8x4 block (w & 1, w >> 1) ----
+    WarpStage& wl = sh.wl[warp];
+    const float pxl = float(lane & 7) + 0.5f, pyl = float(lane >> 3) + 0.5f;  // block-relative
+    const int bxo = int(warp & 1) * 8, byo = int(warp >> 1) * 4;
+    PixState pix{0.0f, 0.0f, 0.0f, 0.0f};
+    bool fresh = true, counted = false;
+    int bx = 0, by = 0;
+    uint32_t k = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint32_t i = 0;; ++i) {
+        const int s = int(i % kCpaStages);
+        mbar_wait_hint<CPA_CONS_HINT>(&sh.full[s], (i / kCpaStages) & 1u);
+        const TmaHdr hd = sh.hdr[s];
+        if (hd.flags & 2u) break;
+        if (fresh) {
+            bx = hd.x0 + bxo;
+            by = hd.y0 + byo;
+            const int x = bx + int(lane & 7), y = by + int(lane >> 3);
+            pix = PixState{(x < width && y < height) ? 1.0f : 0.0f, 0.0f, 0.0f, 0.0f};
+            fresh = false;
+            counted = false;
+        }
+        const CpaStage& st = sh.st[s];
+        bool hit = false;
+        float mlx = 0.f, mly = 0.f;
+        if (lane < hd.n && !counted) {
+            const float2 h = st.h[lane];
+            if (h.x >= 0.0f) {
+                const double2 m = st.m[lane];
+                mlx = float(m.x - double(bx));
+                mly = float(m.y - double(by));
+                hit = mlx - h.x <= 7.5f && mlx + h.x >= 0.5f && mly - h.y <= 3.5f &&
+                      mly + h.y >= 0.5f;
+            }
+        }
+        const unsigned bits = __ballot_sync(0xffffffffu, hit);
+        if (bits) {
+            if (hit) {
+                const int at = __popc(bits & lt);
+                const float4 q0 = st.q0[lane];
+                const float4 col = st.col[lane];
+                wl.geo[at] = make_float4(mlx, mly, q0.x, q0.z);
+                wl.ct[at] = make_float4(q0.y, q0.w, col.x, col.y);
+                wl.gb[at] = make_float2(col.z, col.w);
+                wl.gid[at] = st.slot[lane];
+            }
+            __syncwarp();
+            const PixState saved = pix;
+            bool unsure = false;
+            const int nh = __popc(bits);
+            int kk = 0;
+            for (; kk + 2 <= nh; kk += 2) {
+                blend_sample_fast(wl, kk, pxl, pyl, pix, unsure);
+                blend_sample_fast(wl, kk + 1, pxl, pyl, pix, unsure);
+            }
+            if (kk < nh) blend_sample_fast(wl, kk, pxl, pyl, pix, unsure);
+            if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
+                pix = saved;
+                const double px = double(bx + int(lane & 7)) + 0.5;
+                const double py = double(by + int(lane >> 3)) + 0.5;
+                for (int j = 0; j < nh; ++j) blend_sample_checked(wl, j, pxl, pyl, px, py, g64, pix);
+            }
+        }
+        // every lane releases its own reads of the stage (one warp instruction)
+        mbar_arrive(&sh.empty[s]);
+        if (!counted && __all_sync(0xffffffffu, pix.T == 0.0f)) {
+            counted = true;
+            if (lane == 0) atomicAdd(&sh.done[k % kDoneRing], 1u);
+        }
+        if (hd.flags & 1u) {
+            const int x = bx + int(lane & 7), y = by + int(lane >> 3);
+            if (x < width && y < height) {
+                float* o = image + (size_t(y) * width + x) * 3;
+                o[0] = pix.cr;
+                o[1] = pix.cg;
+                o[2] = pix.cb;
+            }
+            fresh = true;
+            ++k;
+        }
+    }
+}
+
 // Tensor maps of the slot-indexed records for gather4: Gauss32 rows (12 floats)
 // and the first 4 doubles of the Gauss64 rows; boxes of one row, 4 rows per gather.
 static bool encode_record_maps(const Gauss32* g32, const Gauss64* g64, uint64_t rows,
@@ -1727,6 +2039,31 @@ void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned
         grid = std::min(n_tiles, grid);
         launch_pdl(k_blend_g4, grid, kG4Threads, smem, s, offsets, order, keys, m32, m64, g64,
                    width, height, tiles_x, uint32_t(n_tiles), ticket, image);
+        return;
+    }
+    if (kernel == kBlendCpa && !exact && ticket) {
+        const int smem = int(sizeof(CpaShared));
+        static std::mutex mu;
+        static int grid_of[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int grid = 0;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            if (dev < 0 || dev >= 64 || !grid_of[dev]) {
+                cudaFuncSetAttribute(k_blend_cpa, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                int per_sm = 0, n_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blend_cpa, kCpaThreads, smem);
+                cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+                grid = std::max(1, per_sm) * std::max(1, n_sm);
+                if (dev >= 0 && dev < 64) grid_of[dev] = grid;
+            } else {
+                grid = grid_of[dev];
+            }
+        }
+        grid = std::min(n_tiles, grid);
+        launch_pdl(k_blend_cpa, grid, kCpaThreads, smem, s, offsets, order, keys, g64, g32, width,
+                   height, tiles_x, uint32_t(n_tiles), ticket, image);
         return;
     }
     if (kernel == kBlendTma && !exact && records && ticket) {

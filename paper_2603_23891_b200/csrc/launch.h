@@ -131,7 +131,7 @@ void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
 // pair written by the sort when records_packed, else by a pack pass here; each
 // tile's records stream into shared memory with cp.async.bulk), kBlendGather4
 // (TMA tile::gather4 of the n_records slot-indexed g32/g64 rows).
-enum BlendKernel { kBlendWsp = 0, kBlendTma = 1, kBlendGather4 = 2 };
+enum BlendKernel { kBlendWsp = 0, kBlendTma = 1, kBlendGather4 = 2, kBlendCpa = 3 };
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,

@@ -17,6 +17,12 @@
 #include <memory>
 #include <mutex>
 
+// fast-blend kernel of a frame without a LODGS_RENDER_BLEND_* flag (experiment builds
+// override it)
+#ifndef FGS_DEFAULT_BLEND
+#define FGS_DEFAULT_BLEND kBlendCpa
+#endif
+
 namespace fgs {
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -561,7 +567,9 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     // the sort writes next to each key
     const int bk = (p.flags & LODGS_RENDER_BLEND_GATHER4) ? kBlendGather4
                    : (p.flags & LODGS_RENDER_BLEND_TMA)   ? kBlendTma
-                                                           : kBlendWsp;
+                   : (p.flags & LODGS_RENDER_BLEND_CPA)   ? kBlendCpa
+                   : (p.flags & LODGS_RENDER_BLEND_WSP)   ? kBlendWsp
+                                                           : FGS_DEFAULT_BLEND;
     if (bk == kBlendTma && !exact && blend_rec_.n < pair_cap_ * blend_record_bytes())
         blend_rec_.alloc(pair_cap_ * blend_record_bytes());
     const RecOut ro{(bk == kBlendTma && !exact) ? reinterpret_cast<BlendRec*>(blend_rec_.p)
@@ -1373,7 +1381,9 @@ void stage_alpha_blend(const lodgs_tile_pair* sorted, uint64_t n, const lodgs_bl
     launch_triples_to_keys(tri.p, n, keys.p, c.s);
     const int bk = (flags & LODGS_RENDER_BLEND_GATHER4) ? kBlendGather4
                    : (flags & LODGS_RENDER_BLEND_TMA)   ? kBlendTma
-                                                         : kBlendWsp;
+                   : (flags & LODGS_RENDER_BLEND_CPA)   ? kBlendCpa
+                   : (flags & LODGS_RENDER_BLEND_WSP)   ? kBlendWsp
+                                                         : FGS_DEFAULT_BLEND;
     DevBuf<unsigned char> rec;
     if (bk == kBlendTma) rec.alloc(n * blend_record_bytes());
     launch_blend(off.p, ord.p, keys.p, dl.g64.p, dl.g32.p, dl.col64.p, width, height, tiles_x,

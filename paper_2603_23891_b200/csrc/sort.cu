@@ -196,6 +196,31 @@ __device__ __forceinline__ void register_bitonic(const unsigned long long* keys,
     }
 }
 
+// Odd-even transposition over s_out[0, n) until no adjacent pair is out of
+// order: moves keys only inside runs of equal depth (the input is sorted by
+// depth), which puts ties into slot order -- the reference's stable order.
+template <class Bar>
+__device__ __forceinline__ void oddeven_fix(unsigned long long* s_out, uint32_t n, uint32_t tid,
+                                            Bar bar) {
+    while (true) {
+        bool swapped = false;
+#pragma unroll
+        for (int ph = 0; ph < 2; ++ph) {
+            for (uint32_t p = tid; 2 * p + ph + 1 < n; p += kSmallSortThreads) {
+                const uint32_t a = 2 * p + ph;
+                const unsigned long long x = s_out[a], y = s_out[a + 1];
+                if (y < x) {
+                    s_out[a] = y;
+                    s_out[a + 1] = x;
+                    swapped = true;
+                }
+            }
+            bar.sync();
+        }
+        if (!bar.sync_or(swapped)) break;
+    }
+}
+
 // 32-bit variant of the register network for buckets whose depth bits span
 // less than 2^20 (a tile's splats sit in a narrow depth band): key32 =
 // (depth_bits - min) << 12 | position in the bucket.  Half the shuffles, one
@@ -311,30 +336,156 @@ __device__ __forceinline__ bool register_bitonic32(const unsigned long long* key
         if (tid < lanes && i < n) s_out[i] = s_orig[k32[r] & 0xFFFu];
     }
     bar.sync();
-    // odd-even transposition inside runs of equal depth: (depth, slot) order
-    while (true) {
-        bool swapped = false;
-#pragma unroll
-        for (int ph = 0; ph < 2; ++ph) {
-            for (uint32_t p = tid; 2 * p + ph + 1 < n; p += kSmallSortThreads) {
-                const uint32_t a = 2 * p + ph;
-                const unsigned long long x = s_out[a], y = s_out[a + 1];
-                if (y < x) {
-                    s_out[a] = y;
-                    s_out[a + 1] = x;
-                    swapped = true;
-                }
-            }
-            bar.sync();
-        }
-        if (!bar.sync_or(swapped)) break;
-    }
+    oddeven_fix(s_out, n, tid, bar);  // runs of equal depth into slot order
     if (dst)
         for (uint32_t i = tid; i < n; i += kSmallSortThreads) {
             dst[i] = s_out[i];
             if (site) site->put(i, s_out[i]);
         }
     return true;
+}
+
+// LSD radix sort of one bucket (n <= 256 R keys) by depth: the remaining
+// digits of the reference's (tile, depth) radix sort (rasterizer.cpp:100-135)
+// once the tile digit has been resolved by counting (k_emit_keys).  Digits are
+// taken from depth_bits - min over the bucket, only as many as its depth range
+// spans (a tile's splats sit in a narrow band: typically 2-3 passes), at most
+// 8 bits each; every pass is stable, so equal depths keep their bucket order
+// and oddeven_fix then puts them into slot order.
+// Warp w holds the 32 R consecutive positions [32 R w, 32 R (w + 1)), lane l
+// position 32 R w + 32 r + l of round r.  A key's rank: the count of its digit
+// in the warp's earlier rounds (one shared counter per (warp, digit), bumped
+// by the lowest lane of each __match_any_sync group) + its rank in the group;
+// one CTA-wide exclusive scan over (digit, warp) turns the counters into
+// destinations.  Shared memory (s, 32 KB): two key buffers of 1024 and two
+// counter arrays [8][256] (alternating passes, the idle one zeroed during the
+// scan).  The sorted bucket goes to dst (global) and, for the TMA blend, its
+// records through `site`.
+template <int R>
+__device__ __forceinline__ void radix_bucket(const unsigned long long* __restrict__ keys,
+                                             uint32_t n, unsigned long long* dst,
+                                             unsigned long long* s, uint32_t* s_red, uint32_t tid,
+                                             const RecSite* site) {
+    static_assert(R >= 1 && 32 * R * (kSmallSortThreads / 32) <= 1024, "1024 keys at most");
+    constexpr uint32_t kSeg = 32u * R;
+    constexpr int kWarps = kSmallSortThreads / 32;
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(s + 2048);  // [2][kWarps][256]
+    unsigned long long v[R];
+    uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t p = kSeg * warp + 32u * r + lane;
+        v[r] = p < n ? keys[p] : ~0ull;
+        if (p < n) {
+            const uint32_t d = uint32_t(v[r] >> 32);
+            dmin = min(dmin, d);
+            dmax = max(dmax, d);
+        }
+    }
+    for (uint32_t j = tid; j < 2u * kWarps * 256u; j += kSmallSortThreads) cnt[j] = 0u;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        dmin = min(dmin, __shfl_xor_sync(0xffffffffu, dmin, off));
+        dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+    }
+    if (lane == 0) {
+        s_red[warp] = dmin;
+        s_red[kWarps + warp] = dmax;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        dmin = min(dmin, s_red[w]);
+        dmax = max(dmax, s_red[kWarps + w]);
+    }
+    const uint32_t range = dmax - dmin;
+    const int nbits = range ? 32 - __clz(range) : 0;
+    const int passes = (nbits + 7) >> 3;
+    const int width = passes ? (nbits + passes - 1) / passes : 0;
+    const uint32_t mask = (1u << width) - 1u, bins = 1u << width;
+    unsigned long long* out = s;
+    __syncthreads();  // s_red is reused by the scans
+    for (int ps = 0; ps < passes; ++ps) {
+        uint32_t* c = cnt + (ps & 1) * (kWarps * 256);
+        const int shift = ps * width;
+        uint32_t dig[R], rank[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t p = kSeg * warp + 32u * r + lane;
+            const bool ok = p < n;
+            // lanes past n get a private digit: never in anyone's group
+            const uint32_t d = ok ? ((uint32_t(v[r] >> 32) - dmin) >> shift) & mask : 256u + lane;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t below = __popc(peers & ((1u << lane) - 1u));
+            const uint32_t base = ok ? c[warp * 256u + d] : 0u;
+            __syncwarp();
+            if (ok && below == 0) c[warp * 256u + d] = base + __popc(peers);
+            __syncwarp();
+            dig[r] = d;
+            rank[r] = base + below;
+        }
+        __syncthreads();
+        // exclusive scan over (digit, warp); thread t owns digit t
+        uint32_t row[kWarps], tot = 0u;
+        if (tid < bins) {
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                row[w] = c[w * 256u + tid];
+                tot += row[w];
+            }
+        }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= uint32_t(off)) incl += t;
+        }
+        if (lane == 31) s_red[warp] = incl;
+        __syncthreads();
+        uint32_t off = incl - tot;
+        for (uint32_t w = 0; w < warp; ++w) off += s_red[w];
+        if (tid < bins) {
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                c[w * 256u + tid] = off;
+                off += row[w];
+            }
+        }
+        {  // the other counter array (last read by the previous pass) for the next pass
+            uint32_t* c2 = cnt + ((ps + 1) & 1) * (kWarps * 256);
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) c2[w * 256u + tid] = 0u;
+        }
+        __syncthreads();
+        out = s + (ps & 1) * 1024;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t p = kSeg * warp + 32u * r + lane;
+            if (p < n) out[c[warp * 256u + dig[r]] + rank[r]] = v[r];
+        }
+        __syncthreads();
+        if (ps + 1 < passes) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t p = kSeg * warp + 32u * r + lane;
+                v[r] = p < n ? out[p] : ~0ull;
+            }
+        }
+    }
+    if (passes == 0) {  // one depth: bucket order, to be put into slot order
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t p = kSeg * warp + 32u * r + lane;
+            if (p < n) out[p] = v[r];
+        }
+        __syncthreads();
+    }
+    oddeven_fix(out, n, tid, CtaBar{});
+    for (uint32_t i = tid; i < n; i += kSmallSortThreads) {
+        dst[i] = out[i];
+        if (site) site->put(i, out[i]);
+    }
 }
 
 // One run of up to kRun keys (global) sorted into shared memory by 256
@@ -408,6 +559,17 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t*
         rank_merge(s, n, keys + b, tid, kSmallSortThreads, site);
         return;
     }
+#ifndef SORT_RADIX
+#define SORT_RADIX 0  // per-tile LSD radix (measured slower: DESIGN.md 3)
+#endif
+#if SORT_RADIX
+    if (n > 64u) {
+        if (n <= 256u) radix_bucket<1>(keys + b, n, keys + b, s, s_red, tid, sp);
+        else if (n <= 512u) radix_bucket<2>(keys + b, n, keys + b, s, s_red, tid, sp);
+        else radix_bucket<4>(keys + b, n, keys + b, s, s_red, tid, sp);
+        return;
+    }
+#endif
 #if SORT32
     {
         bool done;

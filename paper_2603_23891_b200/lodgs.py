@@ -32,7 +32,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "liblodgs_b200.so")
 LIB_PATH = os.environ.get("LODGS_B200_LIB", LIB_PATH)
 
 ROOT_PARENT = 0xFFFFFFFF  # core.hpp:15
-_BLEND_FLAGS = {"wsp": 0, "tma": 64, "gather4": 128}  # LODGS_RENDER_BLEND_*
+_BLEND_FLAGS = {"cpa": 0, "wsp": 512, "tma": 64, "gather4": 128}  # LODGS_RENDER_BLEND_*
 TILE = 16  # tiles.hpp:8-9
 
 # --------------------------------------------------------------- errors --
@@ -474,7 +474,7 @@ class RenderOptions:
     output_rgb8: bool = False  # render_batch host images are W*H*3 bytes (save_ppm quantisation)
     # fast-blend kernel: "wsp" (default, cp.async producer warps), "tma" (sort-written
     # records streamed with cp.async.bulk), "gather4" (TMA tile::gather4); DESIGN.md 3.7
-    blend_kernel: str = "wsp"
+    blend_kernel: str = "cpa"
 
 
 @dataclasses.dataclass
@@ -759,7 +759,7 @@ class GpuScene:
         if opts.filter_mode not in ("parallel", "serial"):
             raise ValidationError("render: filter_mode is 'parallel' or 'serial'")
         if opts.blend_kernel not in _BLEND_FLAGS:
-            raise ValidationError("render: blend_kernel is 'wsp', 'tma' or 'gather4'")
+            raise ValidationError("render: blend_kernel is 'cpa', 'wsp', 'tma' or 'gather4'")
         flags = (1 if opts.exact_blend else 0) | (2 | 8 if opts.collect_kpc else 0) | \
                 (4 if opts.stage_timing else 0) | (16 if opts.filter_mode == "serial" else 0) | \
                 (32 if opts.output_rgb8 else 0) | _BLEND_FLAGS[opts.blend_kernel]
@@ -1043,7 +1043,7 @@ def sort_pairs(pairs: np.ndarray) -> None:
 
 
 def alpha_blend(sorted_pairs: np.ndarray, lst: BlendList, grid: TileGrid, width: int, height: int,
-                workers: int = 1, exact: bool = False, blend_kernel: str = "wsp") -> Image:
+                workers: int = 1, exact: bool = False, blend_kernel: str = "cpa") -> Image:
     """rasterizer.hpp:67-71 (kpc collection is not part of this stage on the GPU)."""
     sp = np.ascontiguousarray(sorted_pairs, PAIR_DTYPE)
     img = np.empty((height, width, 3), np.float32)

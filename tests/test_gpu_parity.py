@@ -392,17 +392,21 @@ def test_sort_hand_cases(L, gpu):
 
 def test_sort_big_buckets(L, oracle, gpu):
     """Every bucket-size regime of the per-tile sort against the reference's
-    stable LSD sort: register networks (<= 1024), two runs + rank merge in the
+    stable LSD sort: register networks (<= 64), the per-tile LSD radix (65..1024:
+    1, 2 or 4 keys per thread, 0..4 digit passes), two runs + rank merge in the
     small kernel (<= 2048), 3..16 runs in the big-bucket kernel (<= 16384),
-    the global in-place network beyond; narrow depth bands (32-bit keys, with
-    and without ties), wide ones (64-bit networks), both mixed in one bucket."""
+    the global in-place network beyond; one depth only (no digit pass), narrow
+    depth bands (with and without ties), wide ones, both mixed in one bucket."""
     rng = np.random.default_rng(5)
-    sizes = (1023, 1024, 1025, 1500, 2047, 2048, 2049, 3000, 4096, 4097, 8263, 16384, 16385, 30000)
+    sizes = (33, 64, 65, 100, 255, 256, 257, 400, 511, 512, 513, 777, 1023, 1024, 1025, 1500,
+             2047, 2048, 2049, 3000, 4096, 4097, 8263, 16384, 16385, 30000)
     for k, n in enumerate(sizes):
-        for depth in ("ties32", "narrow", "ties64", "wide"):
+        for depth in ("ties32", "narrow", "ties64", "wide", "one"):
             pairs = np.empty(n, L.PAIR_DTYPE)
             pairs["tile"] = rng.integers(0, 2, n) * 5 if k % 3 == 0 else 3
-            if depth == "ties32":  # 4 distinct depths 2^17 ulps apart
+            if depth == "one":  # every key at one depth: slot order decides alone
+                pairs["depth"] = np.float32(7.25)
+            elif depth == "ties32":  # 4 distinct depths 2^17 ulps apart
                 pairs["depth"] = (100 + rng.integers(0, 4, n)).astype(np.float32)
             elif depth == "ties64":
                 pairs["depth"] = rng.integers(0, 300, n).astype(np.float32)
@@ -477,9 +481,11 @@ def test_blend_micro_scenes(L, oracle, gpu):
         assert max_abs(fa, want) <= IMG_TOL, rep
         # the TMA-staged kernels (same certified per-sample code; k_blend_tma rounds the
         # mean tile-relative instead of block-relative, so its last bits may differ)
-        for k in ("tma", "gather4"):
+        for k in ("tma", "gather4", "wsp"):
             fk = L.alpha_blend(pairs, bl, grid, w, h, blend_kernel=k).rgb
             assert max_abs(fk, want) <= IMG_TOL, (rep, k)
+            if k == "wsp":  # same block-relative means and sample order as k_blend_cpa
+                assert fk.tobytes() == fa.tobytes(), (rep, k)
 
 
 def test_blend_needle_splats(L, oracle, gpu):
@@ -519,9 +525,11 @@ def test_blend_needle_splats(L, oracle, gpu):
         assert ex.tobytes() == want.tobytes(), rep
         fa = L.alpha_blend(pairs, bl, grid, w, h, exact=False).rgb
         assert max_abs(fa, want) <= IMG_TOL, (rep, max_abs(fa, want))
-        for k in ("tma", "gather4"):
+        for k in ("tma", "gather4", "wsp"):
             fk = L.alpha_blend(pairs, bl, grid, w, h, blend_kernel=k).rgb
             assert max_abs(fk, want) <= IMG_TOL, (rep, k, max_abs(fk, want))
+            if k == "wsp":
+                assert fk.tobytes() == fa.tobytes(), (rep, k)
 
 
 # ---------------------------------------------------------------- render --
@@ -546,7 +554,7 @@ def _check_render(L, oracle, scene, tree, cam, tau_r, mode):
     assert out.image.rgb.tobytes() == want["image"].tobytes()
     ex = scene.render(cam, L.FilterConfig(tau_r), mode, L.RenderOptions(exact_blend=True))
     assert ex.image.rgb.tobytes() == want["image"].tobytes()
-    # the production frame (flags 0: k_blend_wsp, FP32 + certified FP64 re-check)
+    # the production frame (flags 0: k_blend_cpa, FP32 + certified FP64 re-check)
     fast = scene.render(cam, L.FilterConfig(tau_r), mode)
     assert fast.stats.n_pairs == want["n_pairs"]
     assert scene.read_pairs().tobytes() == want["pairs"].tobytes()

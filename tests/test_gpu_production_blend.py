@@ -1,4 +1,4 @@
-"""The production frame path -- k_blend_wsp, the kernel bench.py times -- against the
+"""The production frame path -- k_blend_cpa, the kernel bench.py times -- against the
 reference renderer itself (oracle/_ref, compiled from /root/reference's sources) on
 the BASELINE.json configurations.
 
@@ -48,7 +48,7 @@ def _compare(ref, rh, cam, tau_r, mode, img, st, what, want=None):
     return want, err, psnr
 
 
-def _async_frames(L, scene, cams, tau_r, mode, blend_kernel="wsp"):
+def _async_frames(L, scene, cams, tau_r, mode, blend_kernel="cpa"):
     """Four frames in flight (render_async), every image to its own host buffer."""
     scene.set_inflight(4)
     p = scene.params(L.FilterConfig(tau_r), mode, L.RenderOptions(blend_kernel=blend_kernel))
@@ -101,7 +101,9 @@ def test_cfg3_bench_frames_async_and_batch(L, ref, cfg3):
     """The frames the driver's `bench.py --steps 20` times (strided over the whole
     300-frame path), through render_async (4 in flight) and render_batch: every image
     against the reference renderer's; then the same frames with the TMA-staged blend
-    kernels (LODGS_RENDER_BLEND_TMA / _GATHER4) against the same images."""
+    kernels (LODGS_RENDER_BLEND_TMA / _GATHER4) and the round-1 default
+    k_blend_wsp (LODGS_RENDER_BLEND_WSP, byte-identical to the default k_blend_cpa) against
+    the same images."""
     b, tree, rh, cams, scene = cfg3
     from paper_2603_23891_b200.sharding import strided_frames
 
@@ -118,10 +120,12 @@ def test_cfg3_bench_frames_async_and_batch(L, ref, cfg3):
         worst = max(worst, err)
         wants.append(want)
     print(f"cfg3 bench frames: worst max-abs {worst:.3g}")
-    for k in ("tma", "gather4"):
+    for k in ("tma", "gather4", "wsp"):
         imgs = _async_frames(L, scene, frames, b.TAU_R, mode, blend_kernel=k)
-        for i, cam, im, want in zip(idx, frames, imgs, wants):
+        for i, cam, im, want, bi in zip(idx, frames, imgs, wants, b_imgs):
             _compare(ref, rh, cam, b.TAU_R, mode, im, None, f"{k} frame {i}", want=want)
+            if k == "wsp":  # k_blend_cpa's means and sample order: the same bytes
+                assert im.tobytes() == bi.tobytes(), f"wsp frame {i} differs from cpa"
 
 
 def test_cfg3_altitudes_and_oblique_keyframes(L, ref, cfg3):

@@ -13,8 +13,13 @@ for spec in "$@"; do
   out=$ROOT/_variants/$name; mkdir -p $out
   objs=$(ls $OBJ/*.o)
   for tu in $TU; do
-    nvcc $NVFLAGS $flags -c $CSRC/$tu -o $out/${tu%.cu}.o
-    objs=$(echo "$objs" | grep -v "/${tu%.cu}.o$")
+    base=${tu%.*}
+    if [ "${tu##*.}" = "cpp" ]; then
+      g++ -O2 -std=c++17 -fPIC -ffp-contract=off -fvisibility=hidden -I/usr/local/cuda/include $flags -c $CSRC/$tu -o $out/$base.o
+    else
+      nvcc $NVFLAGS $flags -c $CSRC/$tu -o $out/$base.o
+    fi
+    objs=$(echo "$objs" | grep -v "/$base.o$")
   done
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $out/liblodgs_b200.so $out/*.o $objs -lpthread -ldl -lrt
   echo "built $out"
