@@ -1,7 +1,8 @@
 """Secondary BASELINE.json workloads (the headline cfg 3 is bench.py's default).
 
   cfg2: 1,007,370-node tree (41x42 roots, L=3), 1920x1080, top-down altitude 50,
-        GTC shrinking on (adaptive tau from GPU calibration, lambda_G given).  SH degree
+        GTC shrinking on (adaptive tau from GPU calibration at each lambda_G given, the
+        paper's 0.2 and a gentle 0.02; PSNR / SSIM against the three-sigma frames).  SH degree
         0: the reference is SH0-only, so SH3 colours would be parity-unpinned.
   cfg4: 50,142,872-node tree (103x104 roots, L=4), 3840x2160, fx=2000, a descent from
         altitude 400 to 110; GTC shrink off (three-sigma) vs on (adaptive).
@@ -168,19 +169,34 @@ def run(which, frames, lambda_g, inflight=2):
     with L.GpuScene(tree) as scene:
         scene.set_inflight(inflight)
         views = cams[:: max(1, len(cams) // 4)][:4]
-        rep = scene.calibrate(views, lambda_g, L.FilterConfig(3.0))
         base = {"workload": which, "nodes": tree.node_count(), "width": cams[0].width,
                 "height": cams[0].height, "frames": len(cams), "tau_r": 3.0,
                 "build_s": build_s, "device_bytes": scene.memory_bytes(),
                 "frames_in_flight": inflight}
-        modes = [("three_sigma", L.ShrinkMode.three_sigma()),
-                 ("adaptive", L.ShrinkMode.adaptive(rep.tau))]
-        for name, mode in modes:
+        modes = [("three_sigma", L.ShrinkMode.three_sigma(), None)]
+        for lg in lambda_g:
+            rep = scene.calibrate(views, lg, L.FilterConfig(3.0))
+            modes.append(("adaptive", L.ShrinkMode.adaptive(rep.tau), (lg, rep)))
+        qviews = cams[:: max(1, len(cams) // 6)][:6]
+        for name, mode, cal in modes:
             r = time_frames(scene, cams, mode)
             rec = dict(base, shrink=name, **r)
-            if name == "adaptive":
-                rec.update(lambda_g=lambda_g, tau=rep.tau, calib_views=rep.n_views,
+            if cal:
+                lg, rep = cal
+                rec.update(lambda_g=lg, tau=rep.tau, calib_views=rep.n_views,
                            scene_gtc=rep.scene_mean)
+                # image quality against the three-sigma frame of the same view (SURVEY
+                # 8(d)'s shrink caveat: the calibrated tau culls most splats at lambda 0.2)
+                ps, ss = [], []
+                for cam in qviews:
+                    scene.render(cam, L.FilterConfig(3.0), L.ShrinkMode.three_sigma())
+                    scene.set_reference_image()
+                    scene.render(cam, L.FilterConfig(3.0), mode)
+                    p_, s_ = scene.compare_reference(True)
+                    ps.append(p_)
+                    ss.append(s_)
+                rec.update(quality_views=len(qviews), psnr_vs_three_sigma_mean=sum(ps) / len(ps),
+                           psnr_vs_three_sigma_min=min(ps), ssim_vs_three_sigma_mean=sum(ss) / len(ss))
             out.append(rec)
             print(json.dumps(rec), flush=True)
     return out
@@ -190,7 +206,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", nargs="+", default=["cfg2", "cfg4"])
     ap.add_argument("--frames", type=int, default=30)
-    ap.add_argument("--lambda-g", type=float, default=0.2)
+    ap.add_argument("--lambda-g", type=float, nargs="+", default=[0.2, 0.02])
     ap.add_argument("--inflight", type=int, default=4, choices=(1, 2, 3, 4))
     args = ap.parse_args()
     for w in args.which:
