@@ -1473,11 +1473,23 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
 #define CPA_LAG 6
 #endif
 constexpr int kCpaLag = CPA_LAG;
+
+// Ring depth by frame size: 20 stages at 1080p, 16 above kCpaBigFrameTiles tiles.
+// At 4K (32,400 tiles) the 20-stage CTAs (4 x 51 KB of shared memory per SM) cost
+// 11 % of cfg 4's frame rate against 12 or 16 stages, while at 1080p 20 stages are
+// 1.5 % ahead of 12 / 16 (cfg 3 3,525 / 3,471 / 3,470, cfg 4 511 / 573 / 572 frames/s;
+// chosen per frame: cfg 3 3,520-3,529, cfg 4 567-572 with 16, 562-567 with 12).
+#ifndef CPA_STAGES_BIG
+#define CPA_STAGES_BIG 16
+#endif
 constexpr int kCpaStages = CPA_STAGES;
+constexpr int kCpaStagesBig = CPA_STAGES_BIG;
+constexpr int kCpaBigFrameTiles = 12288;
 constexpr int kCpaAhead = CPA_AHEAD;
 constexpr int kCpaThreads = (kTmaConsumers + 1) * 32;
-static_assert(kCpaStages < kDoneRing, "a tile has >= 1 stage");
-static_assert(kCpaLag < kCpaStages, "a stage is published before the producer waits for its reuse");
+static_assert(kCpaStages < kDoneRing && kCpaStagesBig < kDoneRing, "a tile has >= 1 stage");
+static_assert(kCpaLag < kCpaStages && kCpaLag < kCpaStagesBig,
+              "a stage is published before the producer waits for its reuse");
 
 struct CpaStage {
     double2 m[32];   // Gauss64 (mx, my)
@@ -1486,11 +1498,12 @@ struct CpaStage {
     float2 h[32];    // Gauss32 (hx, hy)
     uint32_t slot[32];
 };
+template <int S>
 struct CpaShared {
-    CpaStage st[kCpaStages];
+    CpaStage st[S];
     WarpStage wl[kTmaConsumers];
-    TmaHdr hdr[kCpaStages];
-    unsigned long long full[kCpaStages], empty[kCpaStages];
+    TmaHdr hdr[S];
+    unsigned long long full[S], empty[S];
     uint32_t done[kDoneRing];
 };
 
@@ -1501,6 +1514,7 @@ __device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* b) {
                  : "memory");
 }
 
+template <int S>
 __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
     const unsigned long long* __restrict__ keys, const Gauss64* __restrict__ g64,
@@ -1509,10 +1523,10 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
     pdl_wait();  // the sort (and everything before it) is complete and visible
     pdl_trigger();
     extern __shared__ __align__(128) unsigned char cpa_raw[];
-    CpaShared& sh = *reinterpret_cast<CpaShared*>(cpa_raw);
+    CpaShared<S>& sh = *reinterpret_cast<CpaShared<S>*>(cpa_raw);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kCpaStages; ++s) {
+        for (int s = 0; s < S; ++s) {
             mbar_init(&sh.full[s], CPA_ASYNC_ARRIVE ? 33 : 32);  // + the header's arrive
             mbar_init(&sh.empty[s], kTmaConsumers * 32);  // every consumer lane
         }
@@ -1580,9 +1594,9 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
             const G4Chunk ch = fifo[jf];
             fifo[jf] = gen();
             if (ch.tile >= 0 && ch.k == killed) continue;  // rest of a terminated tile
-            const int s = int(i % kCpaStages);
-            if (i >= uint32_t(kCpaStages))
-                mbar_wait_hint<TMA_PROD_HINT>(&sh.empty[s], ((i / kCpaStages) - 1) & 1u);
+            const int s = int(i % S);
+            if (i >= uint32_t(S))
+                mbar_wait_hint<TMA_PROD_HINT>(&sh.empty[s], ((i / S) - 1) & 1u);
             ++i;
             if (ch.tile < 0) {  // the CTA's work is done
                 if (lane == 0) sh.hdr[s] = TmaHdr{0, 0, 0u, 2u};
@@ -1595,7 +1609,7 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
                 cp_async_wait<0>();
                 for (uint32_t q = i - 1 > uint32_t(kCpaLag) ? i - 1 - uint32_t(kCpaLag) : 0u;
                      q < i; ++q)
-                    mbar_arrive(&sh.full[q % kCpaStages]);
+                    mbar_arrive(&sh.full[q % S]);
 #endif
                 finished = true;
                 continue;
@@ -1647,7 +1661,7 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
             cp_async_commit();
             if (i > uint32_t(kCpaLag)) {
                 cp_async_wait<kCpaLag>();
-                mbar_arrive(&sh.full[(i - 1 - uint32_t(kCpaLag)) % kCpaStages]);
+                mbar_arrive(&sh.full[(i - 1 - uint32_t(kCpaLag)) % S]);
             }
 #endif
             first_chunk = last;
@@ -1667,8 +1681,8 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
     uint32_t k = 0;
     const unsigned lt = (1u << lane) - 1u;
     for (uint32_t i = 0;; ++i) {
-        const int s = int(i % kCpaStages);
-        mbar_wait_hint<CPA_CONS_HINT>(&sh.full[s], (i / kCpaStages) & 1u);
+        const int s = int(i % S);
+        mbar_wait_hint<CPA_CONS_HINT>(&sh.full[s], (i / S) & 1u);
         const TmaHdr hd = sh.hdr[s];
         if (hd.flags & 2u) break;
         if (fresh) {
@@ -2007,6 +2021,35 @@ void launch_view_gtc(const uint32_t* offsets, int n_tiles, const double* kpc, ui
 uint64_t blend_record_bytes() { return sizeof(BlendRec); }
 int blend_launches() { return 1; }
 
+template <int S>
+static void launch_cpa(const uint32_t* offsets, const uint32_t* order,
+                       const unsigned long long* keys, const Gauss64* g64, const Gauss32* g32,
+                       int width, int height, int tiles_x, int n_tiles, unsigned* ticket,
+                       float* image, cudaStream_t s) {
+    const int smem = int(sizeof(CpaShared<S>));
+    static std::mutex mu;
+    static int grid_of[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int grid = 0;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev < 0 || dev >= 64 || !grid_of[dev]) {
+            cudaFuncSetAttribute(k_blend_cpa<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            int per_sm = 0, n_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blend_cpa<S>, kCpaThreads, smem);
+            cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+            grid = std::max(1, per_sm) * std::max(1, n_sm);
+            if (dev >= 0 && dev < 64) grid_of[dev] = grid;
+        } else {
+            grid = grid_of[dev];
+        }
+    }
+    grid = std::min(n_tiles, grid);
+    launch_pdl(k_blend_cpa<S>, grid, kCpaThreads, smem, s, offsets, order, keys, g64, g32, width,
+               height, tiles_x, uint32_t(n_tiles), ticket, image);
+}
+
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,
@@ -2042,28 +2085,12 @@ void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned
         return;
     }
     if (kernel == kBlendCpa && !exact && ticket) {
-        const int smem = int(sizeof(CpaShared));
-        static std::mutex mu;
-        static int grid_of[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        int grid = 0;
-        {
-            std::lock_guard<std::mutex> lock(mu);
-            if (dev < 0 || dev >= 64 || !grid_of[dev]) {
-                cudaFuncSetAttribute(k_blend_cpa, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                int per_sm = 0, n_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blend_cpa, kCpaThreads, smem);
-                cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-                grid = std::max(1, per_sm) * std::max(1, n_sm);
-                if (dev >= 0 && dev < 64) grid_of[dev] = grid;
-            } else {
-                grid = grid_of[dev];
-            }
-        }
-        grid = std::min(n_tiles, grid);
-        launch_pdl(k_blend_cpa, grid, kCpaThreads, smem, s, offsets, order, keys, g64, g32, width,
-                   height, tiles_x, uint32_t(n_tiles), ticket, image);
+        if (n_tiles > kCpaBigFrameTiles)
+            launch_cpa<kCpaStagesBig>(offsets, order, keys, g64, g32, width, height, tiles_x,
+                                      n_tiles, ticket, image, s);
+        else
+            launch_cpa<kCpaStages>(offsets, order, keys, g64, g32, width, height, tiles_x,
+                                   n_tiles, ticket, image, s);
         return;
     }
     if (kernel == kBlendTma && !exact && records && ticket) {

@@ -23,8 +23,11 @@ struct DevTree {
     const float4* iquat = nullptr;   // (w, x, y, z) for [0, leaf_begin)
     const uint32_t* parent = nullptr;  // padded to 256 nodes with kRootParent
     const SplatRec* splat = nullptr;
-    // per node, the FP64 world covariance of mark_core (sigma3d, camera
-    // independent): 6 doubles, precomputed at upload for the preprocess
+    // optional SH rest coefficients (lodgs_gpu_scene_set_sh): sh_k per channel
+    // (3 / 8 / 15 for degree 1 / 2 / 3, 0: SH0), per node 3 sh_k floats K-major,
+    // padded to whole float4s (sh_stride of them)
+    const float4* sh = nullptr;
+    int sh_k = 0, sh_stride = 0;
     // Nodes [leaf_begin, n) are all leaves (leaf_begin a multiple of 1024, or n).
     uint64_t leaf_begin = 0;
     // max_i (|mx| + |my| + |mz|) over the tree (rounded up): the FP32 leaf

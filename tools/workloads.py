@@ -39,11 +39,15 @@ def path(width, height, focal, keys, samples):
     return L.sample_camera_path(cams, samples)
 
 
+BLEND = "cpa"  # --blend: the fast-blend kernel (RenderOptions.blend_kernel)
+THREE_SIGMA_ONLY = False
+
+
 def time_frames(scene, cams, mode, tau_r=3.0, reps=1):
     import torch
 
     stream = torch.cuda.ExternalStream(scene.stream_ptr())
-    p = scene.params(L.FilterConfig(tau_r), mode, L.RenderOptions())
+    p = scene.params(L.FilterConfig(tau_r), mode, L.RenderOptions(blend_kernel=BLEND))
     for cam in cams[:3]:  # warm-up and pair-buffer sizing
         scene.render(cam, L.FilterConfig(tau_r), mode)
     for cam in cams:
@@ -174,13 +178,13 @@ def run(which, frames, lambda_g, inflight=2):
                 "build_s": build_s, "device_bytes": scene.memory_bytes(),
                 "frames_in_flight": inflight}
         modes = [("three_sigma", L.ShrinkMode.three_sigma(), None)]
-        for lg in lambda_g:
+        for lg in (lambda_g if not THREE_SIGMA_ONLY else []):
             rep = scene.calibrate(views, lg, L.FilterConfig(3.0))
             modes.append(("adaptive", L.ShrinkMode.adaptive(rep.tau), (lg, rep)))
         qviews = cams[:: max(1, len(cams) // 6)][:6]
         for name, mode, cal in modes:
             r = time_frames(scene, cams, mode)
-            rec = dict(base, shrink=name, **r)
+            rec = dict(base, shrink=name, blend_kernel=BLEND, **r)
             if cal:
                 lg, rep = cal
                 rec.update(lambda_g=lg, tau=rep.tau, calib_views=rep.n_views,
@@ -208,7 +212,12 @@ def main():
     ap.add_argument("--frames", type=int, default=30)
     ap.add_argument("--lambda-g", type=float, nargs="+", default=[0.2, 0.02])
     ap.add_argument("--inflight", type=int, default=4, choices=(1, 2, 3, 4))
+    ap.add_argument("--blend", default="cpa", choices=("cpa", "wsp", "tma", "gather4"))
+    ap.add_argument("--three-sigma-only", action="store_true")
     args = ap.parse_args()
+    global BLEND, THREE_SIGMA_ONLY
+    BLEND = args.blend
+    THREE_SIGMA_ONLY = args.three_sigma_only
     for w in args.which:
         run(w, args.frames, args.lambda_g, args.inflight)
 
