@@ -216,6 +216,18 @@ LODGS_API int lodgs_gpu_sync(lodgs_gpu_scene *scene, lodgs_render_stats *stats);
  * (lodgs_gpu_scene_stream): a frame starts after the work already enqueued
  * there (e.g. a timing event). */
 LODGS_API int lodgs_gpu_scene_set_inflight(lodgs_gpu_scene *scene, int frames);
+
+/* View-dependent colour, spherical harmonics of degree 1..3 (BASELINE configs[1],
+ * "SH deg 3"; an extension: the reference is SH0-only, scene.hpp:15-24, so
+ * these colours have no reference to match -- DESIGN.md 3.9).  sh_rest holds, per node,
+ * K = (degree+1)^2 - 1 coefficients x 3 channels (K-major, the 3DGS features_rest layout),
+ * n_nodes rows.  A node's colour becomes max(rgb + sum_k c_k Y_k(d), 0), d the unit
+ * direction from the camera centre to the node's mean, rgb its SH0 colour; with all
+ * coefficients zero every frame equals the SH0 frame bit for bit.  degree 0 (sh_rest
+ * ignored) goes back to SH0.  2: degree outside 0..3, n_nodes != the scene's node count,
+ * or a non-finite coefficient. */
+LODGS_API int lodgs_gpu_scene_set_sh(lodgs_gpu_scene *scene, int degree, const float *sh_rest,
+                                     uint64_t n_nodes);
 /* Makes the control stream wait for every frame enqueued so far (no host sync):
  * record a timing event on the control stream after this. */
 LODGS_API int lodgs_gpu_join(lodgs_gpu_scene *scene);

@@ -209,6 +209,11 @@ int lodgs_gpu_scene_set_inflight(lodgs_gpu_scene* scene, int frames) {
     return guarded([&] { S(scene).set_inflight(frames); });
 }
 
+int lodgs_gpu_scene_set_sh(lodgs_gpu_scene* scene, int degree, const float* sh_rest,
+                           uint64_t n_nodes) {
+    return guarded([&] { S(scene).set_sh(degree, sh_rest, n_nodes); });
+}
+
 int lodgs_gpu_join(lodgs_gpu_scene* scene) {
     return guarded([&] { S(scene).join(); });
 }

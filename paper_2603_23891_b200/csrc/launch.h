@@ -94,6 +94,9 @@ void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected
                        uint64_t max_selected, int shrink_kind, double tau, int tiles_x,
                        int tiles_y, PrepOut out, FrameCounters* cnt, int grid, cudaStream_t s,
                        bool known_visible = false);
+// SH degree 1..3 colours of the kept slots (after launch_preprocess; no-op without SH)
+void launch_sh_colour(const Geom& g, const DevTree& t, const GaussEmit* emit, Gauss32* g32,
+                      GaussCol64* col64, const FrameCounters* cnt, int grid, cudaStream_t s);
 // Turns the per-tile counts into offsets[n_tiles+1] and per-tile write cursors,
 // lists the tiles whose segment exceeds the in-shared-memory sort capacity, and
 // writes order[n_tiles]: tiles heaviest-first (log2 buckets) for the per-tile grids.

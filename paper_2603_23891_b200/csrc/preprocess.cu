@@ -342,6 +342,118 @@ __global__ void __launch_bounds__(kPrepBlock, PREP_MIN_CTAS) k_preprocess(
     }
 }
 
+// ---------------------------------------------------------------------------
+// View-dependent colour (SH degree 1..3, lodgs_gpu_scene_set_sh): an extension for
+// BASELINE configs[1] ("SH deg 3").  The reference is SH0-only (SPEC.md:78,
+// scene.hpp:15-24), so there is no reference colour to match; the evaluation is
+// the standard real SH basis of 3D Gaussian splatting (constants below) on top of the
+// node's SH0 colour, clamped at 0:
+//     colour = max(rgb + sum_k c_k Y_k(d), 0),  d = (mean - camera centre) * (1 / |.|)
+// in FP64, every operation in the order written (-fmad=false), so
+// tests/test_gpu_sh.py restates it in numpy bit for bit.  With all c_k = 0 the sum
+// adds +-0 and, for rgb >= 0, the colour is rgb exactly: the SH0 frame.  Runs
+// after K3 over the frame's slots and rewrites the colours of the kept ones
+// (Gauss32 r/g/b, and the FP64 colours of the exact blend when present).
+__constant__ double kShC1 = 0.4886025119029199;
+__constant__ double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                               -1.0925484305920792, 0.5462742152960396};
+__constant__ double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                               0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                               -0.5900435899266435};
+
+// Y_k(d) for the K = 3 / 8 / 15 rest coefficients, each product left to right.
+template <int K>
+__device__ __forceinline__ void sh_basis(double x, double y, double z, double (&Y)[K]) {
+    Y[0] = -kShC1 * y;
+    Y[1] = kShC1 * z;
+    Y[2] = -kShC1 * x;
+    if constexpr (K > 3) {
+        const double xx = x * x, yy = y * y, zz = z * z;
+        Y[3] = kShC2[0] * (x * y);
+        Y[4] = kShC2[1] * (y * z);
+        Y[5] = kShC2[2] * (2.0 * zz - xx - yy);
+        Y[6] = kShC2[3] * (x * z);
+        Y[7] = kShC2[4] * (xx - yy);
+        if constexpr (K > 8) {
+            Y[8] = kShC3[0] * y * (3.0 * xx - yy);
+            Y[9] = kShC3[1] * (x * y) * z;
+            Y[10] = kShC3[2] * y * (4.0 * zz - xx - yy);
+            Y[11] = kShC3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+            Y[12] = kShC3[4] * x * (4.0 * zz - xx - yy);
+            Y[13] = kShC3[5] * z * (xx - yy);
+            Y[14] = kShC3[6] * x * (xx - 3.0 * yy);
+        }
+    }
+}
+
+#ifndef SH_MIN_CTAS
+#define SH_MIN_CTAS 1
+#endif
+template <int K>
+__global__ void __launch_bounds__(kPrepBlock, SH_MIN_CTAS) k_sh_colour(
+    const Geom g, const SplatRec* __restrict__ splat, const float4* __restrict__ sh,
+    const GaussEmit* __restrict__ emit, Gauss32* g32, GaussCol64* col64,
+    const FrameCounters* __restrict__ cnt) {
+    pdl_wait();  // K3 is complete and visible
+    pdl_trigger();
+    constexpr int kStride = (3 * K + 3) / 4;  // float4s per node
+    // camera centre in world space: -R^T t (CameraGeom's world-to-camera R, t)
+    const double cx = -((g.rot[0] * g.trans[0] + g.rot[3] * g.trans[1]) + g.rot[6] * g.trans[2]);
+    const double cy = -((g.rot[1] * g.trans[0] + g.rot[4] * g.trans[1]) + g.rot[7] * g.trans[2]);
+    const double cz = -((g.rot[2] * g.trans[0] + g.rot[5] * g.trans[1]) + g.rot[8] * g.trans[2]);
+    const uint64_t n = cnt->n_selected;
+    for (uint64_t s = uint64_t(blockIdx.x) * kPrepBlock + threadIdx.x; s < n;
+         s += uint64_t(gridDim.x) * kPrepBlock) {
+        const GaussEmit e = emit[s];
+        if (e.ty0 == kDropped) continue;
+        const float4* rec = reinterpret_cast<const float4*>(splat + e.node);
+        const float4 m = __ldg(rec), c3 = __ldg(rec + 2), c4 = __ldg(rec + 3);  // mean; cr; cg, cb
+        float c[4 * kStride];
+        const float4* row = sh + uint64_t(e.node) * kStride;
+#pragma unroll
+        for (int j = 0; j < kStride; ++j) {
+            const float4 v = __ldg(row + j);
+            c[4 * j] = v.x;
+            c[4 * j + 1] = v.y;
+            c[4 * j + 2] = v.z;
+            c[4 * j + 3] = v.w;
+        }
+        const double dx = double(m.x) - cx, dy = double(m.y) - cy, dz = double(m.z) - cz;
+        const double inv = 1.0 / sqrt((dx * dx + dy * dy) + dz * dz);
+        double Y[K];
+        sh_basis<K>(dx * inv, dy * inv, dz * inv, Y);
+        double r = double(c3.w), gg = double(c4.x), b = double(c4.y);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            r = r + Y[k] * double(c[3 * k]);
+            gg = gg + Y[k] * double(c[3 * k + 1]);
+            b = b + Y[k] * double(c[3 * k + 2]);
+        }
+        r = r < 0.0 ? 0.0 : r;
+        gg = gg < 0.0 ? 0.0 : gg;
+        b = b < 0.0 ? 0.0 : b;
+        g32[s].r = float(r);
+        g32[s].g = float(gg);
+        g32[s].b = float(b);
+        if (col64) {
+            col64[s].r = r;
+            col64[s].g = gg;
+            col64[s].b = b;
+        }
+    }
+}
+
+void launch_sh_colour(const Geom& g, const DevTree& t, const GaussEmit* emit, Gauss32* g32,
+                      GaussCol64* col64, const FrameCounters* cnt, int grid, cudaStream_t s) {
+    if (!t.sh || t.sh_k <= 0) return;
+    if (t.sh_k == 3)
+        launch_pdl(k_sh_colour<3>, grid, kPrepBlock, 0, s, g, t.splat, t.sh, emit, g32, col64, cnt);
+    else if (t.sh_k == 8)
+        launch_pdl(k_sh_colour<8>, grid, kPrepBlock, 0, s, g, t.splat, t.sh, emit, g32, col64, cnt);
+    else
+        launch_pdl(k_sh_colour<15>, grid, kPrepBlock, 0, s, g, t.splat, t.sh, emit, g32, col64, cnt);
+}
+
 void launch_preprocess(const Geom& g, const DevTree& t, const uint32_t* selected,
                        uint64_t max_selected, int shrink_kind, double tau, int tiles_x,
                        int tiles_y, PrepOut out, FrameCounters* cnt, int grid, cudaStream_t s,

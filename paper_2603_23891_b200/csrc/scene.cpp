@@ -359,6 +359,42 @@ void GpuScene::make_contexts(int n) {
     }
 }
 
+// SH degree 1..3 coefficients (lodgs_gpu_scene_set_sh): packed per node into whole
+// float4s, shared by every frame context.  Frames already in flight finish first.
+void GpuScene::set_sh(int degree, const float* host, uint64_t n) {
+    if (degree < 0 || degree > 3) throw Error(LODGS_ERR_VALIDATION, "sh: degree is 0 to 3");
+    DeviceGuard dg(device_);
+    for (int i = 0; i < kMaxInflight; ++i)
+        if (GpuScene* c = context(i)) FGS_CUDA(cudaStreamSynchronize(c->stream_));
+    int k = 0, stride = 0;
+    if (degree > 0) {
+        if (n != tree_.n) throw Error(LODGS_ERR_VALIDATION, "sh: one row of coefficients per node");
+        if (!host) throw Error(LODGS_ERR_VALIDATION, "sh: null coefficients");
+        k = (degree + 1) * (degree + 1) - 1;
+        stride = (3 * k + 3) / 4;
+        std::vector<float> pack(size_t(n) * size_t(stride) * 4, 0.0f);
+        for (uint64_t i = 0; i < n; ++i)
+            for (int j = 0; j < 3 * k; ++j) {
+                const float v = host[i * uint64_t(3 * k) + uint64_t(j)];
+                if (!std::isfinite(v))
+                    throw Error(LODGS_ERR_VALIDATION,
+                                "sh: coefficient of node " + std::to_string(i) + " is not finite");
+                pack[i * uint64_t(stride) * 4 + uint64_t(j)] = v;
+            }
+        sh_.release();
+        sh_.alloc(n * uint64_t(stride));
+        FGS_CUDA(cudaMemcpy(sh_.p, pack.data(), pack.size() * sizeof(float), cudaMemcpyHostToDevice));
+    } else {
+        sh_.release();
+    }
+    for (int i = 0; i < kMaxInflight; ++i)
+        if (GpuScene* c = context(i)) {
+            c->tree_.sh = degree > 0 ? sh_.p : nullptr;
+            c->tree_.sh_k = k;
+            c->tree_.sh_stride = stride;
+        }
+}
+
 void GpuScene::set_inflight(int n) {
     if (n < 1 || n > kMaxInflight)
         throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1 to 4");
@@ -454,7 +490,7 @@ void GpuScene::reserve_pairs(uint64_t n) {
 
 uint64_t GpuScene::device_bytes() const {
     return (twin_ ? twin_->device_bytes() : 0) + geo_.bytes() + iscale_.bytes() + iquat_.bytes() +
-           parent_.bytes() + splat_.bytes() +
+           parent_.bytes() + splat_.bytes() + sh_.bytes() +
            cand_bits_.bytes() + qint_bits_.bytes() + selected_.bytes() + g64_.bytes() +
            tile_lists_.bytes() + tile_list_len_.bytes() +
            g32_.bytes() + emit_.bytes() + col64_.bytes() + keys_.bytes() + blend_rec_.bytes() +
@@ -554,6 +590,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     launch_preprocess(g, tree_, selected_.p, tree_.n, p.shrink_kind, p.tau, res_.tiles_x,
                       res_.tiles_y, out, d_counters_, persistent_grid_, stream_,
                       /*known_visible=*/true);
+    launch_sh_colour(g, tree_, emit_.p, g32_.p, out.col64, d_counters_, persistent_grid_, stream_);
     launch_tile_offsets(d_tile_count_, n_tiles, res_.tile_offsets.p, res_.tile_cursor.p,
                         res_.big_list.p, res_.tile_order.p, d_counters_, pair_cap_, stream_,
                         totals_.p, log_target_);
@@ -646,7 +683,7 @@ void GpuScene::finish(lodgs_render_stats* stats) {
         stats->filter_barriers = stats->filter_passes;
         stats->big_tiles = c.big_tiles;
         stats->kernel_launches =
-            last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() + n_levels() + filter_launches(tree_.n) - 3) : kLaunchesPerFrame + blend_launches() + filter_launches(tree_.n);
+            last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() + n_levels() + filter_launches(tree_.n) - 3 + sh_launches()) : kLaunchesPerFrame + blend_launches() + filter_launches(tree_.n) + sh_launches();
         if (last_timing_) {
             float ms = 0;
             FGS_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
@@ -789,8 +826,8 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
             s.filter_passes = last_serial_ ? int32_t(c.serial_passes) : 2;
             s.filter_barriers = s.filter_passes;
             s.big_tiles = c.big_tiles;
-            s.kernel_launches = last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() + n_levels() + filter_launches(tree_.n) - 3)
-                                             : kLaunchesPerFrame + blend_launches() + filter_launches(tree_.n);
+            s.kernel_launches = last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() + n_levels() + filter_launches(tree_.n) - 3 + sh_launches())
+                                             : kLaunchesPerFrame + blend_launches() + filter_launches(tree_.n) + sh_launches();
         }
     }
 }
@@ -949,6 +986,7 @@ uint64_t GpuScene::prepare(const lodgs_camera& cam, const uint32_t* selected, ui
     PrepOut po{g64_.p, g32_.p, emit_.p, nullptr, d_tile_count_};
     launch_preprocess(g, tree_, selected_.p, n_sel, kind, tau, res_.tiles_x, res_.tiles_y, po,
                       d_counters_, persistent_grid_, stream_);
+    launch_sh_colour(g, tree_, emit_.p, g32_.p, nullptr, d_counters_, persistent_grid_, stream_);
     maps_valid_ = false;
     FGS_CUDA(cudaGetLastError());
     FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
@@ -1047,7 +1085,9 @@ uint64_t GpuScene::read_gaussians(lodgs_blend_list* out, uint64_t cap) {
         out->conic_b[i] = a[i].cb;
         out->conic_c[i] = a[i].cc;
         out->opacity[i] = a[i].op;
-        out->col_r[i] = double(b[i].r);  // colours are f32 in the tree: exact
+        // colours are f32 in the tree: exact (with SH, set_sh, the FP64 colour rounded to
+        // f32; the exact blend keeps the FP64 one)
+        out->col_r[i] = double(b[i].r);
         out->col_g[i] = double(b[i].g);
         out->col_b[i] = double(b[i].b);
         out->radius[i] = a[i].radius;

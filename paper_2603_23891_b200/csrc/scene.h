@@ -130,6 +130,8 @@ public:
     // control stream; join() makes the control stream wait for all of them.
     // stream() is the control stream.
     void set_inflight(int n);
+    void set_sh(int degree, const float* sh_rest, uint64_t n_nodes);
+    uint32_t sh_launches() const { return tree_.sh_k > 0 ? 1u : 0u; }
     void enqueue_async(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host);
     void join();
     void sync_async(lodgs_render_stats* stats);
@@ -183,6 +185,7 @@ private:
     DevBuf<float4> iquat_;     // internal region: quaternion
     DevBuf<uint32_t> parent_;
     DevBuf<SplatRec> splat_;
+    DevBuf<float4> sh_;        // SH rest coefficients (set_sh), tree_.sh_stride per node
     // frame storage
     DevBuf<uint32_t> cand_bits_, qint_bits_, selected_;
     DevBuf<uint2> tile_lists_;       // K3 -> K4 per-CTA (tile, count) entries (<= kHistMaxTiles)

@@ -179,6 +179,7 @@ ABI_SYMBOLS = (
     "lodgs_gpu_host_free", "lodgs_gpu_read_image_rgb8", "lodgs_gpu_set_reference_image",
     "lodgs_gpu_compare_reference", "lodgs_gpu_image_metrics", "lodgs_gpu_scene_load",
     "lodgs_gpu_scene_info", "lodgs_gpu_scene_set_inflight", "lodgs_gpu_join",
+    "lodgs_gpu_scene_set_sh",
 )
 
 _lib = None
@@ -233,6 +234,7 @@ def load_library():
                                        C.POINTER(C.c_int32)]),
         "lodgs_gpu_read_image_rgb8": (C.c_int, [P, P]),
         "lodgs_gpu_scene_set_inflight": (C.c_int, [P, C.c_int]),
+        "lodgs_gpu_scene_set_sh": (C.c_int, [P, C.c_int, P, C.c_uint64]),
         "lodgs_gpu_join": (C.c_int, [P]),
         "lodgs_gpu_scene_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(P), _DP]),
         "lodgs_gpu_scene_info": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), P,
@@ -822,6 +824,20 @@ class GpuScene:
     def set_inflight(self, frames: int) -> None:
         """Frames in flight for render_async (1 to 4; default 4)."""
         _check(self._lib.lodgs_gpu_scene_set_inflight(self._h, int(frames)))
+
+    def set_sh(self, degree: int, sh_rest=None) -> None:
+        """View-dependent colour of degree 1..3 (an extension: the reference is SH0-only).
+        sh_rest: float32 array (node_count, (degree+1)**2 - 1, 3), the 3DGS features_rest
+        layout; a node's colour becomes max(rgb + sum_k c_k Y_k(dir), 0).  degree 0 goes
+        back to SH0."""
+        if degree == 0 or sh_rest is None:
+            _check(self._lib.lodgs_gpu_scene_set_sh(self._h, int(degree), None, 0))
+            return
+        a = np.ascontiguousarray(sh_rest, dtype=np.float32)
+        k = (int(degree) + 1) ** 2 - 1
+        if a.ndim != 3 or a.shape[1:] != (k, 3):
+            raise ValidationError(f"set_sh: sh_rest must be (nodes, {k}, 3) for degree {degree}")
+        _check(self._lib.lodgs_gpu_scene_set_sh(self._h, int(degree), _ptr(a), a.shape[0]))
 
     def sync(self) -> RenderStats:
         st = RenderStatsC()

@@ -2,8 +2,9 @@
 
   cfg2: 1,007,370-node tree (41x42 roots, L=3), 1920x1080, top-down altitude 50,
         GTC shrinking on (adaptive tau from GPU calibration at each lambda_G given, the
-        paper's 0.2 and a gentle 0.02; PSNR / SSIM against the three-sigma frames).  SH degree
-        0: the reference is SH0-only, so SH3 colours would be parity-unpinned.
+        paper's 0.2 and a gentle 0.02; PSNR / SSIM against the three-sigma frames).  --sh 3
+        adds SH degree-3 colours (synthetic coefficients; the reference is SH0-only,
+        SPEC.md:78, so these colours are parity-unpinned; tests/test_gpu_sh.py).
   cfg4: 50,142,872-node tree (103x104 roots, L=4), 3840x2160, fx=2000, a descent from
         altitude 400 to 110; GTC shrink off (three-sigma) vs on (adaptive).
   cfg5: view-batched rendering -- the cfg 3 tree, 1024 poses sampled from the cfg 3
@@ -41,6 +42,7 @@ def path(width, height, focal, keys, samples):
 
 BLEND = "cpa"  # --blend: the fast-blend kernel (RenderOptions.blend_kernel)
 THREE_SIGMA_ONLY = False
+SH_DEGREE = 0  # --sh: view-dependent colour of this degree (synthetic coefficients)
 
 
 def time_frames(scene, cams, mode, tau_r=3.0, reps=1):
@@ -172,11 +174,18 @@ def run(which, frames, lambda_g, inflight=2):
     build_s = time.perf_counter() - t0
     with L.GpuScene(tree) as scene:
         scene.set_inflight(inflight)
+        if SH_DEGREE:
+            # synthetic view-dependent colour (no reference: SH0-only): seeded
+            # N(0, 0.1) coefficients of degree SH_DEGREE, the 3DGS features_rest layout
+            k = (SH_DEGREE + 1) ** 2 - 1
+            import numpy as np
+            sh = np.random.default_rng(11).normal(0.0, 0.1, (tree.node_count(), k, 3))
+            scene.set_sh(SH_DEGREE, sh.astype(np.float32))
         views = cams[:: max(1, len(cams) // 4)][:4]
         base = {"workload": which, "nodes": tree.node_count(), "width": cams[0].width,
                 "height": cams[0].height, "frames": len(cams), "tau_r": 3.0,
                 "build_s": build_s, "device_bytes": scene.memory_bytes(),
-                "frames_in_flight": inflight}
+                "frames_in_flight": inflight, "sh_degree": SH_DEGREE}
         modes = [("three_sigma", L.ShrinkMode.three_sigma(), None)]
         for lg in (lambda_g if not THREE_SIGMA_ONLY else []):
             rep = scene.calibrate(views, lg, L.FilterConfig(3.0))
@@ -214,8 +223,10 @@ def main():
     ap.add_argument("--inflight", type=int, default=4, choices=(1, 2, 3, 4))
     ap.add_argument("--blend", default="cpa", choices=("cpa", "wsp", "tma", "gather4"))
     ap.add_argument("--three-sigma-only", action="store_true")
+    ap.add_argument("--sh", type=int, default=0, choices=(0, 1, 2, 3))
     args = ap.parse_args()
-    global BLEND, THREE_SIGMA_ONLY
+    global BLEND, THREE_SIGMA_ONLY, SH_DEGREE
+    SH_DEGREE = args.sh
     BLEND = args.blend
     THREE_SIGMA_ONLY = args.three_sigma_only
     for w in args.which:
