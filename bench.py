@@ -288,10 +288,19 @@ def run_b200(args, rank, world, local):
     from paper_2603_23891_b200 import lodgs as L
 
     dist = None
+    # LODGS_BENCH_DIST_BACKEND=gloo: the N>1 path on a box with fewer GPUs than ranks (the
+    # GPU test runs 2 ranks on one B200; ranks share a device, counters reduce on the CPU)
+    backend = os.environ.get("LODGS_BENCH_DIST_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if backend == "gloo" else "cuda"
     torch.cuda.set_device(local)
     t_build = time.perf_counter()
     tree = L.build_synthetic_tree(**TREE)
@@ -360,7 +369,7 @@ def run_b200(args, rank, world, local):
             scene.render_async(cam, params)
         scene.sync()
         vms, _, _ = device_loop(timed)
-        vmax, _ = reduce_timing(dist, vms, [], device="cuda")
+        vmax, _ = reduce_timing(dist, vms, [], device=red_dev)
         variants[name] = world * K / (vmax / 1000.0)
     params = default_params
 
@@ -407,11 +416,11 @@ def run_b200(args, rank, world, local):
         lib.lodgs_gpu_host_free(p)
 
     # max over ranks of the timed regions; per-rank counters summed
-    ms_max, _ = reduce_timing(dist, ms, [], device="cuda")
-    e2e_max, _ = reduce_timing(dist, e2e_s, [], device="cuda")
-    e2e_sync_max, _ = reduce_timing(dist, e2e_sync_s, [], device="cuda")
+    ms_max, _ = reduce_timing(dist, ms, [], device=red_dev)
+    e2e_max, _ = reduce_timing(dist, e2e_s, [], device=red_dev)
+    e2e_sync_max, _ = reduce_timing(dist, e2e_sync_s, [], device=red_dev)
     e2e8_max, (sum_sel, sum_pairs, nf, sum_sort_bytes) = reduce_timing(
-        dist, e2e8_s, [sum_sel, sum_pairs, nf, sum_sort_bytes], device="cuda")
+        dist, e2e8_s, [sum_sel, sum_pairs, nf, sum_sort_bytes], device=red_dev)
     nf = int(nf)
     if rank != 0:
         if dist:

@@ -422,6 +422,10 @@ __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
 // parent load is one contiguous 128 B warp access (arrays padded to a
 // multiple of 256 nodes; leaf_begin a multiple of 1024).  Writes keep words
 // (one ballot each) and the per-tile survivor counts.
+#ifndef LEAF_PER_LANE
+#define LEAF_PER_LANE 4
+#endif
+constexpr int kLeafPerLane = LEAF_PER_LANE;  // leaves per lane (a warp: 32 kLeafPerLane)
 __global__ void __launch_bounds__(256) k_filter_leaves(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const uint32_t* __restrict__ blk_bits, uint32_t* __restrict__ keep_bits,
@@ -431,26 +435,27 @@ __global__ void __launch_bounds__(256) k_filter_leaves(
     clock_start(clk, 2);
     const unsigned lane = threadIdx.x & 31;
     const uint64_t end = t.n;
-    const uint64_t wbase = t.leaf_begin + (uint64_t(blockIdx.x) * 256 + (threadIdx.x & ~31u)) * 4;
+    const uint64_t wbase =
+        t.leaf_begin + (uint64_t(blockIdx.x) * 256 + (threadIdx.x & ~31u)) * kLeafPerLane;
     if (wbase >= end) return;  // warp-uniform
-    uint32_t p[4];
+    uint32_t p[kLeafPerLane];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) p[k] = __ldcs(t.parent + wbase + k * 32 + lane);
+    for (int k = 0; k < kLeafPerLane; ++k) p[k] = __ldcs(t.parent + wbase + k * 32 + lane);
     unsigned need = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kLeafPerLane; ++k) {
         const bool in = wbase + k * 32 + lane < end;  // padding past n never survives
         const bool blocked =
             p[k] != kRootParent && ((__ldg(blk_bits + (p[k] >> 5)) >> (p[k] & 31)) & 1u);
         need |= (in && !blocked) ? (1u << k) : 0u;
     }
-    float4 a[4];
+    float4 a[kLeafPerLane];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < kLeafPerLane; ++k)
         if ((need >> k) & 1u) a[k] = __ldcs(t.geo + wbase + k * 32 + lane);
     unsigned keep = 0, undec = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kLeafPerLane; ++k) {
         if ((need >> k) & 1u) {
             const int vs = frustum_leaf_fp32(f, a[k].x, a[k].y, a[k].z, a[k].w);
             keep |= vs == 1 ? (1u << k) : 0u;
@@ -460,12 +465,12 @@ __global__ void __launch_bounds__(256) k_filter_leaves(
     if (undec) {
         // rare: within ~1e-3 world units of a frustum plane -> exact FP64
         // decision; operands re-read so nothing stays live across the call
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kLeafPerLane; ++k)
             if ((undec >> k) & 1u) keep |= vis_fp64(g, t, wbase + k * 32 + lane) ? (1u << k) : 0u;
     }
     unsigned c = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kLeafPerLane; ++k) {
         const uint32_t w = __ballot_sync(0xffffffffu, (keep >> k) & 1u);
         if (lane == unsigned(k) && (wbase + k * 32) < end) keep_bits[(wbase >> 5) + k] = w;
         c += __popc(w);
@@ -722,9 +727,11 @@ void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand
                    cand_bits, qint_bits, t.parent, split, tile_count, clk);
     }
     if (mid) cudaEventRecord(mid, s);
-    if (t.n > split)
-        launch_pdl(k_filter_leaves, unsigned((t.n - split + 1023) / 1024), 256, 0, s, g, f, t,
-                   static_cast<const uint32_t*>(qint_bits), cand_bits, tile_count, clk);
+    if (t.n > split) {
+        const uint64_t per_cta = 256ull * kLeafPerLane;
+        launch_pdl(k_filter_leaves, unsigned((t.n - split + per_cta - 1) / per_cta), 256, 0, s, g,
+                   f, t, static_cast<const uint32_t*>(qint_bits), cand_bits, tile_count, clk);
+    }
     const uint64_t T = count_tiles(t.n);
     uint32_t* prefix = T > kDirectPrefixTiles ? tile_count + T : nullptr;
     if (prefix)
