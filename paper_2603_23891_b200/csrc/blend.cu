@@ -1463,6 +1463,9 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
 #ifndef CPA_CG
 #define CPA_CG 1
 #endif
+#ifndef CPA_ROTATE
+#define CPA_ROTATE 0
+#endif
 // 1: the copies complete the stage themselves (cp.async.mbarrier.arrive.noinc);
 // 0: the producer publishes stage i - kCpaLag after cp.async.wait_group (lagged).
 // Both are racecheck-clean; 1 is faster (3,517 vs 3,461 frames/s, lag 3 / 6 / 10 alike).
@@ -1686,8 +1689,16 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
         const TmaHdr hd = sh.hdr[s];
         if (hd.flags & 2u) break;
         if (fresh) {
+#if CPA_ROTATE
+            // the CTA's k-th tile: warp w takes block (w + k) & 7, so no warp always
+            // draws the same block position of every tile
+            const uint32_t bw = (warp + k) & 7u;
+            bx = hd.x0 + int(bw & 1u) * 8;
+            by = hd.y0 + int(bw >> 1) * 4;
+#else
             bx = hd.x0 + bxo;
             by = hd.y0 + byo;
+#endif
             const int x = bx + int(lane & 7), y = by + int(lane >> 3);
             pix = PixState{(x < width && y < height) ? 1.0f : 0.0f, 0.0f, 0.0f, 0.0f};
             fresh = false;

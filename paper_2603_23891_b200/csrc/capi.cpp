@@ -185,6 +185,15 @@ int lodgs_gpu_render_batch(lodgs_gpu_scene* scene, const lodgs_camera* cams, uin
     });
 }
 
+int lodgs_gpu_render_views_async(lodgs_gpu_scene* scene, const lodgs_camera* cams, uint64_t n,
+                                 const lodgs_render_params* params, float* const* images_host) {
+    return guarded([&] {
+        if (n) need(cams, "cams");
+        need(params, "params");
+        S(scene).enqueue_views_async(cams, n, *params, images_host);
+    });
+}
+
 int lodgs_gpu_render_async(lodgs_gpu_scene* scene, const lodgs_camera* cam,
                            const lodgs_render_params* params, float* image_host) {
     return guarded([&] {

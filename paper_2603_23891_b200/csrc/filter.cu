@@ -25,6 +25,7 @@
 // bit-exact).  They are reached in FP32 with certified error bounds, and only
 // the nodes whose FP32 value falls inside the bound recompute in FP64.
 #include <algorithm>
+#include <cstring>
 #include <cmath>
 
 #include "launch.h"
@@ -286,7 +287,10 @@ __device__ __forceinline__ void decide_internal(const Geom& g, const GeomF& f, c
 // evaluating the current one, so loads overlap the FP32 EWA arithmetic:
 // frustum, and for visible internal nodes the radius -> cand / qint words by
 // ballot.
-__global__ void __launch_bounds__(kMarkBlock, 3) k_mark_internal(
+#ifndef MARK_MIN_CTAS
+#define MARK_MIN_CTAS 3
+#endif
+__global__ void __launch_bounds__(kMarkBlock, MARK_MIN_CTAS) k_mark_internal(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const double tau_r, uint32_t* __restrict__ cand_bits, uint32_t* __restrict__ qint_bits,
     FilterClock* clk) {
@@ -350,15 +354,12 @@ __device__ __forceinline__ void count_survivors(uint32_t* tile_count, uint64_t t
 // disqualified").  Another warp may read either value of a qint word while
 // walking: for any descendant the OR along its chain is the same, so the
 // result does not depend on the interleaving.
-__global__ void __launch_bounds__(kSelectBlock) k_select_internal(
-    uint32_t* __restrict__ cand_bits, uint32_t* qint_bits, const uint32_t* __restrict__ parent,
-    const uint64_t end, uint32_t* __restrict__ tile_count, FilterClock* clk) {
-    pdl_wait();  // the previous kernel of the frame is complete and visible
-    pdl_trigger();
-    clock_start(clk, 1);
+__device__ __forceinline__ void select_body(uint32_t* __restrict__ cand_bits, uint32_t* qint_bits,
+                                            const uint32_t* __restrict__ parent, const uint64_t end,
+                                            uint32_t* __restrict__ tile_count, const unsigned block) {
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t warp_base =
-        uint64_t(blockIdx.x) * (kSelectBlock * kSelectItems) + uint64_t(warp) * (32 * kSelectItems);
+        uint64_t(block) * (kSelectBlock * kSelectItems) + uint64_t(warp) * (32 * kSelectItems);
     if (warp_base >= end) return;  // warp-uniform
     uint32_t a[kSelectItems];
     bool disq[kSelectItems];
@@ -409,6 +410,15 @@ __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
 #pragma unroll
     for (int off = 4; off > 0; off >>= 1) cntw += __shfl_xor_sync(0xffffffffu, cntw, off);
     if (lane == 0 && cntw) count_survivors(tile_count, warp_base / kTileNodes, cntw);
+}
+
+__global__ void __launch_bounds__(kSelectBlock) k_select_internal(
+    uint32_t* __restrict__ cand_bits, uint32_t* qint_bits, const uint32_t* __restrict__ parent,
+    const uint64_t end, uint32_t* __restrict__ tile_count, FilterClock* clk) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
+    clock_start(clk, 1);
+    select_body(cand_bits, qint_bits, parent, end, tile_count, blockIdx.x);
     clock_end(clk, 1);
 }
 
@@ -525,20 +535,15 @@ __global__ void __launch_bounds__(1024) k_tile_prefix(const uint32_t* __restrict
 // directly: no look-back chain, CTAs never wait on each other).  Warp w owns
 // 32 words; for every non-empty word (broadcast by shuffle) lane b tests bit
 // b, so one popc places 32 nodes with a coalesced store.
-__global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ keep_bits,
-                                                 const uint64_t n_words,
-                                                 const uint32_t* __restrict__ tile_count,
-                                                 uint32_t* __restrict__ selected,
-                                                 FrameCounters* cnt, FilterClock* clk,
-                                                 const int clock_slot,
-                                                 const uint32_t* __restrict__ prefix) {
-    pdl_wait();  // the previous kernel of the frame is complete and visible
-    pdl_trigger();
-    clock_start(clk, clock_slot);
+__device__ __forceinline__ void compact_body(const uint32_t* __restrict__ keep_bits,
+                                             const uint64_t n_words,
+                                             const uint32_t* __restrict__ tile_count,
+                                             uint32_t* __restrict__ selected, FrameCounters* cnt,
+                                             const uint32_t* __restrict__ prefix,
+                                             const unsigned tile, const unsigned n_tiles) {
     __shared__ unsigned s_red[8];
     __shared__ unsigned s_warp[8];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned tile = blockIdx.x;
     // survivors before this tile: scanned by k_tile_prefix, or summed here
     unsigned pre = 0;
     if (prefix) {
@@ -574,7 +579,7 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ ke
         before += k < int(warp) ? s_warp[k] : 0u;
         total += s_warp[k];
     }
-    if (tile == gridDim.x - 1 && threadIdx.x == 0) cnt->n_selected = uint64_t(base) + total;
+    if (tile == n_tiles - 1 && threadIdx.x == 0) cnt->n_selected = uint64_t(base) + total;
     const unsigned long long pos = uint64_t(base) + before;
     const unsigned lt = (1u << lane) - 1u;
     unsigned nz = __ballot_sync(0xffffffffu, keepw != 0u);
@@ -587,6 +592,19 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ ke
         if ((word >> lane) & 1u)
             selected[pos + at + __popc(word & lt)] = uint32_t(warp_node + uint64_t(j) * 32 + lane);
     }
+}
+
+__global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ keep_bits,
+                                                 const uint64_t n_words,
+                                                 const uint32_t* __restrict__ tile_count,
+                                                 uint32_t* __restrict__ selected,
+                                                 FrameCounters* cnt, FilterClock* clk,
+                                                 const int clock_slot,
+                                                 const uint32_t* __restrict__ prefix) {
+    pdl_wait();  // the previous kernel of the frame is complete and visible
+    pdl_trigger();
+    clock_start(clk, clock_slot);
+    compact_body(keep_bits, n_words, tile_count, selected, cnt, prefix, blockIdx.x, gridDim.x);
     clock_end(clk, clock_slot);
 }
 
@@ -719,7 +737,8 @@ void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand
     const uint64_t split = t.leaf_begin;  // [split, n) are all leaves
     if (split > 0) {
         const uint64_t groups = (split + 31) / 32;
-        const unsigned grid = unsigned(std::min<uint64_t>((groups + 7) / 8, uint64_t(sm_count()) * 3));
+        const unsigned grid =
+            unsigned(std::min<uint64_t>((groups + 7) / 8, uint64_t(sm_count()) * MARK_MIN_CTAS));
         launch_pdl(k_mark_internal, grid, kMarkBlock, 0, s, g, f, t, tau_r, cand_bits, qint_bits,
                    clk);
         const uint64_t per = uint64_t(kSelectBlock) * kSelectItems;
@@ -740,6 +759,219 @@ void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand
     launch_pdl(k_compact, unsigned(T), 256, 0, s, static_cast<const uint32_t*>(cand_bits),
                (t.n + 31) / 32, static_cast<const uint32_t*>(tile_count), selected, cnt, clk, 3,
                static_cast<const uint32_t*>(prefix));
+}
+
+// ---- multi-view filter (SURVEY 8(e)'s option: several views per pass) ----
+// One pass over the node arrays serves up to kMaxViews views of the same tree:
+// F1 loads each internal node's three records once and decides it for every
+// view; F3 loads each leaf's parent index once, tests the blk bit of every view
+// and fetches the geo record once if any view needs it.  F2 and F4 run per view
+// (blockIdx.y) with their single-view code.  Every output is the single-view
+// filter's, bit for bit (each view's decisions are the same FP32 / FP64 code).
+struct ViewSetDev {
+    Geom g[kMaxViews];
+    GeomF f[kMaxViews];
+    uint32_t* cand[kMaxViews];
+    uint32_t* qint[kMaxViews];
+    uint32_t* tile_count[kMaxViews];  // survivor counts, then (large trees) their prefix
+    uint32_t* selected[kMaxViews];
+    FrameCounters* cnt[kMaxViews];
+    int n;
+};
+
+__global__ void __launch_bounds__(kMarkBlock, MARK_MIN_CTAS) k_mark_views(
+    const __grid_constant__ ViewSetDev vs, const __grid_constant__ DevTree t, const double tau_r) {
+    pdl_wait();
+    pdl_trigger();
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t end = t.leaf_begin;
+    const uint64_t n_groups = (end + 31) / 32;
+    const uint64_t stride = uint64_t(gridDim.x) * (kMarkBlock / 32);
+    uint64_t grp = uint64_t(blockIdx.x) * (kMarkBlock / 32) + (threadIdx.x >> 5);
+    float4 a, sc, q;
+    auto load = [&](uint64_t gi) {
+        const uint64_t i = gi * 32 + lane;
+        if (gi < n_groups && i < end) {
+            a = __ldcs(t.geo + i);
+            sc = __ldcs(t.iscale + i);
+            q = __ldcs(t.iquat + i);
+        }
+    };
+    load(grp);
+    for (; grp < n_groups; grp += stride) {
+        const uint64_t i = grp * 32 + lane;
+        const float4 ca = a, csc = sc, cq = q;
+        load(grp + stride);
+#pragma unroll 1
+        for (int v = 0; v < vs.n; ++v) {
+            bool cand = false, qint = false;
+            if (i < end) {
+                bool vis;
+                decide_internal(vs.g[v], vs.f[v], t, i, ca, csc, cq, tau_r, vis, qint);
+                cand = vis && (csc.w != 0.0f || qint);
+            }
+            const unsigned cm = __ballot_sync(0xffffffffu, cand);
+            const unsigned qm = __ballot_sync(0xffffffffu, qint);
+            if (lane == 0) {
+                vs.cand[v][grp] = cm;
+                vs.qint[v][grp] = qm;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kSelectBlock) k_select_views(const __grid_constant__ ViewSetDev vs,
+                                                               const uint32_t* __restrict__ parent,
+                                                               const uint64_t end) {
+    pdl_wait();
+    pdl_trigger();
+    const int v = int(blockIdx.y);
+    select_body(vs.cand[v], vs.qint[v], parent, end, vs.tile_count[v], blockIdx.x);
+}
+
+__global__ void __launch_bounds__(256) k_leaves_views(const __grid_constant__ ViewSetDev vs,
+                                                      const __grid_constant__ DevTree t) {
+    pdl_wait();
+    pdl_trigger();
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t end = t.n;
+    const uint64_t wbase =
+        t.leaf_begin + (uint64_t(blockIdx.x) * 256 + (threadIdx.x & ~31u)) * kLeafPerLane;
+    if (wbase >= end) return;  // warp-uniform
+    uint32_t p[kLeafPerLane];
+#pragma unroll
+    for (int k = 0; k < kLeafPerLane; ++k) p[k] = __ldcs(t.parent + wbase + k * 32 + lane);
+    unsigned need[kMaxViews], any = 0;
+#pragma unroll
+    for (int v = 0; v < kMaxViews; ++v) {
+        need[v] = 0;
+        if (v < vs.n) {
+#pragma unroll
+            for (int k = 0; k < kLeafPerLane; ++k) {
+                const bool in = wbase + k * 32 + lane < end;
+                const bool blocked = p[k] != kRootParent &&
+                                     ((__ldg(vs.qint[v] + (p[k] >> 5)) >> (p[k] & 31)) & 1u);
+                need[v] |= (in && !blocked) ? (1u << k) : 0u;
+            }
+            any |= need[v];
+        }
+    }
+    float4 a[kLeafPerLane];
+#pragma unroll
+    for (int k = 0; k < kLeafPerLane; ++k)
+        if ((any >> k) & 1u) a[k] = __ldcs(t.geo + wbase + k * 32 + lane);
+#pragma unroll
+    for (int v = 0; v < kMaxViews; ++v) {
+        if (v >= vs.n) break;
+        unsigned keep = 0, undec = 0;
+#pragma unroll
+        for (int k = 0; k < kLeafPerLane; ++k) {
+            if ((need[v] >> k) & 1u) {
+                const int r = frustum_leaf_fp32(vs.f[v], a[k].x, a[k].y, a[k].z, a[k].w);
+                keep |= r == 1 ? (1u << k) : 0u;
+                undec |= r < 0 ? (1u << k) : 0u;
+            }
+        }
+        if (undec) {
+            for (int k = 0; k < kLeafPerLane; ++k)
+                if ((undec >> k) & 1u)
+                    keep |= vis_fp64(vs.g[v], t, wbase + k * 32 + lane) ? (1u << k) : 0u;
+        }
+        unsigned c = 0;
+#pragma unroll
+        for (int k = 0; k < kLeafPerLane; ++k) {
+            const uint32_t w = __ballot_sync(0xffffffffu, (keep >> k) & 1u);
+            if (lane == unsigned(k) && (wbase + k * 32) < end) vs.cand[v][(wbase >> 5) + k] = w;
+            c += __popc(w);
+        }
+        if (lane == 0 && c) count_survivors(vs.tile_count[v], wbase / kTileNodes, c);
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_tile_prefix_views(const __grid_constant__ ViewSetDev vs,
+                                                            const uint32_t n_tiles) {
+    // k_tile_prefix's scan for view blockIdx.y (large trees only)
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t* tile_count = vs.tile_count[blockIdx.y];
+    uint32_t* prefix = vs.tile_count[blockIdx.y] + n_tiles;
+    __shared__ uint32_t s_warp[32];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t per = (n_tiles + 1023) / 1024;
+    const uint32_t t0 = min(n_tiles, threadIdx.x * per), t1 = min(n_tiles, t0 + per);
+    uint32_t sum = 0;
+    for (uint32_t t = t0; t < t1; ++t) sum += tile_count[t];
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= unsigned(o)) incl += u;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t u = s_warp[lane];
+        uint32_t wi = u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= unsigned(o)) wi += x;
+        }
+        s_warp[lane] = wi - u;
+    }
+    __syncthreads();
+    uint32_t run = s_warp[warp] + (incl - sum);
+    for (uint32_t t = t0; t < t1; ++t) {
+        prefix[t] = run;
+        run += tile_count[t];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_compact_views(const __grid_constant__ ViewSetDev vs,
+                                                       const uint64_t n_words,
+                                                       const int with_prefix) {
+    pdl_wait();
+    pdl_trigger();
+    const int v = int(blockIdx.y);
+    compact_body(vs.cand[v], n_words, vs.tile_count[v], vs.selected[v], vs.cnt[v],
+                 with_prefix ? vs.tile_count[v] + gridDim.x : nullptr, blockIdx.x, gridDim.x);
+}
+
+void launch_filter_views(const ViewSet& views, const DevTree& t, double tau_r, cudaStream_t s) {
+    if (views.n <= 0 || t.n == 0) return;
+    ViewSetDev vs;
+    std::memset(&vs, 0, sizeof(vs));
+    vs.n = views.n;
+    for (int v = 0; v < views.n; ++v) {
+        vs.g[v] = views.g[v];
+        vs.f[v] = make_geomf(views.g[v], tau_r, t.max_l1);
+        vs.cand[v] = views.cand[v];
+        vs.qint[v] = views.qint[v];
+        vs.tile_count[v] = views.tile_count[v];
+        vs.selected[v] = views.selected[v];
+        vs.cnt[v] = views.cnt[v];
+    }
+    const uint64_t split = t.leaf_begin;
+    if (split > 0) {
+        const uint64_t groups = (split + 31) / 32;
+        const unsigned grid =
+            unsigned(std::min<uint64_t>((groups + 7) / 8, uint64_t(sm_count()) * MARK_MIN_CTAS));
+        launch_pdl(k_mark_views, grid, kMarkBlock, 0, s, vs, t, tau_r);
+        const uint64_t per = uint64_t(kSelectBlock) * kSelectItems;
+        launch_pdl(k_select_views, dim3(unsigned((split + per - 1) / per), unsigned(views.n)),
+                   kSelectBlock, 0, s, vs, static_cast<const uint32_t*>(t.parent), split);
+    }
+    if (t.n > split) {
+        const uint64_t per_cta = 256ull * kLeafPerLane;
+        launch_pdl(k_leaves_views, unsigned((t.n - split + per_cta - 1) / per_cta), 256, 0, s, vs,
+                   t);
+    }
+    const uint64_t T = count_tiles(t.n);
+    const int with_prefix = T > kDirectPrefixTiles ? 1 : 0;
+    if (with_prefix)
+        launch_pdl(k_tile_prefix_views, dim3(1, unsigned(views.n)), 1024, 0, s, vs, uint32_t(T));
+    launch_pdl(k_compact_views, dim3(unsigned(T), unsigned(views.n)), 256, 0, s, vs,
+               (t.n + 31) / 32, with_prefix);
 }
 
 void launch_mark_debug(const Geom& g, const DevTree& t, uint64_t begin, uint64_t end,

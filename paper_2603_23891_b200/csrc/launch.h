@@ -58,6 +58,21 @@ void launch_filter(const Geom& g, const DevTree& t, double tau_r, uint32_t* cand
                    uint32_t* qint_bits, uint32_t* tile_count, uint32_t* selected,
                    FrameCounters* cnt, cudaStream_t s, cudaEvent_t mid = nullptr,
                    FilterClock* clk = nullptr);
+// Multi-view filter: up to kMaxViews views of one tree in one pass over the node
+// arrays (F1 and F3 shared, F2 and F4 per view); each view's outputs equal
+// launch_filter's for that view.  The per-view buffers must be zeroed as for
+// launch_filter (tile counts, counters).
+constexpr int kMaxViews = 4;
+struct ViewSet {
+    int n = 0;
+    Geom g[kMaxViews];
+    uint32_t* cand[kMaxViews] = {};
+    uint32_t* qint[kMaxViews] = {};
+    uint32_t* tile_count[kMaxViews] = {};
+    uint32_t* selected[kMaxViews] = {};
+    FrameCounters* cnt[kMaxViews] = {};
+};
+void launch_filter_views(const ViewSet& views, const DevTree& t, double tau_r, cudaStream_t s);
 // Serial (level-wise) filter, filter.cpp:60-113: one kernel per level, then
 // the ordered compaction.  level_flag[n_levels] (zeroed) marks the levels with
 // an active node; level_events (nullable, n_levels + 1) time the levels.

@@ -397,10 +397,74 @@ void GpuScene::set_sh(int degree, const float* host, uint64_t n) {
 
 void GpuScene::set_inflight(int n) {
     if (n < 1 || n > kMaxInflight)
-        throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1 to 4");
+        throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1 to 8");
     join();
     inflight_ = n;
     make_contexts(n);
+}
+
+void GpuScene::enqueue_views_async(const lodgs_camera* cams, uint64_t n,
+                                   const lodgs_render_params& p, float* const* images_host) {
+    DeviceGuard dg(device_);
+    constexpr uint32_t kPerFrameOnly = LODGS_RENDER_STAGE_TIMING | LODGS_RENDER_FILTER_SERIAL |
+                                       LODGS_RENDER_COLLECT_KPC | LODGS_RENDER_KEEP_PAIRS;
+    bool same_res = true;
+    for (uint64_t i = 0; i < n; ++i) {
+        check_frame(cams[i], p);
+        same_res = same_res && cams[i].width == cams[0].width && cams[i].height == cams[0].height;
+    }
+    if (n == 0) return;
+    // groups of V views alternate between two disjoint sets of V contexts, so a group's
+    // filter waits only for the frames of the group before last, and overlaps the
+    // previous group's pipelines (one set would drain the GPU between groups)
+    const int V = std::min(kMaxViews, inflight_ / 2);
+    if (V < 2 || profiling_ || !ctl_ || (p.flags & kPerFrameOnly) || !same_res) {
+        for (uint64_t i = 0; i < n; ++i)
+            enqueue_async(cams[i], p, images_host ? images_host[i] : nullptr);
+        return;
+    }
+    make_contexts(inflight_);
+    ensure_resolution(int(cams[0].width), int(cams[0].height));  // every context follows
+    for (uint64_t base = 0; base < n; base += uint64_t(V)) {
+        const int nv = int(std::min<uint64_t>(uint64_t(V), n - base));
+        GpuScene* ctx[kMaxViews] = {};
+        for (int j = 0; j < nv; ++j) {
+            ctx[j] = context(int((async_frames_ + uint64_t(j)) % uint64_t(2 * V)));
+            if (!ctx[j]->view_ev_)
+                FGS_CUDA(cudaEventCreateWithFlags(&ctx[j]->view_ev_, cudaEventDisableTiming));
+        }
+        async_frames_ += uint64_t(V);  // the next group starts on the other context set
+        // the group's filter runs on its first context's stream, after the control
+        // stream's work and after every member context's previous frame
+        cudaStream_t fs = ctx[0]->stream_;
+        FGS_CUDA(cudaEventRecord(fork_ev_, ctl_));
+        FGS_CUDA(cudaStreamWaitEvent(fs, fork_ev_, 0));
+        ViewSet vs;
+        vs.n = nv;
+        for (int j = 0; j < nv; ++j) {
+            if (j > 0) {
+                FGS_CUDA(cudaEventRecord(ctx[j]->view_ev_, ctx[j]->stream_));
+                FGS_CUDA(cudaStreamWaitEvent(fs, ctx[j]->view_ev_, 0));
+            }
+            launch_zero(ctx[j]->zero_.p, ctx[j]->zero_bytes_, fs);
+            vs.g[j] = camera_geom(cams[base + uint64_t(j)]);
+            vs.cand[j] = ctx[j]->cand_bits_.p;
+            vs.qint[j] = ctx[j]->qint_bits_.p;
+            vs.tile_count[j] = reinterpret_cast<uint32_t*>(ctx[j]->d_status_select_);
+            vs.selected[j] = ctx[j]->selected_.p;
+            vs.cnt[j] = ctx[j]->d_counters_;
+        }
+        launch_filter_views(vs, tree_, p.tau_r, fs);
+        FGS_CUDA(cudaGetLastError());
+        FGS_CUDA(cudaEventRecord(ctx[0]->view_ev_, fs));
+        for (int j = 0; j < nv; ++j) {
+            if (j > 0) FGS_CUDA(cudaStreamWaitEvent(ctx[j]->stream_, ctx[0]->view_ev_, 0));
+            ctx[j]->enqueue_frame(cams[base + uint64_t(j)], p,
+                                  images_host ? images_host[base + uint64_t(j)] : nullptr,
+                                  /*prefiltered=*/true);
+        }
+        last_frame_ = ctx[nv - 1];
+    }
 }
 
 void GpuScene::join() {
@@ -456,6 +520,7 @@ GpuScene::~GpuScene() {
         for (auto& e : join_ev_) cudaEventDestroy(e);
     }
     if (stream_) cudaStreamSynchronize(stream_);
+    if (view_ev_) cudaEventDestroy(view_ev_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (auto& a : prof_events_)
@@ -547,7 +612,7 @@ void GpuScene::clear_frame_state() {
 }
 
 void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int w, int h,
-                                bool timing) {
+                                bool timing, bool prefiltered) {
     (void)w;
     (void)h;
     const int n_tiles = res_.tiles_x * res_.tiles_y;
@@ -565,10 +630,12 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
         }
         pe = prof_events_[prof_used_++].data();
     }
-    clear_frame_state();
+    if (!prefiltered) clear_frame_state();
     if (timing) FGS_CUDA(cudaEventRecord(ev_[0], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[0], stream_));
-    if (p.flags & LODGS_RENDER_FILTER_SERIAL) {
+    if (prefiltered) {
+        // selected list and counters already in place (enqueue_views_async)
+    } else if (p.flags & LODGS_RENDER_FILTER_SERIAL) {
         level_flag_.alloc(uint64_t(n_levels()) + 1);
         FGS_CUDA(cudaMemsetAsync(level_flag_.p, 0, level_flag_.bytes(), stream_));
         launch_filter_serial(g, tree_, p.tau_r, level_begin_.data(), n_levels(), cand_bits_.p,
@@ -632,9 +699,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     FGS_CUDA(cudaGetLastError());
 }
 
-void GpuScene::enqueue_frame(const lodgs_camera& cam, const lodgs_render_params& p,
-                             float* image_host) {
-    DeviceGuard dg(device_);
+void GpuScene::check_frame(const lodgs_camera& cam, const lodgs_render_params& p) const {
     const auto cv = validate_camera(cam);
     if (!cv.empty()) throw Error(LODGS_ERR_VALIDATION, join_violations("invalid camera", cv, cv.size()));
     if (!(p.tau_r > 0)) throw Error(LODGS_ERR_VALIDATION, "filter config: tau_r > 0");
@@ -643,12 +708,20 @@ void GpuScene::enqueue_frame(const lodgs_camera& cam, const lodgs_render_params&
     if (p.shrink_kind != LODGS_SHRINK_THREE_SIGMA && !(p.tau > 0.0 && p.tau < 1.0))
         throw Error(LODGS_ERR_VALIDATION,
                     "render: shrink tau in (0,1); adaptive needs calibration first");
-    ensure_resolution(int(cam.width), int(cam.height));
+}
+
+// prefiltered: the frame's filter already ran (enqueue_views_async) and left its
+// selected list and counters in this context's buffers
+void GpuScene::enqueue_frame(const lodgs_camera& cam, const lodgs_render_params& p,
+                             float* image_host, bool prefiltered) {
+    DeviceGuard dg(device_);
+    check_frame(cam, p);
+    if (!prefiltered) ensure_resolution(int(cam.width), int(cam.height));
     const Geom g = camera_geom(cam);
     last_timing_ = (p.flags & LODGS_RENDER_STAGE_TIMING) != 0;
     last_keep_ = (p.flags & LODGS_RENDER_KEEP_PAIRS) != 0;
     last_exact_ = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
-    enqueue_pipeline(g, p, int(cam.width), int(cam.height), last_timing_);
+    enqueue_pipeline(g, p, int(cam.width), int(cam.height), last_timing_, prefiltered);
     FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
                              cudaMemcpyDeviceToHost, stream_));
     if (image_host) {

@@ -78,7 +78,8 @@ public:
 
     // One frame, enqueued only.  Counters for the frame land in host_counters()
     // once the stream reaches the end of the frame.
-    void enqueue_frame(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host);
+    void enqueue_frame(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host,
+                       bool prefiltered = false);
     // Wait + stats of the last frame.  Throws Error on overflow / non-finite.
     void finish(lodgs_render_stats* stats);
     void render(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host,
@@ -133,6 +134,10 @@ public:
     void set_sh(int degree, const float* sh_rest, uint64_t n_nodes);
     uint32_t sh_launches() const { return tree_.sh_k > 0 ? 1u : 0u; }
     void enqueue_async(const lodgs_camera& cam, const lodgs_render_params& p, float* image_host);
+    // n frames over the in-flight contexts, the filter shared by each group of up to
+    // kMaxViews consecutive frames (launch_filter_views); else as enqueue_async
+    void enqueue_views_async(const lodgs_camera* cams, uint64_t n, const lodgs_render_params& p,
+                             float* const* images_host = nullptr);
     void join();
     void sync_async(lodgs_render_stats* stats);
 
@@ -157,7 +162,9 @@ private:
     void ensure_resolution(int w, int h);
     void build_readback_maps();
     void clear_frame_state();
-    void enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int w, int h, bool timing);
+    void enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int w, int h, bool timing,
+                          bool prefiltered = false);
+    void check_frame(const lodgs_camera& cam, const lodgs_render_params& p) const;
 
     int device_;
     cudaStream_t stream_ = nullptr;
@@ -168,13 +175,14 @@ private:
 #ifndef FGS_INFLIGHT_DEFAULT
 #define FGS_INFLIGHT_DEFAULT 4
 #endif
-    static constexpr int kMaxInflight = 4;
+    static constexpr int kMaxInflight = 8;
     int inflight_ = FGS_INFLIGHT_DEFAULT;
     GpuScene* context(int i);
     void make_contexts(int n);
     std::unique_ptr<GpuScene> twin_;
     cudaStream_t ctl_ = nullptr;
-    cudaEvent_t fork_ev_ = nullptr, join_ev_[4] = {};
+    cudaEvent_t fork_ev_ = nullptr, join_ev_[kMaxInflight] = {};
+    cudaEvent_t view_ev_ = nullptr;  // this context's last enqueued work (multi-view groups)
     uint64_t async_frames_ = 0;
     GpuScene* last_frame_ = nullptr;
     DevBuf<unsigned> level_flag_;        // serial filter: level had an active node

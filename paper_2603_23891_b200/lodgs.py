@@ -179,7 +179,7 @@ ABI_SYMBOLS = (
     "lodgs_gpu_host_free", "lodgs_gpu_read_image_rgb8", "lodgs_gpu_set_reference_image",
     "lodgs_gpu_compare_reference", "lodgs_gpu_image_metrics", "lodgs_gpu_scene_load",
     "lodgs_gpu_scene_info", "lodgs_gpu_scene_set_inflight", "lodgs_gpu_join",
-    "lodgs_gpu_scene_set_sh",
+    "lodgs_gpu_scene_set_sh", "lodgs_gpu_render_views_async",
 )
 
 _lib = None
@@ -235,6 +235,7 @@ def load_library():
         "lodgs_gpu_read_image_rgb8": (C.c_int, [P, P]),
         "lodgs_gpu_scene_set_inflight": (C.c_int, [P, C.c_int]),
         "lodgs_gpu_scene_set_sh": (C.c_int, [P, C.c_int, P, C.c_uint64]),
+        "lodgs_gpu_render_views_async": (C.c_int, [P, P, C.c_uint64, P, P]),
         "lodgs_gpu_join": (C.c_int, [P]),
         "lodgs_gpu_scene_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(P), _DP]),
         "lodgs_gpu_scene_info": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), P,
@@ -817,12 +818,23 @@ class GpuScene:
         c = cam.to_c()
         _check(self._lib.lodgs_gpu_render_async(self._h, C.byref(c), C.byref(params), image_host_ptr))
 
+    def render_views_async(self, cams, params: RenderParamsC, host_ptrs=None) -> None:
+        """len(cams) frames as render_async calls, the LoD filter shared by each group of
+        up to 4 consecutive frames (one pass over the node arrays for the group);
+        host_ptrs (optional): one f32 image buffer per frame (raw pointers)."""
+        n = len(cams)
+        if n == 0:
+            return
+        cc = (CameraC * n)(*[c.to_c() for c in cams])
+        ptrs = (C.c_void_p * n)(*host_ptrs) if host_ptrs is not None else None
+        _check(self._lib.lodgs_gpu_render_views_async(self._h, cc, n, C.byref(params), ptrs))
+
     def join(self) -> None:
         """The control stream (stream_ptr) waits for every frame enqueued so far."""
         _check(self._lib.lodgs_gpu_join(self._h))
 
     def set_inflight(self, frames: int) -> None:
-        """Frames in flight for render_async (1 to 4; default 4)."""
+        """Frames in flight for render_async (1 to 8; default 4)."""
         _check(self._lib.lodgs_gpu_scene_set_inflight(self._h, int(frames)))
 
     def set_sh(self, degree: int, sh_rest=None) -> None:
