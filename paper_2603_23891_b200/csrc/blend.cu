@@ -99,6 +99,9 @@ struct WarpStage {
 struct PixState {
     float T, cr, cg, cb;
 };
+#ifndef BLEND_TMUL
+#define BLEND_TMUL 0
+#endif
 
 __device__ __forceinline__ void sample_fast(const float4 geo, const float4 ct, const float2 gb,
                                             float pxl, float pyl, PixState& p, bool& unsure) {
@@ -115,7 +118,11 @@ __device__ __forceinline__ void sample_fast(const float4 geo, const float4 ct, c
     p.cr = __fmaf_rn(ct.w, w, p.cr);
     p.cg = __fmaf_rn(gb.x, w, p.cg);
     p.cb = __fmaf_rn(gb.y, w, p.cb);
+#if BLEND_TMUL  // T (1 - alpha): one dependent operation fewer on the T chain
+    const float t = p.T * (1.0f - alpha);
+#else
     const float t = p.T - w;
+#endif
     p.T = t < 1e-4f ? 0.0f : t;
 }
 
@@ -147,7 +154,11 @@ __device__ __forceinline__ void sample_checked(const float4 geo, const float4 ct
     p.cr = __fmaf_rn(ct.w, w, p.cr);
     p.cg = __fmaf_rn(gb.x, w, p.cg);
     p.cb = __fmaf_rn(gb.y, w, p.cb);
+#if BLEND_TMUL
+    const float t = take ? p.T * (1.0f - alpha) : p.T;
+#else
     const float t = p.T - w;
+#endif
     p.T = t < 1e-4f ? 0.0f : t;
 }
 

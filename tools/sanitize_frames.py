@@ -1,7 +1,8 @@
 """Frames for compute-sanitizer runs (racecheck / synccheck / memcheck / initcheck):
 cfg-1 and cfg-3 frames through render_async with four frames in flight (the
 persistent blend's ticket queue and mbarrier ring, the DSMEM cluster scan, the
-filter's concurrent qint-word reads/writes), then every stage entry point once.
+filter's concurrent qint-word reads/writes), through render_views_async (the
+multi-view filter), an SH degree-3 frame, then every stage entry point once.
 Not a benchmark.
 
     compute-sanitizer --tool racecheck python tools/sanitize_frames.py --cfg 1
@@ -45,6 +46,16 @@ def main():
             s.render_async(cam, p, im.ctypes.data)
         st = s.sync()
         print(f"cfg{args.cfg}: {len(cams)} frames in flight, last n_pairs {st.n_pairs}")
+        # the multi-view filter: groups of four over two sets of four contexts
+        s.set_inflight(8)
+        s.render_views_async(cams + cams[::-1], p)
+        s.sync()
+        s.set_inflight(4)
+        # SH degree-3 colours (k_sh_colour)
+        rng = np.random.default_rng(1)
+        s.set_sh(3, rng.normal(0.0, 0.1, (tree.node_count(), 15, 3)).astype(np.float32))
+        s.render(cams[0], L.FilterConfig(3.0), mode)
+        s.set_sh(0)
         out = s.render(cams[0], L.FilterConfig(3.0), mode, L.RenderOptions(collect_kpc=True))
         s.render(cams[0], L.FilterConfig(3.0), mode, L.RenderOptions(exact_blend=True))
         s.render(cams[0], L.FilterConfig(3.0), mode, L.RenderOptions(filter_mode="serial"))
