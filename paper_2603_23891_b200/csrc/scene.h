@@ -236,8 +236,12 @@ private:
     bool last_exact_ = false;
     // pipelined batches: second image buffer, copy stream, per-frame counters
     float* image_target_ = nullptr;  // blend output override (nullptr: res_.image)
+// render_batch's image ring: the blend of frame i waits for the D2H copy of frame
+// i - kBatchBufs; a deeper ring absorbs the jitter between the (faster) compute and the
+// PCIe-bound copies (e2e f32 frames/s, cfg 3: 3 / 4 / 6 buffers 2,033-2,047 / 2,082-2,103 /
+// 2,129; the link alone moves 56.4 GB/s = 2,265 frames/s)
 #ifndef FGS_BATCH_BUFS
-#define FGS_BATCH_BUFS 3
+#define FGS_BATCH_BUFS 6
 #endif
     static constexpr int kBatchBufs = FGS_BATCH_BUFS;  // render_batch image ring
     DevBuf<float> image2_[kBatchBufs - 1];
