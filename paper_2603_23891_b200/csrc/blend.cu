@@ -2072,6 +2072,19 @@ static void launch_cpa(const uint32_t* offsets, const uint32_t* order,
                height, tiles_x, uint32_t(n_tiles), ticket, image);
 }
 
+void launch_blend_tiles(const uint32_t* offsets, const uint32_t* order, int n_order,
+                        int frame_tiles, const unsigned long long* keys, const Gauss64* g64,
+                        const Gauss32* g32, int width, int height, int tiles_x, unsigned* ticket,
+                        float* image, cudaStream_t s) {
+    if (n_order <= 0) return;
+    if (frame_tiles > kCpaBigFrameTiles)
+        launch_cpa<kCpaStagesBig>(offsets, order, keys, g64, g32, width, height, tiles_x, n_order,
+                                  ticket, image, s);
+    else
+        launch_cpa<kCpaStages>(offsets, order, keys, g64, g32, width, height, tiles_x, n_order,
+                               ticket, image, s);
+}
+
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,

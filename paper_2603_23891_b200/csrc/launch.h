@@ -153,6 +153,17 @@ void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
 // tile's records stream into shared memory with cp.async.bulk), kBlendGather4
 // (TMA tile::gather4 of the n_records slot-indexed g32/g64 rows).
 enum BlendKernel { kBlendWsp = 0, kBlendTma = 1, kBlendGather4 = 2, kBlendCpa = 3 };
+// Banded blend of a synchronous frame: each band's image rows are copied to the host
+// while the next band blends (GpuScene::enqueue_pipeline).
+constexpr int kMaxBands = 8;
+void launch_band_order(const uint32_t* order, int n_tiles, int tiles_x, int band_rows,
+                       int n_bands, uint32_t* out, unsigned* tickets, cudaStream_t s);
+// k_blend_cpa over the n_order tiles of `order` only (one band); frame_tiles picks the
+// ring depth as for the whole frame
+void launch_blend_tiles(const uint32_t* offsets, const uint32_t* order, int n_order,
+                        int frame_tiles, const unsigned long long* keys, const Gauss64* g64,
+                        const Gauss32* g32, int width, int height, int tiles_x, unsigned* ticket,
+                        float* image, cudaStream_t s);
 void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned long long* keys,
                   const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64, int width,
                   int height, int tiles_x, int tiles_y, bool exact, float* image, cudaStream_t s,

@@ -96,4 +96,64 @@ void launch_zero(void* p, uint64_t bytes, cudaStream_t s) {
     launch_pdl(k_zero_words, grid, 256, 0, s, reinterpret_cast<uint4*>(p), n16);
 }
 
+// Banded blend of a synchronous frame (GpuScene::enqueue_pipeline): the frame's
+// heavy-first tile order stably partitioned by horizontal band of band_rows tile rows,
+// so band b's tiles occupy [b band_rows tiles_x, ...) of `out` in heavy-first order;
+// the bands' blend tickets are cleared.  One CTA: thread k owns a contiguous run of
+// the order, counts it per band, one block scan per band, a stable scatter.
+constexpr int kBandThreads = 1024;
+__global__ void __launch_bounds__(kBandThreads) k_band_order(const uint32_t* __restrict__ order,
+                                                             const int n_tiles, const int tiles_x,
+                                                             const int band_rows,
+                                                             const int n_bands,
+                                                             uint32_t* __restrict__ out,
+                                                             unsigned* tickets) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ uint32_t s_warp[kMaxBands][32];
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < unsigned(n_bands)) tickets[tid] = 0u;
+    const int per = (n_tiles + kBandThreads - 1) / kBandThreads;
+    const int t0 = min(n_tiles, int(tid) * per), t1 = min(n_tiles, t0 + per);
+    uint32_t cnt[kMaxBands];
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b) cnt[b] = 0u;
+    for (int i = t0; i < t1; ++i) {
+        const int b = int(order[i]) / tiles_x / band_rows;
+#pragma unroll
+        for (int k = 0; k < kMaxBands; ++k) cnt[k] += k == b ? 1u : 0u;
+    }
+    // exclusive prefix of each band's counts over the threads
+    uint32_t pre[kMaxBands];
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b) {
+        uint32_t incl = cnt[b];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= unsigned(o)) incl += v;
+        }
+        if (lane == 31) s_warp[b][warp] = incl;
+        pre[b] = incl - cnt[b];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b)
+        for (unsigned w = 0; w < warp; ++w) pre[b] += s_warp[b][w];
+    for (int i = t0; i < t1; ++i) {
+        const uint32_t t = order[i];
+        const int b = int(t) / tiles_x / band_rows;
+#pragma unroll
+        for (int k = 0; k < kMaxBands; ++k)
+            if (k == b) out[uint32_t(k * band_rows * tiles_x) + pre[k]++] = t;
+    }
+}
+
+void launch_band_order(const uint32_t* order, int n_tiles, int tiles_x, int band_rows,
+                       int n_bands, uint32_t* out, unsigned* tickets, cudaStream_t s) {
+    if (n_tiles <= 0) return;
+    launch_pdl(k_band_order, 1, kBandThreads, 0, s, order, n_tiles, tiles_x, band_rows, n_bands,
+               out, tickets);
+}
+
 }  // namespace fgs

@@ -535,6 +535,10 @@ GpuScene::~GpuScene() {
             cudaEventDestroy(copy_done_[k]);
         }
     }
+    if (band_done_) {
+        for (auto& e : band_ev_) cudaEventDestroy(e);
+        cudaEventDestroy(band_done_);
+    }
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -689,6 +693,40 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     if (p.flags & LODGS_RENDER_COLLECT_KPC) {
         launch_blend_exact_kpc(res_.tile_offsets.p, keys_.p, g64_.p, col64_.p, res_.width,
                                res_.height, res_.tiles_x, res_.tiles_y, img_out, kpc_.p, stream_);
+    } else if (band_host_ && bk == kBlendCpa && !exact && !image_target_ && res_.tiles_y >= 2) {
+        // synchronous frame with a host image: blend kSyncBands horizontal bands (each
+        // in heavy-first tile order) and copy each band's rows to the host while the
+        // next one blends -- the D2H of the f32 image (~440 us at 1080p) then overlaps
+        // the blend instead of following it
+#ifndef FGS_SYNC_BANDS
+#define FGS_SYNC_BANDS 4
+#endif
+        constexpr int kSyncBands = FGS_SYNC_BANDS;
+        static_assert(kSyncBands <= kMaxBands, "band tickets");
+        const int band_rows = (res_.tiles_y + kSyncBands - 1) / kSyncBands;
+        const int nbands = (res_.tiles_y + band_rows - 1) / band_rows;
+        band_order_.alloc(uint64_t(n_tiles));
+        band_ticket_.alloc(kMaxBands);
+        ensure_copy_stream();
+        launch_band_order(res_.tile_order.p, n_tiles, res_.tiles_x, band_rows, nbands,
+                          band_order_.p, band_ticket_.p, stream_);
+        const uint64_t row_floats = uint64_t(res_.width) * 3;
+        for (int b = 0; b < nbands; ++b) {
+            const int r0 = b * band_rows, r1 = std::min(res_.tiles_y, r0 + band_rows);
+            launch_blend_tiles(res_.tile_offsets.p, band_order_.p + uint64_t(r0) * res_.tiles_x,
+                               (r1 - r0) * res_.tiles_x, n_tiles, keys_.p, g64_.p, g32_.p,
+                               res_.width, res_.height, res_.tiles_x, band_ticket_.p + b, img_out,
+                               stream_);
+            FGS_CUDA(cudaEventRecord(band_ev_[b], stream_));
+            FGS_CUDA(cudaStreamWaitEvent(copy_stream_, band_ev_[b], 0));
+            const uint64_t y0 = uint64_t(r0) * kTile;
+            const uint64_t y1 = std::min<uint64_t>(uint64_t(res_.height), uint64_t(r1) * kTile);
+            FGS_CUDA(cudaMemcpyAsync(band_host_ + y0 * row_floats, img_out + y0 * row_floats,
+                                     (y1 - y0) * row_floats * sizeof(float),
+                                     cudaMemcpyDeviceToHost, copy_stream_));
+        }
+        FGS_CUDA(cudaEventRecord(band_done_, copy_stream_));
+        band_copied_ = true;  // the stream joins the copies after the blend's timing events
     } else {
         launch_blend(res_.tile_offsets.p, res_.tile_order.p, keys_.p, g64_.p, g32_.p, col64_.p,
                      res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact, img_out, stream_,
@@ -696,6 +734,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     }
     if (timing) FGS_CUDA(cudaEventRecord(ev_[4], stream_));
     if (pe) FGS_CUDA(cudaEventRecord(pe[5], stream_));
+    if (band_copied_) FGS_CUDA(cudaStreamWaitEvent(stream_, band_done_, 0));
     FGS_CUDA(cudaGetLastError());
 }
 
@@ -721,10 +760,13 @@ void GpuScene::enqueue_frame(const lodgs_camera& cam, const lodgs_render_params&
     last_timing_ = (p.flags & LODGS_RENDER_STAGE_TIMING) != 0;
     last_keep_ = (p.flags & LODGS_RENDER_KEEP_PAIRS) != 0;
     last_exact_ = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
+    band_host_ = (image_host && !(p.flags & LODGS_RENDER_OUTPUT_RGB8)) ? image_host : nullptr;
+    band_copied_ = false;
     enqueue_pipeline(g, p, int(cam.width), int(cam.height), last_timing_, prefiltered);
+    band_host_ = nullptr;
     FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
                              cudaMemcpyDeviceToHost, stream_));
-    if (image_host) {
+    if (image_host && !band_copied_) {
         if (p.flags & LODGS_RENDER_OUTPUT_RGB8) {
             // save_ppm bytes (image.cpp:19-22): the host buffer is W*H*3 bytes
             rgb8_.alloc(image_floats());
@@ -735,6 +777,20 @@ void GpuScene::enqueue_frame(const lodgs_camera& cam, const lodgs_render_params&
             FGS_CUDA(cudaMemcpyAsync(image_host, res_.image.p, image_floats() * sizeof(float),
                                      cudaMemcpyDeviceToHost, stream_));
         }
+    }
+}
+
+void GpuScene::ensure_copy_stream() {
+    if (!copy_stream_) {
+        FGS_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+        for (int k = 0; k < kBatchBufs; ++k) {
+            FGS_CUDA(cudaEventCreateWithFlags(&frame_done_[k], cudaEventDisableTiming));
+            FGS_CUDA(cudaEventCreateWithFlags(&copy_done_[k], cudaEventDisableTiming));
+        }
+    }
+    if (!band_done_) {
+        for (auto& e : band_ev_) FGS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        FGS_CUDA(cudaEventCreateWithFlags(&band_done_, cudaEventDisableTiming));
     }
 }
 
@@ -815,13 +871,7 @@ void GpuScene::render_batch(const lodgs_camera* cams, uint64_t n, const lodgs_re
         throw Error(LODGS_ERR_VALIDATION,
                     "render: shrink tau in (0,1); adaptive needs calibration first");
     ensure_resolution(int(cams[0].width), int(cams[0].height));
-    if (!copy_stream_) {
-        FGS_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
-        for (int k = 0; k < kBatchBufs; ++k) {
-            FGS_CUDA(cudaEventCreateWithFlags(&frame_done_[k], cudaEventDisableTiming));
-            FGS_CUDA(cudaEventCreateWithFlags(&copy_done_[k], cudaEventDisableTiming));
-        }
-    }
+    ensure_copy_stream();
     frame_log_.alloc(std::max<uint64_t>(n, 1024));  // one allocation for typical batches
     if (h_batch_cap_ < n) {  // pinned, grown geometrically (cudaMallocHost is slow)
         const uint64_t cap = std::max<uint64_t>(n, std::max<uint64_t>(1024, 2 * h_batch_cap_));

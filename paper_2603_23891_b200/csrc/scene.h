@@ -236,6 +236,14 @@ private:
     bool last_exact_ = false;
     // pipelined batches: second image buffer, copy stream, per-frame counters
     float* image_target_ = nullptr;  // blend output override (nullptr: res_.image)
+    // banded blend + copy of a frame with a host image (enqueue_frame -> enqueue_pipeline):
+    // each band's rows go to band_host_ on copy_stream_ while the next band blends
+    float* band_host_ = nullptr;
+    bool band_copied_ = false;
+    DevBuf<uint32_t> band_order_;
+    DevBuf<unsigned> band_ticket_;
+    cudaEvent_t band_ev_[kMaxBands] = {}, band_done_ = nullptr;
+    void ensure_copy_stream();
 // render_batch's image ring: the blend of frame i waits for the D2H copy of frame
 // i - kBatchBufs; a deeper ring absorbs the jitter between the (faster) compute and the
 // PCIe-bound copies (e2e f32 frames/s, cfg 3: 3 / 4 / 6 buffers 2,033-2,047 / 2,082-2,103 /
