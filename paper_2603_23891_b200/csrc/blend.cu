@@ -136,7 +136,7 @@ __device__ __forceinline__ void blend_sample_fast(const WarpStage& st, int k, fl
 __device__ __forceinline__ void sample_checked(const float4 geo, const float4 ct, const float2 gb,
                                                uint32_t gid, float pxl, float pyl, double px,
                                                double py, const Gauss64* __restrict__ g64,
-                                               PixState& p) {
+                                               const Gauss32* __restrict__ g32, PixState& p) {
     const float dx = pxl - geo.x, dy = pyl - geo.y;
     const float Q = __fmaf_rn(geo.z * dx, dx, geo.w * dy * dy);
     const float ev = __fmaf_rn(ct.x * dx, dy, Q);
@@ -146,7 +146,8 @@ __device__ __forceinline__ void sample_checked(const float4 geo, const float4 ct
     float alpha = fminf(ct.z * ex2_approx(-ev), 0.99f);
     if (fabsf(d) <= margin && p.T > 0.0f) {
         const Gauss64& G = g64[gid];
-        const double a64 = alpha_exact(G.mx, G.my, G.ca, G.cb, G.cc, G.op, px, py);
+        const double2 m = *reinterpret_cast<const double2*>(&g32[gid].mx);
+        const double a64 = alpha_exact(m.x, m.y, G.ca, G.cb, G.cc, G.op, px, py);
         take = a64 >= kMinAlpha;
         alpha = float(a64);
     }
@@ -165,8 +166,9 @@ __device__ __forceinline__ void sample_checked(const float4 geo, const float4 ct
 __device__ __forceinline__ void blend_sample_checked(const WarpStage& st, int k, float pxl,
                                                      float pyl, double px, double py,
                                                      const Gauss64* __restrict__ g64,
+                                                     const Gauss32* __restrict__ g32,
                                                      PixState& p) {
-    sample_checked(st.geo[k], st.ct[k], st.gb[k], st.gid[k], pxl, pyl, px, py, g64, p);
+    sample_checked(st.geo[k], st.ct[k], st.gb[k], st.gid[k], pxl, pyl, px, py, g64, g32, p);
 }
 
 #ifndef BLEND_PREFETCH2
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kFastThreads, BLEND_MIN_CTAS) k_blend_fast(
     };
     auto load_rec = [&](uint32_t gi, Rec& r) {
         if (gi != kNone) {
-            r.m = *reinterpret_cast<const double2*>(&g64[gi].mx);
+            r.m = *reinterpret_cast<const double2*>(&g32[gi].mx);
             r.q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
             r.col = *reinterpret_cast<const float4*>(&g32[gi].op);
             r.h = *reinterpret_cast<const float2*>(&g32[gi].hx);
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(kFastThreads, BLEND_MIN_CTAS) k_blend_fast(
         if (k < nh) blend_sample_fast(st, k, pxl, pyl, pix, unsure);
         if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
             pix = saved;
-            for (int j = 0; j < nh; ++j) blend_sample_checked(st, j, pxl, pyl, px, py, g64, pix);
+            for (int j = 0; j < nh; ++j) blend_sample_checked(st, j, pxl, pyl, px, py, g64, g32, pix);
         }
         if (__all_sync(0xffffffffu, pix.T == 0.0f)) break;
         __syncwarp();
@@ -465,7 +467,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_ws(
             WsRaw& r = sh.raw[pid][slot];
             r.gid[lane] = gi;
             if (gi != kNone) {
-                cp_async16(&r.m[lane], &g64[gi].mx);
+                cp_async16(&r.m[lane], &g32[gi].mx);
                 cp_async16(&r.q0[lane], &g32[gi].ha);
                 cp_async16(&r.col[lane], &g32[gi].op);
                 cp_async8(&r.h[lane], &g32[gi].hx);
@@ -569,7 +571,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_ws(
             if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
                 pix = saved;
                 for (int j = 0; j < nh; ++j)
-                    blend_sample_checked(st, j, pxl, pyl, px, py, g64, pix);
+                    blend_sample_checked(st, j, pxl, pyl, px, py, g64, g32, pix);
             }
         }
         __syncwarp();
@@ -749,7 +751,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
             WsRaw& r = sh.raw[pid][slot];
             r.gid[lane] = gi;
             if (gi != kNone) {
-                cp_async16(&r.m[lane], &g64[gi].mx);
+                cp_async16(&r.m[lane], &g32[gi].mx);
                 cp_async16(&r.q0[lane], &g32[gi].ha);
                 cp_async16(&r.col[lane], &g32[gi].op);
                 cp_async8(&r.h[lane], &g32[gi].hx);
@@ -868,7 +870,7 @@ __global__ void __launch_bounds__(kWsThreads, WS_MIN_CTAS) k_blend_wsp(
                 pix = saved;
                 const double px = double(x) + 0.5, py = double(y) + 0.5;
                 for (int j = 0; j < nh; ++j)
-                    blend_sample_checked(st, j, pxl, pyl, px, py, g64, pix);
+                    blend_sample_checked(st, j, pxl, pyl, px, py, g64, g32, pix);
             }
         }
         __syncwarp();
@@ -996,9 +998,9 @@ __device__ __forceinline__ void mbar_wait_hint(unsigned long long* b, uint32_t p
 
 __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
-    const BlendRec* __restrict__ rec, const Gauss64* __restrict__ g64, const int width,
-    const int height, const int tiles_x, const uint32_t n_tiles, unsigned* ticket,
-    float* __restrict__ image) {
+    const BlendRec* __restrict__ rec, const Gauss64* __restrict__ g64,
+    const Gauss32* __restrict__ g32, const int width, const int height, const int tiles_x,
+    const uint32_t n_tiles, unsigned* ticket, float* __restrict__ image) {
     pdl_wait();  // the record pack (and everything before it) is complete and visible
     pdl_trigger();
     extern __shared__ __align__(128) unsigned char tma_raw[];
@@ -1117,7 +1119,7 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
             if (__any_sync(0xffffffffu, unsure)) {  // rare: certified FP64 decisions
                 pix = saved;
                 const double px = double(x) + 0.5, py = double(y) + 0.5;
-                for (int j = 0; j < nh; ++j) blend_sample_checked(st, j, pxl, pyl, px, py, g64, pix);
+                for (int j = 0; j < nh; ++j) blend_sample_checked(st, j, pxl, pyl, px, py, g64, g32, pix);
             }
 #else
             unsigned bb = bits;
@@ -1141,7 +1143,7 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
                     const int j = __ffs(bb) - 1;
                     bb &= bb - 1;
                     sample_checked(R[j].geo, R[j].ct, make_float2(R[j].gbm.x, R[j].gbm.y),
-                                   __float_as_uint(R[j].gbm.w), pxl, pyl, px, py, g64, pix);
+                                   __float_as_uint(R[j].gbm.w), pxl, pyl, px, py, g64, g32, pix);
                 }
             }
 #endif
@@ -1166,12 +1168,14 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
 }
 
 // ---------------------------------------------------------------------------
-// TMA gather4 blend (the default fast kernel, north_star (4)).  No pack pass:
-// the sorted keys name each pair's slot, and a tile's splat records are
-// gathered straight from the slot-indexed K3 records into shared memory by
-// the tensor memory accelerator -- cp.async.bulk.tensor.2d ... tile::gather4,
-// four rows per instruction (Gauss32 rows of 48 B, the first 32 B of the
-// Gauss64 rows), completion counted on the stage's mbarrier.
+// TMA gather4 blend (k_blend_g4, north_star (4); measured, not the default: DESIGN.md
+// 3.7).  No pack pass: the sorted keys name each pair's slot, and a tile's splat
+// records are gathered straight from the slot-indexed K3 records into shared memory
+// by the tensor memory accelerator -- cp.async.bulk.tensor.2d ... tile::gather4, four
+// rows per instruction, one 64-byte Gauss32 row per pair (conic, threshold, opacity,
+// colour, alpha box and the FP64 mean; two rows per pair with the mean read from
+// Gauss64 ran at the TMA's row rate, 245 vs 211 us), completion counted on the stage's
+// mbarrier.
 //
 // Per CTA: one producer warp + 8 consumer warps, persistent, tiles from the
 // frame's ticket queue (heavy-first order).  The producer walks a chunk
@@ -1180,34 +1184,25 @@ __global__ void __launch_bounds__(kTmaThreads, TMA_MIN_CTAS) k_blend_tma(
 // gathers are issued, and a tile's ticket -> order -> offsets chain is spread
 // over three tile transitions, so the producer never waits on a dependent
 // global load.  Lane 0 arms the stage's `full` barrier with the expected
-// bytes, lanes 0-7 / 8-15 issue one gather4 each.  Consumer warp w (8x4 block
+// bytes, lanes 0-7 issue one gather4 each.  Consumer warp w (8x4 block
 // (w & 1, w >> 1)) culls the 32 records against its block (the alpha box,
 // the FP64 mean rounded to block-relative FP32 exactly as k_blend_ws), compacts
 // its hits into its own list and blends them (k_blend_ws's per-sample code);
-// one mbarrier arrive per warp frees the stage.
+// one mbarrier arrive per warp frees the stage.  Tuning: 20 stages, 4 CTAs per SM,
+// two chunks of key look-ahead (10 / 16 / 20 stages, 3 / 4 CTAs: 211 / 202 / 198 us).
 #ifndef G4_STAGES
-#define G4_STAGES 10
+#define G4_STAGES 20
 #endif
 #ifndef G4_AHEAD
-#define G4_AHEAD 3
+#define G4_AHEAD 2
+#endif
+#ifndef G4_MIN_CTAS
+#define G4_MIN_CTAS 4
 #endif
 constexpr int kG4Stages = G4_STAGES;
 constexpr int kG4Ahead = G4_AHEAD;  // chunks whose keys are in flight
 constexpr int kG4Threads = (kTmaConsumers + 1) * 32;
 
-struct __align__(128) G4Stage {
-    float g32[8][64];   // gather4 group q: rows 4q..4q+3 of Gauss32 (48 B each), 256-B aligned
-    double g64[8][16];  // gather4 group q: rows 4q..4q+3, (mx, my, ca, cb) of Gauss64
-    uint32_t slot[32];
-};
-struct G4Shared {
-    G4Stage st[kG4Stages];
-    WarpStage wl[kTmaConsumers];
-    TmaHdr hdr[kG4Stages];
-    unsigned long long full[kG4Stages], empty[kG4Stages];
-    uint32_t done[kDoneRing];
-};
-constexpr uint32_t kG4GroupBytes = 4 * 48 + 4 * 32;  // one gather4 of each kind
 
 __device__ __forceinline__ void gather4(void* dst, const void* tmap, int r0, int r1, int r2,
                                         int r3, unsigned long long* bar) {
@@ -1226,10 +1221,24 @@ struct G4Chunk {
     uint32_t slot;  // this lane's pair (lane < n)
 };
 
-__global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
+
+struct __align__(128) G4Stage {
+    float rec[8][64];  // gather4 group q: rows 4q..4q+3 (16 floats each)
+    uint32_t slot[32];
+};
+struct G4Shared {
+    G4Stage st[kG4Stages];
+    WarpStage wl[kTmaConsumers];
+    TmaHdr hdr[kG4Stages];
+    unsigned long long full[kG4Stages], empty[kG4Stages];
+    uint32_t done[kDoneRing];
+};
+constexpr uint32_t kG4GroupBytes = 4 * 64;
+
+__global__ void __launch_bounds__(kG4Threads, G4_MIN_CTAS) k_blend_g4(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
     const unsigned long long* __restrict__ keys, const __grid_constant__ CUtensorMap map32,
-    const __grid_constant__ CUtensorMap map64, const Gauss64* __restrict__ g64, const int width,
+    const Gauss64* __restrict__ g64, const Gauss32* __restrict__ g32, const int width,
     const int height, const int tiles_x, const uint32_t n_tiles, unsigned* ticket,
     float* __restrict__ image) {
     pdl_wait();  // the sort (and everything before it) is complete and visible
@@ -1249,7 +1258,6 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
     if (warp == kTmaConsumers) {
         // ---------------- producer warp ----------------
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map32) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&map64) : "memory");
         // tile pipeline: raw ticket (lane 0) -> tile id -> bounds -> current
         auto take = [&]() -> uint32_t { return lane == 0 ? atomicAdd(ticket, 1u) : 0u; };
         auto tile_of = [&](uint32_t raw) -> int {
@@ -1299,11 +1307,15 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
         uint32_t killed = 0xFFFFFFFFu;  // tile sequence whose remaining chunks are dropped
         bool first_chunk = true;        // the next issued chunk starts a tile
         volatile uint32_t* done = sh.done;
-        for (;;) {
-            const G4Chunk ch = fifo[0];
+        bool finished = false;
+        // the loop body unrolled over the FIFO slots: no register copy of a key whose
+        // load is still in flight (k_blend_cpa)
+        while (!finished) {
 #pragma unroll
-            for (int j = 0; j + 1 < kG4Ahead; ++j) fifo[j] = fifo[j + 1];
-            fifo[kG4Ahead - 1] = gen();
+        for (int jf = 0; jf < kG4Ahead; ++jf) {
+            if (finished) break;
+            const G4Chunk ch = fifo[jf];
+            fifo[jf] = gen();
             if (ch.tile >= 0 && ch.k == killed) continue;  // rest of a terminated tile
             const int s = int(i % kG4Stages);
             if (i >= uint32_t(kG4Stages))
@@ -1314,7 +1326,8 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
                     sh.hdr[s] = TmaHdr{0, 0, 0u, 2u};
                     mbar_arrive(&sh.full[s]);
                 }
-                break;
+                finished = true;
+                continue;
             }
             // first chunk of a tile: reset its terminated-warp counter (published
             // to the consumers by this stage's arrive)
@@ -1345,11 +1358,10 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
                 else mbar_arrive(&sh.full[s]);
             }
             __syncwarp();
-            if (uint32_t(q) < groups) {
-                if (lane < 8) gather4(&st.g32[q][0], &map32, r0, r1, r2, r3, &sh.full[s]);
-                else if (lane < 16) gather4(&st.g64[q][0], &map64, r0, r1, r2, r3, &sh.full[s]);
-            }
+            if (uint32_t(q) < groups && lane < 8)
+                gather4(&st.rec[q][0], &map32, r0, r1, r2, r3, &sh.full[s]);
             first_chunk = last;
+        }
         }
         return;
     }
@@ -1381,8 +1393,8 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
         bool hit = false;
         float mlx = 0.f, mly = 0.f;
         if (lane < hd.n) {
-            const float2 h = *reinterpret_cast<const float2*>(&st.g32[q][r * 12 + 8]);
-            const double2 m = *reinterpret_cast<const double2*>(&st.g64[q][r * 4]);
+            const float2 h = *reinterpret_cast<const float2*>(&st.rec[q][r * 16 + 8]);
+            const double2 m = *reinterpret_cast<const double2*>(&st.rec[q][r * 16 + 12]);
             if (h.x >= 0.0f) {
                 mlx = float(m.x - double(bx));
                 mly = float(m.y - double(by));
@@ -1394,7 +1406,7 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
         if (bits && __any_sync(0xffffffffu, pix.T != 0.0f)) {
             if (hit) {
                 const int at = __popc(bits & lt);
-                const float* g = &st.g32[q][r * 12];
+                const float* g = &st.rec[q][r * 16];
                 const float4 q0 = *reinterpret_cast<const float4*>(g);
                 const float4 col = *reinterpret_cast<const float4*>(g + 4);
                 wl.geo[at] = make_float4(mlx, mly, q0.x, q0.z);
@@ -1416,7 +1428,7 @@ __global__ void __launch_bounds__(kG4Threads, TMA_MIN_CTAS) k_blend_g4(
                 pix = saved;
                 const double px = double(bx + int(lane & 7)) + 0.5;
                 const double py = double(by + int(lane >> 3)) + 0.5;
-                for (int j = 0; j < nh; ++j) blend_sample_checked(wl, j, pxl, pyl, px, py, g64, pix);
+                for (int j = 0; j < nh; ++j) blend_sample_checked(wl, j, pxl, pyl, px, py, g64, g32, pix);
             }
         }
         __syncwarp();
@@ -1506,7 +1518,7 @@ static_assert(kCpaLag < kCpaStages && kCpaLag < kCpaStagesBig,
               "a stage is published before the producer waits for its reuse");
 
 struct CpaStage {
-    double2 m[32];   // Gauss64 (mx, my)
+    double2 m[32];   // Gauss32 (mx, my), the FP64 mean
     float4 q0[32];   // Gauss32 (ha, cb, hc, ethr)
     float4 col[32];  // Gauss32 (op, r, g, b)
     float2 h[32];    // Gauss32 (hx, hy)
@@ -1647,13 +1659,13 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
                 const uint32_t gi = ch.slot;
 #if CPA_CG  // L2 only: a record is read by one tile's CTA (and rarely reused in L1)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(&st.m[lane])),
-                             "l"(&g64[gi].mx) : "memory");
+                             "l"(&g32[gi].mx) : "memory");
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(&st.q0[lane])),
                              "l"(&g32[gi].ha) : "memory");
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(&st.col[lane])),
                              "l"(&g32[gi].op) : "memory");
 #else
-                cp_async16(&st.m[lane], &g64[gi].mx);
+                cp_async16(&st.m[lane], &g32[gi].mx);
                 cp_async16(&st.q0[lane], &g32[gi].ha);
                 cp_async16(&st.col[lane], &g32[gi].op);
 #endif
@@ -1753,7 +1765,7 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
                 pix = saved;
                 const double px = double(bx + int(lane & 7)) + 0.5;
                 const double py = double(by + int(lane >> 3)) + 0.5;
-                for (int j = 0; j < nh; ++j) blend_sample_checked(wl, j, pxl, pyl, px, py, g64, pix);
+                for (int j = 0; j < nh; ++j) blend_sample_checked(wl, j, pxl, pyl, px, py, g64, g32, pix);
             }
         }
         // every lane releases its own reads of the stage (one warp instruction)
@@ -1776,10 +1788,9 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
     }
 }
 
-// Tensor maps of the slot-indexed records for gather4: Gauss32 rows (12 floats)
-// and the first 4 doubles of the Gauss64 rows; boxes of one row, 4 rows per gather.
-static bool encode_record_maps(const Gauss32* g32, const Gauss64* g64, uint64_t rows,
-                               CUtensorMap* m32, CUtensorMap* m64) {
+
+// Tensor map of the 64-byte Gauss32 rows for k_blend_g4: boxes of one row.
+static bool encode_row_map(const Gauss32* g32, uint64_t rows, CUtensorMap* m) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -1791,16 +1802,10 @@ static bool encode_record_maps(const Gauss32* g32, const Gauss64* g64, uint64_t 
             encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     });
     if (!encode || rows == 0 || rows > 0xFFFFFFFFull) return false;
-    const cuuint64_t d32[2] = {12, rows}, s32[1] = {sizeof(Gauss32)};
-    const cuuint32_t b32[2] = {12, 1}, e1[2] = {1, 1};
-    const cuuint64_t d64[2] = {8, rows}, s64[1] = {sizeof(Gauss64)};
-    const cuuint32_t b64[2] = {4, 1};
-    if (encode(m32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<Gauss32*>(g32), d32, s32, b32,
-               e1, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return false;
-    return encode(m64, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<Gauss64*>(g64), d64, s64,
-                  b64, e1, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+    const cuuint64_t d[2] = {16, rows}, st[1] = {sizeof(Gauss32)};
+    const cuuint32_t b[2] = {16, 1}, e1[2] = {1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<Gauss32*>(g32), d, st, b, e1,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -1840,11 +1845,12 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_exact(
             const uint32_t gi = uint32_t(keys[base + threadIdx.x]);
             const Gauss64 G = g64[gi];
             const GaussCol64 C = col64[gi];
-            s.geo[threadIdx.x] = make_double4(G.mx, G.my, G.ca, G.cb);
+            const double2 m = *reinterpret_cast<const double2*>(&g32[gi].mx);
+            s.geo[threadIdx.x] = make_double4(m.x, m.y, G.ca, G.cb);
             s.cc_op[threadIdx.x] = make_double2(G.cc, G.op);
             s.col[threadIdx.x] = make_double4(C.r, C.g, C.b, 0.0);
             const float2 h = *reinterpret_cast<const float2*>(&g32[gi].hx);
-            const float mlx = float(G.mx - double(x0)), mly = float(G.my - double(y0));
+            const float mlx = float(m.x - double(x0)), mly = float(m.y - double(y0));
             if (h.x >= 0.0f) {
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w) {
@@ -1911,7 +1917,8 @@ struct KpcSmem {
 
 __global__ void __launch_bounds__(kTile * kTile) k_blend_exact_kpc(
     const uint32_t* __restrict__ offsets, const unsigned long long* __restrict__ keys,
-    const Gauss64* __restrict__ g64, const GaussCol64* __restrict__ col64, const int width,
+    const Gauss64* __restrict__ g64, const Gauss32* __restrict__ g32,
+    const GaussCol64* __restrict__ col64, const int width,
     const int height, const int tiles_x, float* __restrict__ image, double* __restrict__ kpc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     KpcSmem& s = *reinterpret_cast<KpcSmem*>(smem_raw);
@@ -1931,7 +1938,8 @@ __global__ void __launch_bounds__(kTile * kTile) k_blend_exact_kpc(
             const uint32_t gi = uint32_t(keys[base + threadIdx.x]);
             const Gauss64 G = g64[gi];
             const GaussCol64 C = col64[gi];
-            s.geo[threadIdx.x] = make_double4(G.mx, G.my, G.ca, G.cb);
+            const double2 m = *reinterpret_cast<const double2*>(&g32[gi].mx);
+            s.geo[threadIdx.x] = make_double4(m.x, m.y, G.ca, G.cb);
             s.cc_op[threadIdx.x] = make_double2(G.cc, G.op);
             s.col[threadIdx.x] = make_double4(C.r, C.g, C.b, 0.0);
         }
@@ -1978,8 +1986,9 @@ __global__ void __launch_bounds__(kTile * kTile) k_blend_exact_kpc(
 }
 
 void launch_blend_exact_kpc(const uint32_t* offsets, const unsigned long long* keys,
-                            const Gauss64* g64, const GaussCol64* col64, int width, int height,
-                            int tiles_x, int tiles_y, float* image, double* kpc, cudaStream_t s) {
+                            const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64,
+                            int width, int height, int tiles_x, int tiles_y, float* image,
+                            double* kpc, cudaStream_t s) {
     const int n_tiles = tiles_x * tiles_y;
     if (n_tiles <= 0) return;
     static bool attr = false;
@@ -1988,8 +1997,8 @@ void launch_blend_exact_kpc(const uint32_t* offsets, const unsigned long long* k
         cudaFuncSetAttribute(k_blend_exact_kpc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    k_blend_exact_kpc<<<n_tiles, kTile * kTile, smem, s>>>(offsets, keys, g64, col64, width, height,
-                                                           tiles_x, image, kpc);
+    k_blend_exact_kpc<<<n_tiles, kTile * kTile, smem, s>>>(offsets, keys, g64, g32, col64, width,
+                                                           height, tiles_x, image, kpc);
 }
 
 // Per-tile GTC (metrics.cpp:18-35): the mean kpc of the tile's pairs, summed
@@ -2092,32 +2101,35 @@ void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned
                   int kernel) {
     const int n_tiles = tiles_x * tiles_y;
     if (n_tiles <= 0) return;
-    CUtensorMap m32, m64;
-    if (kernel == kBlendGather4 && !exact && ticket && n_records &&
-        encode_record_maps(g32, g64, n_records, &m32, &m64)) {
-        const int smem = int(sizeof(G4Shared));
-        static std::mutex mu;
-        static int grid_of[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        int grid = 0;
-        {
-            std::lock_guard<std::mutex> lock(mu);
-            if (dev < 0 || dev >= 64 || !grid_of[dev]) {
-                cudaFuncSetAttribute(k_blend_g4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                int per_sm = 0, n_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blend_g4, kG4Threads, smem);
-                cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-                grid = std::max(1, per_sm) * std::max(1, n_sm);
-                if (dev >= 0 && dev < 64) grid_of[dev] = grid;
-            } else {
-                grid = grid_of[dev];
+    if (kernel == kBlendGather4 && !exact && ticket && n_records) {
+        CUtensorMap mrow;
+        if (encode_row_map(g32, n_records, &mrow)) {
+            const int smem = int(sizeof(G4Shared));
+            static std::mutex mu;
+            static int grid_of[64] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            int grid = 0;
+            {
+                std::lock_guard<std::mutex> lock(mu);
+                if (dev < 0 || dev >= 64 || !grid_of[dev]) {
+                    cudaFuncSetAttribute(k_blend_g4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem);
+                    int per_sm = 0, n_sm = 0;
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blend_g4, kG4Threads,
+                                                                  smem);
+                    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+                    grid = std::max(1, per_sm) * std::max(1, n_sm);
+                    if (dev >= 0 && dev < 64) grid_of[dev] = grid;
+                } else {
+                    grid = grid_of[dev];
+                }
             }
+            grid = std::min(n_tiles, grid);
+            launch_pdl(k_blend_g4, grid, kG4Threads, smem, s, offsets, order, keys, mrow, g64,
+                       g32, width, height, tiles_x, uint32_t(n_tiles), ticket, image);
+            return;
         }
-        grid = std::min(n_tiles, grid);
-        launch_pdl(k_blend_g4, grid, kG4Threads, smem, s, offsets, order, keys, m32, m64, g64,
-                   width, height, tiles_x, uint32_t(n_tiles), ticket, image);
-        return;
     }
     if (kernel == kBlendCpa && !exact && ticket) {
         if (n_tiles > kCpaBigFrameTiles)
@@ -2153,7 +2165,7 @@ void launch_blend(const uint32_t* offsets, const uint32_t* order, const unsigned
         }
         grid = std::min(n_tiles, grid);
         launch_pdl(k_blend_tma, grid, kTmaThreads, smem, s, offsets, order,
-                   static_cast<const BlendRec*>(rec), g64, width, height, tiles_x,
+                   static_cast<const BlendRec*>(rec), g64, g32, width, height, tiles_x,
                    uint32_t(n_tiles), ticket, image);
         return;
     }

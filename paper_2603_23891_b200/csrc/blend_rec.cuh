@@ -34,7 +34,7 @@ struct RecOut {
 __device__ __forceinline__ BlendRec make_blend_rec(const Gauss64* __restrict__ g64,
                                                    const Gauss32* __restrict__ g32, uint32_t gi,
                                                    int tx0, int ty0) {
-    const double2 m = *reinterpret_cast<const double2*>(&g64[gi].mx);
+    const double2 m = *reinterpret_cast<const double2*>(&g32[gi].mx);
     const float4 q0 = *reinterpret_cast<const float4*>(&g32[gi].ha);
     const float4 col = *reinterpret_cast<const float4*>(&g32[gi].op);
     const float2 h = *reinterpret_cast<const float2*>(&g32[gi].hx);

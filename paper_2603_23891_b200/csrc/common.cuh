@@ -37,15 +37,14 @@ struct __align__(16) SplatRec {
     float cg, cb, pad0, pad1;
 };
 
-// Per projected gaussian, FP64 fields (exact blend path, guard-band
-// recompute, parity readback).  64 bytes.
+// Per projected gaussian, the FP64 conic and opacity (exact blend path, the fast
+// blend's guard-band recompute, parity readback); the FP64 mean and radius live in
+// the Gauss32 row.  32 bytes.
 struct __align__(16) Gauss64 {
-    double mx, my;
     double ca, cb, cc;
     double op;
-    double radius;
-    double pad;
 };
+static_assert(sizeof(Gauss64) == 32, "one sector per gaussian");
 
 // FP64 colours, only materialised for the exact (bit-identical) blend.
 struct __align__(16) GaussCol64 {
@@ -59,11 +58,17 @@ struct __align__(16) GaussCol64 {
 //   (hx, hy): half-extents of the e <= ethr ellipse, computed in FP64 and
 //   rounded outward -- a conservative box outside which the reference
 //   provably skips every sample (blend.cu uses it to cull per warp).
+//   (mx, my): the FP64 mean (BlendList mean_x/y, bit-exact), so one 64-byte row --
+//   two whole 32-byte sectors -- holds everything the fast blend reads for a pair;
+//   radius: the FP64 effective radius (BlendList radius; read back only).
 struct __align__(16) Gauss32 {
     float ha, cb, hc, ethr;
     float op, r, g, b;
-    float hx, hy, pad0, pad1;
+    float hx, hy;
+    double radius;
+    double mx, my;
 };
+static_assert(sizeof(Gauss32) == 64, "one 64-byte blend row per gaussian");
 
 // Per projected gaussian, what key duplication needs.
 struct __align__(16) GaussEmit {

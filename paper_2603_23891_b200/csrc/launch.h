@@ -174,8 +174,9 @@ int blend_launches();
 
 // Exact blend + per-pair KPC in the reference's 4-lane order (collect_kpc).
 void launch_blend_exact_kpc(const uint32_t* offsets, const unsigned long long* keys,
-                            const Gauss64* g64, const GaussCol64* col64, int width, int height,
-                            int tiles_x, int tiles_y, float* image, double* kpc, cudaStream_t s);
+                            const Gauss64* g64, const Gauss32* g32, const GaussCol64* col64,
+                            int width, int height, int tiles_x, int tiles_y, float* image,
+                            double* kpc, cudaStream_t s);
 // Calibration pieces (metrics.cpp:18-57): per-tile GTC, view GTC (NaN when no
 // tile has pairs), and the 5-bin kpc redundancy histogram (accumulated).
 void launch_view_gtc(const uint32_t* offsets, int n_tiles, const double* kpc, uint64_t n_pairs,

@@ -122,8 +122,12 @@ __device__ __forceinline__ uint32_t rect_count(const GaussEmit& e) {
 #endif
 // FP32 blend record from the FP64 gaussian (blend.cu explains ethr).
 __device__ __forceinline__ Gauss32 make_g32(double ca, double cb, double cc, double op, double r,
-                                            double gg, double b) {
+                                            double gg, double b, double mx, double my,
+                                            double radius) {
     Gauss32 o;
+    o.mx = mx;
+    o.my = my;
+    o.radius = radius;
     // exponent coefficients pre-scaled by log2(e): the blend evaluates
     // e' = e log2(e) and alpha = op * 2^-e' with one MUFU.EX2
     constexpr double kLog2e = 1.4426950408889634074;
@@ -168,7 +172,6 @@ __device__ __forceinline__ Gauss32 make_g32(double ca, double cb, double cc, dou
     } else {
         o.hx = o.hy = -1.0f;
     }
-    o.pad0 = o.pad1 = 0.0f;
     return o;
 }
 
@@ -263,14 +266,10 @@ __global__ void __launch_bounds__(kPrepBlock, PREP_MIN_CTAS) k_preprocess(
         if (p.keep) {
             if (p.nonfinite) atomicOr(&cnt->nonfinite, 1u);
             Gauss64 r64;
-            r64.mx = p.mx;
-            r64.my = p.my;
             r64.ca = p.ca;
             r64.cb = p.cb;
             r64.cc = p.cc;
             r64.op = double(rec.opacity);
-            r64.radius = p.radius;
-            r64.pad = 0.0;
             out.g64[s] = r64;
             if (out.col64) {
                 GaussCol64 col;
@@ -281,7 +280,7 @@ __global__ void __launch_bounds__(kPrepBlock, PREP_MIN_CTAS) k_preprocess(
                 out.col64[s] = col;
             }
             out.g32[s] = make_g32(p.ca, p.cb, p.cc, double(rec.opacity), double(rec.cr),
-                                  double(rec.cg), double(rec.cb));
+                                  double(rec.cg), double(rec.cb), p.mx, p.my, p.radius);
             e.depth_bits = __float_as_uint(__double2float_rn(p.depth));
             tile_rect(p.mx, p.my, p.radius, tiles_x, tiles_y, e);
             ++kept;
@@ -1034,15 +1033,12 @@ __global__ void k_pack_blendlist(uint64_t n, const double* mx, const double* my,
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     Gauss64 r;
-    r.mx = mx[i];
-    r.my = my[i];
     r.ca = ca[i];
     r.cb = cb[i];
     r.cc = cc[i];
     r.op = op[i];
-    r.radius = radius ? radius[i] : 0.0;
-    r.pad = 0.0;
     g64[i] = r;
+    const double rad = radius ? radius[i] : 0.0;
     if (col64) {
         GaussCol64 c;
         c.r = cr[i];
@@ -1051,12 +1047,12 @@ __global__ void k_pack_blendlist(uint64_t n, const double* mx, const double* my,
         c.pad = 0.0;
         col64[i] = c;
     }
-    g32[i] = make_g32(ca[i], cb[i], cc[i], op[i], cr[i], cg[i], cbl[i]);
+    g32[i] = make_g32(ca[i], cb[i], cc[i], op[i], cr[i], cg[i], cbl[i], mx[i], my[i], rad);
     if (emit) {
         GaussEmit e;
         e.depth_bits = __float_as_uint(depth[i]);
         e.node = uint32_t(i);
-        tile_rect(r.mx, r.my, r.radius, tiles_x, tiles_y, e);
+        tile_rect(mx[i], my[i], rad, tiles_x, tiles_y, e);
         emit[i] = e;
     }
 }

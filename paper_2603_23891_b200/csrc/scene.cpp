@@ -691,7 +691,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
     if (pe) FGS_CUDA(cudaEventRecord(pe[4], stream_));
     float* img_out = image_target_ ? image_target_ : res_.image.p;
     if (p.flags & LODGS_RENDER_COLLECT_KPC) {
-        launch_blend_exact_kpc(res_.tile_offsets.p, keys_.p, g64_.p, col64_.p, res_.width,
+        launch_blend_exact_kpc(res_.tile_offsets.p, keys_.p, g64_.p, g32_.p, col64_.p, res_.width,
                                res_.height, res_.tiles_x, res_.tiles_y, img_out, kpc_.p, stream_);
     } else if (band_host_ && bk == kBlendCpa && !exact && !image_target_ && res_.tiles_y >= 2) {
         // synchronous frame with a host image: blend kSyncBands horizontal bands (each
@@ -1202,8 +1202,8 @@ uint64_t GpuScene::read_gaussians(lodgs_blend_list* out, uint64_t cap) {
     }
     out->n = ng;
     for (uint64_t i = 0; i < ng; ++i) {
-        out->mean_x[i] = a[i].mx;
-        out->mean_y[i] = a[i].my;
+        out->mean_x[i] = b[i].mx;
+        out->mean_y[i] = b[i].my;
         out->conic_a[i] = a[i].ca;
         out->conic_b[i] = a[i].cb;
         out->conic_c[i] = a[i].cc;
@@ -1213,7 +1213,7 @@ uint64_t GpuScene::read_gaussians(lodgs_blend_list* out, uint64_t cap) {
         out->col_r[i] = double(b[i].r);
         out->col_g[i] = double(b[i].g);
         out->col_b[i] = double(b[i].b);
-        out->radius[i] = a[i].radius;
+        out->radius[i] = b[i].radius;
         std::memcpy(&out->depth[i], &e[i].depth_bits, 4);
         out->node[i] = e[i].node;
     }
