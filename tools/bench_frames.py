@@ -1,5 +1,5 @@
 """Render exactly the frames `bench.py --steps K` times (strided over the 300-frame
-cfg-3 path), one synchronous frame at a time, inside an NVTX range "bench_frames" so an
+cfg-3 path), one frame at a time, inside an NVTX range "bench_frames" so an
 ncu capture can be restricted to them (not a benchmark; numbers under ncu are never
 bench values):
 
@@ -30,10 +30,15 @@ def main():
         for cam in cams[::10]:  # pair-buffer sizing, as the bench
             s.render(cam, L.FilterConfig(bench.TAU_R), mode)
         frames = strided_frames(len(cams), 0, 1, args.steps)
+        # one frame at a time without a host image (render_async + sync): the kernels of
+        # the bench's per-frame path and of its stage split -- a host image would take the
+        # synchronous render's banded blend + copy instead
+        p = s.params(L.FilterConfig(bench.TAU_R), mode, L.RenderOptions())
         torch.cuda.nvtx.range_push("bench_frames")
         pairs = 0
         for i in frames:
-            pairs += s.render(cams[i], L.FilterConfig(bench.TAU_R), mode).stats.n_pairs
+            s.render_async(cams[i], p)
+            pairs += s.sync().n_pairs
         torch.cuda.nvtx.range_pop()
     print(f"{len(frames)} frames, mean pairs {pairs / len(frames):.0f}")
 

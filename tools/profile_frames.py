@@ -25,11 +25,12 @@ def main():
     tree = L.build_synthetic_tree(nx=args.nx, ny=args.nx, seed=1, depth=3, build_seed=7)
     with L.GpuScene(tree) as s:
         opts = L.RenderOptions(exact_blend=args.exact, stage_timing=True)
+        p = s.params(L.FilterConfig(3.0), L.ShrinkMode.three_sigma(), opts)
         for alt in args.alt:
             cam = topdown_camera(1920, 1080, 1000.0, alt)
-            for _ in range(args.frames):
-                out = s.render(cam, L.FilterConfig(3.0), L.ShrinkMode.three_sigma(), opts)
-            st = out.stats
+            for _ in range(args.frames):  # no host image: the whole-frame blend, not the bands
+                s.render_async(cam, p)
+                st = s.sync()
             print(f"alt {alt}: sel {st.n_selected} pairs {st.n_pairs} big_tiles {st.big_tiles} "
                   f"calc {st.t_calc_ms:.3f} prepr {st.t_prepr_ms:.3f} sort {st.t_sort_ms:.3f} "
                   f"alpha {st.t_alpha_ms:.3f} ms")
