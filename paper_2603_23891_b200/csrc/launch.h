@@ -147,11 +147,12 @@ void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
                           cudaStream_t s, RecOut ro = {}, int tiles_x = 1);
 
 // ---- blend (rasterizer.cpp:137-165, blend_scalar.cpp:13-55) ----
-// Fast-blend kernels (certified-identical): kBlendWsp (default,
-// cp.async producer warps), kBlendTma (`records` holds blend_record_bytes() per
-// pair written by the sort when records_packed, else by a pack pass here; each
-// tile's records stream into shared memory with cp.async.bulk), kBlendGather4
-// (TMA tile::gather4 of the n_records slot-indexed g32/g64 rows).
+// Fast-blend kernels (certified-identical): kBlendCpa (default: one
+// producer warp, per-lane cp.async into a stage ring completed by the copies),
+// kBlendWsp (round 1: two producer warps that cull), kBlendTma (`records` holds
+// blend_record_bytes() per pair written by the sort when records_packed, else by a
+// pack pass here; each tile's records stream into shared memory with cp.async.bulk),
+// kBlendGather4 (TMA tile::gather4 of the n_records slot-indexed 64-byte g32 rows).
 enum BlendKernel { kBlendWsp = 0, kBlendTma = 1, kBlendGather4 = 2, kBlendCpa = 3 };
 // Banded blend of a synchronous frame: each band's image rows are copied to the host
 // while the next band blends (GpuScene::enqueue_pipeline).
