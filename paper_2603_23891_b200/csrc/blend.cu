@@ -980,6 +980,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #endif
 // mbarrier wait with a suspend-time hint: the thread is descheduled until the
 // phase completes (or the hint expires) instead of re-issuing the poll
+// one poll of the phase (no blocking)
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{ .reg .pred p;\n"
+        "  mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "  selp.u32 %0, 1, 0, p;\n"
+        "}"
+        : "=r"(ok)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 template <int kHintNs>
 __device__ __forceinline__ void mbar_wait_hint(unsigned long long* b, uint32_t parity) {
     if (kHintNs == 0) {
@@ -1483,6 +1497,9 @@ __global__ void __launch_bounds__(kG4Threads, G4_MIN_CTAS) k_blend_g4(
 #ifndef CPA_CONS_HINT
 #define CPA_CONS_HINT 0
 #endif
+#ifndef CPA_CONS_SLEEP
+#define CPA_CONS_SLEEP 0  // ns of __nanosleep between the consumers' polls (0: try_wait)
+#endif
 #ifndef CPA_CG
 #define CPA_CG 1
 #endif
@@ -1708,7 +1725,12 @@ __global__ void __launch_bounds__(kCpaThreads, CPA_MIN_CTAS) k_blend_cpa(
     const unsigned lt = (1u << lane) - 1u;
     for (uint32_t i = 0;; ++i) {
         const int s = int(i % S);
+#if CPA_CONS_SLEEP
+        // back off with __nanosleep between polls: a sleeping warp issues nothing
+        while (!mbar_try(&sh.full[s], (i / S) & 1u)) __nanosleep(CPA_CONS_SLEEP);
+#else
         mbar_wait_hint<CPA_CONS_HINT>(&sh.full[s], (i / S) & 1u);
+#endif
         const TmaHdr hd = sh.hdr[s];
         if (hd.flags & 2u) break;
         if (fresh) {

@@ -779,7 +779,10 @@ struct ViewSetDev {
     int n;
 };
 
-__global__ void __launch_bounds__(kMarkBlock, MARK_MIN_CTAS) k_mark_views(
+#ifndef MARK_VIEWS_MIN_CTAS
+#define MARK_VIEWS_MIN_CTAS MARK_MIN_CTAS
+#endif
+__global__ void __launch_bounds__(kMarkBlock, MARK_VIEWS_MIN_CTAS) k_mark_views(
     const __grid_constant__ ViewSetDev vs, const __grid_constant__ DevTree t, const double tau_r) {
     pdl_wait();
     pdl_trigger();
@@ -956,7 +959,9 @@ void launch_filter_views(const ViewSet& views, const DevTree& t, double tau_r, c
         const uint64_t groups = (split + 31) / 32;
         const unsigned grid =
             unsigned(std::min<uint64_t>((groups + 7) / 8, uint64_t(sm_count()) * MARK_MIN_CTAS));
-        launch_pdl(k_mark_views, grid, kMarkBlock, 0, s, vs, t, tau_r);
+        const unsigned vgrid = unsigned(
+            std::min<uint64_t>((groups + 7) / 8, uint64_t(sm_count()) * MARK_VIEWS_MIN_CTAS));
+        launch_pdl(k_mark_views, vgrid, kMarkBlock, 0, s, vs, t, tau_r);
         const uint64_t per = uint64_t(kSelectBlock) * kSelectItems;
         launch_pdl(k_select_views, dim3(unsigned((split + per - 1) / per), unsigned(views.n)),
                    kSelectBlock, 0, s, vs, static_cast<const uint32_t*>(t.parent), split);

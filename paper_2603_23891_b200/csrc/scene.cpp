@@ -727,6 +727,7 @@ void GpuScene::enqueue_pipeline(const Geom& g, const lodgs_render_params& p, int
         }
         FGS_CUDA(cudaEventRecord(band_done_, copy_stream_));
         band_copied_ = true;  // the stream joins the copies after the blend's timing events
+        band_launches_ = uint32_t(nbands);  // nbands blends + k_band_order for one blend
     } else {
         launch_blend(res_.tile_offsets.p, res_.tile_order.p, keys_.p, g64_.p, g32_.p, col64_.p,
                      res_.width, res_.height, res_.tiles_x, res_.tiles_y, exact, img_out, stream_,
@@ -760,8 +761,19 @@ void GpuScene::enqueue_frame(const lodgs_camera& cam, const lodgs_render_params&
     last_timing_ = (p.flags & LODGS_RENDER_STAGE_TIMING) != 0;
     last_keep_ = (p.flags & LODGS_RENDER_KEEP_PAIRS) != 0;
     last_exact_ = (p.flags & LODGS_RENDER_EXACT_BLEND) != 0;
-    band_host_ = (image_host && !(p.flags & LODGS_RENDER_OUTPUT_RGB8)) ? image_host : nullptr;
+    // banded blend + copy only into pinned (page-locked / registered) host memory: a D2H
+    // copy into pageable memory blocks the host thread until it has landed, so the bands
+    // would serialise (and the stage timers would count the copies); not with stage timing
+    band_host_ = nullptr;
+    if (image_host && !(p.flags & LODGS_RENDER_OUTPUT_RGB8) && !last_timing_) {
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, image_host) == cudaSuccess &&
+            attr.type == cudaMemoryTypeHost)
+            band_host_ = image_host;
+        cudaGetLastError();  // a pageable pointer may leave an error behind on old drivers
+    }
     band_copied_ = false;
+    band_launches_ = 0;
     enqueue_pipeline(g, p, int(cam.width), int(cam.height), last_timing_, prefiltered);
     band_host_ = nullptr;
     FGS_CUDA(cudaMemcpyAsync(h_counters_, d_counters_, sizeof(FrameCounters),
@@ -812,7 +824,8 @@ void GpuScene::finish(lodgs_render_stats* stats) {
         stats->filter_barriers = stats->filter_passes;
         stats->big_tiles = c.big_tiles;
         stats->kernel_launches =
-            last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() + n_levels() + filter_launches(tree_.n) - 3 + sh_launches()) : kLaunchesPerFrame + blend_launches() + filter_launches(tree_.n) + sh_launches();
+            (last_serial_ ? uint32_t(kLaunchesPerFrame + blend_launches() + n_levels() + filter_launches(tree_.n) - 3 + sh_launches()) : kLaunchesPerFrame + blend_launches() + filter_launches(tree_.n) + sh_launches()) +
+            band_launches_;
         if (last_timing_) {
             float ms = 0;
             FGS_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));

@@ -240,6 +240,7 @@ private:
     // each band's rows go to band_host_ on copy_stream_ while the next band blends
     float* band_host_ = nullptr;
     bool band_copied_ = false;
+    uint32_t band_launches_ = 0;  // extra launches of the last banded frame (stats)
     DevBuf<uint32_t> band_order_;
     DevBuf<unsigned> band_ticket_;
     cudaEvent_t band_ev_[kMaxBands] = {}, band_done_ = nullptr;

@@ -1030,6 +1030,33 @@ def _metrics(a, b, want_psnr, want_ssim):
     return p.value, q.value
 
 
+class PinnedImage:
+    """An f32 RGB image in pinned host memory (lodgs_gpu_host_alloc): a synchronous render
+    into it copies each band of rows while the next band blends (pageable memory gets one
+    copy after the blend).  Use as a context manager; .rgb is the (H, W, 3) array."""
+
+    def __init__(self, width: int, height: int):
+        self._lib = load_library()
+        n = int(width) * int(height) * 3
+        p = C.c_void_p()
+        _check(self._lib.lodgs_gpu_host_alloc(n * 4, C.byref(p)))
+        self._p = p.value
+        self.rgb = np.ctypeslib.as_array((C.c_float * n).from_address(self._p)).reshape(
+            int(height), int(width), 3)
+
+    def close(self) -> None:
+        if self._p:
+            self.rgb = None
+            self._lib.lodgs_gpu_host_free(self._p)
+            self._p = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 def psnr(a, b) -> float:
     """metrics.hpp psnr (metrics.cpp:121-132) on the device; +inf if identical."""
     return _metrics(a, b, True, False)[0]

@@ -128,6 +128,33 @@ def test_cfg3_bench_frames_async_and_batch(L, ref, cfg3):
                 assert im.tobytes() == bi.tobytes(), f"wsp frame {i} differs from cpa"
 
 
+def test_sync_render_pinned_bands(L, ref, cfg3):
+    """A synchronous render into pinned host memory blends in four horizontal bands and
+    copies each band while the next one blends: the 20 bench frames equal
+    the pageable-memory renders (one blend, one copy) byte for byte, with four more
+    launches; short images (2 and 3 tile rows) and stage timing (no bands) too."""
+    b, tree, rh, cams, scene = cfg3
+    from paper_2603_23891_b200.sharding import strided_frames
+
+    mode = L.ShrinkMode.three_sigma()
+    with L.PinnedImage(1920, 1080) as pin:
+        for i in strided_frames(len(cams), 0, 1, 20):
+            want = scene.render(cams[i], L.FilterConfig(b.TAU_R), mode)
+            got = scene.render(cams[i], L.FilterConfig(b.TAU_R), mode, image_out=pin.rgb)
+            assert got.stats.kernel_launches == want.stats.kernel_launches + 4, i
+            assert pin.rgb.tobytes() == want.image.rgb.tobytes(), f"frame {i}"
+        t = scene.render(cams[150], L.FilterConfig(b.TAU_R), mode,
+                         L.RenderOptions(stage_timing=True), image_out=pin.rgb)
+        assert t.stats.kernel_launches == want.stats.kernel_launches  # no bands when timed
+    for w, h, bands in ((640, 40, 3), (640, 17, 2)):
+        cam = topdown_camera(w, h, 300.0, 60.0)
+        want = scene.render(cam, L.FilterConfig(b.TAU_R), mode)
+        with L.PinnedImage(w, h) as pin:
+            got = scene.render(cam, L.FilterConfig(b.TAU_R), mode, image_out=pin.rgb)
+            assert got.stats.kernel_launches == want.stats.kernel_launches + bands, (w, h)
+            assert pin.rgb.tobytes() == want.image.rgb.tobytes(), (w, h)
+
+
 def test_cfg3_altitudes_and_oblique_keyframes(L, ref, cfg3):
     """Top-down frames at altitudes 400 / 200 / 140 and the two oblique keyframes
     (260 and 140), synchronous production renders: pairs and BlendList bit-exact,
@@ -216,6 +243,11 @@ def test_cfg4_50m_4k_production(L, ref, gpu):
             assert out.stats.big_tiles > 0  # the big-bucket sort ran
             a = _async_frames(L, s, [hi, lo], 3.0, mode)
             assert a[1].tobytes() == out.image.rgb.tobytes()
+            # the synchronous render into pinned memory: 4K, the 16-stage blend, in bands
+            with L.PinnedImage(3840, 2160) as pin:
+                pb = s.render(lo, L.FilterConfig(3.0), mode, image_out=pin.rgb)
+                assert pb.stats.kernel_launches == out.stats.kernel_launches + 4
+                assert pin.rgb.tobytes() == out.image.rgb.tobytes()
             # tools/workloads.py cfg 4: a 30-frame descent 400 -> 300 -> 110, 4 views
             b = _bench()
             keys = []
