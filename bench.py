@@ -525,6 +525,9 @@ def run_b200(args, rank, world, local):
         "config": config(world, K),
         "frames": timed_idx if world == 1 else f"{K} per rank, round-robin over the path",
         "mean_selected": mean_sel, "mean_pairs": mean_pairs,
+        # north_star's secondary unit: the same throughput as selected Gaussians (LoD nodes
+        # the filter keeps) and (Gaussian, tile) pairs per second
+        "gaussians_per_s": fps * mean_sel, "pairs_per_s": fps * mean_pairs,
         "stage_ms_per_frame": per_stage,
         "roofline": roofline, "stages": stages, "blend": blend,
         "per_frame_fps": per_frame_fps,
