@@ -44,6 +44,7 @@ def path(width, height, focal, keys, samples):
 
 BLEND = "cpa"  # --blend: the fast-blend kernel (RenderOptions.blend_kernel)
 THREE_SIGMA_ONLY = False
+INFLIGHT = 4  # frames in flight of the per-frame timing (run's --inflight)
 SH_DEGREE = 0  # --sh: view-dependent colour of this degree (synthetic coefficients)
 
 
@@ -68,8 +69,26 @@ def time_frames(scene, cams, mode, tau_r=3.0, reps=1):
     ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
     frames, sel, pairs = scene.take_totals()
-    return {"fps": frames / (ms / 1e3), "ms_per_frame": ms / frames, "frames": frames,
-            "mean_selected": sel / frames, "mean_pairs": pairs / frames}
+    out = {"fps": frames / (ms / 1e3), "ms_per_frame": ms / frames, "frames": frames,
+           "mean_selected": sel / frames, "mean_pairs": pairs / frames}
+    # the same frames through render_views_async (the multi-view filter, groups of four
+    # over two sets of four contexts)
+    scene.set_inflight(8)
+    scene.render_views_async(cams[:16], p)
+    scene.sync()
+    scene.take_totals()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(reps):
+        scene.render_views_async(cams, p)
+    scene.join()
+    ev1.record(stream)
+    ev1.synchronize()
+    vms = ev0.elapsed_time(ev1)
+    vf, _, _ = scene.take_totals()
+    scene.set_inflight(INFLIGHT)
+    out["fps_views"] = vf / (vms / 1e3)
+    return out
 
 
 def run_cfg5(n_views=1024):
@@ -192,6 +211,8 @@ def run(which, frames, lambda_g, inflight=2):
                     [n // 2, n - n // 2])
     build_s = time.perf_counter() - t0
     with L.GpuScene(tree) as scene:
+        global INFLIGHT
+        INFLIGHT = inflight
         scene.set_inflight(inflight)
         if SH_DEGREE:
             # synthetic view-dependent colour (no reference: SH0-only): seeded
