@@ -51,6 +51,9 @@ def main():
         s.render_views_async(cams + cams[::-1], p)
         s.sync()
         s.set_inflight(4)
+        # the synchronous render into pinned memory: banded blend + copies
+        with L.PinnedImage(cams[0].width, cams[0].height) as pin:
+            s.render(cams[0], L.FilterConfig(3.0), mode, image_out=pin.rgb)
         # SH degree-3 colours (k_sh_colour)
         rng = np.random.default_rng(1)
         s.set_sh(3, rng.normal(0.0, 0.1, (tree.node_count(), 15, 3)).astype(np.float32))
