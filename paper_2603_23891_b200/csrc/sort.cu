@@ -530,7 +530,13 @@ __device__ __forceinline__ void rank_merge(const unsigned long long* runs, uint3
     }
 }
 
-__global__ void __launch_bounds__(kSmallSortThreads) k_tile_sort(const uint32_t* __restrict__ offsets,
+// CTAs per SM the register budget is cut for: the per-bucket sort is latency-bound, so
+// occupancy wins -- 4 / 5 / 6 (56 / 48 / 40 registers; 6 spills 16 bytes, and the
+// 33.8 KB of shared memory caps it there): tile sort 49.4 / 45.6 / 44.1 us per frame
+#ifndef SORT_LB
+#define SORT_LB 6
+#endif
+__global__ void __launch_bounds__(kSmallSortThreads, SORT_LB) k_tile_sort(const uint32_t* __restrict__ offsets,
                                                                  const uint32_t* __restrict__ order,
                                                                  unsigned long long* keys,
                                                                  const RecOut ro, const int tiles_x) {
