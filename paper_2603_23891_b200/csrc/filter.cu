@@ -436,7 +436,13 @@ __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
 #define LEAF_PER_LANE 4
 #endif
 constexpr int kLeafPerLane = LEAF_PER_LANE;  // leaves per lane (a warp: 32 kLeafPerLane)
-__global__ void __launch_bounds__(256) k_filter_leaves(
+// F3 (and its multi-view form) budgeted for 8 CTAs per SM (32 registers): the leaf pass
+// is a dependent load chain, occupancy hides it (leaves + compaction 31.5 -> 30.4 us per
+// frame; F2 likewise at 8 CTAs was slower, 28.4 -> 31.9 us)
+#ifndef LEAF_LB
+#define LEAF_LB 8
+#endif
+__global__ void __launch_bounds__(256, LEAF_LB) k_filter_leaves(
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const uint32_t* __restrict__ blk_bits, uint32_t* __restrict__ keep_bits,
     uint32_t* __restrict__ tile_count, FilterClock* clk) {
@@ -832,7 +838,12 @@ __global__ void __launch_bounds__(kSelectBlock) k_select_views(const __grid_cons
     select_body(vs.cand[v], vs.qint[v], parent, end, vs.tile_count[v], blockIdx.x);
 }
 
-__global__ void __launch_bounds__(256) k_leaves_views(const __grid_constant__ ViewSetDev vs,
+// the multi-view leaf pass measured alike at 4 / 6 / 8 CTAs per SM (64 / 40 / 32
+// registers; 6 and 8 spill): 4
+#ifndef LEAF_VIEWS_LB
+#define LEAF_VIEWS_LB 4
+#endif
+__global__ void __launch_bounds__(256, LEAF_VIEWS_LB) k_leaves_views(const __grid_constant__ ViewSetDev vs,
                                                       const __grid_constant__ DevTree t) {
     pdl_wait();
     pdl_trigger();
