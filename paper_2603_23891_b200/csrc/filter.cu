@@ -412,7 +412,14 @@ __device__ __forceinline__ void select_body(uint32_t* __restrict__ cand_bits, ui
     if (lane == 0 && cntw) count_survivors(tile_count, warp_base / kTileNodes, cntw);
 }
 
+#ifndef SELECT_LB
+#define SELECT_LB 0
+#endif
+#if SELECT_LB
+__global__ void __launch_bounds__(kSelectBlock, SELECT_LB) k_select_internal(
+#else
 __global__ void __launch_bounds__(kSelectBlock) k_select_internal(
+#endif
     uint32_t* __restrict__ cand_bits, uint32_t* qint_bits, const uint32_t* __restrict__ parent,
     const uint64_t end, uint32_t* __restrict__ tile_count, FilterClock* clk) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
@@ -442,7 +449,11 @@ constexpr int kLeafPerLane = LEAF_PER_LANE;  // leaves per lane (a warp: 32 kLea
 #ifndef LEAF_LB
 #define LEAF_LB 8
 #endif
+#if LEAF_LB
 __global__ void __launch_bounds__(256, LEAF_LB) k_filter_leaves(
+#else
+__global__ void __launch_bounds__(256) k_filter_leaves(
+#endif
     const __grid_constant__ Geom g, const GeomF f, const __grid_constant__ DevTree t,
     const uint32_t* __restrict__ blk_bits, uint32_t* __restrict__ keep_bits,
     uint32_t* __restrict__ tile_count, FilterClock* clk) {

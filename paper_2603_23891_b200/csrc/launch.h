@@ -42,7 +42,10 @@ struct DevTree {
 constexpr int kLaunchesPerFrame = 6;
 constexpr int kMarkBlock = 256;
 constexpr int kSelectBlock = 256;
-constexpr int kSelectItems = 8;  // nodes per thread -> 2048-node tiles
+#ifndef SELECT_ITEMS
+#define SELECT_ITEMS 8
+#endif
+constexpr int kSelectItems = SELECT_ITEMS;  // nodes per thread -> 2048-node tiles
 // bitmask words, rounded up to whole 8192-node compaction tiles
 inline uint64_t bit_words(uint64_t n) { return (n + 8191) / 8192 * 256; }
 inline uint32_t select_tiles(uint64_t n) {

@@ -530,16 +530,17 @@ __device__ __forceinline__ void rank_merge(const unsigned long long* runs, uint3
     }
 }
 
-// CTAs per SM the register budget is cut for: the per-bucket sort is latency-bound, so
-// occupancy wins -- 4 / 5 / 6 (56 / 48 / 40 registers; 6 spills 16 bytes, and the
-// 33.8 KB of shared memory caps it there): tile sort 49.4 / 45.6 / 44.1 us per frame
-#ifndef SORT_LB
-#define SORT_LB 6
-#endif
-__global__ void __launch_bounds__(kSmallSortThreads, SORT_LB) k_tile_sort(const uint32_t* __restrict__ offsets,
-                                                                 const uint32_t* __restrict__ order,
-                                                                 unsigned long long* keys,
-                                                                 const RecOut ro, const int tiles_x) {
+// CTAs per SM the register budget is cut for.  The per-bucket sort is latency-bound,
+// so occupancy wins at 1080p -- 4 / 5 / 6 CTAs (56 / 48 / 40 registers; 6 spills 16
+// bytes, and the 33.8 KB of shared memory caps it there): tile sort 49.4 / 45.6 / 44.1 us
+// per cfg-3 frame -- but at 4K, where many buckets take the two-run path, 6 loses 9 % of
+// cfg 4's frame rate to 5 (527 vs 576 frames/s).  Both are built, chosen per frame size.
+constexpr int kSortCtasSmall = 6, kSortCtasBig = 5;
+constexpr int kSortBigFrameTiles = 12288;
+template <int kCtas>
+__global__ void __launch_bounds__(kSmallSortThreads, kCtas) k_tile_sort(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ order,
+    unsigned long long* keys, const RecOut ro, const int tiles_x) {
     pdl_wait();  // the previous kernel of the frame is complete and visible
     pdl_trigger();
     static_assert(kSmallSortCap == 2 * int(kRun), "two runs + their staging fill s");
@@ -657,7 +658,12 @@ __global__ void __launch_bounds__(kBigSortThreads) k_tile_sort_big(const uint32_
 void launch_tile_sort(const uint32_t* offsets, const uint32_t* order, int n_tiles,
                       unsigned long long* keys, cudaStream_t s, RecOut ro, int tiles_x) {
     if (n_tiles <= 0) return;
-    launch_pdl(k_tile_sort, n_tiles, kSmallSortThreads, 0, s, offsets, order, keys, ro, tiles_x);
+    if (n_tiles > kSortBigFrameTiles)
+        launch_pdl(k_tile_sort<kSortCtasBig>, n_tiles, kSmallSortThreads, 0, s, offsets, order,
+                   keys, ro, tiles_x);
+    else
+        launch_pdl(k_tile_sort<kSortCtasSmall>, n_tiles, kSmallSortThreads, 0, s, offsets, order,
+                   keys, ro, tiles_x);
 }
 
 void launch_tile_sort_big(const uint32_t* offsets, unsigned long long* keys,
