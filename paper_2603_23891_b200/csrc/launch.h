@@ -46,6 +46,8 @@ constexpr int kSelectBlock = 256;
 #define SELECT_ITEMS 8
 #endif
 constexpr int kSelectItems = SELECT_ITEMS;  // nodes per thread -> 2048-node tiles
+// k_select_internal's per-warp survivor sum covers 8 words (4 and 8 measured alike)
+static_assert(kSelectItems >= 1 && kSelectItems <= 8, "select: at most 8 nodes per thread");
 // bitmask words, rounded up to whole 8192-node compaction tiles
 inline uint64_t bit_words(uint64_t n) { return (n + 8191) / 8192 * 256; }
 inline uint32_t select_tiles(uint64_t n) {
