@@ -1236,12 +1236,19 @@ struct G4Chunk {
 };
 
 
-struct __align__(128) G4Stage {
+// With G4_SWIZZLE the tensor map's 64-byte swizzle stores row R's 16-byte chunk c at
+// chunk c ^ ((R >> 1) & 3): the consumers' per-lane row reads (64-byte stride) then
+// spread over all banks instead of two bank groups (16-way conflicts).  The swizzle
+// phase comes from smem address bits [8:7], so the rows sit in 512-byte-aligned stages.
+#ifndef G4_SWIZZLE
+#define G4_SWIZZLE 1
+#endif
+struct __align__(512) G4Stage {
     float rec[8][64];  // gather4 group q: rows 4q..4q+3 (16 floats each)
-    uint32_t slot[32];
 };
 struct G4Shared {
     G4Stage st[kG4Stages];
+    uint32_t slot[kG4Stages][32];
     WarpStage wl[kTmaConsumers];
     TmaHdr hdr[kG4Stages];
     unsigned long long full[kG4Stages], empty[kG4Stages];
@@ -1257,7 +1264,7 @@ __global__ void __launch_bounds__(kG4Threads, G4_MIN_CTAS) k_blend_g4(
     float* __restrict__ image) {
     pdl_wait();  // the sort (and everything before it) is complete and visible
     pdl_trigger();
-    extern __shared__ __align__(128) unsigned char g4_raw[];
+    extern __shared__ __align__(1024) unsigned char g4_raw[];
     G4Shared& sh = *reinterpret_cast<G4Shared*>(g4_raw);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
@@ -1355,7 +1362,7 @@ __global__ void __launch_bounds__(kG4Threads, G4_MIN_CTAS) k_blend_g4(
             // lanes past n name a valid row (lane 0's): their bytes are fetched, never read
             const uint32_t s0 = __shfl_sync(0xffffffffu, ch.slot, 0);
             const uint32_t slot = lane < ch.n ? ch.slot : s0;
-            st.slot[lane] = slot;
+            sh.slot[s][lane] = slot;
             const uint32_t groups = (ch.n + 3u) >> 2;
             const int q = int(lane & 7);
             const int r0 = int(__shfl_sync(0xffffffffu, slot, 4 * q + 0));
@@ -1403,12 +1410,15 @@ __global__ void __launch_bounds__(kG4Threads, G4_MIN_CTAS) k_blend_g4(
             counted = false;
         }
         const G4Stage& st = sh.st[s];
-        const int q = int(lane >> 2), r = int(lane & 3);
+        // this lane's row (row lane of the stage) and its chunks' physical positions
+        const float* row = &st.rec[0][0] + lane * 16;
+        const unsigned sw = G4_SWIZZLE ? (lane >> 1) & 3u : 0u;
+        auto chunk = [&](unsigned c) { return row + 4 * (c ^ sw); };
         bool hit = false;
         float mlx = 0.f, mly = 0.f;
         if (lane < hd.n) {
-            const float2 h = *reinterpret_cast<const float2*>(&st.rec[q][r * 16 + 8]);
-            const double2 m = *reinterpret_cast<const double2*>(&st.rec[q][r * 16 + 12]);
+            const float2 h = *reinterpret_cast<const float2*>(chunk(2));
+            const double2 m = *reinterpret_cast<const double2*>(chunk(3));
             if (h.x >= 0.0f) {
                 mlx = float(m.x - double(bx));
                 mly = float(m.y - double(by));
@@ -1420,13 +1430,12 @@ __global__ void __launch_bounds__(kG4Threads, G4_MIN_CTAS) k_blend_g4(
         if (bits && __any_sync(0xffffffffu, pix.T != 0.0f)) {
             if (hit) {
                 const int at = __popc(bits & lt);
-                const float* g = &st.rec[q][r * 16];
-                const float4 q0 = *reinterpret_cast<const float4*>(g);
-                const float4 col = *reinterpret_cast<const float4*>(g + 4);
+                const float4 q0 = *reinterpret_cast<const float4*>(chunk(0));
+                const float4 col = *reinterpret_cast<const float4*>(chunk(1));
                 wl.geo[at] = make_float4(mlx, mly, q0.x, q0.z);
                 wl.ct[at] = make_float4(q0.y, q0.w, col.x, col.y);
                 wl.gb[at] = make_float2(col.z, col.w);
-                wl.gid[at] = st.slot[lane];
+                wl.gid[at] = sh.slot[s][lane];
             }
             __syncwarp();
             const PixState saved = pix;
@@ -1827,7 +1836,8 @@ static bool encode_row_map(const Gauss32* g32, uint64_t rows, CUtensorMap* m) {
     const cuuint64_t d[2] = {16, rows}, st[1] = {sizeof(Gauss32)};
     const cuuint32_t b[2] = {16, 1}, e1[2] = {1, 1};
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<Gauss32*>(g32), d, st, b, e1,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  G4_SWIZZLE ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
