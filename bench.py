@@ -48,7 +48,7 @@ from paper_2603_23891_b200.sharding import reduce_timing, strided_frames  # noqa
 METRIC = "FPS @1080p on 10M-node LoD tree; filter+sort HBM GB/s vs peak; tile pairs"
 TREE = dict(nx=131, ny=131, seed=1, depth=3, build_seed=7)
 W, H, FOCAL, TAU_R = 1920, 1080, 1000.0, 3.0
-VIEWS_INFLIGHT = 8  # render_views_async: two sets of four contexts, groups of four views
+VIEWS_INFLIGHT = 12  # render_views_async: three sets of four contexts, groups of four views
 PATH_SAMPLES = (100, 100, 99)  # 300 frames = sum + 1
 N_PATH = sum(PATH_SAMPLES) + 1
 WORKLOAD = ("cfg3: 10,039,185-node LoD tree, 1920x1080, 300-frame fly-through "
@@ -98,7 +98,7 @@ def config(world, k):
     return {"workload": WORKLOAD, "nodes": 10039185, "width": W, "height": H,
             "frames_per_rank": k, "frame_schedule": "strided_frames(300, rank, N, K)",
             "enqueue": "render_views_async: the LoD filter shared by each group of 4 frames, "
-                       "groups alternating over two sets of 4 in-flight contexts",
+                       "groups rotating over three sets of 4 in-flight contexts",
             "l2": "inputs larger than L2 (tree 1.1 GB in HBM, the filter streams ~0.3 GB "
                   "per frame)", "parallelism": f"view-sharded x{world}"}
 
@@ -353,8 +353,8 @@ def run_b200(args, rank, world, local):
 
     # The headline loop: the frames through render_views_async -- the LoD filter shared
     # by each group of four frames (one pass over the node arrays), groups
-    # alternating between two sets of four in-flight contexts.  Warm-up:
-    # the W warm-up frames, cycled until every one of the 8 contexts has rendered.
+    # rotating over three sets of four in-flight contexts.  Warm-up:
+    # the W warm-up frames, cycled until every one of the 12 contexts has rendered.
     scene.set_inflight(VIEWS_INFLIGHT)
     warm_all = [warm[i % len(warm)] for i in range(max(len(warm), 2 * VIEWS_INFLIGHT))]
     scene.render_views_async(warm_all, params)

@@ -210,8 +210,8 @@ LODGS_API int lodgs_gpu_render_async(lodgs_gpu_scene *scene, const lodgs_camera 
 /* n frames enqueued like n lodgs_gpu_render_async calls, with the LoD filter shared
  * by each group of V = min(4, frames in flight / 2) consecutive frames: one pass over
  * the node arrays decides every node for all the group's views (SURVEY.md 8(e)'s
- * multi-view option; filter.cpp:115-150 per view); groups alternate between two sets
- * of V contexts.  Each frame's outputs equal its single-view render bit for bit.
+ * multi-view option; filter.cpp:115-150 per view); groups rotate over the in-flight / V
+ * disjoint sets of V contexts.  Each frame's outputs equal its single-view render bit for bit.
  * Frames with per-frame-only flags (stage timing, serial filter, collect_kpc, keep
  * pairs), mixed resolutions or fewer than 4 frames in flight fall back to per-frame
  * enqueues. */
@@ -220,7 +220,7 @@ LODGS_API int lodgs_gpu_render_views_async(lodgs_gpu_scene *scene, const lodgs_c
                                            float *const *images_host);
 /* Waits for every in-flight frame; stats (nullable) = the last frame's. */
 LODGS_API int lodgs_gpu_sync(lodgs_gpu_scene *scene, lodgs_render_stats *stats);
-/* Frames in flight for lodgs_gpu_render_async: 1 to 8 (default 4) -- consecutive
+/* Frames in flight for lodgs_gpu_render_async: 1 to 12 (default 4) -- consecutive
  * frames rotate over the scene and up to three twin contexts (own stream and
  * per-frame buffers over the same device tree), so one frame's latency-bound
  * kernels overlap the others'.  All fork from the scene's control stream

@@ -397,7 +397,7 @@ void GpuScene::set_sh(int degree, const float* host, uint64_t n) {
 
 void GpuScene::set_inflight(int n) {
     if (n < 1 || n > kMaxInflight)
-        throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1 to 8");
+        throw Error(LODGS_ERR_VALIDATION, "frames in flight: 1 to 12");
     join();
     inflight_ = n;
     make_contexts(n);
@@ -425,11 +425,12 @@ void GpuScene::enqueue_views_async(const lodgs_camera* cams, uint64_t n,
     }
     make_contexts(inflight_);
     ensure_resolution(int(cams[0].width), int(cams[0].height));  // every context follows
+    const int nsets = inflight_ / V;  // >= 2 disjoint sets of V contexts, used in turn
     for (uint64_t base = 0; base < n; base += uint64_t(V)) {
         const int nv = int(std::min<uint64_t>(uint64_t(V), n - base));
         GpuScene* ctx[kMaxViews] = {};
         for (int j = 0; j < nv; ++j) {
-            ctx[j] = context(int((async_frames_ + uint64_t(j)) % uint64_t(2 * V)));
+            ctx[j] = context(int((async_frames_ + uint64_t(j)) % uint64_t(nsets * V)));
             if (!ctx[j]->view_ev_)
                 FGS_CUDA(cudaEventCreateWithFlags(&ctx[j]->view_ev_, cudaEventDisableTiming));
         }

@@ -175,7 +175,7 @@ private:
 #ifndef FGS_INFLIGHT_DEFAULT
 #define FGS_INFLIGHT_DEFAULT 4
 #endif
-    static constexpr int kMaxInflight = 8;
+    static constexpr int kMaxInflight = 12;
     int inflight_ = FGS_INFLIGHT_DEFAULT;
     GpuScene* context(int i);
     void make_contexts(int n);

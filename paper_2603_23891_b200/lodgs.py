@@ -834,7 +834,7 @@ class GpuScene:
         _check(self._lib.lodgs_gpu_join(self._h))
 
     def set_inflight(self, frames: int) -> None:
-        """Frames in flight for render_async (1 to 8; default 4)."""
+        """Frames in flight for render_async (1 to 12; default 4)."""
         _check(self._lib.lodgs_gpu_scene_set_inflight(self._h, int(frames)))
 
     def set_sh(self, degree: int, sh_rest=None) -> None:

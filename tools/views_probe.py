@@ -28,7 +28,7 @@ def main():
     with L.GpuScene(tree) as s:
         stream = torch.cuda.ExternalStream(s.stream_ptr())
         p = s.params(L.FilterConfig(bench.TAU_R), L.ShrinkMode.three_sigma(), L.RenderOptions())
-        for inflight in (4, 6, 8):
+        for inflight in tuple(int(x) for x in os.environ.get("VIEWS_INFLIGHT", "4,6,8").split(",")):
             s.set_inflight(inflight)
             for mode in ("frames", "views"):
                 best = 0.0
