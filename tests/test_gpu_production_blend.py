@@ -59,6 +59,14 @@ def _async_frames(L, scene, cams, tau_r, mode, blend_kernel="cpa"):
     return imgs
 
 
+def _views(L, scene, cams, tau_r, mode):
+    imgs = [np.empty((c.height, c.width, 3), np.float32) for c in cams]
+    p = scene.params(L.FilterConfig(tau_r), mode, L.RenderOptions())
+    scene.render_views_async(cams, p, host_ptrs=[im.ctypes.data for im in imgs])
+    scene.sync()
+    return imgs
+
+
 def _batch_frames(L, scene, cams, tau_r, mode):
     imgs = [np.empty((c.height, c.width, 3), np.float32) for c in cams]
     stats = scene.render_batch(cams, L.FilterConfig(tau_r), mode,
@@ -248,6 +256,13 @@ def test_cfg4_50m_4k_production(L, ref, gpu):
                 pb = s.render(lo, L.FilterConfig(3.0), mode, image_out=pin.rgb)
                 assert pb.stats.kernel_launches == out.stats.kernel_launches + 4
                 assert pin.rgb.tobytes() == out.image.rgb.tobytes()
+            # the multi-view filter on the 50M tree (groups of four over two context sets)
+            s.set_inflight(8)
+            v = _views(L, s, [hi, lo, hi, lo, lo], 3.0, mode)
+            assert v[1].tobytes() == out.image.rgb.tobytes()
+            assert v[4].tobytes() == out.image.rgb.tobytes()
+            assert v[0].tobytes() == v[2].tobytes() == a[0].tobytes()
+            s.set_inflight(4)
             # tools/workloads.py cfg 4: a 30-frame descent 400 -> 300 -> 110, 4 views
             b = _bench()
             keys = []

@@ -147,6 +147,14 @@ def test_sh_frames_in_flight(L, scene_sh):
         s.render_async(c, p)
         s.sync()
         assert s.read_image(c).tobytes() == w.tobytes()
+    # the multi-view filter: SH colours on every context
+    s.set_inflight(8)
+    vimgs = [np.empty((c.height, c.width, 3), np.float32) for c in cams]
+    s.render_views_async(cams, p, host_ptrs=[im.ctypes.data for im in vimgs])
+    s.sync()
+    for w, im in zip(want, vimgs):
+        assert im.tobytes() == w.tobytes()
+    s.set_inflight(4)
     s.set_sh(0)
 
 
