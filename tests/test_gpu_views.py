@@ -101,3 +101,33 @@ def test_views_fall_back_per_frame(L, city):
     s.sync()
     for w, g in zip(want, imgs):
         assert g.tobytes() == w.tobytes()
+
+
+def test_views_adaptive_and_rgb8(L, city):
+    """Adaptive shrinking (the filter is mode-independent, K3 is not) and 8-bit host images
+    (LODGS_RENDER_OUTPUT_RGB8) through render_views_async: equal to the per-frame path."""
+    from paper_2603_23891_b200.sharding import strided_frames
+
+    tree, cams, s = city
+    s.set_inflight(8)
+    frames = [cams[i] for i in strided_frames(len(cams), 0, 1, 8)]
+    mode = L.ShrinkMode.adaptive(0.05)
+    want = [s.render(c, L.FilterConfig(3.0), mode).image.rgb.copy() for c in frames]
+    imgs = [np.empty((c.height, c.width, 3), np.float32) for c in frames]
+    p = s.params(L.FilterConfig(3.0), mode, L.RenderOptions())
+    s.render_views_async(frames, p, host_ptrs=[im.ctypes.data for im in imgs])
+    s.sync()
+    for i, (w, g) in enumerate(zip(want, imgs)):
+        assert g.tobytes() == w.tobytes(), f"adaptive frame {i}"
+    three = L.ShrinkMode.three_sigma()
+    want8 = []
+    for c in frames:
+        s.render(c, L.FilterConfig(3.0), three)
+        want8.append(s.read_image_rgb8(c))
+    b8 = [np.empty((c.height, c.width, 3), np.uint8) for c in frames]
+    p8 = s.params(L.FilterConfig(3.0), three, L.RenderOptions(output_rgb8=True))
+    s.render_views_async(frames, p8, host_ptrs=[im.ctypes.data for im in b8])
+    s.sync()
+    for i, (w, g) in enumerate(zip(want8, b8)):
+        assert g.tobytes() == w.tobytes(), f"rgb8 frame {i}"
+    s.set_inflight(4)
