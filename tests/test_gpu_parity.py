@@ -657,7 +657,7 @@ def test_render_async_frames_in_flight(L, oracle, gpu):
     """lodgs_gpu_render_async with 4, 3, 2 and 1 frames in flight (the scene
     and up to three twin contexts): every frame's image and the run totals
     equal the synchronous renders; the last frame is what sync() reports and
-    read_image() returns; more than 8 is refused."""
+    read_image() returns; more than 12 is refused."""
     tree = L.make_tree(23, 3, 8, 0.5, 4, 4, 2)
     rng = oracle.rng(29)
     cams = [oracle.orbit_camera(rng, 200, 150, 16.0) for _ in range(7)]
@@ -666,7 +666,7 @@ def test_render_async_frames_in_flight(L, oracle, gpu):
     mode = L.ShrinkMode.three_sigma()
     with L.GpuScene(tree) as s:
         ref = [s.render(cam, L.FilterConfig(4.0), mode) for cam in cams]
-        for inflight in (4, 3, 2, 1, 8, 6, 4):
+        for inflight in (4, 3, 2, 1, 8, 12, 6, 4):
             s.set_inflight(inflight)
             p = s.params(L.FilterConfig(4.0), mode, L.RenderOptions())
             imgs = [np.empty((150, 200, 3), np.float32) for _ in cams]
@@ -682,7 +682,7 @@ def test_render_async_frames_in_flight(L, oracle, gpu):
                 assert im.tobytes() == r.image.rgb.tobytes()
             assert last.n_pairs == ref[-1].stats.n_pairs
             assert s.read_image(cams[-1]).tobytes() == ref[-1].image.rgb.tobytes()
-        for bad in (0, 9):
+        for bad in (0, 13):
             with pytest.raises(L.ValidationError):
                 s.set_inflight(bad)
 
