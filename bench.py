@@ -542,7 +542,8 @@ def run_b200(args, rank, world, local):
         "e2e_sync": {"value": world * K / e2e_sync_max, "unit": "frames/s",
                      "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": img_bytes + 64,
                      "call": "lodgs_gpu_render, one synchronous call per frame (the drop-in "
-                             "lodgs::render shim's call)"},
+                             "lodgs::render shim's call) into pinned host memory: blend in 4 "
+                             "bands, each band's rows copied while the next blends"},
         "e2e_rgb8": {"value": world * K / e2e8_max, "unit": "frames/s",
                      "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": W * H * 3 + 64,
                      "call": "lodgs_gpu_render_batch + LODGS_RENDER_OUTPUT_RGB8 (save_ppm bytes)"},
