@@ -1,0 +1,69 @@
+"""Every frame of the 300-frame cfg-3 fly-through through the bench's enqueue
+(render_views_async, the production kernels) against the reference renderer itself
+(oracle/_ref, all host threads): selected and pair counts equal, image within the
+north-star tolerance (max-abs 1e-3, PSNR > 60 dB).  Writes one JSON summary line.
+Test infrastructure (loads oracle/_ref); a few minutes of CPU for the reference.
+
+    python tools/full_path_parity.py > profiles/r2_full_path_parity.json
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+
+import bench  # noqa: E402
+from oracle_bind import Ref  # noqa: E402
+from paper_2603_23891_b200 import lodgs as L  # noqa: E402
+
+
+def main():
+    ref = Ref()
+    threads = os.cpu_count() or 1
+    tree = L.build_synthetic_tree(**bench.TREE)
+    rh = ref.tree_from(tree)
+    cams = bench.flythrough(L)
+    mode = L.ShrinkMode.three_sigma()
+    t0 = time.perf_counter()
+    with L.GpuScene(tree) as s:
+        s.set_inflight(12)
+        for c in cams[::10]:
+            s.render(c, L.FilterConfig(bench.TAU_R), mode)  # pair-buffer sizing
+        p = s.params(L.FilterConfig(bench.TAU_R), mode, L.RenderOptions())
+        worst_err, worst_psnr, bad, count_mismatch = 0.0, float("inf"), [], []
+        for b in range(0, len(cams), 20):
+            chunk = cams[b:b + 20]
+            imgs = [np.empty((c.height, c.width, 3), np.float32) for c in chunk]
+            s.take_totals()
+            s.render_views_async(chunk, p, host_ptrs=[im.ctypes.data for im in imgs])
+            s.sync()
+            nf, gsel, gpairs = s.take_totals()
+            wsel = wpairs = 0
+            for k, (c, im) in enumerate(zip(chunk, imgs)):
+                want = ref.render(rh, c, bench.TAU_R, mode, workers=threads)
+                wsel += want["n_selected"]
+                wpairs += want["n_pairs"]
+                err = float(np.abs(im.astype(np.float64) - want["image"]).max())
+                psnr = ref.psnr(im, want["image"]) if err > 0 else float("inf")
+                worst_err = max(worst_err, err)
+                worst_psnr = min(worst_psnr, psnr)
+                if err > 1e-3 or psnr <= 60.0:
+                    bad.append(b + k)
+            if (nf, gsel, gpairs) != (len(chunk), wsel, wpairs):
+                count_mismatch.append(b)
+    print(json.dumps({"frames": len(cams), "tree_nodes": tree.node_count(),
+                      "enqueue": "render_views_async (12 contexts, groups of 4)",
+                      "worst_max_abs": worst_err, "worst_psnr_db": worst_psnr,
+                      "frames_out_of_tolerance": bad, "tolerance": "max-abs 1e-3, PSNR > 60 dB",
+                      "chunks_with_count_mismatch": count_mismatch,
+                      "counts": "selected and pair totals per 20-frame chunk equal the reference's",
+                      "reference_threads": threads,
+                      "wall_s": time.perf_counter() - t0}))
+
+
+if __name__ == "__main__":
+    main()
