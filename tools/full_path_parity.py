@@ -4,7 +4,7 @@
 north-star tolerance (max-abs 1e-3, PSNR > 60 dB).  Writes one JSON summary line.
 Test infrastructure (loads oracle/_ref); a few minutes of CPU for the reference.
 
-    python tools/full_path_parity.py > profiles/r2_full_path_parity.json
+    python tools/full_path_parity.py --which cfg3|cfg2|cfg4 >> profiles/r2_full_path_parity.json
 """
 import json
 import os
@@ -21,16 +21,48 @@ from oracle_bind import Ref  # noqa: E402
 from paper_2603_23891_b200 import lodgs as L  # noqa: E402
 
 
+def workload(which):
+    """(tree, cams, [(name, mode)]) of tools/workloads.py's paths; cfg 3: the bench's."""
+    import workloads as W
+
+    if which == "cfg3":
+        return (L.build_synthetic_tree(**bench.TREE), bench.flythrough(L),
+                [("three_sigma", L.ShrinkMode.three_sigma())])
+    if which == "cfg2":
+        tree = L.build_synthetic_tree(nx=41, ny=42, seed=1, depth=3, build_seed=7)
+        cams = W.path(1920, 1080, 1000.0, [((0.0, 0.0, 60.0), (0.0, 0.0001, 0.0)),
+                                           ((5.0, -3.0, 50.0), (5.0, -2.9999, 0.0))], [29])
+        # the device-calibrated taus of lambda_G 0.2 / 0.02 (profiles/r2_workloads_*)
+        return tree, cams, [("three_sigma", L.ShrinkMode.three_sigma()),
+                            ("adaptive_0.797", L.ShrinkMode.adaptive(0.7972857536526123)),
+                            ("adaptive_0.0797", L.ShrinkMode.adaptive(0.07972857536526123))]
+    tree = L.build_synthetic_tree(nx=103, ny=104, seed=1, depth=4, build_seed=7)
+    cams = W.path(3840, 2160, 2000.0, [((0.0, 0.0, 400.0), (0.0, 0.0001, 0.0)),
+                                       ((20.0, -10.0, 300.0), (20.0, -9.9999, 0.0)),
+                                       ((-10.0, 15.0, 110.0), (-10.0, 15.0001, 0.0))], [14, 15])
+    return tree, cams, [("three_sigma", L.ShrinkMode.three_sigma()),
+                        ("adaptive_0.0844", L.ShrinkMode.adaptive(0.08441517068141142))]
+
+
 def main():
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", default="cfg3", choices=("cfg2", "cfg3", "cfg4"))
+    args = ap.parse_args()
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
     ref = Ref()
     threads = os.cpu_count() or 1
-    tree = L.build_synthetic_tree(**bench.TREE)
+    tree, cams, modes = workload(args.which)
     rh = ref.tree_from(tree)
-    cams = bench.flythrough(L)
-    mode = L.ShrinkMode.three_sigma()
+    for mname, mode in modes:
+        run(ref, rh, tree, cams, mode, mname, args.which, threads)
+
+
+def run(ref, rh, tree, cams, mode, mname, which, threads):
     t0 = time.perf_counter()
     with L.GpuScene(tree) as s:
-        s.set_inflight(12)
+        s.set_inflight(12 if which != "cfg4" else 8)
         for c in cams[::10]:
             s.render(c, L.FilterConfig(bench.TAU_R), mode)  # pair-buffer sizing
         p = s.params(L.FilterConfig(bench.TAU_R), mode, L.RenderOptions())
@@ -55,8 +87,9 @@ def main():
                     bad.append(b + k)
             if (nf, gsel, gpairs) != (len(chunk), wsel, wpairs):
                 count_mismatch.append(b)
-    print(json.dumps({"frames": len(cams), "tree_nodes": tree.node_count(),
-                      "enqueue": "render_views_async (12 contexts, groups of 4)",
+    print(json.dumps({"workload": which, "shrink": mname, "frames": len(cams),
+                      "tree_nodes": tree.node_count(),
+                      "enqueue": "render_views_async (groups of 4)",
                       "worst_max_abs": worst_err, "worst_psnr_db": worst_psnr,
                       "frames_out_of_tolerance": bad, "tolerance": "max-abs 1e-3, PSNR > 60 dB",
                       "chunks_with_count_mismatch": count_mismatch,
