@@ -1,10 +1,10 @@
-"""Every frame of the 300-frame cfg-3 fly-through through the bench's enqueue
+"""Every frame of a workload path (cfg 3: the 300-frame fly-through) through the bench's enqueue
 (render_views_async, the production kernels) against the reference renderer itself
 (oracle/_ref, all host threads): selected and pair counts equal, image within the
 north-star tolerance (max-abs 1e-3, PSNR > 60 dB).  Writes one JSON summary line.
 Test infrastructure (loads oracle/_ref); a few minutes of CPU for the reference.
 
-    python tools/full_path_parity.py --which cfg3|cfg2|cfg4 >> profiles/r2_full_path_parity.json
+    python tools/full_path_parity.py --which cfg3|cfg2|cfg4|cfg5 >> profiles/r2_full_path_parity.jsonl
 """
 import json
 import os
@@ -28,6 +28,13 @@ def workload(which):
     if which == "cfg3":
         return (L.build_synthetic_tree(**bench.TREE), bench.flythrough(L),
                 [("three_sigma", L.ShrinkMode.three_sigma())])
+    if which == "cfg5":  # the 1,024 poses of tools/workloads.py run_cfg5 (cfg-3 tree)
+        keys_cams = bench.flythrough(L)
+        keys = [keys_cams[0], keys_cams[100], keys_cams[200], keys_cams[-1]]
+        n = 1023
+        return (L.build_synthetic_tree(**bench.TREE),
+                L.sample_camera_path(keys, (n // 3, n // 3, n - 2 * (n // 3))),
+                [("three_sigma", L.ShrinkMode.three_sigma())])
     if which == "cfg2":
         tree = L.build_synthetic_tree(nx=41, ny=42, seed=1, depth=3, build_seed=7)
         cams = W.path(1920, 1080, 1000.0, [((0.0, 0.0, 60.0), (0.0, 0.0001, 0.0)),
@@ -48,7 +55,7 @@ def main():
     import argparse
 
     ap = argparse.ArgumentParser()
-    ap.add_argument("--which", default="cfg3", choices=("cfg2", "cfg3", "cfg4"))
+    ap.add_argument("--which", default="cfg3", choices=("cfg2", "cfg3", "cfg4", "cfg5"))
     args = ap.parse_args()
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     ref = Ref()
